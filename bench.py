@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark of the blocked Floyd–Warshall APSP hot path (arxiv 1811.01201) on B200.
+
+Metric (BASELINE.json): APSP GFLOPS = 2 n^3 / t at n = 16384 FP32 (configs[3]), plus the
+phase-3 fraction of the FP32 add+min issue roofline. A "step" is one complete solve
+(validate, pad/init, R = n/BS rounds of phases 1-3, next-hop post-pass) of a fresh copy of
+the seeded synthetic input already resident in HBM.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config C4]
+
+Prints ONE JSON line on rank 0. See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import apsp_inputs as gen  # noqa: E402
+
+METRIC = "APSP GFLOPS (2n³/s) at n=16384 FP32, 1/2/4/8 B200; % of FP32 add+min roofline"
+CONFIG_DESC = {
+    "C1": "n=512 complete digraph, FP32 integer weights [1,100], BS=32, next-hop P",
+    "C2": "n=4096 complete digraph, FP32 real weights [1,100), BS=128, next-hop P",
+    "C3": "n=8192 ER p=0.1 digraph, INT32 weights [1,1000], INF=INT32_MAX/2, BS=128, next-hop P",
+    "C4": "n=16384 complete digraph, FP32 integer weights [1,100], BS=128, next-hop P",
+    "C5": "n=32768 complete digraph, FP32 real weights [1,100), BS=128, next-hop P",
+}
+PROFILE_TRAFFIC = os.path.join(ROOT, "profiles", "phase3_traffic.json")
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample(cfg: dict, seconds_target: float = 15.0):
+    """Time the oracle (as it stands) on the host cores on a bounded sample of the same
+    workload: the first k-iterations of the triple loop on the full n x n matrix (each
+    k-iteration is n^2 relaxations = 2 n^2 flop), scaled to GFLOPS."""
+    import oracle
+    n = cfg["n"]
+    W = gen.config_matrix(cfg["name"]) if cfg["kind"] != "er_int" else None
+    if W is None:   # INT32 config: the timing sample uses the FP32 loop on the same values
+        Wi = gen.config_matrix(cfg["name"])
+        W = np.where(Wi >= gen.INF_I32, np.inf, Wi).astype(np.float32)
+    np.fill_diagonal(W, 0)
+    i = np.arange(n)
+    P = np.where(np.isinf(W), -1, i[None, :]).astype(np.int32)
+    P[i, i] = i
+    # calibrate: one step, then enough steps for ~seconds_target
+    t0 = time.perf_counter()
+    oracle.fw_steps(W, P, 0, 1)
+    t1 = time.perf_counter() - t0
+    ks = int(max(1, min(n - 1, seconds_target / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.fw_steps(W, P, 1, 1 + ks)
+    dt = time.perf_counter() - t0
+    gflops = 2.0 * n * n * ks / dt / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    return {"value": gflops, "unit": "GFLOPS", "cores": cores, "kind": "oracle",
+            "sample": f"oracle C triple loop (next-hop), k-iterations 1..{ks} of {n} on the full "
+                      f"{n}x{n} {cfg['name']} matrix ({ks} x n^2 relaxations, {dt:.1f} s); "
+                      f"GFLOPS = 2*n^2*k_steps/t"}
+
+
+def config_for(name: str) -> dict:
+    c = dict(gen.CONFIGS[name])
+    c["name"] = name
+    return c
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    base = cpu_sample(cfg, seconds_target=max(2.0, 20.0 / max(1, args.steps + args.warmup)))
+    # each step is one bounded sample; report the median over steps
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample(cfg, seconds_target=3.0)
+    for _ in range(args.steps):
+        vals.append(cpu_sample(cfg, seconds_target=max(2.0, 30.0 / max(1, args.steps)))["value"])
+    v = statistics.median(vals) if vals else base["value"]
+    n = cfg["n"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2.0 * n ** 3 / (v * 1e9) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": CONFIG_DESC[cfg["name"]], "n": n,
+                                        "block": cfg["block"], "seed": cfg["seed"]},
+        "cpu_baseline": {**base, "value": v},
+        "e2e": {"value": v, "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, cfg):
+    import torch
+    import paper_1811_01201_b200 as fw
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n, BS = cfg["n"], args.block or cfg["block"]
+    is_int = cfg["kind"] == "er_int"
+    W = gen.config_matrix(cfg["name"])
+    dW = torch.from_numpy(W).to(dev)                       # resident input (never modified)
+    dD = torch.empty_like(dW)
+    dP = torch.empty((n, n), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    solve = fw.fw_solve_device_i32 if is_int else fw.fw_solve_device_f32
+
+    fw.fw_init(0, fw.FW_TIMING)
+
+    def step():
+        dD.copy_(dW)                                         # fresh input, device-resident
+        solve(dD, dP, block=BS, stream=stream)
+        return fw.fw_last_stats()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            stats.append(step())
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_per_step = ms_total / args.steps
+    flops = 2.0 * float(n) ** 3
+    # replicas: each rank solves its own copy (the partitioned multi-GPU driver is not in
+    # this build yet) -> whole-job throughput = world x per-rank
+    gflops = world * flops * args.steps / (ms_total * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (phase 3): algorithmic flops per launch / avg duration
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    max_mhz = 1965.0
+    try:
+        import pynvml  # nvidia_ml_py
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local)
+        max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+    except Exception:
+        pass
+    peak_tflops = sms * 128 * max_mhz * 1e6 / 1e12       # SMs x 128 lanes x f (2 flop/relax)
+    p3_ms = sum(s.phase3_ms for s in stats)
+    p3_launches = sum(s.phase3_launches for s in stats)
+    p3_relax = sum(s.phase3_relaxations for s in stats)
+    avg_launch_ms = p3_ms / max(1, p3_launches)
+    achieved_tflops = 2.0 * p3_relax / (p3_ms * 1e-3) / 1e12 if p3_ms > 0 else None
+    traffic = None
+    if os.path.exists(PROFILE_TRAFFIC):
+        try:
+            traffic = json.load(open(PROFILE_TRAFFIC)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "alu", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+            "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
+            "traffic": traffic, "kernel": "minplus_tile_kernel<float,128,128,32,TAGS> (phase 3)",
+            "avg_launch_ms": avg_launch_ms,
+            "peak_basis": f"stated FP32 add+min issue roofline: {sms} SMs x 128 lanes x {max_mhz:.0f} MHz "
+                          "(2 flop per relaxation, BASELINE north_star)",
+            "phase_ms_per_step": {"phase1": sum(s.phase1_ms for s in stats) / len(stats),
+                                  "phase2": sum(s.phase2_ms for s in stats) / len(stats),
+                                  "phase3": p3_ms / len(stats),
+                                  "post": sum(s.post_ms for s in stats) / len(stats)}}
+    launches_per_step = 2 + 4 * stats[-1].rounds + (2 if True else 0)
+
+    # e2e: the same metric through the public host entry point with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.from_numpy(W).pin_memory()
+        hD = torch.empty_like(host_in).pin_memory()
+        hP = torch.empty((n, n), dtype=torch.int32).pin_memory()
+        f_host = fw.fw_solve_i32 if is_int else fw.fw_solve
+        ts = []
+        for it in range(max(1, args.e2e_steps) + 1):
+            hD.copy_(host_in)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            f_host(hD, hP, block=BS)
+            dt = time.perf_counter() - t0
+            if it > 0:       # first call warms the host-side staging
+                ts.append(dt)
+        e2e = {"value": flops / statistics.median(ts) / 1e9 * world, "unit": "GFLOPS",
+               "h2d_bytes_per_step": int(n * n * 4), "d2h_bytes_per_step": int(2 * n * n * 4),
+               "ms_per_step": statistics.median(ts) * 1e3}
+    fw.fw_free()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_sample(cfg)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": gflops, "unit": "GFLOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if world == 1 else "weak", "vs_baseline": None,
+            "dtype": "i32" if is_int else "f32", "data": "synthetic",
+            "config": {"workload": CONFIG_DESC[cfg["name"]], "config": cfg["name"], "n": n,
+                       "block": BS, "seed": cfg["seed"], "path": "next-hop",
+                       "l2": "inputs larger than L2 (D and P 1 GiB each at n=16384)",
+                       "parallelism": "single GPU" if world == 1 else f"{world} replicas"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "context": "paper: 338 GFLOPS on a 68-core Xeon Phi 7250 (KNL), PAPER.md P:202 (not a target)",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=sorted(gen.CONFIGS))
+    ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = config_for(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,132 @@
+/*
+ * fw.h — C ABI of the B200-native blocked Floyd–Warshall APSP library (libfwb200.so).
+ *
+ * Method: Rucci, De Giusti, Naiouf, "Blocked All-Pairs Shortest Paths Algorithm on
+ * Intel Xeon Phi KNL Processor: A Case Study" (arxiv 1811.01201). Citations:
+ *   P:n  = /root/reference/PAPER.md line n        S:n = SPEC.md line n
+ *   BJ   = /root/repo/BASELINE.json (north_star)  R# = DESIGN.md "Readings of the paper"
+ *
+ * The operation (§3): given an n x n distance matrix D initialised with the
+ * edge weights, for k = 0..n-1 relax D[i][j] = min(D[i][j], D[i][k] + D[k][j]); a path
+ * matrix P is produced "when the reconstruction of the shortest path is required"
+ * (P:78). The library computes it with the blocked algorithm of §4.1:
+ * R = n_pad/BS rounds, each with phase 1 (diagonal block), phase 2 (pivot row
+ * and column strips) and phase 3 (all remaining blocks).
+ *
+ * Conventions (DESIGN.md readings):
+ *   R1  P is returned as a NEXT-HOP matrix by default (BJ:5 "next-hop");
+ *       FW_PATH_LAST_K returns the paper's "most recently added intermediate node" form.
+ *   R2  Relaxation is strict '<' (ties keep the old value).
+ *   R3  No-edge sentinel: FP32 +INFINITY; INT32 FW_INF_I32 = 0x3FFFFFFF (INT32_MAX/2, BJ
+ *       configs[2]). Unreachable outputs are exactly the sentinel, with next = -1.
+ *   R4  The diagonal is forced to 0.
+ *   R11 n is padded internally to a multiple of 128 with isolated vertices.
+ *
+ * Layout: every matrix is row-major and contiguous (leading dimension = n for host
+ * buffers, `ld` elements for device buffers), element (i,j) at [i*ld + j].
+ *
+ * Errors: every function returns FW_OK (0) or a positive fw_status. fw_last_error()
+ * returns a thread-local, human-readable message for the last non-OK return.
+ *  - FW_EINVAL / FW_ERANGE are detected BEFORE any output is written: dist and next
+ *    are left untouched.
+ *  - After FW_ECUDA / FW_ENCCL the outputs are unspecified; call fw_free().
+ *  - Calling fw_solve* before fw_init returns FW_ESTATE.
+ * Ownership: the caller owns every buffer it passes; the library keeps no pointer to
+ * them after a call returns. Device workspaces and streams live in the context created
+ * by fw_init and are released by fw_free. Calls are serialised per process.
+ */
+#ifndef FW_B200_H
+#define FW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FW_INF_I32 0x3FFFFFFF /* INT32 no-edge / unreachable sentinel (R3) */
+
+enum fw_status {
+  FW_OK = 0,
+  FW_EINVAL = 1, /* bad argument or out-of-domain weight (negative, NaN, > FW_INF_I32) */
+  FW_ENOMEM = 2, /* device or pinned-host allocation failed                          */
+  FW_ECUDA = 3,  /* a CUDA runtime call or kernel failed                              */
+  FW_ENCCL = 4,  /* reserved for the multi-GPU transport                               */
+  FW_ESTATE = 5, /* fw_init not called, or called twice                               */
+  FW_ERANGE = 6  /* INT32: (n-1) * max finite weight >= FW_INF_I32 (sums could hit INF) */
+};
+
+/* fw_init flags */
+enum fw_flags {
+  FW_PATH_NEXT_HOP = 0u,  /* P = next hop (default, R1)                          */
+  FW_PATH_LAST_K = 1u,    /* P = last intermediate vertex k, -1 = direct edge */
+  FW_TIMING = 2u          /* record per-phase CUDA-event times into fw_stats      */
+};
+
+/* Statistics of the last successful solve (fw_last_stats). Times in milliseconds. */
+typedef struct fw_stats {
+  int64_t n;            /* user n                                              */
+  int64_t n_pad;        /* padded n (multiple of 128)                          */
+  int32_t block;        /* BS used                                             */
+  int32_t rounds;       /* rounds executed (rounds lying wholly in padding are skipped) */
+  int32_t is_int;       /* 1 = INT32 solve                                     */
+  int32_t path_mode;    /* -1 = no P, 0 = next hop, 1 = last k                 */
+  double solve_ms;      /* device-resident solve (init .. post-pass), CUDA events */
+  double phase1_ms;     /* FW_TIMING only: sum over rounds                     */
+  double phase2_ms;
+  double phase3_ms;
+  double post_ms;       /* P resolution post-pass                              */
+  double h2d_ms;        /* host entry points only                              */
+  double d2h_ms;
+  int64_t phase3_launches;
+  double phase3_relaxations; /* relaxations issued by phase-3 launches (algorithmic) */
+} fw_stats;
+
+/* Create the process-wide context. ngpus_max: 0 = all visible devices (this build
+ * solves on device 0 of the calling process; multi-GPU runs one process per GPU).
+ * flags: FW_PATH_* | FW_TIMING. Returns FW_ESTATE if already initialised. */
+int fw_init(int ngpus_max, unsigned flags);
+
+/* Release every device buffer, stream and event of the context. Idempotent. */
+int fw_free(void);
+
+/* Host-memory solve, FP32.
+ *   dist  in/out, n*n floats: W in (+inf = no edge, weights >= 0, no NaN), D out.
+ *   next  out, n*n int32, or NULL for a distance-only solve. Next-hop mode: next[i][j] is
+ *         the first vertex after i on a shortest i->j path, next[i][i] = i, -1 when j is
+ *         unreachable. LAST_K mode: an intermediate k with D[i][j] = D[i][k] + D[k][j], or
+ *         -1 for a direct edge, the diagonal, or an unreachable pair.
+ *   n     number of vertices, 1 <= n <= 65536.
+ *   block BS in {32, 64, 128}, or 0 = auto (128 for n >= 4096, else 64).
+ *   ngpus must be 0 or 1 in this single-process entry point.
+ * Pinned (cudaHostAlloc/registered) buffers are copied directly; pageable buffers are
+ * staged through an internal pinned buffer. */
+int fw_solve(float *dist, int32_t *next, int64_t n, int block, int ngpus);
+
+/* Host-memory solve, INT32 (no-edge = FW_INF_I32; weights in [0, FW_INF_I32]). */
+int fw_solve_i32(int32_t *dist, int32_t *next, int64_t n, int block, int ngpus);
+
+/* Device-memory solve on the current device, enqueued on `stream` (a cudaStream_t; NULL =
+ * legacy default stream). d_dist: n rows of `ld` >= n floats (in/out); d_next: n rows of
+ * `ld` int32 or NULL. When n % 128 == 0 and ld == n the solve runs in place with no copy;
+ * otherwise through an internal padded workspace. Returns after the solve completes
+ * (the stream is synchronised: validation must finish before the rounds are issued). */
+int fw_solve_device_f32(float *d_dist, int32_t *d_next, int64_t n, int64_t ld, int block,
+                        void *stream);
+int fw_solve_device_i32(int32_t *d_dist, int32_t *d_next, int64_t n, int64_t ld, int block,
+                        void *stream);
+
+/* Message for the last non-OK return on this thread ("" if none). */
+const char *fw_last_error(void);
+
+/* Copy the statistics of the last successful solve. FW_ESTATE if none yet. */
+int fw_last_stats(fw_stats *out);
+
+/* Library version string, e.g. "fwb200 0.1 sm_100a". */
+const char *fw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FW_B200_H */

@@ -57,6 +57,7 @@ def lib():
         I64 = ctypes.c_int64
         L.oracle_fw_f32.argtypes = [P, P, I64, ctypes.c_int]
         L.oracle_fw_i32.argtypes = [P, P, I64, ctypes.c_int]
+        L.oracle_fw_f32_steps.argtypes = [P, P, I64, I64, I64]
         L.oracle_dijkstra_f32.argtypes = [P, I64, P, I64, P]
         L.oracle_dijkstra_i32.argtypes = [P, I64, P, I64, P]
         L.oracle_bruteforce_f64.argtypes = [P, I64, P]
@@ -93,6 +94,14 @@ def fw(W: np.ndarray, path: str | None = "next"):
         raise TypeError(f"unsupported dtype {D.dtype}")
     assert rc == 0
     return D, P
+
+
+def fw_steps(D: np.ndarray, P: np.ndarray | None, k0: int, k1: int) -> None:
+    """Outer iterations k in [k0, k1) of the FP32 triple loop, in place (timing samples)."""
+    assert D.dtype == np.float32 and D.flags["C_CONTIGUOUS"]
+    n = D.shape[0]
+    rc = lib().oracle_fw_f32_steps(_ptr(D), _ptr(P) if P is not None else None, n, k0, k1)
+    assert rc == 0
 
 
 def dijkstra(W: np.ndarray, srcs) -> np.ndarray:

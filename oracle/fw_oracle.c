@@ -74,6 +74,32 @@ int oracle_fw_f32(float *D, int32_t *P, int64_t n, int mode) {
   return 0;
 }
 
+/* ---- bounded sample: outer iterations k in [k0, k1) of the same FP32 triple loop ----------
+ * Used only by bench.py's cpu_baseline / --impl reference legs to time the oracle on a
+ * bounded slice of the benchmark workload (each k-step is n^2 relaxations). D must
+ * already hold W with a zero diagonal; P (next-hop) may be NULL. */
+int oracle_fw_f32_steps(float *D, int32_t *P, int64_t n, int64_t k0, int64_t k1) {
+  for (int64_t k = k0; k < k1 && k < n; ++k) {
+    const float *Dk = D + k * n;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      float *Di = D + i * n;
+      const float dik = Di[k];
+      if (isinf(dik)) continue;
+      int32_t *Pi = P ? P + i * n : NULL;
+      const int32_t pik = P ? Pi[k] : 0;
+      for (int64_t j = 0; j < n; ++j) {
+        const float s = dik + Dk[j];
+        if (s < Di[j]) {
+          Di[j] = s;
+          if (Pi) Pi[j] = pik;
+        }
+      }
+    }
+  }
+  return 0;
+}
+
 /* ---- Floyd–Warshall, INT32 (INF = 0x3FFFFFFF, sums of two values <= 2^31-2) ---- */
 int oracle_fw_i32(int32_t *D, int32_t *P, int64_t n, int mode) {
   for (int64_t i = 0; i < n; ++i) D[i * n + i] = 0;

@@ -1,0 +1,150 @@
+"""ctypes binding for libfwb200.so: same names as include/fw.h, argument marshalling only.
+
+Arrays may be numpy arrays (host entry points) or torch tensors (host or CUDA); raw
+integer addresses are accepted too. Non-zero status codes raise FwError carrying the
+code and fw_last_error().
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libfwb200.so")
+
+FW_INF_I32 = 0x3FFFFFFF
+FW_OK, FW_EINVAL, FW_ENOMEM, FW_ECUDA, FW_ENCCL, FW_ESTATE, FW_ERANGE = range(7)
+FW_PATH_NEXT_HOP, FW_PATH_LAST_K, FW_TIMING = 0, 1, 2
+_NAMES = {0: "FW_OK", 1: "FW_EINVAL", 2: "FW_ENOMEM", 3: "FW_ECUDA", 4: "FW_ENCCL",
+          5: "FW_ESTATE", 6: "FW_ERANGE"}
+
+
+class FwError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class FwStats(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64), ("n_pad", ctypes.c_int64), ("block", ctypes.c_int32),
+        ("rounds", ctypes.c_int32), ("is_int", ctypes.c_int32), ("path_mode", ctypes.c_int32),
+        ("solve_ms", ctypes.c_double), ("phase1_ms", ctypes.c_double),
+        ("phase2_ms", ctypes.c_double), ("phase3_ms", ctypes.c_double),
+        ("post_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
+        ("phase3_launches", ctypes.c_int64), ("phase3_relaxations", ctypes.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"{_LIB_PATH} is missing: build the CUDA extension first "
+                      "(python -c 'import __graft_entry__ as g; g.build()')")
+
+_lib = ctypes.CDLL(_LIB_PATH)
+_P, _I64, _I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+_lib.fw_init.argtypes = [_I, ctypes.c_uint]
+_lib.fw_free.argtypes = []
+_lib.fw_solve.argtypes = [_P, _P, _I64, _I, _I]
+_lib.fw_solve_i32.argtypes = [_P, _P, _I64, _I, _I]
+_lib.fw_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _P]
+_lib.fw_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _P]
+_lib.fw_last_error.restype = ctypes.c_char_p
+_lib.fw_last_stats.argtypes = [ctypes.POINTER(FwStats)]
+_lib.fw_version.restype = ctypes.c_char_p
+
+
+def _check(rc: int):
+    if rc != FW_OK:
+        raise FwError(rc, _lib.fw_last_error().decode())
+
+
+def _addr(x, dtype_name: str | None = None):
+    """Address of a numpy array / torch tensor / int; None -> NULL."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):          # torch.Tensor
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        if dtype_name and str(x.dtype) != f"torch.{dtype_name}":
+            raise TypeError(f"expected torch.{dtype_name}, got {x.dtype}")
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):            # numpy.ndarray
+        if not x.flags["C_CONTIGUOUS"] or not x.flags["WRITEABLE"]:
+            raise ValueError("array must be C-contiguous and writeable")
+        if dtype_name and x.dtype.name != dtype_name:
+            raise TypeError(f"expected {dtype_name}, got {x.dtype}")
+        return x.ctypes.data
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+def _n_of(dist, n):
+    if n is not None:
+        return int(n)
+    shape = tuple(dist.shape)
+    if len(shape) != 2 or shape[0] != shape[1]:
+        raise ValueError(f"dist must be n x n, got {shape}")
+    return shape[0]
+
+
+def fw_init(ngpus_max: int = 0, flags: int = 0) -> None:
+    _check(_lib.fw_init(ngpus_max, flags))
+
+
+def fw_free() -> None:
+    _check(_lib.fw_free())
+
+
+def fw_solve(dist, next=None, n=None, block: int = 0, ngpus: int = 0) -> None:
+    """FP32 host solve in place (dist: n x n float32; next: n x n int32 or None)."""
+    _check(_lib.fw_solve(_addr(dist, "float32"), _addr(next, "int32"), _n_of(dist, n), block, ngpus))
+
+
+def fw_solve_i32(dist, next=None, n=None, block: int = 0, ngpus: int = 0) -> None:
+    """INT32 host solve in place (no-edge = FW_INF_I32)."""
+    _check(_lib.fw_solve_i32(_addr(dist, "int32"), _addr(next, "int32"), _n_of(dist, n), block, ngpus))
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream   # torch.cuda.Stream
+
+
+def fw_solve_device_f32(d_dist, d_next=None, n=None, ld=None, block: int = 0, stream=None) -> None:
+    """FP32 device solve in place; d_dist/d_next CUDA tensors (or device addresses)."""
+    n = _n_of(d_dist, n)
+    ld = n if ld is None else ld
+    _check(_lib.fw_solve_device_f32(_addr(d_dist, "float32"), _addr(d_next, "int32"), n, ld, block,
+                                    _stream_handle(stream)))
+
+
+def fw_solve_device_i32(d_dist, d_next=None, n=None, ld=None, block: int = 0, stream=None) -> None:
+    n = _n_of(d_dist, n)
+    ld = n if ld is None else ld
+    _check(_lib.fw_solve_device_i32(_addr(d_dist, "int32"), _addr(d_next, "int32"), n, ld, block,
+                                    _stream_handle(stream)))
+
+
+def fw_last_error() -> str:
+    return _lib.fw_last_error().decode()
+
+
+def fw_last_stats() -> FwStats:
+    s = FwStats()
+    _check(_lib.fw_last_stats(ctypes.byref(s)))
+    return s
+
+
+def fw_version() -> str:
+    return _lib.fw_version().decode()

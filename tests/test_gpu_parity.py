@@ -1,0 +1,296 @@
+"""GPU parity: the CUDA path (through the C ABI, include/fw.h) against the CPU oracle
+(oracle/) on seeded synthetic inputs. BASELINE.json north_star correctness requirements:
+bit-exact D for integer-valued weights, rel 1e-5 for real FP32, P validated by
+reconstructing paths (never bitwise: ties are legal), Dijkstra rows at n >= 16384.
+"""
+import numpy as np
+import pytest
+
+import apsp_inputs as gen
+import oracle
+from helpers import INF, assert_D_matches, exact_data, next_consistency
+
+pytestmark = pytest.mark.gpu
+
+fw = pytest.importorskip("paper_1811_01201_b200")
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+class Ctx:
+    def __init__(self, flags):
+        self.flags = flags
+
+    def __enter__(self):
+        fw.fw_init(0, self.flags)
+        return self
+
+    def __exit__(self, *a):
+        fw.fw_free()
+
+
+def solve(W, block=0, path="next", device=False):
+    """Run the CUDA path on W (numpy); returns (D, P or None)."""
+    flags = fw.FW_PATH_LAST_K if path == "lastk" else 0
+    D = W.copy()
+    P = np.empty(W.shape, dtype=np.int32) if path else None
+    with Ctx(flags):
+        if device:
+            dD = torch.from_numpy(D).cuda()
+            dP = torch.from_numpy(P).cuda() if P is not None else None
+            f = fw.fw_solve_device_i32 if W.dtype == np.int32 else fw.fw_solve_device_f32
+            f(dD, dP, block=block, stream=torch.cuda.current_stream())
+            D = dD.cpu().numpy()
+            P = dP.cpu().numpy() if dP is not None else None
+        else:
+            f = fw.fw_solve_i32 if W.dtype == np.int32 else fw.fw_solve
+            f(D, P, block=block)
+    return D, P
+
+
+def check_against_oracle(W, block, path="next", device=False):
+    D, P = solve(W, block, path, device)
+    Dref, _ = oracle.fw(W, None)
+    exact = exact_data(W)
+    assert_D_matches(D, Dref, exact)
+    if path:
+        bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5, mode=path)
+        assert bad == 0, f"{bad} invalid paths, first at {divmod(first, W.shape[0])}"
+    return D, P
+
+
+# ---- sizes spanning several tiles with ragged tails, every block size, both types ----
+SIZES = [1, 2, 3, 31, 33, 127, 129, 200, 257, 383, 513]
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("block", [32, 64, 128])
+def test_complete_int_f32(n, block):
+    check_against_oracle(gen.generate("complete_int", n, 100 + n), block)
+
+
+@pytest.mark.parametrize("n", [65, 300, 640])
+@pytest.mark.parametrize("block", [32, 64, 128])
+def test_complete_real_f32(n, block):
+    check_against_oracle(gen.generate("complete_real", n, 200 + n), block)
+
+
+@pytest.mark.parametrize("n,p", [(100, 0.02), (257, 0.01), (500, 0.004), (700, 0.1)])
+@pytest.mark.parametrize("block", [32, 128])
+def test_er_int32_unreachable(n, p, block):
+    W = gen.generate("er_int", n, 300 + n, p=p, lo=1, hi=1000)
+    D, _ = check_against_oracle(W, block)
+    if p <= 0.01:
+        assert (D == INF).any()           # INF outputs really exercised (reading C-14)
+
+
+@pytest.mark.parametrize("n,p", [(333, 0.01), (450, 0.05)])
+def test_er_f32_inf(n, p):
+    D, P = check_against_oracle(gen.generate("er_int_f32", n, 400 + n, p=p, lo=1, hi=1000), 64)
+    assert np.isinf(D).any() == (p < 0.03)
+    assert ((P == -1) == (np.isinf(D))).all()
+
+
+@pytest.mark.parametrize("n", [100, 385])
+@pytest.mark.parametrize("block", [32, 128])
+def test_lastk_mode(n, block):
+    check_against_oracle(gen.generate("complete_int", n, 500 + n), block, path="lastk")
+    check_against_oracle(gen.generate("er_int", n, 501 + n, p=0.02, lo=1, hi=1000), block, path="lastk")
+
+
+@pytest.mark.parametrize("n", [64, 250, 512])
+def test_distance_only(n):
+    W = gen.generate("complete_real", n, 600 + n)
+    D, P = solve(W, 64, path=None)
+    assert P is None
+    assert_D_matches(D, oracle.fw(W, None)[0], exact=False)
+
+
+@pytest.mark.parametrize("n", [128, 256, 300])
+@pytest.mark.parametrize("dtype", [np.float32, np.int32])
+def test_device_entry(n, dtype):
+    kind = "complete_int" if dtype == np.float32 else "er_int"
+    W = gen.generate(kind, n, 700 + n, p=0.05, lo=1, hi=100)
+    check_against_oracle(W, 0, device=True)
+
+
+def test_device_entry_ld_and_stream():
+    """d_dist with a leading dimension > n, on a side stream."""
+    n, ld = 200, 256
+    W = gen.generate("complete_int", n, 42)
+    big = np.full((n, ld), 123.0, dtype=np.float32)
+    big[:, :n] = W
+    dD = torch.from_numpy(big).cuda()
+    dP = torch.full((n, ld), -7, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with Ctx(0):
+        fw.fw_solve_device_f32(dD, dP, n=n, ld=ld, block=64, stream=s)
+    D = dD.cpu().numpy()
+    P = dP.cpu().numpy()
+    assert (D[:, n:] == 123.0).all() and (P[:, n:] == -7).all()     # padding columns untouched
+    Dref, _ = oracle.fw(W, None)
+    np.testing.assert_array_equal(D[:, :n], Dref)
+    assert oracle.check_paths(W, D[:, :n].copy(), P[:, :n].copy())[0] == 0
+
+
+# ---- closed forms and degenerate cases ------------------------------------------------
+@pytest.mark.parametrize("n", [1, 2, 130, 1000])
+def test_ring(n):
+    W = gen.ring(n, 1)
+    D, P = solve(W, 64)
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    np.testing.assert_array_equal(D, ((j - i) % n).astype(np.float32))
+    np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % n))
+
+
+def test_abs_diff_and_uniform():
+    n = 300
+    W = gen.abs_diff(n)
+    D, P = solve(W, 32)
+    np.testing.assert_array_equal(D, W)
+    np.testing.assert_array_equal(P, np.broadcast_to(np.arange(n), (n, n)))
+    U = gen.uniform_complete(257, 5.0)
+    D, P = solve(U, 128)
+    np.testing.assert_array_equal(D, U)
+
+
+def test_empty_graph_and_two_components():
+    E = gen.empty_graph(150, np.int32)
+    D, P = solve(E, 32)
+    np.testing.assert_array_equal(D, E)
+    assert (P[~np.eye(150, dtype=bool)] == -1).all() and (np.diag(P) == np.arange(150)).all()
+    W = gen.two_components(400, 9, p=0.05)
+    D, _ = check_against_oracle(W, 64)
+    assert (D[:200, 200:] == INF).all() and (D[200:, :200] == INF).all()
+
+
+def test_diagonal_forced_zero():
+    W = gen.generate("complete_int", 70, 3)
+    np.fill_diagonal(W, 55.0)
+    D, P = solve(W, 32)
+    assert (np.diag(D) == 0).all()
+    W0 = W.copy()
+    np.fill_diagonal(W0, 0)
+    np.testing.assert_array_equal(D, oracle.fw(W0, None)[0])
+
+
+def test_block_size_invariance_integer():
+    """Integer data: D bitwise identical across BS (reading C-6)."""
+    W = gen.generate("er_int", 450, 77, p=0.03, lo=1, hi=1000)
+    Ds = [solve(W, b)[0] for b in (32, 64, 128)]
+    assert all(np.array_equal(Ds[0], d) for d in Ds[1:])
+
+
+def test_determinism():
+    W = gen.generate("complete_real", 513, 5)
+    a = solve(W, 128)
+    b = solve(W, 128)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+# ---- validation / error contract (fw.h) -----------------------------------------------
+def test_validation_errors_leave_outputs_untouched():
+    n = 40
+    with Ctx(0):
+        for bad in (-1.0, np.nan):
+            W = gen.generate("complete_int", n, 1)
+            W[3, 5] = bad
+            D = W.copy()
+            P = np.full((n, n), 77, dtype=np.int32)
+            with pytest.raises(fw.FwError) as e:
+                fw.fw_solve(D, P, block=32)
+            assert e.value.code == fw.FW_EINVAL
+            np.testing.assert_array_equal(np.isnan(D), np.isnan(W))
+            np.testing.assert_array_equal(D[~np.isnan(W)], W[~np.isnan(W)])
+            assert (P == 77).all()
+        Wi = gen.generate("er_int", n, 2, p=0.5, lo=1, hi=10)
+        Wi[1, 2] = INF + 1
+        with pytest.raises(fw.FwError) as e:
+            fw.fw_solve_i32(Wi.copy(), None, block=32)
+        assert e.value.code == fw.FW_EINVAL
+        Wi[1, 2] = 40_000_000            # (n-1) * w >= INF -> FW_ERANGE
+        with pytest.raises(fw.FwError) as e:
+            fw.fw_solve_i32(Wi.copy(), None, block=32)
+        assert e.value.code == fw.FW_ERANGE
+        with pytest.raises(fw.FwError) as e:
+            fw.fw_solve(gen.generate("complete_int", n, 1), None, block=48)
+        assert e.value.code == fw.FW_EINVAL
+        with pytest.raises(fw.FwError) as e:
+            fw.fw_solve(np.zeros((4, 4), np.float32), None, block=0, ngpus=2)
+        assert e.value.code == fw.FW_EINVAL
+    with pytest.raises(fw.FwError):
+        fw.fw_solve(np.zeros((4, 4), np.float32))   # after fw_free: FW_ESTATE
+
+
+def test_stats_and_timing():
+    W = gen.generate("complete_int", 1000, 8)
+    with Ctx(fw.FW_TIMING):
+        D = W.copy()
+        P = np.empty_like(W, dtype=np.int32)
+        fw.fw_solve(D, P, block=128)
+        s = fw.fw_last_stats()
+    assert s.n == 1000 and s.n_pad == 1024 and s.block == 128 and s.rounds == 8
+    assert s.solve_ms > 0 and s.phase3_ms > 0 and s.phase1_ms > 0 and s.post_ms >= 0
+    assert s.phase3_ms <= s.solve_ms
+
+
+# ---- BASELINE.json configs ---------------------------------------------------------------
+def test_config_C1_full():
+    """configs[0]: n=512 complete, FP32 integers [1,100], tile 32: bit-exact D, all paths."""
+    W = gen.config_matrix("C1")
+    check_against_oracle(W, 32)
+
+
+def test_config_C2_full_oracle():
+    """configs[1]: n=4096 complete, real [1,100), BS=128: rel 1e-5, paths for all pairs."""
+    W = gen.config_matrix("C2")
+    check_against_oracle(W, 128)
+
+
+def _dijkstra_rows_check(W, D, P, seed, exact, count=64):
+    src = gen.sources(W.shape[0], seed, count)
+    R = oracle.dijkstra(W, src)
+    Dr = D[src]
+    if W.dtype == np.int32:
+        np.testing.assert_array_equal(Dr.astype(np.int64), R)
+    elif exact:
+        np.testing.assert_array_equal(Dr.astype(np.float64), R)
+    else:
+        rel = np.abs(Dr.astype(np.float64) - R) / np.maximum(1.0, np.abs(R))
+        assert np.array_equal(np.isinf(Dr), np.isinf(R)) and rel[np.isfinite(R)].max() <= 1e-5
+    bad, first = oracle.check_paths(W, D, P, rows=src, rtol=0.0 if exact else 1e-5)
+    assert bad == 0, f"{bad} bad paths from the seeded sources, first {first}"
+
+
+def test_config_C3_er_int32():
+    """configs[2]: n=8192 ER p=0.1 INT32 [1,1000]: Dijkstra rows bitwise + O(n^2) next check."""
+    c = gen.CONFIGS["C3"]
+    W = gen.config_matrix("C3")
+    D, P = solve(W, 128)
+    _dijkstra_rows_check(W, D, P, c["seed"], True)
+    assert next_consistency(W, D, P, exact=True) == 0
+
+
+def test_config_C3_sparse_unreachable():
+    """Supplementary C3' (reading C-14): sparse ER so INF outputs and next = -1 occur."""
+    W = gen.generate("er_int", 4096, 33, p=0.0004, lo=1, hi=1000)
+    D, P = solve(W, 128)
+    assert (D == INF).any()
+    _dijkstra_rows_check(W, D, P, 33, True)
+    assert next_consistency(W, D, P, exact=True) == 0
+
+
+@pytest.mark.slow
+def test_config_C4_16384():
+    """configs[3]: n=16384 complete, FP32 integers: Dijkstra rows bitwise, next O(n^2)."""
+    c = gen.CONFIGS["C4"]
+    W = gen.config_matrix("C4")
+    D, P = solve(W, 128)
+    _dijkstra_rows_check(W, D, P, c["seed"], True)
+    assert next_consistency(W, D, P, exact=True) == 0

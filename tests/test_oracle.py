@@ -237,3 +237,18 @@ def test_sources():
     assert len(s) == 64 and len(set(s.tolist())) == 64 and (np.diff(s) > 0).all()
     np.testing.assert_array_equal(s, gen.sources(16384, 4))
     assert len(gen.sources(10, 1)) == 10
+
+
+def test_fw_steps_equals_full_loop():
+    """The bounded-sample entry used for CPU timing runs the same loop as oracle.fw."""
+    n = 96
+    W = gen.generate("complete_real", n, 4)
+    D, P = oracle.fw(W)
+    D2 = W.copy()
+    np.fill_diagonal(D2, 0)
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    P2 = np.where(i == j, i, np.where(np.isinf(D2), -1, j)).astype(np.int32)
+    oracle.fw_steps(D2, P2, 0, 40)
+    oracle.fw_steps(D2, P2, 40, n)
+    np.testing.assert_array_equal(D, D2)
+    np.testing.assert_array_equal(P, P2)
