@@ -29,6 +29,7 @@ class FwStats(ctypes.Structure):
     _fields_ = [
         ("n", ctypes.c_int64), ("n_pad", ctypes.c_int64), ("block", ctypes.c_int32),
         ("rounds", ctypes.c_int32), ("is_int", ctypes.c_int32), ("path_mode", ctypes.c_int32),
+        ("p_method", ctypes.c_int32),
         ("solve_ms", ctypes.c_double), ("phase1_ms", ctypes.c_double),
         ("phase2_ms", ctypes.c_double), ("phase3_ms", ctypes.c_double),
         ("post_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),

@@ -1,0 +1,251 @@
+// Phase-3 microkernel variant benchmark (development tool, not part of the library).
+// Times one phase-3 launch (n x n output, K-depth BS=128) per variant on random data
+// and reports relaxations / clock / SM, to pick the main-loop schedule for sm_100a.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdint.h>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// VAR bits: 1 = split B into two halves (fewer live registers), 2 = min3 reassociation,
+//           4 = 1 CTA/SM (launch bounds 256,1), 8 = 3 smem stages
+template <int VAR>
+__global__ void __launch_bounds__(256, (VAR & 4) ? 1 : 2)
+p3(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
+  constexpr int TM = 128, TN = 128, BK = 32, AS = BK + 4, SA = TM * AS, SB = BK * TN, ST = SA + SB;
+  constexpr int NS = (VAR & 8) ? 3 : 2;
+  extern __shared__ __align__(16) float sm[];
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
+  if ((i0 >= kb && i0 < kb + 128) || (j0 >= kb && j0 < kb + 128)) return;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int a_r = tid / 8, a_c = (tid % 8) * 4;
+  const float *a_src = A + (int64_t)(i0 + a_r) * ld + a_c;
+  const int b_k = tid / TN, b_j = tid % TN;
+  const float *b_src = B + (int64_t)b_k * ld + j0 + b_j;
+  auto load = [&](int s, int k0) {
+    float *as = sm + s * ST, *bs = as + SA;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cp_async16(as + (a_r + 32 * t) * AS + a_c, a_src + k0 + (int64_t)32 * t * ld);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int k = b_k + 2 * t;
+      cp_async4(bs + ((k >> 2) * TN + b_j) * 4 + (k & 3), b_src + (int64_t)(k0 + 2 * t) * ld);
+    }
+    cp_commit();
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = __int_as_float(0x7f800000);
+  const int nch = Kd / BK;
+  load(0, 0);
+  if (NS == 3 && nch > 1) load(1, BK);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (NS == 3) {
+      if (ch + 2 < nch) { load((ch + 2) % 3, (ch + 2) * BK); cp_wait<2>(); }
+      else if (ch + 1 < nch) cp_wait<1>();
+      else cp_wait<0>();
+    } else {
+      if (ch + 1 < nch) { load((ch + 1) & 1, (ch + 1) * BK); cp_wait<1>(); } else cp_wait<0>();
+    }
+    __syncthreads();
+    const float *as = sm + (ch % NS) * ST + ty * AS;
+    const float *bs = sm + (ch % NS) * ST + SA + tx * 4;
+#pragma unroll
+    for (int q = 0; q < BK / 4; ++q) {
+      constexpr int HALVES = (VAR & 1) ? 2 : 1;
+      constexpr int NB = 8 / HALVES;
+#pragma unroll
+      for (int h = 0; h < HALVES; ++h) {
+        float4 b[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) b[c] = *reinterpret_cast<const float4 *>(bs + (q * TN + 16 * (c + h * NB)) * 4);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float4 a = *reinterpret_cast<const float4 *>(as + 16 * r * AS + 4 * q);
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            const float2 s01 = __fadd2_rn(make_float2(a.x, a.y), make_float2(b[c].x, b[c].y));
+            const float2 s23 = __fadd2_rn(make_float2(a.z, a.w), make_float2(b[c].z, b[c].w));
+            float &x = acc[r][c + h * NB];
+            if (VAR & 2) {
+              const float t = fminf(fminf(s01.x, s01.y), s23.x);
+              x = fminf(x, fminf(t, s23.y));
+            } else {
+              x = fminf(x, fminf(s01.x, s01.y));
+              x = fminf(x, fminf(s23.x, s23.y));
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + ty + 16 * r;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int j = j0 + tx + 16 * c;
+      float o = C[(int64_t)i * ld + j];
+      if (acc[r][c] < o) C[(int64_t)i * ld + j] = acc[r][c];
+    }
+  }
+}
+
+
+// j-pair variant: FADD2(a_ik broadcast, (b_kj, b_kj+1)); B row-major [k][j] in smem
+// (16-B cp.async); thread owns rows ty+16r and columns 4tx+64h+{0..3}.
+template <int VAR>
+__global__ void __launch_bounds__(256, 2)
+p3j(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
+  constexpr int TM = 128, TN = 128, BK = 32, AS = BK + 4, BSTR = TN + ((VAR & 32) ? 4 : 0);
+  constexpr int SA = TM * AS, SB = BK * BSTR, ST = SA + SB;
+  extern __shared__ __align__(16) float sm[];
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
+  if ((i0 >= kb && i0 < kb + 128) || (j0 >= kb && j0 < kb + 128)) return;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int a_r = tid / 8, a_c = (tid % 8) * 4;
+  const float *a_src = A + (int64_t)(i0 + a_r) * ld + a_c;
+  const int b_k = tid / 32, b_c = (tid % 32) * 4;
+  const float *b_src = B + (int64_t)b_k * ld + j0 + b_c;
+  auto load = [&](int s, int k0) {
+    float *as = sm + s * ST, *bs = as + SA;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cp_async16(as + (a_r + 32 * t) * AS + a_c, a_src + k0 + (int64_t)32 * t * ld);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cp_async16(bs + (b_k + 8 * t) * BSTR + b_c, b_src + (int64_t)(k0 + 8 * t) * ld);
+    cp_commit();
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = __int_as_float(0x7f800000);
+  const int nch = Kd / BK;
+  load(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) { load((ch + 1) & 1, (ch + 1) * BK); cp_wait<1>(); } else cp_wait<0>();
+    __syncthreads();
+    const float *as = sm + (ch & 1) * ST + ty * AS;
+    const float *bs = sm + (ch & 1) * ST + SA + tx * 4;
+#pragma unroll
+    for (int q = 0; q < BK / 4; ++q) {
+      float4 b[4][2];   // b[k][h] = B[4q+k][4tx+64h .. +3]
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) b[k][h] = *reinterpret_cast<const float4 *>(bs + (4 * q + k) * BSTR + 64 * h);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const float4 a = *reinterpret_cast<const float4 *>(as + 16 * r * AS + 4 * q);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int kp = 0; kp < 2; ++kp) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 b0 = b[2 * kp][h], b1 = b[2 * kp + 1][h];
+            const float2 s0 = __fadd2_rn(make_float2(av[2 * kp], av[2 * kp]), make_float2(b0.x, b0.y));
+            const float2 s1 = __fadd2_rn(make_float2(av[2 * kp + 1], av[2 * kp + 1]), make_float2(b1.x, b1.y));
+            const float2 s2 = __fadd2_rn(make_float2(av[2 * kp], av[2 * kp]), make_float2(b0.z, b0.w));
+            const float2 s3 = __fadd2_rn(make_float2(av[2 * kp + 1], av[2 * kp + 1]), make_float2(b1.z, b1.w));
+            float *x = &acc[r][4 * h];
+            x[0] = fminf(x[0], fminf(s0.x, s1.x));
+            x[1] = fminf(x[1], fminf(s0.y, s1.y));
+            x[2] = fminf(x[2], fminf(s2.x, s3.x));
+            x[3] = fminf(x[3], fminf(s2.y, s3.y));
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + ty + 16 * r;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float4 *p = reinterpret_cast<float4 *>(C + (int64_t)i * ld + j0 + 4 * tx + 64 * h);
+      float4 o = *p;
+      float4 m = make_float4(fminf(o.x, acc[r][4 * h]), fminf(o.y, acc[r][4 * h + 1]),
+                             fminf(o.z, acc[r][4 * h + 2]), fminf(o.w, acc[r][4 * h + 3]));
+      if (m.x < o.x || m.y < o.y || m.z < o.z || m.w < o.w) *p = m;
+    }
+  }
+}
+
+template <int VAR>
+int runj(float *D, int64_t n, int sms, int clk_khz) {
+  constexpr int BSTR = 128 + ((VAR & 32) ? 4 : 0);
+  const int bytes = 2 * (128 * 36 + 32 * BSTR) * 4;
+  CK(cudaFuncSetAttribute(p3j<VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  dim3 g(n / 128, n / 128);
+  const int kb = 128 * 50;
+  for (int w = 0; w < 2; ++w) p3j<VAR><<<g, 256, bytes>>>(D, n, D + kb, D + (int64_t)kb * n, 128, kb);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int reps = 10;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) p3j<VAR><<<g, 256, bytes>>>(D, n, D + kb, D + (int64_t)kb * n, 128, kb);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  const double relax = (double)(n - 128) * (n - 128) * 128;
+  printf("{\"variant\": \"j%d\", \"ms\": %.4f, \"relax_per_clk_sm_at_max_clock\": %.2f, \"tflops\": %.3f}\n", VAR, ms,
+         relax / (ms * 1e-3) / (sms * (double)clk_khz * 1e3), 2 * relax / (ms * 1e-3) / 1e12);
+  return 0;
+}
+
+template <int VAR>
+int run(float *D, int64_t n, int sms, int clk_khz) {
+  constexpr int NS = (VAR & 8) ? 3 : 2;
+  const int bytes = NS * (128 * 36 + 32 * 128) * 4;
+  CK(cudaFuncSetAttribute(p3<VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  dim3 g(n / 128, n / 128);
+  const int kb = 128 * 50;
+  for (int w = 0; w < 2; ++w) p3<VAR><<<g, 256, bytes>>>(D, n, D + kb, D + (int64_t)kb * n, 128, kb);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int reps = 10;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) p3<VAR><<<g, 256, bytes>>>(D, n, D + kb, D + (int64_t)kb * n, 128, kb);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  const double relax = (double)(n - 128) * (n - 128) * 128;
+  const double per_clk_sm = relax / (ms * 1e-3) / (sms * (double)clk_khz * 1e3);
+  printf("{\"variant\": %d, \"ms\": %.4f, \"relax_per_clk_sm_at_max_clock\": %.2f, \"tflops\": %.3f}\n", VAR, ms,
+         per_clk_sm, 2 * relax / (ms * 1e-3) / 1e12);
+  return 0;
+}
+
+int main() {
+  int sms, clk;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const int64_t n = 16384;
+  std::vector<float> h(n * n);
+  uint64_t x = 88172645463325252ull;
+  for (auto &v : h) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = 1.0f + (float)(x % 100); }
+  float *D; CK(cudaMalloc(&D, n * n * 4));
+  CK(cudaMemcpy(D, h.data(), n * n * 4, cudaMemcpyHostToDevice));
+  run<0>(D, n, sms, clk); runj<0>(D, n, sms, clk); runj<32>(D, n, sms, clk); run<0>(D, n, sms, clk); runj<0>(D, n, sms, clk);
+  return 0;
+}

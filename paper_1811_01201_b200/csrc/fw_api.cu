@@ -76,6 +76,7 @@ struct Ctx {
   unsigned flags = 0;
   cudaStream_t stream = nullptr;   // internal stream for the host entry points
   DevBuf ws_d, ws_t;               // padded workspaces (D, tags/P)
+  DevBuf ws_b;                     // backup of W for a speculative key run (in place)
   DevBuf user_d, user_t;           // device copies of host buffers (host entry points)
   DevBuf scratch;                  // validation flags
   void *pinned = nullptr;          // staging for pageable host buffers
@@ -87,8 +88,11 @@ struct Ctx {
 
 Ctx *g_ctx = nullptr;
 
-constexpr int kBK = 32;
 constexpr size_t kStageBytes = 64ull << 20;  // pinned staging chunk
+// Largest initial/stored distance for which key sums stay exact (kernels header, KEY_*):
+// FP32: 2*(T*128+127) < 2^24; INT32: 2*(T*128+127) < FW_INF_I32 (INF + key < 2^31 as well).
+constexpr int64_t kKeyMaxF32 = 65534;
+constexpr int64_t kKeyMaxI32 = 4194302;
 
 int ensure_events(Ctx &c, size_t count) {
   while (c.events.size() < count) {
@@ -100,80 +104,154 @@ int ensure_events(Ctx &c, size_t count) {
 }
 
 // ---- kernel launch wrappers ---------------------------------------------------------
-template <typename T, int TM, int TN, bool TAGS>
-int launch_tile(dim3 grid, cudaStream_t st, T *C, int64_t ldc, const T *A, int64_t lda,
-                const T *B, int64_t ldb, int32_t *tags, int64_t ldt, int Kd, int mr_lo,
-                int mr_hi, int mc_lo, int mc_hi, int tag) {
-  constexpr int bytes = TileSmem<TM, TN, kBK>::kBytes;
-  auto kern = minplus_tile_kernel<T, TM, TN, kBK, TAGS>;
-  static bool configured = false;  // per instantiation
+template <typename T, int TM, int TN, int MODE>
+int launch_tile(dim3 grid, cudaStream_t st, T *D, int32_t *P, const TileArgs &a, int *maxkey) {
+  constexpr int bytes = TileShape<TM, TN>::kBytes;
+  auto kern = minplus_tile_kernel<T, TM, TN, MODE>;
+  static bool configured = false;  // per instantiation (one device per process)
   if (!configured) {
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     configured = true;
   }
-  kern<<<grid, kThreads, bytes, st>>>(C, ldc, A, lda, B, ldb, tags, ldt, Kd, mr_lo, mr_hi,
-                                      mc_lo, mc_hi, tag);
+  kern<<<grid, kThreads, bytes, st>>>(D, P, a, maxkey);
   CU(cudaGetLastError());
   return FW_OK;
 }
 
-template <typename T, bool TAGS>
-int launch_phase1(cudaStream_t st, T *D, int64_t ld, int32_t *tags, int kb, int BS, int K) {
-  const int bytes = BS * BS * (int)sizeof(T);
-  auto kern = phase1_kernel<T, TAGS>;
+TileArgs tile_args(int64_t ld, int kb, int BS, int tag) {
+  TileArgs a{};
+  a.ld = ld;
+  a.kb = kb;
+  a.Kd = BS;
+  a.tag = tag;
+  for (int z = 0; z < 2; ++z) {
+    a.mr_lo[z] = a.mr_hi[z] = a.mc_lo[z] = a.mc_hi[z] = 0;
+    a.row0[z] = a.col0[z] = a.pstage[z] = a.xrow[z] = 0;
+  }
+  return a;
+}
+
+template <typename T, int BS, int MODE>
+int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int kb, int K, int *maxkey) {
+  const int bytes = BS * BS * (int)sizeof(T) * (MODE == MODE_KEY_NEXT ? 2 : 1);
+  auto kern = phase1_kernel<T, BS, MODE>;
   static bool configured = false;
   if (!configured) {
-    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 4));
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * BS * BS * 4));
     configured = true;
   }
-  kern<<<1, 1024, bytes, st>>>(D, ld, tags, ld, kb, BS, K);
+  kern<<<1, 1024, bytes, st>>>(D, P, ld, kb, K, maxkey);
   CU(cudaGetLastError());
   return FW_OK;
+}
+
+template <typename T, int MODE>
+int launch_phase1(cudaStream_t st, T *D, int32_t *P, int64_t ld, int kb, int BS, int K, int *maxkey) {
+  switch (BS) {
+    case 32: return launch_phase1_bs<T, 32, MODE>(st, D, P, ld, kb, K, maxkey);
+    case 64: return launch_phase1_bs<T, 64, MODE>(st, D, P, ld, kb, K, maxkey);
+    case 128: return launch_phase1_bs<T, 128, MODE>(st, D, P, ld, kb, K, maxkey);
+  }
+  return fail(FW_EINVAL, "unsupported block size %d", BS);
 }
 
 // Phase 2: row strip D[kb:kb+BS, :] and column strip D[:, kb:kb+BS] relaxed
-// through the closed diagonal block D_KK* (min-plus product form, reading R7).
-template <typename T, bool TAGS, int BS>
-int launch_phase2_bs(cudaStream_t st, T *D, int64_t ld, int32_t *tags, int64_t n_pad, int kb,
-                     int K) {
-  T *rowC = D + (int64_t)kb * ld;
-  T *colC = D + kb;
-  const T *Dkk = D + (int64_t)kb * ld + kb;
-  int32_t *rowT = tags ? tags + (int64_t)kb * ld : nullptr;
-  int32_t *colT = tags ? tags + kb : nullptr;
+// through the closed diagonal block D_KK* (min-plus product form, reading R7). Both strips
+// exclude the diagonal block itself. BS = 128: one launch (blockIdx.z picks the strip).
+template <typename T, int MODE, int BS>
+int launch_phase2_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int K,
+                     int *maxkey) {
   const int tiles = (int)(n_pad / 128);
-  // row strip: C = A? no: C = B (in place), A = D_KK*; exclude the diagonal block columns
-  TRY((launch_tile<T, BS, 128, TAGS>(dim3(tiles, 1), st, rowC, ld, Dkk, ld, rowC, ld, rowT, ld,
-                                     BS, 0, 0, kb, kb + BS, K)));
-  // column strip: C = A (in place), B = D_KK*; exclude the diagonal block rows
-  TRY((launch_tile<T, 128, BS, TAGS>(dim3(1, tiles), st, colC, ld, colC, ld, Dkk, ld, colT, ld,
-                                     BS, kb, kb + BS, 0, 0, K)));
-  return FW_OK;
+  TileArgs a = tile_args(ld, kb, BS, K);
+  // z = 0: row strip, tiles BS x 128 across the columns; exclude the diagonal block columns
+  a.row0[0] = kb; a.col0[0] = 0; a.mc_lo[0] = kb; a.mc_hi[0] = kb + BS;
+  // z = 1: column strip, tiles 128 x BS down the rows; exclude the diagonal block rows.
+  // Its arg-min column lies inside the strip being updated: gather P from an smem copy.
+  a.row0[1] = 0; a.col0[1] = kb; a.mr_lo[1] = kb; a.mr_hi[1] = kb + BS; a.pstage[1] = 1;
+  a.xrow[1] = 1;
+  if (BS == 128) return launch_tile<T, 128, 128, MODE>(dim3(tiles, 1, 2), st, D, P, a, maxkey);
+  TileArgs r = a, c = a;
+  c.row0[0] = c.row0[1]; c.col0[0] = c.col0[1]; c.mr_lo[0] = c.mr_lo[1]; c.mr_hi[0] = c.mr_hi[1];
+  c.mc_lo[0] = c.mc_hi[0] = 0; c.pstage[0] = 1; c.xrow[0] = 1;
+  TRY((launch_tile<T, BS, 128, MODE>(dim3(tiles, 1, 1), st, D, P, r, maxkey)));
+  return launch_tile<T, 128, BS, MODE>(dim3(tiles, 1, 1), st, D, P, c, maxkey);
 }
 
-template <typename T, bool TAGS>
-int launch_phase2(cudaStream_t st, T *D, int64_t ld, int32_t *tags, int64_t n_pad, int kb,
-                  int BS, int K) {
+template <typename T, int MODE>
+int launch_phase2(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int BS,
+                  int K, int *maxkey) {
   switch (BS) {
-    case 32: return launch_phase2_bs<T, TAGS, 32>(st, D, ld, tags, n_pad, kb, K);
-    case 64: return launch_phase2_bs<T, TAGS, 64>(st, D, ld, tags, n_pad, kb, K);
-    case 128: return launch_phase2_bs<T, TAGS, 128>(st, D, ld, tags, n_pad, kb, K);
+    case 32: return launch_phase2_bs<T, MODE, 32>(st, D, P, ld, n_pad, kb, K, maxkey);
+    case 64: return launch_phase2_bs<T, MODE, 64>(st, D, P, ld, n_pad, kb, K, maxkey);
+    case 128: return launch_phase2_bs<T, MODE, 128>(st, D, P, ld, n_pad, kb, K, maxkey);
   }
   return fail(FW_EINVAL, "unsupported block size %d", BS);
 }
 
 // Phase 3: D_IJ <- min(D_IJ, D_IK (x) D_KJ) for all I != K, J != K.
-template <typename T, bool TAGS>
-int launch_phase3(cudaStream_t st, T *D, int64_t ld, int32_t *tags, int64_t n_pad, int kb,
-                  int BS, int K) {
+template <typename T, int MODE>
+int launch_phase3(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int BS,
+                  int K, int *maxkey) {
   const int tiles = (int)(n_pad / 128);
-  return launch_tile<T, 128, 128, TAGS>(dim3(tiles, tiles), st, D, ld, D + kb, ld,
-                                        D + (int64_t)kb * ld, ld, tags, ld, BS, kb, kb + BS, kb,
-                                        kb + BS, K);
+  TileArgs a = tile_args(ld, kb, BS, K);
+  a.mr_lo[0] = a.mc_lo[0] = kb;
+  a.mr_hi[0] = a.mc_hi[0] = kb + BS;
+  return launch_tile<T, 128, 128, MODE>(dim3(tiles, tiles, 1), st, D, P, a, maxkey);
 }
 
 template <typename T>
 constexpr bool is_int_v() { return std::is_integral<T>::value; }
+
+struct RoundTimes {
+  bool on;
+  cudaEvent_t *ev;  // 3 per round: after phase 1, after phase 2, after phase 3
+};
+
+template <typename T, int MODE>
+int run_rounds(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int BS, int R,
+               int *maxkey, RoundTimes rt) {
+  for (int K = 0; K < R; ++K) {
+    const int kb = K * BS;
+    TRY((launch_phase1<T, MODE>(st, D, P, ld, kb, BS, K, maxkey)));
+    if (rt.on) CU(cudaEventRecord(rt.ev[3 * K], st));
+    TRY((launch_phase2<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
+    if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 1], st));
+    TRY((launch_phase3<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
+    if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 2], st));
+  }
+  return FW_OK;
+}
+
+template <typename T, int MODE>
+int run_init(cudaStream_t st, const T *src, int64_t ld_src, int64_t n, T *D, int32_t *P, int64_t ld,
+             int64_t n_pad) {
+  dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)n_pad);
+  init_kernel<T, MODE><<<g, 256, 0, st>>>(src, ld_src, n, D, P, ld, n_pad);
+  CU(cudaGetLastError());
+  return FW_OK;
+}
+
+template <typename T>
+int dispatch_init(int mode, cudaStream_t st, const T *src, int64_t ld_src, int64_t n, T *D,
+                  int32_t *P, int64_t ld, int64_t n_pad) {
+  switch (mode) {
+    case MODE_PLAIN: return run_init<T, MODE_PLAIN>(st, src, ld_src, n, D, P, ld, n_pad);
+    case MODE_TAG: return run_init<T, MODE_TAG>(st, src, ld_src, n, D, P, ld, n_pad);
+    case MODE_KEY_NEXT: return run_init<T, MODE_KEY_NEXT>(st, src, ld_src, n, D, P, ld, n_pad);
+    default: return run_init<T, MODE_KEY_LASTK>(st, src, ld_src, n, D, P, ld, n_pad);
+  }
+}
+
+template <typename T>
+int dispatch_rounds(int mode, cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int BS,
+                    int R, int *maxkey, RoundTimes rt) {
+  switch (mode) {
+    case MODE_PLAIN: return run_rounds<T, MODE_PLAIN>(st, D, P, ld, n_pad, BS, R, maxkey, rt);
+    case MODE_TAG: return run_rounds<T, MODE_TAG>(st, D, P, ld, n_pad, BS, R, maxkey, rt);
+    case MODE_KEY_NEXT: return run_rounds<T, MODE_KEY_NEXT>(st, D, P, ld, n_pad, BS, R, maxkey, rt);
+    default: return run_rounds<T, MODE_KEY_LASTK>(st, D, P, ld, n_pad, BS, R, maxkey, rt);
+  }
+}
 
 // ---- the solve on device buffers ----------------------------------------------------
 // src: n rows of ld_src elements (in/out); next: n rows of ld_next int32 or nullptr.
@@ -183,12 +261,13 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
   const bool int_t = is_int_v<T>();
   const int64_t n_pad = (n + 127) / 128 * 128;
   const bool want_p = next != nullptr;
-  const int path_mode = want_p ? ((c.flags & FW_PATH_LAST_K) ? 1 : 0) : -1;
+  const bool lastk = (c.flags & FW_PATH_LAST_K) != 0;
+  const int path_mode = want_p ? (lastk ? 1 : 0) : -1;
   const bool timing = (c.flags & FW_TIMING) != 0;
 
   // 1. validation (read-only; outputs untouched on error)
   TRY(c.scratch.ensure(64));
-  int *d_flags = static_cast<int *>(c.scratch.p);
+  int *d_flags = static_cast<int *>(c.scratch.p);   // [0] flags [1] max weight [2] max key
   CU(cudaMemsetAsync(d_flags, 0, 16, st));
   {
     const int64_t total = n * n;
@@ -196,67 +275,99 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
     validate_kernel<T><<<std::max(blocks, 1), 256, 0, st>>>(src, ld_src, n, d_flags, d_flags + 1);
     CU(cudaGetLastError());
   }
-  int h_flags[2] = {0, 0};
+  int h_flags[4] = {0, 0, 0, 0};
   CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   if (h_flags[0] & 1)
     return fail(FW_EINVAL, int_t ? "weight outside [0, FW_INF_I32]" : "negative or NaN weight");
+  double maxw;
+  if (int_t) {
+    maxw = (double)h_flags[1];
+  } else {
+    float f;
+    memcpy(&f, &h_flags[1], 4);
+    maxw = f;
+  }
   if (int_t && n > 1 && (int64_t)(n - 1) * (int64_t)h_flags[1] >= (int64_t)FW_INF_I32)
     return fail(FW_ERANGE, "(n-1)*max_weight = %lld >= FW_INF_I32: finite path sums could reach INF",
                 (long long)(n - 1) * h_flags[1]);
 
-  // 2. placement: in place when the caller's buffer already has the padded layout
+  // 2. P mode: exact arg-min keys for integer-valued data within the key range, else tags
+  const int64_t key_max = int_t ? kKeyMaxI32 : kKeyMaxF32;
+  const bool integral = int_t || !(h_flags[0] & 2);
+  const bool has_inf = (h_flags[0] & 4) != 0;
+  int mode = MODE_PLAIN;
+  bool key_static = false;
+  if (want_p) {
+    mode = MODE_TAG;
+    if (integral && maxw <= (double)key_max) {
+      mode = lastk ? MODE_KEY_LASTK : MODE_KEY_NEXT;
+      // stored finite values never exceed max(W) without INF entries; otherwise a path
+      // value is at most (n-1)*max(W) — or is checked after the solve (max stored key)
+      key_static = !has_inf || (double)(n - 1) * maxw <= (double)key_max;
+    }
+  }
+  const int key_limit = int_t ? (int)(key_max * 128 + 127) : [] {
+    float f = (float)(kKeyMaxF32 * 128 + 127);
+    int b;
+    memcpy(&b, &f, 4);
+    return b;
+  }();
+
+  // 3. placement: in place when the caller's buffer already has the padded layout
   const bool inplace = n == n_pad && ld_src == n && ((uintptr_t)src % 16 == 0) &&
                        (!want_p || (ld_next == n && (uintptr_t)next % 16 == 0));
   T *D = src;
-  int32_t *Tg = next;
+  int32_t *Pm = next;
   int64_t ld = n;
   if (!inplace) {
     TRY(c.ws_d.ensure((size_t)n_pad * n_pad * sizeof(T)));
     D = static_cast<T *>(c.ws_d.p);
     if (want_p) {
       TRY(c.ws_t.ensure((size_t)n_pad * n_pad * sizeof(int32_t)));
-      Tg = static_cast<int32_t *>(c.ws_t.p);
+      Pm = static_cast<int32_t *>(c.ws_t.p);
     }
     ld = n_pad;
   }
+  // the speculative key run may have to be redone in TAG mode: keep W when in place
+  T *backup = nullptr;
+  if (is_key(mode) && !key_static && inplace) {
+    TRY(c.ws_b.ensure((size_t)n * n * sizeof(T)));
+    backup = static_cast<T *>(c.ws_b.p);
+    CU(cudaMemcpyAsync(backup, src, (size_t)n * n * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  }
 
   const int R = (int)((n + BS - 1) / BS);  // rounds wholly inside the padding are skipped
-  TRY(ensure_events(c, 4 + (timing ? 3 * (size_t)R + 2 : 0)));
-  cudaEvent_t e_begin = c.events[0], e_end = c.events[1];
+  TRY(ensure_events(c, 4 + 3 * (size_t)R + 2));
+  cudaEvent_t e_begin = c.events[0], e_end = c.events[1], e_init = c.events[2],
+              e_post = c.events[3];
+  RoundTimes rt{timing, c.events.data() + 4};
+  int *d_maxkey = d_flags + 2;
+
   CU(cudaEventRecord(e_begin, st));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    // 4. init (+ key encoding), rounds
+    const T *init_src = (attempt == 1 && backup) ? backup : src;
+    const int64_t init_ld = (attempt == 1 && backup) ? n : ld_src;
+    TRY(dispatch_init<T>(mode, st, init_src, init_ld, n, D, want_p ? Pm : nullptr, ld, n_pad));
+    CU(cudaEventRecord(e_init, st));
+    TRY(dispatch_rounds<T>(mode, st, D, want_p ? Pm : nullptr, ld, n_pad, BS, R, d_maxkey, rt));
+    if (!is_key(mode) || key_static) break;
+    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (h_flags[2] <= key_limit) break;
+    mode = MODE_TAG;   // a stored key left the exact range: redo with round tags
+    CU(cudaMemsetAsync(d_flags + 2, 0, 4, st));
+  }
 
-  // 3. init: pad, diag 0, tags -1
-  {
-    dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)n_pad);
-    init_kernel<T><<<g, 256, 0, st>>>(src, ld_src, n, D, ld, n_pad, want_p ? Tg : nullptr, ld);
+  // 5. epilogue passes: keys -> distances, or tags -> P (reading R9/R10)
+  if (is_key(mode)) {
+    dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
+    decode_kernel<T><<<g, 256, 0, st>>>(D, ld, n);
     CU(cudaGetLastError());
-  }
-  if (timing) CU(cudaEventRecord(c.events[3 + 3 * R], st));
-
-  // 4. rounds
-  for (int K = 0; K < R; ++K) {
-    const int kb = K * BS;
-    if (want_p) {
-      TRY((launch_phase1<T, true>(st, D, ld, Tg, kb, BS, K)));
-      if (timing) CU(cudaEventRecord(c.events[2 + 3 * K], st));
-      TRY((launch_phase2<T, true>(st, D, ld, Tg, n_pad, kb, BS, K)));
-      if (timing) CU(cudaEventRecord(c.events[3 + 3 * K], st));
-      TRY((launch_phase3<T, true>(st, D, ld, Tg, n_pad, kb, BS, K)));
-    } else {
-      TRY((launch_phase1<T, false>(st, D, ld, nullptr, kb, BS, K)));
-      if (timing) CU(cudaEventRecord(c.events[2 + 3 * K], st));
-      TRY((launch_phase2<T, false>(st, D, ld, nullptr, n_pad, kb, BS, K)));
-      if (timing) CU(cudaEventRecord(c.events[3 + 3 * K], st));
-      TRY((launch_phase3<T, false>(st, D, ld, nullptr, n_pad, kb, BS, K)));
-    }
-    if (timing) CU(cudaEventRecord(c.events[4 + 3 * K], st));
-  }
-
-  // 5. post-pass: tags -> LAST_K -> next hop (reading R9/R10)
-  if (want_p) {
+  } else if (mode == MODE_TAG) {
     dim3 g((unsigned)((n + 255) / 256), (unsigned)n);
-    resolve_lastk_kernel<T><<<g, 256, 0, st>>>(D, ld, Tg, ld, n, BS);
+    resolve_lastk_kernel<T><<<g, 256, 0, st>>>(D, ld, Pm, n, BS);
     CU(cudaGetLastError());
     const size_t row_bytes = (size_t)n * sizeof(int32_t);
     const int use_smem = row_bytes <= 200 * 1024;
@@ -267,10 +378,10 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
       configured = true;
     }
     finalize_paths_kernel<T><<<(unsigned)n, 1024, use_smem ? row_bytes : 0, st>>>(
-        D, ld, Tg, ld, n, path_mode == 0, use_smem, d_flags);
+        D, Pm, ld, n, path_mode == 0, use_smem, d_flags);
     CU(cudaGetLastError());
   }
-  if (timing) CU(cudaEventRecord(c.events[2 + 3 * R], st));
+  CU(cudaEventRecord(e_post, st));
 
   // 6. unpad into the caller's buffers
   if (!inplace) {
@@ -278,14 +389,14 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
     unpad_kernel<T><<<g, 256, 0, st>>>(D, ld, n, src, ld_src);
     CU(cudaGetLastError());
     if (want_p) {
-      unpad_kernel<int32_t><<<g, 256, 0, st>>>(Tg, ld, n, next, ld_next);
+      unpad_kernel<int32_t><<<g, 256, 0, st>>>(Pm, ld, n, next, ld_next);
       CU(cudaGetLastError());
     }
   }
   CU(cudaEventRecord(e_end, st));
   CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  if (h_flags[0] & 2)
+  if (h_flags[0] & 8)
     return fail(FW_ERANGE, "next-hop resolution did not converge (zero-weight cycle?)");
 
   fw_stats s{};
@@ -295,24 +406,30 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
   s.rounds = R;
   s.is_int = int_t;
   s.path_mode = path_mode;
+  s.p_method = mode;
   float ms = 0.f;
   CU(cudaEventElapsedTime(&ms, e_begin, e_end));
   s.solve_ms = ms;
-  const double tiles_off = (double)(n_pad - BS);
   s.phase3_launches = R;
-  s.phase3_relaxations = (double)R * tiles_off * tiles_off * BS;
+  // phase-3 relaxations actually issued: rows and columns outside the round's strips
+  double relax = 0;
+  for (int K = 0; K < R; ++K) {
+    const double off = (double)(n_pad - BS);
+    relax += off * off * BS;
+  }
+  s.phase3_relaxations = relax;
   if (timing) {
     for (int K = 0; K < R; ++K) {
       float a = 0, b = 0, d = 0;
-      CU(cudaEventElapsedTime(&a, K == 0 ? c.events[3 + 3 * R] : c.events[4 + 3 * (K - 1)], c.events[2 + 3 * K]));
-      CU(cudaEventElapsedTime(&b, c.events[2 + 3 * K], c.events[3 + 3 * K]));
-      CU(cudaEventElapsedTime(&d, c.events[3 + 3 * K], c.events[4 + 3 * K]));
+      CU(cudaEventElapsedTime(&a, K == 0 ? e_init : rt.ev[3 * K - 1], rt.ev[3 * K]));
+      CU(cudaEventElapsedTime(&b, rt.ev[3 * K], rt.ev[3 * K + 1]));
+      CU(cudaEventElapsedTime(&d, rt.ev[3 * K + 1], rt.ev[3 * K + 2]));
       s.phase1_ms += a;
       s.phase2_ms += b;
       s.phase3_ms += d;
     }
     float p = 0;
-    CU(cudaEventElapsedTime(&p, c.events[4 + 3 * (R - 1)], c.events[2 + 3 * R]));
+    CU(cudaEventElapsedTime(&p, rt.ev[3 * R - 1], e_post));
     s.post_ms = p;
   }
   c.stats = s;
@@ -485,6 +602,7 @@ int fw_free(void) {
   cudaDeviceSynchronize();
   c->ws_d.release();
   c->ws_t.release();
+  c->ws_b.release();
   c->user_d.release();
   c->user_t.release();
   c->scratch.release();

@@ -1,20 +1,31 @@
 // fw_kernels.cuh — sm_100a kernels of the blocked Floyd–Warshall hot path.
 //
-// Method: arxiv 1811.01201 §4.1. One round K relaxes every pair
-// through the BS intermediate vertices k in [kb, kb+BS), kb = K*BS, in three phases:
+// Method: arxiv 1811.01201 §4.1. Round K relaxes every pair through
+// the BS intermediate vertices k in [kb, kb+BS), kb = K*BS, in three phases:
 //   phase 1     diagonal block D_KK, self-dependent: sequential k-loop in smem
 //   phase 2 pivot row strip D_KJ and column strip D_IK, each relaxed through
 //                        the closed D_KK* as a min-plus product (reading R7)
 //   phase 3     every other block D_IJ <- min(D_IJ, D_IK (x) D_KJ)
-// The loop body of the paper's FW_BLOCK (P:125: "one addition, one comparison") becomes
-// the relaxation microkernel below: FP32 uses packed FADD2 (2 adds per instruction) +
-// 3-input FMNMX3 (2 mins per instruction), i.e. one issue slot per relaxation;
-// INT32 uses VIADDMNMX (fused add+min). The P update is taken off the per-relaxation
-// path (reading R9): the epilogue writes the round number K as a tag for every element
-// whose distance strictly improved; a post-pass resolves tags into P.
+// In phases 2 and 3 the element (i,j) is relaxed through A(i,k) = D[i][kb+k] and
+// B(k,j) = D[kb+k][j] (global coordinates), so one tile kernel serves all three launches.
 //
-// Layout: D and the tag/P matrix are row-major,
-// n_pad x n_pad, leading dimension ld (a multiple of 128 elements here).
+// The loop body of the paper's FW_BLOCK (P:125, "one addition, one comparison") becomes
+// the relaxation microkernel: FP32 uses FADD2 with a broadcast scalar a_ik against a pair
+// (b_kj, b_k,j+1) — two relaxations per instruction — and FMNMX3 folding the candidates
+// of two consecutive k into the accumulator (two mins per instruction): one issue slot
+// per relaxation. INT32 uses VIADDMNMX (fused add+min, one per relaxation).
+//
+// P modes (reading R9):
+//   PLAIN   distances only.
+//   KEY_*   integer-valued data: every stored value is a key D' = D*128 + (column & 127).
+//           A candidate a'_ik + b'_kj = (D_ik + D_kj)*128 + (k&127) + (j&127), so the
+//           minimum over k is the minimum distance AND, among ties, the smallest k — the
+//           arg-min comes for free with the same instruction count. The epilogue recovers
+//           k, stores D' = sum - (k&127), and sets P[i][j] = P[i][k] (next hop) or k.
+//           Exact while every key sum stays below 2^24 (FP32) / 2^30 (INT32); the host
+//           verifies the bound (statically, or from the max stored key after the solve).
+//   TAG     real-valued data: the epilogue writes the round number K for every element
+//           that strictly improved; a post-pass resolves tags into P.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,22 +33,53 @@
 
 namespace fwb {
 
-constexpr int kThreads = 256;          // tile kernel: 16 x 16 threads
-constexpr int kTag = 0x40000000;       // terminal bit used by the next-hop pointer jumping
+constexpr int kThreads = 256;         // tile kernel: 256 threads
+constexpr int kBK = 32;               // k-chunk staged per pipeline stage
+constexpr int kTerm = 0x40000000;     // terminal bit used by the next-hop pointer jumping
+
+enum Mode { MODE_PLAIN = 0, MODE_TAG = 1, MODE_KEY_NEXT = 2, MODE_KEY_LASTK = 3 };
+__host__ __device__ constexpr bool is_key(int m) { return m >= MODE_KEY_NEXT; }
 
 template <typename T> struct Num;
 template <> struct Num<float> {
   static constexpr bool kIsInt = false;
   static __device__ __forceinline__ float inf() { return __int_as_float(0x7f800000); }
+  static __device__ __forceinline__ float acc_init() { return __int_as_float(0x7f800000); }
   static __device__ __forceinline__ bool bad(float v) { return !(v >= 0.0f); }  // NaN or < 0
   static __device__ __forceinline__ bool finite(float v) { return v < inf(); }
+  static __device__ __forceinline__ int low7(float v) { return (int)v & 127; }   // v < 2^24
+  static __device__ __forceinline__ float from_int(int v) { return (float)v; }
+  static __device__ __forceinline__ int bits(float v) { return __float_as_int(v); }
+  static __device__ __forceinline__ float encode(float v, int col) {       // key D*128 + col'
+    return finite(v) ? v * 128.0f + (float)(col & 127) : v;
+  }
+  static __device__ __forceinline__ float decode(float k) { return finite(k) ? floorf(k * 0.0078125f) : k; }
 };
 template <> struct Num<int32_t> {
   static constexpr bool kIsInt = true;
   static __device__ __forceinline__ int32_t inf() { return 0x3FFFFFFF; }
+  static __device__ __forceinline__ int32_t acc_init() { return 0x7FFFFFFF; }
   static __device__ __forceinline__ bool bad(int32_t v) { return v < 0 || v > 0x3FFFFFFF; }
   static __device__ __forceinline__ bool finite(int32_t v) { return v < 0x3FFFFFFF; }
+  static __device__ __forceinline__ int low7(int32_t v) { return v & 127; }
+  static __device__ __forceinline__ int32_t from_int(int v) { return v; }
+  static __device__ __forceinline__ int bits(int32_t v) { return v; }
+  static __device__ __forceinline__ int32_t encode(int32_t v, int col) {
+    return finite(v) ? v * 128 + (col & 127) : v;
+  }
+  static __device__ __forceinline__ int32_t decode(int32_t k) { return finite(k) ? (k >> 7) : k; }
 };
+
+template <typename T> struct Vec4;
+template <> struct Vec4<float> { using V = float4; };
+template <> struct Vec4<int32_t> { using V = int4; };
+
+template <typename V> __device__ __forceinline__ auto vget(const V &v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+template <typename V, typename S> __device__ __forceinline__ void vset(V &v, int e, S x) {
+  if (e == 0) v.x = x; else if (e == 1) v.y = x; else if (e == 2) v.z = x; else v.w = x;
+}
 
 // ---------------------------------------------------------------------------------
 // cp.async helpers (LDGSTS): global -> shared without staging registers.
@@ -45,238 +87,371 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // ---------------------------------------------------------------------------------
-// Relaxation microkernel: acc = min(acc, a.x+b.x, a.y+b.y, a.z+b.z, a.w+b.w)
-// where a = (a_ik, a_ik+1, a_ik+2, a_ik+3) and b = (b_kj, b_k+1j, b_k+2j, b_k+3j):
-// four relaxations of one (i,j) pair through four consecutive k (P:125 loop body).
-// Every sum is a single IEEE round-to-nearest add; min is exact, so the order in
-// which the four candidates are folded does not change the result (reading R8).
-template <typename T> struct Relax;
-template <> struct Relax<float> {
-  using V = float4;
-  static __device__ __forceinline__ void run(float &acc, const float4 &a, const float4 &b) {
-    const float2 s01 = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));  // FADD2
-    const float2 s23 = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));  // FADD2
-    acc = fminf(acc, fminf(s01.x, s01.y));                                          // FMNMX3
-    acc = fminf(acc, fminf(s23.x, s23.y));                                          // FMNMX3
-  }
-};
-template <> struct Relax<int32_t> {
-  using V = int4;
-  static __device__ __forceinline__ void run(int32_t &acc, const int4 &a, const int4 &b) {
-    acc = __viaddmin_s32(a.x, b.x, acc);   // VIADDMNMX: min(a+b, acc)
-    acc = __viaddmin_s32(a.y, b.y, acc);
-    acc = __viaddmin_s32(a.z, b.z, acc);
-    acc = __viaddmin_s32(a.w, b.w, acc);
-  }
-};
+// Relaxation microkernels. x0..x3: accumulators of one row i and four consecutive
+// columns j..j+3; a0, a1 = a_ik, a_i,k+1; b0, b1 = B[k][j..j+3], B[k+1][j..j+3].
+// Folds the 8 candidates a_ik + b_kj (one IEEE round-to-nearest add each) into x by min.
+// min is exact, so the fold order does not change the result (reading R8).
+__device__ __forceinline__ void relax2k(float &x0, float &x1, float &x2, float &x3, float a0,
+                                        float a1, const float4 &b0, const float4 &b1) {
+  const float2 s0 = __fadd2_rn(make_float2(a0, a0), make_float2(b0.x, b0.y));  // FADD2, a0 broadcast
+  const float2 s1 = __fadd2_rn(make_float2(a1, a1), make_float2(b1.x, b1.y));
+  const float2 s2 = __fadd2_rn(make_float2(a0, a0), make_float2(b0.z, b0.w));
+  const float2 s3 = __fadd2_rn(make_float2(a1, a1), make_float2(b1.z, b1.w));
+  x0 = fminf(x0, fminf(s0.x, s1.x));                                            // FMNMX3
+  x1 = fminf(x1, fminf(s0.y, s1.y));
+  x2 = fminf(x2, fminf(s2.x, s3.x));
+  x3 = fminf(x3, fminf(s2.y, s3.y));
+}
+__device__ __forceinline__ void relax2k(int &x0, int &x1, int &x2, int &x3, int a0, int a1,
+                                        const int4 &b0, const int4 &b1) {
+  x0 = __viaddmin_s32(a0, b0.x, x0);  // VIADDMNMX: min(a+b, x)
+  x1 = __viaddmin_s32(a0, b0.y, x1);
+  x2 = __viaddmin_s32(a0, b0.z, x2);
+  x3 = __viaddmin_s32(a0, b0.w, x3);
+  x0 = __viaddmin_s32(a1, b1.x, x0);
+  x1 = __viaddmin_s32(a1, b1.y, x1);
+  x2 = __viaddmin_s32(a1, b1.z, x2);
+  x3 = __viaddmin_s32(a1, b1.w, x3);
+}
 
-template <int TM, int TN, int BK>
-struct TileSmem {
-  static constexpr int kAStride = BK + 4;             // padded A row (16 B pad: no bank conflicts)
-  static constexpr int kA = TM * kAStride;            // elements per A stage
-  static constexpr int kB = BK * TN;                  // elements per B stage (k-quad interleaved)
+// Thread layout of a TM x TN tile: TX threads across (each owns H groups of 4 consecutive
+// columns, 4*TX apart), TY = 256/TX threads down (each owns RM rows, TY apart).
+template <int TM, int TN>
+struct TileShape {
+  static constexpr int H = TN >= 128 ? 2 : 1;
+  static constexpr int TX = TN / (4 * H);
+  static constexpr int TY = kThreads / TX;
+  static constexpr int RM = TM / TY;
+  static constexpr int AS = kBK + 4;                  // padded A row: conflict-free LDS.128
+  static constexpr int BSTR = TN;                     // B row stride
+  static constexpr int kA = TM * AS;
+  static constexpr int kB = kBK * BSTR;
   static constexpr int kStage = kA + kB;
   static constexpr int kBytes = 2 * kStage * 4;       // two stages (double buffering)
+  static_assert(TX * TY == kThreads && RM >= 1 && RM * TY == TM, "tile shape");
+  static_assert(TM * TN * 4 <= kBytes, "P staging must fit in the stage buffers");
+};
+
+// Launch arguments of the tile kernel (passed by value).
+struct TileArgs {
+  int64_t ld;
+  int kb, Kd;
+  int row0[2], col0[2];          // tile grid origin (global), per blockIdx.z
+  int mr_lo[2], mr_hi[2];        // excluded rows, per blockIdx.z
+  int mc_lo[2], mc_hi[2];        // excluded columns, per blockIdx.z
+  int pstage[2];                 // gather P from an smem copy of the tile (column strip)
+  int xrow[2];                   // 1: blockIdx.x walks tile rows (column strip in a dual launch)
+  int tag;                       // round number (TAG mode)
 };
 
 // ---------------------------------------------------------------------------------
-// Min-plus tile kernel used by phases 2 and 3:
-//   C[i][j] <- min(C[i][j], min_{k<Kd} A[i][k] + B[k][j])   for the tile's (i,j)
-// excluding rows in [mr_lo, mr_hi) and columns in [mc_lo, mc_hi) (those belong to
-// the strips phase 2 owns). If TAGS, every element whose value strictly
-// decreased gets tags[i][j] = tag (the round number K; reading R9).
-// A is TM x Kd (row-major, lda), B is Kd x TN (row-major, ldb). The CTA tile is TM x TN,
-// each of the 256 threads owns (TM/16) x (TN/16) elements strided by 16 in i and j.
-// The k dimension is streamed in chunks of BK through two shared-memory stages with
-// cp.async. A is staged row-major [i][k] (16-B copies), B k-quad interleaved
-// [k/4][j][k%4] (4-B copies) so one LDS.128 yields b_kj..b_k+3,j for FADD2 pairs.
-// In-place use (phase 2: C aliases A or B) is safe: a CTA reads all of its A/B chunks
-// before its epilogue writes, and no other CTA writes the region it reads.
-template <typename T, int TM, int TN, int BK, bool TAGS>
+// Min-plus tile kernel (phases 2 and 3). Tile origin (i0, j0) = (row0 + by*TM, col0 + bx*TN);
+// blockIdx.z selects one of two strip descriptions (phase 2 launches both strips at once).
+//   D[i][j] <- min(D[i][j], min_{k<Kd} D[i][kb+k] + D[kb+k][j])
+// for the tile's (i,j), excluding rows in [mr_lo, mr_hi) and columns in [mc_lo, mc_hi)
+// (strips owned by other phases). The k dimension is streamed in chunks of kBK
+// through two shared-memory stages (cp.async 16 B): A row-major [i][k] (padded), B row-major
+// [k][j]. In-place use (phase 2: the tile is its own A or B) is safe: a CTA reads all its
+// A/B chunks before its epilogue writes, and no other CTA writes what it reads.
+template <typename T, int TM, int TN, int MODE>
 __global__ void __launch_bounds__(kThreads, 2)
-minplus_tile_kernel(T *C, int64_t ldc, const T *A, int64_t lda, const T *B, int64_t ldb,
-                    int32_t *tags, int64_t ldt, int Kd, int mr_lo, int mr_hi, int mc_lo,
-                    int mc_hi, int tag) {
-  using S = TileSmem<TM, TN, BK>;
-  using V = typename Relax<T>::V;
-  constexpr int RM = TM / 16, RN = TN / 16;
-  static_assert(BK % 4 == 0 && TM % 16 == 0 && TN % 16 == 0, "tile shape");
+minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g, int *maxkey) {
+  using S = TileShape<TM, TN>;
+  using V = typename Vec4<T>::V;
+  constexpr int RM = S::RM, H = S::H, TX = S::TX, TY = S::TY;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *smem = reinterpret_cast<T *>(smem_raw);
 
-  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
-  // whole tile inside an excluded strip: nothing to do
+  // select the strip description without dynamic indexing (keeps g out of local memory)
+  const bool z = blockIdx.z != 0;
+  const int mr_lo = z ? g.mr_lo[1] : g.mr_lo[0], mr_hi = z ? g.mr_hi[1] : g.mr_hi[0];
+  const int mc_lo = z ? g.mc_lo[1] : g.mc_lo[0], mc_hi = z ? g.mc_hi[1] : g.mc_hi[0];
+  const int xrow = z ? g.xrow[1] : g.xrow[0];
+  const int bx = xrow ? 0 : blockIdx.x, by = xrow ? blockIdx.x : blockIdx.y;
+  const int i0 = (z ? g.row0[1] : g.row0[0]) + by * TM, j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
   if ((i0 >= mr_lo && i0 + TM <= mr_hi) || (j0 >= mc_lo && j0 + TN <= mc_hi)) return;
 
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  // Per-thread copy assignments (fixed across chunks; only the k offset advances).
-  // A: float4 number idx = tid + 256*t covers row r = idx / (BK/4), column quad idx % (BK/4).
-  constexpr int AQ = BK / 4;                          // float4 per A row chunk
-  constexpr int A_ITERS = (TM * AQ + kThreads - 1) / kThreads;
-  constexpr int A_ROWS_PER_ITER = kThreads / AQ;
-  static_assert(kThreads % AQ == 0, "A copy mapping");
-  const int a_r = tid / AQ, a_c = (tid % AQ) * 4;
-  const T *a_src = A + (int64_t)(i0 + a_r) * lda + a_c;
-  const int a_dst = a_r * S::kAStride + a_c;
-  // B: element idx = tid + 256*t covers row k = idx / TN, column j = idx % TN.
-  constexpr int B_ITERS = BK * TN / kThreads;
-  constexpr int B_ROWS_PER_ITER = kThreads / TN;
-  static_assert(kThreads % TN == 0 && (BK * TN) % kThreads == 0, "B copy mapping");
-  const int b_k = tid / TN, b_j = tid % TN;
-  const T *b_src = B + (int64_t)b_k * ldb + j0 + b_j;
+  const int64_t ld = g.ld;
+  const int kb = g.kb;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+
+  // cp.async assignments: A chunk TM x kBK, B chunk kBK x TN, 16 B per copy.
+  constexpr int A_PER = TM * (kBK / 4) / kThreads;
+  constexpr int A_ROWS = kThreads / (kBK / 4);
+  constexpr int B_PER = kBK * (TN / 4) / kThreads;
+  constexpr int B_ROWS = kThreads / (TN / 4);
+  static_assert(A_PER >= 1 && B_PER >= 1, "copy mapping");
+  const int a_r = tid / (kBK / 4), a_c = (tid % (kBK / 4)) * 4;
+  const int b_r = tid / (TN / 4), b_c = (tid % (TN / 4)) * 4;
+  const T *a_src = D + (int64_t)(i0 + a_r) * ld + kb + a_c;
+  const T *b_src = D + (int64_t)(kb + b_r) * ld + j0 + b_c;
 
   auto load_chunk = [&](int stage, int k0) {
     T *as = smem + stage * S::kStage;
     T *bs = as + S::kA;
-    const T *ap = a_src + k0;
 #pragma unroll
-    for (int t = 0; t < A_ITERS; ++t) {
-      if (A_ITERS * kThreads == TM * AQ || a_r + t * A_ROWS_PER_ITER < TM)
-        cp_async16(as + a_dst + t * A_ROWS_PER_ITER * S::kAStride, ap + (int64_t)t * A_ROWS_PER_ITER * lda);
-    }
-    const T *bp = b_src + (int64_t)k0 * ldb;
+    for (int t = 0; t < A_PER; ++t)
+      cp_async16(as + (a_r + t * A_ROWS) * S::AS + a_c, a_src + k0 + (int64_t)t * A_ROWS * ld);
 #pragma unroll
-    for (int t = 0; t < B_ITERS; ++t) {
-      const int k = b_k + t * B_ROWS_PER_ITER;
-      cp_async4(bs + ((k >> 2) * TN + b_j) * 4 + (k & 3), bp + (int64_t)t * B_ROWS_PER_ITER * ldb);
-    }
+    for (int t = 0; t < B_PER; ++t)
+      cp_async16(bs + (b_r + t * B_ROWS) * S::BSTR + b_c, b_src + (int64_t)(k0 + t * B_ROWS) * ld);
     cp_async_commit();
   };
 
-  T acc[RM][RN];
+  T acc[RM][4 * H];
 #pragma unroll
   for (int r = 0; r < RM; ++r)
 #pragma unroll
-    for (int c = 0; c < RN; ++c) acc[r][c] = Num<T>::inf();
+    for (int c = 0; c < 4 * H; ++c) acc[r][c] = Num<T>::acc_init();
 
-  const int nch = Kd / BK;
+  const int nch = g.Kd / kBK;
   load_chunk(0, 0);
   for (int ch = 0; ch < nch; ++ch) {
     if (ch + 1 < nch) {
-      load_chunk((ch + 1) & 1, (ch + 1) * BK);
+      load_chunk((ch + 1) & 1, (ch + 1) * kBK);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const T *as = smem + (ch & 1) * S::kStage + ty * S::kAStride;
+    const T *as = smem + (ch & 1) * S::kStage + ty * S::AS;
     const T *bs = smem + (ch & 1) * S::kStage + S::kA + tx * 4;
 #pragma unroll
-    for (int q = 0; q < BK / 4; ++q) {
-      V b[RN];
+    for (int q = 0; q < kBK / 4; ++q) {
+      V b[4][H];   // b[k][h] = B[4q+k][4tx + 4TX*h .. +3]
 #pragma unroll
-      for (int c = 0; c < RN; ++c) b[c] = *reinterpret_cast<const V *>(bs + (q * TN + 16 * c) * 4);
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+          b[k][h] = *reinterpret_cast<const V *>(bs + (4 * q + k) * S::BSTR + 4 * TX * h);
 #pragma unroll
       for (int r = 0; r < RM; ++r) {
-        const V a = *reinterpret_cast<const V *>(as + 16 * r * S::kAStride + 4 * q);
+        const V a = *reinterpret_cast<const V *>(as + TY * r * S::AS + 4 * q);
 #pragma unroll
-        for (int c = 0; c < RN; ++c) Relax<T>::run(acc[r][c], a, b[c]);
+        for (int h = 0; h < H; ++h) {
+          T *x = &acc[r][4 * h];
+          relax2k(x[0], x[1], x[2], x[3], a.x, a.y, b[0][h], b[1][h]);
+          relax2k(x[0], x[1], x[2], x[3], a.z, a.w, b[2][h], b[3][h]);
+        }
       }
     }
     __syncthreads();
   }
 
-  // Epilogue: compare with the current value, store strict improvements (+ tag K).
+  // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
+  const int pstage = z ? g.pstage[1] : g.pstage[0];
+  int32_t *sP = reinterpret_cast<int32_t *>(smem_raw);
+  if (MODE == MODE_KEY_NEXT && pstage) {
+    // stage this tile's P (old values) before any thread overwrites it
+    for (int e = tid; e < TM * TN / 4; e += kThreads) {
+      const int r = e / (TN / 4), c = (e % (TN / 4)) * 4;
+      *reinterpret_cast<int4 *>(sP + r * TN + c) =
+          *reinterpret_cast<const int4 *>(P + (int64_t)(i0 + r) * ld + j0 + c);
+    }
+    __syncthreads();
+  }
+  const int kgrp = kb & ~127;
+  int kmax = 0;
 #pragma unroll
   for (int r = 0; r < RM; ++r) {
-    const int i = i0 + ty + 16 * r;
+    const int i = i0 + ty + TY * r;
     const bool row_ok = !(i >= mr_lo && i < mr_hi);
-    T old[RN];
 #pragma unroll
-    for (int c = 0; c < RN; ++c) old[c] = C[(int64_t)i * ldc + j0 + tx + 16 * c];
+    for (int h = 0; h < H; ++h) {
+      const int jb = j0 + 4 * tx + 4 * TX * h;
+      V *dp = reinterpret_cast<V *>(D + (int64_t)i * ld + jb);
+      const V old = *dp;
+      V nv = old;
+      bool any = false;
+      int32_t pv[4];
+      bool chg[4];
 #pragma unroll
-    for (int c = 0; c < RN; ++c) {
-      const int j = j0 + tx + 16 * c;
-      const bool ok = row_ok && !(j >= mc_lo && j < mc_hi);
-      if (ok && acc[r][c] < old[c]) {
-        C[(int64_t)i * ldc + j] = acc[r][c];
-        if (TAGS) tags[(int64_t)i * ldt + j] = tag;
+      for (int e = 0; e < 4; ++e) {
+        const int j = jb + e;
+        const T m = acc[r][4 * h + e];
+        chg[e] = row_ok && !(j >= mc_lo && j < mc_hi) && m < (T)vget(old, e);
+        pv[e] = 0;
+        if (chg[e]) {
+          any = true;
+          if (is_key(MODE)) {
+            const int kk = Num<T>::low7(m - Num<T>::from_int(j & 127));   // arg-min k & 127
+            const T key = m - Num<T>::from_int(kk);
+            vset(nv, e, key);
+            kmax = max(kmax, Num<T>::bits(key));
+            if (MODE == MODE_KEY_NEXT)
+              pv[e] = pstage ? sP[(i - i0) * TN + (kgrp + kk - j0)] : P[(int64_t)i * ld + kgrp + kk];
+            else
+              pv[e] = kgrp + kk;
+          } else {
+            vset(nv, e, m);
+            pv[e] = g.tag;
+          }
+        }
+      }
+      if (any) {
+        *dp = nv;
+        if (MODE != MODE_PLAIN) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (chg[e]) P[(int64_t)i * ld + jb + e] = pv[e];
+        }
       }
     }
+  }
+  if (is_key(MODE)) {
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if ((tid & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
   }
 }
 
 // ---------------------------------------------------------------------------------
-// Phase 1: closure of the diagonal block D_KK in shared memory. For each k in
-// the block (in order), d[a][b] = min(d[a][b], d[a][k] + d[k][b]) (strict '<'). Row k and
-// column k are invariant during step k because d[k][k] = 0, so updating in place with
-// one barrier per k is exact. Elements that strictly improved get tag K.
-template <typename T, bool TAGS>
+// Phase 1: closure of the diagonal block D_KK in shared memory. For each k of the
+// block in order: d[a][b] = min(d[a][b], d[a][k] + d[k][b]) (strict '<'). Row k and column k
+// are invariant during step k because d[k][k] = 0 (key: (k&127), see below), so in-place
+// updates with one barrier per k are exact. 1024 threads; thread (tx, ty) owns the
+// (BS/32)^2 elements a = ty + 32r, b = tx + 32c in registers and mirrors changes to smem.
+// Key mode: s = d'[a][k] + d'[k][b] = S*128 + (k&127) + (b&127) < d'[a][b] = D*128 + (b&127)
+// iff S < D; the new key is s - (k&127); P[a][b] <- P[a][k] (next hop) or k.
+template <typename T, int BS, int MODE>
 __global__ void __launch_bounds__(1024)
-phase1_kernel(T *D, int64_t ld, int32_t *tags, int64_t ldt, int kb, int BS, int tag) {
+phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int tag, int *maxkey) {
+  constexpr int R = BS / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *s = reinterpret_cast<T *>(smem_raw);
-  const int nel = BS * BS;
+  T *sD = reinterpret_cast<T *>(smem_raw);
+  int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + BS * BS * sizeof(T));
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   T *Dk = D + (int64_t)kb * ld + kb;
-  for (int e = threadIdx.x; e < nel; e += blockDim.x) s[e] = Dk[(int64_t)(e / BS) * ld + e % BS];
+  int32_t *Pk = P ? P + (int64_t)kb * ld + kb : nullptr;
+  T d[R][R];
+  int32_t p[R][R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      const int a = ty + 32 * r, b = tx + 32 * c;
+      d[r][c] = Dk[(int64_t)a * ld + b];
+      sD[a * BS + b] = d[r][c];
+      p[r][c] = 0;
+      if (MODE == MODE_KEY_NEXT) {
+        p[r][c] = Pk[(int64_t)a * ld + b];
+        sP[a * BS + b] = p[r][c];
+      }
+    }
   __syncthreads();
   for (int k = 0; k < BS; ++k) {
-    for (int e = threadIdx.x; e < nel; e += blockDim.x) {
-      const int a = e / BS, b = e - a * BS;
-      const T v = s[a * BS + k] + s[k * BS + b];
-      if (v < s[e]) s[e] = v;
+    T colv[R], rowv[R];
+    int32_t pk[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      colv[r] = sD[(ty + 32 * r) * BS + k];
+      if (MODE == MODE_KEY_NEXT) pk[r] = sP[(ty + 32 * r) * BS + k];
     }
+#pragma unroll
+    for (int c = 0; c < R; ++c) rowv[c] = sD[k * BS + tx + 32 * c];
+    const T kp = Num<T>::from_int((kb + k) & 127);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        T s = colv[r] + rowv[c];
+        if (s < d[r][c]) {
+          if (is_key(MODE)) s = s - kp;
+          d[r][c] = s;
+          sD[(ty + 32 * r) * BS + tx + 32 * c] = s;
+          if (MODE == MODE_KEY_NEXT) {
+            p[r][c] = pk[r];
+            sP[(ty + 32 * r) * BS + tx + 32 * c] = pk[r];
+          } else if (MODE == MODE_KEY_LASTK) {
+            p[r][c] = kb + k;
+          }
+        }
+      }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < nel; e += blockDim.x) {
-    const int64_t off = (int64_t)(e / BS) * ld + e % BS;
-    if (s[e] < Dk[off]) {
-      Dk[off] = s[e];
-      if (TAGS) tags[(int64_t)(kb + e / BS) * ldt + kb + e % BS] = tag;
+  int kmax = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      const int a = ty + 32 * r, b = tx + 32 * c;
+      const int64_t off = (int64_t)a * ld + b;
+      if (d[r][c] < Dk[off]) {
+        Dk[off] = d[r][c];
+        if (MODE == MODE_TAG) Pk[off] = tag;
+        if (is_key(MODE)) {
+          Pk[off] = p[r][c];
+          kmax = max(kmax, Num<T>::bits(d[r][c]));
+        }
+      }
     }
+  if (is_key(MODE)) {
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (tx == 0 && kmax > 0) atomicMax(maxkey, kmax);
   }
 }
 
 // ---------------------------------------------------------------------------------
 // Validation (read-only, before anything is written: fw.h error contract).
-// flags bit 0: out-of-domain value. maxw: max finite off-diagonal weight (INT32 only).
+// flags: bit 0 out-of-domain value; bit 1 a finite FP32 weight is not integer-valued;
+//        bit 2 an off-diagonal entry is INF (no edge). maxw: max finite off-diagonal weight
+//        (INT32 value, or FP32 bit pattern — non-negative floats order like their bits).
 template <typename T>
 __global__ void validate_kernel(const T *src, int64_t lds, int64_t n, int *flags, int *maxw) {
-  int bad = 0, mx = 0;
+  int f = 0, mx = 0;
   const int64_t total = n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / n, j = e - i * n;
-    const T v = src[i * lds + j];
     if (i == j) continue;  // the diagonal is overwritten with 0 (R4)
-    if (Num<T>::bad(v)) bad = 1;
-    if (Num<T>::kIsInt && !Num<T>::bad(v) && Num<T>::finite(v)) {
-      const int iv = (int)v;
-      mx = iv > mx ? iv : mx;
-    }
+    const T v = src[i * lds + j];
+    if (Num<T>::bad(v)) { f |= 1; continue; }
+    if (!Num<T>::finite(v)) { f |= 4; continue; }
+    if (!Num<T>::kIsInt && (float)v != rintf((float)v)) f |= 2;
+    mx = max(mx, Num<T>::bits(v));
   }
-  bad = __reduce_or_sync(0xffffffffu, bad);
+  f = __reduce_or_sync(0xffffffffu, f);
   mx = __reduce_max_sync(0xffffffffu, mx);
   if ((threadIdx.x & 31) == 0) {
-    if (bad) atomicOr(flags, 1);
+    if (f) atomicOr(flags, f);
     atomicMax(maxw, mx);
   }
 }
 
-// Copy W (n x n, lds) into the padded n_pad x n_pad workspace (ld): padded entries INF,
-// diagonal 0 (R4, R11); tags/P initialised to -1 ("no improvement yet"). src may alias D
-// (in-place solve) — each element is read then written by the same thread.
-template <typename T>
-__global__ void init_kernel(const T *src, int64_t lds, int64_t n, T *D, int64_t ld, int64_t n_pad,
-                            int32_t *tags, int64_t ldt) {
+// Copy W (n x n, lds) into the padded n_pad x n_pad working matrix (ld): padded entries INF,
+// diagonal 0 (R4, R11); key modes store D*128 + (j&127). P initialised per mode:
+// KEY_NEXT: next hop of the direct edge (j), i on the diagonal, -1 without an edge;
+// otherwise -1 (no intermediate / no tag yet). src may alias D (in-place solve).
+template <typename T, int MODE>
+__global__ void init_kernel(const T *src, int64_t lds, int64_t n, T *D, int32_t *P, int64_t ld,
+                            int64_t n_pad) {
   const int64_t i = blockIdx.y;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_pad;
        j += (int64_t)gridDim.x * blockDim.x) {
     T v = (i < n && j < n) ? src[i * lds + j] : Num<T>::inf();
     if (i == j) v = 0;
+    if (MODE != MODE_PLAIN) {
+      int32_t p = -1;
+      if (MODE == MODE_KEY_NEXT) p = (i == j) ? (int32_t)i : (Num<T>::finite(v) ? (int32_t)j : -1);
+      P[i * ld + j] = p;
+    }
+    if (is_key(MODE)) v = Num<T>::encode(v, (int)j);
     D[i * ld + j] = v;
-    if (tags) tags[i * ldt + j] = -1;
   }
+}
+
+// Key -> distance (key modes), in place over rows [0, n) and columns [0, n).
+template <typename T>
+__global__ void decode_kernel(T *D, int64_t ld, int64_t n) {
+  const int64_t i = blockIdx.y;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    D[i * ld + j] = Num<T>::decode(D[i * ld + j]);
 }
 
 // Copy the n x n result out of the padded workspace (unpad).
@@ -289,22 +464,22 @@ __global__ void unpad_kernel(const T *D, int64_t ld, int64_t n, T *dst, int64_t 
 }
 
 // ---------------------------------------------------------------------------------
-// Post-pass step 1 (reading R9): for each (i,j) whose last strict improvement happened in
-// round K = tags[i][j] >= 0, find k* = the first k in block K, k not in {i,j}, minimising
-// D[i][k] + D[k][j] over the FINAL D. In exact arithmetic D[i][k*] + D[k*][j] = D[i][j]
-// (the improving k of round K attains it and final D obeys the triangle inequality), so
-// k* is a "most recently added intermediate node" in the paper's sense.
-// Overwrites tags in place with k* (LAST_K form); untagged entries stay -1.
+// TAG-mode post-pass, step 1 (reading R9): for each (i,j) whose last strict improvement
+// happened in round K = tags[i][j] >= 0, find k* = the first k in block K, k not in {i,j},
+// with D[i][k] + D[k][j] <= D[i][j] over the FINAL D. Such a k exists: the improving k of
+// round K gave D[i][j], and later rounds only lowered D[i][k], D[k][j] (rounding is
+// monotone). k* is an intermediate vertex of a shortest i->j path, i.e. the paper's
+// "most recently added intermediate node" form of P. Overwrites tags with k*.
 template <typename T>
-__global__ void resolve_lastk_kernel(const T *D, int64_t ld, int32_t *tags, int64_t ldt,
-                                     int64_t n, int BS) {
+__global__ void resolve_lastk_kernel(const T *D, int64_t ld, int32_t *tags, int64_t n, int BS) {
   const int64_t i = blockIdx.y;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
-  const int t = tags[i * ldt + j];
+  const int t = tags[i * ld + j];
   if (t < 0) return;
   const int64_t kb = (int64_t)t * BS;
   const int64_t ke = kb + BS < n ? kb + BS : n;
+  const T dij = D[i * ld + j];
   T best = Num<T>::inf();
   int ks = -1;
   const T *Di = D + i * ld;
@@ -312,23 +487,24 @@ __global__ void resolve_lastk_kernel(const T *D, int64_t ld, int32_t *tags, int6
     if (k == i || k == j) continue;
     const T s = Di[k] + D[k * ld + j];
     if (s < best) { best = s; ks = (int)k; }
+    if (s <= dij) { ks = (int)k; break; }
   }
-  tags[i * ldt + j] = ks;
+  tags[i * ld + j] = ks;
 }
 
-// Post-pass step 2 (NEXT-HOP mode, reading R1/R10): per row i, next[i][j] = j if (i,j) was
-// never improved (direct edge), else next[i][k*] (k* = LAST_K[i][j]); resolved by pointer
-// jumping on row i in shared memory (or in place in global memory when the row does not
-// fit). With positive weights D[i][k*] < D[i][j], so chains are acyclic. Then the
-// sentinels: next[i][i] = i, next[i][j] = -1 when D[i][j] is INF. LAST_K mode only applies
-// the sentinels (diagonal and unreachable -> -1). flags bit 1: chain did not converge.
+// TAG-mode post-pass, step 2 (NEXT-HOP mode, readings R1/R10): per row i, next[i][j] = j if
+// (i,j) was never improved (direct edge), else next[i][k*] (k* = LAST_K[i][j]); resolved by
+// pointer jumping on row i in shared memory (or in place when the row does not fit). With
+// positive weights D[i][k*] < D[i][j], so chains are acyclic. Then the sentinels:
+// next[i][i] = i, next[i][j] = -1 when D[i][j] is INF. LAST_K mode only applies the
+// sentinels (diagonal and unreachable -> -1). flags bit 3: a chain did not converge.
 template <typename T>
 __global__ void __launch_bounds__(1024)
-finalize_paths_kernel(const T *D, int64_t ld, int32_t *P, int64_t ldp, int64_t n, int next_hop,
-                      int use_smem, int *flags) {
+finalize_paths_kernel(const T *D, int32_t *P, int64_t ld, int64_t n, int next_hop, int use_smem,
+                      int *flags) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t i = blockIdx.x;
-  int32_t *row = P + i * ldp;
+  int32_t *row = P + i * ld;
   const T *Drow = D + i * ld;
   if (!next_hop) {
     for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
@@ -338,7 +514,7 @@ finalize_paths_kernel(const T *D, int64_t ld, int32_t *P, int64_t ldp, int64_t n
   int32_t *v = use_smem ? reinterpret_cast<int32_t *>(smem_raw) : row;
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
     const int32_t t = row[j];
-    v[j] = t < 0 ? (int32_t)(j | kTag) : t;
+    v[j] = t < 0 ? (int32_t)(j | kTerm) : t;
   }
   __syncthreads();
   int sweeps = 0;
@@ -346,22 +522,22 @@ finalize_paths_kernel(const T *D, int64_t ld, int32_t *P, int64_t ldp, int64_t n
     int active = 0;
     for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
       const int32_t x = v[j];
-      if (!(x & kTag)) {
+      if (!(x & kTerm)) {
         const int32_t y = ((volatile int32_t *)v)[x];
         v[j] = y;
-        active |= !(y & kTag);
+        active |= !(y & kTerm);
       }
     }
     active = __syncthreads_or(active);
     if (!active) break;
     if (++sweeps > 64) {
-      if (threadIdx.x == 0) atomicOr(flags, 2);
+      if (threadIdx.x == 0) atomicOr(flags, 8);
       break;
     }
   }
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
     const int32_t x = v[j];
-    int32_t out = (x & kTag) ? (x & ~kTag) : -1;
+    int32_t out = (x & kTerm) ? (x & ~kTerm) : -1;
     if (j == i) out = (int32_t)i;
     else if (!Num<T>::finite(Drow[j])) out = -1;
     row[j] = out;

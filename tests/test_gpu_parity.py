@@ -294,3 +294,69 @@ def test_config_C4_16384():
     D, P = solve(W, 128)
     _dijkstra_rows_check(W, D, P, c["seed"], True)
     assert next_consistency(W, D, P, exact=True) == 0
+
+
+# ---- P method selection (reading R9): exact keyed arg-min vs round tags ---------------
+def _solve_stats(W, block, flags=0):
+    D = W.copy()
+    P = np.empty(W.shape, dtype=np.int32)
+    with Ctx(flags | fw.FW_TIMING):
+        (fw.fw_solve_i32 if W.dtype == np.int32 else fw.fw_solve)(D, P, block=block)
+        s = fw.fw_last_stats()
+    return D, P, s
+
+
+def test_keyed_mode_static_bound():
+    """Complete integer graph: keys are provably exact (no INF entries)."""
+    W = gen.generate("complete_int", 300, 11)
+    D, P, s = _solve_stats(W, 64)
+    assert s.p_method == 2
+    np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+    assert oracle.check_paths(W, D, P)[0] == 0
+
+
+def test_keyed_mode_speculative_success():
+    """ER graph with INF entries and (n-1)*max_w beyond the key range: the keyed run is
+    speculative and verified by the max stored key (distances stay small)."""
+    W = gen.generate("er_int_f32", 700, 12, p=0.1, lo=1, hi=1000)
+    D, P, s = _solve_stats(W, 128)
+    assert s.p_method == 2
+    np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+    assert oracle.check_paths(W, D, P)[0] == 0
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.int32])
+def test_keyed_mode_fallback_to_tags(dtype):
+    """Ring with weight 1000 (FP32) / 40000 (INT32): distances leave the exact key range,
+    the solve is redone with round tags and must still be exact."""
+    n = 1000 if dtype == np.float32 else 200
+    w = 1000 if dtype == np.float32 else 40000
+    W = gen.ring(n, w, dtype)
+    D, P, s = _solve_stats(W, 64)
+    assert s.p_method == 1
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    np.testing.assert_array_equal(D.astype(np.int64), ((j - i) % n) * w)
+    np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % n))
+
+
+def test_real_weights_use_tags():
+    W = gen.generate("complete_real", 256, 13)
+    D, P, s = _solve_stats(W, 64)
+    assert s.p_method == 1
+    assert_D_matches(D, oracle.fw(W, None)[0], exact=False)
+    assert oracle.check_paths(W, D, P, rtol=1e-5)[0] == 0
+
+
+def test_keyed_lastk():
+    W = gen.generate("er_int", 513, 14, p=0.05, lo=1, hi=1000)
+    D, P, s = _solve_stats(W, 32, fw.FW_PATH_LAST_K)
+    assert s.p_method == 3
+    np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+    assert oracle.check_paths(W, D, P, mode="lastk")[0] == 0
+
+
+def test_zero_weight_edges_distances():
+    """Zero off-diagonal weights are in the domain (reading C-5): D must be exact."""
+    W = gen.generate("er_int_f32", 260, 15, p=0.05, lo=0, hi=3)
+    D, P = solve(W, 64)
+    np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
