@@ -72,7 +72,7 @@ typedef struct fw_stats {
   int32_t is_int;       /* 1 = INT32 solve                                     */
   int32_t path_mode;    /* -1 = no P, 0 = next hop, 1 = last k                 */
   int32_t p_method;     /* 0 = no P; 1 = round tags + post-pass (real-valued data);
-                           2/3 = exact arg-min keys (integer-valued data, next hop / last k) */
+                           2 = exact arg-min keys (integer-valued data)           */
   double solve_ms;      /* device-resident solve (init .. post-pass), CUDA events */
   double phase1_ms;     /* FW_TIMING only: sum over rounds                     */
   double phase2_ms;

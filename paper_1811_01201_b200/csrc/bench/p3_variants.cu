@@ -5,10 +5,11 @@
 #include <stdio.h>
 #include <stdint.h>
 #include <vector>
+#include "../fw_kernels.cuh"
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+__device__ __forceinline__ void l_cp_async16(void *smem, const void *gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
@@ -37,7 +38,7 @@ p3(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
   auto load = [&](int s, int k0) {
     float *as = sm + s * ST, *bs = as + SA;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) cp_async16(as + (a_r + 32 * t) * AS + a_c, a_src + k0 + (int64_t)32 * t * ld);
+    for (int t = 0; t < 4; ++t) l_cp_async16(as + (a_r + 32 * t) * AS + a_c, a_src + k0 + (int64_t)32 * t * ld);
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
       const int k = b_k + 2 * t;
@@ -111,7 +112,7 @@ p3(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
 // (16-B cp.async); thread owns rows ty+16r and columns 4tx+64h+{0..3}.
 template <int VAR>
 __global__ void __launch_bounds__(256, 2)
-p3j(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
+p3j(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb, int *P, int *maxkey) {
   constexpr int TM = 128, TN = 128, BK = 32, AS = BK + 4, BSTR = TN + ((VAR & 32) ? 4 : 0);
   constexpr int SA = TM * AS, SB = BK * BSTR, ST = SA + SB;
   extern __shared__ __align__(16) float sm[];
@@ -125,9 +126,9 @@ p3j(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
   auto load = [&](int s, int k0) {
     float *as = sm + s * ST, *bs = as + SA;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) cp_async16(as + (a_r + 32 * t) * AS + a_c, a_src + k0 + (int64_t)32 * t * ld);
+    for (int t = 0; t < 4; ++t) l_cp_async16(as + (a_r + 32 * t) * AS + a_c, a_src + k0 + (int64_t)32 * t * ld);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) cp_async16(bs + (b_k + 8 * t) * BSTR + b_c, b_src + (int64_t)(k0 + 8 * t) * ld);
+    for (int t = 0; t < 4; ++t) l_cp_async16(bs + (b_k + 8 * t) * BSTR + b_c, b_src + (int64_t)(k0 + 8 * t) * ld);
     cp_commit();
   };
   float acc[8][8];
@@ -144,6 +145,34 @@ p3j(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
     const float *bs = sm + (ch & 1) * ST + SA + tx * 4;
 #pragma unroll
     for (int q = 0; q < BK / 4; ++q) {
+      if (VAR & 64) {
+#pragma unroll
+        for (int kp = 0; kp < 2; ++kp) {
+          float4 b[2][2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) b[k][h] = *reinterpret_cast<const float4 *>(bs + (4 * q + 2 * kp + k) * BSTR + 64 * h);
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const float2 a = *reinterpret_cast<const float2 *>(as + 16 * r * AS + 4 * q + 2 * kp);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float4 b0 = b[0][h], b1 = b[1][h];
+              const float2 s0 = __fadd2_rn(make_float2(a.x, a.x), make_float2(b0.x, b0.y));
+              const float2 s1 = __fadd2_rn(make_float2(a.y, a.y), make_float2(b1.x, b1.y));
+              const float2 s2 = __fadd2_rn(make_float2(a.x, a.x), make_float2(b0.z, b0.w));
+              const float2 s3 = __fadd2_rn(make_float2(a.y, a.y), make_float2(b1.z, b1.w));
+              float *x = &acc[r][4 * h];
+              x[0] = fminf(x[0], fminf(s0.x, s1.x));
+              x[1] = fminf(x[1], fminf(s0.y, s1.y));
+              x[2] = fminf(x[2], fminf(s2.x, s3.x));
+              x[3] = fminf(x[3], fminf(s2.y, s3.y));
+            }
+          }
+        }
+        continue;
+      }
       float4 b[4][2];   // b[k][h] = B[4q+k][4tx+64h .. +3]
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -173,6 +202,57 @@ p3j(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
     }
     __syncthreads();
   }
+  if (VAR & (128 | 256)) {
+    const int kgrp = kb & ~127;
+    int kmax = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int i = i0 + ty + 16 * r;
+      const bool row_ok = (VAR & 512) ? true : !(i >= kb && i < kb + 128);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int jb = j0 + 4 * tx + 64 * h;
+        float4 *dp = reinterpret_cast<float4 *>(C + (int64_t)i * ld + jb);
+        const float4 old = *dp;
+        float4 nv = old;
+        bool any = false;
+        int pv[4];
+        bool chg[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = jb + e;
+          const float m = acc[r][4 * h + e];
+          const float o = e == 0 ? old.x : e == 1 ? old.y : e == 2 ? old.z : old.w;
+          chg[e] = (VAR & 512) ? (m < o) : (row_ok && !(j >= kb && j < kb + 128) && m < o);
+          pv[e] = 0;
+          if (chg[e]) {
+            any = true;
+            float key = m;
+            if (VAR & 256) {
+              const int kk = (int)(m - (float)(j & 127)) & 127;
+              key = m - (float)kk;
+              kmax = max(kmax, __float_as_int(key));
+              pv[e] = kgrp + kk;
+            }
+            if (e == 0) nv.x = key; else if (e == 1) nv.y = key; else if (e == 2) nv.z = key; else nv.w = key;
+          }
+        }
+        if (any) {
+          *dp = nv;
+          if (VAR & 256) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (chg[e]) P[(int64_t)i * ld + jb + e] = pv[e];
+          }
+        }
+      }
+    }
+    if (VAR & 256) {
+      kmax = __reduce_max_sync(0xffffffffu, kmax);
+      if ((tid & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
+    }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int i = i0 + ty + 16 * r;
@@ -188,19 +268,19 @@ p3j(float *C, int64_t ld, const float *A, const float *B, int Kd, int kb) {
 }
 
 template <int VAR>
-int runj(float *D, int64_t n, int sms, int clk_khz) {
+int runj(float *D, int64_t n, int sms, int clk_khz, int *P = nullptr, int *mk = nullptr) {
   constexpr int BSTR = 128 + ((VAR & 32) ? 4 : 0);
   const int bytes = 2 * (128 * 36 + 32 * BSTR) * 4;
   CK(cudaFuncSetAttribute(p3j<VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   dim3 g(n / 128, n / 128);
   const int kb = 128 * 50;
-  for (int w = 0; w < 2; ++w) p3j<VAR><<<g, 256, bytes>>>(D, n, D + kb, D + (int64_t)kb * n, 128, kb);
+  for (int w = 0; w < 2; ++w) p3j<VAR><<<g, 256, bytes>>>(D, n, D + kb, D + (int64_t)kb * n, 128, kb, P, mk);
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int reps = 10;
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) p3j<VAR><<<g, 256, bytes>>>(D, n, D + kb, D + (int64_t)kb * n, 128, kb);
+  for (int r = 0; r < reps; ++r) p3j<VAR><<<g, 256, bytes>>>(D, n, D + kb, D + (int64_t)kb * n, 128, kb, P, mk);
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -236,6 +316,34 @@ int run(float *D, int64_t n, int sms, int clk_khz) {
   return 0;
 }
 
+
+template <int MODE, int TM = 128, int TN = 128>
+int runlib(float *D, int32_t *P, int *mk, int64_t n, int sms, int clk_khz) {
+  using namespace fwb;
+  constexpr int bytes = TileShape<TM, TN>::kBytes;
+  auto kern = minplus_tile_kernel<float, TM, TN, MODE, false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  TileArgs a{};
+  a.ld = n; a.kb = 128 * 50; a.Kd = 128;
+  a.mr_lo[0] = a.mc_lo[0] = a.kb; a.mr_hi[0] = a.mc_hi[0] = a.kb + 128;
+  dim3 g(n / TN, n / TM);
+  for (int w = 0; w < 2; ++w) kern<<<g, 256, bytes>>>(D, P, a, mk);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int reps = 10;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) kern<<<g, 256, bytes>>>(D, P, a, mk);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  const double relax = (double)(n - 128) * (n - 128) * 128;
+  printf("{\"variant\": \"lib%d_%dx%d\", \"ms\": %.4f, \"relax_per_clk_sm_at_max_clock\": %.2f, \"tflops\": %.3f}\n", MODE, TM, TN, ms,
+         relax / (ms * 1e-3) / (sms * (double)clk_khz * 1e3), 2 * relax / (ms * 1e-3) / 1e12);
+  return 0;
+}
+
 int main() {
   int sms, clk;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -246,6 +354,9 @@ int main() {
   for (auto &v : h) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = 1.0f + (float)(x % 100); }
   float *D; CK(cudaMalloc(&D, n * n * 4));
   CK(cudaMemcpy(D, h.data(), n * n * 4, cudaMemcpyHostToDevice));
-  run<0>(D, n, sms, clk); runj<0>(D, n, sms, clk); runj<32>(D, n, sms, clk); run<0>(D, n, sms, clk); runj<0>(D, n, sms, clk);
+  int32_t *P; int *mk;
+  CK(cudaMalloc(&P, n * n * 4)); CK(cudaMalloc(&mk, 4));
+  runj<0>(D, n, sms, clk); runj<128 + 512>(D, n, sms, clk, P, mk); runj<256 + 512>(D, n, sms, clk, P, mk);
+  runlib<0>(D, P, mk, n, sms, clk); runlib<2>(D, P, mk, n, sms, clk); runj<0>(D, n, sms, clk);
   return 0;
 }

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -75,6 +76,8 @@ struct Ctx {
   int dev = 0;
   unsigned flags = 0;
   cudaStream_t stream = nullptr;   // internal stream for the host entry points
+  cudaStream_t side = nullptr;     // high-priority stream for the look-ahead pivot phases
+  bool lookahead = true;
   DevBuf ws_d, ws_t;               // padded workspaces (D, tags/P)
   DevBuf ws_b;                     // backup of W for a speculative key run (in place)
   DevBuf user_d, user_t;           // device copies of host buffers (host entry points)
@@ -107,10 +110,14 @@ int ensure_events(Ctx &c, size_t count) {
 template <typename T, int TM, int TN, int MODE>
 int launch_tile(dim3 grid, cudaStream_t st, T *D, int32_t *P, const TileArgs &a, int *maxkey) {
   constexpr int bytes = TileShape<TM, TN>::kBytes;
-  auto kern = minplus_tile_kernel<T, TM, TN, MODE>;
+  auto kern = grid.z > 1 ? minplus_tile_kernel<T, TM, TN, MODE, true>
+                         : minplus_tile_kernel<T, TM, TN, MODE, false>;
   static bool configured = false;  // per instantiation (one device per process)
   if (!configured) {
-    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CU(cudaFuncSetAttribute(minplus_tile_kernel<T, TM, TN, MODE, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CU(cudaFuncSetAttribute(minplus_tile_kernel<T, TM, TN, MODE, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     configured = true;
   }
   kern<<<grid, kThreads, bytes, st>>>(D, P, a, maxkey);
@@ -126,18 +133,18 @@ TileArgs tile_args(int64_t ld, int kb, int BS, int tag) {
   a.tag = tag;
   for (int z = 0; z < 2; ++z) {
     a.mr_lo[z] = a.mr_hi[z] = a.mc_lo[z] = a.mc_hi[z] = 0;
-    a.row0[z] = a.col0[z] = a.pstage[z] = a.xrow[z] = 0;
+    a.row0[z] = a.col0[z] = a.xrow[z] = 0;
   }
   return a;
 }
 
 template <typename T, int BS, int MODE>
 int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int kb, int K, int *maxkey) {
-  const int bytes = BS * BS * (int)sizeof(T) * (MODE == MODE_KEY_NEXT ? 2 : 1);
+  const int bytes = 2 * BS * BS * (int)sizeof(T);   // row-major + transposed copy of D_KK
   auto kern = phase1_kernel<T, BS, MODE>;
   static bool configured = false;
   if (!configured) {
-    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * BS * BS * 4));
+    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     configured = true;
   }
   kern<<<1, 1024, bytes, st>>>(D, P, ld, kb, K, maxkey);
@@ -165,15 +172,13 @@ int launch_phase2_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pa
   TileArgs a = tile_args(ld, kb, BS, K);
   // z = 0: row strip, tiles BS x 128 across the columns; exclude the diagonal block columns
   a.row0[0] = kb; a.col0[0] = 0; a.mc_lo[0] = kb; a.mc_hi[0] = kb + BS;
-  // z = 1: column strip, tiles 128 x BS down the rows; exclude the diagonal block rows.
-  // Its arg-min column lies inside the strip being updated: gather P from an smem copy.
-  a.row0[1] = 0; a.col0[1] = kb; a.mr_lo[1] = kb; a.mr_hi[1] = kb + BS; a.pstage[1] = 1;
-  a.xrow[1] = 1;
+  // z = 1: column strip, tiles 128 x BS down the rows; exclude the diagonal block rows
+  a.row0[1] = 0; a.col0[1] = kb; a.mr_lo[1] = kb; a.mr_hi[1] = kb + BS; a.xrow[1] = 1;
   if (BS == 128) return launch_tile<T, 128, 128, MODE>(dim3(tiles, 1, 2), st, D, P, a, maxkey);
-  TileArgs r = a, c = a;
-  c.row0[0] = c.row0[1]; c.col0[0] = c.col0[1]; c.mr_lo[0] = c.mr_lo[1]; c.mr_hi[0] = c.mr_hi[1];
-  c.mc_lo[0] = c.mc_hi[0] = 0; c.pstage[0] = 1; c.xrow[0] = 1;
-  TRY((launch_tile<T, BS, 128, MODE>(dim3(tiles, 1, 1), st, D, P, r, maxkey)));
+  TileArgs c = a;
+  c.row0[0] = 0; c.col0[0] = kb; c.mr_lo[0] = kb; c.mr_hi[0] = kb + BS; c.mc_lo[0] = c.mc_hi[0] = 0;
+  c.xrow[0] = 1;
+  TRY((launch_tile<T, BS, 128, MODE>(dim3(tiles, 1, 1), st, D, P, a, maxkey)));
   return launch_tile<T, 128, BS, MODE>(dim3(tiles, 1, 1), st, D, P, c, maxkey);
 }
 
@@ -199,6 +204,31 @@ int launch_phase3(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, 
   return launch_tile<T, 128, 128, MODE>(dim3(tiles, tiles, 1), st, D, P, a, maxkey);
 }
 
+// Look-ahead split of phase 3 (BS = 128). P3a: the tiles of block-row K+1 and block-column
+// K+1 (what phases 1-2 of round K+1 read), so round K+1 can start on the side stream while
+// P3b — every other tile — finishes round K on the main stream.
+template <typename T, int MODE>
+int launch_phase3a(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int K,
+                   int *maxkey) {
+  const int tiles = (int)(n_pad / 128), BS = 128, kn = kb + BS;
+  TileArgs a = tile_args(ld, kb, BS, K);
+  // z = 0: block-row K+1 across all columns except the column strip of round K
+  a.row0[0] = kn; a.col0[0] = 0; a.mc_lo[0] = kb; a.mc_hi[0] = kb + BS;
+  // z = 1: block-column K+1 down all rows except the row strip of K and block-row K+1
+  a.row0[1] = 0; a.col0[1] = kn; a.mr_lo[1] = kb; a.mr_hi[1] = kn + BS; a.xrow[1] = 1;
+  return launch_tile<T, 128, 128, MODE>(dim3(tiles, 1, 2), st, D, P, a, maxkey);
+}
+
+template <typename T, int MODE>
+int launch_phase3b(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int K,
+                   int *maxkey) {
+  const int tiles = (int)(n_pad / 128), BS = 128;
+  TileArgs a = tile_args(ld, kb, BS, K);
+  a.mr_lo[0] = a.mc_lo[0] = kb;            // strips of round K and block-row/column K+1
+  a.mr_hi[0] = a.mc_hi[0] = kb + 2 * BS;
+  return launch_tile<T, 128, 128, MODE>(dim3(tiles, tiles, 1), st, D, P, a, maxkey);
+}
+
 template <typename T>
 constexpr bool is_int_v() { return std::is_integral<T>::value; }
 
@@ -207,17 +237,53 @@ struct RoundTimes {
   cudaEvent_t *ev;  // 3 per round: after phase 1, after phase 2, after phase 3
 };
 
+// Streams for the look-ahead: phases 1-2 of round K+1 run on `side` while the bulk of
+// phase 3 of round K runs on the caller's stream (readings R12).
+struct Streams {
+  cudaStream_t main, side;
+  cudaEvent_t *sync;   // 2 per round
+};
+
 template <typename T, int MODE>
-int run_rounds(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int BS, int R,
-               int *maxkey, RoundTimes rt) {
+int run_rounds(Streams s, T *D, int32_t *P, int64_t ld, int64_t n_pad, int BS, int R, int *maxkey,
+               RoundTimes rt, bool lookahead) {
+  cudaStream_t st = s.main;
+  if (!lookahead || BS != 128 || R < 2) {
+    for (int K = 0; K < R; ++K) {
+      const int kb = K * BS;
+      TRY((launch_phase1<T, MODE>(st, D, P, ld, kb, BS, K, maxkey)));
+      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K], st));
+      TRY((launch_phase2<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
+      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 1], st));
+      TRY((launch_phase3<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
+      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 2], st));
+    }
+    return FW_OK;
+  }
+  // round 0 pivot phases on the main stream
+  TRY((launch_phase1<T, MODE>(st, D, P, ld, 0, BS, 0, maxkey)));
+  if (rt.on) CU(cudaEventRecord(rt.ev[0], st));
+  TRY((launch_phase2<T, MODE>(st, D, P, ld, n_pad, 0, BS, 0, maxkey)));
+  if (rt.on) CU(cudaEventRecord(rt.ev[1], st));
   for (int K = 0; K < R; ++K) {
     const int kb = K * BS;
-    TRY((launch_phase1<T, MODE>(st, D, P, ld, kb, BS, K, maxkey)));
-    if (rt.on) CU(cudaEventRecord(rt.ev[3 * K], st));
-    TRY((launch_phase2<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
-    if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 1], st));
-    TRY((launch_phase3<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
-    if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 2], st));
+    if (K + 1 < R) {
+      TRY((launch_phase3a<T, MODE>(st, D, P, ld, n_pad, kb, K, maxkey)));
+      CU(cudaEventRecord(s.sync[2 * K], st));
+      // side: phases 1-2 of round K+1 (they only touch block-row/column K+1)
+      CU(cudaStreamWaitEvent(s.side, s.sync[2 * K], 0));
+      TRY((launch_phase1<T, MODE>(s.side, D, P, ld, kb + BS, BS, K + 1, maxkey)));
+      if (rt.on) CU(cudaEventRecord(rt.ev[3 * (K + 1)], s.side));
+      TRY((launch_phase2<T, MODE>(s.side, D, P, ld, n_pad, kb + BS, BS, K + 1, maxkey)));
+      if (rt.on) CU(cudaEventRecord(rt.ev[3 * (K + 1) + 1], s.side));
+      CU(cudaEventRecord(s.sync[2 * K + 1], s.side));
+      TRY((launch_phase3b<T, MODE>(st, D, P, ld, n_pad, kb, K, maxkey)));
+      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 2], st));
+      CU(cudaStreamWaitEvent(st, s.sync[2 * K + 1], 0));
+    } else {
+      TRY((launch_phase3<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
+      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 2], st));
+    }
   }
   return FW_OK;
 }
@@ -237,19 +303,17 @@ int dispatch_init(int mode, cudaStream_t st, const T *src, int64_t ld_src, int64
   switch (mode) {
     case MODE_PLAIN: return run_init<T, MODE_PLAIN>(st, src, ld_src, n, D, P, ld, n_pad);
     case MODE_TAG: return run_init<T, MODE_TAG>(st, src, ld_src, n, D, P, ld, n_pad);
-    case MODE_KEY_NEXT: return run_init<T, MODE_KEY_NEXT>(st, src, ld_src, n, D, P, ld, n_pad);
-    default: return run_init<T, MODE_KEY_LASTK>(st, src, ld_src, n, D, P, ld, n_pad);
+    default: return run_init<T, MODE_KEY>(st, src, ld_src, n, D, P, ld, n_pad);
   }
 }
 
 template <typename T>
-int dispatch_rounds(int mode, cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int BS,
-                    int R, int *maxkey, RoundTimes rt) {
+int dispatch_rounds(int mode, Streams s, T *D, int32_t *P, int64_t ld, int64_t n_pad, int BS, int R,
+                    int *maxkey, RoundTimes rt, bool lookahead) {
   switch (mode) {
-    case MODE_PLAIN: return run_rounds<T, MODE_PLAIN>(st, D, P, ld, n_pad, BS, R, maxkey, rt);
-    case MODE_TAG: return run_rounds<T, MODE_TAG>(st, D, P, ld, n_pad, BS, R, maxkey, rt);
-    case MODE_KEY_NEXT: return run_rounds<T, MODE_KEY_NEXT>(st, D, P, ld, n_pad, BS, R, maxkey, rt);
-    default: return run_rounds<T, MODE_KEY_LASTK>(st, D, P, ld, n_pad, BS, R, maxkey, rt);
+    case MODE_PLAIN: return run_rounds<T, MODE_PLAIN>(s, D, P, ld, n_pad, BS, R, maxkey, rt, lookahead);
+    case MODE_TAG: return run_rounds<T, MODE_TAG>(s, D, P, ld, n_pad, BS, R, maxkey, rt, lookahead);
+    default: return run_rounds<T, MODE_KEY>(s, D, P, ld, n_pad, BS, R, maxkey, rt, lookahead);
   }
 }
 
@@ -301,7 +365,7 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
   if (want_p) {
     mode = MODE_TAG;
     if (integral && maxw <= (double)key_max) {
-      mode = lastk ? MODE_KEY_LASTK : MODE_KEY_NEXT;
+      mode = MODE_KEY;
       // stored finite values never exceed max(W) without INF entries; otherwise a path
       // value is at most (n-1)*max(W) — or is checked after the solve (max stored key)
       key_static = !has_inf || (double)(n - 1) * maxw <= (double)key_max;
@@ -338,20 +402,23 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
   }
 
   const int R = (int)((n + BS - 1) / BS);  // rounds wholly inside the padding are skipped
-  TRY(ensure_events(c, 4 + 3 * (size_t)R + 2));
+  TRY(ensure_events(c, 4 + 3 * (size_t)R + 2 + 2 * (size_t)R));
+  Streams streams{st, c.side, c.events.data() + 4 + 3 * (size_t)R + 2};
   cudaEvent_t e_begin = c.events[0], e_end = c.events[1], e_init = c.events[2],
               e_post = c.events[3];
   RoundTimes rt{timing, c.events.data() + 4};
   int *d_maxkey = d_flags + 2;
 
   CU(cudaEventRecord(e_begin, st));
+  CU(cudaStreamWaitEvent(c.side, e_begin, 0));   // the side stream follows the caller's stream
   for (int attempt = 0; attempt < 2; ++attempt) {
     // 4. init (+ key encoding), rounds
     const T *init_src = (attempt == 1 && backup) ? backup : src;
     const int64_t init_ld = (attempt == 1 && backup) ? n : ld_src;
     TRY(dispatch_init<T>(mode, st, init_src, init_ld, n, D, want_p ? Pm : nullptr, ld, n_pad));
     CU(cudaEventRecord(e_init, st));
-    TRY(dispatch_rounds<T>(mode, st, D, want_p ? Pm : nullptr, ld, n_pad, BS, R, d_maxkey, rt));
+    TRY(dispatch_rounds<T>(mode, streams, D, want_p ? Pm : nullptr, ld, n_pad, BS, R, d_maxkey, rt,
+                           c.lookahead));
     if (!is_key(mode) || key_static) break;
     CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
@@ -360,15 +427,18 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
     CU(cudaMemsetAsync(d_flags + 2, 0, 4, st));
   }
 
-  // 5. epilogue passes: keys -> distances, or tags -> P (reading R9/R10)
+  // 5. epilogue passes: keys -> distances; tags -> last k; last k -> next hop (R9/R10)
   if (is_key(mode)) {
     dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
     decode_kernel<T><<<g, 256, 0, st>>>(D, ld, n);
     CU(cudaGetLastError());
-  } else if (mode == MODE_TAG) {
+  }
+  if (mode == MODE_TAG) {
     dim3 g((unsigned)((n + 255) / 256), (unsigned)n);
     resolve_lastk_kernel<T><<<g, 256, 0, st>>>(D, ld, Pm, n, BS);
     CU(cudaGetLastError());
+  }
+  if (want_p) {
     const size_t row_bytes = (size_t)n * sizeof(int32_t);
     const int use_smem = row_bytes <= 200 * 1024;
     static bool configured = false;
@@ -419,18 +489,25 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
   }
   s.phase3_relaxations = relax;
   if (timing) {
+    // absolute event times (ms since e_begin); with the look-ahead, phases 1-2 of round K
+    // run on the side stream from the end of P3a(K-1), concurrently with P3b(K-1)
+    auto at = [&](cudaEvent_t e) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e_begin, e);
+      return (double)t;
+    };
+    const bool la = c.lookahead && BS == 128 && R >= 2;
+    const cudaEvent_t *sy = streams.sync;
+    double prev_p3_end = at(e_init);
     for (int K = 0; K < R; ++K) {
-      float a = 0, b = 0, d = 0;
-      CU(cudaEventElapsedTime(&a, K == 0 ? e_init : rt.ev[3 * K - 1], rt.ev[3 * K]));
-      CU(cudaEventElapsedTime(&b, rt.ev[3 * K], rt.ev[3 * K + 1]));
-      CU(cudaEventElapsedTime(&d, rt.ev[3 * K + 1], rt.ev[3 * K + 2]));
-      s.phase1_ms += a;
-      s.phase2_ms += b;
-      s.phase3_ms += d;
+      const double p1 = at(rt.ev[3 * K]), p2 = at(rt.ev[3 * K + 1]), p3 = at(rt.ev[3 * K + 2]);
+      const double p1_start = (la && K > 0) ? at(sy[2 * (K - 1)]) : prev_p3_end;
+      s.phase1_ms += p1 - p1_start;
+      s.phase2_ms += p2 - p1;
+      s.phase3_ms += p3 - std::max(prev_p3_end, p2);
+      prev_p3_end = p3;
     }
-    float p = 0;
-    CU(cudaEventElapsedTime(&p, rt.ev[3 * R - 1], e_post));
-    s.post_ms = p;
+    s.post_ms = at(e_post) - prev_p3_end;
   }
   c.stats = s;
   c.has_stats = true;
@@ -591,6 +668,11 @@ int fw_init(int ngpus_max, unsigned flags) {
                 prop.major, prop.minor);
   }
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;
+  CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi));
+  const char *la = getenv("FW_LOOKAHEAD");
+  c->lookahead = !(la && la[0] == '0');
   g_ctx = c;
   g_err.clear();
   return FW_OK;
@@ -609,6 +691,7 @@ int fw_free(void) {
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->side) cudaStreamDestroy(c->side);
   delete c;
   g_ctx = nullptr;
   return FW_OK;

@@ -21,7 +21,8 @@
 //           A candidate a'_ik + b'_kj = (D_ik + D_kj)*128 + (k&127) + (j&127), so the
 //           minimum over k is the minimum distance AND, among ties, the smallest k — the
 //           arg-min comes for free with the same instruction count. The epilogue recovers
-//           k, stores D' = sum - (k&127), and sets P[i][j] = P[i][k] (next hop) or k.
+//           k, stores D' = sum - (k&127) and P[i][j] = k (the paper's last intermediate
+//           vertex); a per-row pointer-jumping pass turns it into next hops.
 //           Exact while every key sum stays below 2^24 (FP32) / 2^30 (INT32); the host
 //           verifies the bound (statically, or from the max stored key after the solve).
 //   TAG     real-valued data: the epilogue writes the round number K for every element
@@ -30,6 +31,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#include <type_traits>
 
 namespace fwb {
 
@@ -37,8 +39,8 @@ constexpr int kThreads = 256;         // tile kernel: 256 threads
 constexpr int kBK = 32;               // k-chunk staged per pipeline stage
 constexpr int kTerm = 0x40000000;     // terminal bit used by the next-hop pointer jumping
 
-enum Mode { MODE_PLAIN = 0, MODE_TAG = 1, MODE_KEY_NEXT = 2, MODE_KEY_LASTK = 3 };
-__host__ __device__ constexpr bool is_key(int m) { return m >= MODE_KEY_NEXT; }
+enum Mode { MODE_PLAIN = 0, MODE_TAG = 1, MODE_KEY = 2 };
+__host__ __device__ constexpr bool is_key(int m) { return m == MODE_KEY; }
 
 template <typename T> struct Num;
 template <> struct Num<float> {
@@ -134,6 +136,7 @@ struct TileShape {
   static constexpr int kB = kBK * BSTR;
   static constexpr int kStage = kA + kB;
   static constexpr int kBytes = 2 * kStage * 4;       // two stages (double buffering)
+  static constexpr int kMinBlocks = TM * TN >= 128 * 128 ? 2 : 3;   // register budget 128 / 85
   static_assert(TX * TY == kThreads && RM >= 1 && RM * TY == TM, "tile shape");
   static_assert(TM * TN * 4 <= kBytes, "P staging must fit in the stage buffers");
 };
@@ -145,7 +148,6 @@ struct TileArgs {
   int row0[2], col0[2];          // tile grid origin (global), per blockIdx.z
   int mr_lo[2], mr_hi[2];        // excluded rows, per blockIdx.z
   int mc_lo[2], mc_hi[2];        // excluded columns, per blockIdx.z
-  int pstage[2];                 // gather P from an smem copy of the tile (column strip)
   int xrow[2];                   // 1: blockIdx.x walks tile rows (column strip in a dual launch)
   int tag;                       // round number (TAG mode)
 };
@@ -159,8 +161,8 @@ struct TileArgs {
 // through two shared-memory stages (cp.async 16 B): A row-major [i][k] (padded), B row-major
 // [k][j]. In-place use (phase 2: the tile is its own A or B) is safe: a CTA reads all its
 // A/B chunks before its epilogue writes, and no other CTA writes what it reads.
-template <typename T, int TM, int TN, int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+template <typename T, int TM, int TN, int MODE, bool DUAL = false>
+__global__ void __launch_bounds__(kThreads, TileShape<TM, TN>::kMinBlocks)
 minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g, int *maxkey) {
   using S = TileShape<TM, TN>;
   using V = typename Vec4<T>::V;
@@ -168,8 +170,9 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *smem = reinterpret_cast<T *>(smem_raw);
 
-  // select the strip description without dynamic indexing (keeps g out of local memory)
-  const bool z = blockIdx.z != 0;
+  // select the strip description without dynamic indexing (keeps g out of local memory);
+  // single-strip launches (phase 3) read everything straight from the parameter bank
+  const bool z = DUAL && blockIdx.z != 0;
   const int mr_lo = z ? g.mr_lo[1] : g.mr_lo[0], mr_hi = z ? g.mr_hi[1] : g.mr_hi[0];
   const int mc_lo = z ? g.mc_lo[1] : g.mc_lo[0], mc_hi = z ? g.mc_hi[1] : g.mc_hi[0];
   const int xrow = z ? g.xrow[1] : g.xrow[0];
@@ -233,10 +236,16 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
 #pragma unroll
       for (int r = 0; r < RM; ++r) {
         const V a = *reinterpret_cast<const V *>(as + TY * r * S::AS + 4 * q);
+        // k-pair outer, column group inner: consecutive FMNMX3 on one accumulator are
+        // H*4 instructions apart (hides the FADD2 -> FMNMX3 -> FMNMX3 latency chain)
 #pragma unroll
         for (int h = 0; h < H; ++h) {
           T *x = &acc[r][4 * h];
           relax2k(x[0], x[1], x[2], x[3], a.x, a.y, b[0][h], b[1][h]);
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          T *x = &acc[r][4 * h];
           relax2k(x[0], x[1], x[2], x[3], a.z, a.w, b[2][h], b[3][h]);
         }
       }
@@ -245,17 +254,6 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   }
 
   // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
-  const int pstage = z ? g.pstage[1] : g.pstage[0];
-  int32_t *sP = reinterpret_cast<int32_t *>(smem_raw);
-  if (MODE == MODE_KEY_NEXT && pstage) {
-    // stage this tile's P (old values) before any thread overwrites it
-    for (int e = tid; e < TM * TN / 4; e += kThreads) {
-      const int r = e / (TN / 4), c = (e % (TN / 4)) * 4;
-      *reinterpret_cast<int4 *>(sP + r * TN + c) =
-          *reinterpret_cast<const int4 *>(P + (int64_t)(i0 + r) * ld + j0 + c);
-    }
-    __syncthreads();
-  }
   const int kgrp = kb & ~127;
   int kmax = 0;
 #pragma unroll
@@ -276,7 +274,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
         const int j = jb + e;
         const T m = acc[r][4 * h + e];
         chg[e] = row_ok && !(j >= mc_lo && j < mc_hi) && m < (T)vget(old, e);
-        pv[e] = 0;
+        pv[e] = g.tag;
         if (chg[e]) {
           any = true;
           if (is_key(MODE)) {
@@ -284,13 +282,9 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
             const T key = m - Num<T>::from_int(kk);
             vset(nv, e, key);
             kmax = max(kmax, Num<T>::bits(key));
-            if (MODE == MODE_KEY_NEXT)
-              pv[e] = pstage ? sP[(i - i0) * TN + (kgrp + kk - j0)] : P[(int64_t)i * ld + kgrp + kk];
-            else
-              pv[e] = kgrp + kk;
+            pv[e] = kgrp + kk;
           } else {
             vset(nv, e, m);
-            pv[e] = g.tag;
           }
         }
       }
@@ -313,18 +307,22 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
 // ---------------------------------------------------------------------------------
 // Phase 1: closure of the diagonal block D_KK in shared memory. For each k of the
 // block in order: d[a][b] = min(d[a][b], d[a][k] + d[k][b]) (strict '<'). Row k and column k
-// are invariant during step k because d[k][k] = 0 (key: (k&127), see below), so in-place
-// updates with one barrier per k are exact. 1024 threads; thread (tx, ty) owns the
-// (BS/32)^2 elements a = ty + 32r, b = tx + 32c in registers and mirrors changes to smem.
-// Key mode: s = d'[a][k] + d'[k][b] = S*128 + (k&127) + (b&127) < d'[a][b] = D*128 + (b&127)
-// iff S < D; the new key is s - (k&127); P[a][b] <- P[a][k] (next hop) or k.
+// are invariant during step k because d[k][k] = 0, so one barrier per k is exact.
+// 1024 threads; thread (tx, ty) owns the R x R elements a = R*ty + r, b = R*tx + c in
+// registers (R = BS/32). Step k reads row k from sD and column k from its transposed copy
+// sDT (one vector load each); the owners of row k+1 and column k+1 publish them to shared
+// memory before the barrier, so no other element needs mirroring.
+// Key mode: candidate (d'[a][k] - (k&127)) + d'[k][b] = S*128 + (b&127) is directly the new
+// key when S < D, so min() keeps keys exact; P[a][b] <- k (last improving k) on change.
 template <typename T, int BS, int MODE>
 __global__ void __launch_bounds__(1024)
 phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int tag, int *maxkey) {
   constexpr int R = BS / 32;
+  using VR = typename std::conditional<R == 4, typename Vec4<T>::V,
+             typename std::conditional<R == 2, typename std::conditional<Num<T>::kIsInt, int2, float2>::type, T>::type>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *sD = reinterpret_cast<T *>(smem_raw);
-  int32_t *sP = reinterpret_cast<int32_t *>(smem_raw + BS * BS * sizeof(T));
+  T *sD = reinterpret_cast<T *>(smem_raw);     // row-major copy   [a][b]
+  T *sDT = sD + BS * BS;                        // transposed copy  [b][a]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   T *Dk = D + (int64_t)kb * ld + kb;
   int32_t *Pk = P ? P + (int64_t)kb * ld + kb : nullptr;
@@ -334,52 +332,57 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, in
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < R; ++c) {
-      const int a = ty + 32 * r, b = tx + 32 * c;
+      const int a = R * ty + r, b = R * tx + c;
       d[r][c] = Dk[(int64_t)a * ld + b];
       sD[a * BS + b] = d[r][c];
-      p[r][c] = 0;
-      if (MODE == MODE_KEY_NEXT) {
-        p[r][c] = Pk[(int64_t)a * ld + b];
-        sP[a * BS + b] = p[r][c];
-      }
+      sDT[b * BS + a] = d[r][c];
+      p[r][c] = -1;
     }
   __syncthreads();
-  for (int k = 0; k < BS; ++k) {
-    T colv[R], rowv[R];
-    int32_t pk[R];
+  // k is unrolled by R so that "row/column k+1 lives in register slot (k+1) % R" is a
+  // compile-time index (a runtime index into d[][] would spill the register array)
+  for (int k0 = 0; k0 < BS; k0 += R) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      colv[r] = sD[(ty + 32 * r) * BS + k];
-      if (MODE == MODE_KEY_NEXT) pk[r] = sP[(ty + 32 * r) * BS + k];
-    }
+    for (int kr = 0; kr < R; ++kr) {
+      const int k = k0 + kr;
+      const VR cv = *reinterpret_cast<const VR *>(sDT + k * BS + R * ty);   // d[a][k], own rows
+      const VR rv = *reinterpret_cast<const VR *>(sD + k * BS + R * tx);    // d[k][b], own cols
+      const T *colv = reinterpret_cast<const T *>(&cv);
+      const T *rowv = reinterpret_cast<const T *>(&rv);
+      const T kp = is_key(MODE) ? Num<T>::from_int((kb + k) & 127) : (T)0;
 #pragma unroll
-    for (int c = 0; c < R; ++c) rowv[c] = sD[k * BS + tx + 32 * c];
-    const T kp = Num<T>::from_int((kb + k) & 127);
+      for (int r = 0; r < R; ++r) {
+        // exact (keys are integers < 2^24 / 2^30); INF must stay INF (INT32 sentinel arithmetic)
+        const T cr = (is_key(MODE) && Num<T>::finite(colv[r])) ? colv[r] - kp : colv[r];
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < R; ++c) {
-        T s = colv[r] + rowv[c];
-        if (s < d[r][c]) {
-          if (is_key(MODE)) s = s - kp;
-          d[r][c] = s;
-          sD[(ty + 32 * r) * BS + tx + 32 * c] = s;
-          if (MODE == MODE_KEY_NEXT) {
-            p[r][c] = pk[r];
-            sP[(ty + 32 * r) * BS + tx + 32 * c] = pk[r];
-          } else if (MODE == MODE_KEY_LASTK) {
-            p[r][c] = kb + k;
-          }
+        for (int c = 0; c < R; ++c) {
+          const T s = cr + rowv[c];
+          if (is_key(MODE)) p[r][c] = s < d[r][c] ? kb + k : p[r][c];
+          d[r][c] = s < d[r][c] ? s : d[r][c];
         }
       }
-    __syncthreads();
+      // publish row k+1 and column k+1 (register slot (kr+1) % R of owner ty / tx) for step k+1
+      const int slot = (kr + 1) % R;   // constant after unrolling
+      const int owner = (k0 + kr + 1) / R;
+      if (k + 1 < BS) {
+        if (owner == ty) {
+#pragma unroll
+          for (int c = 0; c < R; ++c) sD[(k + 1) * BS + R * tx + c] = d[slot][c];
+        }
+        if (owner == tx) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) sDT[(k + 1) * BS + R * ty + r] = d[r][slot];
+        }
+      }
+      __syncthreads();
+    }
   }
   int kmax = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int c = 0; c < R; ++c) {
-      const int a = ty + 32 * r, b = tx + 32 * c;
+      const int a = R * ty + r, b = R * tx + c;
       const int64_t off = (int64_t)a * ld + b;
       if (d[r][c] < Dk[off]) {
         Dk[off] = d[r][c];
@@ -424,9 +427,8 @@ __global__ void validate_kernel(const T *src, int64_t lds, int64_t n, int *flags
 }
 
 // Copy W (n x n, lds) into the padded n_pad x n_pad working matrix (ld): padded entries INF,
-// diagonal 0 (R4, R11); key modes store D*128 + (j&127). P initialised per mode:
-// KEY_NEXT: next hop of the direct edge (j), i on the diagonal, -1 without an edge;
-// otherwise -1 (no intermediate / no tag yet). src may alias D (in-place solve).
+// diagonal 0 (R4, R11); key mode stores D*128 + (j&127). P (tags / last k) initialised to -1
+// ("no intermediate yet"). src may alias D (in-place solve).
 template <typename T, int MODE>
 __global__ void init_kernel(const T *src, int64_t lds, int64_t n, T *D, int32_t *P, int64_t ld,
                             int64_t n_pad) {
@@ -435,11 +437,7 @@ __global__ void init_kernel(const T *src, int64_t lds, int64_t n, T *D, int32_t 
        j += (int64_t)gridDim.x * blockDim.x) {
     T v = (i < n && j < n) ? src[i * lds + j] : Num<T>::inf();
     if (i == j) v = 0;
-    if (MODE != MODE_PLAIN) {
-      int32_t p = -1;
-      if (MODE == MODE_KEY_NEXT) p = (i == j) ? (int32_t)i : (Num<T>::finite(v) ? (int32_t)j : -1);
-      P[i * ld + j] = p;
-    }
+    if (MODE != MODE_PLAIN) P[i * ld + j] = -1;
     if (is_key(MODE)) v = Num<T>::encode(v, (int)j);
     D[i * ld + j] = v;
   }

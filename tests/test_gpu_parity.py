@@ -350,7 +350,7 @@ def test_real_weights_use_tags():
 def test_keyed_lastk():
     W = gen.generate("er_int", 513, 14, p=0.05, lo=1, hi=1000)
     D, P, s = _solve_stats(W, 32, fw.FW_PATH_LAST_K)
-    assert s.p_method == 3
+    assert s.p_method == 2
     np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
     assert oracle.check_paths(W, D, P, mode="lastk")[0] == 0
 
