@@ -51,7 +51,7 @@ enum fw_status {
   FW_EINVAL = 1, /* bad argument or out-of-domain weight (negative, NaN, > FW_INF_I32) */
   FW_ENOMEM = 2, /* device or pinned-host allocation failed                          */
   FW_ECUDA = 3,  /* a CUDA runtime call or kernel failed                              */
-  FW_ENCCL = 4,  /* reserved for the multi-GPU transport                               */
+  FW_ENCCL = 4,  /* NCCL (multi-GPU transport) unavailable or failed                    */
   FW_ESTATE = 5, /* fw_init not called, or called twice                               */
   FW_ERANGE = 6  /* INT32: (n-1) * max finite weight >= FW_INF_I32 (sums could hit INF) */
 };
@@ -118,13 +118,52 @@ int fw_solve_device_f32(float *d_dist, int32_t *d_next, int64_t n, int64_t ld, i
 int fw_solve_device_i32(int32_t *d_dist, int32_t *d_next, int64_t n, int64_t ld, int block,
                         void *stream);
 
+/* ---- multi-GPU: one process per GPU (SURVEY §8 e; BJ north_star) ----------------------------
+ * D and P are partitioned by contiguous block-rows: the n_pad/128 tile rows are split over
+ * `world` ranks in ranges whose sizes differ by at most one. Each round the owner of the pivot
+ * block-row runs phases 1-2 on it and broadcasts the pivot row strip (BS x n_pad elements,
+ * ncclBroadcast over NVLink); every rank then updates its own rows (phase-2 column strip and
+ * phase 3). This is the method's only exchange step; the look-ahead overlaps it with phase 3.
+ *
+ * fw_dist_partition: host-only (no GPU needed). Rows [row0, row0 + nrows) of the n x n matrix
+ *   belong to `rank` (nrows = 0 when a rank gets only padding). Returns FW_EINVAL on bad args.
+ * fw_dist_owner: rank owning (padded) global row `row`, or -1.
+ * fw_comm_unique_id: fill out[128] with an NCCL unique id (call on one rank; the caller ships
+ *   the bytes to the others, e.g. with torch.distributed). FW_ENCCL if NCCL cannot be loaded.
+ * fw_comm_init: after fw_init, join the communicator of `world` ranks as `rank` on the current
+ *   device. While a communicator is active only fw_dist_solve_* may solve; fw_comm_free
+ *   returns the context to single-GPU use.
+ * fw_dist_solve_device_f32/i32: collective; every rank calls it with the same n and block and
+ *   its own rows: d_rows holds rows [row0, row0 + nrows) of the n x n input (row pitch ld >= n),
+ *   overwritten with the same rows of D; d_next_rows (same shape, int32) receives P or is
+ *   NULL on every rank. Errors are agreed on by all ranks (validation is all-reduced). */
+int fw_dist_partition(int64_t n, int world, int rank, int64_t *row0, int64_t *nrows);
+int fw_dist_owner(int64_t n, int world, int64_t row);
+int fw_comm_unique_id(unsigned char *out);
+int fw_comm_init(const unsigned char *id, int rank, int world);
+int fw_comm_free(void);
+int fw_dist_solve_device_f32(float *d_rows, int32_t *d_next_rows, int64_t n, int64_t ld, int block,
+                             void *stream);
+int fw_dist_solve_device_i32(int32_t *d_rows, int32_t *d_next_rows, int64_t n, int64_t ld,
+                             int block, void *stream);
+
+/* Loopback transport (testing the partitioned path on one GPU): every rank of a `world`-way
+ * block-row partition is emulated in this process on `stream` — per-rank phase launches on its
+ * own rows, the pivot-strip broadcast as a device copy into each rank's receive buffer, the
+ * look-ahead tile split per rank. Same arguments and results as fw_solve_device_*; world in
+ * [1, 64]. Not a performance path. */
+int fw_dist_loopback_solve_device_f32(float *d_dist, int32_t *d_next, int64_t n, int64_t ld,
+                                      int block, int world, void *stream);
+int fw_dist_loopback_solve_device_i32(int32_t *d_dist, int32_t *d_next, int64_t n, int64_t ld,
+                                      int block, int world, void *stream);
+
 /* Message for the last non-OK return on this thread ("" if none). */
 const char *fw_last_error(void);
 
 /* Copy the statistics of the last successful solve. FW_ESTATE if none yet. */
 int fw_last_stats(fw_stats *out);
 
-/* Library version string, e.g. "fwb200 0.1 sm_100a". */
+/* Library version string, e.g. "fwb200 0.2 sm_100a". */
 const char *fw_version(void);
 
 #ifdef __cplusplus

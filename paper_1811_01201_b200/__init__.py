@@ -17,6 +17,15 @@ from ._binding import (  # noqa: F401
     fw_solve_device_f32,
     fw_solve_device_i32,
     fw_last_error,
+    fw_dist_partition,
+    fw_dist_owner,
+    fw_comm_unique_id,
+    fw_comm_init,
+    fw_comm_free,
+    fw_dist_solve_device_f32,
+    fw_dist_solve_device_i32,
+    fw_dist_loopback_solve_device_f32,
+    fw_dist_loopback_solve_device_i32,
     fw_last_stats,
     fw_version,
     library_path,

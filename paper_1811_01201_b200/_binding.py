@@ -56,6 +56,15 @@ _lib.fw_solve.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_solve_i32.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _P]
+_lib.fw_dist_partition.argtypes = [_I64, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+_lib.fw_dist_owner.argtypes = [_I64, _I, _I64]
+_lib.fw_comm_unique_id.argtypes = [ctypes.c_char_p]
+_lib.fw_comm_init.argtypes = [ctypes.c_char_p, _I, _I]
+_lib.fw_comm_free.argtypes = []
+_lib.fw_dist_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _P]
+_lib.fw_dist_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _P]
+_lib.fw_dist_loopback_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _I, _P]
+_lib.fw_dist_loopback_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _I, _P]
 _lib.fw_last_error.restype = ctypes.c_char_p
 _lib.fw_last_stats.argtypes = [ctypes.POINTER(FwStats)]
 _lib.fw_version.restype = ctypes.c_char_p
@@ -135,6 +144,67 @@ def fw_solve_device_i32(d_dist, d_next=None, n=None, ld=None, block: int = 0, st
     ld = n if ld is None else ld
     _check(_lib.fw_solve_device_i32(_addr(d_dist, "int32"), _addr(d_next, "int32"), n, ld, block,
                                     _stream_handle(stream)))
+
+
+def fw_dist_partition(n: int, world: int, rank: int) -> tuple[int, int]:
+    """(row0, nrows): the rows of the n x n matrix rank `rank` of `world` holds (host-only)."""
+    r0, nr = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.fw_dist_partition(n, world, rank, ctypes.byref(r0), ctypes.byref(nr)))
+    return r0.value, nr.value
+
+
+def fw_dist_owner(n: int, world: int, row: int) -> int:
+    return _lib.fw_dist_owner(n, world, row)
+
+
+def fw_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.fw_comm_unique_id(buf))
+    return buf.raw
+
+
+def fw_comm_init(uid: bytes, rank: int, world: int) -> None:
+    if len(uid) != 128:
+        raise ValueError("NCCL unique id must be 128 bytes")
+    _check(_lib.fw_comm_init(uid, rank, world))
+
+
+def fw_comm_free() -> None:
+    _check(_lib.fw_comm_free())
+
+
+def fw_dist_solve_device_f32(d_rows, d_next_rows=None, n=None, ld=None, block: int = 0, stream=None) -> None:
+    """Collective FP32 solve of this rank's rows (see fw_dist_partition)."""
+    if n is None:
+        raise ValueError("n (global vertex count) is required")
+    ld = d_rows.shape[1] if ld is None else ld
+    _check(_lib.fw_dist_solve_device_f32(_addr(d_rows, "float32"), _addr(d_next_rows, "int32"), n, ld,
+                                         block, _stream_handle(stream)))
+
+
+def fw_dist_solve_device_i32(d_rows, d_next_rows=None, n=None, ld=None, block: int = 0, stream=None) -> None:
+    if n is None:
+        raise ValueError("n (global vertex count) is required")
+    ld = d_rows.shape[1] if ld is None else ld
+    _check(_lib.fw_dist_solve_device_i32(_addr(d_rows, "int32"), _addr(d_next_rows, "int32"), n, ld,
+                                         block, _stream_handle(stream)))
+
+
+def fw_dist_loopback_solve_device_f32(d_dist, d_next=None, n=None, ld=None, block: int = 0, world: int = 2,
+                                      stream=None) -> None:
+    """Every rank of a `world`-way partition emulated on this GPU (testing transport)."""
+    n = _n_of(d_dist, n)
+    ld = n if ld is None else ld
+    _check(_lib.fw_dist_loopback_solve_device_f32(_addr(d_dist, "float32"), _addr(d_next, "int32"), n, ld,
+                                                  block, world, _stream_handle(stream)))
+
+
+def fw_dist_loopback_solve_device_i32(d_dist, d_next=None, n=None, ld=None, block: int = 0, world: int = 2,
+                                      stream=None) -> None:
+    n = _n_of(d_dist, n)
+    ld = n if ld is None else ld
+    _check(_lib.fw_dist_loopback_solve_device_i32(_addr(d_dist, "int32"), _addr(d_next, "int32"), n, ld,
+                                                  block, world, _stream_handle(stream)))
 
 
 def fw_last_error() -> str:

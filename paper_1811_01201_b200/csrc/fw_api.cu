@@ -1,15 +1,23 @@
-// fw_api.cu — C ABI (include/fw.h) and the single-GPU round driver of the blocked
-// Floyd–Warshall solve (arxiv 1811.01201 §4.1).
+// fw_api.cu — C ABI (include/fw.h) and the round driver of the blocked Floyd–Warshall solve
+// (arxiv 1811.01201 §4.1), on one GPU or on a block-row partition over
+// several GPUs (one process per GPU, NCCL over NVLink).
 //
-// Round loop (OpenMP structure of P:151-155 mapped to stream-ordered
-// launches): for K in 0..R-1: phase 1 on D_KK (1 CTA), phase 2 on the pivot row strip
-// and column strip (two launches), phase 3 on the rest (one launch of 128x128 tiles).
-// Stream order replaces the paper's implicit OpenMP barriers; the host only enqueues.
-// After the rounds, the post-pass turns the round tags into P (reading R9).
+// Round K (the OpenMP structure of P:151-155 becomes stream order):
+//   owner(K)  phase 1 on D_KK, phase 2 on its row strip
+//   owner(K)  -> all: broadcast of the pivot row strip (BS x n_pad) — the only exchange
+//   every GPU phase 2 column strip of its rows (D_KK* comes with the strip)
+//   every GPU phase 3 on its rows with A = own column strip, B = the pivot row strip
+// Look-ahead (a8): phase 3 of round K is split so that the tiles round K+1's pivot phases
+// read are done first (P3a); the pivot phases and broadcast of round K+1 then run on a
+// high-priority side stream while the rest of phase 3 (P3b) runs on the main stream.
+// After the rounds the post-pass turns keys / round tags into P (reading R9).
+// One GPU is the world = 1 case of the same driver (no broadcast: B is read in place).
 #include "fw_kernels.cuh"
 #include "../../include/fw.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -50,6 +58,44 @@ int fail(int code, const char *fmt, ...) {
     if (rc_ != FW_OK) return rc_; \
   } while (0)
 
+// ---- NCCL, loaded on first use (the libnccl.so.2 torch has already loaded, when present) ----
+struct Nccl {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl g_nccl;
+
+int load_nccl() {
+  if (g_nccl.h) return FW_OK;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(FW_ENCCL, "cannot load libnccl.so.2: %s", dlerror());
+#define SYM(name)                                                                        \
+  *reinterpret_cast<void **>(&g_nccl.name) = dlsym(h, "nccl" #name);                     \
+  if (!g_nccl.name) return fail(FW_ENCCL, "libnccl.so.2 lacks nccl" #name);
+  SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(Broadcast) SYM(AllReduce)
+  SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
+#undef SYM
+  g_nccl.h = h;
+  return FW_OK;
+}
+
+#define NC(call)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return fail(FW_ENCCL, "%s failed: %s", #call, g_nccl.GetErrorString(r_));           \
+  } while (0)
+
+// ---- device / host buffers --------------------------------------------------------------
 struct DevBuf {
   void *p = nullptr;
   size_t bytes = 0;
@@ -78,13 +124,17 @@ struct Ctx {
   cudaStream_t stream = nullptr;   // internal stream for the host entry points
   cudaStream_t side = nullptr;     // high-priority stream for the look-ahead pivot phases
   bool lookahead = true;
-  DevBuf ws_d, ws_t;               // padded workspaces (D, tags/P)
+  DevBuf ws_d, ws_t;               // padded local workspaces (D, tags/P)
   DevBuf ws_b;                     // backup of W for a speculative key run (in place)
+  DevBuf ws_s;                     // two pivot-strip receive buffers (multi-GPU)
+  DevBuf ws_full;                  // gathered final D (multi-GPU, round tags only)
   DevBuf user_d, user_t;           // device copies of host buffers (host entry points)
-  DevBuf scratch;                  // validation flags
+  DevBuf scratch;                  // flags / reductions
   void *pinned = nullptr;          // staging for pageable host buffers
   size_t pinned_bytes = 0;
   std::vector<cudaEvent_t> events;
+  ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init)
+  int rank = 0, world = 1;
   fw_stats stats{};
   bool has_stats = false;
 };
@@ -92,7 +142,7 @@ struct Ctx {
 Ctx *g_ctx = nullptr;
 
 constexpr size_t kStageBytes = 64ull << 20;  // pinned staging chunk
-// Largest initial/stored distance for which key sums stay exact (kernels header, KEY_*):
+// Largest initial/stored distance for which key sums stay exact (kernels header, KEY mode):
 // FP32: 2*(T*128+127) < 2^24; INT32: 2*(T*128+127) < FW_INF_I32 (INF + key < 2^31 as well).
 constexpr int64_t kKeyMaxF32 = 65534;
 constexpr int64_t kKeyMaxI32 = 4194302;
@@ -106,9 +156,31 @@ int ensure_events(Ctx &c, size_t count) {
   return FW_OK;
 }
 
-// ---- kernel launch wrappers ---------------------------------------------------------
+// ---- block-row partition (SURVEY §8 e) ------------------------------------------------------
+// The n_pad/128 tile rows are split into `world` contiguous ranges whose sizes differ by at
+// most one tile row; rank r owns global rows [row0, row0 + nrows) of the padded matrix.
+void partition(int64_t n, int world, int rank, int64_t *row0, int64_t *nrows) {
+  const int64_t tiles = (n + 127) / 128;
+  const int64_t base = tiles / world, rem = tiles % world;
+  const int64_t t0 = rank * base + std::min<int64_t>(rank, rem);
+  const int64_t cnt = base + (rank < rem ? 1 : 0);
+  *row0 = t0 * 128;
+  *nrows = cnt * 128;
+}
+
+int owner_of(int64_t n, int world, int64_t row) {
+  for (int r = 0; r < world; ++r) {
+    int64_t r0, nr;
+    partition(n, world, r, &r0, &nr);
+    if (row >= r0 && row < r0 + nr) return r;
+  }
+  return -1;
+}
+
+// ---- kernel launch wrappers ----------------------------------------------------------------
 template <typename T, int TM, int TN, int MODE>
 int launch_tile(dim3 grid, cudaStream_t st, T *D, int32_t *P, const TileArgs &a, int *maxkey) {
+  if (grid.x == 0 || grid.y == 0) return FW_OK;
   constexpr int bytes = TileShape<TM, TN>::kBytes;
   auto kern = grid.z > 1 ? minplus_tile_kernel<T, TM, TN, MODE, true>
                          : minplus_tile_kernel<T, TM, TN, MODE, false>;
@@ -125,21 +197,35 @@ int launch_tile(dim3 grid, cudaStream_t st, T *D, int32_t *P, const TileArgs &a,
   return FW_OK;
 }
 
-TileArgs tile_args(int64_t ld, int kb, int BS, int tag) {
+// One strip description (z slot) of a tile launch: tile grid origin (local row, global
+// column), excluded local rows [mr_lo, mr_hi) and global columns [mc_lo, mc_hi), and whether
+// blockIdx.x walks tile rows (a column strip sharing a launch with a row strip).
+struct Strip {
+  int row0, col0, mr_lo, mr_hi, mc_lo, mc_hi, xrow;
+};
+
+TileArgs tile_args(int64_t ld, const void *B, int64_t ldb, int kb, int BS, int tag, int64_t rows,
+                   int64_t cols) {
   TileArgs a{};
   a.ld = ld;
+  a.rows_lim = (int)rows;
+  a.cols_lim = (int)cols;
+  a.B = B;
+  a.ldb = ldb;
   a.kb = kb;
   a.Kd = BS;
   a.tag = tag;
-  for (int z = 0; z < 2; ++z) {
-    a.mr_lo[z] = a.mr_hi[z] = a.mc_lo[z] = a.mc_hi[z] = 0;
-    a.row0[z] = a.col0[z] = a.xrow[z] = 0;
-  }
   return a;
 }
 
+void put(TileArgs &a, int z, const Strip &s) {
+  a.row0[z] = s.row0; a.col0[z] = s.col0; a.mr_lo[z] = s.mr_lo; a.mr_hi[z] = s.mr_hi;
+  a.mc_lo[z] = s.mc_lo; a.mc_hi[z] = s.mc_hi; a.xrow[z] = s.xrow;
+}
+
 template <typename T, int BS, int MODE>
-int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int kb, int K, int *maxkey) {
+int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int kb, int K,
+                     int *maxkey) {
   const int bytes = 2 * BS * BS * (int)sizeof(T);   // row-major + transposed copy of D_KK
   auto kern = phase1_kernel<T, BS, MODE>;
   static bool configured = false;
@@ -147,198 +233,293 @@ int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int kb, int 
     CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     configured = true;
   }
-  kern<<<1, 1024, bytes, st>>>(D, P, ld, kb, K, maxkey);
+  kern<<<1, 1024, bytes, st>>>(D, P, ld, r0, kb, K, maxkey);
   CU(cudaGetLastError());
   return FW_OK;
 }
 
+// Per-round event slots: 3 per round (after phase 1, after phase 2, after phase 3) and 2
+// look-ahead synchronisation events per round.
+struct Events {
+  bool timing;
+  cudaEvent_t *ev;
+  cudaEvent_t *sync;
+};
+
+// The rounds of one GPU's rows (local rows [0, nrows) = global [row0, row0 + nrows)).
 template <typename T, int MODE>
-int launch_phase1(cudaStream_t st, T *D, int32_t *P, int64_t ld, int kb, int BS, int K, int *maxkey) {
-  switch (BS) {
-    case 32: return launch_phase1_bs<T, 32, MODE>(st, D, P, ld, kb, K, maxkey);
-    case 64: return launch_phase1_bs<T, 64, MODE>(st, D, P, ld, kb, K, maxkey);
-    case 128: return launch_phase1_bs<T, 128, MODE>(st, D, P, ld, kb, K, maxkey);
+struct Rounds {
+  Ctx &c;
+  int world;     // ranks of the partition (1, the NCCL communicator, or loopback parts)
+  T *D;
+  int32_t *P;
+  int64_t ld, n, n_pad, row0, nrows;
+  int BS, R;
+  int *maxkey;
+  T *strip[2];   // receive buffers of the pivot row strip (world > 1)
+
+  bool owns(int K) const {
+    const int64_t kb = (int64_t)K * BS;
+    return kb >= row0 && kb < row0 + nrows;
   }
-  return fail(FW_EINVAL, "unsupported block size %d", BS);
-}
-
-// Phase 2: row strip D[kb:kb+BS, :] and column strip D[:, kb:kb+BS] relaxed
-// through the closed diagonal block D_KK* (min-plus product form, reading R7). Both strips
-// exclude the diagonal block itself. BS = 128: one launch (blockIdx.z picks the strip).
-template <typename T, int MODE, int BS>
-int launch_phase2_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int K,
-                     int *maxkey) {
-  const int tiles = (int)(n_pad / 128);
-  TileArgs a = tile_args(ld, kb, BS, K);
-  // z = 0: row strip, tiles BS x 128 across the columns; exclude the diagonal block columns
-  a.row0[0] = kb; a.col0[0] = 0; a.mc_lo[0] = kb; a.mc_hi[0] = kb + BS;
-  // z = 1: column strip, tiles 128 x BS down the rows; exclude the diagonal block rows
-  a.row0[1] = 0; a.col0[1] = kb; a.mr_lo[1] = kb; a.mr_hi[1] = kb + BS; a.xrow[1] = 1;
-  if (BS == 128) return launch_tile<T, 128, 128, MODE>(dim3(tiles, 1, 2), st, D, P, a, maxkey);
-  TileArgs c = a;
-  c.row0[0] = 0; c.col0[0] = kb; c.mr_lo[0] = kb; c.mr_hi[0] = kb + BS; c.mc_lo[0] = c.mc_hi[0] = 0;
-  c.xrow[0] = 1;
-  TRY((launch_tile<T, BS, 128, MODE>(dim3(tiles, 1, 1), st, D, P, a, maxkey)));
-  return launch_tile<T, 128, BS, MODE>(dim3(tiles, 1, 1), st, D, P, c, maxkey);
-}
-
-template <typename T, int MODE>
-int launch_phase2(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int BS,
-                  int K, int *maxkey) {
-  switch (BS) {
-    case 32: return launch_phase2_bs<T, MODE, 32>(st, D, P, ld, n_pad, kb, K, maxkey);
-    case 64: return launch_phase2_bs<T, MODE, 64>(st, D, P, ld, n_pad, kb, K, maxkey);
-    case 128: return launch_phase2_bs<T, MODE, 128>(st, D, P, ld, n_pad, kb, K, maxkey);
+  int lrow(int K) const { return (int)((int64_t)K * BS - row0); }
+  // B operand of round K: the pivot row strip (global rows kb..kb+BS), read in place on its
+  // owner and from the broadcast buffer elsewhere
+  const T *bstrip(int K) const {
+    return (world == 1 || owns(K)) ? D + (int64_t)lrow(K) * ld : strip[K & 1];
   }
-  return fail(FW_EINVAL, "unsupported block size %d", BS);
+
+  int phase1(cudaStream_t st, int K) {
+    if (!owns(K)) return FW_OK;
+    switch (BS) {
+      case 32: return launch_phase1_bs<T, 32, MODE>(st, D, P, ld, lrow(K), K * BS, K, maxkey);
+      case 64: return launch_phase1_bs<T, 64, MODE>(st, D, P, ld, lrow(K), K * BS, K, maxkey);
+      default: return launch_phase1_bs<T, 128, MODE>(st, D, P, ld, lrow(K), K * BS, K, maxkey);
+    }
+  }
+
+  // Phase 2: row strip (owner) and column strip (local rows) relaxed through the
+  // closed diagonal block D_KK* (product form, reading R7); the diagonal block is excluded.
+  template <int B>
+  int phase2_bs(cudaStream_t st, int K, bool row_strip, bool col_strip) {
+    const int kb = K * B, tiles_c = (int)(n_pad / 128), tiles_r = (int)(nrows / 128);
+    TileArgs a = tile_args(ld, bstrip(K), ld, kb, B, K, nrows, n_pad);
+    const bool own = owns(K);
+    const int lr = own ? lrow(K) : 0;
+    const Strip row{lr, 0, 0, 0, kb, kb + B, 0};                          // B x 128 tiles
+    const Strip col{0, kb, own ? lr : 0, own ? lr + B : 0, 0, 0, 1};      // 128 x B tiles
+    row_strip = row_strip && own;
+    if (B == 128 && row_strip && col_strip) {
+      put(a, 0, row);
+      put(a, 1, col);
+      return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 1, 2), st, D, P, a,
+                                            maxkey);
+    }
+    if (row_strip) {
+      put(a, 0, row);
+      TRY((launch_tile<T, B, 128, MODE>(dim3(tiles_c, 1, 1), st, D, P, a, maxkey)));
+    }
+    if (col_strip) {
+      put(a, 0, col);
+      TRY((launch_tile<T, 128, B, MODE>(dim3(tiles_r, 1, 1), st, D, P, a, maxkey)));
+    }
+    return FW_OK;
+  }
+  int phase2(cudaStream_t st, int K, bool row_strip, bool col_strip) {
+    switch (BS) {
+      case 32: return phase2_bs<32>(st, K, row_strip, col_strip);
+      case 64: return phase2_bs<64>(st, K, row_strip, col_strip);
+      default: return phase2_bs<128>(st, K, row_strip, col_strip);
+    }
+  }
+
+  // Phase 3 on the local rows except rows [rx_lo, rx_hi) and columns [cx_lo, cx_hi).
+  int phase3(cudaStream_t st, int K, int rx_lo, int rx_hi, int cx_lo, int cx_hi) {
+    TileArgs a = tile_args(ld, bstrip(K), ld, K * BS, BS, K, nrows, n_pad);
+    put(a, 0, Strip{0, 0, rx_lo, rx_hi, cx_lo, cx_hi, 0});
+    return launch_tile<T, 128, 128, MODE>(dim3((unsigned)(n_pad / 128), (unsigned)(nrows / 128), 1),
+                                          st, D, P, a, maxkey);
+  }
+  int phase3_full(cudaStream_t st, int K) {
+    const int kb = K * BS;
+    const bool own = owns(K);
+    return phase3(st, K, own ? lrow(K) : 0, own ? lrow(K) + BS : 0, kb, kb + BS);
+  }
+
+  // Look-ahead split (BS = 128): P3a = the tiles round K+1's pivot phases read (block-row
+  // K+1 if local; block-column K+1 of the local rows), P3b = every other tile.
+  int phase3a(cudaStream_t st, int K) {
+    const int kb = K * BS, kn = kb + BS;
+    TileArgs a = tile_args(ld, bstrip(K), ld, kb, BS, K, nrows, n_pad);
+    const bool own_k = owns(K), own_n = owns(K + 1);
+    int ex_lo = own_k ? lrow(K) : 0, ex_hi = own_k ? lrow(K) + BS : 0;   // rows of strip K
+    const int rn = own_n ? lrow(K + 1) : 0;
+    if (own_n) {   // also exclude block-row K+1 (done by z = 0); adjacent to strip K if local
+      if (own_k) ex_hi = rn + BS;
+      else { ex_lo = rn; ex_hi = rn + BS; }
+    }
+    const Strip col{0, kn, ex_lo, ex_hi, 0, 0, 1};
+    const int tiles_c = (int)(n_pad / 128), tiles_r = (int)(nrows / 128);
+    if (own_n) {
+      put(a, 0, Strip{rn, 0, 0, 0, kb, kb + BS, 0});   // block-row K+1, all columns but strip K
+      put(a, 1, col);
+      return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 1, 2), st, D, P, a,
+                                            maxkey);
+    }
+    put(a, 0, col);
+    return launch_tile<T, 128, 128, MODE>(dim3(tiles_r, 1, 1), st, D, P, a, maxkey);
+  }
+  int phase3b(cudaStream_t st, int K) {
+    int lo = 0, hi = 0;   // local rows of blocks K and K+1 (contiguous when both are local)
+    if (owns(K)) { lo = lrow(K); hi = lrow(K) + BS; }
+    if (owns(K + 1)) { if (hi == 0) lo = lrow(K + 1); hi = lrow(K + 1) + BS; }
+    return phase3(st, K, lo, hi, K * BS, K * BS + 2 * BS);
+  }
+
+  int run(cudaStream_t st, const Events &e, bool lookahead) {
+    cudaEvent_t *ev = e.ev;
+    if (!lookahead || BS != 128 || R < 2) {
+      for (int K = 0; K < R; ++K) {
+        TRY(phase1(st, K));
+        if (e.timing) CU(cudaEventRecord(ev[3 * K], st));
+        TRY(pivot_rest(st, K));
+        if (e.timing) CU(cudaEventRecord(ev[3 * K + 1], st));
+        TRY(phase3_full(st, K));
+        if (e.timing) CU(cudaEventRecord(ev[3 * K + 2], st));
+      }
+      return FW_OK;
+    }
+    cudaStream_t side = c.side;
+    TRY(phase1(st, 0));
+    if (e.timing) CU(cudaEventRecord(ev[0], st));
+    TRY(pivot_rest(st, 0));
+    if (e.timing) CU(cudaEventRecord(ev[1], st));
+    for (int K = 0; K < R; ++K) {
+      if (K + 1 < R) {
+        TRY(phase3a(st, K));
+        CU(cudaEventRecord(e.sync[2 * K], st));
+        CU(cudaStreamWaitEvent(side, e.sync[2 * K], 0));
+        TRY(phase1(side, K + 1));
+        if (e.timing) CU(cudaEventRecord(ev[3 * (K + 1)], side));
+        TRY(pivot_rest(side, K + 1));
+        if (e.timing) CU(cudaEventRecord(ev[3 * (K + 1) + 1], side));
+        CU(cudaEventRecord(e.sync[2 * K + 1], side));
+        TRY(phase3b(st, K));
+        if (e.timing) CU(cudaEventRecord(ev[3 * K + 2], st));
+        CU(cudaStreamWaitEvent(st, e.sync[2 * K + 1], 0));
+      } else {
+        TRY(phase3_full(st, K));
+        if (e.timing) CU(cudaEventRecord(ev[3 * K + 2], st));
+      }
+    }
+    return FW_OK;
+  }
+
+  // pivot phases after phase 1: strips and (multi-GPU) the broadcast
+  int pivot_rest(cudaStream_t st, int K) {
+    if (world == 1) return phase2(st, K, true, true);
+    TRY(phase2(st, K, true, false));
+    void *buf = owns(K) ? (void *)(D + (int64_t)lrow(K) * ld) : (void *)strip[K & 1];
+    NC(g_nccl.Broadcast(buf, buf, (size_t)BS * (size_t)n_pad,
+                        std::is_integral<T>::value ? ncclInt32 : ncclFloat32,
+                        owner_of(n_pad, world, (int64_t)K * BS), c.comm, st));
+    return phase2(st, K, false, true);
+  }
+};
+
+// Loopback transport: all ranks of the partition emulated in this process on one stream
+// (the broadcast becomes a device-to-device copy). Kernels never wait on one another, so
+// running the ranks one after another exercises the partitioned indexing, the strip
+// ownership and the look-ahead tile split of the multi-GPU path on a single GPU.
+template <typename T, int MODE>
+int run_loopback(std::vector<Rounds<T, MODE>> &rk, cudaStream_t st, bool lookahead) {
+  const int R = rk[0].R, BS = rk[0].BS, W = (int)rk.size();
+  const int64_t n_pad = rk[0].n_pad;
+  auto pivot = [&](int K) -> int {
+    const int o = owner_of(n_pad, W, (int64_t)K * BS);
+    TRY(rk[o].phase1(st, K));
+    TRY(rk[o].phase2(st, K, true, false));
+    const T *src = rk[o].D + (int64_t)rk[o].lrow(K) * rk[o].ld;
+    for (int r = 0; r < W; ++r)
+      if (r != o)
+        CU(cudaMemcpy2DAsync(rk[r].strip[K & 1], n_pad * sizeof(T), src, rk[o].ld * sizeof(T),
+                             n_pad * sizeof(T), BS, cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < W; ++r) TRY(rk[r].phase2(st, K, false, true));
+    return FW_OK;
+  };
+  if (!lookahead || BS != 128 || R < 2) {
+    for (int K = 0; K < R; ++K) {
+      TRY(pivot(K));
+      for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(st, K));
+    }
+    return FW_OK;
+  }
+  TRY(pivot(0));
+  for (int K = 0; K < R; ++K) {
+    if (K + 1 < R) {
+      for (int r = 0; r < W; ++r) TRY(rk[r].phase3a(st, K));
+      TRY(pivot(K + 1));
+      for (int r = 0; r < W; ++r) TRY(rk[r].phase3b(st, K));
+    } else {
+      for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(st, K));
+    }
+  }
+  return FW_OK;
 }
 
-// Phase 3: D_IJ <- min(D_IJ, D_IK (x) D_KJ) for all I != K, J != K.
-template <typename T, int MODE>
-int launch_phase3(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int BS,
-                  int K, int *maxkey) {
-  const int tiles = (int)(n_pad / 128);
-  TileArgs a = tile_args(ld, kb, BS, K);
-  a.mr_lo[0] = a.mc_lo[0] = kb;
-  a.mr_hi[0] = a.mc_hi[0] = kb + BS;
-  return launch_tile<T, 128, 128, MODE>(dim3(tiles, tiles, 1), st, D, P, a, maxkey);
-}
 
-// Look-ahead split of phase 3 (BS = 128). P3a: the tiles of block-row K+1 and block-column
-// K+1 (what phases 1-2 of round K+1 read), so round K+1 can start on the side stream while
-// P3b — every other tile — finishes round K on the main stream.
-template <typename T, int MODE>
-int launch_phase3a(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int K,
-                   int *maxkey) {
-  const int tiles = (int)(n_pad / 128), BS = 128, kn = kb + BS;
-  TileArgs a = tile_args(ld, kb, BS, K);
-  // z = 0: block-row K+1 across all columns except the column strip of round K
-  a.row0[0] = kn; a.col0[0] = 0; a.mc_lo[0] = kb; a.mc_hi[0] = kb + BS;
-  // z = 1: block-column K+1 down all rows except the row strip of K and block-row K+1
-  a.row0[1] = 0; a.col0[1] = kn; a.mr_lo[1] = kb; a.mr_hi[1] = kn + BS; a.xrow[1] = 1;
-  return launch_tile<T, 128, 128, MODE>(dim3(tiles, 1, 2), st, D, P, a, maxkey);
-}
+// ---- the solve ---------------------------------------------------------------------------
+enum Transport { T_LOCAL = 0, T_NCCL = 1, T_LOOPBACK = 2 };
+
+// One rank's part of a solve: the caller's rows and where they are solved.
+template <typename T>
+struct Part {
+  T *src;            // caller's rows [row0, row0 + nsrc) of the n x n matrix, pitch ld_src
+  int64_t ld_src;
+  int32_t *next;     // same rows of P, pitch ld_next, or nullptr
+  int64_t ld_next;
+  int rank;
+  int64_t row0, nrows, nsrc;
+  T *D = nullptr;    // padded working rows (nrows x n_pad, pitch ld)
+  int32_t *P = nullptr;
+  int64_t ld = 0;
+  bool inplace = false;
+  T *strip[2] = {nullptr, nullptr};
+  T *backup = nullptr;
+};
 
 template <typename T, int MODE>
-int launch_phase3b(cudaStream_t st, T *D, int32_t *P, int64_t ld, int64_t n_pad, int kb, int K,
-                   int *maxkey) {
-  const int tiles = (int)(n_pad / 128), BS = 128;
-  TileArgs a = tile_args(ld, kb, BS, K);
-  a.mr_lo[0] = a.mc_lo[0] = kb;            // strips of round K and block-row/column K+1
-  a.mr_hi[0] = a.mc_hi[0] = kb + 2 * BS;
-  return launch_tile<T, 128, 128, MODE>(dim3(tiles, tiles, 1), st, D, P, a, maxkey);
+int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS,
+               int R, int *maxkey, cudaStream_t st, const Events &ev, bool la) {
+  const int64_t n_pad = (n + 127) / 128 * 128;
+  std::vector<Rounds<T, MODE>> rk;
+  for (auto &p : parts)
+    rk.push_back(Rounds<T, MODE>{c, world, p.D, p.P, p.ld, n, n_pad, p.row0, p.nrows, BS, R, maxkey,
+                                 {p.strip[0], p.strip[1]}});
+  if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
+  return rk[0].run(st, ev, la);
+}
+
+template <typename T, int MODE>
+int run_init(cudaStream_t st, const T *src, int64_t ld_src, int64_t nsrc, int64_t n, int64_t row0,
+             T *D, int32_t *P, int64_t ld, int64_t nrows, int64_t n_pad) {
+  if (nrows == 0) return FW_OK;
+  dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)nrows);
+  init_kernel<T, MODE><<<g, 256, 0, st>>>(src, ld_src, nsrc, n, row0, D, P, ld, n_pad);
+  CU(cudaGetLastError());
+  return FW_OK;
 }
 
 template <typename T>
 constexpr bool is_int_v() { return std::is_integral<T>::value; }
 
-struct RoundTimes {
-  bool on;
-  cudaEvent_t *ev;  // 3 per round: after phase 1, after phase 2, after phase 3
-};
-
-// Streams for the look-ahead: phases 1-2 of round K+1 run on `side` while the bulk of
-// phase 3 of round K runs on the caller's stream (readings R12).
-struct Streams {
-  cudaStream_t main, side;
-  cudaEvent_t *sync;   // 2 per round
-};
-
-template <typename T, int MODE>
-int run_rounds(Streams s, T *D, int32_t *P, int64_t ld, int64_t n_pad, int BS, int R, int *maxkey,
-               RoundTimes rt, bool lookahead) {
-  cudaStream_t st = s.main;
-  if (!lookahead || BS != 128 || R < 2) {
-    for (int K = 0; K < R; ++K) {
-      const int kb = K * BS;
-      TRY((launch_phase1<T, MODE>(st, D, P, ld, kb, BS, K, maxkey)));
-      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K], st));
-      TRY((launch_phase2<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
-      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 1], st));
-      TRY((launch_phase3<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
-      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 2], st));
-    }
-    return FW_OK;
-  }
-  // round 0 pivot phases on the main stream
-  TRY((launch_phase1<T, MODE>(st, D, P, ld, 0, BS, 0, maxkey)));
-  if (rt.on) CU(cudaEventRecord(rt.ev[0], st));
-  TRY((launch_phase2<T, MODE>(st, D, P, ld, n_pad, 0, BS, 0, maxkey)));
-  if (rt.on) CU(cudaEventRecord(rt.ev[1], st));
-  for (int K = 0; K < R; ++K) {
-    const int kb = K * BS;
-    if (K + 1 < R) {
-      TRY((launch_phase3a<T, MODE>(st, D, P, ld, n_pad, kb, K, maxkey)));
-      CU(cudaEventRecord(s.sync[2 * K], st));
-      // side: phases 1-2 of round K+1 (they only touch block-row/column K+1)
-      CU(cudaStreamWaitEvent(s.side, s.sync[2 * K], 0));
-      TRY((launch_phase1<T, MODE>(s.side, D, P, ld, kb + BS, BS, K + 1, maxkey)));
-      if (rt.on) CU(cudaEventRecord(rt.ev[3 * (K + 1)], s.side));
-      TRY((launch_phase2<T, MODE>(s.side, D, P, ld, n_pad, kb + BS, BS, K + 1, maxkey)));
-      if (rt.on) CU(cudaEventRecord(rt.ev[3 * (K + 1) + 1], s.side));
-      CU(cudaEventRecord(s.sync[2 * K + 1], s.side));
-      TRY((launch_phase3b<T, MODE>(st, D, P, ld, n_pad, kb, K, maxkey)));
-      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 2], st));
-      CU(cudaStreamWaitEvent(st, s.sync[2 * K + 1], 0));
-    } else {
-      TRY((launch_phase3<T, MODE>(st, D, P, ld, n_pad, kb, BS, K, maxkey)));
-      if (rt.on) CU(cudaEventRecord(rt.ev[3 * K + 2], st));
-    }
-  }
-  return FW_OK;
-}
-
-template <typename T, int MODE>
-int run_init(cudaStream_t st, const T *src, int64_t ld_src, int64_t n, T *D, int32_t *P, int64_t ld,
-             int64_t n_pad) {
-  dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)n_pad);
-  init_kernel<T, MODE><<<g, 256, 0, st>>>(src, ld_src, n, D, P, ld, n_pad);
-  CU(cudaGetLastError());
-  return FW_OK;
-}
-
+// Solve over `parts` (one part = one rank's rows): T_LOCAL (one GPU, all rows), T_NCCL (this
+// process's rank of an NCCL communicator), T_LOOPBACK (every rank emulated here).
 template <typename T>
-int dispatch_init(int mode, cudaStream_t st, const T *src, int64_t ld_src, int64_t n, T *D,
-                  int32_t *P, int64_t ld, int64_t n_pad) {
-  switch (mode) {
-    case MODE_PLAIN: return run_init<T, MODE_PLAIN>(st, src, ld_src, n, D, P, ld, n_pad);
-    case MODE_TAG: return run_init<T, MODE_TAG>(st, src, ld_src, n, D, P, ld, n_pad);
-    default: return run_init<T, MODE_KEY>(st, src, ld_src, n, D, P, ld, n_pad);
-  }
-}
-
-template <typename T>
-int dispatch_rounds(int mode, Streams s, T *D, int32_t *P, int64_t ld, int64_t n_pad, int BS, int R,
-                    int *maxkey, RoundTimes rt, bool lookahead) {
-  switch (mode) {
-    case MODE_PLAIN: return run_rounds<T, MODE_PLAIN>(s, D, P, ld, n_pad, BS, R, maxkey, rt, lookahead);
-    case MODE_TAG: return run_rounds<T, MODE_TAG>(s, D, P, ld, n_pad, BS, R, maxkey, rt, lookahead);
-    default: return run_rounds<T, MODE_KEY>(s, D, P, ld, n_pad, BS, R, maxkey, rt, lookahead);
-  }
-}
-
-// ---- the solve on device buffers ----------------------------------------------------
-// src: n rows of ld_src elements (in/out); next: n rows of ld_next int32 or nullptr.
-template <typename T>
-int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next, int64_t n,
-                 int BS, cudaStream_t st) {
+int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS,
+                cudaStream_t st) {
   const bool int_t = is_int_v<T>();
   const int64_t n_pad = (n + 127) / 128 * 128;
-  const bool want_p = next != nullptr;
+  const bool want_p = parts[0].next != nullptr;
   const bool lastk = (c.flags & FW_PATH_LAST_K) != 0;
   const int path_mode = want_p ? (lastk ? 1 : 0) : -1;
-  const bool timing = (c.flags & FW_TIMING) != 0;
+  const bool timing = (c.flags & FW_TIMING) != 0 && tr != T_LOOPBACK;
+  const bool nccl = tr == T_NCCL && world > 1;
 
-  // 1. validation (read-only; outputs untouched on error)
+  // 1. validation (read-only; outputs untouched on error), reduced over all ranks
   TRY(c.scratch.ensure(64));
   int *d_flags = static_cast<int *>(c.scratch.p);   // [0] flags [1] max weight [2] max key
   CU(cudaMemsetAsync(d_flags, 0, 16, st));
-  {
-    const int64_t total = n * n;
+  for (auto &p : parts) {
+    if (p.nsrc == 0) continue;
+    const int64_t total = p.nsrc * n;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    validate_kernel<T><<<std::max(blocks, 1), 256, 0, st>>>(src, ld_src, n, d_flags, d_flags + 1);
+    validate_kernel<T><<<std::max(blocks, 1), 256, 0, st>>>(p.src, p.ld_src, p.nsrc, n, p.row0,
+                                                            d_flags, d_flags + 1);
     CU(cudaGetLastError());
   }
+  // flag bits are combined with max: the rank holding a bit holds the max value as well
+  if (nccl) NC(g_nccl.AllReduce(d_flags, d_flags, 2, ncclInt32, ncclMax, c.comm, st));
   int h_flags[4] = {0, 0, 0, 0};
   CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -378,65 +559,126 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
     return b;
   }();
 
-  // 3. placement: in place when the caller's buffer already has the padded layout
-  const bool inplace = n == n_pad && ld_src == n && ((uintptr_t)src % 16 == 0) &&
-                       (!want_p || (ld_next == n && (uintptr_t)next % 16 == 0));
-  T *D = src;
-  int32_t *Pm = next;
-  int64_t ld = n;
-  if (!inplace) {
+  // 3. placement
+  if (tr == T_LOOPBACK) {
+    // one padded n_pad x n_pad workspace: each part uses its own rows of it
     TRY(c.ws_d.ensure((size_t)n_pad * n_pad * sizeof(T)));
-    D = static_cast<T *>(c.ws_d.p);
-    if (want_p) {
-      TRY(c.ws_t.ensure((size_t)n_pad * n_pad * sizeof(int32_t)));
-      Pm = static_cast<int32_t *>(c.ws_t.p);
+    if (want_p) TRY(c.ws_t.ensure((size_t)n_pad * n_pad * sizeof(int32_t)));
+    const size_t sb = (size_t)BS * n_pad * sizeof(T);
+    TRY(c.ws_s.ensure(2 * sb * parts.size()));
+    for (size_t r = 0; r < parts.size(); ++r) {
+      Part<T> &p = parts[r];
+      p.ld = n_pad;
+      p.D = static_cast<T *>(c.ws_d.p) + p.row0 * n_pad;
+      p.P = want_p ? static_cast<int32_t *>(c.ws_t.p) + p.row0 * n_pad : nullptr;
+      p.strip[0] = reinterpret_cast<T *>(static_cast<char *>(c.ws_s.p) + 2 * r * sb);
+      p.strip[1] = reinterpret_cast<T *>(static_cast<char *>(c.ws_s.p) + (2 * r + 1) * sb);
     }
-    ld = n_pad;
-  }
-  // the speculative key run may have to be redone in TAG mode: keep W when in place
-  T *backup = nullptr;
-  if (is_key(mode) && !key_static && inplace) {
-    TRY(c.ws_b.ensure((size_t)n * n * sizeof(T)));
-    backup = static_cast<T *>(c.ws_b.p);
-    CU(cudaMemcpyAsync(backup, src, (size_t)n * n * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  } else {
+    Part<T> &p = parts[0];
+    p.inplace = p.nsrc == p.nrows && n == n_pad && p.ld_src == n && ((uintptr_t)p.src % 16 == 0) &&
+                (!want_p || (p.ld_next == n && (uintptr_t)p.next % 16 == 0));
+    p.D = p.src;
+    p.P = p.next;
+    p.ld = n;
+    if (!p.inplace) {
+      TRY(c.ws_d.ensure((size_t)std::max<int64_t>(p.nrows, 1) * n_pad * sizeof(T)));
+      p.D = static_cast<T *>(c.ws_d.p);
+      if (want_p) {
+        TRY(c.ws_t.ensure((size_t)std::max<int64_t>(p.nrows, 1) * n_pad * sizeof(int32_t)));
+        p.P = static_cast<int32_t *>(c.ws_t.p);
+      }
+      p.ld = n_pad;
+    }
+    if (!want_p) p.P = nullptr;
+    if (nccl) {
+      const size_t sb = (size_t)BS * n_pad * sizeof(T);
+      TRY(c.ws_s.ensure(2 * sb));
+      p.strip[0] = static_cast<T *>(c.ws_s.p);
+      p.strip[1] = reinterpret_cast<T *>(static_cast<char *>(c.ws_s.p) + sb);
+    }
+    // the speculative key run may have to be redone with tags: keep W when solving in place
+    if (is_key(mode) && !key_static && p.inplace && p.nsrc > 0) {
+      TRY(c.ws_b.ensure((size_t)p.nsrc * n * sizeof(T)));
+      p.backup = static_cast<T *>(c.ws_b.p);
+      CU(cudaMemcpy2DAsync(p.backup, n * sizeof(T), p.src, p.ld_src * sizeof(T), n * sizeof(T),
+                           p.nsrc, cudaMemcpyDeviceToDevice, st));
+    }
   }
 
   const int R = (int)((n + BS - 1) / BS);  // rounds wholly inside the padding are skipped
-  TRY(ensure_events(c, 4 + 3 * (size_t)R + 2 + 2 * (size_t)R));
-  Streams streams{st, c.side, c.events.data() + 4 + 3 * (size_t)R + 2};
+  TRY(ensure_events(c, 4 + 3 * (size_t)R + 2 * (size_t)R));
   cudaEvent_t e_begin = c.events[0], e_end = c.events[1], e_init = c.events[2],
               e_post = c.events[3];
-  RoundTimes rt{timing, c.events.data() + 4};
+  Events ev{timing, c.events.data() + 4, c.events.data() + 4 + 3 * (size_t)R};
   int *d_maxkey = d_flags + 2;
+  const bool la = c.lookahead && BS == 128 && R >= 2;
 
   CU(cudaEventRecord(e_begin, st));
   CU(cudaStreamWaitEvent(c.side, e_begin, 0));   // the side stream follows the caller's stream
   for (int attempt = 0; attempt < 2; ++attempt) {
     // 4. init (+ key encoding), rounds
-    const T *init_src = (attempt == 1 && backup) ? backup : src;
-    const int64_t init_ld = (attempt == 1 && backup) ? n : ld_src;
-    TRY(dispatch_init<T>(mode, st, init_src, init_ld, n, D, want_p ? Pm : nullptr, ld, n_pad));
+    for (auto &p : parts) {
+      const T *isrc = (attempt == 1 && p.backup) ? p.backup : p.src;
+      const int64_t ild = (attempt == 1 && p.backup) ? n : p.ld_src;
+      switch (mode) {
+        case MODE_PLAIN: TRY((run_init<T, MODE_PLAIN>(st, isrc, ild, p.nsrc, n, p.row0, p.D, p.P, p.ld, p.nrows, n_pad))); break;
+        case MODE_TAG: TRY((run_init<T, MODE_TAG>(st, isrc, ild, p.nsrc, n, p.row0, p.D, p.P, p.ld, p.nrows, n_pad))); break;
+        default: TRY((run_init<T, MODE_KEY>(st, isrc, ild, p.nsrc, n, p.row0, p.D, p.P, p.ld, p.nrows, n_pad)));
+      }
+    }
     CU(cudaEventRecord(e_init, st));
-    TRY(dispatch_rounds<T>(mode, streams, D, want_p ? Pm : nullptr, ld, n_pad, BS, R, d_maxkey, rt,
-                           c.lookahead));
+    switch (mode) {
+      case MODE_PLAIN: TRY((run_rounds<T, MODE_PLAIN>(c, parts, tr, world, n, BS, R, d_maxkey, st, ev, la))); break;
+      case MODE_TAG: TRY((run_rounds<T, MODE_TAG>(c, parts, tr, world, n, BS, R, d_maxkey, st, ev, la))); break;
+      default: TRY((run_rounds<T, MODE_KEY>(c, parts, tr, world, n, BS, R, d_maxkey, st, ev, la)));
+    }
     if (!is_key(mode) || key_static) break;
+    if (nccl) NC(g_nccl.AllReduce(d_maxkey, d_maxkey, 1, ncclInt32, ncclMax, c.comm, st));
     CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (h_flags[2] <= key_limit) break;
     mode = MODE_TAG;   // a stored key left the exact range: redo with round tags
-    CU(cudaMemsetAsync(d_flags + 2, 0, 4, st));
+    CU(cudaMemsetAsync(d_maxkey, 0, 4, st));
   }
 
   // 5. epilogue passes: keys -> distances; tags -> last k; last k -> next hop (R9/R10)
   if (is_key(mode)) {
-    dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
-    decode_kernel<T><<<g, 256, 0, st>>>(D, ld, n);
-    CU(cudaGetLastError());
+    for (auto &p : parts) {
+      if (p.nrows == 0) continue;
+      dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)p.nrows);
+      decode_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n);
+      CU(cudaGetLastError());
+    }
   }
   if (mode == MODE_TAG) {
-    dim3 g((unsigned)((n + 255) / 256), (unsigned)n);
-    resolve_lastk_kernel<T><<<g, 256, 0, st>>>(D, ld, Pm, n, BS);
-    CU(cudaGetLastError());
+    // the search reads rows of block K wherever they live: the full final D
+    const T *Dfull = parts[0].D - (tr == T_LOOPBACK ? parts[0].row0 * n_pad : 0);
+    if (nccl) {
+      Part<T> &p = parts[0];
+      TRY(c.ws_full.ensure((size_t)n_pad * n_pad * sizeof(T)));
+      T *full = static_cast<T *>(c.ws_full.p);
+      if (p.nrows > 0)
+        CU(cudaMemcpy2DAsync(full + p.row0 * n_pad, n_pad * sizeof(T), p.D, p.ld * sizeof(T),
+                             n_pad * sizeof(T), p.nrows, cudaMemcpyDeviceToDevice, st));
+      NC(g_nccl.GroupStart());
+      for (int r = 0; r < world; ++r) {
+        int64_t r0, nr;
+        partition(n, world, r, &r0, &nr);
+        if (nr == 0) continue;
+        T *dst = full + r0 * n_pad;
+        NC(g_nccl.Broadcast(dst, dst, (size_t)nr * n_pad, int_t ? ncclInt32 : ncclFloat32, r, c.comm, st));
+      }
+      NC(g_nccl.GroupEnd());
+      Dfull = full;
+    }
+    for (auto &p : parts) {
+      if (p.nrows == 0) continue;
+      // Dfull pitch: n_pad when gathered / shared; one GPU: the local pitch (the same matrix)
+      dim3 g((unsigned)((n + 255) / 256), (unsigned)p.nrows);
+      resolve_lastk_kernel<T><<<g, 256, 0, st>>>(p.D, Dfull, p.ld, p.row0, p.P, n, BS);
+      CU(cudaGetLastError());
+    }
   }
   if (want_p) {
     const size_t row_bytes = (size_t)n * sizeof(int32_t);
@@ -447,19 +689,23 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
                               200 * 1024));
       configured = true;
     }
-    finalize_paths_kernel<T><<<(unsigned)n, 1024, use_smem ? row_bytes : 0, st>>>(
-        D, Pm, ld, n, path_mode == 0, use_smem, d_flags);
-    CU(cudaGetLastError());
+    for (auto &p : parts) {
+      if (p.nsrc == 0) continue;
+      finalize_paths_kernel<T><<<(unsigned)p.nsrc, 1024, use_smem ? row_bytes : 0, st>>>(
+          p.D, p.P, p.ld, p.row0, n, path_mode == 0, use_smem, d_flags);
+      CU(cudaGetLastError());
+    }
   }
   CU(cudaEventRecord(e_post, st));
 
   // 6. unpad into the caller's buffers
-  if (!inplace) {
-    dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
-    unpad_kernel<T><<<g, 256, 0, st>>>(D, ld, n, src, ld_src);
+  for (auto &p : parts) {
+    if (p.inplace || p.nsrc == 0) continue;
+    dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)p.nsrc);
+    unpad_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n, p.src, p.ld_src);
     CU(cudaGetLastError());
     if (want_p) {
-      unpad_kernel<int32_t><<<g, 256, 0, st>>>(Pm, ld, n, next, ld_next);
+      unpad_kernel<int32_t><<<g, 256, 0, st>>>(p.P, p.ld, n, p.next, p.ld_next);
       CU(cudaGetLastError());
     }
   }
@@ -481,12 +727,14 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
   CU(cudaEventElapsedTime(&ms, e_begin, e_end));
   s.solve_ms = ms;
   s.phase3_launches = R;
-  // phase-3 relaxations actually issued: rows and columns outside the round's strips
+  // phase-3 relaxations of this process's rows: rows and columns outside the round's strips
   double relax = 0;
-  for (int K = 0; K < R; ++K) {
-    const double off = (double)(n_pad - BS);
-    relax += off * off * BS;
-  }
+  for (auto &p : parts)
+    for (int K = 0; K < R; ++K) {
+      const int64_t kb = (int64_t)K * BS;
+      const double rows = (double)p.nrows - ((kb >= p.row0 && kb < p.row0 + p.nrows) ? BS : 0);
+      relax += rows * (double)(n_pad - BS) * BS;
+    }
   s.phase3_relaxations = relax;
   if (timing) {
     // absolute event times (ms since e_begin); with the look-ahead, phases 1-2 of round K
@@ -496,12 +744,10 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
       cudaEventElapsedTime(&t, e_begin, e);
       return (double)t;
     };
-    const bool la = c.lookahead && BS == 128 && R >= 2;
-    const cudaEvent_t *sy = streams.sync;
     double prev_p3_end = at(e_init);
     for (int K = 0; K < R; ++K) {
-      const double p1 = at(rt.ev[3 * K]), p2 = at(rt.ev[3 * K + 1]), p3 = at(rt.ev[3 * K + 2]);
-      const double p1_start = (la && K > 0) ? at(sy[2 * (K - 1)]) : prev_p3_end;
+      const double p1 = at(ev.ev[3 * K]), p2 = at(ev.ev[3 * K + 1]), p3 = at(ev.ev[3 * K + 2]);
+      const double p1_start = (la && K > 0) ? at(ev.sync[2 * (K - 1)]) : prev_p3_end;
       s.phase1_ms += p1 - p1_start;
       s.phase2_ms += p2 - p1;
       s.phase3_ms += p3 - std::max(prev_p3_end, p2);
@@ -512,6 +758,39 @@ int solve_device(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next,
   c.stats = s;
   c.has_stats = true;
   return FW_OK;
+}
+
+// This process's rows as one part (T_LOCAL: all rows; T_NCCL: the communicator rank's rows).
+template <typename T>
+int solve_rows(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next, int64_t n, int BS,
+               cudaStream_t st) {
+  const int world = c.comm ? c.world : 1;
+  const int rank = c.comm ? c.rank : 0;
+  Part<T> p{};
+  p.src = src; p.ld_src = ld_src; p.next = next; p.ld_next = ld_next; p.rank = rank;
+  partition(n, world, rank, &p.row0, &p.nrows);
+  p.nsrc = std::max<int64_t>(0, std::min(p.nrows, n - p.row0));
+  std::vector<Part<T>> parts{p};
+  return solve_parts<T>(c, parts, world > 1 ? T_NCCL : T_LOCAL, world, n, BS, st);
+}
+
+// Every rank of a `world`-way partition emulated in this process (loopback transport).
+template <typename T>
+int solve_loopback(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next, int64_t n,
+                   int BS, int world, cudaStream_t st) {
+  std::vector<Part<T>> parts;
+  for (int r = 0; r < world; ++r) {
+    Part<T> p{};
+    p.rank = r;
+    partition(n, world, r, &p.row0, &p.nrows);
+    p.nsrc = std::max<int64_t>(0, std::min(p.nrows, n - p.row0));
+    p.src = src + std::min(p.row0, n) * ld_src;
+    p.ld_src = ld_src;
+    p.next = next ? next + std::min(p.row0, n) * ld_next : nullptr;
+    p.ld_next = ld_next;
+    parts.push_back(p);
+  }
+  return solve_parts<T>(c, parts, T_LOOPBACK, world, n, BS, st);
 }
 
 int pick_block(int64_t n, int block, int *BS) {
@@ -552,15 +831,16 @@ int ensure_pinned(Ctx &c, size_t bytes) {
 }
 
 // Host <-> device copies: direct when the host buffer is pinned, otherwise through two
-// pinned staging chunks (copy engine overlaps the host memcpy of the next chunk).
+// pinned staging chunks (the copy engine overlaps the host memcpy of the next chunk).
 int copy_h2d(Ctx &c, void *dst, const void *src, size_t bytes, cudaStream_t st) {
   if (is_pinned(src)) {
     CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
     return FW_OK;
   }
   TRY(ensure_pinned(c, 2 * kStageBytes));
-  TRY(ensure_events(c, 4));
-  cudaEvent_t done[2] = {c.events[2], c.events[3]};
+  cudaEvent_t done[2];
+  CU(cudaEventCreate(&done[0]));
+  CU(cudaEventCreate(&done[1]));
   bool used[2] = {false, false};
   size_t off = 0;
   for (int b = 0; off < bytes; b ^= 1) {
@@ -573,6 +853,9 @@ int copy_h2d(Ctx &c, void *dst, const void *src, size_t bytes, cudaStream_t st) 
     used[b] = true;
     off += len;
   }
+  CU(cudaStreamSynchronize(st));
+  cudaEventDestroy(done[0]);
+  cudaEventDestroy(done[1]);
   return FW_OK;
 }
 
@@ -599,9 +882,11 @@ int solve_host(T *dist, int32_t *next, int64_t n, int block, int ngpus) {
   int BS = 0;
   TRY(check_common(n, dist, block, &BS));
   if (ngpus < 0 || ngpus > 1)
-    return fail(FW_EINVAL, "the single-process entry point solves on one GPU (ngpus = 0 or 1); "
-                           "multi-GPU runs one process per GPU (paper_1811_01201_b200.dist)");
+    return fail(FW_EINVAL, "the host entry point solves on this process's GPU (ngpus = 0 or 1); "
+                           "multi-GPU runs one process per GPU (fw_comm_init + fw_dist_solve_*)");
   Ctx &c = *g_ctx;
+  if (c.comm)
+    return fail(FW_ESTATE, "a multi-GPU communicator is active: use fw_dist_solve_* or fw_comm_free");
   CU(cudaSetDevice(c.dev));
   const size_t bytes = (size_t)n * n * sizeof(T);
   TRY(c.user_d.ensure(bytes));
@@ -614,7 +899,7 @@ int solve_host(T *dist, int32_t *next, int64_t n, int block, int ngpus) {
   CU(cudaEventRecord(h0, c.stream));
   int rc = copy_h2d(c, d, dist, bytes, c.stream);
   if (rc == FW_OK) rc = (cudaEventRecord(h1, c.stream) == cudaSuccess) ? FW_OK : FW_ECUDA;
-  if (rc == FW_OK) rc = solve_device<T>(c, d, n, t, n, n, BS, c.stream);
+  if (rc == FW_OK) rc = solve_rows<T>(c, d, n, t, n, n, BS, c.stream);
   float h2d = 0;
   if (rc == FW_OK) cudaEventElapsedTime(&h2d, h0, h1);
   if (rc == FW_OK) {
@@ -636,12 +921,17 @@ int solve_host(T *dist, int32_t *next, int64_t n, int block, int ngpus) {
 }
 
 template <typename T>
-int solve_dev_entry(T *d_dist, int32_t *d_next, int64_t n, int64_t ld, int block, void *stream) {
+int solve_dev_entry(T *d_dist, int32_t *d_next, int64_t n, int64_t ld, int block, void *stream,
+                    bool dist) {
   int BS = 0;
   TRY(check_common(n, d_dist, block, &BS));
   if (ld < n) return fail(FW_EINVAL, "ld (%lld) < n (%lld)", (long long)ld, (long long)n);
   Ctx &c = *g_ctx;
-  return solve_device<T>(c, d_dist, ld, d_next, ld, n, BS, static_cast<cudaStream_t>(stream));
+  if (!dist && c.comm)
+    return fail(FW_ESTATE, "a multi-GPU communicator is active: use fw_dist_solve_* or fw_comm_free");
+  if (dist && c.comm == nullptr)
+    return fail(FW_ESTATE, "fw_dist_solve_* needs fw_comm_init first");
+  return solve_rows<T>(c, d_dist, ld, d_next, ld, n, BS, static_cast<cudaStream_t>(stream));
 }
 
 }  // namespace
@@ -682,9 +972,12 @@ int fw_free(void) {
   if (!g_ctx) return FW_OK;
   Ctx *c = g_ctx;
   cudaDeviceSynchronize();
+  if (c->comm) g_nccl.CommDestroy(c->comm);
   c->ws_d.release();
   c->ws_t.release();
   c->ws_b.release();
+  c->ws_s.release();
+  c->ws_full.release();
   c->user_d.release();
   c->user_t.release();
   c->scratch.release();
@@ -707,12 +1000,92 @@ int fw_solve_i32(int32_t *dist, int32_t *next, int64_t n, int block, int ngpus) 
 
 int fw_solve_device_f32(float *d_dist, int32_t *d_next, int64_t n, int64_t ld, int block,
                         void *stream) {
-  return solve_dev_entry<float>(d_dist, d_next, n, ld, block, stream);
+  return solve_dev_entry<float>(d_dist, d_next, n, ld, block, stream, false);
 }
 
 int fw_solve_device_i32(int32_t *d_dist, int32_t *d_next, int64_t n, int64_t ld, int block,
                         void *stream) {
-  return solve_dev_entry<int32_t>(d_dist, d_next, n, ld, block, stream);
+  return solve_dev_entry<int32_t>(d_dist, d_next, n, ld, block, stream, false);
+}
+
+int fw_dist_partition(int64_t n, int world, int rank, int64_t *row0, int64_t *nrows) {
+  if (n <= 0 || world <= 0 || rank < 0 || rank >= world || !row0 || !nrows)
+    return fail(FW_EINVAL, "bad partition arguments (n=%lld world=%d rank=%d)", (long long)n, world, rank);
+  partition(n, world, rank, row0, nrows);
+  // rows the caller holds: the real rows of the range
+  *nrows = std::max<int64_t>(0, std::min<int64_t>(*nrows, n - *row0));
+  return FW_OK;
+}
+
+int fw_dist_owner(int64_t n, int world, int64_t row) {
+  if (n <= 0 || world <= 0 || row < 0 || row >= (n + 127) / 128 * 128) return -1;
+  return owner_of(n, world, row);
+}
+
+int fw_comm_unique_id(unsigned char *out) {
+  if (!out) return fail(FW_EINVAL, "out is NULL");
+  TRY(load_nccl());
+  ncclUniqueId id;
+  NC(g_nccl.GetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return FW_OK;
+}
+
+int fw_comm_init(const unsigned char *id, int rank, int world) {
+  if (!g_ctx) return fail(FW_ESTATE, "fw_init has not been called");
+  if (!id || world <= 0 || rank < 0 || rank >= world)
+    return fail(FW_EINVAL, "bad communicator arguments (rank=%d world=%d)", rank, world);
+  if (g_ctx->comm) return fail(FW_ESTATE, "a communicator is already initialised");
+  TRY(load_nccl());
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof uid);
+  CU(cudaSetDevice(g_ctx->dev));
+  NC(g_nccl.CommInitRank(&g_ctx->comm, world, uid, rank));
+  g_ctx->rank = rank;
+  g_ctx->world = world;
+  return FW_OK;
+}
+
+int fw_comm_free(void) {
+  if (!g_ctx) return FW_OK;
+  if (g_ctx->comm) {
+    cudaDeviceSynchronize();
+    g_nccl.CommDestroy(g_ctx->comm);
+  }
+  g_ctx->comm = nullptr;
+  g_ctx->rank = 0;
+  g_ctx->world = 1;
+  return FW_OK;
+}
+
+int fw_dist_loopback_solve_device_f32(float *d_dist, int32_t *d_next, int64_t n, int64_t ld,
+                                      int block, int world, void *stream) {
+  int BS = 0;
+  TRY(check_common(n, d_dist, block, &BS));
+  if (ld < n) return fail(FW_EINVAL, "ld (%lld) < n (%lld)", (long long)ld, (long long)n);
+  if (world < 1 || world > 64) return fail(FW_EINVAL, "world must be in [1, 64] (got %d)", world);
+  return solve_loopback<float>(*g_ctx, d_dist, ld, d_next, ld, n, BS, world,
+                               static_cast<cudaStream_t>(stream));
+}
+
+int fw_dist_loopback_solve_device_i32(int32_t *d_dist, int32_t *d_next, int64_t n, int64_t ld,
+                                      int block, int world, void *stream) {
+  int BS = 0;
+  TRY(check_common(n, d_dist, block, &BS));
+  if (ld < n) return fail(FW_EINVAL, "ld (%lld) < n (%lld)", (long long)ld, (long long)n);
+  if (world < 1 || world > 64) return fail(FW_EINVAL, "world must be in [1, 64] (got %d)", world);
+  return solve_loopback<int32_t>(*g_ctx, d_dist, ld, d_next, ld, n, BS, world,
+                                 static_cast<cudaStream_t>(stream));
+}
+
+int fw_dist_solve_device_f32(float *d_rows, int32_t *d_next_rows, int64_t n, int64_t ld, int block,
+                             void *stream) {
+  return solve_dev_entry<float>(d_rows, d_next_rows, n, ld, block, stream, true);
+}
+
+int fw_dist_solve_device_i32(int32_t *d_rows, int32_t *d_next_rows, int64_t n, int64_t ld,
+                             int block, void *stream) {
+  return solve_dev_entry<int32_t>(d_rows, d_next_rows, n, ld, block, stream, true);
 }
 
 const char *fw_last_error(void) { return g_err.c_str(); }
@@ -724,6 +1097,6 @@ int fw_last_stats(fw_stats *out) {
   return FW_OK;
 }
 
-const char *fw_version(void) { return "fwb200 0.1 sm_100a"; }
+const char *fw_version(void) { return "fwb200 0.2 sm_100a"; }
 
 }  // extern "C"

@@ -143,8 +143,11 @@ struct TileShape {
 // Launch arguments of the tile kernel (passed by value).
 struct TileArgs {
   int64_t ld;
+  const void *B;                 // B(k, j) = B[k * ldb + j]: the pivot row strip (rows kb..kb+Kd)
+  int64_t ldb;
   int kb, Kd;
-  int row0[2], col0[2];          // tile grid origin (global), per blockIdx.z
+  int rows_lim, cols_lim;        // local rows / columns of D (tiles beyond them exit)
+  int row0[2], col0[2];          // tile grid origin (local row, global column), per blockIdx.z
   int mr_lo[2], mr_hi[2];        // excluded rows, per blockIdx.z
   int mc_lo[2], mc_hi[2];        // excluded columns, per blockIdx.z
   int xrow[2];                   // 1: blockIdx.x walks tile rows (column strip in a dual launch)
@@ -154,8 +157,10 @@ struct TileArgs {
 // ---------------------------------------------------------------------------------
 // Min-plus tile kernel (phases 2 and 3). Tile origin (i0, j0) = (row0 + by*TM, col0 + bx*TN);
 // blockIdx.z selects one of two strip descriptions (phase 2 launches both strips at once).
-//   D[i][j] <- min(D[i][j], min_{k<Kd} D[i][kb+k] + D[kb+k][j])
-// for the tile's (i,j), excluding rows in [mr_lo, mr_hi) and columns in [mc_lo, mc_hi)
+//   D[i][j] <- min(D[i][j], min_{k<Kd} D[i][kb+k] + B[k][j])
+// with i a LOCAL row of this GPU's block-row partition (all rows on one GPU) and B the pivot
+// row strip (rows kb..kb+Kd of the global matrix: in D on its owner, the broadcast buffer
+// elsewhere), for the tile's (i,j), excluding rows in [mr_lo, mr_hi) and columns in [mc_lo, mc_hi)
 // (strips owned by other phases). The k dimension is streamed in chunks of kBK
 // through two shared-memory stages (cp.async 16 B): A row-major [i][k] (padded), B row-major
 // [k][j]. In-place use (phase 2: the tile is its own A or B) is safe: a CTA reads all its
@@ -177,7 +182,9 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   const int xrow = z ? g.xrow[1] : g.xrow[0];
   const int bx = xrow ? 0 : blockIdx.x, by = xrow ? blockIdx.x : blockIdx.y;
   const int i0 = (z ? g.row0[1] : g.row0[0]) + by * TM, j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
-  if ((i0 >= mr_lo && i0 + TM <= mr_hi) || (j0 >= mc_lo && j0 + TN <= mc_hi)) return;
+  if ((i0 >= mr_lo && i0 + TM <= mr_hi) || (j0 >= mc_lo && j0 + TN <= mc_hi) ||
+      i0 >= g.rows_lim || j0 >= g.cols_lim)
+    return;
 
   const int64_t ld = g.ld;
   const int kb = g.kb;
@@ -200,7 +207,8 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   const int a_r = tid / (kBK / 4), a_c = (tid % (kBK / 4)) * 4;
   const int b_r = tid / (TN / 4), b_c = (tid % (TN / 4)) * 4;
   const T *a_src = D + (int64_t)(i0 + a_r) * ld + kb + a_c;
-  const T *b_src = D + (int64_t)(kb + b_r) * ld + j0 + b_c;
+  const int64_t ldb = g.ldb;
+  const T *b_src = static_cast<const T *>(g.B) + (int64_t)b_r * ldb + j0 + b_c;
 
   auto load_chunk = [&](int stage, int k0) {
     T *as = smem + stage * S::kStage;
@@ -210,7 +218,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
       cp_async16(as + (a_r + t * A_ROWS) * S::AS + a_c, a_src + k0 + (int64_t)t * A_ROWS * ld);
 #pragma unroll
     for (int t = 0; t < B_PER; ++t)
-      cp_async16(bs + (b_r + t * B_ROWS) * S::BSTR + b_c, b_src + (int64_t)(k0 + t * B_ROWS) * ld);
+      cp_async16(bs + (b_r + t * B_ROWS) * S::BSTR + b_c, b_src + (int64_t)(k0 + t * B_ROWS) * ldb);
     cp_async_commit();
   };
 
@@ -323,7 +331,8 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
 // key when S < D, so min() keeps keys exact; P[a][b] <- k (last improving k) on change.
 template <typename T, int BS, int MODE>
 __global__ void __launch_bounds__(1024)
-phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int tag, int *maxkey) {
+phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag,
+              int *maxkey) {
   constexpr int R = BS / 32;
   using VR = typename std::conditional<R == 4, typename Vec4<T>::V,
              typename std::conditional<R == 2, typename std::conditional<Num<T>::kIsInt, int2, float2>::type, T>::type>::type;
@@ -331,8 +340,8 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, in
   T *sD = reinterpret_cast<T *>(smem_raw);     // row-major copy   [a][b]
   T *sDT = sD + BS * BS;                        // transposed copy  [b][a]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  T *Dk = D + (int64_t)kb * ld + kb;
-  int32_t *Pk = P ? P + (int64_t)kb * ld + kb : nullptr;
+  T *Dk = D + (int64_t)r0 * ld + kb;                // D_KK: local row r0, global column kb
+  int32_t *Pk = P ? P + (int64_t)r0 * ld + kb : nullptr;
   T d[R][R];
   int32_t p[R][R];
 #pragma unroll
@@ -412,13 +421,14 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, in
 //        bit 2 an off-diagonal entry is INF (no edge). maxw: max finite off-diagonal weight
 //        (INT32 value, or FP32 bit pattern — non-negative floats order like their bits).
 template <typename T>
-__global__ void validate_kernel(const T *src, int64_t lds, int64_t n, int *flags, int *maxw) {
+__global__ void validate_kernel(const T *src, int64_t lds, int64_t nrows, int64_t n, int64_t row0,
+                                int *flags, int *maxw) {
   int f = 0, mx = 0;
-  const int64_t total = n * n;
+  const int64_t total = nrows * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / n, j = e - i * n;
-    if (i == j) continue;  // the diagonal is overwritten with 0 (R4)
+    if (row0 + i == j) continue;  // the diagonal is overwritten with 0 (R4)
     const T v = src[i * lds + j];
     if (Num<T>::bad(v)) { f |= 1; continue; }
     if (!Num<T>::finite(v)) { f |= 4; continue; }
@@ -437,13 +447,14 @@ __global__ void validate_kernel(const T *src, int64_t lds, int64_t n, int *flags
 // diagonal 0 (R4, R11); key mode stores D*128 + (j&127). P (tags / last k) initialised to -1
 // ("no intermediate yet"). src may alias D (in-place solve).
 template <typename T, int MODE>
-__global__ void init_kernel(const T *src, int64_t lds, int64_t n, T *D, int32_t *P, int64_t ld,
-                            int64_t n_pad) {
-  const int64_t i = blockIdx.y;
+__global__ void init_kernel(const T *src, int64_t lds, int64_t nsrc, int64_t n, int64_t row0, T *D,
+                            int32_t *P, int64_t ld, int64_t n_pad) {
+  const int64_t i = blockIdx.y;          // local row; global row row0 + i
+  const int64_t gi = row0 + i;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_pad;
        j += (int64_t)gridDim.x * blockDim.x) {
-    T v = (i < n && j < n) ? src[i * lds + j] : Num<T>::inf();
-    if (i == j) v = 0;
+    T v = (i < nsrc && gi < n && j < n) ? src[i * lds + j] : Num<T>::inf();
+    if (gi == j) v = 0;
     if (MODE != MODE_PLAIN) P[i * ld + j] = -1;
     if (is_key(MODE)) v = Num<T>::encode(v, (int)j);
     D[i * ld + j] = v;
@@ -452,7 +463,7 @@ __global__ void init_kernel(const T *src, int64_t lds, int64_t n, T *D, int32_t 
 
 // Key -> distance (key modes), in place over rows [0, n) and columns [0, n).
 template <typename T>
-__global__ void decode_kernel(T *D, int64_t ld, int64_t n) {
+__global__ void decode_kernel(T *D, int64_t ld, int64_t n) {   // grid.y = rows, n = columns
   const int64_t i = blockIdx.y;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x)
@@ -476,8 +487,10 @@ __global__ void unpad_kernel(const T *D, int64_t ld, int64_t n, T *dst, int64_t 
 // monotone). k* is an intermediate vertex of a shortest i->j path, i.e. the paper's
 // "most recently added intermediate node" form of P. Overwrites tags with k*.
 template <typename T>
-__global__ void resolve_lastk_kernel(const T *D, int64_t ld, int32_t *tags, int64_t n, int BS) {
-  const int64_t i = blockIdx.y;
+__global__ void resolve_lastk_kernel(const T *D, const T *Dfull, int64_t ld, int64_t row0,
+                                     int32_t *tags, int64_t n, int BS) {
+  const int64_t i = blockIdx.y;                       // local row
+  const int64_t gi = row0 + i;
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int t = tags[i * ld + j];
@@ -489,8 +502,8 @@ __global__ void resolve_lastk_kernel(const T *D, int64_t ld, int32_t *tags, int6
   int ks = -1;
   const T *Di = D + i * ld;
   for (int64_t k = kb; k < ke; ++k) {
-    if (k == i || k == j) continue;
-    const T s = Di[k] + D[k * ld + j];
+    if (k == gi || k == j) continue;
+    const T s = Di[k] + Dfull[k * ld + j];
     if (s < best) { best = s; ks = (int)k; }
     if (s <= dij) { ks = (int)k; break; }
   }
@@ -505,12 +518,13 @@ __global__ void resolve_lastk_kernel(const T *D, int64_t ld, int32_t *tags, int6
 // sentinels (diagonal and unreachable -> -1). flags bit 3: a chain did not converge.
 template <typename T>
 __global__ void __launch_bounds__(1024)
-finalize_paths_kernel(const T *D, int32_t *P, int64_t ld, int64_t n, int next_hop, int use_smem,
-                      int *flags) {
+finalize_paths_kernel(const T *D, int32_t *P, int64_t ld, int64_t row0, int64_t n, int next_hop,
+                      int use_smem, int *flags) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t i = blockIdx.x;
-  int32_t *row = P + i * ld;
-  const T *Drow = D + i * ld;
+  const int64_t li = blockIdx.x;          // local row
+  const int64_t i = row0 + li;            // global row
+  int32_t *row = P + li * ld;
+  const T *Drow = D + li * ld;
   if (!next_hop) {
     for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
       if (j == i || !Num<T>::finite(Drow[j])) row[j] = -1;

@@ -1,0 +1,158 @@
+"""Multi-GPU host logic on CPU (no GPU): the block-row partition exported by the C ABI
+(fw_dist_partition / fw_dist_owner) and the per-round schedule of the partitioned solve —
+owner(K) runs phase 1 and its row strip, broadcasts the pivot row strip, every rank updates
+its own rows (column strip, phase 3) — run as world-size 2 and 3 `gloo` process groups.
+The per-phase arithmetic here is a NumPy test double of the CUDA kernels (exact arg-min
+LAST_K semantics, reading R9); the partition and owners come from the product library.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import apsp_inputs as gen
+import oracle
+import paper_1811_01201_b200 as fw
+
+
+@pytest.mark.parametrize("n", [1, 100, 128, 129, 1000, 4096, 16384, 32768, 65536])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 7, 8])
+def test_partition_covers_rows(n, world):
+    n_pad = (n + 127) // 128 * 128
+    parts = [fw.fw_dist_partition(n, world, r) for r in range(world)]
+    pos = 0
+    padded = []
+    for r, (r0, nr) in enumerate(parts):
+        assert r0 % 128 == 0
+        if nr:
+            assert r0 == pos
+            pos += nr
+        # padded extent of the rank (row0 of the next rank, or n_pad)
+        nxt = parts[r + 1][0] if r + 1 < world else n_pad
+        padded.append(max(0, nxt - r0) if r0 < n_pad else 0)
+    assert pos == n
+    assert sum(padded) == n_pad
+    assert max(padded) - min(padded) <= 128
+    for row in range(0, n_pad, 37):
+        o = fw.fw_dist_owner(n, world, row)
+        r0 = parts[o][0]
+        assert r0 <= row < r0 + padded[o]
+    assert fw.fw_dist_owner(n, world, n_pad) == -1
+
+
+def test_partition_errors():
+    with pytest.raises(fw.FwError):
+        fw.fw_dist_partition(0, 2, 0)
+    with pytest.raises(fw.FwError):
+        fw.fw_dist_partition(100, 2, 2)
+
+
+# ---- NumPy test double of the phase kernels (LAST_K keyed semantics) ----------------------
+def _relax(C, Pc, A, B, kb, rows_mask=None, cols_mask=None):
+    """C <- min(C, min_k A[:,k] + B[k,:]) (first arg-min k), P = kb + k where strictly better."""
+    if C.size == 0:
+        return
+    S = A[:, :, None] + B[None, :, :]               # i x k x j
+    kmin = np.argmin(S, axis=1)                     # first k on ties
+    m = np.take_along_axis(S, kmin[:, None, :], axis=1)[:, 0, :]
+    better = m < C
+    if rows_mask is not None:
+        better &= rows_mask[:, None]
+    if cols_mask is not None:
+        better &= cols_mask[None, :]
+    C[better] = m[better]
+    Pc[better] = (kb + kmin)[better]
+
+
+def _phase1(D, P, r, kb, BS):
+    blk = D[r:r + BS, kb:kb + BS]
+    pb = P[r:r + BS, kb:kb + BS]
+    for k in range(BS):
+        s = blk[:, [k]] + blk[[k], :]
+        better = s < blk
+        blk[better] = s[better]
+        pb[better] = kb + k
+
+
+def _rank_main(rank, world, port, n, BS, seed, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n_pad = (n + 127) // 128 * 128
+    W = gen.generate("er_int_f32", n, seed, p=0.2, lo=1, hi=50)
+    row0, nsrc = fw.fw_dist_partition(n, world, rank)
+    nxt = fw.fw_dist_partition(n, world, rank + 1)[0] if rank + 1 < world else n_pad
+    nrows = max(0, nxt - row0) if row0 < n_pad else 0
+    # this rank's padded rows (init kernel semantics: INF padding, zero diagonal)
+    D = np.full((nrows, n_pad), np.inf, dtype=np.float32)
+    D[:nsrc, :n] = W[row0:row0 + nsrc]
+    for i in range(nrows):
+        if row0 + i < n_pad:
+            D[i, row0 + i] = 0
+    P = np.full((nrows, n_pad), -1, dtype=np.int32)
+    R = (n + BS - 1) // BS
+    for K in range(R):
+        kb = K * BS
+        owner = fw.fw_dist_owner(n, world, kb)
+        strip = torch.empty((BS, n_pad), dtype=torch.float32)
+        if owner == rank:
+            r = kb - row0
+            _phase1(D, P, r, kb, BS)
+            cols = np.ones(n_pad, dtype=bool)
+            cols[kb:kb + BS] = False                  # the diagonal block is phase 1's
+            _relax(D[r:r + BS], P[r:r + BS], D[r:r + BS, kb:kb + BS], D[r:r + BS].copy(), kb,
+                   cols_mask=cols)
+            strip = torch.from_numpy(D[r:r + BS].copy())
+        dist.broadcast(strip, src=owner)              # the only exchange of a round
+        B = strip.numpy()
+        rows = np.ones(nrows, dtype=bool)
+        if owner == rank:
+            rows[kb - row0:kb - row0 + BS] = False
+        # column strip of the local rows through D_KK* (from the broadcast strip)
+        _relax(D[:, kb:kb + BS], P[:, kb:kb + BS], D[:, kb:kb + BS].copy(), B[:, kb:kb + BS], kb,
+               rows_mask=rows)
+        # phase 3 on the local rows outside the strips
+        cols = np.ones(n_pad, dtype=bool)
+        cols[kb:kb + BS] = False
+        _relax(D, P, D[:, kb:kb + BS].copy(), B, kb, rows_mask=rows, cols_mask=cols)
+    Dt = torch.from_numpy(np.ascontiguousarray(D[:nsrc, :n]))
+    Pt = torch.from_numpy(np.ascontiguousarray(P[:nsrc, :n]))
+    gD = [None] * world
+    gP = [None] * world
+    dist.all_gather_object(gD, Dt)
+    dist.all_gather_object(gP, Pt)
+    if rank == 0:
+        out.put((np.concatenate([g.numpy() for g in gD]), np.concatenate([g.numpy() for g in gP])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world,n,BS", [(2, 300, 64), (3, 500, 128), (2, 257, 32), (4, 300, 64)])
+def test_partitioned_schedule_gloo(world, n, BS):
+    """The partitioned round schedule reproduces the oracle's D (bitwise, integer data) and a
+    valid LAST_K P, with the pivot strip as the only data crossing ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, n, BS, 7, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    D, P = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    W = gen.generate("er_int_f32", n, 7, p=0.2, lo=1, hi=50)
+    Dref, _ = oracle.fw(W, None)
+    np.testing.assert_array_equal(D, Dref)
+    P = np.where(np.isinf(D) | np.eye(n, dtype=bool), -1, P).astype(np.int32)
+    assert oracle.check_paths(W, D, P, mode="lastk")[0] == 0
