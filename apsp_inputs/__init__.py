@@ -60,7 +60,7 @@ def _real_weights(z: np.ndarray) -> np.ndarray:
 
 
 def generate(kind: str, n: int, seed: int, p: float = 1.0, lo: int = 1, hi: int = 100,
-             chunk_rows: int = 512) -> np.ndarray:
+             chunk_rows: int = 512, rows: tuple[int, int] | None = None) -> np.ndarray:
     """Adjacency matrix W (n x n, row-major, C-contiguous) for one workload kind.
 
     kind:
@@ -69,15 +69,17 @@ def generate(kind: str, n: int, seed: int, p: float = 1.0, lo: int = 1, hi: int 
       "er_int"        INT32 integers in [lo,hi] with prob p, else INF_I32   (configs[2])
       "er_int_f32"    FP32 integers in [lo,hi] with prob p, else +inf
       "er_real"       FP32 real in [1,100) with prob p, else +inf
-    The diagonal is 0 in every kind.
+    The diagonal is 0 in every kind. rows=(r0, r1) draws only rows [r0, r1) of the same
+    matrix (a multi-GPU rank's block-rows).
     """
     if n <= 0:
         raise ValueError("n must be positive")
     dtype = np.int32 if kind == "er_int" else np.float32
-    W = np.empty((n, n), dtype=dtype)
+    lo_row, hi_row = (0, n) if rows is None else (max(0, rows[0]), min(n, rows[1]))
+    W = np.empty((max(0, hi_row - lo_row), n), dtype=dtype)
     cols = np.arange(n, dtype=np.int64)
-    for r0 in range(0, n, chunk_rows):
-        rows = np.arange(r0, min(n, r0 + chunk_rows), dtype=np.int64)
+    for r0 in range(lo_row, hi_row, chunk_rows):
+        rows = np.arange(r0, min(hi_row, r0 + chunk_rows), dtype=np.int64)
         z0 = counter(seed, 0, n, rows, cols)
         if kind in ("complete_int", "er_int", "er_int_f32"):
             w = _int_weights(z0, lo, hi)
@@ -92,7 +94,7 @@ def generate(kind: str, n: int, seed: int, p: float = 1.0, lo: int = 1, hi: int 
             del z1
             inf = INF_I32 if dtype == np.int32 else np.inf
             w = np.where(present, w, inf)
-        blk = W[rows[0]:rows[-1] + 1]
+        blk = W[rows[0] - lo_row:rows[-1] + 1 - lo_row]
         blk[...] = w.astype(dtype)
         blk[np.arange(len(rows)), rows] = 0
     return W
@@ -182,6 +184,7 @@ CONFIGS = {
 }
 
 
-def config_matrix(name: str) -> np.ndarray:
+def config_matrix(name: str, rows: tuple[int, int] | None = None) -> np.ndarray:
     c = CONFIGS[name]
-    return generate(c["kind"], c["n"], c["seed"], p=c.get("p", 1.0), lo=c.get("lo", 1), hi=c.get("hi", 100))
+    return generate(c["kind"], c["n"], c["seed"], p=c.get("p", 1.0), lo=c.get("lo", 1), hi=c.get("hi", 100),
+                    rows=rows)

@@ -167,26 +167,40 @@ def run_gpu(args, cfg):
     import paper_1811_01201_b200 as fw
 
     rank, world, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
     n, BS = cfg["n"], args.block or cfg["block"]
     is_int = cfg["kind"] == "er_int"
-    W = gen.config_matrix(cfg["name"])
+    fw.fw_init(0, fw.FW_TIMING)
+    if world > 1:
+        from paper_1811_01201_b200 import dist as fwdist
+        fwdist.comm_init_from_torch()
+    # this rank's block-rows (all rows on one GPU): the partition the library uses
+    row0, nrows = fw.fw_dist_partition(n, world, rank)
+    W = gen.config_matrix(cfg["name"], rows=(row0, row0 + nrows))
     dW = torch.from_numpy(W).to(dev)                       # resident input (never modified)
     dD = torch.empty_like(dW)
-    dP = torch.empty((n, n), dtype=torch.int32, device=dev)
+    dP = torch.empty((nrows, n), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
-    solve = fw.fw_solve_device_i32 if is_int else fw.fw_solve_device_f32
-
-    fw.fw_init(0, fw.FW_TIMING)
+    if world > 1:
+        solve = fw.fw_dist_solve_device_i32 if is_int else fw.fw_dist_solve_device_f32
+    else:
+        solve = fw.fw_solve_device_i32 if is_int else fw.fw_solve_device_f32
 
     def step():
         dD.copy_(dW)                                         # fresh input, device-resident
-        solve(dD, dP, block=BS, stream=stream)
+        solve(dD, dP, n=n, ld=n, block=BS, stream=stream)
         return fw.fw_last_stats()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         step()
@@ -203,16 +217,10 @@ def run_gpu(args, cfg):
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    ms_total = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
     ms_per_step = ms_total / args.steps
     flops = 2.0 * float(n) ** 3
-    # replicas: each rank solves its own copy (the partitioned multi-GPU driver is not in
-    # this build yet) -> whole-job throughput = world x per-rank
-    gflops = world * flops * args.steps / (ms_total * 1e-3) / 1e9
+    gflops = flops * args.steps / (ms_total * 1e-3) / 1e9      # whole job (strong scaling)
 
     # roofline of the dominant kernel (phase 3): algorithmic flops per launch / avg duration
     props = torch.cuda.get_device_properties(dev)
@@ -239,7 +247,7 @@ def run_gpu(args, cfg):
             traffic = None
     roof = {"bound": "alu", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
-            "traffic": traffic, "kernel": "minplus_tile_kernel<float,128,128,32,TAGS> (phase 3)",
+            "traffic": traffic, "kernel": "minplus_tile_kernel<float,128,128,KEY> (phase 3, rank 0)",
             "avg_launch_ms": avg_launch_ms,
             "peak_basis": f"stated FP32 add+min issue roofline: {sms} SMs x 128 lanes x {max_mhz:.0f} MHz "
                           "(2 flop per relaxation, BASELINE north_star)",
@@ -247,27 +255,39 @@ def run_gpu(args, cfg):
                                   "phase2": sum(s.phase2_ms for s in stats) / len(stats),
                                   "phase3": p3_ms / len(stats),
                                   "post": sum(s.post_ms for s in stats) / len(stats)}}
-    launches_per_step = 2 + 4 * stats[-1].rounds + (2 if True else 0)
+    launches = sum(s.kernel_launches for s in stats)
 
-    # e2e: the same metric through the public host entry point with pinned host buffers
+    # e2e: the same metric through the public API with pinned host buffers, H2D + solve + D2H
     e2e = None
     if not args.no_e2e:
         host_in = torch.from_numpy(W).pin_memory()
         hD = torch.empty_like(host_in).pin_memory()
-        hP = torch.empty((n, n), dtype=torch.int32).pin_memory()
-        f_host = fw.fw_solve_i32 if is_int else fw.fw_solve
+        hP = torch.empty((nrows, n), dtype=torch.int32).pin_memory()
         ts = []
         for it in range(max(1, args.e2e_steps) + 1):
             hD.copy_(host_in)
             torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
             t0 = time.perf_counter()
-            f_host(hD, hP, block=BS)
-            dt = time.perf_counter() - t0
-            if it > 0:       # first call warms the host-side staging
+            if world == 1:
+                (fw.fw_solve_i32 if is_int else fw.fw_solve)(hD, hP, block=BS)
+            else:
+                dD.copy_(hD, non_blocking=True)
+                solve(dD, dP, n=n, ld=n, block=BS, stream=stream)
+                hD.copy_(dD, non_blocking=True)
+                hP.copy_(dP, non_blocking=True)
+                torch.cuda.synchronize()
+            dt = max_over_ranks(time.perf_counter() - t0)
+            if it > 0:       # the first call warms the host-side staging
                 ts.append(dt)
-        e2e = {"value": flops / statistics.median(ts) / 1e9 * world, "unit": "GFLOPS",
+        e2e = {"value": flops / statistics.median(ts) / 1e9, "unit": "GFLOPS",
                "h2d_bytes_per_step": int(n * n * 4), "d2h_bytes_per_step": int(2 * n * n * 4),
-               "ms_per_step": statistics.median(ts) * 1e3}
+               "ms_per_step": statistics.median(ts) * 1e3,
+               "path": "fw_solve (host buffers)" if world == 1 else
+                       "pinned rows H2D + fw_dist_solve_device + D2H, per rank"}
+    if world > 1:
+        fw.fw_comm_free()
     fw.fw_free()
 
     cpu = None
@@ -278,16 +298,17 @@ def run_gpu(args, cfg):
         line = {
             "metric": METRIC, "value": gflops, "unit": "GFLOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if world == 1 else "weak", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "i32" if is_int else "f32", "data": "synthetic",
             "config": {"workload": CONFIG_DESC[cfg["name"]], "config": cfg["name"], "n": n,
                        "block": BS, "seed": cfg["seed"], "path": "next-hop",
                        "l2": "inputs larger than L2 (D and P 1 GiB each at n=16384)",
-                       "parallelism": "single GPU" if world == 1 else f"{world} replicas"},
+                       "parallelism": "single GPU" if world == 1 else
+                       f"{world}-way block-row partition, per-round NCCL pivot-strip broadcast"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches,
             "clocks": clk.summary(),
             "context": "paper: 338 GFLOPS on a 68-core Xeon Phi 7250 (KNL), PAPER.md P:202 (not a target)",
         }

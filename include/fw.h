@@ -82,6 +82,7 @@ typedef struct fw_stats {
   double d2h_ms;
   int64_t phase3_launches;
   double phase3_relaxations; /* relaxations issued by phase-3 launches (algorithmic) */
+  int64_t kernel_launches; /* kernels this library launched for the solve (incl. validation) */
 } fw_stats;
 
 /* Create the process-wide context. ngpus_max: 0 = all visible devices (this build

@@ -140,6 +140,7 @@ struct Ctx {
 };
 
 Ctx *g_ctx = nullptr;
+int64_t g_launches = 0;   // kernels this library launched (fw_stats.kernel_launches)
 
 constexpr size_t kStageBytes = 64ull << 20;  // pinned staging chunk
 // Largest initial/stored distance for which key sums stay exact (kernels header, KEY mode):
@@ -193,6 +194,7 @@ int launch_tile(dim3 grid, cudaStream_t st, T *D, int32_t *P, const TileArgs &a,
     configured = true;
   }
   kern<<<grid, kThreads, bytes, st>>>(D, P, a, maxkey);
+  ++g_launches;
   CU(cudaGetLastError());
   return FW_OK;
 }
@@ -234,6 +236,7 @@ int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int 
     configured = true;
   }
   kern<<<1, 1024, bytes, st>>>(D, P, ld, r0, kb, K, maxkey);
+  ++g_launches;
   CU(cudaGetLastError());
   return FW_OK;
 }
@@ -486,6 +489,7 @@ int run_init(cudaStream_t st, const T *src, int64_t ld_src, int64_t nsrc, int64_
   if (nrows == 0) return FW_OK;
   dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)nrows);
   init_kernel<T, MODE><<<g, 256, 0, st>>>(src, ld_src, nsrc, n, row0, D, P, ld, n_pad);
+  ++g_launches;
   CU(cudaGetLastError());
   return FW_OK;
 }
@@ -516,6 +520,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     validate_kernel<T><<<std::max(blocks, 1), 256, 0, st>>>(p.src, p.ld_src, p.nsrc, n, p.row0,
                                                             d_flags, d_flags + 1);
+    ++g_launches;
     CU(cudaGetLastError());
   }
   // flag bits are combined with max: the rank holding a bit holds the max value as well
@@ -614,6 +619,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   int *d_maxkey = d_flags + 2;
   const bool la = c.lookahead && BS == 128 && R >= 2;
 
+  const int64_t launches0 = g_launches - (int64_t)parts.size();   // + the validation launches
   CU(cudaEventRecord(e_begin, st));
   CU(cudaStreamWaitEvent(c.side, e_begin, 0));   // the side stream follows the caller's stream
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -648,6 +654,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
       if (p.nrows == 0) continue;
       dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)p.nrows);
       decode_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n);
+      ++g_launches;
       CU(cudaGetLastError());
     }
   }
@@ -677,6 +684,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
       // Dfull pitch: n_pad when gathered / shared; one GPU: the local pitch (the same matrix)
       dim3 g((unsigned)((n + 255) / 256), (unsigned)p.nrows);
       resolve_lastk_kernel<T><<<g, 256, 0, st>>>(p.D, Dfull, p.ld, p.row0, p.P, n, BS);
+      ++g_launches;
       CU(cudaGetLastError());
     }
   }
@@ -693,6 +701,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
       if (p.nsrc == 0) continue;
       finalize_paths_kernel<T><<<(unsigned)p.nsrc, 1024, use_smem ? row_bytes : 0, st>>>(
           p.D, p.P, p.ld, p.row0, n, path_mode == 0, use_smem, d_flags);
+      ++g_launches;
       CU(cudaGetLastError());
     }
   }
@@ -703,9 +712,11 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     if (p.inplace || p.nsrc == 0) continue;
     dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)p.nsrc);
     unpad_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n, p.src, p.ld_src);
+    ++g_launches;
     CU(cudaGetLastError());
     if (want_p) {
       unpad_kernel<int32_t><<<g, 256, 0, st>>>(p.P, p.ld, n, p.next, p.ld_next);
+      ++g_launches;
       CU(cudaGetLastError());
     }
   }
@@ -727,6 +738,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   CU(cudaEventElapsedTime(&ms, e_begin, e_end));
   s.solve_ms = ms;
   s.phase3_launches = R;
+  s.kernel_launches = g_launches - launches0;
   // phase-3 relaxations of this process's rows: rows and columns outside the round's strips
   double relax = 0;
   for (auto &p : parts)

@@ -252,3 +252,11 @@ def test_fw_steps_equals_full_loop():
     oracle.fw_steps(D2, P2, 40, n)
     np.testing.assert_array_equal(D, D2)
     np.testing.assert_array_equal(P, P2)
+
+
+def test_generator_row_ranges():
+    """A rank's rows drawn alone equal the same rows of the full matrix."""
+    full = gen.generate("er_int", 700, 5, p=0.1, lo=1, hi=1000)
+    part = gen.generate("er_int", 700, 5, p=0.1, lo=1, hi=1000, rows=(256, 512), chunk_rows=100)
+    np.testing.assert_array_equal(part, full[256:512])
+    assert gen.generate("complete_real", 300, 1, rows=(384, 512)).shape == (0, 300)
