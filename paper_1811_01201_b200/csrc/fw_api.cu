@@ -128,6 +128,7 @@ struct Ctx {
   DevBuf ws_b;                     // backup of W for a speculative key run (in place)
   DevBuf ws_s;                     // two pivot-strip receive buffers (multi-GPU)
   DevBuf ws_full;                  // gathered final D (multi-GPU, round tags only)
+  DevBuf ws_tr;                    // transposed final D (round tags only)
   DevBuf user_d, user_t;           // device copies of host buffers (host entry points)
   DevBuf scratch;                  // flags / reductions
   void *pinned = nullptr;          // staging for pageable host buffers
@@ -659,8 +660,10 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     }
   }
   if (mode == MODE_TAG) {
-    // the search reads rows of block K wherever they live: the full final D
+    // the search reads column segments D[kb..kb+BS)[j] of rows wherever they live: gather the
+    // final D (multi-GPU), then transpose it so each segment is one contiguous 4*BS-byte read
     const T *Dfull = parts[0].D - (tr == T_LOOPBACK ? parts[0].row0 * n_pad : 0);
+    int64_t ldf = parts[0].ld;
     if (nccl) {
       Part<T> &p = parts[0];
       TRY(c.ws_full.ensure((size_t)n_pad * n_pad * sizeof(T)));
@@ -678,14 +681,37 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
       }
       NC(g_nccl.GroupEnd());
       Dfull = full;
+      ldf = n_pad;
     }
-    for (auto &p : parts) {
-      if (p.nrows == 0) continue;
-      // Dfull pitch: n_pad when gathered / shared; one GPU: the local pitch (the same matrix)
-      dim3 g((unsigned)((n + 255) / 256), (unsigned)p.nrows);
-      resolve_lastk_kernel<T><<<g, 256, 0, st>>>(p.D, Dfull, p.ld, p.row0, p.P, n, BS);
-      ++g_launches;
+    TRY(c.ws_tr.ensure((size_t)n_pad * n_pad * sizeof(T)));
+    T *Dt = static_cast<T *>(c.ws_tr.p);
+    {
+      dim3 g((unsigned)(n_pad / 32), (unsigned)(n_pad / 32));
+      transpose_kernel<T><<<g, dim3(32, 8), 0, st>>>(Dfull, ldf, n_pad, n_pad, Dt, n_pad);
       CU(cudaGetLastError());
+      ++g_launches;
+    }
+    const size_t rb = (size_t)n_pad * sizeof(T);
+    const int use_smem = rb <= 200 * 1024;
+    auto launch = [&](auto kern) -> int {
+      static bool configured = false;
+      if (!configured) {
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+      }
+      for (auto &p : parts) {
+        if (p.nsrc == 0) continue;
+        kern<<<(unsigned)p.nsrc, 512, use_smem ? rb : 0, st>>>(p.D, Dt, p.ld, n_pad, p.row0, n,
+                                                              n_pad, p.P, use_smem);
+        CU(cudaGetLastError());
+        ++g_launches;
+      }
+      return FW_OK;
+    };
+    switch (BS) {
+      case 32: TRY(launch(resolve_lastk_kernel<T, 1>)); break;
+      case 64: TRY(launch(resolve_lastk_kernel<T, 2>)); break;
+      default: TRY(launch(resolve_lastk_kernel<T, 4>));
     }
   }
   if (want_p) {
@@ -990,6 +1016,7 @@ int fw_free(void) {
   c->ws_b.release();
   c->ws_s.release();
   c->ws_full.release();
+  c->ws_tr.release();
   c->user_d.release();
   c->user_t.release();
   c->scratch.release();

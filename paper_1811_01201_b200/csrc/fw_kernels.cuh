@@ -486,28 +486,97 @@ __global__ void unpad_kernel(const T *D, int64_t ld, int64_t n, T *dst, int64_t 
 // round K gave D[i][j], and later rounds only lowered D[i][k], D[k][j] (rounding is
 // monotone). k* is an intermediate vertex of a shortest i->j path, i.e. the paper's
 // "most recently added intermediate node" form of P. Overwrites tags with k*.
+//
+// One CTA per row i (row i of D staged in shared memory when it fits); one warp per element:
+// lane l tests k = kb + CH*l .. + CH-1 with one vector load of the transposed column segment
+// Dt[j][kb..kb+BS) (512 B coalesced per warp at BS = 128) and a ballot picks the first k.
+// U elements per warp iteration keep U independent segment loads in flight.
+
+// Dt = D^T for a rows x cols matrix (pitch ld -> pitch ldt), 32x32 shared-memory tiles.
 template <typename T>
-__global__ void resolve_lastk_kernel(const T *D, const T *Dfull, int64_t ld, int64_t row0,
-                                     int32_t *tags, int64_t n, int BS) {
-  const int64_t i = blockIdx.y;                       // local row
-  const int64_t gi = row0 + i;
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const int t = tags[i * ld + j];
-  if (t < 0) return;
-  const int64_t kb = (int64_t)t * BS;
-  const int64_t ke = kb + BS < n ? kb + BS : n;
-  const T dij = D[i * ld + j];
-  T best = Num<T>::inf();
-  int ks = -1;
-  const T *Di = D + i * ld;
-  for (int64_t k = kb; k < ke; ++k) {
-    if (k == gi || k == j) continue;
-    const T s = Di[k] + Dfull[k * ld + j];
-    if (s < best) { best = s; ks = (int)k; }
-    if (s <= dij) { ks = (int)k; break; }
+__global__ void transpose_kernel(const T *D, int64_t ld, int64_t rows, int64_t cols, T *Dt,
+                                 int64_t ldt) {
+  __shared__ T tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[y][threadIdx.x] = D[r * ld + c];
   }
-  tags[i * ld + j] = ks;
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + y, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) Dt[c * ldt + r] = tile[threadIdx.x][y];
+  }
+}
+
+template <typename T, int CH>
+__global__ void __launch_bounds__(512)
+resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t row0, int64_t n,
+                     int64_t n_pad, int32_t *tags, int use_smem) {
+  constexpr int U = 4;                     // elements in flight per warp
+  constexpr int BS = 32 * CH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *srow = reinterpret_cast<T *>(smem_raw);
+  const int64_t li = blockIdx.x, gi = row0 + li;
+  const T *Drow = D + li * ld;
+  int32_t *trow = tags + li * ld;
+  if (use_smem) {
+    for (int64_t j = threadIdx.x; j < n_pad; j += blockDim.x) srow[j] = Drow[j];
+    __syncthreads();
+  }
+  const T *A = use_smem ? srow : Drow;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t j0 = (int64_t)warp * U; j0 < n; j0 += (int64_t)nw * U) {
+    int tg[U];
+    T dij[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + u;
+      tg[u] = j < n ? trow[j] : -1;
+      dij[u] = j < n ? Drow[j] : (T)0;
+    }
+    T a[U][CH], b[U][CH];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (tg[u] < 0) continue;
+      const int64_t k0 = (int64_t)tg[u] * BS + CH * lane;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        a[u][c] = A[k0 + c];
+        b[u][c] = Dt[(j0 + u) * ldt + k0 + c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (tg[u] < 0) continue;           // warp-uniform
+      const int64_t j = j0 + u;
+      const int64_t k0 = (int64_t)tg[u] * BS + CH * lane;
+      int first = -1;
+      T best = Num<T>::inf();
+      int bestk = -1;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int64_t k = k0 + c;
+        const bool valid = k < n && k != gi && k != j;
+        const T sum = a[u][c] + b[u][c];
+        if (valid && sum <= dij[u] && first < 0) first = (int)k;
+        if (valid && sum < best) { best = sum; bestk = (int)k; }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, first >= 0);
+      int ks;
+      if (m) {
+        ks = __shfl_sync(0xffffffffu, first, __ffs(m) - 1);
+      } else {   // rounding left no candidate <= D[i][j]: take the arg-min (first on ties)
+        for (int off = 16; off > 0; off >>= 1) {
+          const T ob = __shfl_down_sync(0xffffffffu, best, off);
+          const int ok = __shfl_down_sync(0xffffffffu, bestk, off);
+          if (ob < best || (ob == best && ok >= 0 && (bestk < 0 || ok < bestk))) { best = ob; bestk = ok; }
+        }
+        ks = __shfl_sync(0xffffffffu, bestk, 0);
+      }
+      if (lane == 0) trow[j] = ks;
+    }
+  }
 }
 
 // TAG-mode post-pass, step 2 (NEXT-HOP mode, readings R1/R10): per row i, next[i][j] = j if
