@@ -40,17 +40,18 @@ def next_consistency(W: np.ndarray, D: np.ndarray, nxt: np.ndarray, exact: bool,
     i != j, h = next[i][j] is an edge of W and W[i][h] + D[h][j] == D[i][j] (exact for
     integer data, rel rtol for reals); next[i][i] == i; unreachable -> -1. Returns #bad."""
     n = W.shape[0]
-    Wf = W.astype(np.float64)
-    Df = D.astype(np.float64)
-    if W.dtype == np.int32:
-        Wf[W >= INF] = np.inf
-        Df[D >= INF] = np.inf
+
+    def f64(a):   # gathered values only: the full matrices may be 4 GiB (C5)
+        out = a.astype(np.float64)
+        if W.dtype == np.int32:
+            out[a >= INF] = np.inf
+        return out
     rows = np.arange(n) if rows is None else np.asarray(rows)
     bad = 0
     for s in range(0, len(rows), chunk):
         r = rows[s:s + chunk]
         h = nxt[r]
-        d = Df[r]
+        d = f64(D[r])
         reach = np.isfinite(d)
         diag = (r[:, None] == np.arange(n)[None, :])
         bad += int(np.sum(diag & (h != r[:, None])))
@@ -60,8 +61,8 @@ def next_consistency(W: np.ndarray, D: np.ndarray, nxt: np.ndarray, exact: bool,
         ok_range = (hh >= 0) & (hh < n)
         bad += int(np.sum(m & ~ok_range))
         hh = np.clip(hh, 0, n - 1)
-        w = Wf[r[:, None], hh]
-        dh = Df[hh, np.arange(n)[None, :]]
+        w = f64(W[r[:, None], hh])
+        dh = f64(D[hh, np.arange(n)[None, :]])
         lhs = w + dh
         if exact:
             good = lhs == d

@@ -296,6 +296,20 @@ def test_config_C4_16384():
     assert next_consistency(W, D, P, exact=True) == 0
 
 
+@pytest.mark.slow
+def test_config_C5_32768():
+    """configs[4]: n=32768 complete, real FP32 [1,100) (4 GiB D + 4 GiB P) on one GPU —
+    the 1-GPU denominator of the multi-GPU speedup. Dijkstra from the 64 seeded sources
+    within rel 1e-5 (exact double sums), the paths from those sources reconstructed through
+    next within rel 1e-5, and the O(n) next-hop check on 256 sampled rows."""
+    c = gen.CONFIGS["C5"]
+    W = gen.config_matrix("C5")
+    D, P = solve(W, 128)
+    _dijkstra_rows_check(W, D, P, c["seed"], False)
+    rows = np.sort(gen.sources(W.shape[0], c["seed"] + 100, 256))
+    assert next_consistency(W, D, P, exact=False, rows=rows, chunk=64) == 0
+
+
 # ---- P method selection (reading R9): exact keyed arg-min vs round tags ---------------
 def _solve_stats(W, block, flags=0):
     D = W.copy()
