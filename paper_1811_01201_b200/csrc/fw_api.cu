@@ -694,11 +694,9 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     const size_t rb = (size_t)n_pad * sizeof(T);
     const int use_smem = rb <= 200 * 1024;
     auto launch = [&](auto kern) -> int {
-      static bool configured = false;
-      if (!configured) {
-        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
-      }
+      // every call: the three CH instantiations share this lambda's parameter type (one
+      // function-pointer type), so a "configured once" flag here would cover only one of them
+      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       for (auto &p : parts) {
         if (p.nsrc == 0) continue;
         kern<<<(unsigned)p.nsrc, 512, use_smem ? rb : 0, st>>>(p.D, Dt, p.ld, n_pad, p.row0, n,

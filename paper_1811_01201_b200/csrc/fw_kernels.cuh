@@ -490,7 +490,9 @@ __global__ void unpad_kernel(const T *D, int64_t ld, int64_t n, T *dst, int64_t 
 // One CTA per row i (row i of D staged in shared memory when it fits); one warp per element:
 // lane l tests k = kb + CH*l .. + CH-1 with one vector load of the transposed column segment
 // Dt[j][kb..kb+BS) (512 B coalesced per warp at BS = 128) and a ballot picks the first k.
-// U elements per warp iteration keep U independent segment loads in flight.
+// U = 8 elements per warp iteration keep 8 independent 512-B segment loads in flight and the
+// next group's tags / D[i][j] are loaded before the current group is searched: the kernel
+// reads ~4*BS bytes per tagged element (HBM-bound: ~n^2 * 512 B at BS = 128).
 
 // Dt = D^T for a rows x cols matrix (pitch ld -> pitch ldt), 32x32 shared-memory tiles.
 template <typename T>
@@ -509,12 +511,26 @@ __global__ void transpose_kernel(const T *D, int64_t ld, int64_t rows, int64_t c
   }
 }
 
+// Vector of CH consecutive T (CH = 1, 2, 4) for one 4*CH-byte load.
+template <typename T, int CH> struct VecN;
+template <typename T> struct VecN<T, 1> { using V = T; };
+template <> struct VecN<float, 2> { using V = float2; };
+template <> struct VecN<int32_t, 2> { using V = int2; };
+template <> struct VecN<float, 4> { using V = float4; };
+template <> struct VecN<int32_t, 4> { using V = int4; };
+template <typename V> __device__ __forceinline__ auto velem(const V &v, int c) { return vget(v, c); }
+__device__ __forceinline__ float velem(const float &v, int) { return v; }
+__device__ __forceinline__ int32_t velem(const int32_t &v, int) { return v; }
+__device__ __forceinline__ float velem(const float2 &v, int c) { return c ? v.y : v.x; }
+__device__ __forceinline__ int32_t velem(const int2 &v, int c) { return c ? v.y : v.x; }
+
 template <typename T, int CH>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, 1)
 resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t row0, int64_t n,
                      int64_t n_pad, int32_t *tags, int use_smem) {
-  constexpr int U = 4;                     // elements in flight per warp
+  constexpr int U = 8;                     // elements in flight per warp (8 x 4*BS bytes)
   constexpr int BS = 32 * CH;
+  using V = typename VecN<T, CH>::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *srow = reinterpret_cast<T *>(smem_raw);
   const int64_t li = blockIdx.x, gi = row0 + li;
@@ -526,41 +542,49 @@ resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t r
   }
   const T *A = use_smem ? srow : Drow;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int64_t j0 = (int64_t)warp * U; j0 < n; j0 += (int64_t)nw * U) {
-    int tg[U];
-    T dij[U];
+  const int64_t step = (int64_t)nw * U;
+  // group metadata (tags, D[i][j]) is loaded one group ahead of the segment loads
+  int tg[U];
+  T dij[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + u;
-      tg[u] = j < n ? trow[j] : -1;
-      dij[u] = j < n ? Drow[j] : (T)0;
-    }
-    T a[U][CH], b[U][CH];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (tg[u] < 0) continue;
-      const int64_t k0 = (int64_t)tg[u] * BS + CH * lane;
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        a[u][c] = A[k0 + c];
-        b[u][c] = Dt[(j0 + u) * ldt + k0 + c];
-      }
-    }
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = (int64_t)warp * U + u;
+    tg[u] = j < n ? trow[j] : -1;
+    dij[u] = j < n ? Drow[j] : (T)0;
+  }
+  for (int64_t j0 = (int64_t)warp * U; j0 < n; j0 += step) {
+    V b[U];                                // the global segment loads, all in flight
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (tg[u] < 0) continue;           // warp-uniform
+      b[u] = *reinterpret_cast<const V *>(Dt + (j0 + u) * ldt + (int64_t)tg[u] * BS + CH * lane);
+    }
+    int tgn[U];
+    T dijn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + step + u;
+      tgn[u] = j < n ? trow[j] : -1;
+      dijn[u] = j < n ? Drow[j] : (T)0;
+    }
+    int res = -1;                          // lane u keeps the result of element u
+    bool wr = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (tg[u] < 0) continue;             // warp-uniform
       const int64_t j = j0 + u;
       const int64_t k0 = (int64_t)tg[u] * BS + CH * lane;
+      const V a = *reinterpret_cast<const V *>(A + k0);   // row i: shared memory (or L1)
       int first = -1;
       T best = Num<T>::inf();
       int bestk = -1;
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
+      for (int c = CH - 1; c >= 0; --c) {  // descending: the last assignment is the first k
         const int64_t k = k0 + c;
         const bool valid = k < n && k != gi && k != j;
-        const T sum = a[u][c] + b[u][c];
-        if (valid && sum <= dij[u] && first < 0) first = (int)k;
-        if (valid && sum < best) { best = sum; bestk = (int)k; }
+        const T sum = (T)velem(a, c) + (T)velem(b[u], c);
+        if (valid && sum <= dij[u]) first = (int)k;
+        if (valid && sum <= best) { best = sum; bestk = (int)k; }
       }
       const unsigned m = __ballot_sync(0xffffffffu, first >= 0);
       int ks;
@@ -574,8 +598,11 @@ resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t r
         }
         ks = __shfl_sync(0xffffffffu, bestk, 0);
       }
-      if (lane == 0) trow[j] = ks;
+      if (lane == u) { res = ks; wr = true; }
     }
+    if (wr) trow[j0 + lane] = res;
+#pragma unroll
+    for (int u = 0; u < U; ++u) { tg[u] = tgn[u]; dij[u] = dijn[u]; }
   }
 }
 
