@@ -100,6 +100,60 @@ def generate(kind: str, n: int, seed: int, p: float = 1.0, lo: int = 1, hi: int 
     return W
 
 
+def _s64(c: int) -> int:
+    """uint64 constant as the int64 with the same bits (torch has no full uint64 arithmetic)."""
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+def generate_torch(kind: str, n: int, seed: int, device="cpu", p: float = 1.0, lo: int = 1,
+                   hi: int = 100, rows: tuple[int, int] | None = None, chunk_rows: int = 1024):
+    """The same matrix as generate(), drawn with torch int64 ops (wrapping multiply, logical
+    shifts emulated by masking) so large inputs can be created directly in device memory
+    (bench.py at n >= 32768). Bit-identical to generate() (tests/test_oracle.py pins it)."""
+    import torch
+    if n <= 0:
+        raise ValueError("n must be positive")
+    is_int = kind == "er_int"
+    dtype = torch.int32 if is_int else torch.float32
+    lo_row, hi_row = (0, n) if rows is None else (max(0, rows[0]), min(n, rows[1]))
+    W = torch.empty((max(0, hi_row - lo_row), n), dtype=dtype, device=device)
+    G, M1, M2, H = (_s64(int(c)) for c in (_G, _M1, _M2, _H))
+
+    def shr(x, s):                       # logical right shift of the 64-bit pattern
+        return (x >> s) & ((1 << (64 - s)) - 1)
+
+    def fin(x):
+        x = x + G
+        x = (x ^ shr(x, 30)) * M1
+        x = (x ^ shr(x, 27)) * M2
+        return x ^ shr(x, 31)
+
+    def z_of(stream, r):
+        base = _s64((seed * int(_G)) % (1 << 64) ^ (stream * int(_H)) % (1 << 64))
+        idx = r[:, None] * n + torch.arange(n, dtype=torch.int64, device=device)[None, :]
+        return fin(base ^ idx)
+
+    for r0 in range(lo_row, hi_row, chunk_rows):
+        r = torch.arange(r0, min(hi_row, r0 + chunk_rows), dtype=torch.int64, device=device)
+        z0 = z_of(0, r)
+        if kind in ("complete_int", "er_int", "er_int_f32"):
+            w = lo + ((shr(z0, 32) * (hi - lo + 1)) >> 32)
+        elif kind in ("complete_real", "er_real"):
+            w = (1.0 + 99.0 * (shr(z0, 40).to(torch.float64) * (2.0 ** -24))).to(torch.float32)
+        else:
+            raise ValueError(f"unknown kind {kind!r}")
+        del z0
+        if kind.startswith("er_"):
+            z1 = z_of(1, r)
+            present = shr(z1, 11).to(torch.float64) * (2.0 ** -53) < p
+            del z1
+            w = torch.where(present, w, INF_I32 if is_int else float("inf"))
+        blk = W[r0 - lo_row:r0 - lo_row + len(r)]
+        blk.copy_(w.to(dtype))
+        blk[torch.arange(len(r), device=device), r] = 0
+    return W
+
+
 def sources(n: int, seed: int, count: int = 64) -> np.ndarray:
     """`count` distinct seeded source vertices (sorted), SURVEY.md C-16."""
     count = min(count, n)

@@ -101,16 +101,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_sample(cfg: dict, seconds_target: float = 15.0):
+def host_matrix(cfg: dict) -> np.ndarray:
+    """The whole n x n input on the host (apsp_inputs.generate)."""
+    return gen.generate(cfg["kind"], cfg["n"], cfg["seed"], p=cfg.get("p", 1.0),
+                        lo=cfg.get("lo", 1), hi=cfg.get("hi", 100))
+
+
+def cpu_sample(cfg: dict, seconds_target: float = 15.0, W: np.ndarray | None = None):
     """Time the oracle (as it stands) on the host cores on a bounded sample of the same
     workload: the first k-iterations of the triple loop on the full n x n matrix (each
     k-iteration is n^2 relaxations = 2 n^2 flop), scaled to GFLOPS."""
     import oracle
     n = cfg["n"]
-    W = gen.config_matrix(cfg["name"]) if cfg["kind"] != "er_int" else None
-    if W is None:   # INT32 config: the timing sample uses the FP32 loop on the same values
-        Wi = gen.config_matrix(cfg["name"])
-        W = np.where(Wi >= gen.INF_I32, np.inf, Wi).astype(np.float32)
+    W = host_matrix(cfg) if W is None else W.copy()
+    if W.dtype == np.int32:   # INT32 config: the timing sample uses the FP32 loop on the same values
+        W = np.where(W >= gen.INF_I32, np.inf, W).astype(np.float32)
     np.fill_diagonal(W, 0)
     i = np.arange(n)
     P = np.where(np.isinf(W), -1, i[None, :]).astype(np.int32)
@@ -131,31 +136,46 @@ def cpu_sample(cfg: dict, seconds_target: float = 15.0):
                       f"GFLOPS = 2*n^2*k_steps/t"}
 
 
-def config_for(name: str) -> dict:
+def config_for(name: str, n: int = 0) -> dict:
     c = dict(gen.CONFIGS[name])
     c["name"] = name
+    c["desc"] = CONFIG_DESC[name]
+    if n and n != c["n"]:   # the config's recipe at another size (e.g. the paper's N=65536)
+        c["desc"] = c["desc"].replace(f"n={c['n']}", f"n={n}")
+        c["n"] = n
     return c
+
+
+def config_json(cfg: dict, block: int, world: int) -> dict:
+    """The JSON `config` object (identical on both arms)."""
+    n = cfg["n"]
+    return {"workload": cfg["desc"], "config": cfg["name"], "n": n, "block": block,
+            "seed": cfg["seed"], "path": "next-hop",
+            "l2": (f"inputs larger than L2 (D and P {n * n * 4 / 2**30:g} GiB each)" if n * n * 4 > 126e6
+                   else f"inputs fit in L2 ({n * n * 4 / 2**20:g} MiB), not flushed between steps"),
+            "parallelism": "single GPU" if world == 1 else
+            f"{world}-way block-row partition, per-round NCCL pivot-strip broadcast"}
 
 
 def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    base = cpu_sample(cfg, seconds_target=max(2.0, 20.0 / max(1, args.steps + args.warmup)))
+    W = host_matrix(cfg)
+    base = cpu_sample(cfg, seconds_target=max(2.0, 20.0 / max(1, args.steps + args.warmup)), W=W)
     # each step is one bounded sample; report the median over steps
     vals = []
     for _ in range(args.warmup):
-        cpu_sample(cfg, seconds_target=3.0)
+        cpu_sample(cfg, seconds_target=3.0, W=W)
     for _ in range(args.steps):
-        vals.append(cpu_sample(cfg, seconds_target=max(2.0, 30.0 / max(1, args.steps)))["value"])
+        vals.append(cpu_sample(cfg, seconds_target=max(2.0, 30.0 / max(1, args.steps)), W=W)["value"])
     v = statistics.median(vals) if vals else base["value"]
     n = cfg["n"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOPS", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2.0 * n ** 3 / (v * 1e9) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": CONFIG_DESC[cfg["name"]], "n": n,
-                                        "block": cfg["block"], "seed": cfg["seed"]},
+        "data": "synthetic", "config": config_json(cfg, args.block or cfg["block"], args.gpus),
         "cpu_baseline": {**base, "value": v},
         "e2e": {"value": v, "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -180,8 +200,10 @@ def run_gpu(args, cfg):
         fwdist.comm_init_from_torch()
     # this rank's block-rows (all rows on one GPU): the partition the library uses
     row0, nrows = fw.fw_dist_partition(n, world, rank)
-    W = gen.config_matrix(cfg["name"], rows=(row0, row0 + nrows))
-    dW = torch.from_numpy(W).to(dev)                       # resident input (never modified)
+    dW = gen.generate_torch(cfg["kind"], n, cfg["seed"], device=dev, p=cfg.get("p", 1.0),
+                            lo=cfg.get("lo", 1), hi=cfg.get("hi", 100),
+                            rows=(row0, row0 + nrows))  # resident input (never modified)
+    torch.cuda.synchronize()
     dD = torch.empty_like(dW)
     dP = torch.empty((nrows, n), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
@@ -259,6 +281,7 @@ def run_gpu(args, cfg):
 
     # e2e: the same metric through the public API with pinned host buffers, H2D + solve + D2H
     e2e = None
+    W = dW.cpu().numpy() if (not args.no_e2e or (rank == 0 and world == 1 and not args.no_cpu)) else None
     if not args.no_e2e:
         host_in = torch.from_numpy(W).pin_memory()
         hD = torch.empty_like(host_in).pin_memory()
@@ -292,7 +315,7 @@ def run_gpu(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_sample(cfg)
+        cpu = cpu_sample(cfg, W=W)
 
     if rank == 0:
         line = {
@@ -300,11 +323,7 @@ def run_gpu(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
             "dtype": "i32" if is_int else "f32", "data": "synthetic",
-            "config": {"workload": CONFIG_DESC[cfg["name"]], "config": cfg["name"], "n": n,
-                       "block": BS, "seed": cfg["seed"], "path": "next-hop",
-                       "l2": "inputs larger than L2 (D and P 1 GiB each at n=16384)",
-                       "parallelism": "single GPU" if world == 1 else
-                       f"{world}-way block-row partition, per-round NCCL pivot-strip broadcast"},
+            "config": config_json(cfg, BS, world),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -325,11 +344,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4", choices=sorted(gen.CONFIGS))
     ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--n", type=int, default=0, help="the config's recipe at another n (f3: 65536)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    cfg = config_for(args.config)
+    cfg = config_for(args.config, args.n)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
