@@ -262,9 +262,11 @@ def run_gpu(args, cfg):
     avg_launch_ms = p3_ms / max(1, p3_launches)
     achieved_tflops = 2.0 * p3_relax / (p3_ms * 1e-3) / 1e12 if p3_ms > 0 else None
     traffic = None
-    if os.path.exists(PROFILE_TRAFFIC):
+    if os.path.exists(PROFILE_TRAFFIC):   # ncu capture of this config's phase-3 launch, if any
         try:
-            traffic = json.load(open(PROFILE_TRAFFIC)).get("bytes_per_launch")
+            t = json.load(open(PROFILE_TRAFFIC))
+            if t.get("n") == n and t.get("block") == BS and t.get("config") == cfg["name"]:
+                traffic = t.get("bytes_per_launch")
         except Exception:
             traffic = None
     roof = {"bound": "alu", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",

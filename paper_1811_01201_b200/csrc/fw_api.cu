@@ -488,8 +488,8 @@ template <typename T, int MODE>
 int run_init(cudaStream_t st, const T *src, int64_t ld_src, int64_t nsrc, int64_t n, int64_t row0,
              T *D, int32_t *P, int64_t ld, int64_t nrows, int64_t n_pad) {
   if (nrows == 0) return FW_OK;
-  dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)nrows);
-  init_kernel<T, MODE><<<g, 256, 0, st>>>(src, ld_src, nsrc, n, row0, D, P, ld, n_pad);
+  dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)std::min<int64_t>(nrows, 65535));
+  init_kernel<T, MODE><<<g, 256, 0, st>>>(src, ld_src, nsrc, n, row0, D, P, ld, n_pad, nrows);
   ++g_launches;
   CU(cudaGetLastError());
   return FW_OK;
@@ -653,8 +653,8 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   if (is_key(mode)) {
     for (auto &p : parts) {
       if (p.nrows == 0) continue;
-      dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)p.nrows);
-      decode_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n);
+      dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(p.nrows, 65535));
+      decode_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n, p.nrows);
       ++g_launches;
       CU(cudaGetLastError());
     }
@@ -734,12 +734,12 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   // 6. unpad into the caller's buffers
   for (auto &p : parts) {
     if (p.inplace || p.nsrc == 0) continue;
-    dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)p.nsrc);
-    unpad_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n, p.src, p.ld_src);
+    dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(p.nsrc, 65535));
+    unpad_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n, p.src, p.ld_src, p.nsrc);
     ++g_launches;
     CU(cudaGetLastError());
     if (want_p) {
-      unpad_kernel<int32_t><<<g, 256, 0, st>>>(p.P, p.ld, n, p.next, p.ld_next);
+      unpad_kernel<int32_t><<<g, 256, 0, st>>>(p.P, p.ld, n, p.next, p.ld_next, p.nsrc);
       ++g_launches;
       CU(cudaGetLastError());
     }

@@ -446,37 +446,39 @@ __global__ void validate_kernel(const T *src, int64_t lds, int64_t nrows, int64_
 // Copy W (n x n, lds) into the padded n_pad x n_pad working matrix (ld): padded entries INF,
 // diagonal 0 (R4, R11); key mode stores D*128 + (j&127). P (tags / last k) initialised to -1
 // ("no intermediate yet"). src may alias D (in-place solve).
+// Row loops stride by gridDim.y (grid.y is capped at 65535 rows per launch).
 template <typename T, int MODE>
 __global__ void init_kernel(const T *src, int64_t lds, int64_t nsrc, int64_t n, int64_t row0, T *D,
-                            int32_t *P, int64_t ld, int64_t n_pad) {
-  const int64_t i = blockIdx.y;          // local row; global row row0 + i
-  const int64_t gi = row0 + i;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_pad;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    T v = (i < nsrc && gi < n && j < n) ? src[i * lds + j] : Num<T>::inf();
-    if (gi == j) v = 0;
-    if (MODE != MODE_PLAIN) P[i * ld + j] = -1;
-    if (is_key(MODE)) v = Num<T>::encode(v, (int)j);
-    D[i * ld + j] = v;
+                            int32_t *P, int64_t ld, int64_t n_pad, int64_t nrows) {
+  for (int64_t i = blockIdx.y; i < nrows; i += gridDim.y) {   // local row; global row0 + i
+    const int64_t gi = row0 + i;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_pad;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      T v = (i < nsrc && gi < n && j < n) ? src[i * lds + j] : Num<T>::inf();
+      if (gi == j) v = 0;
+      if (MODE != MODE_PLAIN) P[i * ld + j] = -1;
+      if (is_key(MODE)) v = Num<T>::encode(v, (int)j);
+      D[i * ld + j] = v;
+    }
   }
 }
 
-// Key -> distance (key modes), in place over rows [0, n) and columns [0, n).
+// Key -> distance (key modes), in place over `rows` rows and columns [0, n).
 template <typename T>
-__global__ void decode_kernel(T *D, int64_t ld, int64_t n) {   // grid.y = rows, n = columns
-  const int64_t i = blockIdx.y;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    D[i * ld + j] = Num<T>::decode(D[i * ld + j]);
+__global__ void decode_kernel(T *D, int64_t ld, int64_t n, int64_t rows) {
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+      D[i * ld + j] = Num<T>::decode(D[i * ld + j]);
 }
 
-// Copy the n x n result out of the padded workspace (unpad).
+// Copy the `rows` x n result out of the padded workspace (unpad).
 template <typename T>
-__global__ void unpad_kernel(const T *D, int64_t ld, int64_t n, T *dst, int64_t ldd) {
-  const int64_t i = blockIdx.y;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    dst[i * ldd + j] = D[i * ld + j];
+__global__ void unpad_kernel(const T *D, int64_t ld, int64_t n, T *dst, int64_t ldd, int64_t rows) {
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+      dst[i * ldd + j] = D[i * ld + j];
 }
 
 // ---------------------------------------------------------------------------------

@@ -310,6 +310,29 @@ def test_config_C5_32768():
     assert next_consistency(W, D, P, exact=False, rows=rows, chunk=64) == 0
 
 
+@pytest.mark.slow
+def test_paper_largest_n65536():
+    """the paper's largest workload N=65536 (16 GiB D + 16 GiB P) with the
+    configs[3] recipe (complete, FP32 integers [1,100]) on one GPU, device entry point:
+    Dijkstra from 8 seeded sources bitwise, next-hop check on 64 sampled rows."""
+    n, seed = 65536, 4
+    dW = gen.generate_torch("complete_int", n, seed, device="cuda")
+    W = dW.cpu().numpy()
+    dP = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    with Ctx(fw.FW_TIMING):
+        fw.fw_solve_device_f32(dW, dP, block=128, stream=torch.cuda.current_stream())
+        s = fw.fw_last_stats()
+    assert s.n_pad == n and s.rounds == n // 128 and s.p_method == 2
+    D = dW.cpu().numpy()
+    del dW
+    P = dP.cpu().numpy()
+    del dP
+    src = gen.sources(n, seed, 8)
+    np.testing.assert_array_equal(D[src].astype(np.float64), oracle.dijkstra(W, src))
+    rows = np.sort(gen.sources(n, seed + 100, 64))
+    assert next_consistency(W, D, P, exact=True, rows=rows, chunk=16) == 0
+
+
 # ---- P method selection (reading R9): exact keyed arg-min vs round tags ---------------
 def _solve_stats(W, block, flags=0):
     D = W.copy()
