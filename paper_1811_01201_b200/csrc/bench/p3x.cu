@@ -99,6 +99,13 @@ p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
       }
       __syncthreads();
     }
+    if ((VAR & 256) && ch == nch - 1) {   // stage the epilogue's old-D lines into L1 (~1/4 tile ahead)
+#pragma unroll
+      for (int r = 0; r < RM; ++r)
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(D + (int64_t)(i0 + ty + TY * r) * ld + j0 + 4 * tx + 4 * TX * h));
+    }
     const float *as = sm + ((VAR & 32) ? 0 : (ch % NS)) * ST + ty * AS;
     const float *bs = sm + ((VAR & 32) ? 0 : (ch % NS)) * ST + SA + tx * 4;
 #pragma unroll
@@ -440,18 +447,12 @@ int main() {
     CK(cudaMemcpy(Sp, sp.data(), n * n * 4, cudaMemcpyHostToDevice));
   }
   run<8, 2, 16, 16, 2, 32, 2, 3>("prod", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 3>("prod-3st", D, P, mk, n, sms, clk);
   run<8, 2, 16, 16, 2, 32, 2, 8>("prod-noepi", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 8>("prod-3st-noepi", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 2, 64 + 3>("fadd", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 64 + 3>("fadd-3st", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 2, 64 + 8>("fadd-noepi", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 2, 128 + 3>("mixed", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 128 + 3>("mixed-3st", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 2, 128 + 8>("mixed-noepi", D, P, mk, n, sms, clk);
-  run<8, 1, 16, 16, 3, 32, 3, 3>("8x4-3cta-3st", D, P, mk, n, sms, clk);
-  run<8, 1, 16, 16, 3, 32, 3, 64 + 3>("8x4-3cta-3st-fadd", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 16, 4, 3>("prod-bk16-4st", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 3>("prod-3st-again", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 2, 256 + 3>("prod-L1pf", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 2, 256 + 1>("prod-L1pf-noL2pf", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 256 + 3>("prod-3st-L1pf", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 16, 4, 256 + 3>("prod-bk16-4st-L1pf", D, P, mk, n, sms, clk);
+  run<8, 1, 16, 16, 3, 32, 2, 256 + 3>("8x4-3cta-L1pf", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 2, 3>("prod-again", D, P, mk, n, sms, clk);
   return 0;
 }

@@ -261,6 +261,7 @@ struct Rounds {
   int BS, R;
   int *maxkey;
   T *strip[2];   // receive buffers of the pivot row strip (world > 1)
+  int *done;     // R look-ahead tile counters (zeroed per solve)
 
   bool owns(int K) const {
     const int64_t kb = (int64_t)K * BS;
@@ -330,34 +331,26 @@ struct Rounds {
     return phase3(st, K, own ? lrow(K) : 0, own ? lrow(K) + BS : 0, kb, kb + BS);
   }
 
-  // Look-ahead split (BS = 128): P3a = the tiles round K+1's pivot phases read (block-row
-  // K+1 if local; block-column K+1 of the local rows), P3b = every other tile.
-  int phase3a(cudaStream_t st, int K) {
-    const int kb = K * BS, kn = kb + BS;
-    TileArgs a = tile_args(ld, bstrip(K), ld, kb, BS, K, nrows, n_pad);
-    const bool own_k = owns(K), own_n = owns(K + 1);
-    int ex_lo = own_k ? lrow(K) : 0, ex_hi = own_k ? lrow(K) + BS : 0;   // rows of strip K
-    const int rn = own_n ? lrow(K + 1) : 0;
-    if (own_n) {   // also exclude block-row K+1 (done by z = 0); adjacent to strip K if local
-      if (own_k) ex_hi = rn + BS;
-      else { ex_lo = rn; ex_hi = rn + BS; }
-    }
-    const Strip col{0, kn, ex_lo, ex_hi, 0, 0, 1};
-    const int tiles_c = (int)(n_pad / 128), tiles_r = (int)(nrows / 128);
-    if (own_n) {
-      put(a, 0, Strip{rn, 0, 0, 0, kb, kb + BS, 0});   // block-row K+1, all columns but strip K
-      put(a, 1, col);
-      return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 1, 2), st, D, P, a,
-                                            maxkey);
-    }
-    put(a, 0, col);
-    return launch_tile<T, 128, 128, MODE>(dim3(tiles_r, 1, 1), st, D, P, a, maxkey);
-  }
-  int phase3b(cudaStream_t st, int K) {
-    int lo = 0, hi = 0;   // local rows of blocks K and K+1 (contiguous when both are local)
-    if (owns(K)) { lo = lrow(K); hi = lrow(K) + BS; }
-    if (owns(K + 1)) { if (hi == 0) lo = lrow(K + 1); hi = lrow(K + 1) + BS; }
-    return phase3(st, K, lo, hi, K * BS, K * BS + 2 * BS);
+  // Look-ahead (BS = 128): one ordered phase-3 launch per round whose first nprio CTAs are
+  // the tiles round K+1's pivot phases read (block-row K+1 if local, block-column K+1 of the
+  // local rows); they count themselves into done[K] and the pivot stream waits on that count
+  // (wait_count_kernel) instead of a kernel boundary.
+  int phase3_ordered(cudaStream_t st, int K, int *done, int *nprio_out) {
+    TileArgs a = tile_args(ld, bstrip(K), ld, K * BS, BS, K, nrows, n_pad);
+    a.order = 1;
+    a.tiles_r = (int)(nrows / 128);
+    a.tiles_c = (int)(n_pad / 128);
+    a.rowK = owns(K) ? lrow(K) / 128 : -1;
+    a.rowN = owns(K + 1) ? lrow(K + 1) / 128 : -1;
+    a.colK = K;
+    a.colN = K + 1;
+    const int nA1 = a.rowN >= 0 ? a.tiles_c - 1 : 0;
+    const int rows_b = a.tiles_r - (a.rowK >= 0) - (a.rowN >= 0);
+    a.nprio = nA1 + rows_b;
+    a.done = done;
+    *nprio_out = a.nprio;
+    const int64_t total = (int64_t)nA1 + rows_b + (int64_t)rows_b * (a.tiles_c - 2);
+    return launch_tile<T, 128, 128, MODE>(dim3((unsigned)total, 1, 1), st, D, P, a, maxkey);
   }
 
   int run(cudaStream_t st, const Events &e, bool lookahead) {
@@ -378,18 +371,23 @@ struct Rounds {
     if (e.timing) CU(cudaEventRecord(ev[0], st));
     TRY(pivot_rest(st, 0));
     if (e.timing) CU(cudaEventRecord(ev[1], st));
+    CU(cudaEventRecord(e.sync[0], st));
+    CU(cudaStreamWaitEvent(side, e.sync[0], 0));      // the pivot stream follows round 0's pivot
     for (int K = 0; K < R; ++K) {
       if (K + 1 < R) {
-        TRY(phase3a(st, K));
-        CU(cudaEventRecord(e.sync[2 * K], st));
-        CU(cudaStreamWaitEvent(side, e.sync[2 * K], 0));
+        int nprio = 0;
+        TRY(phase3_ordered(st, K, done + K, &nprio));
+        if (e.timing) CU(cudaEventRecord(ev[3 * K + 2], st));
+        // pivot stream: wait for the look-ahead tiles of round K, then round K+1's pivot
+        wait_count_kernel<<<1, 1, 0, side>>>(done + K, nprio);
+        ++g_launches;
+        CU(cudaGetLastError());
+        if (e.timing) CU(cudaEventRecord(e.sync[2 * K + 2], side));
         TRY(phase1(side, K + 1));
         if (e.timing) CU(cudaEventRecord(ev[3 * (K + 1)], side));
         TRY(pivot_rest(side, K + 1));
         if (e.timing) CU(cudaEventRecord(ev[3 * (K + 1) + 1], side));
         CU(cudaEventRecord(e.sync[2 * K + 1], side));
-        TRY(phase3b(st, K));
-        if (e.timing) CU(cudaEventRecord(ev[3 * K + 2], st));
         CU(cudaStreamWaitEvent(st, e.sync[2 * K + 1], 0));
       } else {
         TRY(phase3_full(st, K));
@@ -441,9 +439,9 @@ int run_loopback(std::vector<Rounds<T, MODE>> &rk, cudaStream_t st, bool lookahe
   TRY(pivot(0));
   for (int K = 0; K < R; ++K) {
     if (K + 1 < R) {
-      for (int r = 0; r < W; ++r) TRY(rk[r].phase3a(st, K));
+      int nprio = 0;
+      for (int r = 0; r < W; ++r) TRY(rk[r].phase3_ordered(st, K, rk[r].done + K, &nprio));
       TRY(pivot(K + 1));
-      for (int r = 0; r < W; ++r) TRY(rk[r].phase3b(st, K));
     } else {
       for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(st, K));
     }
@@ -474,12 +472,12 @@ struct Part {
 
 template <typename T, int MODE>
 int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS,
-               int R, int *maxkey, cudaStream_t st, const Events &ev, bool la) {
+               int R, int *maxkey, int *done, cudaStream_t st, const Events &ev, bool la) {
   const int64_t n_pad = (n + 127) / 128 * 128;
   std::vector<Rounds<T, MODE>> rk;
   for (auto &p : parts)
     rk.push_back(Rounds<T, MODE>{c, world, p.D, p.P, p.ld, n, n_pad, p.row0, p.nrows, BS, R, maxkey,
-                                 {p.strip[0], p.strip[1]}});
+                                 {p.strip[0], p.strip[1]}, done});
   if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
   return rk[0].run(st, ev, la);
 }
@@ -512,8 +510,10 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   const bool nccl = tr == T_NCCL && world > 1;
 
   // 1. validation (read-only; outputs untouched on error), reduced over all ranks
-  TRY(c.scratch.ensure(64));
+  const int R = (int)((n + BS - 1) / BS);  // rounds wholly inside the padding are skipped
+  TRY(c.scratch.ensure(64 + 4 * (size_t)R));
   int *d_flags = static_cast<int *>(c.scratch.p);   // [0] flags [1] max weight [2] max key
+  int *d_done = d_flags + 16;                        // R look-ahead tile counters
   CU(cudaMemsetAsync(d_flags, 0, 16, st));
   for (auto &p : parts) {
     if (p.nsrc == 0) continue;
@@ -612,7 +612,6 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     }
   }
 
-  const int R = (int)((n + BS - 1) / BS);  // rounds wholly inside the padding are skipped
   TRY(ensure_events(c, 4 + 3 * (size_t)R + 2 * (size_t)R));
   cudaEvent_t e_begin = c.events[0], e_end = c.events[1], e_init = c.events[2],
               e_post = c.events[3];
@@ -634,11 +633,12 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
         default: TRY((run_init<T, MODE_KEY>(st, isrc, ild, p.nsrc, n, p.row0, p.D, p.P, p.ld, p.nrows, n_pad)));
       }
     }
+    CU(cudaMemsetAsync(d_done, 0, 4 * (size_t)R, st));
     CU(cudaEventRecord(e_init, st));
     switch (mode) {
-      case MODE_PLAIN: TRY((run_rounds<T, MODE_PLAIN>(c, parts, tr, world, n, BS, R, d_maxkey, st, ev, la))); break;
-      case MODE_TAG: TRY((run_rounds<T, MODE_TAG>(c, parts, tr, world, n, BS, R, d_maxkey, st, ev, la))); break;
-      default: TRY((run_rounds<T, MODE_KEY>(c, parts, tr, world, n, BS, R, d_maxkey, st, ev, la)));
+      case MODE_PLAIN: TRY((run_rounds<T, MODE_PLAIN>(c, parts, tr, world, n, BS, R, d_maxkey, d_done, st, ev, la))); break;
+      case MODE_TAG: TRY((run_rounds<T, MODE_TAG>(c, parts, tr, world, n, BS, R, d_maxkey, d_done, st, ev, la))); break;
+      default: TRY((run_rounds<T, MODE_KEY>(c, parts, tr, world, n, BS, R, d_maxkey, d_done, st, ev, la)));
     }
     if (!is_key(mode) || key_static) break;
     if (nccl) NC(g_nccl.AllReduce(d_maxkey, d_maxkey, 1, ncclInt32, ncclMax, c.comm, st));
@@ -783,7 +783,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     double prev_p3_end = at(e_init);
     for (int K = 0; K < R; ++K) {
       const double p1 = at(ev.ev[3 * K]), p2 = at(ev.ev[3 * K + 1]), p3 = at(ev.ev[3 * K + 2]);
-      const double p1_start = (la && K > 0) ? at(ev.sync[2 * (K - 1)]) : prev_p3_end;
+      const double p1_start = (la && K > 0) ? at(ev.sync[2 * K]) : prev_p3_end;
       s.phase1_ms += p1 - p1_start;
       s.phase2_ms += p2 - p1;
       s.phase3_ms += p3 - std::max(prev_p3_end, p2);

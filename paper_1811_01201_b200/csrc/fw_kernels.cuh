@@ -152,7 +152,26 @@ struct TileArgs {
   int mc_lo[2], mc_hi[2];        // excluded columns, per blockIdx.z
   int xrow[2];                   // 1: blockIdx.x walks tile rows (column strip in a dual launch)
   int tag;                       // round number (TAG mode)
+  // Ordered phase-3 launch (order = 1, 1-D grid, 128 x 128 tiles): blockIdx.x enumerates the
+  // round's tiles with the look-ahead set first — A1 = tile-row rowN (next pivot block-row,
+  // -1 if not local) except tile-column colK; A2 = tile-column colN except tile-rows rowK and
+  // rowN; then B = every tile outside tile-rows {rowK, rowN} and tile-columns {colK, colN}.
+  // The CTAs of A1 + A2 (the first nprio) count themselves into *done after their stores, so
+  // the next round's pivot phases can start while B is still running.
+  int order;
+  int tiles_r, tiles_c;          // local tile-rows, tile-columns
+  int rowK, rowN, colK, colN;    // local tile-row of pivot blocks K / K+1 (-1: not local); tile-columns
+  int nprio;                     // |A1| + |A2|
+  int *done;                     // per-round counter of finished look-ahead tiles
 };
+
+// k-th element of {0, .., n-1} \ {x, y} (x, y < 0 or distinct: not excluded twice)
+__device__ __forceinline__ int skip2(int k, int x, int y) {
+  const int lo = (x >= 0 && y >= 0) ? min(x, y) : max(x, y), hi = (x >= 0 && y >= 0) ? max(x, y) : -1;
+  if (lo >= 0 && k >= lo) ++k;
+  if (hi >= 0 && k >= hi) ++k;
+  return k;
+}
 
 // ---------------------------------------------------------------------------------
 // Min-plus tile kernel (phases 2 and 3). Tile origin (i0, j0) = (row0 + by*TM, col0 + bx*TN);
@@ -177,14 +196,37 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   // select the strip description without dynamic indexing (keeps g out of local memory);
   // single-strip launches (phase 3) read everything straight from the parameter bank
   const bool z = DUAL && blockIdx.z != 0;
-  const int mr_lo = z ? g.mr_lo[1] : g.mr_lo[0], mr_hi = z ? g.mr_hi[1] : g.mr_hi[0];
-  const int mc_lo = z ? g.mc_lo[1] : g.mc_lo[0], mc_hi = z ? g.mc_hi[1] : g.mc_hi[0];
-  const int xrow = z ? g.xrow[1] : g.xrow[0];
-  const int bx = xrow ? 0 : blockIdx.x, by = xrow ? blockIdx.x : blockIdx.y;
-  const int i0 = (z ? g.row0[1] : g.row0[0]) + by * TM, j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
-  if ((i0 >= mr_lo && i0 + TM <= mr_hi) || (j0 >= mc_lo && j0 + TN <= mc_hi) ||
-      i0 >= g.rows_lim || j0 >= g.cols_lim)
-    return;
+  int mr_lo = z ? g.mr_lo[1] : g.mr_lo[0], mr_hi = z ? g.mr_hi[1] : g.mr_hi[0];
+  int mc_lo = z ? g.mc_lo[1] : g.mc_lo[0], mc_hi = z ? g.mc_hi[1] : g.mc_hi[0];
+  int i0, j0;
+  if (!DUAL && TM == 128 && TN == 128 && g.order) {   // ordered phase 3: the tile list above
+    int t = blockIdx.x, by, bx;
+    const int nA1 = g.rowN >= 0 ? g.tiles_c - 1 : 0;
+    const int nA2 = g.tiles_r - (g.rowK >= 0) - (g.rowN >= 0);
+    if (t < nA1) {
+      by = g.rowN;
+      bx = skip2(t, g.colK, -1);
+    } else if ((t -= nA1) < nA2) {
+      by = skip2(t, g.rowK, g.rowN);
+      bx = g.colN;
+    } else {
+      t -= nA2;
+      const int nc = g.tiles_c - 2;
+      by = skip2(t / nc, g.rowK, g.rowN);
+      bx = skip2(t % nc, g.colK, g.colN);
+    }
+    i0 = by * TM;
+    j0 = bx * TN;
+    mr_lo = mr_hi = mc_lo = mc_hi = 0;
+  } else {
+    const int xrow = z ? g.xrow[1] : g.xrow[0];
+    const int bx = xrow ? 0 : blockIdx.x, by = xrow ? blockIdx.x : blockIdx.y;
+    i0 = (z ? g.row0[1] : g.row0[0]) + by * TM;
+    j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
+    if ((i0 >= mr_lo && i0 + TM <= mr_hi) || (j0 >= mc_lo && j0 + TN <= mc_hi) ||
+        i0 >= g.rows_lim || j0 >= g.cols_lim)
+      return;
+  }
 
   const int64_t ld = g.ld;
   const int kb = g.kb;
@@ -316,6 +358,22 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   if (is_key(MODE)) {
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if ((tid & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
+  }
+  if (!DUAL && TM == 128 && TN == 128 && g.order && (int)blockIdx.x < g.nprio) {
+    __threadfence();                       // this CTA's D / P stores before the count
+    __syncthreads();
+    if (tid == 0) atomicAdd(g.done, 1);
+  }
+}
+
+// Look-ahead gate: the pivot stream waits until `target` look-ahead tiles of the running
+// ordered phase-3 launch have been stored (one thread; acquire load + back-off).
+__global__ void wait_count_kernel(const int *done, int target) {
+  int v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+    if (v >= target) break;
+    __nanosleep(256);
   }
 }
 
