@@ -166,7 +166,7 @@ p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
         }
       }
     }
-    if (!(VAR & 32)) __syncthreads();
+    if (!(VAR & 32) && !((VAR & 512) && NS >= 3)) __syncthreads();   // 512: one barrier per chunk (NS >= 3)
     else asm volatile("" ::: "memory");
   }
   if (VAR & 8) {   // no epilogue: keep acc live
@@ -447,12 +447,12 @@ int main() {
     CK(cudaMemcpy(Sp, sp.data(), n * n * 4, cudaMemcpyHostToDevice));
   }
   run<8, 2, 16, 16, 2, 32, 2, 3>("prod", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 2, 8>("prod-noepi", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 2, 256 + 3>("prod-L1pf", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 2, 256 + 1>("prod-L1pf-noL2pf", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 256 + 3>("prod-3st-L1pf", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 16, 4, 256 + 3>("prod-bk16-4st-L1pf", D, P, mk, n, sms, clk);
-  run<8, 1, 16, 16, 3, 32, 2, 256 + 3>("8x4-3cta-L1pf", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 3>("prod-3st", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 512 + 3>("prod-3st-1bar", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 16, 4, 512 + 3>("prod-bk16-4st-1bar", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 16, 3, 512 + 3>("prod-bk16-3st-1bar", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 512 + 8>("prod-3st-1bar-noepi", D, P, mk, n, sms, clk);
+  run<8, 1, 16, 16, 3, 32, 3, 512 + 3>("8x4-3cta-3st-1bar", D, P, mk, n, sms, clk);
   run<8, 2, 16, 16, 2, 32, 2, 3>("prod-again", D, P, mk, n, sms, clk);
   return 0;
 }
