@@ -83,6 +83,8 @@ typedef struct fw_stats {
   int64_t phase3_launches;
   double phase3_relaxations; /* relaxations issued by phase-3 launches (algorithmic) */
   int64_t kernel_launches; /* kernels this library launched for the solve (incl. validation) */
+  int32_t compute_f32;  /* 1 = relaxations ran in FP32: FP32 data, or INT32 data whose stored
+                           values are integers < 2^24 (exact in FP32)     */
 } fw_stats;
 
 /* Create the process-wide context. ngpus_max: 0 = all visible devices (this build

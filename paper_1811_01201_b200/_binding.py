@@ -34,7 +34,7 @@ class FwStats(ctypes.Structure):
         ("phase2_ms", ctypes.c_double), ("phase3_ms", ctypes.c_double),
         ("post_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
         ("phase3_launches", ctypes.c_int64), ("phase3_relaxations", ctypes.c_double),
-        ("kernel_launches", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64), ("compute_f32", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

@@ -31,7 +31,13 @@ __global__ void __launch_bounds__(256, MINB) probe(float *out, int iters, float 
   for (int i = 0; i < 2 * RM; ++i) a[i] = seed * (threadIdx.x + i);
 #pragma unroll
   for (int i = 0; i < 8; ++i) { float p = seed + i, q = seed - i; asm("mov.b64 %0, {%1,%2};" : "=l"(b[i]) : "f"(p), "f"(q)); }
+  unsigned long long zero;
+  { float z0 = 0.f; asm("mov.b64 %0, {%1,%1};" : "=l"(zero) : "f"(z0)); }
   for (int it = 0; it < iters; ++it) {
+    // loop-carried B operands (b + 0, not foldable because of signed zero): without this
+    // ptxas CSEs the FADD2s across iterations (8 extra FADD2 per 8*RM, not counted)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(b[i]) : "l"(zero));
 #pragma unroll
     for (int r = 0; r < RM; ++r) {
       if (ORDER == 0) {   // production order: per 4 columns: 4 FADD2 then 4 FMNMX3

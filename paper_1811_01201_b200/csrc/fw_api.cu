@@ -482,12 +482,12 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
   return rk[0].run(st, ev, la);
 }
 
-template <typename T, int MODE>
-int run_init(cudaStream_t st, const T *src, int64_t ld_src, int64_t nsrc, int64_t n, int64_t row0,
+template <typename T, int MODE, typename S>
+int run_init(cudaStream_t st, const S *src, int64_t ld_src, int64_t nsrc, int64_t n, int64_t row0,
              T *D, int32_t *P, int64_t ld, int64_t nrows, int64_t n_pad) {
   if (nrows == 0) return FW_OK;
   dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)std::min<int64_t>(nrows, 65535));
-  init_kernel<T, MODE><<<g, 256, 0, st>>>(src, ld_src, nsrc, n, row0, D, P, ld, n_pad, nrows);
+  init_kernel<T, MODE, S><<<g, 256, 0, st>>>(src, ld_src, nsrc, n, row0, D, P, ld, n_pad, nrows);
   ++g_launches;
   CU(cudaGetLastError());
   return FW_OK;
@@ -495,6 +495,161 @@ int run_init(cudaStream_t st, const T *src, int64_t ld_src, int64_t nsrc, int64_
 
 template <typename T>
 constexpr bool is_int_v() { return std::is_integral<T>::value; }
+
+// One entry of a solve's plan: P method, compute type, whether the key range is guaranteed,
+// and the largest stored key (bit pattern) a speculative key run may leave.
+struct Attempt {
+  int mode;
+  bool f32;          // relax in FP32 (INT32 data whose stored values are integers < 2^24)
+  bool key_static;
+  int key_limit;
+};
+
+int key_limit_f32() {
+  const float f = (float)(kKeyMaxF32 * 128 + 127);
+  int b;
+  memcpy(&b, &f, 4);
+  return b;
+}
+
+// The parts' working buffers viewed in compute type C (same 4-byte slots).
+template <typename C, typename T>
+std::vector<Part<C>> view_as(const std::vector<Part<T>> &parts) {
+  static_assert(sizeof(C) == sizeof(T), "same element size");
+  std::vector<Part<C>> v;
+  for (const auto &p : parts) {
+    Part<C> q{};
+    q.src = reinterpret_cast<C *>(p.src);
+    q.ld_src = p.ld_src;
+    q.next = p.next;
+    q.ld_next = p.ld_next;
+    q.rank = p.rank;
+    q.row0 = p.row0;
+    q.nrows = p.nrows;
+    q.nsrc = p.nsrc;
+    q.D = reinterpret_cast<C *>(p.D);
+    q.P = p.P;
+    q.ld = p.ld;
+    q.inplace = p.inplace;
+    q.strip[0] = reinterpret_cast<C *>(p.strip[0]);
+    q.strip[1] = reinterpret_cast<C *>(p.strip[1]);
+    v.push_back(q);
+  }
+  return v;
+}
+
+// Init (pad, diagonal, key encoding; source type T converted to compute type C) and the
+// R rounds of one attempt. from_backup: re-read W from the backup of an in-place solve.
+template <typename C, typename T>
+int run_attempt(Ctx &c, std::vector<Part<T>> &parts, std::vector<Part<C>> &cv, Transport tr, int world,
+                int64_t n, int BS, int R, int mode, bool from_backup, int *maxkey, int *done,
+                cudaStream_t st, const Events &ev, bool la, cudaEvent_t e_init) {
+  const int64_t n_pad = (n + 127) / 128 * 128;
+  for (size_t i = 0; i < parts.size(); ++i) {
+    const Part<T> &p = parts[i];
+    Part<C> &q = cv[i];
+    const T *isrc = (from_backup && p.backup) ? p.backup : p.src;
+    const int64_t ild = (from_backup && p.backup) ? n : p.ld_src;
+    switch (mode) {
+      case MODE_PLAIN: TRY((run_init<C, MODE_PLAIN, T>(st, isrc, ild, p.nsrc, n, p.row0, q.D, q.P, q.ld, q.nrows, n_pad))); break;
+      case MODE_TAG: TRY((run_init<C, MODE_TAG, T>(st, isrc, ild, p.nsrc, n, p.row0, q.D, q.P, q.ld, q.nrows, n_pad))); break;
+      default: TRY((run_init<C, MODE_KEY, T>(st, isrc, ild, p.nsrc, n, p.row0, q.D, q.P, q.ld, q.nrows, n_pad)));
+    }
+  }
+  CU(cudaMemsetAsync(done, 0, 4 * (size_t)R, st));
+  CU(cudaEventRecord(e_init, st));
+  switch (mode) {
+    case MODE_PLAIN: return run_rounds<C, MODE_PLAIN>(c, cv, tr, world, n, BS, R, maxkey, done, st, ev, la);
+    case MODE_TAG: return run_rounds<C, MODE_TAG>(c, cv, tr, world, n, BS, R, maxkey, done, st, ev, la);
+    default: return run_rounds<C, MODE_KEY>(c, cv, tr, world, n, BS, R, maxkey, done, st, ev, la);
+  }
+}
+
+// Epilogue passes (reading R9/R10): keys -> distances; round tags -> last k (gathering and
+// transposing the final D); last k -> next hop and the sentinels.
+template <typename T>
+int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS, int mode,
+              int path_mode, int *d_flags, cudaStream_t st) {
+  const int64_t n_pad = (n + 127) / 128 * 128;
+  const bool nccl = tr == T_NCCL && world > 1;
+  if (is_key(mode)) {
+    for (auto &p : parts) {
+      if (p.nrows == 0) continue;
+      dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(p.nrows, 65535));
+      decode_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n, p.nrows);
+      ++g_launches;
+      CU(cudaGetLastError());
+    }
+  }
+  if (mode == MODE_TAG && path_mode >= 0) {
+    // the search reads column segments D[kb..kb+BS)[j] of rows wherever they live: gather the
+    // final D (multi-GPU), then transpose it so each segment is one contiguous 4*BS-byte read
+    const T *Dfull = parts[0].D - (tr == T_LOOPBACK ? parts[0].row0 * n_pad : 0);
+    int64_t ldf = parts[0].ld;
+    if (nccl) {
+      Part<T> &p = parts[0];
+      TRY(c.ws_full.ensure((size_t)n_pad * n_pad * sizeof(T)));
+      T *full = static_cast<T *>(c.ws_full.p);
+      if (p.nrows > 0)
+        CU(cudaMemcpy2DAsync(full + p.row0 * n_pad, n_pad * sizeof(T), p.D, p.ld * sizeof(T),
+                             n_pad * sizeof(T), p.nrows, cudaMemcpyDeviceToDevice, st));
+      NC(g_nccl.GroupStart());
+      for (int r = 0; r < world; ++r) {
+        int64_t r0, nr;
+        partition(n, world, r, &r0, &nr);
+        if (nr == 0) continue;
+        T *dst = full + r0 * n_pad;
+        NC(g_nccl.Broadcast(dst, dst, (size_t)nr * n_pad, is_int_v<T>() ? ncclInt32 : ncclFloat32, r,
+                            c.comm, st));
+      }
+      NC(g_nccl.GroupEnd());
+      Dfull = full;
+      ldf = n_pad;
+    }
+    TRY(c.ws_tr.ensure((size_t)n_pad * n_pad * sizeof(T)));
+    T *Dt = static_cast<T *>(c.ws_tr.p);
+    {
+      dim3 g((unsigned)(n_pad / 32), (unsigned)(n_pad / 32));
+      transpose_kernel<T><<<g, dim3(32, 8), 0, st>>>(Dfull, ldf, n_pad, n_pad, Dt, n_pad);
+      CU(cudaGetLastError());
+      ++g_launches;
+    }
+    const size_t rb = (size_t)n_pad * sizeof(T);
+    const int use_smem = rb <= 200 * 1024;
+    auto launch = [&](auto kern) -> int {
+      // every call: the three CH instantiations share this lambda's parameter type (one
+      // function-pointer type), so a "configured once" flag here would cover only one of them
+      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      for (auto &p : parts) {
+        if (p.nsrc == 0) continue;
+        kern<<<(unsigned)p.nsrc, 512, use_smem ? rb : 0, st>>>(p.D, Dt, p.ld, n_pad, p.row0, n,
+                                                              n_pad, p.P, use_smem);
+        CU(cudaGetLastError());
+        ++g_launches;
+      }
+      return FW_OK;
+    };
+    switch (BS) {
+      case 32: TRY(launch(resolve_lastk_kernel<T, 1>)); break;
+      case 64: TRY(launch(resolve_lastk_kernel<T, 2>)); break;
+      default: TRY(launch(resolve_lastk_kernel<T, 4>));
+    }
+  }
+  if (path_mode >= 0) {
+    const size_t row_bytes = (size_t)n * sizeof(int32_t);
+    const int use_smem = row_bytes <= 200 * 1024;
+    CU(cudaFuncSetAttribute(finalize_paths_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            200 * 1024));
+    for (auto &p : parts) {
+      if (p.nsrc == 0) continue;
+      finalize_paths_kernel<T><<<(unsigned)p.nsrc, 1024, use_smem ? row_bytes : 0, st>>>(
+          p.D, p.P, p.ld, p.row0, n, path_mode == 0, use_smem, d_flags);
+      ++g_launches;
+      CU(cudaGetLastError());
+    }
+  }
+  return FW_OK;
+}
 
 // Solve over `parts` (one part = one rank's rows): T_LOCAL (one GPU, all rows), T_NCCL (this
 // process's rank of an NCCL communicator), T_LOOPBACK (every rank emulated here).
@@ -543,27 +698,24 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     return fail(FW_ERANGE, "(n-1)*max_weight = %lld >= FW_INF_I32: finite path sums could reach INF",
                 (long long)(n - 1) * h_flags[1]);
 
-  // 2. P mode: exact arg-min keys for integer-valued data within the key range, else tags
-  const int64_t key_max = int_t ? kKeyMaxI32 : kKeyMaxF32;
+  // 2. plan: exact arg-min keys for integer-valued data within the key range (static, or
+  //    speculative and verified by the max stored key), else round tags; INT32 data runs in
+  //    FP32 when every value it can store is an integer below 2^24 (keys: max key checked)
   const bool integral = int_t || !(h_flags[0] & 2);
   const bool has_inf = (h_flags[0] & 4) != 0;
-  int mode = MODE_PLAIN;
-  bool key_static = false;
-  if (want_p) {
-    mode = MODE_TAG;
-    if (integral && maxw <= (double)key_max) {
-      mode = MODE_KEY;
-      // stored finite values never exceed max(W) without INF entries; otherwise a path
-      // value is at most (n-1)*max(W) — or is checked after the solve (max stored key)
-      key_static = !has_inf || (double)(n - 1) * maxw <= (double)key_max;
-    }
+  const double path_max = (double)(n > 1 ? n - 1 : 1) * maxw;   // bound on any finite distance
+  const bool f32_exact = int_t && path_max < 16777216.0;         // 2^24: PLAIN / TAG in FP32
+  std::vector<Attempt> plan;
+  if (want_p && integral) {
+    if (int_t && maxw <= (double)kKeyMaxF32)
+      plan.push_back({MODE_KEY, true, !has_inf || path_max <= (double)kKeyMaxF32, key_limit_f32()});
+    const int64_t kmax = int_t ? kKeyMaxI32 : kKeyMaxF32;
+    if (maxw <= (double)kmax && !(int_t && plan.size() && plan[0].key_static))
+      plan.push_back({MODE_KEY, false, !has_inf || path_max <= (double)kmax,
+                      int_t ? (int)(kKeyMaxI32 * 128 + 127) : key_limit_f32()});
   }
-  const int key_limit = int_t ? (int)(key_max * 128 + 127) : [] {
-    float f = (float)(kKeyMaxF32 * 128 + 127);
-    int b;
-    memcpy(&b, &f, 4);
-    return b;
-  }();
+  if (want_p && (plan.empty() || !plan.back().key_static)) plan.push_back({MODE_TAG, f32_exact, true, 0});
+  if (!want_p) plan.push_back({MODE_PLAIN, f32_exact, true, 0});
 
   // 3. placement
   if (tr == T_LOOPBACK) {
@@ -603,8 +755,8 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
       p.strip[0] = static_cast<T *>(c.ws_s.p);
       p.strip[1] = reinterpret_cast<T *>(static_cast<char *>(c.ws_s.p) + sb);
     }
-    // the speculative key run may have to be redone with tags: keep W when solving in place
-    if (is_key(mode) && !key_static && p.inplace && p.nsrc > 0) {
+    // a speculative key run may have to be redone: keep W when solving in place
+    if (plan.size() > 1 && p.inplace && p.nsrc > 0) {
       TRY(c.ws_b.ensure((size_t)p.nsrc * n * sizeof(T)));
       p.backup = static_cast<T *>(c.ws_b.p);
       CU(cudaMemcpy2DAsync(p.backup, n * sizeof(T), p.src, p.ld_src * sizeof(T), n * sizeof(T),
@@ -619,115 +771,44 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   int *d_maxkey = d_flags + 2;
   const bool la = c.lookahead && BS == 128 && R >= 2;
 
+  // 4. attempts: the first that is exact wins (plan built above); FP32 compute for INT32 data
+  //    whose stored values stay below 2^24
   const int64_t launches0 = g_launches - (int64_t)parts.size();   // + the validation launches
   CU(cudaEventRecord(e_begin, st));
   CU(cudaStreamWaitEvent(c.side, e_begin, 0));   // the side stream follows the caller's stream
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    // 4. init (+ key encoding), rounds
-    for (auto &p : parts) {
-      const T *isrc = (attempt == 1 && p.backup) ? p.backup : p.src;
-      const int64_t ild = (attempt == 1 && p.backup) ? n : p.ld_src;
-      switch (mode) {
-        case MODE_PLAIN: TRY((run_init<T, MODE_PLAIN>(st, isrc, ild, p.nsrc, n, p.row0, p.D, p.P, p.ld, p.nrows, n_pad))); break;
-        case MODE_TAG: TRY((run_init<T, MODE_TAG>(st, isrc, ild, p.nsrc, n, p.row0, p.D, p.P, p.ld, p.nrows, n_pad))); break;
-        default: TRY((run_init<T, MODE_KEY>(st, isrc, ild, p.nsrc, n, p.row0, p.D, p.P, p.ld, p.nrows, n_pad)));
-      }
-    }
-    CU(cudaMemsetAsync(d_done, 0, 4 * (size_t)R, st));
-    CU(cudaEventRecord(e_init, st));
-    switch (mode) {
-      case MODE_PLAIN: TRY((run_rounds<T, MODE_PLAIN>(c, parts, tr, world, n, BS, R, d_maxkey, d_done, st, ev, la))); break;
-      case MODE_TAG: TRY((run_rounds<T, MODE_TAG>(c, parts, tr, world, n, BS, R, d_maxkey, d_done, st, ev, la))); break;
-      default: TRY((run_rounds<T, MODE_KEY>(c, parts, tr, world, n, BS, R, d_maxkey, d_done, st, ev, la)));
-    }
-    if (!is_key(mode) || key_static) break;
+  std::vector<Part<float>> fview = view_as<float>(parts);
+  Attempt used = plan[0];
+  for (size_t a = 0; a < plan.size(); ++a) {
+    used = plan[a];
+    const bool from_backup = a > 0;
+    if (used.f32)
+      TRY((run_attempt<float, T>(c, parts, fview, tr, world, n, BS, R, used.mode, from_backup, d_maxkey,
+                                 d_done, st, ev, la, e_init)));
+    else
+      TRY((run_attempt<T, T>(c, parts, parts, tr, world, n, BS, R, used.mode, from_backup, d_maxkey,
+                             d_done, st, ev, la, e_init)));
+    if (!is_key(used.mode) || used.key_static) break;
     if (nccl) NC(g_nccl.AllReduce(d_maxkey, d_maxkey, 1, ncclInt32, ncclMax, c.comm, st));
     CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    if (h_flags[2] <= key_limit) break;
-    mode = MODE_TAG;   // a stored key left the exact range: redo with round tags
-    CU(cudaMemsetAsync(d_maxkey, 0, 4, st));
+    if (h_flags[2] <= used.key_limit || a + 1 == plan.size()) break;
+    CU(cudaMemsetAsync(d_maxkey, 0, 4, st));   // a stored key left the exact range: next plan
   }
+  const int mode = used.mode;
 
-  // 5. epilogue passes: keys -> distances; tags -> last k; last k -> next hop (R9/R10)
-  if (is_key(mode)) {
-    for (auto &p : parts) {
-      if (p.nrows == 0) continue;
-      dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(p.nrows, 65535));
-      decode_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n, p.nrows);
-      ++g_launches;
-      CU(cudaGetLastError());
-    }
-  }
-  if (mode == MODE_TAG) {
-    // the search reads column segments D[kb..kb+BS)[j] of rows wherever they live: gather the
-    // final D (multi-GPU), then transpose it so each segment is one contiguous 4*BS-byte read
-    const T *Dfull = parts[0].D - (tr == T_LOOPBACK ? parts[0].row0 * n_pad : 0);
-    int64_t ldf = parts[0].ld;
-    if (nccl) {
-      Part<T> &p = parts[0];
-      TRY(c.ws_full.ensure((size_t)n_pad * n_pad * sizeof(T)));
-      T *full = static_cast<T *>(c.ws_full.p);
-      if (p.nrows > 0)
-        CU(cudaMemcpy2DAsync(full + p.row0 * n_pad, n_pad * sizeof(T), p.D, p.ld * sizeof(T),
-                             n_pad * sizeof(T), p.nrows, cudaMemcpyDeviceToDevice, st));
-      NC(g_nccl.GroupStart());
-      for (int r = 0; r < world; ++r) {
-        int64_t r0, nr;
-        partition(n, world, r, &r0, &nr);
-        if (nr == 0) continue;
-        T *dst = full + r0 * n_pad;
-        NC(g_nccl.Broadcast(dst, dst, (size_t)nr * n_pad, int_t ? ncclInt32 : ncclFloat32, r, c.comm, st));
-      }
-      NC(g_nccl.GroupEnd());
-      Dfull = full;
-      ldf = n_pad;
-    }
-    TRY(c.ws_tr.ensure((size_t)n_pad * n_pad * sizeof(T)));
-    T *Dt = static_cast<T *>(c.ws_tr.p);
-    {
-      dim3 g((unsigned)(n_pad / 32), (unsigned)(n_pad / 32));
-      transpose_kernel<T><<<g, dim3(32, 8), 0, st>>>(Dfull, ldf, n_pad, n_pad, Dt, n_pad);
-      CU(cudaGetLastError());
-      ++g_launches;
-    }
-    const size_t rb = (size_t)n_pad * sizeof(T);
-    const int use_smem = rb <= 200 * 1024;
-    auto launch = [&](auto kern) -> int {
-      // every call: the three CH instantiations share this lambda's parameter type (one
-      // function-pointer type), so a "configured once" flag here would cover only one of them
-      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      for (auto &p : parts) {
+  // 5. epilogue passes in the compute type; FP32 results of INT32 data back to INT32
+  if (used.f32) {
+    TRY(post_pass<float>(c, fview, tr, world, n, BS, mode, path_mode, d_flags, st));
+    if (!std::is_same<T, float>::value)
+      for (auto &p : fview) {
         if (p.nsrc == 0) continue;
-        kern<<<(unsigned)p.nsrc, 512, use_smem ? rb : 0, st>>>(p.D, Dt, p.ld, n_pad, p.row0, n,
-                                                              n_pad, p.P, use_smem);
-        CU(cudaGetLastError());
+        dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(p.nsrc, 65535));
+        f32_to_i32_kernel<<<g, 256, 0, st>>>(p.D, p.ld, n, p.nsrc);
         ++g_launches;
+        CU(cudaGetLastError());
       }
-      return FW_OK;
-    };
-    switch (BS) {
-      case 32: TRY(launch(resolve_lastk_kernel<T, 1>)); break;
-      case 64: TRY(launch(resolve_lastk_kernel<T, 2>)); break;
-      default: TRY(launch(resolve_lastk_kernel<T, 4>));
-    }
-  }
-  if (want_p) {
-    const size_t row_bytes = (size_t)n * sizeof(int32_t);
-    const int use_smem = row_bytes <= 200 * 1024;
-    static bool configured = false;
-    if (!configured) {
-      CU(cudaFuncSetAttribute(finalize_paths_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              200 * 1024));
-      configured = true;
-    }
-    for (auto &p : parts) {
-      if (p.nsrc == 0) continue;
-      finalize_paths_kernel<T><<<(unsigned)p.nsrc, 1024, use_smem ? row_bytes : 0, st>>>(
-          p.D, p.P, p.ld, p.row0, n, path_mode == 0, use_smem, d_flags);
-      ++g_launches;
-      CU(cudaGetLastError());
-    }
+  } else {
+    TRY(post_pass<T>(c, parts, tr, world, n, BS, mode, path_mode, d_flags, st));
   }
   CU(cudaEventRecord(e_post, st));
 
@@ -758,6 +839,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   s.is_int = int_t;
   s.path_mode = path_mode;
   s.p_method = mode;
+  s.compute_f32 = (used.f32 || !int_t) ? 1 : 0;
   float ms = 0.f;
   CU(cudaEventElapsedTime(&ms, e_begin, e_end));
   s.solve_ms = ms;
@@ -774,7 +856,8 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   s.phase3_relaxations = relax;
   if (timing) {
     // absolute event times (ms since e_begin); with the look-ahead, phases 1-2 of round K
-    // run on the side stream from the end of P3a(K-1), concurrently with P3b(K-1)
+    // run on the side stream from the wait for round K-1's look-ahead tiles, concurrently
+    // with the rest of round K-1's phase 3
     auto at = [&](cudaEvent_t e) {
       float t = 0.f;
       cudaEventElapsedTime(&t, e_begin, e);

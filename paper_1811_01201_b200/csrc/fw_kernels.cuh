@@ -504,15 +504,24 @@ __global__ void validate_kernel(const T *src, int64_t lds, int64_t nrows, int64_
 // Copy W (n x n, lds) into the padded n_pad x n_pad working matrix (ld): padded entries INF,
 // diagonal 0 (R4, R11); key mode stores D*128 + (j&127). P (tags / last k) initialised to -1
 // ("no intermediate yet"). src may alias D (in-place solve).
+// Source value in the compute type C: identity, or INT32 -> FP32 (FW_INF_I32 -> +inf; finite
+// INT32 weights below 2^24 are exact in FP32 — the host only picks FP32 compute when every
+// value the solve can store stays below 2^24).
+template <typename C, typename S> __device__ __forceinline__ C to_compute(S v) { return (C)v; }
+template <> __device__ __forceinline__ float to_compute<float, int32_t>(int32_t v) {
+  return v >= 0x3FFFFFFF ? __int_as_float(0x7f800000) : (float)v;
+}
+
 // Row loops stride by gridDim.y (grid.y is capped at 65535 rows per launch).
-template <typename T, int MODE>
-__global__ void init_kernel(const T *src, int64_t lds, int64_t nsrc, int64_t n, int64_t row0, T *D,
+// src (type S) may alias D (type T, same 4-byte slots): each element is read before it is written.
+template <typename T, int MODE, typename S = T>
+__global__ void init_kernel(const S *src, int64_t lds, int64_t nsrc, int64_t n, int64_t row0, T *D,
                             int32_t *P, int64_t ld, int64_t n_pad, int64_t nrows) {
   for (int64_t i = blockIdx.y; i < nrows; i += gridDim.y) {   // local row; global row0 + i
     const int64_t gi = row0 + i;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_pad;
          j += (int64_t)gridDim.x * blockDim.x) {
-      T v = (i < nsrc && gi < n && j < n) ? src[i * lds + j] : Num<T>::inf();
+      T v = (i < nsrc && gi < n && j < n) ? to_compute<T, S>(src[i * lds + j]) : Num<T>::inf();
       if (gi == j) v = 0;
       if (MODE != MODE_PLAIN) P[i * ld + j] = -1;
       if (is_key(MODE)) v = Num<T>::encode(v, (int)j);
@@ -528,6 +537,16 @@ __global__ void decode_kernel(T *D, int64_t ld, int64_t n, int64_t rows) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x)
       D[i * ld + j] = Num<T>::decode(D[i * ld + j]);
+}
+
+// FP32 compute -> INT32 storage in place (integer values below 2^24; +inf -> FW_INF_I32).
+__global__ void f32_to_i32_kernel(float *D, int64_t ld, int64_t n, int64_t rows) {
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      const float v = D[i * ld + j];
+      reinterpret_cast<int32_t *>(D)[i * ld + j] = v < __int_as_float(0x7f800000) ? (int32_t)v : 0x3FFFFFFF;
+    }
 }
 
 // Copy the `rows` x n result out of the padded workspace (unpad).

@@ -392,6 +392,28 @@ def test_keyed_lastk():
     assert oracle.check_paths(W, D, P, mode="lastk")[0] == 0
 
 
+@pytest.mark.parametrize("n,hi,p,block,want_f32", [
+    (700, 1000, 0.1, 128, 1),       # C3-like: keys fit FP32 (speculative, verified)
+    (300, 3000, 0.05, 64, 1),       # larger weights, keys still below 2^24 after the solve
+    (257, 3_000_000, 0.05, 32, 0),  # (n-1)*max_w >= 2^24 and keys out of FP32 range: INT32 compute
+])
+def test_int32_compute_type(n, hi, p, block, want_f32):
+    """INT32 data relaxes in FP32 when every stored value is an integer below 2^24 (DESIGN.md
+    §4.7), natively otherwise; D bit-exact and paths valid either way."""
+    W = gen.generate("er_int", n, 21, p=p, lo=1, hi=hi)
+    for path in ("next", None):
+        D = W.copy()
+        P = np.empty(W.shape, dtype=np.int32) if path else None
+        with Ctx(fw.FW_TIMING):
+            fw.fw_solve_i32(D, P, block=block)
+            s = fw.fw_last_stats()
+        if path or want_f32 == 0:
+            assert s.compute_f32 == want_f32, (s.compute_f32, s.p_method)
+        np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+        if path:
+            assert oracle.check_paths(W, D, P)[0] == 0
+
+
 def test_zero_weight_edges_distances():
     """Zero off-diagonal weights are in the domain (reading C-5): D must be exact."""
     W = gen.generate("er_int_f32", 260, 15, p=0.05, lo=0, hi=3)
