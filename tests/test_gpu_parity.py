@@ -419,3 +419,37 @@ def test_zero_weight_edges_distances():
     W = gen.generate("er_int_f32", 260, 15, p=0.05, lo=0, hi=3)
     D, P = solve(W, 64)
     np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+
+
+# ---- one context, many solves: workspace growth/shrink, per-kernel configuration, counters -
+def test_mixed_sequence_one_context():
+    """A seeded sequence of solves through ONE fw_init context: sizes up and down, every block
+    size, FP32 integer / real / INF data and INT32, next-hop / LAST_K / distance-only, host and
+    device entry points — each checked against the oracle (catches state carried between solves:
+    workspaces, lazily configured kernel attributes, look-ahead counters, key fallbacks)."""
+    rng = np.random.default_rng(2024)
+    kinds = ["complete_int", "complete_real", "er_int", "er_int_f32", "er_real"]
+    with Ctx(fw.FW_TIMING):
+        for step in range(24):
+            n = int(rng.choice([1, 5, 64, 129, 300, 520, 1100]))
+            kind = kinds[step % len(kinds)]
+            block = int(rng.choice([0, 32, 64, 128]))
+            W = gen.generate(kind, n, 900 + step, p=0.05, lo=1, hi=int(rng.choice([9, 1000])))
+            path = [None, "next"][step % 2]
+            device = bool(step % 3 == 0)
+            D = W.copy()
+            P = np.empty(W.shape, dtype=np.int32) if path else None
+            if device:
+                dD = torch.from_numpy(D).cuda()
+                dP = torch.from_numpy(P).cuda() if P is not None else None
+                f = fw.fw_solve_device_i32 if W.dtype == np.int32 else fw.fw_solve_device_f32
+                f(dD, dP, block=block, stream=torch.cuda.current_stream())
+                D = dD.cpu().numpy()
+                P = dP.cpu().numpy() if dP is not None else None
+            else:
+                (fw.fw_solve_i32 if W.dtype == np.int32 else fw.fw_solve)(D, P, block=block)
+            exact = exact_data(W)
+            assert_D_matches(D, oracle.fw(W, None)[0], exact)
+            if path:
+                bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5)
+                assert bad == 0, (step, kind, n, block, bad, first)
