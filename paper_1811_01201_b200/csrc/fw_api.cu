@@ -230,13 +230,22 @@ template <typename T, int BS, int MODE>
 int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int kb, int K,
                      int *maxkey) {
   const int bytes = 2 * BS * BS * (int)sizeof(T);   // row-major + transposed copy of D_KK
-  auto kern = phase1_kernel<T, BS, MODE>;
   static bool configured = false;
-  if (!configured) {
-    CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    configured = true;
+  if (std::is_same<T, float>::value && is_key(MODE)) {   // FP32 keys: select-free variant
+    auto kern = phase1_key_f32_kernel<BS>;
+    if (!configured) {
+      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      configured = true;
+    }
+    kern<<<1, 1024, bytes, st>>>(reinterpret_cast<float *>(D), P, ld, r0, kb, maxkey);
+  } else {
+    auto kern = phase1_kernel<T, BS, MODE>;
+    if (!configured) {
+      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      configured = true;
+    }
+    kern<<<1, 1024, bytes, st>>>(D, P, ld, r0, kb, K, maxkey);
   }
-  kern<<<1, 1024, bytes, st>>>(D, P, ld, r0, kb, K, maxkey);
   ++g_launches;
   CU(cudaGetLastError());
   return FW_OK;

@@ -473,6 +473,89 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
   }
 }
 
+// Phase 1, FP32 keyed mode, without a per-relaxation select for P. The running value of
+// (a, b) is kept in the form  x = D*128 - 0.5  while unchanged, and a candidate through k is
+// the integer  c_k = D[a][k]*128 + k' + D[k][b]*128  (k' = (kb + k) & 127, increasing in k
+// inside a block): c_k < x  <=>  D[a][k] + D[k][b] < D (strict, P:125 / reading R2), and the
+// minimum over the sequence is the smallest distance reached first, with its k in the low 7
+// bits — the sequential strict-< result of the paper's loop, with one FADD + one FMNMX per
+// relaxation. Row k+1 is published as D*128 (B side), column k+1 as D*128 + k' (A side), both
+// recovered as floor((x + 0.5) / 128) * 128. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
+template <int BS>
+__global__ void __launch_bounds__(1024)
+phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
+                      int *maxkey) {
+  constexpr int R = BS / 32;
+  using VR = typename std::conditional<R == 4, float4, typename std::conditional<R == 2, float2, float>::type>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *sD = reinterpret_cast<float *>(smem_raw);   // row-major, B form  D*128
+  float *sDT = sD + BS * BS;                         // transposed, A form D*128 + k'
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  float *Dk = D + (int64_t)r0 * ld + kb;
+  const int kgrp = kb & ~127, klow = kb & 127;
+  float x[R][R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      const int a = R * ty + r, b = R * tx + c;
+      const float key = Dk[(int64_t)a * ld + b];        // D*128 + ((kb + b) & 127), or +inf
+      const float base = key - (float)(klow + b);        // D*128 (+inf stays +inf)
+      x[r][c] = base - 0.5f;
+      sD[a * BS + b] = base;
+      sDT[b * BS + a] = key;
+    }
+  __syncthreads();
+  for (int k0 = 0; k0 < BS; k0 += R) {
+#pragma unroll
+    for (int kr = 0; kr < R; ++kr) {
+      const int k = k0 + kr;
+      const VR cv = *reinterpret_cast<const VR *>(sDT + k * BS + R * ty);   // A side, own rows
+      const VR rv = *reinterpret_cast<const VR *>(sD + k * BS + R * tx);    // B side, own cols
+      const float *colv = reinterpret_cast<const float *>(&cv);
+      const float *rowv = reinterpret_cast<const float *>(&rv);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < R; ++c) x[r][c] = fminf(x[r][c], colv[r] + rowv[c]);
+      const int slot = (kr + 1) % R;
+      const int owner = (k + 1) / R;
+      if (k + 1 < BS) {
+        if (owner == ty) {
+#pragma unroll
+          for (int c = 0; c < R; ++c)
+            sD[(k + 1) * BS + R * tx + c] = floorf((x[slot][c] + 0.5f) * 0.0078125f) * 128.0f;
+        }
+        if (owner == tx) {
+          const float kp = (float)(klow + k + 1);
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            sDT[(k + 1) * BS + R * ty + r] = floorf((x[r][slot] + 0.5f) * 0.0078125f) * 128.0f + kp;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int kmax = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      const float v = x[r][c];
+      if (v < __int_as_float(0x7f800000) && v == floorf(v)) {   // an integer: strictly improved
+        const int a = R * ty + r, b = R * tx + c;
+        const float hi = floorf(v * 0.0078125f) * 128.0f;
+        const int kk = (int)(v - hi);
+        const float key = hi + (float)(klow + b);
+        Dk[(int64_t)a * ld + b] = key;
+        P[(int64_t)(r0 + a) * ld + kb + b] = kgrp + kk;
+        kmax = max(kmax, __float_as_int(key));
+      }
+    }
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (tx == 0 && kmax > 0) atomicMax(maxkey, kmax);
+}
+
 // ---------------------------------------------------------------------------------
 // Validation (read-only, before anything is written: fw.h error contract).
 // flags: bit 0 out-of-domain value; bit 1 a finite FP32 weight is not integer-valued;
