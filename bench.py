@@ -296,7 +296,7 @@ def run_gpu(args, cfg):
                 torch.distributed.barrier()
             t0 = time.perf_counter()
             if world == 1:
-                (fw.fw_solve_i32 if is_int else fw.fw_solve)(hD, hP, block=BS)
+                (fw.fw_solve_i32 if is_int else fw.fw_solve)(hD, hP, block=BS, ngpus=1)
             else:
                 dD.copy_(hD, non_blocking=True)
                 solve(dD, dP, n=n, ld=n, block=BS, stream=stream)

@@ -87,9 +87,9 @@ typedef struct fw_stats {
                            values are integers < 2^24 (exact in FP32)     */
 } fw_stats;
 
-/* Create the process-wide context. ngpus_max: 0 = all visible devices (this build
- * solves on device 0 of the calling process; multi-GPU runs one process per GPU).
- * flags: FW_PATH_* | FW_TIMING. Returns FW_ESTATE if already initialised. */
+/* Create the process-wide context. ngpus_max: the most devices one fw_solve may use,
+ * 0 = all visible devices; the single-GPU entry points run on the calling thread's current
+ * device. flags: FW_PATH_* | FW_TIMING. Returns FW_ESTATE if already initialised. */
 int fw_init(int ngpus_max, unsigned flags);
 
 /* Release every device buffer, stream and event of the context. Idempotent. */
@@ -103,7 +103,14 @@ int fw_free(void);
  *         -1 for a direct edge, the diagonal, or an unreachable pair.
  *   n     number of vertices, 1 <= n <= 65536.
  *   block BS in {32, 64, 128}, or 0 = auto (128 for n >= 4096, else 64).
- *   ngpus must be 0 or 1 in this single-process entry point.
+ *   ngpus 1 = the current device; G in [2, ngpus_max] = devices 0..G-1 of this process,
+ *         block-row partitioned (BJ north_star; SURVEY §8 e): one host thread per device,
+ *         an NCCL communicator over them (created on first use, kept until fw_free), the
+ *         per-round pivot-strip broadcast, each device copying its own rows in and out;
+ *         0 = ngpus_max. FW_EINVAL outside [0, ngpus_max]; FW_ESTATE while a
+ *         fw_comm_init communicator (one process per GPU) is active; FW_ENCCL if NCCL
+ *         cannot be loaded or initialised. A failing rank's message is prefixed with its
+ *         rank and device.
  * Pinned (cudaHostAlloc/registered) buffers are copied directly; pageable buffers are
  * staged through an internal pinned buffer. */
 int fw_solve(float *dist, int32_t *next, int64_t n, int block, int ngpus);

@@ -114,12 +114,13 @@ def fw_free() -> None:
     _check(_lib.fw_free())
 
 
-def fw_solve(dist, next=None, n=None, block: int = 0, ngpus: int = 0) -> None:
-    """FP32 host solve in place (dist: n x n float32; next: n x n int32 or None)."""
+def fw_solve(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:
+    """FP32 host solve in place (dist: n x n float32; next: n x n int32 or None).
+    ngpus: 1 = current device (default here), G > 1 = devices 0..G-1, 0 = fw_init's ngpus_max."""
     _check(_lib.fw_solve(_addr(dist, "float32"), _addr(next, "int32"), _n_of(dist, n), block, ngpus))
 
 
-def fw_solve_i32(dist, next=None, n=None, block: int = 0, ngpus: int = 0) -> None:
+def fw_solve_i32(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:
     """INT32 host solve in place (no-edge = FW_INF_I32)."""
     _check(_lib.fw_solve_i32(_addr(dist, "int32"), _addr(next, "int32"), _n_of(dist, n), block, ngpus))
 

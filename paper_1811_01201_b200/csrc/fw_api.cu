@@ -24,8 +24,13 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <map>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 using namespace fwb;
@@ -63,6 +68,7 @@ struct Nccl {
   void *h = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t *, int, const int *) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
                             cudaStream_t) = nullptr;
@@ -81,7 +87,7 @@ int load_nccl() {
 #define SYM(name)                                                                        \
   *reinterpret_cast<void **>(&g_nccl.name) = dlsym(h, "nccl" #name);                     \
   if (!g_nccl.name) return fail(FW_ENCCL, "libnccl.so.2 lacks nccl" #name);
-  SYM(GetUniqueId) SYM(CommInitRank) SYM(CommDestroy) SYM(Broadcast) SYM(AllReduce)
+  SYM(GetUniqueId) SYM(CommInitRank) SYM(CommInitAll) SYM(CommDestroy) SYM(Broadcast) SYM(AllReduce)
   SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
 #undef SYM
   g_nccl.h = h;
@@ -134,14 +140,34 @@ struct Ctx {
   void *pinned = nullptr;          // staging for pageable host buffers
   size_t pinned_bytes = 0;
   std::vector<cudaEvent_t> events;
-  ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init)
+  ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
   int rank = 0, world = 1;
+  int ngpus_max = 1;               // fw_init's limit (0 there = every visible device)
+  std::vector<Ctx *> team;         // fw_solve with ngpus > 1: one context per device, rank = device
   fw_stats stats{};
   bool has_stats = false;
 };
 
 Ctx *g_ctx = nullptr;
-int64_t g_launches = 0;   // kernels this library launched (fw_stats.kernel_launches)
+// kernels this library launched (fw_stats.kernel_launches); per host thread, so the rank
+// threads of a single-process multi-GPU solve count their own launches
+thread_local int64_t g_launches = 0;
+
+// Dynamic shared memory limits are a per-device function attribute: set once per
+// (kernel, device) — a process may drive several devices (fw_solve with ngpus > 1).
+std::mutex g_attr_mu;
+std::map<std::pair<const void *, int>, int> g_attr_done;
+
+int smem_attr(const void *fn, int bytes) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  int &have = g_attr_done[{fn, dev}];
+  if (have >= bytes) return FW_OK;
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+  return FW_OK;
+}
 
 constexpr size_t kStageBytes = 64ull << 20;  // pinned staging chunk
 // Largest initial/stored distance for which key sums stay exact (kernels header, KEY mode):
@@ -186,14 +212,7 @@ int launch_tile(dim3 grid, cudaStream_t st, T *D, int32_t *P, const TileArgs &a,
   constexpr int bytes = TileShape<TM, TN>::kBytes;
   auto kern = grid.z > 1 ? minplus_tile_kernel<T, TM, TN, MODE, true>
                          : minplus_tile_kernel<T, TM, TN, MODE, false>;
-  static bool configured = false;  // per instantiation (one device per process)
-  if (!configured) {
-    CU(cudaFuncSetAttribute(minplus_tile_kernel<T, TM, TN, MODE, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    CU(cudaFuncSetAttribute(minplus_tile_kernel<T, TM, TN, MODE, false>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    configured = true;
-  }
+  TRY(smem_attr((const void *)kern, bytes));
   kern<<<grid, kThreads, bytes, st>>>(D, P, a, maxkey);
   ++g_launches;
   CU(cudaGetLastError());
@@ -230,20 +249,13 @@ template <typename T, int BS, int MODE>
 int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int kb, int K,
                      int *maxkey) {
   const int bytes = 2 * BS * BS * (int)sizeof(T);   // row-major + transposed copy of D_KK
-  static bool configured = false;
   if (std::is_same<T, float>::value && is_key(MODE)) {   // FP32 keys: select-free variant
     auto kern = phase1_key_f32_kernel<BS>;
-    if (!configured) {
-      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      configured = true;
-    }
+    TRY(smem_attr((const void *)kern, bytes));
     kern<<<1, 1024, bytes, st>>>(reinterpret_cast<float *>(D), P, ld, r0, kb, maxkey);
   } else {
     auto kern = phase1_kernel<T, BS, MODE>;
-    if (!configured) {
-      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      configured = true;
-    }
+    TRY(smem_attr((const void *)kern, bytes));
     kern<<<1, 1024, bytes, st>>>(D, P, ld, r0, kb, K, maxkey);
   }
   ++g_launches;
@@ -626,9 +638,7 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
     const size_t rb = (size_t)n_pad * sizeof(T);
     const int use_smem = rb <= 200 * 1024;
     auto launch = [&](auto kern) -> int {
-      // every call: the three CH instantiations share this lambda's parameter type (one
-      // function-pointer type), so a "configured once" flag here would cover only one of them
-      CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      TRY(smem_attr((const void *)kern, 200 * 1024));
       for (auto &p : parts) {
         if (p.nsrc == 0) continue;
         kern<<<(unsigned)p.nsrc, 512, use_smem ? rb : 0, st>>>(p.D, Dt, p.ld, n_pad, p.row0, n,
@@ -647,8 +657,7 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
   if (path_mode >= 0) {
     const size_t row_bytes = (size_t)n * sizeof(int32_t);
     const int use_smem = row_bytes <= 200 * 1024;
-    CU(cudaFuncSetAttribute(finalize_paths_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            200 * 1024));
+    TRY(smem_attr((const void *)finalize_paths_kernel<T>, 200 * 1024));
     for (auto &p : parts) {
       if (p.nsrc == 0) continue;
       finalize_paths_kernel<T><<<(unsigned)p.nsrc, 1024, use_smem ? row_bytes : 0, st>>>(
@@ -1005,16 +1014,134 @@ int copy_d2h(Ctx &c, void *dst, const void *src, size_t bytes, cudaStream_t st) 
   return FW_OK;
 }
 
+// ---- single-process multi-GPU (fw_solve with ngpus > 1) ---------------------------------
+// One context per device (its own streams, workspaces, staging), an NCCL communicator over the
+// devices (ncclCommInitAll), and one host thread per device running the same per-rank driver
+// as the one-process-per-GPU path (solve_rows over the communicator rank's block-rows).
+int ctx_setup(Ctx *c, int dev, unsigned flags, bool lookahead) {
+  CU(cudaSetDevice(dev));
+  c->dev = dev;
+  c->flags = flags;
+  c->lookahead = lookahead;
+  CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;
+  CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi));
+  return FW_OK;
+}
+
+void ctx_release(Ctx *c) {
+  cudaSetDevice(c->dev);
+  cudaDeviceSynchronize();
+  for (Ctx *t : c->team) {
+    ctx_release(t);
+    delete t;
+  }
+  c->team.clear();
+  cudaSetDevice(c->dev);
+  if (c->comm) g_nccl.CommDestroy(c->comm);
+  c->comm = nullptr;
+  for (DevBuf *b : {&c->ws_d, &c->ws_t, &c->ws_b, &c->ws_s, &c->ws_full, &c->ws_tr, &c->user_d,
+                    &c->user_t, &c->scratch})
+    b->release();
+  if (c->pinned) cudaFreeHost(c->pinned);
+  c->pinned = nullptr;
+  c->pinned_bytes = 0;
+  for (auto e : c->events) cudaEventDestroy(e);
+  c->events.clear();
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  c->stream = c->side = nullptr;
+}
+
+int team_setup(Ctx &c, int G) {
+  if ((int)c.team.size() == G) return FW_OK;
+  for (Ctx *t : c.team) {
+    ctx_release(t);
+    delete t;
+  }
+  c.team.clear();
+  TRY(load_nccl());
+  std::vector<int> devs(G);
+  for (int d = 0; d < G; ++d) {
+    devs[d] = d;
+    Ctx *t = new Ctx();
+    c.team.push_back(t);
+    TRY(ctx_setup(t, d, c.flags, c.lookahead));
+    t->rank = d;
+    t->world = G;
+  }
+  std::vector<ncclComm_t> comms(G);
+  NC(g_nccl.CommInitAll(comms.data(), G, devs.data()));
+  for (int d = 0; d < G; ++d) c.team[d]->comm = comms[d];
+  CU(cudaSetDevice(c.dev));
+  return FW_OK;
+}
+
+// One rank of a team solve: copy its block-rows of the host matrix in, solve, copy them out.
+template <typename T>
+int team_rank_solve(Ctx &t, T *dist, int32_t *next, int64_t n, int BS) {
+  CU(cudaSetDevice(t.dev));
+  int64_t row0, nrows;
+  partition(n, t.world, t.rank, &row0, &nrows);
+  const int64_t nsrc = std::max<int64_t>(0, std::min(nrows, n - row0));
+  const size_t bytes = (size_t)nsrc * n * sizeof(T), pbytes = (size_t)nsrc * n * sizeof(int32_t);
+  TRY(t.user_d.ensure(std::max<size_t>(bytes, 16)));
+  if (next) TRY(t.user_t.ensure(std::max<size_t>(pbytes, 16)));
+  T *d = static_cast<T *>(t.user_d.p);
+  int32_t *tp = next ? static_cast<int32_t *>(t.user_t.p) : nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  if (bytes) TRY(copy_h2d(t, d, dist + row0 * n, bytes, t.stream));
+  CU(cudaStreamSynchronize(t.stream));
+  const auto t1 = std::chrono::steady_clock::now();
+  TRY(solve_rows<T>(t, d, n, tp, n, n, BS, t.stream));
+  const auto t2 = std::chrono::steady_clock::now();
+  if (bytes) TRY(copy_d2h(t, dist + row0 * n, d, bytes, t.stream));
+  if (next && pbytes) TRY(copy_d2h(t, next + row0 * n, tp, pbytes, t.stream));
+  CU(cudaStreamSynchronize(t.stream));
+  const auto t3 = std::chrono::steady_clock::now();
+  t.stats.h2d_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  t.stats.d2h_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
+  return FW_OK;
+}
+
+template <typename T>
+int solve_host_team(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, int G) {
+  TRY(team_setup(c, G));
+  std::vector<int> rc(G, FW_OK);
+  std::vector<std::string> err(G);
+  std::vector<std::thread> th;
+  for (int d = 0; d < G; ++d)
+    th.emplace_back([&, d] {
+      rc[d] = team_rank_solve<T>(*c.team[d], dist, next, n, BS);
+      if (rc[d] != FW_OK) err[d] = g_err;   // g_err is thread-local
+    });
+  for (auto &x : th) x.join();
+  cudaSetDevice(c.dev);
+  for (int d = 0; d < G; ++d)
+    if (rc[d] != FW_OK) return fail(rc[d], "rank %d (device %d): %s", d, c.team[d]->dev, err[d].c_str());
+  c.stats = c.team[0]->stats;   // rank 0's solve; host copies: the slowest rank
+  for (int d = 1; d < G; ++d) {
+    c.stats.h2d_ms = std::max(c.stats.h2d_ms, c.team[d]->stats.h2d_ms);
+    c.stats.d2h_ms = std::max(c.stats.d2h_ms, c.team[d]->stats.d2h_ms);
+    c.stats.solve_ms = std::max(c.stats.solve_ms, c.team[d]->stats.solve_ms);
+  }
+  c.has_stats = true;
+  return FW_OK;
+}
+
 template <typename T>
 int solve_host(T *dist, int32_t *next, int64_t n, int block, int ngpus) {
   int BS = 0;
   TRY(check_common(n, dist, block, &BS));
-  if (ngpus < 0 || ngpus > 1)
-    return fail(FW_EINVAL, "the host entry point solves on this process's GPU (ngpus = 0 or 1); "
-                           "multi-GPU runs one process per GPU (fw_comm_init + fw_dist_solve_*)");
   Ctx &c = *g_ctx;
+  if (ngpus == 0) ngpus = c.ngpus_max;
+  if (ngpus < 1 || ngpus > c.ngpus_max)
+    return fail(FW_EINVAL, "ngpus = %d outside [0, %d] (fw_init's ngpus_max / visible devices)", ngpus,
+                c.ngpus_max);
   if (c.comm)
     return fail(FW_ESTATE, "a multi-GPU communicator is active: use fw_dist_solve_* or fw_comm_free");
+  if (ngpus > 1) return solve_host_team<T>(c, dist, next, n, BS, ngpus);
   CU(cudaSetDevice(c.dev));
   const size_t bytes = (size_t)n * n * sizeof(T);
   TRY(c.user_d.ensure(bytes));
@@ -1077,6 +1204,7 @@ int fw_init(int ngpus_max, unsigned flags) {
     return fail(FW_EINVAL, "ngpus_max = %d but %d device(s) visible", ngpus_max, count);
   Ctx *c = new Ctx();
   c->flags = flags;
+  c->ngpus_max = ngpus_max == 0 ? count : ngpus_max;
   CU(cudaGetDevice(&c->dev));
   cudaDeviceProp prop;
   CU(cudaGetDeviceProperties(&prop, c->dev));
@@ -1098,23 +1226,8 @@ int fw_init(int ngpus_max, unsigned flags) {
 
 int fw_free(void) {
   if (!g_ctx) return FW_OK;
-  Ctx *c = g_ctx;
-  cudaDeviceSynchronize();
-  if (c->comm) g_nccl.CommDestroy(c->comm);
-  c->ws_d.release();
-  c->ws_t.release();
-  c->ws_b.release();
-  c->ws_s.release();
-  c->ws_full.release();
-  c->ws_tr.release();
-  c->user_d.release();
-  c->user_t.release();
-  c->scratch.release();
-  if (c->pinned) cudaFreeHost(c->pinned);
-  for (auto e : c->events) cudaEventDestroy(e);
-  if (c->stream) cudaStreamDestroy(c->stream);
-  if (c->side) cudaStreamDestroy(c->side);
-  delete c;
+  ctx_release(g_ctx);
+  delete g_ctx;
   g_ctx = nullptr;
   return FW_OK;
 }

@@ -107,3 +107,31 @@ def test_nccl_single_rank_communicator():
         fw.fw_free()
     np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
     assert oracle.check_paths(W, D, P)[0] == 0
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 visible GPUs")
+@pytest.mark.parametrize("kind,n,block", [("complete_int", 1000, 128), ("complete_real", 777, 64),
+                                          ("er_int", 600, 32)])
+def test_team_solve_matches_single_gpu(kind, n, block):
+    """fw_solve(..., ngpus=G): G devices of this process, block-row partition + NCCL pivot
+    broadcast (one host thread per device); integer data bitwise equal to the 1-GPU solve,
+    real data within rel 1e-5, next-hop paths valid."""
+    W = gen.generate(kind, n, 31, p=0.05, lo=1, hi=1000)
+    G = min(torch.cuda.device_count(), 4)
+    out = []
+    for g in (1, G):
+        D = W.copy()
+        P = np.empty(W.shape, dtype=np.int32)
+        fw.fw_init(0, 0)
+        try:
+            (fw.fw_solve_i32 if W.dtype == np.int32 else fw.fw_solve)(D, P, block=block, ngpus=g)
+        finally:
+            fw.fw_free()
+        out.append((D, P))
+    exact = W.dtype == np.int32 or kind == "complete_int"
+    if exact:
+        np.testing.assert_array_equal(out[0][0], out[1][0])
+    else:
+        np.testing.assert_allclose(out[1][0], out[0][0], rtol=1e-5)
+    assert oracle.check_paths(W, out[1][0], out[1][1], rtol=0.0 if exact else 1e-5)[0] == 0
