@@ -644,17 +644,18 @@ __global__ void unpad_kernel(const T *D, int64_t ld, int64_t n, T *dst, int64_t 
 // ---------------------------------------------------------------------------------
 // TAG-mode post-pass, step 1 (reading R9): for each (i,j) whose last strict improvement
 // happened in round K = tags[i][j] >= 0, find k* = the first k in block K, k not in {i,j},
-// with D[i][k] + D[k][j] <= D[i][j] over the FINAL D. Such a k exists: the improving k of
-// round K gave D[i][j], and later rounds only lowered D[i][k], D[k][j] (rounding is
-// monotone). k* is an intermediate vertex of a shortest i->j path, i.e. the paper's
+// minimising D[i][k] + D[k][j] over the FINAL D. That minimum is D[i][j] in exact arithmetic:
+// the improving k of round K reached D[i][j], later rounds only lowered D[i][k] and D[k][j],
+// and the final D satisfies the triangle inequality; with rounding the arg-min is the most
+// robust choice. k* is an intermediate vertex of a shortest i->j path, i.e. the paper's
 // "most recently added intermediate node" form of P. Overwrites tags with k*.
 //
 // One CTA per row i (row i of D staged in shared memory when it fits); one warp per element:
-// lane l tests k = kb + CH*l .. + CH-1 with one vector load of the transposed column segment
-// Dt[j][kb..kb+BS) (512 B coalesced per warp at BS = 128) and a ballot picks the first k.
-// U = 8 elements per warp iteration keep 8 independent 512-B segment loads in flight and the
-// next group's tags / D[i][j] are loaded before the current group is searched: the kernel
-// reads ~4*BS bytes per tagged element (HBM-bound: ~n^2 * 512 B at BS = 128).
+// lane l takes k = kb + CH*l .. + CH-1 with one vector load of the transposed column segment
+// Dt[j][kb..kb+BS) (512 B coalesced per warp at BS = 128); a warp min-reduction and a ballot
+// pick the first arg-min, branch-free. U = 8 elements per warp iteration keep 8 independent
+// 512-B segment loads in flight and the next group's tags are loaded before the current
+// group is searched: the kernel reads ~4*BS bytes per element (~n^2 * 512 B at BS = 128).
 
 // Dt = D^T for a rows x cols matrix (pitch ld -> pitch ldt), 32x32 shared-memory tiles.
 template <typename T>
@@ -695,76 +696,67 @@ resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t r
   using V = typename VecN<T, CH>::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *srow = reinterpret_cast<T *>(smem_raw);
-  const int64_t li = blockIdx.x, gi = row0 + li;
+  const int64_t li = blockIdx.x;
+  const int gi = (int)(row0 + li), nn = (int)n;
   const T *Drow = D + li * ld;
   int32_t *trow = tags + li * ld;
   if (use_smem) {
-    for (int64_t j = threadIdx.x; j < n_pad; j += blockDim.x) srow[j] = Drow[j];
+    for (int j = threadIdx.x; j < (int)n_pad; j += blockDim.x) srow[j] = Drow[j];
     __syncthreads();
   }
   const T *A = use_smem ? srow : Drow;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t step = (int64_t)nw * U;
+  const int step = nw * U;
   // group metadata (tags, D[i][j]) is loaded one group ahead of the segment loads
   int tg[U];
-  T dij[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const int64_t j = (int64_t)warp * U + u;
-    tg[u] = j < n ? trow[j] : -1;
-    dij[u] = j < n ? Drow[j] : (T)0;
+    const int j = warp * U + u;
+    tg[u] = j < nn ? trow[j] : -1;
   }
-  for (int64_t j0 = (int64_t)warp * U; j0 < n; j0 += step) {
-    V b[U];                                // the global segment loads, all in flight
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (tg[u] < 0) continue;           // warp-uniform
-      b[u] = *reinterpret_cast<const V *>(Dt + (j0 + u) * ldt + (int64_t)tg[u] * BS + CH * lane);
-    }
+  for (int j0 = warp * U; j0 < nn; j0 += step) {
+    V b[U];                                // the global segment loads, all in flight (padded
+#pragma unroll                             // rows/blocks exist, so untagged ones load block 0)
+    for (int u = 0; u < U; ++u)
+      b[u] = *reinterpret_cast<const V *>(Dt + (int64_t)(j0 + u) * ldt + max(tg[u], 0) * BS + CH * lane);
     int tgn[U];
-    T dijn[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + step + u;
-      tgn[u] = j < n ? trow[j] : -1;
-      dijn[u] = j < n ? Drow[j] : (T)0;
+      const int j = j0 + step + u;
+      tgn[u] = j < nn ? trow[j] : -1;
     }
     int res = -1;                          // lane u keeps the result of element u
-    bool wr = false;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (tg[u] < 0) continue;             // warp-uniform
-      const int64_t j = j0 + u;
-      const int64_t k0 = (int64_t)tg[u] * BS + CH * lane;
+      const int j = j0 + u;
+      const int k0 = max(tg[u], 0) * BS + CH * lane;
       const V a = *reinterpret_cast<const V *>(A + k0);   // row i: shared memory (or L1)
-      int first = -1;
-      T best = Num<T>::inf();
-      int bestk = -1;
+      // lane arg-min over its CH candidates, first k on ties; k = i, k = j, k >= n excluded
+      T best = Num<T>::acc_init();
+      int bk = -1;
 #pragma unroll
-      for (int c = CH - 1; c >= 0; --c) {  // descending: the last assignment is the first k
-        const int64_t k = k0 + c;
-        const bool valid = k < n && k != gi && k != j;
+      for (int c = CH - 1; c >= 0; --c) {
+        const int k = k0 + c;
         const T sum = (T)velem(a, c) + (T)velem(b[u], c);
-        if (valid && sum <= dij[u]) first = (int)k;
-        if (valid && sum <= best) { best = sum; bestk = (int)k; }
+        if (k != gi && k != j && k < nn && sum <= best) { best = sum; bk = k; }
       }
-      const unsigned m = __ballot_sync(0xffffffffu, first >= 0);
-      int ks;
-      if (m) {
-        ks = __shfl_sync(0xffffffffu, first, __ffs(m) - 1);
-      } else {   // rounding left no candidate <= D[i][j]: take the arg-min (first on ties)
-        for (int off = 16; off > 0; off >>= 1) {
-          const T ob = __shfl_down_sync(0xffffffffu, best, off);
-          const int ok = __shfl_down_sync(0xffffffffu, bestk, off);
-          if (ob < best || (ob == best && ok >= 0 && (bestk < 0 || ok < bestk))) { best = ob; bestk = ok; }
-        }
-        ks = __shfl_sync(0xffffffffu, bestk, 0);
-      }
-      if (lane == u) { res = ks; wr = true; }
+      // warp arg-min (non-negative FP32 orders like its bit pattern): min over the block K
+      // equals D[i][j] in exact arithmetic (reading R9), the first such k wins
+      const int key = bk >= 0 ? Num<T>::bits(best) : 0x7fffffff;
+      const int wmin = __reduce_min_sync(0xffffffffu, key);
+      const unsigned m = __ballot_sync(0xffffffffu, key == wmin && bk >= 0);
+      const int ks = __shfl_sync(0xffffffffu, bk, m ? __ffs(m) - 1 : 0);
+      if (lane == u) res = m ? ks : -1;
     }
-    if (wr) trow[j0 + lane] = res;
+    if (lane < U && j0 + lane < nn) {
+      // tg[lane] without dynamic register indexing
+      int t = tg[0];
 #pragma unroll
-    for (int u = 0; u < U; ++u) { tg[u] = tgn[u]; dij[u] = dijn[u]; }
+      for (int u = 1; u < U; ++u) t = lane == u ? tg[u] : t;
+      if (t >= 0) trow[j0 + lane] = res;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) tg[u] = tgn[u];
   }
 }
 
