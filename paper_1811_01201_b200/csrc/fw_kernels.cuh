@@ -691,7 +691,7 @@ template <typename T, int CH>
 __global__ void __launch_bounds__(512, 1)
 resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t row0, int64_t n,
                      int64_t n_pad, int32_t *tags, int use_smem) {
-  constexpr int U = 8;                     // elements in flight per warp (8 x 4*BS bytes)
+  constexpr int U = 16;                    // elements in flight per warp (16 x 4*BS bytes)
   constexpr int BS = 32 * CH;
   using V = typename VecN<T, CH>::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
