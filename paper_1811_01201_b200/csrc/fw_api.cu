@@ -593,15 +593,8 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
               int path_mode, int *d_flags, cudaStream_t st) {
   const int64_t n_pad = (n + 127) / 128 * 128;
   const bool nccl = tr == T_NCCL && world > 1;
-  if (is_key(mode)) {
-    for (auto &p : parts) {
-      if (p.nrows == 0) continue;
-      dim3 g((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(p.nrows, 65535));
-      decode_kernel<T><<<g, 256, 0, st>>>(p.D, p.ld, n, p.nrows);
-      ++g_launches;
-      CU(cudaGetLastError());
-    }
-  }
+  // keyed mode: keys -> distances inside finalize_paths_kernel (decode = 1); keys only exist
+  // with P (want_p), so the finalize pass always runs then
   if (mode == MODE_TAG && path_mode >= 0) {
     // the search reads column segments D[kb..kb+BS)[j] of rows wherever they live: gather the
     // final D (multi-GPU), then transpose it so each segment is one contiguous 4*BS-byte read
@@ -661,7 +654,7 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
     for (auto &p : parts) {
       if (p.nsrc == 0) continue;
       finalize_paths_kernel<T><<<(unsigned)p.nsrc, 1024, use_smem ? row_bytes : 0, st>>>(
-          p.D, p.P, p.ld, p.row0, n, path_mode == 0, use_smem, d_flags);
+          p.D, p.P, p.ld, p.row0, n, path_mode == 0, use_smem, d_flags, is_key(mode) ? 1 : 0);
       ++g_launches;
       CU(cudaGetLastError());
     }
@@ -690,10 +683,9 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   CU(cudaMemsetAsync(d_flags, 0, 16, st));
   for (auto &p : parts) {
     if (p.nsrc == 0) continue;
-    const int64_t total = p.nsrc * n;
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    validate_kernel<T><<<std::max(blocks, 1), 256, 0, st>>>(p.src, p.ld_src, p.nsrc, n, p.row0,
-                                                            d_flags, d_flags + 1);
+    const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 16)),
+                 (unsigned)std::min<int64_t>(p.nsrc, 148 * 8));
+    validate_kernel<T><<<g, 256, 0, st>>>(p.src, p.ld_src, p.nsrc, n, p.row0, d_flags, d_flags + 1);
     ++g_launches;
     CU(cudaGetLastError());
   }

@@ -562,25 +562,41 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
 //        bit 2 an off-diagonal entry is INF (no edge). maxw: max finite off-diagonal weight
 //        (INT32 value, or FP32 bit pattern — non-negative floats order like their bits).
 template <typename T>
+__device__ __forceinline__ void validate_one(T v, int &f, int &mx) {
+  if (Num<T>::bad(v)) { f |= 1; return; }
+  if (!Num<T>::finite(v)) { f |= 4; return; }
+  if (!Num<T>::kIsInt && (float)v != rintf((float)v)) f |= 2;
+  mx = max(mx, Num<T>::bits(v));
+}
+
+// Rows stride over (blockIdx.y, gridDim.y), columns over the x threads; 16-B vector loads when
+// the rows are 16-B aligned (lds % 4 == 0 and an aligned base), a scalar tail otherwise.
+template <typename T>
 __global__ void validate_kernel(const T *src, int64_t lds, int64_t nrows, int64_t n, int64_t row0,
                                 int *flags, int *maxw) {
+  using V = typename Vec4<T>::V;
   int f = 0, mx = 0;
-  const int64_t total = nrows * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / n, j = e - i * n;
-    if (row0 + i == j) continue;  // the diagonal is overwritten with 0 (R4)
-    const T v = src[i * lds + j];
-    if (Num<T>::bad(v)) { f |= 1; continue; }
-    if (!Num<T>::finite(v)) { f |= 4; continue; }
-    if (!Num<T>::kIsInt && (float)v != rintf((float)v)) f |= 2;
-    mx = max(mx, Num<T>::bits(v));
+  const bool vec = (lds % 4 == 0) && ((uintptr_t)src % 16 == 0);
+  const int64_t nv = vec ? n / 4 : 0;          // vectorised columns [0, 4 nv)
+  for (int64_t i = blockIdx.y; i < nrows; i += gridDim.y) {
+    const T *row = src + i * lds;
+    const int64_t diag = row0 + i;               // the diagonal is overwritten with 0 (R4)
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nv;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const V v = reinterpret_cast<const V *>(row)[q];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e != diag) validate_one<T>(vget(v, e), f, mx);
+    }
+    for (int64_t j = 4 * nv + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+      if (j != diag) validate_one<T>(row[j], f, mx);
   }
   f = __reduce_or_sync(0xffffffffu, f);
   mx = __reduce_max_sync(0xffffffffu, mx);
   if ((threadIdx.x & 31) == 0) {
     if (f) atomicOr(flags, f);
-    atomicMax(maxw, mx);
+    if (mx) atomicMax(maxw, mx);
   }
 }
 
@@ -611,15 +627,6 @@ __global__ void init_kernel(const S *src, int64_t lds, int64_t nsrc, int64_t n, 
       D[i * ld + j] = v;
     }
   }
-}
-
-// Key -> distance (key modes), in place over `rows` rows and columns [0, n).
-template <typename T>
-__global__ void decode_kernel(T *D, int64_t ld, int64_t n, int64_t rows) {
-  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y)
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-         j += (int64_t)gridDim.x * blockDim.x)
-      D[i * ld + j] = Num<T>::decode(D[i * ld + j]);
 }
 
 // FP32 compute -> INT32 storage in place (integer values below 2^24; +inf -> FW_INF_I32).
@@ -766,18 +773,22 @@ resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t r
 // positive weights D[i][k*] < D[i][j], so chains are acyclic. Then the sentinels:
 // next[i][i] = i, next[i][j] = -1 when D[i][j] is INF. LAST_K mode only applies the
 // sentinels (diagonal and unreachable -> -1). flags bit 3: a chain did not converge.
+// decode = 1 (keyed mode): also turns the row's keys into distances (Num<T>::decode).
 template <typename T>
 __global__ void __launch_bounds__(1024)
-finalize_paths_kernel(const T *D, int32_t *P, int64_t ld, int64_t row0, int64_t n, int next_hop,
-                      int use_smem, int *flags) {
+finalize_paths_kernel(T *D, int32_t *P, int64_t ld, int64_t row0, int64_t n, int next_hop,
+                      int use_smem, int *flags, int decode) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t li = blockIdx.x;          // local row
   const int64_t i = row0 + li;            // global row
   int32_t *row = P + li * ld;
-  const T *Drow = D + li * ld;
+  T *Drow = D + li * ld;
   if (!next_hop) {
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x)
-      if (j == i || !Num<T>::finite(Drow[j])) row[j] = -1;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      const T d = Drow[j];
+      if (decode) Drow[j] = Num<T>::decode(d);
+      if (j == i || !Num<T>::finite(d)) row[j] = -1;
+    }
     return;
   }
   int32_t *v = use_smem ? reinterpret_cast<int32_t *>(smem_raw) : row;
@@ -806,9 +817,11 @@ finalize_paths_kernel(const T *D, int32_t *P, int64_t ld, int64_t row0, int64_t 
   }
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
     const int32_t x = v[j];
+    const T d = Drow[j];
+    if (decode) Drow[j] = Num<T>::decode(d);
     int32_t out = (x & kTerm) ? (x & ~kTerm) : -1;
     if (j == i) out = (int32_t)i;
-    else if (!Num<T>::finite(Drow[j])) out = -1;
+    else if (!Num<T>::finite(d)) out = -1;
     row[j] = out;
   }
 }
