@@ -91,7 +91,12 @@ p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
   if (VAR & 32) { cpw<0>(); __syncthreads(); }
 #pragma unroll 1
   for (int ch = 0; ch < nch * ((VAR & 32) ? 8 : 1); ++ch) {
-    if (!(VAR & 32)) {
+    if ((VAR & 1024) && NS >= 3) {   // 1024: wait, barrier, then issue chunk ch+NS-1 (one barrier per chunk)
+      const int ahead = min(NS - 2, nch - 1 - ch);
+      if (ahead >= 2) cpw<2>(); else if (ahead == 1) cpw<1>(); else cpw<0>();
+      __syncthreads();
+      if (ch + NS - 1 < nch) load((ch + NS - 1) % NS, (ch + NS - 1) * BK);
+    } else if (!(VAR & 32)) {
       if (ch + NS - 1 < nch) { load((ch + NS - 1) % NS, (ch + NS - 1) * BK); cpw<NS - 1>(); }
       else {
         const int ahead = nch - 1 - ch;   // chunks already in flight beyond ch
@@ -166,7 +171,7 @@ p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
         }
       }
     }
-    if (!(VAR & 32) && !((VAR & 512) && NS >= 3)) __syncthreads();   // 512: one barrier per chunk (NS >= 3)
+    if (!(VAR & 32) && !((VAR & (512 | 1024)) && NS >= 3)) __syncthreads();   // 512/1024: one barrier per chunk
     else asm volatile("" ::: "memory");
   }
   if (VAR & 8) {   // no epilogue: keep acc live
@@ -447,12 +452,10 @@ int main() {
     CK(cudaMemcpy(Sp, sp.data(), n * n * 4, cudaMemcpyHostToDevice));
   }
   run<8, 2, 16, 16, 2, 32, 2, 3>("prod", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 3>("prod-3st", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 512 + 3>("prod-3st-1bar", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 16, 4, 512 + 3>("prod-bk16-4st-1bar", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 16, 3, 512 + 3>("prod-bk16-3st-1bar", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 512 + 8>("prod-3st-1bar-noepi", D, P, mk, n, sms, clk);
-  run<8, 1, 16, 16, 3, 32, 3, 512 + 3>("8x4-3cta-3st-1bar", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar-ok", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 16, 4, 1024 + 3>("bk16-4st-1bar-ok", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 16, 5, 1024 + 3>("bk16-5st-1bar-ok", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 1024 + 8>("3st-1bar-ok-noepi", D, P, mk, n, sms, clk);
   run<8, 2, 16, 16, 2, 32, 2, 3>("prod-again", D, P, mk, n, sms, clk);
   return 0;
 }

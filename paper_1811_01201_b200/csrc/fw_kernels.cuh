@@ -37,6 +37,7 @@ namespace fwb {
 
 constexpr int kThreads = 256;         // tile kernel: 256 threads
 constexpr int kBK = 32;               // k-chunk staged per pipeline stage
+constexpr int kStages = 3;            // cp.async pipeline depth (one barrier per chunk)
 constexpr int kTerm = 0x40000000;     // terminal bit used by the next-hop pointer jumping
 
 enum Mode { MODE_PLAIN = 0, MODE_TAG = 1, MODE_KEY = 2 };
@@ -135,7 +136,7 @@ struct TileShape {
   static constexpr int kA = TM * AS;
   static constexpr int kB = kBK * BSTR;
   static constexpr int kStage = kA + kB;
-  static constexpr int kBytes = 2 * kStage * 4;       // two stages (double buffering)
+  static constexpr int kBytes = kStages * kStage * 4;
   static constexpr int kMinBlocks = TM * TN > 128 * 128 ? 1 : (TM * TN == 128 * 128 ? 2 : 3);
   static_assert(TX * TY == kThreads && RM >= 1 && RM * TY == TM, "tile shape");
 };
@@ -181,7 +182,7 @@ __device__ __forceinline__ int skip2(int k, int x, int y) {
 // row strip (rows kb..kb+Kd of the global matrix: in D on its owner, the broadcast buffer
 // elsewhere), for the tile's (i,j), excluding rows in [mr_lo, mr_hi) and columns in [mc_lo, mc_hi)
 // (strips owned by other phases). The k dimension is streamed in chunks of kBK
-// through two shared-memory stages (cp.async 16 B): A row-major [i][k] (padded), B row-major
+// through kStages shared-memory stages (cp.async 16 B): A row-major [i][k] (padded), B row-major
 // [k][j]. In-place use (phase 2: the tile is its own A or B) is safe: a CTA reads all its
 // A/B chunks before its epilogue writes, and no other CTA writes what it reads.
 template <typename T, int TM, int TN, int MODE, bool DUAL = false>
@@ -270,18 +271,19 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
 #pragma unroll
     for (int c = 0; c < 4 * H; ++c) acc[r][c] = Num<T>::acc_init();
 
+  // kStages-deep pipeline with one barrier per chunk: after the barrier of chunk ch every warp
+  // is past chunk ch-1, so chunk ch + kStages - 1 is issued into that stage.
   const int nch = g.Kd / kBK;
-  load_chunk(0, 0);
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s)
+    if (s < nch) load_chunk(s, s * kBK);
   for (int ch = 0; ch < nch; ++ch) {
-    if (ch + 1 < nch) {
-      load_chunk((ch + 1) & 1, (ch + 1) * kBK);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    if (nch - 1 - ch >= kStages - 2) cp_async_wait<kStages - 2>();   // chunk ch has landed
+    else cp_async_wait<0>();
     __syncthreads();
-    const T *as = smem + (ch & 1) * S::kStage + ty * S::AS;
-    const T *bs = smem + (ch & 1) * S::kStage + S::kA + tx * 4;
+    if (ch + kStages - 1 < nch) load_chunk((ch + kStages - 1) % kStages, (ch + kStages - 1) * kBK);
+    const T *as = smem + (ch % kStages) * S::kStage + ty * S::AS;
+    const T *bs = smem + (ch % kStages) * S::kStage + S::kA + tx * 4;
 #pragma unroll
     for (int q = 0; q < kBK / 4; ++q) {
       V b[4][H];   // b[k][h] = B[4q+k][4tx + 4TX*h .. +3]
@@ -307,7 +309,6 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
         }
       }
     }
-    __syncthreads();
   }
 
   // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
