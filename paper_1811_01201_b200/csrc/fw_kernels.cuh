@@ -185,6 +185,62 @@ __device__ __forceinline__ int skip2(int k, int x, int y) {
 // through kStages shared-memory stages (cp.async 16 B): A row-major [i][k] (padded), B row-major
 // [k][j]. In-place use (phase 2: the tile is its own A or B) is safe: a CTA reads all its
 // A/B chunks before its epilogue writes, and no other CTA writes what it reads.
+// Tile origin (local row, global column) and excluded rows / columns of one CTA of a tile
+// launch; skip = the tile lies in an excluded strip or outside the local rows / columns.
+struct TileSlot {
+  int i0, j0, mr_lo, mr_hi, mc_lo, mc_hi;
+  bool skip;
+};
+
+template <int TM, int TN, bool DUAL>
+__device__ __forceinline__ TileSlot tile_slot(const TileArgs &g, int bxr, int byr, int bzr) {
+  TileSlot t{};
+  // select the strip description without dynamic indexing (keeps g out of local memory)
+  const bool z = DUAL && bzr != 0;
+  if (!DUAL && TM == 128 && TN == 128 && g.order) {   // ordered phase 3: the tile list above
+    int q = bxr, by, bx;
+    const int nA1 = g.rowN >= 0 ? g.tiles_c - 1 : 0;
+    const int nA2 = g.tiles_r - (g.rowK >= 0) - (g.rowN >= 0);
+    if (q < nA1) {
+      by = g.rowN;
+      bx = skip2(q, g.colK, -1);
+    } else if ((q -= nA1) < nA2) {
+      by = skip2(q, g.rowK, g.rowN);
+      bx = g.colN;
+    } else {
+      q -= nA2;
+      const int nc = g.tiles_c - 2;
+      by = skip2(q / nc, g.rowK, g.rowN);
+      bx = skip2(q % nc, g.colK, g.colN);
+    }
+    t.i0 = by * TM;
+    t.j0 = bx * TN;
+    t.skip = false;
+    return t;
+  }
+  t.mr_lo = z ? g.mr_lo[1] : g.mr_lo[0];
+  t.mr_hi = z ? g.mr_hi[1] : g.mr_hi[0];
+  t.mc_lo = z ? g.mc_lo[1] : g.mc_lo[0];
+  t.mc_hi = z ? g.mc_hi[1] : g.mc_hi[0];
+  const int xrow = z ? g.xrow[1] : g.xrow[0];
+  const int bx = xrow ? 0 : bxr, by = xrow ? bxr : byr;
+  t.i0 = (z ? g.row0[1] : g.row0[0]) + by * TM;
+  t.j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
+  t.skip = (t.i0 >= t.mr_lo && t.i0 + TM <= t.mr_hi) || (t.j0 >= t.mc_lo && t.j0 + TN <= t.mc_hi) ||
+           t.i0 >= g.rows_lim || t.j0 >= g.cols_lim;
+  return t;
+}
+
+// blockIdx through inline asm: the epilogue recomputes its tile slot instead of keeping it
+// live in registers across the main loop (the loop needs all 128).
+__device__ __forceinline__ int ctaid(int dim) {
+  int v;
+  if (dim == 0) asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(v));
+  else if (dim == 1) asm volatile("mov.u32 %0, %%ctaid.y;" : "=r"(v));
+  else asm volatile("mov.u32 %0, %%ctaid.z;" : "=r"(v));
+  return v;
+}
+
 template <typename T, int TM, int TN, int MODE, bool DUAL = false>
 __global__ void __launch_bounds__(kThreads, TileShape<TM, TN>::kMinBlocks)
 minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g, int *maxkey) {
@@ -194,40 +250,10 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *smem = reinterpret_cast<T *>(smem_raw);
 
-  // select the strip description without dynamic indexing (keeps g out of local memory);
-  // single-strip launches (phase 3) read everything straight from the parameter bank
-  const bool z = DUAL && blockIdx.z != 0;
-  int mr_lo = z ? g.mr_lo[1] : g.mr_lo[0], mr_hi = z ? g.mr_hi[1] : g.mr_hi[0];
-  int mc_lo = z ? g.mc_lo[1] : g.mc_lo[0], mc_hi = z ? g.mc_hi[1] : g.mc_hi[0];
-  int i0, j0;
-  if (!DUAL && TM == 128 && TN == 128 && g.order) {   // ordered phase 3: the tile list above
-    int t = blockIdx.x, by, bx;
-    const int nA1 = g.rowN >= 0 ? g.tiles_c - 1 : 0;
-    const int nA2 = g.tiles_r - (g.rowK >= 0) - (g.rowN >= 0);
-    if (t < nA1) {
-      by = g.rowN;
-      bx = skip2(t, g.colK, -1);
-    } else if ((t -= nA1) < nA2) {
-      by = skip2(t, g.rowK, g.rowN);
-      bx = g.colN;
-    } else {
-      t -= nA2;
-      const int nc = g.tiles_c - 2;
-      by = skip2(t / nc, g.rowK, g.rowN);
-      bx = skip2(t % nc, g.colK, g.colN);
-    }
-    i0 = by * TM;
-    j0 = bx * TN;
-    mr_lo = mr_hi = mc_lo = mc_hi = 0;
-  } else {
-    const int xrow = z ? g.xrow[1] : g.xrow[0];
-    const int bx = xrow ? 0 : blockIdx.x, by = xrow ? blockIdx.x : blockIdx.y;
-    i0 = (z ? g.row0[1] : g.row0[0]) + by * TM;
-    j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
-    if ((i0 >= mr_lo && i0 + TM <= mr_hi) || (j0 >= mc_lo && j0 + TN <= mc_hi) ||
-        i0 >= g.rows_lim || j0 >= g.cols_lim)
-      return;
-  }
+  // tile origin and exclusions (computed again after the main loop: see the epilogue)
+  const TileSlot ts = tile_slot<TM, TN, DUAL>(g, blockIdx.x, blockIdx.y, blockIdx.z);
+  if (ts.skip) return;
+  const int i0 = ts.i0, j0 = ts.j0;
 
   const int64_t ld = g.ld;
   const int kb = g.kb;
@@ -312,16 +338,18 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   }
 
   // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
-  const int kgrp = kb & ~127;
+  const TileSlot te = tile_slot<TM, TN, DUAL>(g, ctaid(0), ctaid(1), ctaid(2));
+  const int mr_lo = te.mr_lo, mr_hi = te.mr_hi, mc_lo = te.mc_lo, mc_hi = te.mc_hi;
+  const int kgrp = g.kb & ~127;
   int kmax = 0;
 #pragma unroll
   for (int r = 0; r < RM; ++r) {
-    const int i = i0 + ty + TY * r;
+    const int i = te.i0 + ty + TY * r;
     const bool row_ok = !(i >= mr_lo && i < mr_hi);
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      const int jb = j0 + 4 * tx + 4 * TX * h;
-      V *dp = reinterpret_cast<V *>(D + (int64_t)i * ld + jb);
+      const int jb = te.j0 + 4 * tx + 4 * TX * h;
+      V *dp = reinterpret_cast<V *>(D + (int64_t)i * g.ld + jb);
       const V old = *dp;
       V nv = old;
       bool any = false;
@@ -351,7 +379,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
         if (MODE != MODE_PLAIN) {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (chg[e]) P[(int64_t)i * ld + jb + e] = pv[e];
+            if (chg[e]) P[(int64_t)i * g.ld + jb + e] = pv[e];
         }
       }
     }
