@@ -158,6 +158,32 @@ p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
 #pragma unroll
         for (int r = 0; r < RM; ++r) {
           const float4 a = *reinterpret_cast<const float4 *>(as + TY * r * AS + 4 * q);
+          if (VAR & 2048) {   // scalar-reuse order: all FADD2 of a_k, then of a_k+1, then the FMNMX3s
+#pragma unroll
+            for (int kp = 0; kp < 2; ++kp) {
+              const float a0 = kp ? a.z : a.x, a1 = kp ? a.w : a.y;
+              float2 s0[H][2], s1[H][2];
+#pragma unroll
+              for (int h = 0; h < H; ++h) {
+                s0[h][0] = __fadd2_rn(make_float2(a0, a0), make_float2(b[2 * kp][h].x, b[2 * kp][h].y));
+                s0[h][1] = __fadd2_rn(make_float2(a0, a0), make_float2(b[2 * kp][h].z, b[2 * kp][h].w));
+              }
+#pragma unroll
+              for (int h = 0; h < H; ++h) {
+                s1[h][0] = __fadd2_rn(make_float2(a1, a1), make_float2(b[2 * kp + 1][h].x, b[2 * kp + 1][h].y));
+                s1[h][1] = __fadd2_rn(make_float2(a1, a1), make_float2(b[2 * kp + 1][h].z, b[2 * kp + 1][h].w));
+              }
+#pragma unroll
+              for (int h = 0; h < H; ++h) {
+                float *x = &acc[r][4 * h];
+                x[0] = fminf(x[0], fminf(s0[h][0].x, s1[h][0].x));
+                x[1] = fminf(x[1], fminf(s0[h][0].y, s1[h][0].y));
+                x[2] = fminf(x[2], fminf(s0[h][1].x, s1[h][1].x));
+                x[3] = fminf(x[3], fminf(s0[h][1].y, s1[h][1].y));
+              }
+            }
+            continue;
+          }
 #pragma unroll
           for (int h = 0; h < H; ++h) {
             float *x = &acc[r][4 * h];
@@ -451,11 +477,9 @@ int main() {
       for (int64_t j = 0; j < n; ++j) { sp[(k / 2) * 2 * n + 2 * j] = g_init[k * n + j]; sp[(k / 2) * 2 * n + 2 * j + 1] = g_init[(k + 1) * n + j]; }
     CK(cudaMemcpy(Sp, sp.data(), n * n * 4, cudaMemcpyHostToDevice));
   }
-  run<8, 2, 16, 16, 2, 32, 2, 3>("prod", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar-ok", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 16, 4, 1024 + 3>("bk16-4st-1bar-ok", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 16, 5, 1024 + 3>("bk16-5st-1bar-ok", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 1024 + 8>("3st-1bar-ok-noepi", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 2, 3>("prod-again", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 2048 + 1024 + 3>("3st-1bar-reuse", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 2048 + 1024 + 8>("3st-1bar-reuse-noepi", D, P, mk, n, sms, clk);
+  run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar-again", D, P, mk, n, sms, clk);
   return 0;
 }
