@@ -269,14 +269,37 @@ def run_gpu(args, cfg):
                 traffic = t.get("bytes_per_launch")
         except Exception:
             traffic = None
+    s0 = stats[0]
+    mode = {0: "PLAIN", 1: "TAG", 2: "KEY"}.get(s0.p_method, "?")
+    ctype = "float" if s0.compute_f32 else "int32_t"
+    # other ceilings, for context: FADD2 + FMNMX3 issue once per relaxation (2x the stated
+    # model), and the L0 probe's measured FADD2+FMNMX3 mix (profiles/r01_isa_probe.jsonl)
+    single_issue = sms * 128 * max_mhz * 1e6 * 2 / 1e12
+    mix = sms * 95.53 * max_mhz * 1e6 * 2 / 1e12
+    phase2_ms = sum(s.phase2_ms for s in stats) / len(stats)
+    p2_bytes = 2.0 * BS * ((n + 127) // 128 * 128) * 4 * s0.rounds   # both pivot strips read per round
     roof = {"bound": "alu", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
-            "traffic": traffic, "kernel": "minplus_tile_kernel<float,128,128,KEY> (phase 3, rank 0)",
+            "traffic": traffic, "kernel": f"minplus_tile_kernel<{ctype},128,128,{mode}> (phase 3, rank 0)",
             "avg_launch_ms": avg_launch_ms,
             "peak_basis": f"stated FP32 add+min issue roofline: {sms} SMs x 128 lanes x {max_mhz:.0f} MHz "
                           "(2 flop per relaxation, BASELINE north_star)",
+            "other_ceilings": {
+                "single_issue_tflops": single_issue,
+                "frac_single_issue": (achieved_tflops / single_issue) if achieved_tflops else None,
+                "measured_mix_tflops": mix,
+                "frac_measured_mix": (achieved_tflops / mix) if achieved_tflops else None,
+                "basis": "FADD2 (2 adds) + FMNMX3 (2 mins) = one issue slot per relaxation: "
+                         "SMs x 128 relax/clk; L0 probe FADD2+FMNMX3 mix 95.5 relax/clk/SM"},
+            "phase2_hbm": {"gbps": p2_bytes / (phase2_ms * 1e-3) / 1e9 if phase2_ms > 0 else None,
+                           "bytes_per_step": p2_bytes,
+                           "note": "algorithmic reads of the row and column pivot strips per round "
+                                   "(changed-element writes not counted) over the phase-2 event time; "
+                                   "phase 2 runs on the look-ahead stream under phase 3, so this "
+                                   "understates the strip kernels' own bandwidth (ncu: "
+                                   "profiles/r01b_p2_c4_ncu_summary.txt)"},
             "phase_ms_per_step": {"phase1": sum(s.phase1_ms for s in stats) / len(stats),
-                                  "phase2": sum(s.phase2_ms for s in stats) / len(stats),
+                                  "phase2": phase2_ms,
                                   "phase3": p3_ms / len(stats),
                                   "post": sum(s.post_ms for s in stats) / len(stats)}}
     launches = sum(s.kernel_launches for s in stats)
