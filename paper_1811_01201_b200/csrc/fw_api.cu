@@ -248,15 +248,13 @@ void put(TileArgs &a, int z, const Strip &s) {
 template <typename T, int BS, int MODE>
 int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int kb, int K,
                      int *maxkey) {
-  const int bytes = 2 * BS * BS * (int)sizeof(T);   // row-major + transposed copy of D_KK
+  // the tile lives in registers; shared memory holds only row / column k (static, 2 KB at BS = 128),
+  // so the CTA fits beside a phase-3 CTA on one SM (the look-ahead starts it early)
   if (std::is_same<T, float>::value && is_key(MODE)) {   // FP32 keys: select-free variant
-    auto kern = phase1_key_f32_kernel<BS>;
-    TRY(smem_attr((const void *)kern, bytes));
-    kern<<<1, 1024, bytes, st>>>(reinterpret_cast<float *>(D), P, ld, r0, kb, maxkey);
+    phase1_key_f32_kernel<BS><<<1, kP1Side * kP1Side, 0, st>>>(reinterpret_cast<float *>(D), P, ld, r0, kb,
+                                                              maxkey);
   } else {
-    auto kern = phase1_kernel<T, BS, MODE>;
-    TRY(smem_attr((const void *)kern, bytes));
-    kern<<<1, 1024, bytes, st>>>(D, P, ld, r0, kb, K, maxkey);
+    phase1_kernel<T, BS, MODE><<<1, kP1Side * kP1Side, 0, st>>>(D, P, ld, r0, kb, K, maxkey);
   }
   ++g_launches;
   CU(cudaGetLastError());

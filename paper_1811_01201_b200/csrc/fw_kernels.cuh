@@ -39,6 +39,7 @@ constexpr int kThreads = 256;         // tile kernel: 256 threads
 constexpr int kBK = 32;               // k-chunk staged per pipeline stage
 constexpr int kStages = 3;            // cp.async pipeline depth (one barrier per chunk)
 constexpr int kTerm = 0x40000000;     // terminal bit used by the next-hop pointer jumping
+constexpr int kP1Side = 16;           // phase 1: kP1Side^2 threads, (BS/kP1Side)^2 elements each
 
 enum Mode { MODE_PLAIN = 0, MODE_TAG = 1, MODE_KEY = 2 };
 __host__ __device__ constexpr bool is_key(int m) { return m == MODE_KEY; }
@@ -416,42 +417,64 @@ __global__ void wait_count_kernel(const int *done, int target) {
 // memory before the barrier, so no other element needs mirroring.
 // Key mode: candidate (d'[a][k] - (k&127)) + d'[k][b] = S*128 + (b&127) is directly the new
 // key when S < D, so min() keeps keys exact; P[a][b] <- k (last improving k) on change.
-template <typename T, int BS, int MODE>
-__global__ void __launch_bounds__(1024)
+// R consecutive values of shared memory into registers with the widest aligned vector loads.
+template <typename T, int R>
+__device__ __forceinline__ void lds_vec(T (&out)[R], const T *src) {
+  if constexpr (R % 4 == 0) {
+    using V = typename Vec4<T>::V;
+#pragma unroll
+    for (int q = 0; q < R / 4; ++q) {
+      const V v = reinterpret_cast<const V *>(src)[q];
+      out[4 * q] = v.x; out[4 * q + 1] = v.y; out[4 * q + 2] = v.z; out[4 * q + 3] = v.w;
+    }
+  } else if constexpr (R == 2) {
+    using V2 = typename std::conditional<Num<T>::kIsInt, int2, float2>::type;
+    const V2 v = *reinterpret_cast<const V2 *>(src);
+    out[0] = v.x; out[1] = v.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < R; ++q) out[q] = src[q];
+  }
+}
+
+template <typename T, int BS, int MODE, int NT = kP1Side>
+__global__ void __launch_bounds__(NT * NT)
 phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag,
               int *maxkey) {
-  constexpr int R = BS / 32;
-  using VR = typename std::conditional<R == 4, typename Vec4<T>::V,
-             typename std::conditional<R == 2, typename std::conditional<Num<T>::kIsInt, int2, float2>::type, T>::type>::type;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *sD = reinterpret_cast<T *>(smem_raw);     // row-major copy   [a][b]
-  T *sDT = sD + BS * BS;                        // transposed copy  [b][a]
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  constexpr int R = BS / NT;
+  static_assert(R % 2 == 0, "step parity = register slot parity needs an even R");
+  // row k and column k of the current step, double-buffered by step parity (2 KB at BS = 128)
+  __shared__ __align__(16) T rowb[2][BS];
+  __shared__ __align__(16) T colb[2][BS];
+  const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
   T *Dk = D + (int64_t)r0 * ld + kb;                // D_KK: local row r0, global column kb
   int32_t *Pk = P ? P + (int64_t)r0 * ld + kb : nullptr;
   T d[R][R];
   int32_t p[R][R];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int r = 0; r < R; ++r) {
+    lds_vec<T, R>(d[r], Dk + (int64_t)(R * ty + r) * ld + R * tx);   // 16-B global loads
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
-      const int a = R * ty + r, b = R * tx + c;
-      d[r][c] = Dk[(int64_t)a * ld + b];
-      sD[a * BS + b] = d[r][c];
-      sDT[b * BS + a] = d[r][c];
-      p[r][c] = -1;
-    }
+    for (int c = 0; c < R; ++c) p[r][c] = -1;
+  }
+  if (ty == 0) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) rowb[0][R * tx + c] = d[0][c];
+  }
+  if (tx == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) colb[0][R * ty + r] = d[r][0];
+  }
   __syncthreads();
   // k is unrolled by R so that "row/column k+1 lives in register slot (k+1) % R" is a
   // compile-time index (a runtime index into d[][] would spill the register array)
   for (int k0 = 0; k0 < BS; k0 += R) {
 #pragma unroll
     for (int kr = 0; kr < R; ++kr) {
-      const int k = k0 + kr;
-      const VR cv = *reinterpret_cast<const VR *>(sDT + k * BS + R * ty);   // d[a][k], own rows
-      const VR rv = *reinterpret_cast<const VR *>(sD + k * BS + R * tx);    // d[k][b], own cols
-      const T *colv = reinterpret_cast<const T *>(&cv);
-      const T *rowv = reinterpret_cast<const T *>(&rv);
+      const int k = k0 + kr, buf = kr & 1;       // R is even: k & 1 == kr & 1
+      T colv[R], rowv[R];
+      lds_vec<T, R>(colv, &colb[buf][R * ty]);   // d[a][k], own rows
+      lds_vec<T, R>(rowv, &rowb[buf][R * tx]);   // d[k][b], own cols
       const T kp = is_key(MODE) ? Num<T>::from_int((kb + k) & 127) : (T)0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -464,17 +487,18 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
           d[r][c] = s < d[r][c] ? s : d[r][c];
         }
       }
-      // publish row k+1 and column k+1 (register slot (kr+1) % R of owner ty / tx) for step k+1
+      // publish row k+1 and column k+1 (register slot (kr+1) % R of owner ty / tx) into the
+      // other buffer; everyone finished reading it before the previous barrier
       const int slot = (kr + 1) % R;   // constant after unrolling
-      const int owner = (k0 + kr + 1) / R;
+      const int owner = (k + 1) / R;
       if (k + 1 < BS) {
         if (owner == ty) {
 #pragma unroll
-          for (int c = 0; c < R; ++c) sD[(k + 1) * BS + R * tx + c] = d[slot][c];
+          for (int c = 0; c < R; ++c) rowb[buf ^ 1][R * tx + c] = d[slot][c];
         }
         if (owner == tx) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) sDT[(k + 1) * BS + R * ty + r] = d[r][slot];
+          for (int r = 0; r < R; ++r) colb[buf ^ 1][R * ty + r] = d[r][slot];
         }
       }
       __syncthreads();
@@ -498,7 +522,7 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
     }
   if (is_key(MODE)) {
     kmax = __reduce_max_sync(0xffffffffu, kmax);
-    if (tx == 0 && kmax > 0) atomicMax(maxkey, kmax);
+    if ((threadIdx.x & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
   }
 }
 
@@ -510,39 +534,41 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
 // bits — the sequential strict-< result of the paper's loop, with one FADD + one FMNMX per
 // relaxation. Row k+1 is published as D*128 (B side), column k+1 as D*128 + k' (A side), both
 // recovered as floor((x + 0.5) / 128) * 128. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
-template <int BS>
-__global__ void __launch_bounds__(1024)
+template <int BS, int NT = kP1Side>
+__global__ void __launch_bounds__(NT * NT)
 phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
                       int *maxkey) {
-  constexpr int R = BS / 32;
-  using VR = typename std::conditional<R == 4, float4, typename std::conditional<R == 2, float2, float>::type>::type;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float *sD = reinterpret_cast<float *>(smem_raw);   // row-major, B form  D*128
-  float *sDT = sD + BS * BS;                         // transposed, A form D*128 + k'
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  constexpr int R = BS / NT;
+  static_assert(R % 2 == 0, "step parity = register slot parity needs an even R");
+  __shared__ __align__(16) float rowb[2][BS];   // row k, B form  D*128        (step parity)
+  __shared__ __align__(16) float colb[2][BS];   // column k, A form D*128 + k'
+  const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
   float *Dk = D + (int64_t)r0 * ld + kb;
   const int kgrp = kb & ~127, klow = kb & 127;
   float x[R][R];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int r = 0; r < R; ++r) {
+    float key[R];
+    lds_vec<float, R>(key, Dk + (int64_t)(R * ty + r) * ld + R * tx);  // D*128 + ((kb+b)&127) or +inf
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
-      const int a = R * ty + r, b = R * tx + c;
-      const float key = Dk[(int64_t)a * ld + b];        // D*128 + ((kb + b) & 127), or +inf
-      const float base = key - (float)(klow + b);        // D*128 (+inf stays +inf)
-      x[r][c] = base - 0.5f;
-      sD[a * BS + b] = base;
-      sDT[b * BS + a] = key;
-    }
+    for (int c = 0; c < R; ++c) x[r][c] = key[c] - (float)(klow + R * tx + c) - 0.5f;   // D*128 - 0.5
+  }
+  if (ty == 0) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) rowb[0][R * tx + c] = x[0][c] + 0.5f;                      // D*128
+  }
+  if (tx == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) colb[0][R * ty + r] = x[r][0] + 0.5f + (float)klow;        // + k'
+  }
   __syncthreads();
   for (int k0 = 0; k0 < BS; k0 += R) {
 #pragma unroll
     for (int kr = 0; kr < R; ++kr) {
-      const int k = k0 + kr;
-      const VR cv = *reinterpret_cast<const VR *>(sDT + k * BS + R * ty);   // A side, own rows
-      const VR rv = *reinterpret_cast<const VR *>(sD + k * BS + R * tx);    // B side, own cols
-      const float *colv = reinterpret_cast<const float *>(&cv);
-      const float *rowv = reinterpret_cast<const float *>(&rv);
+      const int k = k0 + kr, buf = kr & 1;
+      float colv[R], rowv[R];
+      lds_vec<float, R>(colv, &colb[buf][R * ty]);   // A side, own rows
+      lds_vec<float, R>(rowv, &rowb[buf][R * tx]);   // B side, own cols
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -553,13 +579,13 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
         if (owner == ty) {
 #pragma unroll
           for (int c = 0; c < R; ++c)
-            sD[(k + 1) * BS + R * tx + c] = floorf((x[slot][c] + 0.5f) * 0.0078125f) * 128.0f;
+            rowb[buf ^ 1][R * tx + c] = floorf((x[slot][c] + 0.5f) * 0.0078125f) * 128.0f;
         }
         if (owner == tx) {
           const float kp = (float)(klow + k + 1);
 #pragma unroll
           for (int r = 0; r < R; ++r)
-            sDT[(k + 1) * BS + R * ty + r] = floorf((x[r][slot] + 0.5f) * 0.0078125f) * 128.0f + kp;
+            colb[buf ^ 1][R * ty + r] = floorf((x[r][slot] + 0.5f) * 0.0078125f) * 128.0f + kp;
         }
       }
       __syncthreads();
@@ -582,7 +608,7 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
       }
     }
   kmax = __reduce_max_sync(0xffffffffu, kmax);
-  if (tx == 0 && kmax > 0) atomicMax(maxkey, kmax);
+  if ((threadIdx.x & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
 }
 
 // ---------------------------------------------------------------------------------
