@@ -454,6 +454,169 @@ int runk(const char *tag, float *D, int32_t *P, const float *Sp, int *mk, int64_
   return 0;
 }
 
+
+// Persistent variant of the 3-stage / one-barrier 8x8 kernel: grid = 2 CTAs per SM, each CTA
+// walks tiles blockIdx.x, blockIdx.x + gridDim.x, ... and the cp.async chunk stream runs across
+// tile boundaries (the next tile's first chunks load during this tile's last chunk + epilogue).
+template <int VAR>
+__global__ void __launch_bounds__(256, 2)
+p3p(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *maxkey, int tiles) {
+  constexpr int TM = 128, TN = 128, BK = 32, NS = 3, AS = BK + 4, SA = TM * AS, SB = BK * TN, ST = SA + SB;
+  constexpr int NCH = 128 / BK, RM = 8, H = 2, TX = 16, TY = 16;
+  extern __shared__ __align__(16) float sm[];
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const int tk = kb / 128, ntc = tiles - 1;                 // tiles per dim; one excluded
+  const int my = (ntc * ntc - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;   // my tile count
+  const int total = my * NCH;
+  auto origin = [&](int i, int &i0, int &j0) {
+    const int t = blockIdx.x + i * gridDim.x;
+    int by = t / ntc, bx = t % ntc;
+    by += by >= tk;
+    bx += bx >= tk;
+    i0 = by * TM;
+    j0 = bx * TN;
+  };
+  const int a_r = tid / (BK / 4), a_c = (tid % (BK / 4)) * 4;
+  const int b_r = tid / (TN / 4), b_c = (tid % (TN / 4)) * 4;
+  const unsigned s_a = (unsigned)__cvta_generic_to_shared(sm + a_r * AS + a_c);
+  const unsigned s_b = (unsigned)__cvta_generic_to_shared(sm + SA + b_r * TN + b_c);
+  auto load = [&](int gch) {
+    int i0, j0;
+    origin(gch / NCH, i0, j0);
+    const int k0 = (gch % NCH) * BK, s = gch % NS;
+    const float *a_src = D + (int64_t)(i0 + a_r) * ld + kb + a_c + k0;
+    const float *b_src = D + (int64_t)(kb + k0 + b_r) * ld + j0 + b_c;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s_a + (s * ST + t * 32 * AS) * 4),
+                   "l"(a_src + (int64_t)t * 32 * ld) : "memory");
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s_b + (s * ST + t * 8 * TN) * 4),
+                   "l"(b_src + (int64_t)t * 8 * ld) : "memory");
+    cpc();
+  };
+  float acc[RM][4 * H];
+  if (total > 0) load(0);
+  if (total > 1) load(1);
+#pragma unroll 1
+  for (int gch = 0; gch < total; ++gch) {
+    if (gch + 1 < total) cpw<1>(); else cpw<0>();
+    __syncthreads();
+    if (gch + 2 < total) load(gch + 2);
+    const int ch = gch % NCH;
+    if (ch == 0) {
+#pragma unroll
+      for (int r = 0; r < RM; ++r)
+#pragma unroll
+        for (int c = 0; c < 4 * H; ++c) acc[r][c] = __int_as_float(0x7f800000);
+      if (VAR & 2) {
+        int i0, j0;
+        origin(gch / NCH, i0, j0);
+        for (int l = tid; l < TM * 4; l += 256)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)(i0 + l / 4) * ld + j0 + (l % 4) * 32));
+      }
+    }
+    const float *as = sm + (gch % NS) * ST + ty * AS;
+    const float *bs = sm + (gch % NS) * ST + SA + tx * 4;
+#pragma unroll
+    for (int q = 0; q < BK / 4; ++q) {
+      float4 b[4][H];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < H; ++h) b[k][h] = *reinterpret_cast<const float4 *>(bs + (4 * q + k) * TN + 4 * TX * h);
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const float4 a = *reinterpret_cast<const float4 *>(as + TY * r * AS + 4 * q);
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          float *x = &acc[r][4 * h];
+          fwb::relax2k(x[0], x[1], x[2], x[3], a.x, a.y, b[0][h], b[1][h]);
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          float *x = &acc[r][4 * h];
+          fwb::relax2k(x[0], x[1], x[2], x[3], a.z, a.w, b[2][h], b[3][h]);
+        }
+      }
+    }
+    if (ch == NCH - 1) {   // epilogue of this tile (keyed, as the library's)
+      int i0, j0;
+      origin(gch / NCH, i0, j0);
+      const int kgrp = kb & ~127;
+      int kmax = 0;
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const int i = i0 + ty + TY * r;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const int jb = j0 + 4 * tx + 4 * TX * h;
+          float4 *dp = reinterpret_cast<float4 *>(D + (int64_t)i * ld + jb);
+          const float4 old = *dp;
+          float4 nv = old;
+          bool any = false;
+          int pv[4];
+          bool chg[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = jb + e;
+            const float m = acc[r][4 * h + e];
+            chg[e] = m < fwb::vget(old, e);
+            pv[e] = 0;
+            if (chg[e]) {
+              any = true;
+              const int kk = (int)(m - (float)(j & 127)) & 127;
+              const float key = m - (float)kk;
+              kmax = max(kmax, __float_as_int(key));
+              pv[e] = kgrp + kk;
+              fwb::vset(nv, e, key);
+            }
+          }
+          if (any) {
+            *dp = nv;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (chg[e]) P[(int64_t)i * ld + jb + e] = pv[e];
+          }
+        }
+      }
+      kmax = __reduce_max_sync(0xffffffffu, kmax);
+      if ((tid & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
+    }
+  }
+}
+
+template <int VAR>
+int runp(const char *tag, float *D, int32_t *P, int *mk, int64_t n, int sms, int clk_khz, int per_sm) {
+  const int bytes = 3 * (128 * 36 + 32 * 128) * 4;
+  auto kern = p3p<VAR>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  CK(cudaMemcpy(D, g_init.data(), n * n * 4, cudaMemcpyHostToDevice));
+  const int tiles = (int)(n / 128), kb = 128 * 50;
+  const int grid = sms * per_sm;
+  for (int w = 0; w < 2; ++w) kern<<<grid, 256, bytes>>>(D, P, n, kb, mk, tiles);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int reps = 10;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) kern<<<grid, 256, bytes>>>(D, P, n, kb, mk, tiles);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  const double relax = (double)(tiles - 1) * 128 * (tiles - 1) * 128 * 128;
+  printf("{\"variant\": \"%s\", \"RM\": 8, \"H\": 2, \"TX\": 16, \"TY\": 16, \"minb\": 2, \"BK\": 32, \"NS\": 3, \"var\": %d, "
+         "\"regs\": %d, \"spill\": %d, \"occ\": %d, \"ms\": %.4f, \"relax_per_clk_sm_at_max_clock\": %.2f, \"tflops\": %.3f}\n",
+         tag, VAR, fa.numRegs, (int)fa.localSizeBytes, per_sm, ms,
+         relax / (ms * 1e-3) / (sms * (double)clk_khz * 1e3), 2 * relax / (ms * 1e-3) / 1e12);
+  fflush(stdout);
+  return 0;
+}
+
 int main() {
   int sms, clk;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -478,8 +641,9 @@ int main() {
     CK(cudaMemcpy(Sp, sp.data(), n * n * 4, cudaMemcpyHostToDevice));
   }
   run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 2048 + 1024 + 3>("3st-1bar-reuse", D, P, mk, n, sms, clk);
-  run<8, 2, 16, 16, 2, 32, 3, 2048 + 1024 + 8>("3st-1bar-reuse-noepi", D, P, mk, n, sms, clk);
+  runp<3>("persistent-3st", D, P, mk, n, sms, clk, 2);
+  runp<1>("persistent-3st-nopf", D, P, mk, n, sms, clk, 2);
   run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar-again", D, P, mk, n, sms, clk);
+  runp<3>("persistent-3st-again", D, P, mk, n, sms, clk, 2);
   return 0;
 }
