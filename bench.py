@@ -311,7 +311,7 @@ def run_gpu(args, cfg):
         host_in = torch.from_numpy(W).pin_memory()
         hD = torch.empty_like(host_in).pin_memory()
         hP = torch.empty((nrows, n), dtype=torch.int32).pin_memory()
-        ts = []
+        ts, hs = [], []
         for it in range(max(1, args.e2e_steps) + 1):
             hD.copy_(host_in)
             torch.cuda.synchronize()
@@ -329,11 +329,20 @@ def run_gpu(args, cfg):
             dt = max_over_ranks(time.perf_counter() - t0)
             if it > 0:       # the first call warms the host-side staging
                 ts.append(dt)
+                if world == 1:
+                    hs.append(fw.fw_last_stats())
         e2e = {"value": flops / statistics.median(ts) / 1e9, "unit": "GFLOPS",
                "h2d_bytes_per_step": int(n * n * 4), "d2h_bytes_per_step": int(2 * n * n * 4),
                "ms_per_step": statistics.median(ts) * 1e3,
                "path": "fw_solve (host buffers)" if world == 1 else
                        "pinned rows H2D + fw_dist_solve_device + D2H, per rank"}
+        if hs:
+            # host pipeline: chunks whose copies overlapped the solve, and the
+            # exposed copy time (before the first chunk landed / after the last one computed)
+            e2e["host_chunks"] = hs[-1].host_chunks
+            e2e["exposed_h2d_ms"] = statistics.median(s.h2d_ms for s in hs)
+            e2e["exposed_d2h_ms"] = statistics.median(s.d2h_ms for s in hs)
+            e2e["library_ms"] = statistics.median(s.solve_ms for s in hs)
     if world > 1:
         fw.fw_comm_free()
     fw.fw_free()

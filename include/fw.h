@@ -85,6 +85,10 @@ typedef struct fw_stats {
   int64_t kernel_launches; /* kernels this library launched for the solve (incl. validation) */
   int32_t compute_f32;  /* 1 = relaxations ran in FP32: FP32 data, or INT32 data whose stored
                            values are integers < 2^24 (exact in FP32)     */
+  int32_t host_chunks;  /* host entry points: row chunks whose H2D / D2H overlapped the solve
+                           (DESIGN.md §4.8); 0 = copies not overlapped. With a pipeline,
+                           h2d_ms / d2h_ms are the EXPOSED parts (until the first chunk
+                           landed / after the last chunk computed) and solve_ms the whole call */
 } fw_stats;
 
 /* Create the process-wide context. ngpus_max: the most devices one fw_solve may use,
@@ -114,6 +118,19 @@ int fw_free(void);
  * Pinned (cudaHostAlloc/registered) buffers are copied directly; pageable buffers are
  * staged through an internal pinned buffer. */
 int fw_solve(float *dist, int32_t *next, int64_t n, int block, int ngpus);
+
+/* Host pipeline of the single-GPU host entry points. When both host buffers
+ * are pinned, block = 128 and the plan needs no post-solve check (integer-valued data with a
+ * static key range, or next == NULL), the rows are split into chunks of `chunk_tiles` x 128 rows:
+ * each chunk is copied in, validated and relaxed through the rounds whose pivots exist as soon
+ * as it lands, and copied out as soon as it has finished, so the copies overlap the solve.
+ * Results: D identical to the unpipelined solve (any order of rounds per row that reads
+ * completed pivot strips gives the same distances: reading R16); P a valid next hop / last k
+ * (ties may resolve differently). Error contract unchanged (validation completes before any
+ * output is written). chunk_tiles: -1 = auto (16 tile-rows when n >= 8192, else off),
+ * 0 = off, k >= 1 = k tile-rows whenever the matrix has at least two chunks.
+ * FW_ESTATE before fw_init; FW_EINVAL for chunk_tiles < -1. */
+int fw_set_host_pipeline(int chunk_tiles);
 
 /* Host-memory solve, INT32 (no-edge = FW_INF_I32; weights in [0, FW_INF_I32]). */
 int fw_solve_i32(int32_t *dist, int32_t *next, int64_t n, int block, int ngpus);

@@ -35,6 +35,7 @@ class FwStats(ctypes.Structure):
         ("post_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
         ("phase3_launches", ctypes.c_int64), ("phase3_relaxations", ctypes.c_double),
         ("kernel_launches", ctypes.c_int64), ("compute_f32", ctypes.c_int32),
+        ("host_chunks", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -55,6 +56,7 @@ _lib.fw_init.argtypes = [_I, ctypes.c_uint]
 _lib.fw_free.argtypes = []
 _lib.fw_solve.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_solve_i32.argtypes = [_P, _P, _I64, _I, _I]
+_lib.fw_set_host_pipeline.argtypes = [_I]
 _lib.fw_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_dist_partition.argtypes = [_I64, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
@@ -118,6 +120,11 @@ def fw_solve(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:
     """FP32 host solve in place (dist: n x n float32; next: n x n int32 or None).
     ngpus: 1 = current device (default here), G > 1 = devices 0..G-1, 0 = fw_init's ngpus_max."""
     _check(_lib.fw_solve(_addr(dist, "float32"), _addr(next, "int32"), _n_of(dist, n), block, ngpus))
+
+
+def fw_set_host_pipeline(chunk_tiles: int = -1) -> None:
+    """Host-entry copy/solve pipeline: -1 auto, 0 off, k = chunks of k x 128 rows."""
+    _check(_lib.fw_set_host_pipeline(chunk_tiles))
 
 
 def fw_solve_i32(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:

@@ -140,6 +140,9 @@ struct Ctx {
   void *pinned = nullptr;          // staging for pageable host buffers
   size_t pinned_bytes = 0;
   std::vector<cudaEvent_t> events;
+  cudaStream_t copy = nullptr;     // host pipeline: H2D / D2H of row chunks
+  std::vector<cudaEvent_t> pev;    // host pipeline: per-chunk landed / finished events
+  int pipe_tiles = -1;             // host pipeline chunk in tile-rows (-1 auto, 0 off)
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
   int rank = 0, world = 1;
   int ngpus_max = 1;               // fw_init's limit (0 there = every visible device)
@@ -281,6 +284,8 @@ struct Rounds {
   int *maxkey;
   T *strip[2];   // receive buffers of the pivot row strip (world > 1)
   int *done;     // R look-ahead tile counters (zeroed per solve)
+  const T *Dg = nullptr;   // one GPU, a row range of the matrix (host pipeline): global row 0,
+                           // so the pivot strips of other rows are read in place
 
   bool owns(int K) const {
     const int64_t kb = (int64_t)K * BS;
@@ -290,7 +295,9 @@ struct Rounds {
   // B operand of round K: the pivot row strip (global rows kb..kb+BS), read in place on its
   // owner and from the broadcast buffer elsewhere
   const T *bstrip(int K) const {
-    return (world == 1 || owns(K)) ? D + (int64_t)lrow(K) * ld : strip[K & 1];
+    if (owns(K)) return D + (int64_t)lrow(K) * ld;
+    if (Dg) return Dg + (int64_t)K * BS * ld;
+    return world == 1 ? D + (int64_t)lrow(K) * ld : strip[K & 1];
   }
 
   int phase1(cudaStream_t st, int K) {
@@ -372,10 +379,14 @@ struct Rounds {
     return launch_tile<T, 128, 128, MODE>(dim3((unsigned)total, 1, 1), st, D, P, a, maxkey);
   }
 
-  int run(cudaStream_t st, const Events &e, bool lookahead) {
+  // Rounds [K0, K1) of these rows (default: all). A row range of the host pipeline runs
+  // its rounds in several calls; every round's pivot strip must have completed that round.
+  int run(cudaStream_t st, const Events &e, bool lookahead, int K0 = 0, int K1 = -1) {
     cudaEvent_t *ev = e.ev;
-    if (!lookahead || BS != 128 || R < 2) {
-      for (int K = 0; K < R; ++K) {
+    if (K1 < 0) K1 = R;
+    if (K0 >= K1) return FW_OK;
+    if (!lookahead || BS != 128 || K1 - K0 < 2) {
+      for (int K = K0; K < K1; ++K) {
         TRY(phase1(st, K));
         if (e.timing) CU(cudaEventRecord(ev[3 * K], st));
         TRY(pivot_rest(st, K));
@@ -386,14 +397,14 @@ struct Rounds {
       return FW_OK;
     }
     cudaStream_t side = c.side;
-    TRY(phase1(st, 0));
-    if (e.timing) CU(cudaEventRecord(ev[0], st));
-    TRY(pivot_rest(st, 0));
-    if (e.timing) CU(cudaEventRecord(ev[1], st));
-    CU(cudaEventRecord(e.sync[0], st));
-    CU(cudaStreamWaitEvent(side, e.sync[0], 0));      // the pivot stream follows round 0's pivot
-    for (int K = 0; K < R; ++K) {
-      if (K + 1 < R) {
+    TRY(phase1(st, K0));
+    if (e.timing) CU(cudaEventRecord(ev[3 * K0], st));
+    TRY(pivot_rest(st, K0));
+    if (e.timing) CU(cudaEventRecord(ev[3 * K0 + 1], st));
+    CU(cudaEventRecord(e.sync[2 * K0], st));
+    CU(cudaStreamWaitEvent(side, e.sync[2 * K0], 0));   // the pivot stream follows round K0's pivot
+    for (int K = K0; K < K1; ++K) {
+      if (K + 1 < K1) {
         int nprio = 0;
         TRY(phase3_ordered(st, K, done + K, &nprio));
         if (e.timing) CU(cudaEventRecord(ev[3 * K + 2], st));
@@ -529,6 +540,43 @@ int key_limit_f32() {
   int b;
   memcpy(&b, &f, 4);
   return b;
+}
+
+// Domain checks on the validation flags ([0] flags, [1] max weight bits) and the solve's plan:
+// exact arg-min keys for integer-valued data within the key range (static, or speculative and
+// verified by the max stored key), else round tags; INT32 data runs in FP32 when every value
+// it can store is an integer below 2^24 (keys: max key checked).
+int make_plan(bool int_t, bool want_p, const int *h_flags, int64_t n, std::vector<Attempt> *out) {
+  if (h_flags[0] & 1)
+    return fail(FW_EINVAL, int_t ? "weight outside [0, FW_INF_I32]" : "negative or NaN weight");
+  double maxw;
+  if (int_t) {
+    maxw = (double)h_flags[1];
+  } else {
+    float f;
+    memcpy(&f, &h_flags[1], 4);
+    maxw = f;
+  }
+  if (int_t && n > 1 && (int64_t)(n - 1) * (int64_t)h_flags[1] >= (int64_t)FW_INF_I32)
+    return fail(FW_ERANGE, "(n-1)*max_weight = %lld >= FW_INF_I32: finite path sums could reach INF",
+                (long long)(n - 1) * h_flags[1]);
+  const bool integral = int_t || !(h_flags[0] & 2);
+  const bool has_inf = (h_flags[0] & 4) != 0;
+  const double path_max = (double)(n > 1 ? n - 1 : 1) * maxw;   // bound on any finite distance
+  const bool f32_exact = int_t && path_max < 16777216.0;         // 2^24: PLAIN / TAG in FP32
+  std::vector<Attempt> &plan = *out;
+  plan.clear();
+  if (want_p && integral) {
+    if (int_t && maxw <= (double)kKeyMaxF32)
+      plan.push_back({MODE_KEY, true, !has_inf || path_max <= (double)kKeyMaxF32, key_limit_f32()});
+    const int64_t kmax = int_t ? kKeyMaxI32 : kKeyMaxF32;
+    if (maxw <= (double)kmax && !(int_t && plan.size() && plan[0].key_static))
+      plan.push_back({MODE_KEY, false, !has_inf || path_max <= (double)kmax,
+                      int_t ? (int)(kKeyMaxI32 * 128 + 127) : key_limit_f32()});
+  }
+  if (want_p && (plan.empty() || !plan.back().key_static)) plan.push_back({MODE_TAG, f32_exact, true, 0});
+  if (!want_p) plan.push_back({MODE_PLAIN, f32_exact, true, 0});
+  return FW_OK;
 }
 
 // The parts' working buffers viewed in compute type C (same 4-byte slots).
@@ -692,38 +740,8 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   int h_flags[4] = {0, 0, 0, 0};
   CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
-  if (h_flags[0] & 1)
-    return fail(FW_EINVAL, int_t ? "weight outside [0, FW_INF_I32]" : "negative or NaN weight");
-  double maxw;
-  if (int_t) {
-    maxw = (double)h_flags[1];
-  } else {
-    float f;
-    memcpy(&f, &h_flags[1], 4);
-    maxw = f;
-  }
-  if (int_t && n > 1 && (int64_t)(n - 1) * (int64_t)h_flags[1] >= (int64_t)FW_INF_I32)
-    return fail(FW_ERANGE, "(n-1)*max_weight = %lld >= FW_INF_I32: finite path sums could reach INF",
-                (long long)(n - 1) * h_flags[1]);
-
-  // 2. plan: exact arg-min keys for integer-valued data within the key range (static, or
-  //    speculative and verified by the max stored key), else round tags; INT32 data runs in
-  //    FP32 when every value it can store is an integer below 2^24 (keys: max key checked)
-  const bool integral = int_t || !(h_flags[0] & 2);
-  const bool has_inf = (h_flags[0] & 4) != 0;
-  const double path_max = (double)(n > 1 ? n - 1 : 1) * maxw;   // bound on any finite distance
-  const bool f32_exact = int_t && path_max < 16777216.0;         // 2^24: PLAIN / TAG in FP32
   std::vector<Attempt> plan;
-  if (want_p && integral) {
-    if (int_t && maxw <= (double)kKeyMaxF32)
-      plan.push_back({MODE_KEY, true, !has_inf || path_max <= (double)kKeyMaxF32, key_limit_f32()});
-    const int64_t kmax = int_t ? kKeyMaxI32 : kKeyMaxF32;
-    if (maxw <= (double)kmax && !(int_t && plan.size() && plan[0].key_static))
-      plan.push_back({MODE_KEY, false, !has_inf || path_max <= (double)kmax,
-                      int_t ? (int)(kKeyMaxI32 * 128 + 127) : key_limit_f32()});
-  }
-  if (want_p && (plan.empty() || !plan.back().key_static)) plan.push_back({MODE_TAG, f32_exact, true, 0});
-  if (!want_p) plan.push_back({MODE_PLAIN, f32_exact, true, 0});
+  TRY(make_plan(int_t, want_p, h_flags, n, &plan));
 
   // 3. placement
   if (tr == T_LOOPBACK) {
@@ -1004,6 +1022,260 @@ int copy_d2h(Ctx &c, void *dst, const void *src, size_t bytes, cudaStream_t st) 
   return FW_OK;
 }
 
+// ---- host pipeline: copies overlapped with the solve (one GPU, pinned host buffers) ----------
+// DESIGN.md §4.8, reading R16. The rows are split into chunks (tile-row boundaries
+// t_0 = 0 < t_1 < .. < t_C); chunk c holds the pivots of rounds [t_c, t_c+1) (BS = 128).
+//   arrival    c = 0..C-1: H2D + validation of chunk c on the copy stream; init and rounds
+//              [0, t_c+1) of chunk c, in order, on the compute stream. The pivots of rounds
+//              < t_c belong to earlier chunks, which completed those rounds on arrival; chunk c
+//              computes its own pivots. Each row runs its rounds in order and reads pivot
+//              strips that have completed the round: values are lengths of real paths and only
+//              decrease, so "after round K, D[i][j] <= the shortest i->j path through blocks
+//              <= K" holds as in the standard schedule.
+//   check      every chunk validated: the plan taken from chunk 0's flags must be the plan of
+//              the whole matrix, else the pipelined work is dropped and the standard solve runs
+//              (nothing has been written to the caller's buffers yet).
+//   departure  c = C-1..0: chunk c is final (its arrival did rounds < t_c+1, the steps before
+//              did every later block on it): emit its D out of place, run its P post-pass,
+//              D2H on the copy stream; meanwhile the rows [0, t_c) (one launch per round)
+//              run the rounds of block range [t_c, t_c+1), whose pivots (chunk c) are FINAL.
+//              With final pivots the remaining blocks may come in any order: on a shortest
+//              i->j path, let v be the first intermediate in a block not yet done; after the
+//              arrival D[i][v] <= |i..v| (all its intermediates lie in done blocks), and the
+//              round of v's block sets D[i][j] <= D[i][v] + D[v][j] = |i..j|. Keys / last k
+//              stay valid (D[i][j] = D[i][k] + D[k][j] on the final D, the triangle argument).
+// The last chunk departs as soon as the arrival ends; chunk 0 (small) departs last, so only
+// its copy is exposed. Chunk sizes grow geometrically so the arrival has work as soon as the
+// first chunk lands and most launches cover many tile-rows.
+struct PipeGeom {
+  int64_t n, n_pad, ld;
+  int BS, R;
+  std::vector<int> tb;   // chunk boundaries in tile-rows: tb[0] = 0 .. tb[C] = n_pad / 128
+  int nchunks() const { return (int)tb.size() - 1; }
+  int64_t rows_of(int t) const { return (int64_t)t * 128; }
+  int kend(int c) const { return (int)std::min<int64_t>(R, tb[c + 1]); }   // rounds [0, kend) on arrival
+  int64_t nsrc(int c) const {
+    return std::max<int64_t>(0, std::min<int64_t>(rows_of(tb[c + 1]), n) - rows_of(tb[c]));
+  }
+};
+
+int pipe_events(Ctx &c, size_t count) {
+  while (c.pev.size() < count) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.pev.push_back(e);
+  }
+  return FW_OK;
+}
+
+// H2D + validation of chunk ci on the copy stream; pev[ci] = landed.
+template <typename T>
+int pipe_arrive(Ctx &c, const PipeGeom &g, int ci, const T *dist_h, T *raw, int *d_flags) {
+  const int64_t r0 = g.rows_of(g.tb[ci]), nsrc = g.nsrc(ci);
+  if (nsrc > 0) {
+    CU(cudaMemcpyAsync(raw + r0 * g.n, dist_h + r0 * g.n, (size_t)nsrc * g.n * sizeof(T),
+                       cudaMemcpyHostToDevice, c.copy));
+    const dim3 gr((unsigned)std::max<int64_t>(1, std::min<int64_t>((g.n / 4 + 255) / 256, 16)),
+                  (unsigned)std::min<int64_t>(nsrc, 148 * 8));
+    validate_kernel<T><<<gr, 256, 0, c.copy>>>(raw + r0 * g.n, g.n, nsrc, g.n, r0, d_flags, d_flags + 1);
+    ++g_launches;
+    CU(cudaGetLastError());
+  }
+  CU(cudaEventRecord(c.pev[ci], c.copy));
+  return FW_OK;
+}
+
+// Everything after chunk 0's flags chose the plan `spec` (compute type C, P mode MODE).
+template <typename C, int MODE, typename T>
+int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C *D, int32_t *P,
+               int *d_flags, int *h_flags, const Attempt &spec, int path_mode, bool *fallback,
+               cudaEvent_t e_comp_end) {
+  const int NC = g.nchunks();
+  cudaStream_t st = c.stream;
+  int *d_done = d_flags + 16;
+  const Events ev{false, c.events.data() + 4, c.events.data() + 4 + 3 * (size_t)g.R};
+  const bool la = c.lookahead && g.BS == 128;
+  // rounds [K0, K1) on tile-rows [t0, t1), pivot strips read in place from the whole matrix
+  auto run = [&](int t0, int t1, int K0, int K1) -> int {
+    if (t1 <= t0 || K1 <= K0) return FW_OK;
+    const int64_t r0 = g.rows_of(t0);
+    CU(cudaMemsetAsync(d_done, 0, 4 * (size_t)g.R, st));
+    Rounds<C, MODE> rk{c, 1, D + r0 * g.ld, P ? P + r0 * g.ld : nullptr, g.ld, g.n, g.n_pad, r0,
+                       g.rows_of(t1 - t0), g.BS, g.R, d_flags + 2, {nullptr, nullptr}, d_done, D};
+    return rk.run(st, ev, la, K0, K1);
+  };
+  for (int ci = 1; ci < NC; ++ci) TRY(pipe_arrive<T>(c, g, ci, dist_h, raw, d_flags));
+  // arrival: init + rounds [0, t_c+1) of each chunk as it lands
+  for (int ci = 0; ci < NC; ++ci) {
+    const int64_t r0 = g.rows_of(g.tb[ci]);
+    CU(cudaStreamWaitEvent(st, c.pev[ci], 0));
+    TRY((run_init<C, MODE, T>(st, raw + r0 * g.n, g.n, g.nsrc(ci), g.n, r0, D + r0 * g.ld,
+                              P ? P + r0 * g.ld : nullptr, g.ld, g.rows_of(g.tb[ci + 1] - g.tb[ci]),
+                              g.n_pad)));
+    TRY(run(g.tb[ci], g.tb[ci + 1], 0, g.kend(ci)));
+  }
+  // check: the whole matrix's plan must be the speculated one
+  CU(cudaMemcpyAsync(h_flags, d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.copy));
+  CU(cudaStreamSynchronize(c.copy));
+  std::vector<Attempt> plan;
+  const int rc = make_plan(std::is_integral<T>::value, next_h != nullptr, h_flags, g.n, &plan);
+  if (rc != FW_OK || plan[0].mode != spec.mode || plan[0].f32 != spec.f32 ||
+      plan[0].key_static != spec.key_static) {
+    CU(cudaStreamSynchronize(st));
+    CU(cudaStreamSynchronize(c.side));
+    if (rc == FW_OK) *fallback = true;
+    return rc;
+  }
+  // departure: chunk c final -> post-pass, out-of-place emit, D2H; rows [0, t_c) take block c
+  TRY(smem_attr((const void *)finalize_paths_kernel<C>, 200 * 1024));
+  for (int ci = NC - 1; ci >= 0; --ci) {
+    const int64_t r0 = g.rows_of(g.tb[ci]), nsrc = g.nsrc(ci);
+    if (nsrc > 0) {
+      if (path_mode >= 0) {
+        const size_t row_bytes = (size_t)g.n * sizeof(int32_t);
+        const int use_smem = row_bytes <= 200 * 1024;
+        finalize_paths_kernel<C><<<(unsigned)nsrc, 1024, use_smem ? row_bytes : 0, st>>>(
+            D + r0 * g.ld, P + r0 * g.ld, g.ld, r0, g.n, path_mode == 0, use_smem, d_flags, 0);
+        ++g_launches;
+        CU(cudaGetLastError());
+      }
+      const dim3 gr((unsigned)std::min<int64_t>((g.n + 255) / 256, 64), (unsigned)std::min<int64_t>(nsrc, 65535));
+      emit_rows_kernel<C, T><<<gr, 256, 0, st>>>(D + r0 * g.ld, g.ld, g.n, nsrc, raw + r0 * g.n, g.n,
+                                                 is_key(MODE) ? 1 : 0);
+      ++g_launches;
+      CU(cudaGetLastError());
+      CU(cudaEventRecord(c.pev[NC + ci], st));
+      CU(cudaStreamWaitEvent(c.copy, c.pev[NC + ci], 0));
+      CU(cudaMemcpyAsync(dist_h + r0 * g.n, raw + r0 * g.n, (size_t)nsrc * g.n * sizeof(T),
+                         cudaMemcpyDeviceToHost, c.copy));
+      if (path_mode >= 0)
+        CU(cudaMemcpy2DAsync(next_h + r0 * g.n, g.n * sizeof(int32_t), P + r0 * g.ld,
+                             g.ld * sizeof(int32_t), g.n * sizeof(int32_t), nsrc, cudaMemcpyDeviceToHost,
+                             c.copy));
+    }
+    TRY(run(0, g.tb[ci], g.tb[ci], g.kend(ci)));
+  }
+  CU(cudaEventRecord(e_comp_end, st));
+  CU(cudaStreamWaitEvent(c.copy, e_comp_end, 0));
+  return FW_OK;
+}
+
+template <typename C, typename T>
+int pipe_dispatch(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, int *d_flags,
+                  int *h_flags, const Attempt &spec, int path_mode, bool *fallback, cudaEvent_t e_comp_end) {
+  C *D = static_cast<C *>(c.ws_d.p);
+  int32_t *P = path_mode >= 0 ? static_cast<int32_t *>(c.ws_t.p) : nullptr;
+  if (spec.mode == MODE_KEY)
+    return pipe_solve<C, MODE_KEY, T>(c, g, dist_h, next_h, raw, D, P, d_flags, h_flags, spec, path_mode,
+                                      fallback, e_comp_end);
+  return pipe_solve<C, MODE_PLAIN, T>(c, g, dist_h, next_h, raw, D, nullptr, d_flags, h_flags, spec,
+                                      path_mode, fallback, e_comp_end);
+}
+
+// Chunk boundaries (tile-rows) of the host pipeline; empty = no pipeline. Auto (pipe_tiles < 0):
+// at n >= 8192, chunks of 8, 8, 16, 32, .. tile-rows (doubling; the last takes the rest).
+// pipe_tiles = k > 0: uniform chunks of k tile-rows when there are at least two.
+std::vector<int> pipe_bounds(const Ctx &c, int64_t n) {
+  const int tiles = (int)((n + 127) / 128);
+  std::vector<int> tb;
+  if (c.pipe_tiles == 0) return tb;
+  if (c.pipe_tiles > 0) {
+    if (tiles < 2 * c.pipe_tiles) return tb;
+    for (int t = 0; t < tiles; t += c.pipe_tiles) tb.push_back(t);
+    tb.push_back(tiles);
+    return tb;
+  }
+  if (tiles < 64) return tb;
+  tb.push_back(0);
+  int t = 8, step = 8;
+  tb.push_back(t);
+  while (t + 2 * step < tiles) {   // the next chunk would not be the last: keep doubling
+    t += step;
+    tb.push_back(t);
+    step *= 2;
+  }
+  tb.push_back(tiles);
+  return tb;
+}
+
+// Pipelined host solve; returns FW_OK with *done = false when the standard path must run.
+template <typename T>
+int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool *done) {
+  *done = false;
+  PipeGeom g{};
+  g.tb = pipe_bounds(c, n);
+  if (g.tb.size() < 3 || BS != 128 || !is_pinned(dist) || (next && !is_pinned(next))) return FW_OK;
+  g.n = n;
+  g.n_pad = (n + 127) / 128 * 128;
+  g.ld = g.n_pad;
+  g.BS = BS;
+  g.R = (int)((n + BS - 1) / BS);
+  const int path_mode = next ? ((c.flags & FW_PATH_LAST_K) ? 1 : 0) : -1;
+  const bool want_p = next != nullptr;
+  if (!c.copy) CU(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+  TRY(c.user_d.ensure((size_t)n * n * sizeof(T)));
+  TRY(c.ws_d.ensure((size_t)g.n_pad * g.n_pad * sizeof(T)));
+  if (want_p) TRY(c.ws_t.ensure((size_t)g.n_pad * g.n_pad * sizeof(int32_t)));
+  TRY(c.scratch.ensure(64 + 4 * (size_t)g.R));
+  TRY(ensure_events(c, 4 + 3 * (size_t)g.R + 2 * (size_t)g.R));
+  TRY(pipe_events(c, 2 * (size_t)g.nchunks()));
+  T *raw = static_cast<T *>(c.user_d.p);
+  int *d_flags = static_cast<int *>(c.scratch.p);
+  cudaEvent_t e_begin = c.events[0], e_end = c.events[1], e_land0 = c.events[2], e_comp = c.events[3];
+  const int64_t launches0 = g_launches;
+
+  // chunk 0: lands, is validated, and its flags choose the plan (speculation, checked later)
+  CU(cudaEventRecord(e_begin, c.copy));
+  CU(cudaMemsetAsync(d_flags, 0, 16, c.copy));
+  TRY(pipe_arrive<T>(c, g, 0, dist, raw, d_flags));
+  CU(cudaEventRecord(e_land0, c.copy));
+  int h_flags[4] = {0, 0, 0, 0};
+  CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, c.copy));
+  CU(cudaStreamSynchronize(c.copy));
+  std::vector<Attempt> plan;
+  TRY(make_plan(std::is_integral<T>::value, want_p, h_flags, n, &plan));
+  const Attempt spec = plan[0];
+  if (spec.mode == MODE_TAG || !spec.key_static) return FW_OK;   // not pipelined: standard path
+  CU(cudaStreamWaitEvent(c.stream, e_begin, 0));
+  CU(cudaStreamWaitEvent(c.side, e_begin, 0));
+
+  bool fallback = false;
+  int rc = spec.f32 ? pipe_dispatch<float, T>(c, g, dist, next, raw, d_flags, h_flags, spec, path_mode,
+                                              &fallback, e_comp)
+                    : pipe_dispatch<T, T>(c, g, dist, next, raw, d_flags, h_flags, spec, path_mode,
+                                          &fallback, e_comp);
+  if (rc != FW_OK || fallback) return rc;
+  CU(cudaEventRecord(e_end, c.copy));
+  CU(cudaStreamSynchronize(c.copy));
+  CU(cudaMemcpy(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost));
+  if (h_flags[0] & 8)
+    return fail(FW_ERANGE, "next-hop resolution did not converge (zero-weight cycle?)");
+
+  fw_stats s{};
+  s.n = n;
+  s.n_pad = g.n_pad;
+  s.block = BS;
+  s.rounds = g.R;
+  s.is_int = std::is_integral<T>::value;
+  s.path_mode = path_mode;
+  s.p_method = spec.mode;
+  s.compute_f32 = (spec.f32 || !std::is_integral<T>::value) ? 1 : 0;
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, e_begin, e_end));
+  s.solve_ms = ms;
+  CU(cudaEventElapsedTime(&ms, e_begin, e_land0));
+  s.h2d_ms = ms;                        // exposed: until chunk 0 has landed
+  CU(cudaEventElapsedTime(&ms, e_comp, e_end));
+  s.d2h_ms = ms;                        // exposed: after the last chunk's compute
+  s.phase3_relaxations = (double)g.R * (double)(g.n_pad - BS) * (double)(g.n_pad - BS) * BS;
+  s.kernel_launches = g_launches - launches0;
+  s.host_chunks = g.nchunks();
+  c.stats = s;
+  c.has_stats = true;
+  *done = true;
+  return FW_OK;
+}
+
 // ---- single-process multi-GPU (fw_solve with ngpus > 1) ---------------------------------
 // One context per device (its own streams, workspaces, staging), an NCCL communicator over the
 // devices (ncclCommInitAll), and one host thread per device running the same per-rank driver
@@ -1039,6 +1311,10 @@ void ctx_release(Ctx *c) {
   c->pinned_bytes = 0;
   for (auto e : c->events) cudaEventDestroy(e);
   c->events.clear();
+  for (auto e : c->pev) cudaEventDestroy(e);
+  c->pev.clear();
+  if (c->copy) cudaStreamDestroy(c->copy);
+  c->copy = nullptr;
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->side) cudaStreamDestroy(c->side);
   c->stream = c->side = nullptr;
@@ -1133,6 +1409,9 @@ int solve_host(T *dist, int32_t *next, int64_t n, int block, int ngpus) {
     return fail(FW_ESTATE, "a multi-GPU communicator is active: use fw_dist_solve_* or fw_comm_free");
   if (ngpus > 1) return solve_host_team<T>(c, dist, next, n, BS, ngpus);
   CU(cudaSetDevice(c.dev));
+  bool piped = false;
+  TRY(solve_host_pipelined<T>(c, dist, next, n, BS, &piped));
+  if (piped) return FW_OK;
   const size_t bytes = (size_t)n * n * sizeof(T);
   TRY(c.user_d.ensure(bytes));
   if (next) TRY(c.user_t.ensure((size_t)n * n * sizeof(int32_t)));
@@ -1224,6 +1503,13 @@ int fw_free(void) {
 
 int fw_solve(float *dist, int32_t *next, int64_t n, int block, int ngpus) {
   return solve_host<float>(dist, next, n, block, ngpus);
+}
+
+int fw_set_host_pipeline(int chunk_tiles) {
+  if (!g_ctx) return fail(FW_ESTATE, "fw_init has not been called");
+  if (chunk_tiles < -1) return fail(FW_EINVAL, "chunk_tiles must be >= -1 (got %d)", chunk_tiles);
+  g_ctx->pipe_tiles = chunk_tiles;
+  return FW_OK;
 }
 
 int fw_solve_i32(int32_t *dist, int32_t *next, int64_t n, int block, int ngpus) {

@@ -703,6 +703,25 @@ __global__ void unpad_kernel(const T *D, int64_t ld, int64_t n, T *dst, int64_t 
       dst[i * ldd + j] = D[i * ld + j];
 }
 
+// Host pipeline (fw_api.cu): a chunk's final distances into a dense output
+// buffer (pitch ldo, n columns), out of place — the working rows stay intact because they
+// are still read as pivot strips by the rounds other chunks have left. decode: keys ->
+// distances; O = int32_t with T = float: FP32 compute back to INT32 storage (+inf -> FW_INF_I32).
+template <typename O, typename T> __device__ __forceinline__ O to_storage(T v) { return (O)v; }
+template <> __device__ __forceinline__ int32_t to_storage<int32_t, float>(float v) {
+  return v < __int_as_float(0x7f800000) ? (int32_t)v : 0x3FFFFFFF;
+}
+template <typename T, typename O>
+__global__ void emit_rows_kernel(const T *D, int64_t ld, int64_t n, int64_t rows, O *out, int64_t ldo,
+                                 int decode) {
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+      const T v = D[i * ld + j];
+      out[i * ldo + j] = to_storage<O, T>(decode ? Num<T>::decode(v) : v);
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // TAG-mode post-pass, step 1 (reading R9): for each (i,j) whose last strict improvement
 // happened in round K = tags[i][j] >= 0, find k* = the first k in block K, k not in {i,j},

@@ -1,0 +1,216 @@
+"""GPU parity of the host pipeline (reading R16): fw_solve / fw_solve_i32 with
+pinned host buffers split the rows into chunks whose H2D, rounds and D2H overlap. Against the
+CPU oracle: D bit-exact for integer data (rel 1e-5 for reals), P valid by path reconstruction;
+the speculative plan (taken from the first chunk) falls back to the standard solve when the
+whole matrix needs another plan, and validation errors still leave the outputs untouched.
+Small chunk sizes (fw_set_host_pipeline) make several chunks and ragged tails at oracle sizes.
+"""
+import numpy as np
+import pytest
+
+import apsp_inputs as gen
+import oracle
+from helpers import INF, assert_D_matches, exact_data, next_consistency
+
+pytestmark = pytest.mark.gpu
+
+fw = pytest.importorskip("paper_1811_01201_b200")
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def pinned(a: np.ndarray):
+    t = torch.from_numpy(a.copy()).pin_memory()
+    return t
+
+
+def solve_pinned(W, chunk_tiles, path="next", block=128):
+    """fw_solve on pinned host tensors with the given pipeline chunk; (D, P, stats)."""
+    flags = fw.FW_PATH_LAST_K if path == "lastk" else 0
+    hD = pinned(W)
+    hP = torch.full(W.shape, -5, dtype=torch.int32).pin_memory() if path else None
+    fw.fw_init(0, flags)
+    try:
+        fw.fw_set_host_pipeline(chunk_tiles)
+        f = fw.fw_solve_i32 if W.dtype == np.int32 else fw.fw_solve
+        f(hD, hP, block=block)
+        st = fw.fw_last_stats()
+    finally:
+        fw.fw_free()
+    return hD.numpy(), (hP.numpy() if hP is not None else None), st
+
+
+def check(W, chunk_tiles, path="next", expect_chunks=None):
+    D, P, st = solve_pinned(W, chunk_tiles, path)
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    if path:
+        bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5, mode=path)
+        assert bad == 0, f"{bad} invalid paths, first at {divmod(first, W.shape[0])}"
+    if expect_chunks is not None:
+        assert st.host_chunks == expect_chunks, st.host_chunks
+    return D, P, st
+
+
+@pytest.mark.parametrize("n,ct", [(256, 1), (300, 1), (513, 2), (777, 2), (1000, 3), (1024, 4)])
+def test_pipeline_complete_int_f32(n, ct):
+    tiles = (n + 127) // 128
+    check(gen.generate("complete_int", n, 900 + n), ct, expect_chunks=-(-tiles // ct))
+
+
+@pytest.mark.parametrize("n,ct", [(640, 1), (900, 2)])
+def test_pipeline_int32_small_weights(n, ct):
+    """INT32 data whose keys fit FP32 run through the FP32 keyed kernels in the pipeline."""
+    W = gen.generate("er_int", n, 910 + n, p=1.0, lo=1, hi=100)
+    D, P, st = check(W, ct, expect_chunks=-(-((n + 127) // 128) // ct))
+    assert st.compute_f32 == 1
+
+
+@pytest.mark.parametrize("n,ct", [(384, 1), (700, 2)])
+def test_pipeline_lastk(n, ct):
+    check(gen.generate("complete_int", n, 920 + n), ct, path="lastk",
+          expect_chunks=-(-((n + 127) // 128) // ct))
+
+
+@pytest.mark.parametrize("n,ct", [(500, 1), (1000, 2)])
+def test_pipeline_distance_only_real(n, ct):
+    """next = NULL: the PLAIN plan is always static, real weights pipeline too."""
+    check(gen.generate("complete_real", n, 930 + n), ct, path=None,
+          expect_chunks=-(-((n + 127) // 128) // ct))
+
+
+def test_pipeline_closed_form_ring():
+    """Ring + heavy chords at several chunks: D = (j - i) mod n, next = i + 1."""
+    n = 1100
+    W = np.full((n, n), np.float32(n), dtype=np.float32)
+    i = np.arange(n)
+    W[i, (i + 1) % n] = 1.0
+    D, P, st = solve_pinned(W, 2)
+    assert st.host_chunks == 5
+    ii, jj = np.meshgrid(i, i, indexing="ij")
+    np.testing.assert_array_equal(D, ((jj - ii) % n).astype(np.float32))
+    np.testing.assert_array_equal(P, np.where(ii == jj, ii, (ii + 1) % n))
+
+
+def test_pipeline_matches_standard_D():
+    """Pipelined and unpipelined host solves give bitwise-identical D on integer data."""
+    W = gen.generate("complete_int", 1280, 77)
+    D1, P1, s1 = solve_pinned(W, 2)
+    D0, P0, s0 = solve_pinned(W, 0)
+    assert s1.host_chunks == 5 and s0.host_chunks == 0
+    np.testing.assert_array_equal(D1, D0)
+    assert next_consistency(W, D1, P1, exact=True) == 0
+
+
+def test_pipeline_deterministic():
+    W = gen.generate("complete_int", 900, 78)
+    a = solve_pinned(W, 1)
+    b = solve_pinned(W, 1)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_pipeline_fallback_real_weight_late():
+    """Chunk 0 is integer-valued (keyed plan speculated) but a later chunk holds a real weight:
+    the whole matrix needs round tags, so the pipelined work is dropped and the standard
+    solve runs (host_chunks = 0); results still match the oracle."""
+    n = 700
+    W = gen.generate("complete_int", n, 940)
+    W[600, 5] = np.float32(37.25)
+    D, P, st = check(W, 1, expect_chunks=0)
+    assert st.p_method == 1
+
+
+def test_pipeline_fallback_inf_late():
+    """A no-edge entry outside chunk 0 makes the key range speculative: standard path."""
+    n = 640
+    W = gen.generate("complete_int", n, 941)
+    W[500, 3] = np.inf
+    W[500, 4] = 1000.0     # (n-1) * max_w > 65534: the key range is no longer static
+    check(W, 1, expect_chunks=0)
+
+
+def test_pipeline_not_used_for_tags():
+    """Real weights with P: round tags need the whole final D, no pipeline."""
+    check(gen.generate("complete_real", 520, 942), 1, expect_chunks=0)
+
+
+@pytest.mark.parametrize("bad", [-1.0, np.nan])
+def test_pipeline_error_in_late_chunk_leaves_outputs(bad):
+    """A negative / NaN weight in the last chunk: FW_EINVAL, dist and next untouched."""
+    n = 600
+    W = gen.generate("complete_int", n, 943)
+    W[590, 17] = bad
+    hD = pinned(W)
+    hP = torch.full(W.shape, -5, dtype=torch.int32).pin_memory()
+    fw.fw_init(0, 0)
+    try:
+        fw.fw_set_host_pipeline(1)
+        with pytest.raises(fw.FwError) as e:
+            fw.fw_solve(hD, hP, block=128)
+        assert e.value.code == fw.FW_EINVAL
+    finally:
+        fw.fw_free()
+    D = hD.numpy()
+    np.testing.assert_array_equal(np.isnan(D), np.isnan(W))
+    np.testing.assert_array_equal(D[~np.isnan(W)], W[~np.isnan(W)])
+    assert (hP.numpy() == -5).all()
+
+
+def test_pipeline_int32_erange_late():
+    """INT32: a weight in a later chunk makes (n-1)*max_w reach INF: FW_ERANGE, untouched."""
+    n = 520
+    W = gen.generate("er_int", n, 944, p=1.0, lo=1, hi=100)
+    W[515, 2] = 0x3FFFFFFF // 400
+    hD = pinned(W)
+    fw.fw_init(0, 0)
+    try:
+        fw.fw_set_host_pipeline(1)
+        with pytest.raises(fw.FwError) as e:
+            fw.fw_solve_i32(hD, None, block=128)
+        assert e.value.code == fw.FW_ERANGE
+    finally:
+        fw.fw_free()
+    np.testing.assert_array_equal(hD.numpy(), W)
+
+
+def test_pipeline_pageable_uses_standard_path():
+    W = gen.generate("complete_int", 512, 945)
+    D = W.copy()
+    P = np.empty(W.shape, np.int32)
+    fw.fw_init(0, 0)
+    try:
+        fw.fw_set_host_pipeline(1)
+        fw.fw_solve(D, P, block=128)
+        assert fw.fw_last_stats().host_chunks == 0
+    finally:
+        fw.fw_free()
+    np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+
+
+@pytest.mark.slow
+def test_pipeline_auto_c4_dijkstra_rows():
+    """C4 (n = 16384, BASELINE configs[3]) through the auto pipeline (chunks of 8, 8, 16, 32, 64
+    tile-rows):
+    Dijkstra rows from 64 seeded sources bit-exact, next-hop consistency on those rows."""
+    c = gen.CONFIGS["C4"]
+    n = c["n"]
+    W = gen.config_matrix("C4")
+    hD = torch.from_numpy(W).pin_memory()
+    hP = torch.empty((n, n), dtype=torch.int32).pin_memory()
+    fw.fw_init(0, 0)
+    try:
+        fw.fw_solve(hD, hP, block=128)
+        st = fw.fw_last_stats()
+    finally:
+        fw.fw_free()
+    assert st.host_chunks == 5
+    D, P = hD.numpy(), hP.numpy()
+    src = gen.sources(n, c["seed"])
+    np.testing.assert_array_equal(D[src].astype(np.float64), oracle.dijkstra(W, src))
+    assert next_consistency(W, D, P, exact=True, rows=src) == 0
