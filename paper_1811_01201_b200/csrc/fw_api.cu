@@ -636,7 +636,7 @@ int run_attempt(Ctx &c, std::vector<Part<T>> &parts, std::vector<Part<C>> &cv, T
 // transposing the final D); last k -> next hop and the sentinels.
 template <typename T>
 int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS, int mode,
-              int path_mode, int *d_flags, cudaStream_t st) {
+              int path_mode, int *d_flags, cudaStream_t st, bool transposed = false) {
   const int64_t n_pad = (n + 127) / 128 * 128;
   const bool nccl = tr == T_NCCL && world > 1;
   // keyed mode: keys -> distances inside finalize_paths_kernel (decode = 1); keys only exist
@@ -668,7 +668,7 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
     }
     TRY(c.ws_tr.ensure((size_t)n_pad * n_pad * sizeof(T)));
     T *Dt = static_cast<T *>(c.ws_tr.p);
-    {
+    if (!transposed) {   // host pipeline: the caller transposed the final D once for all chunks
       dim3 g((unsigned)(n_pad / 32), (unsigned)(n_pad / 32));
       transpose_kernel<T><<<g, dim3(32, 8), 0, st>>>(Dfull, ldf, n_pad, n_pad, Dt, n_pad);
       CU(cudaGetLastError());
@@ -1131,7 +1131,7 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
   for (int ci = NC - 1; ci >= 0; --ci) {
     const int64_t r0 = g.rows_of(g.tb[ci]), nsrc = g.nsrc(ci);
     if (nsrc > 0) {
-      if (path_mode >= 0) {
+      if (path_mode >= 0 && MODE != MODE_TAG) {   // TAG: P needs the whole final D (after the loop)
         const size_t row_bytes = (size_t)g.n * sizeof(int32_t);
         const int use_smem = row_bytes <= 200 * 1024;
         finalize_paths_kernel<C><<<(unsigned)nsrc, 1024, use_smem ? row_bytes : 0, st>>>(
@@ -1148,12 +1148,41 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
       CU(cudaStreamWaitEvent(c.copy, c.pev[NC + ci], 0));
       CU(cudaMemcpyAsync(dist_h + r0 * g.n, raw + r0 * g.n, (size_t)nsrc * g.n * sizeof(T),
                          cudaMemcpyDeviceToHost, c.copy));
-      if (path_mode >= 0)
+      if (path_mode >= 0 && MODE != MODE_TAG)
         CU(cudaMemcpy2DAsync(next_h + r0 * g.n, g.n * sizeof(int32_t), P + r0 * g.ld,
                              g.ld * sizeof(int32_t), g.n * sizeof(int32_t), nsrc, cudaMemcpyDeviceToHost,
                              c.copy));
     }
     TRY(run(0, g.tb[ci], g.tb[ci], g.kend(ci)));
+  }
+  if (MODE == MODE_TAG && path_mode >= 0) {
+    // round tags -> last k (reading R9: valid for any round order, the last improvement in time
+    // wrote the tag) -> next hop, on the whole final D (transposed once); per row chunk of
+    // kTagRows rows, so each chunk's P copy overlaps the next chunk's search
+    constexpr int64_t kTagRows = 2048;
+    for (int64_t r0 = 0, q = 0; r0 < g.n; r0 += kTagRows, ++q) {
+      std::vector<Part<C>> part(1);
+      part[0].D = D + r0 * g.ld;
+      part[0].P = P + r0 * g.ld;
+      part[0].ld = g.ld;
+      part[0].row0 = r0;
+      part[0].nrows = std::min<int64_t>(kTagRows, g.n_pad - r0);
+      part[0].nsrc = std::min<int64_t>(kTagRows, g.n - r0);
+      if (q == 0) {   // the transpose of the whole final D (the search reads column segments)
+        TRY(c.ws_tr.ensure((size_t)g.n_pad * g.n_pad * sizeof(C)));
+        dim3 gt((unsigned)(g.n_pad / 32), (unsigned)(g.n_pad / 32));
+        transpose_kernel<C><<<gt, dim3(32, 8), 0, st>>>(D, g.ld, g.n_pad, g.n_pad, static_cast<C *>(c.ws_tr.p),
+                                                      g.n_pad);
+        CU(cudaGetLastError());
+        ++g_launches;
+      }
+      TRY(post_pass<C>(c, part, T_LOCAL, 1, g.n, g.BS, MODE_TAG, path_mode, d_flags, st, true));
+      cudaEvent_t ev_q = c.pev[2 * NC + (q & 1)];
+      CU(cudaEventRecord(ev_q, st));
+      CU(cudaStreamWaitEvent(c.copy, ev_q, 0));
+      CU(cudaMemcpy2DAsync(next_h + r0 * g.n, g.n * sizeof(int32_t), P + r0 * g.ld, g.ld * sizeof(int32_t),
+                           g.n * sizeof(int32_t), part[0].nsrc, cudaMemcpyDeviceToHost, c.copy));
+    }
   }
   CU(cudaEventRecord(e_comp_end, st));
   CU(cudaStreamWaitEvent(c.copy, e_comp_end, 0));
@@ -1167,6 +1196,9 @@ int pipe_dispatch(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw,
   int32_t *P = path_mode >= 0 ? static_cast<int32_t *>(c.ws_t.p) : nullptr;
   if (spec.mode == MODE_KEY)
     return pipe_solve<C, MODE_KEY, T>(c, g, dist_h, next_h, raw, D, P, d_flags, h_flags, spec, path_mode,
+                                      fallback, e_comp_end);
+  if (spec.mode == MODE_TAG)
+    return pipe_solve<C, MODE_TAG, T>(c, g, dist_h, next_h, raw, D, P, d_flags, h_flags, spec, path_mode,
                                       fallback, e_comp_end);
   return pipe_solve<C, MODE_PLAIN, T>(c, g, dist_h, next_h, raw, D, nullptr, d_flags, h_flags, spec,
                                       path_mode, fallback, e_comp_end);
@@ -1218,7 +1250,7 @@ int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool
   if (want_p) TRY(c.ws_t.ensure((size_t)g.n_pad * g.n_pad * sizeof(int32_t)));
   TRY(c.scratch.ensure(64 + 4 * (size_t)g.R));
   TRY(ensure_events(c, 4 + 3 * (size_t)g.R + 2 * (size_t)g.R));
-  TRY(pipe_events(c, 2 * (size_t)g.nchunks()));
+  TRY(pipe_events(c, 2 * (size_t)g.nchunks() + 2));
   T *raw = static_cast<T *>(c.user_d.p);
   int *d_flags = static_cast<int *>(c.scratch.p);
   cudaEvent_t e_begin = c.events[0], e_end = c.events[1], e_land0 = c.events[2], e_comp = c.events[3];
@@ -1235,7 +1267,7 @@ int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool
   std::vector<Attempt> plan;
   TRY(make_plan(std::is_integral<T>::value, want_p, h_flags, n, &plan));
   const Attempt spec = plan[0];
-  if (spec.mode == MODE_TAG || !spec.key_static) return FW_OK;   // not pipelined: standard path
+  if (!spec.key_static) return FW_OK;   // speculative keys need the max-key check: standard path
   CU(cudaStreamWaitEvent(c.stream, e_begin, 0));
   CU(cudaStreamWaitEvent(c.side, e_begin, 0));
 

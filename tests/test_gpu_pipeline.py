@@ -135,9 +135,25 @@ def test_pipeline_fallback_inf_late():
     check(W, 1, expect_chunks=0)
 
 
-def test_pipeline_not_used_for_tags():
-    """Real weights with P: round tags need the whole final D, no pipeline."""
-    check(gen.generate("complete_real", 520, 942), 1, expect_chunks=0)
+@pytest.mark.parametrize("n,ct,path", [(520, 1, "next"), (700, 2, "next"), (640, 1, "lastk")])
+def test_pipeline_round_tags(n, ct, path):
+    """Real weights with P (round tags): D leaves chunk by chunk, the tag post-pass runs on the
+    whole final D after the last chunk (reading R9 holds for any round order), then P leaves."""
+    D, P, st = check(gen.generate("complete_real", n, 942 + n), ct, path=path,
+                     expect_chunks=-(-((n + 127) // 128) // ct))
+    assert st.p_method == 1
+
+
+def test_pipeline_round_tags_with_inf():
+    """Real weights with no-edge entries (unreachable pairs) through the tag pipeline."""
+    n = 600
+    W = gen.generate("complete_real", n, 950)
+    rng = np.random.default_rng(950)
+    W[rng.random((n, n)) < 0.995] = np.inf
+    np.fill_diagonal(W, 0)
+    D, P, st = check(W, 1, expect_chunks=5)
+    assert np.isinf(D).any()
+    assert ((P == -1) == np.isinf(D)).all()
 
 
 @pytest.mark.parametrize("bad", [-1.0, np.nan])
