@@ -120,8 +120,9 @@ int fw_free(void);
 int fw_solve(float *dist, int32_t *next, int64_t n, int block, int ngpus);
 
 /* Host pipeline of the single-GPU host entry points. When both host buffers
- * are pinned, block = 128 and the plan needs no post-solve check (static key range, round tags
- * for real-valued data, or next == NULL; not the speculative key run), the rows are split into chunks of `chunk_tiles` x 128 rows:
+ * are pinned and block = 128 (any plan: keys, round tags, next == NULL; a speculative key run is
+ * checked chunk by chunk before each chunk is copied out and falls back to the standard solve
+ * from the device copy of the input), the rows are split into chunks of `chunk_tiles` x 128 rows:
  * each chunk is copied in, validated and relaxed through the rounds whose pivots exist as soon
  * as it lands, and copied out as soon as it has finished, so the copies overlap the solve.
  * Results: D identical to the unpipelined solve (any order of rounds per row that reads

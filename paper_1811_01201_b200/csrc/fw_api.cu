@@ -138,6 +138,7 @@ struct Ctx {
   DevBuf user_d, user_t;           // device copies of host buffers (host entry points)
   DevBuf scratch;                  // flags / reductions
   void *pinned = nullptr;          // staging for pageable host buffers
+  int *pin_small = nullptr;        // host pipeline: per-chunk max-key snapshots (pinned)
   size_t pinned_bytes = 0;
   std::vector<cudaEvent_t> events;
   cudaStream_t copy = nullptr;     // host pipeline: H2D / D2H of row chunks
@@ -1126,7 +1127,13 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
     if (rc == FW_OK) *fallback = true;
     return rc;
   }
-  // departure: chunk c final -> post-pass, out-of-place emit, D2H; rows [0, t_c) take block c
+  // departure: chunk c final -> post-pass, out-of-place emit, D2H; rows [0, t_c) take block c.
+  // A speculative key run (keys not statically exact) is checked before each chunk leaves: the
+  // chunk's values came from sums of keys stored so far, exact iff the running max key is in
+  // range then (it only grows). Its D is emitted into a separate buffer so the input survives
+  // for the standard solve if a check fails.
+  const bool check_keys = is_key(MODE) && !spec.key_static;
+  T *out = check_keys ? static_cast<T *>(c.ws_b.p) : raw;
   TRY(smem_attr((const void *)finalize_paths_kernel<C>, 200 * 1024));
   for (int ci = NC - 1; ci >= 0; --ci) {
     const int64_t r0 = g.rows_of(g.tb[ci]), nsrc = g.nsrc(ci);
@@ -1140,20 +1147,34 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
         CU(cudaGetLastError());
       }
       const dim3 gr((unsigned)std::min<int64_t>((g.n + 255) / 256, 64), (unsigned)std::min<int64_t>(nsrc, 65535));
-      emit_rows_kernel<C, T><<<gr, 256, 0, st>>>(D + r0 * g.ld, g.ld, g.n, nsrc, raw + r0 * g.n, g.n,
+      emit_rows_kernel<C, T><<<gr, 256, 0, st>>>(D + r0 * g.ld, g.ld, g.n, nsrc, out + r0 * g.n, g.n,
                                                  is_key(MODE) ? 1 : 0);
       ++g_launches;
       CU(cudaGetLastError());
+      if (check_keys)
+        CU(cudaMemcpyAsync(c.pin_small + ci, d_flags + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
       CU(cudaEventRecord(c.pev[NC + ci], st));
+    }
+    TRY(run(0, g.tb[ci], g.tb[ci], g.kend(ci)));   // queued before the host waits on the check
+    if (nsrc > 0) {
+      if (check_keys) {
+        CU(cudaEventSynchronize(c.pev[NC + ci]));
+        if (c.pin_small[ci] > spec.key_limit) {   // a stored key left the exact range
+          CU(cudaStreamSynchronize(st));
+          CU(cudaStreamSynchronize(c.side));
+          CU(cudaStreamSynchronize(c.copy));
+          *fallback = true;
+          return FW_OK;
+        }
+      }
       CU(cudaStreamWaitEvent(c.copy, c.pev[NC + ci], 0));
-      CU(cudaMemcpyAsync(dist_h + r0 * g.n, raw + r0 * g.n, (size_t)nsrc * g.n * sizeof(T),
+      CU(cudaMemcpyAsync(dist_h + r0 * g.n, out + r0 * g.n, (size_t)nsrc * g.n * sizeof(T),
                          cudaMemcpyDeviceToHost, c.copy));
       if (path_mode >= 0 && MODE != MODE_TAG)
         CU(cudaMemcpy2DAsync(next_h + r0 * g.n, g.n * sizeof(int32_t), P + r0 * g.ld,
                              g.ld * sizeof(int32_t), g.n * sizeof(int32_t), nsrc, cudaMemcpyDeviceToHost,
                              c.copy));
     }
-    TRY(run(0, g.tb[ci], g.tb[ci], g.kend(ci)));
   }
   if (MODE == MODE_TAG && path_mode >= 0) {
     // round tags -> last k (reading R9: valid for any round order, the last improvement in time
@@ -1230,10 +1251,12 @@ std::vector<int> pipe_bounds(const Ctx &c, int64_t n) {
   return tb;
 }
 
-// Pipelined host solve; returns FW_OK with *done = false when the standard path must run.
+// Pipelined host solve; returns FW_OK with *done = false when the standard path must run, and
+// *raw_ready = true when the caller's input is then already on the device (c.user_d, n x n).
 template <typename T>
-int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool *done) {
+int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool *done, bool *raw_ready) {
   *done = false;
+  *raw_ready = false;
   PipeGeom g{};
   g.tb = pipe_bounds(c, n);
   if (g.tb.size() < 3 || BS != 128 || !is_pinned(dist) || (next && !is_pinned(next))) return FW_OK;
@@ -1267,7 +1290,18 @@ int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool
   std::vector<Attempt> plan;
   TRY(make_plan(std::is_integral<T>::value, want_p, h_flags, n, &plan));
   const Attempt spec = plan[0];
-  if (!spec.key_static) return FW_OK;   // speculative keys need the max-key check: standard path
+  if (!spec.key_static) {   // speculative keys: checked per departing chunk (pipe_solve)
+    TRY(c.ws_b.ensure((size_t)n * n * sizeof(T)));
+    if (!c.pin_small) {
+      void *p = nullptr;
+      if (cudaHostAlloc(&p, 64 * 1024, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FW_ENOMEM, "cudaHostAlloc(64 KiB) failed");
+      }
+      c.pin_small = static_cast<int *>(p);
+    }
+    if (g.nchunks() > 16 * 1024) return FW_OK;
+  }
   CU(cudaStreamWaitEvent(c.stream, e_begin, 0));
   CU(cudaStreamWaitEvent(c.side, e_begin, 0));
 
@@ -1276,7 +1310,11 @@ int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool
                                               &fallback, e_comp)
                     : pipe_dispatch<T, T>(c, g, dist, next, raw, d_flags, h_flags, spec, path_mode,
                                           &fallback, e_comp);
-  if (rc != FW_OK || fallback) return rc;
+  if (rc != FW_OK) return rc;
+  if (fallback) {   // every chunk landed and user_d still holds the input
+    *raw_ready = true;
+    return FW_OK;
+  }
   CU(cudaEventRecord(e_end, c.copy));
   CU(cudaStreamSynchronize(c.copy));
   CU(cudaMemcpy(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost));
@@ -1341,6 +1379,8 @@ void ctx_release(Ctx *c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   c->pinned = nullptr;
   c->pinned_bytes = 0;
+  if (c->pin_small) cudaFreeHost(c->pin_small);
+  c->pin_small = nullptr;
   for (auto e : c->events) cudaEventDestroy(e);
   c->events.clear();
   for (auto e : c->pev) cudaEventDestroy(e);
@@ -1441,8 +1481,8 @@ int solve_host(T *dist, int32_t *next, int64_t n, int block, int ngpus) {
     return fail(FW_ESTATE, "a multi-GPU communicator is active: use fw_dist_solve_* or fw_comm_free");
   if (ngpus > 1) return solve_host_team<T>(c, dist, next, n, BS, ngpus);
   CU(cudaSetDevice(c.dev));
-  bool piped = false;
-  TRY(solve_host_pipelined<T>(c, dist, next, n, BS, &piped));
+  bool piped = false, raw_ready = false;
+  TRY(solve_host_pipelined<T>(c, dist, next, n, BS, &piped, &raw_ready));
   if (piped) return FW_OK;
   const size_t bytes = (size_t)n * n * sizeof(T);
   TRY(c.user_d.ensure(bytes));
@@ -1453,7 +1493,8 @@ int solve_host(T *dist, int32_t *next, int64_t n, int block, int ngpus) {
   CU(cudaEventCreate(&h0));
   CU(cudaEventCreate(&h1));
   CU(cudaEventRecord(h0, c.stream));
-  int rc = copy_h2d(c, d, dist, bytes, c.stream);
+  // after a dropped pipeline the input is already on the device (and `dist` may hold rows of D)
+  int rc = raw_ready ? FW_OK : copy_h2d(c, d, dist, bytes, c.stream);
   if (rc == FW_OK) rc = (cudaEventRecord(h1, c.stream) == cudaSuccess) ? FW_OK : FW_ECUDA;
   if (rc == FW_OK) rc = solve_rows<T>(c, d, n, t, n, n, BS, c.stream);
   float h2d = 0;

@@ -230,3 +230,29 @@ def test_pipeline_auto_c4_dijkstra_rows():
     src = gen.sources(n, c["seed"])
     np.testing.assert_array_equal(D[src].astype(np.float64), oracle.dijkstra(W, src))
     assert next_consistency(W, D, P, exact=True, rows=src) == 0
+
+
+@pytest.mark.parametrize("n,p,ct", [(1000, 0.1, 1), (900, 0.003, 2)])
+def test_pipeline_speculative_keys_er_int32(n, p, ct):
+    """INT32 ER graphs with no-edge entries (BASELINE configs[2] recipe, small n): the key range
+    is only speculatively exact ((n-1) * max_w > 65534), so each chunk is checked against the
+    running max key before it leaves; here every check passes and the pipeline completes."""
+    W = gen.generate("er_int", n, 960 + n, p=p, lo=1, hi=1000)
+    D, P, st = check(W, ct, expect_chunks=-(-((n + 127) // 128) // ct))
+    assert st.p_method == 2
+    if p < 0.05:
+        assert (D == INF).any()
+
+
+def test_pipeline_speculative_keys_fail_falls_back():
+    """A ring with weight 1000 stores distances up to 999000: FP32 keys leave the exact range,
+    the first departure check fails before anything is copied out, and the standard solve runs
+    from the device copy of the input (INT32 keys): D = ((j - i) mod n) * 1000, next = i + 1."""
+    n = 1000
+    W = gen.ring(n, 1000, dtype=np.int32)
+    D, P, st = solve_pinned(W, 1)
+    assert st.host_chunks == 0 and st.p_method == 2
+    i = np.arange(n)
+    ii, jj = np.meshgrid(i, i, indexing="ij")
+    np.testing.assert_array_equal(D.astype(np.int64), ((jj - ii) % n) * 1000)
+    np.testing.assert_array_equal(P, np.where(ii == jj, ii, (ii + 1) % n))
