@@ -6,10 +6,10 @@ O=gpurun_out/ev
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/gpu.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
-timeout 900 python bench.py > $O/bench_c4.json 2> $O/bench_c4.err
+timeout 900 python bench.py --e2e-steps 3 > $O/bench_c4.json 2> $O/bench_c4.err
 timeout 900 python bench.py --config C5 --no-cpu > $O/bench_c5.json 2> $O/bench_c5.err
-timeout 600 python bench.py --config C3 --no-cpu > $O/bench_c3.json 2> $O/bench_c3.err
-timeout 600 python bench.py --config C2 --no-cpu > $O/bench_c2.json 2> $O/bench_c2.err
+timeout 600 python bench.py --config C3 --no-cpu --e2e-steps 3 > $O/bench_c3.json 2> $O/bench_c3.err
+timeout 600 python bench.py --config C2 --no-cpu --e2e-steps 3 > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 1200 python bench.py --n 65536 --steps 1 --warmup 1 --no-e2e --no-cpu > $O/bench_n65536.json 2> $O/bench_n65536.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches_c4.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > $O/ncu_list.log 2>&1
 python tools/launch_summary.py $O/launches_c4.csv > $O/launches_c4_summary.txt 2>&1
