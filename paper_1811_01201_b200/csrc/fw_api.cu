@@ -257,7 +257,10 @@ int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int 
   if (std::is_same<T, float>::value && is_key(MODE)) {   // FP32 keys: select-free variant
     phase1_key_f32_kernel<BS><<<1, kP1Side * kP1Side, 0, st>>>(reinterpret_cast<float *>(D), P, ld, r0, kb,
                                                               maxkey);
-  } else {
+  } else if (!is_key(MODE)) {                             // PLAIN / TAG: two steps per barrier
+    phase1_pair_kernel<T, BS, is_key(MODE) ? MODE_PLAIN : MODE><<<1, kP1Side * kP1Side, 0, st>>>(D, P, ld, r0,
+                                                                                               kb, K);
+  } else {                                                // INT32 keys: per-step P select
     phase1_kernel<T, BS, MODE><<<1, kP1Side * kP1Side, 0, st>>>(D, P, ld, r0, kb, K, maxkey);
   }
   ++g_launches;

@@ -407,6 +407,25 @@ __global__ void wait_count_kernel(const int *done, int target) {
   }
 }
 
+// Phase 1, two steps per barrier: columns c, c+1 of one row relaxed through k and k+1
+// (candidates a0 + b0*, a1 + b1*): FADD2 + FMNMX3 (FP32) or VIADDMNMX (INT32).
+__device__ __forceinline__ void relax_pair2(float &x0, float &x1, float a0, float a1, float b00, float b01,
+                                            float b10, float b11) {
+  const float2 s0 = __fadd2_rn(make_float2(a0, a0), make_float2(b00, b01));
+  const float2 s1 = __fadd2_rn(make_float2(a1, a1), make_float2(b10, b11));
+  x0 = fminf(x0, fminf(s0.x, s1.x));
+  x1 = fminf(x1, fminf(s0.y, s1.y));
+}
+__device__ __forceinline__ void relax_pair2(int &x0, int &x1, int a0, int a1, int b00, int b01, int b10,
+                                            int b11) {
+  x0 = __viaddmin_s32(a0, b00, x0);
+  x0 = __viaddmin_s32(a1, b10, x0);
+  x1 = __viaddmin_s32(a0, b01, x1);
+  x1 = __viaddmin_s32(a1, b11, x1);
+}
+__device__ __forceinline__ float tmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ int tmin(int a, int b) { return min(a, b); }
+
 // ---------------------------------------------------------------------------------
 // Phase 1: closure of the diagonal block D_KK in shared memory. For each k of the
 // block in order: d[a][b] = min(d[a][b], d[a][k] + d[k][b]) (strict '<'). Row k and column k
@@ -526,6 +545,85 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
   }
 }
 
+// Phase 1 for PLAIN / TAG (no per-step P), two steps per barrier: row / column k+1 are brought
+// to their state after step k by every thread (col'[a] = min(col_k1[a], col_k[a] + D[k][k+1]),
+// row'[b] = min(row_k1[b], D[k+1][k] + row_k[b])), then x = min(x, c_k, c'_k+1) — exactly the
+// sequential loop's values (min is exact; each candidate is the same single rounded sum).
+template <typename T, int BS, int MODE, int NT = kP1Side>
+__global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
+phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {
+  constexpr int R = BS / NT;
+  static_assert(R % 2 == 0 && !is_key(MODE), "pairs of steps; keyed modes use their own kernels");
+  using T2 = typename std::conditional<Num<T>::kIsInt, int2, float2>::type;
+  __shared__ __align__(16) T rowb[2][2][BS];   // rows k, k+1 (pair parity)
+  __shared__ __align__(16) T2 colb[2][BS];     // (column k, column k+1) per row
+  const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
+  T *Dk = D + (int64_t)r0 * ld + kb;
+  T d[R][R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) lds_vec<T, R>(d[r], Dk + (int64_t)(R * ty + r) * ld + R * tx);
+  if (ty == 0) {
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      rowb[0][0][R * tx + c] = d[0][c];
+      rowb[0][1][R * tx + c] = d[1][c];
+    }
+  }
+  if (tx == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) colb[0][R * ty + r] = T2{d[r][0], d[r][1]};
+  }
+  __syncthreads();
+  for (int k0 = 0; k0 < BS; k0 += R) {
+#pragma unroll
+    for (int kr = 0; kr < R; kr += 2) {
+      const int k = k0 + kr, buf = (k >> 1) & 1;
+      T rk[R], rk1[R];
+      lds_vec<T, R>(rk, &rowb[buf][0][R * tx]);
+      lds_vec<T, R>(rk1, &rowb[buf][1][R * tx]);
+      const T d01 = rowb[buf][0][k + 1];   // D[k][k+1]
+      const T d10 = colb[buf][k + 1].x;    // D[k+1][k]
+#pragma unroll
+      for (int c = 0; c < R; ++c) rk1[c] = tmin(rk1[c], d10 + rk[c]);   // INT32: <= 2 INF, no overflow
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const T2 ca = colb[buf][R * ty + r];
+        const T ck1 = tmin(ca.y, ca.x + d01);
+#pragma unroll
+        for (int c = 0; c < R; c += 2)
+          relax_pair2(d[r][c], d[r][c + 1], ca.x, ck1, rk[c], rk[c + 1], rk1[c], rk1[c + 1]);
+      }
+      if (k + 2 < BS) {
+        const int s2 = (kr + 2) % R, s3 = (kr + 3) % R;
+        const int owner = (k + 2) / R;
+        if (owner == ty) {
+#pragma unroll
+          for (int c = 0; c < R; ++c) {
+            rowb[buf ^ 1][0][R * tx + c] = d[s2][c];
+            rowb[buf ^ 1][1][R * tx + c] = d[s3][c];
+          }
+        }
+        if (owner == tx) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) colb[buf ^ 1][R * ty + r] = T2{d[r][s2], d[r][s3]};
+        }
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      const int a = R * ty + r, b = R * tx + c;
+      const int64_t off = (int64_t)a * ld + b;
+      if (d[r][c] < Dk[off]) {
+        Dk[off] = d[r][c];
+        if (MODE == MODE_TAG) P[(int64_t)(r0 + a) * ld + kb + b] = tag;
+      }
+    }
+}
+
 // Phase 1, FP32 keyed mode, without a per-relaxation select for P. The running value of
 // (a, b) is kept in the form  x = D*128 - 0.5  while unchanged, and a candidate through k is
 // the integer  c_k = D[a][k]*128 + k' + D[k][b]*128  (k' = (kb + k) & 127, increasing in k
@@ -535,13 +633,13 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
 // relaxation. Row k+1 is published as D*128 (B side), column k+1 as D*128 + k' (A side), both
 // recovered as floor((x + 0.5) / 128) * 128. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
 template <int BS, int NT = kP1Side>
-__global__ void __launch_bounds__(NT * NT)
+__global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
 phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
                       int *maxkey) {
   constexpr int R = BS / NT;
   static_assert(R % 2 == 0, "step parity = register slot parity needs an even R");
-  __shared__ __align__(16) float rowb[2][BS];   // row k, B form  D*128        (step parity)
-  __shared__ __align__(16) float colb[2][BS];   // column k, A form D*128 + k'
+  __shared__ __align__(16) float rowb[2][2][BS];   // rows k, k+1, B form D*128  (pair parity)
+  __shared__ __align__(16) float2 colb[2][BS];     // (column k, column k+1) per row, A form D*128 + k'
   const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
   float *Dk = D + (int64_t)r0 * ld + kb;
   const int kgrp = kb & ~127, klow = kb & 127;
@@ -553,39 +651,61 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
 #pragma unroll
     for (int c = 0; c < R; ++c) x[r][c] = key[c] - (float)(klow + R * tx + c) - 0.5f;   // D*128 - 0.5
   }
+  // steps k and k+1 per barrier (the sequential loop's values, two steps at a time): every
+  // thread brings row / column k+1 to their state after step k itself,
+  //   col'[a] = min(col_k1[a], col_k[a] + D[k][k+1]*128 + 1)   ((k+1)' = k' + 1 inside the block)
+  //   row'[b] = min(row_k1[b], D[k+1][k]*128 + row_k[b])
+  // and folds both candidates into x with FADD2 + FMNMX3: x = min(x, c_k, c'_k+1) (min is exact,
+  // every candidate is the same integer sum as in the one-step loop).
   if (ty == 0) {
 #pragma unroll
-    for (int c = 0; c < R; ++c) rowb[0][R * tx + c] = x[0][c] + 0.5f;                      // D*128
+    for (int c = 0; c < R; ++c) {
+      rowb[0][0][R * tx + c] = x[0][c] + 0.5f;                           // D*128
+      rowb[0][1][R * tx + c] = x[1][c] + 0.5f;
+    }
   }
   if (tx == 0) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) colb[0][R * ty + r] = x[r][0] + 0.5f + (float)klow;        // + k'
+    for (int r = 0; r < R; ++r)                                          // + k'
+      colb[0][R * ty + r] = make_float2(x[r][0] + 0.5f + (float)klow, x[r][1] + 0.5f + (float)(klow + 1));
   }
   __syncthreads();
   for (int k0 = 0; k0 < BS; k0 += R) {
 #pragma unroll
-    for (int kr = 0; kr < R; ++kr) {
-      const int k = k0 + kr, buf = kr & 1;
-      float colv[R], rowv[R];
-      lds_vec<float, R>(colv, &colb[buf][R * ty]);   // A side, own rows
-      lds_vec<float, R>(rowv, &rowb[buf][R * tx]);   // B side, own cols
+    for (int kr = 0; kr < R; kr += 2) {
+      const int k = k0 + kr, buf = (k >> 1) & 1;
+      float rk[R], rk1[R];
+      lds_vec<float, R>(rk, &rowb[buf][0][R * tx]);    // B side, own cols
+      lds_vec<float, R>(rk1, &rowb[buf][1][R * tx]);
+      const float d01 = rowb[buf][0][k + 1] + 1.0f;              // D[k][k+1]*128 + 1
+      const float d10 = colb[buf][k + 1].x - (float)(klow + k);  // D[k+1][k]*128 (exact; inf stays)
 #pragma unroll
-      for (int r = 0; r < R; ++r)
+      for (int c = 0; c < R; ++c) rk1[c] = fminf(rk1[c], d10 + rk[c]);
 #pragma unroll
-        for (int c = 0; c < R; ++c) x[r][c] = fminf(x[r][c], colv[r] + rowv[c]);
-      const int slot = (kr + 1) % R;
-      const int owner = (k + 1) / R;
-      if (k + 1 < BS) {
+      for (int r = 0; r < R; ++r) {
+        const float2 ca = colb[buf][R * ty + r];                 // A side, own row (broadcast)
+        const float ck1 = fminf(ca.y, ca.x + d01);
+#pragma unroll
+        for (int c = 0; c < R; c += 2)
+          relax_pair2(x[r][c], x[r][c + 1], ca.x, ck1, rk[c], rk[c + 1], rk1[c], rk1[c + 1]);
+      }
+      // publish rows / columns k+2 and k+3 (register slots (kr+2)%R, (kr+3)%R of one owner)
+      if (k + 2 < BS) {
+        const int s2 = (kr + 2) % R, s3 = (kr + 3) % R;
+        const int owner = (k + 2) / R;
         if (owner == ty) {
 #pragma unroll
-          for (int c = 0; c < R; ++c)
-            rowb[buf ^ 1][R * tx + c] = floorf((x[slot][c] + 0.5f) * 0.0078125f) * 128.0f;
+          for (int c = 0; c < R; ++c) {
+            rowb[buf ^ 1][0][R * tx + c] = floorf((x[s2][c] + 0.5f) * 0.0078125f) * 128.0f;
+            rowb[buf ^ 1][1][R * tx + c] = floorf((x[s3][c] + 0.5f) * 0.0078125f) * 128.0f;
+          }
         }
         if (owner == tx) {
-          const float kp = (float)(klow + k + 1);
+          const float kp = (float)(klow + k + 2);
 #pragma unroll
           for (int r = 0; r < R; ++r)
-            colb[buf ^ 1][R * ty + r] = floorf((x[r][slot] + 0.5f) * 0.0078125f) * 128.0f + kp;
+            colb[buf ^ 1][R * ty + r] = make_float2(floorf((x[r][s2] + 0.5f) * 0.0078125f) * 128.0f + kp,
+                                                    floorf((x[r][s3] + 0.5f) * 0.0078125f) * 128.0f + kp + 1.0f);
         }
       }
       __syncthreads();
