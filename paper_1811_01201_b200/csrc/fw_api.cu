@@ -144,6 +144,7 @@ struct Ctx {
   cudaStream_t copy = nullptr;     // host pipeline: H2D / D2H of row chunks
   std::vector<cudaEvent_t> pev;    // host pipeline: per-chunk landed / finished events
   int pipe_tiles = -1;             // host pipeline chunk in tile-rows (-1 auto, 0 off)
+  int pipe_first = 8;              // auto geometry: first chunk (tile-rows; env FW_PIPE_FIRST)
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
   int rank = 0, world = 1;
   int ngpus_max = 1;               // fw_init's limit (0 there = every visible device)
@@ -359,6 +360,27 @@ struct Rounds {
     const int kb = K * BS;
     const bool own = owns(K);
     return phase3(st, K, own ? lrow(K) : 0, own ? lrow(K) + BS : 0, kb, kb + BS);
+  }
+
+  // Rounds [K0, K1) whose pivot strips (rows of other chunks, read in place through Dg) have
+  // completed those rounds (host pipeline, BS = 128, reading R16): no pivot phases, so each
+  // round is one phase-3 launch that leaves the round's own column block alone, and the
+  // column-strip products of all K1 - K0 blocks follow in one launch (colstrip mode). The
+  // column-strip update may come after later rounds: phase 3 of round K reaches every path
+  // through block K via its FIRST block-K vertex u (D[i][u] needs no block-K intermediate,
+  // D[u][j] is complete), and the strip's own elements only need it before these rows' next
+  // pivot phases or their end.
+  int run_plain(cudaStream_t st, int K0, int K1) {
+    if (K0 >= K1 || nrows == 0) return FW_OK;
+    for (int K = K0; K < K1; ++K) {
+      const int kb = K * BS;
+      TRY(phase3(st, K, 0, 0, kb, kb + BS));
+    }
+    TileArgs a = tile_args(ld, Dg, ld, 0, BS, 0, nrows, n_pad);
+    a.colstrip = 1;
+    put(a, 0, Strip{0, K0 * BS, 0, 0, 0, 0, 0});
+    return launch_tile<T, 128, 128, MODE>(dim3((unsigned)(K1 - K0), (unsigned)(nrows / 128), 1), st, D, P, a,
+                                          maxkey);
   }
 
   // Look-ahead (BS = 128): one ordered phase-3 launch per round whose first nprio CTAs are
@@ -1099,14 +1121,21 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
   int *d_done = d_flags + 16;
   const Events ev{false, c.events.data() + 4, c.events.data() + 4 + 3 * (size_t)g.R};
   const bool la = c.lookahead && g.BS == 128;
-  // rounds [K0, K1) on tile-rows [t0, t1), pivot strips read in place from the whole matrix
+  // rounds [K0, K1) on tile-rows [t0, t1), pivot strips read in place from the whole matrix:
+  // rounds whose pivots lie outside the rows as plain phase-3 launches + one column-strip batch,
+  // the rows' own rounds with their pivot phases and the look-ahead
   auto run = [&](int t0, int t1, int K0, int K1) -> int {
     if (t1 <= t0 || K1 <= K0) return FW_OK;
     const int64_t r0 = g.rows_of(t0);
-    CU(cudaMemsetAsync(d_done, 0, 4 * (size_t)g.R, st));
     Rounds<C, MODE> rk{c, 1, D + r0 * g.ld, P ? P + r0 * g.ld : nullptr, g.ld, g.n, g.n_pad, r0,
                        g.rows_of(t1 - t0), g.BS, g.R, d_flags + 2, {nullptr, nullptr}, d_done, D};
-    return rk.run(st, ev, la, K0, K1);
+    const int own0 = std::max(K0, std::min(K1, t0)), own1 = std::max(own0, std::min(K1, t1));
+    TRY(rk.run_plain(st, K0, own0));                 // pivots in earlier rows
+    if (own1 > own0) {
+      CU(cudaMemsetAsync(d_done, 0, 4 * (size_t)g.R, st));
+      TRY(rk.run(st, ev, la, own0, own1));           // own pivots
+    }
+    return rk.run_plain(st, own1, K1);               // pivots in later rows
   };
   for (int ci = 1; ci < NC; ++ci) TRY(pipe_arrive<T>(c, g, ci, dist_h, raw, d_flags));
   // arrival: init + rounds [0, t_c+1) of each chunk as it lands
@@ -1243,7 +1272,8 @@ std::vector<int> pipe_bounds(const Ctx &c, int64_t n) {
   }
   if (tiles < 64) return tb;
   tb.push_back(0);
-  int t = 8, step = 8;
+  int t = c.pipe_first, step = c.pipe_first;
+  if (2 * t > tiles) return std::vector<int>();
   tb.push_back(t);
   while (t + 2 * step < tiles) {   // the next chunk would not be the last: keep doubling
     t += step;
@@ -1564,6 +1594,8 @@ int fw_init(int ngpus_max, unsigned flags) {
   CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi));
   const char *la = getenv("FW_LOOKAHEAD");
   c->lookahead = !(la && la[0] == '0');
+  const char *pf = getenv("FW_PIPE_FIRST");   // tuning: first chunk of the auto host pipeline
+  if (pf && atoi(pf) >= 1 && atoi(pf) <= 64) c->pipe_first = atoi(pf);
   g_ctx = c;
   g_err.clear();
   return FW_OK;

@@ -154,6 +154,10 @@ struct TileArgs {
   int mc_lo[2], mc_hi[2];        // excluded columns, per blockIdx.z
   int xrow[2];                   // 1: blockIdx.x walks tile rows (column strip in a dual launch)
   int tag;                       // round number (TAG mode)
+  // Column-strip batch (host pipeline, BS = 128): every CTA relaxes its tile
+  // through the block of its own columns, k in [j0, j0 + 128): A = the tile itself, B = rows
+  // j0.. of the matrix whose row 0 is at g.B (pitch ldb), tag = j0 / 128 (that block's round).
+  int colstrip;
   // Ordered phase-3 launch (order = 1, 1-D grid, 128 x 128 tiles): blockIdx.x enumerates the
   // round's tiles with the look-ahead set first — A1 = tile-row rowN (next pivot block-row,
   // -1 if not local) except tile-column colK; A2 = tile-column colN except tile-rows rowK and
@@ -257,7 +261,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   const int i0 = ts.i0, j0 = ts.j0;
 
   const int64_t ld = g.ld;
-  const int kb = g.kb;
+  const int kb = g.colstrip ? j0 : g.kb;
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   // Warm L2 with this tile of D for the epilogue's compare (128-B lines, per-thread
   // addresses): the tile is read once per round from HBM, and its latency was the
@@ -278,7 +282,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   const int b_r = tid / (TN / 4), b_c = (tid % (TN / 4)) * 4;
   const T *a_src = D + (int64_t)(i0 + a_r) * ld + kb + a_c;
   const int64_t ldb = g.ldb;
-  const T *b_src = static_cast<const T *>(g.B) + (int64_t)b_r * ldb + j0 + b_c;
+  const T *b_src = static_cast<const T *>(g.B) + (int64_t)((g.colstrip ? j0 : 0) + b_r) * ldb + j0 + b_c;
 
   auto load_chunk = [&](int stage, int k0) {
     T *as = smem + stage * S::kStage;
@@ -341,7 +345,8 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
   const TileSlot te = tile_slot<TM, TN, DUAL>(g, ctaid(0), ctaid(1), ctaid(2));
   const int mr_lo = te.mr_lo, mr_hi = te.mr_hi, mc_lo = te.mc_lo, mc_hi = te.mc_hi;
-  const int kgrp = g.kb & ~127;
+  const int kgrp = (g.colstrip ? te.j0 : g.kb) & ~127;
+  const int tag = g.colstrip ? te.j0 >> 7 : g.tag;
   int kmax = 0;
 #pragma unroll
   for (int r = 0; r < RM; ++r) {
@@ -361,7 +366,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
         const int j = jb + e;
         const T m = acc[r][4 * h + e];
         chg[e] = row_ok && !(j >= mc_lo && j < mc_hi) && m < (T)vget(old, e);
-        pv[e] = g.tag;
+        pv[e] = tag;
         if (chg[e]) {
           any = true;
           if (is_key(MODE)) {
