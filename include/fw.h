@@ -133,6 +133,13 @@ int fw_solve(float *dist, int32_t *next, int64_t n, int block, int ngpus);
  * FW_ESTATE before fw_init; FW_EINVAL for chunk_tiles < -1. */
 int fw_set_host_pipeline(int chunk_tiles);
 
+/* Host-only (no GPU, no fw_init): the host pipeline's chunk boundaries for n, in tile-rows of
+ * 128 (out[0] = 0 < out[1] < .. < out[C] = ceil(n/128)): chunk_tiles as fw_set_host_pipeline,
+ * first_tiles the first chunk of the auto (-1) geometry (8 unless FW_PIPE_FIRST is set).
+ * Returns the number of boundaries written (0 = that solve is not pipelined), or -FW_EINVAL
+ * for bad arguments or max_out too small. */
+int fw_host_pipeline_bounds(int64_t n, int chunk_tiles, int first_tiles, int32_t *out, int max_out);
+
 /* Host-memory solve, INT32 (no-edge = FW_INF_I32; weights in [0, FW_INF_I32]). */
 int fw_solve_i32(int32_t *dist, int32_t *next, int64_t n, int block, int ngpus);
 

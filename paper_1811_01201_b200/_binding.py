@@ -57,6 +57,7 @@ _lib.fw_free.argtypes = []
 _lib.fw_solve.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_solve_i32.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_set_host_pipeline.argtypes = [_I]
+_lib.fw_host_pipeline_bounds.argtypes = [_I64, _I, _I, ctypes.POINTER(ctypes.c_int32), _I]
 _lib.fw_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_dist_partition.argtypes = [_I64, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
@@ -125,6 +126,15 @@ def fw_solve(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:
 def fw_set_host_pipeline(chunk_tiles: int = -1) -> None:
     """Host-entry copy/solve pipeline: -1 auto, 0 off, k = chunks of k x 128 rows."""
     _check(_lib.fw_set_host_pipeline(chunk_tiles))
+
+
+def fw_host_pipeline_bounds(n: int, chunk_tiles: int = -1, first_tiles: int = 8) -> list[int]:
+    """Chunk boundaries (tile-rows) of the host pipeline for n (host-only); [] = not pipelined."""
+    buf = (ctypes.c_int32 * 1024)()
+    r = _lib.fw_host_pipeline_bounds(n, chunk_tiles, first_tiles, buf, 1024)
+    if r < 0:
+        _check(-r)
+    return list(buf[:r])
 
 
 def fw_solve_i32(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:

@@ -1260,20 +1260,19 @@ int pipe_dispatch(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw,
 // Chunk boundaries (tile-rows) of the host pipeline; empty = no pipeline. Auto (pipe_tiles < 0):
 // at n >= 8192, chunks of 8, 8, 16, 32, .. tile-rows (doubling; the last takes the rest).
 // pipe_tiles = k > 0: uniform chunks of k tile-rows when there are at least two.
-std::vector<int> pipe_bounds(const Ctx &c, int64_t n) {
+std::vector<int> pipe_bounds_of(int64_t n, int pipe_tiles, int pipe_first) {
   const int tiles = (int)((n + 127) / 128);
   std::vector<int> tb;
-  if (c.pipe_tiles == 0) return tb;
-  if (c.pipe_tiles > 0) {
-    if (tiles < 2 * c.pipe_tiles) return tb;
-    for (int t = 0; t < tiles; t += c.pipe_tiles) tb.push_back(t);
+  if (pipe_tiles == 0) return tb;
+  if (pipe_tiles > 0) {
+    if (tiles < 2 * pipe_tiles) return tb;
+    for (int t = 0; t < tiles; t += pipe_tiles) tb.push_back(t);
     tb.push_back(tiles);
     return tb;
   }
-  if (tiles < 64) return tb;
+  if (tiles < 64 || pipe_first < 1 || 2 * pipe_first > tiles) return tb;
   tb.push_back(0);
-  int t = c.pipe_first, step = c.pipe_first;
-  if (2 * t > tiles) return std::vector<int>();
+  int t = pipe_first, step = pipe_first;
   tb.push_back(t);
   while (t + 2 * step < tiles) {   // the next chunk would not be the last: keep doubling
     t += step;
@@ -1283,6 +1282,7 @@ std::vector<int> pipe_bounds(const Ctx &c, int64_t n) {
   tb.push_back(tiles);
   return tb;
 }
+std::vector<int> pipe_bounds(const Ctx &c, int64_t n) { return pipe_bounds_of(n, c.pipe_tiles, c.pipe_first); }
 
 // Pipelined host solve; returns FW_OK with *done = false when the standard path must run, and
 // *raw_ready = true when the caller's input is then already on the device (c.user_d, n x n).
@@ -1618,6 +1618,17 @@ int fw_set_host_pipeline(int chunk_tiles) {
   if (chunk_tiles < -1) return fail(FW_EINVAL, "chunk_tiles must be >= -1 (got %d)", chunk_tiles);
   g_ctx->pipe_tiles = chunk_tiles;
   return FW_OK;
+}
+
+int fw_host_pipeline_bounds(int64_t n, int chunk_tiles, int first_tiles, int32_t *out, int max_out) {
+  if (n <= 0 || n > 65536 || chunk_tiles < -1 || (chunk_tiles == -1 && first_tiles < 1) || max_out < 0 ||
+      (max_out > 0 && !out))
+    return -fail(FW_EINVAL, "bad arguments (n=%lld chunk_tiles=%d first_tiles=%d)", (long long)n, chunk_tiles,
+                 first_tiles);
+  const std::vector<int> tb = pipe_bounds_of(n, chunk_tiles, first_tiles);
+  if ((int)tb.size() > max_out) return -fail(FW_EINVAL, "max_out = %d < %zu bounds", max_out, tb.size());
+  for (size_t i = 0; i < tb.size(); ++i) out[i] = tb[i];
+  return (int)tb.size();
 }
 
 int fw_solve_i32(int32_t *dist, int32_t *next, int64_t n, int block, int ngpus) {
