@@ -116,13 +116,14 @@ int fw_free(void);
  *         cannot be loaded or initialised. A failing rank's message is prefixed with its
  *         rank and device.
  * Pinned (cudaHostAlloc/registered) buffers are copied directly; pageable buffers are
- * staged through an internal pinned buffer. */
+ * staged through an internal ring of pinned slices (fw_set_host_pipeline overlaps either
+ * with the solve). */
 int fw_solve(float *dist, int32_t *next, int64_t n, int block, int ngpus);
 
-/* Host pipeline of the single-GPU host entry points. When both host buffers
- * are pinned and block = 128 (any plan: keys, round tags, next == NULL; a speculative key run is
+/* Host pipeline of the single-GPU host entry points. When block = 128 (any plan: keys, round tags, next == NULL; a speculative key run is
  * checked chunk by chunk before each chunk is copied out and falls back to the standard solve
- * from the device copy of the input), the rows are split into chunks of `chunk_tiles` x 128 rows:
+ * from the device copy of the input; pageable host buffers are staged through a pinned ring
+ * by a pool of copy threads, pinned ones are copied directly), the rows are split into chunks of `chunk_tiles` x 128 rows:
  * each chunk is copied in, validated and relaxed through the rounds whose pivots exist as soon
  * as it lands, and copied out as soon as it has finished, so the copies overlap the solve.
  * Results: D identical to the unpipelined solve (any order of rounds per row that reads

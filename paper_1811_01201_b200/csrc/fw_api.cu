@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <chrono>
 #include <map>
+#include <condition_variable>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -139,6 +140,9 @@ struct Ctx {
   DevBuf scratch;                  // flags / reductions
   void *pinned = nullptr;          // staging for pageable host buffers
   int *pin_small = nullptr;        // host pipeline: per-chunk max-key snapshots (pinned)
+  std::vector<cudaEvent_t> ring_ev; // staging ring (pageable host buffers): last copy per slot
+  std::vector<bool> ring_used;
+  int ring_pos = 0;
   size_t pinned_bytes = 0;
   std::vector<cudaEvent_t> events;
   cudaStream_t copy = nullptr;     // host pipeline: H2D / D2H of row chunks
@@ -174,7 +178,6 @@ int smem_attr(const void *fn, int bytes) {
   return FW_OK;
 }
 
-constexpr size_t kStageBytes = 64ull << 20;  // pinned staging chunk
 // Largest initial/stored distance for which key sums stay exact (kernels header, KEY mode):
 // FP32: 2*(T*128+127) < 2^24; INT32: 2*(T*128+127) < FW_INF_I32 (INF + key < 2^31 as well).
 constexpr int64_t kKeyMaxF32 = 65534;
@@ -1001,50 +1004,178 @@ int ensure_pinned(Ctx &c, size_t bytes) {
   return FW_OK;
 }
 
-// Host <-> device copies: direct when the host buffer is pinned, otherwise through two
-// pinned staging chunks (the copy engine overlaps the host memcpy of the next chunk).
-int copy_h2d(Ctx &c, void *dst, const void *src, size_t bytes, cudaStream_t st) {
-  if (is_pinned(src)) {
+// ---- host <-> device copies --------------------------------------------------------------------
+// Pinned host buffers go straight to the copy engine. Pageable ones go through a ring of pinned
+// staging slices; the host side of each slice (pageable <-> pinned) is copied by a small pool
+// of threads (one memcpy thread reaches ~11 GB/s here, PCIe ~53 GB/s).
+class CopyPool {
+ public:
+  static CopyPool &get() {
+    static CopyPool pool;
+    return pool;
+  }
+  void copy(void *dst, const void *src, size_t bytes) {
+    // one parallel copy at a time (rank threads of a team solve share the pool): when the pool
+    // is busy, or the copy is small, the calling thread copies alone
+    std::unique_lock<std::mutex> busy(call_mu_, std::try_to_lock);
+    if (bytes < (4u << 20) || nth_ == 0 || !busy.owns_lock()) {
+      memcpy(dst, src, bytes);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(mu_);
+    dst_ = static_cast<char *>(dst);
+    src_ = static_cast<const char *>(src);
+    bytes_ = bytes;
+    part_ = (bytes / (nth_ + 1) + 63) & ~size_t(63);
+    pending_ = nth_;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    run_part(0);                                  // the caller copies part 0
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto &t : th_) t.join();
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    nth_ = (int)std::min(7u, hw > 2 ? hw / 2 - 1 : 0u);
+    for (int w = 1; w <= nth_; ++w) th_.emplace_back([this, w] { loop(w); });
+  }
+  void run_part(int w) {
+    const size_t lo = std::min(bytes_, (size_t)w * part_), hi = std::min(bytes_, lo + part_);
+    if (hi > lo) memcpy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void loop(int w) {
+    int seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (stop_) return;
+      lk.unlock();
+      run_part(w);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_;
+  char *dst_ = nullptr;
+  const char *src_ = nullptr;
+  size_t bytes_ = 0, part_ = 0;
+  int nth_ = 0, gen_ = 0, pending_ = 0;
+  bool stop_ = false;
+};
+
+constexpr int kSlots = 4;                       // staging ring: kSlots slices of kSlice bytes
+constexpr size_t kSlice = 32ull << 20;
+
+int ring_slot(Ctx &c, char **slot, int *idx) {
+  TRY(ensure_pinned(c, kSlots * kSlice));
+  while (c.ring_ev.size() < (size_t)kSlots) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.ring_ev.push_back(e);
+    c.ring_used.push_back(false);
+  }
+  const int s = c.ring_pos++ % kSlots;
+  if (c.ring_used[s]) CU(cudaEventSynchronize(c.ring_ev[s]));   // its last copy is done
+  *slot = static_cast<char *>(c.pinned) + (size_t)s * kSlice;
+  *idx = s;
+  return FW_OK;
+}
+
+// Enqueue an H2D copy on st. Pageable sources are staged slice by slice (the host returns once
+// the last slice is in the ring; the ring's events keep the slices alive until copied).
+int host_h2d(Ctx &c, void *dst, const void *src, size_t bytes, cudaStream_t st, bool pinned) {
+  if (pinned) {
     CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
     return FW_OK;
   }
-  TRY(ensure_pinned(c, 2 * kStageBytes));
-  cudaEvent_t done[2];
-  CU(cudaEventCreate(&done[0]));
-  CU(cudaEventCreate(&done[1]));
-  bool used[2] = {false, false};
-  size_t off = 0;
-  for (int b = 0; off < bytes; b ^= 1) {
-    const size_t len = std::min(kStageBytes, bytes - off);
-    char *stage = static_cast<char *>(c.pinned) + b * kStageBytes;
-    if (used[b]) CU(cudaEventSynchronize(done[b]));
-    memcpy(stage, static_cast<const char *>(src) + off, len);
-    CU(cudaMemcpyAsync(static_cast<char *>(dst) + off, stage, len, cudaMemcpyHostToDevice, st));
-    CU(cudaEventRecord(done[b], st));
-    used[b] = true;
-    off += len;
+  for (size_t off = 0; off < bytes; off += kSlice) {
+    const size_t len = std::min(kSlice, bytes - off);
+    char *slot = nullptr;
+    int s = 0;
+    TRY(ring_slot(c, &slot, &s));
+    CopyPool::get().copy(slot, static_cast<const char *>(src) + off, len);
+    CU(cudaMemcpyAsync(static_cast<char *>(dst) + off, slot, len, cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(c.ring_ev[s], st));
+    c.ring_used[s] = true;
   }
+  return FW_OK;
+}
+
+// D2H of `rows` rows of `width` bytes (device pitch spitch -> host pitch dpitch) on st. Pinned:
+// enqueued only. Pageable: staged, and the data is in dst when this returns (the DMA of the next
+// slice overlaps the host copy of the previous one).
+int host_d2h(Ctx &c, void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t rows,
+             cudaStream_t st, bool pinned) {
+  if (rows == 0 || width == 0) return FW_OK;
+  if (!pinned && width > kSlice) return fail(FW_EINVAL, "host_d2h: row of %zu bytes > staging slice", width);
+  if (pinned) {
+    CU(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, st));
+    return FW_OK;
+  }
+  const size_t per = std::max<size_t>(1, kSlice / width);
+  int prev = -1;
+  size_t prev_r = 0, prev_n = 0;
+  char *prev_slot = nullptr;
+  auto drain = [&]() -> int {
+    if (prev < 0) return FW_OK;
+    CU(cudaEventSynchronize(c.ring_ev[prev]));
+    for (size_t r = 0; r < prev_n; ++r) {        // contiguous rows: one parallel copy
+      if (dpitch == width) {
+        CopyPool::get().copy(static_cast<char *>(dst) + prev_r * dpitch, prev_slot, prev_n * width);
+        break;
+      }
+      memcpy(static_cast<char *>(dst) + (prev_r + r) * dpitch, prev_slot + r * width, width);
+    }
+    prev = -1;
+    return FW_OK;
+  };
+  for (size_t r0 = 0; r0 < rows; r0 += per) {
+    const size_t nr = std::min(per, rows - r0);
+    char *slot = nullptr;
+    int s = 0;
+    TRY(ring_slot(c, &slot, &s));
+    CU(cudaMemcpy2DAsync(slot, width, static_cast<const char *>(src) + r0 * spitch, spitch, width, nr,
+                         cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(c.ring_ev[s], st));
+    c.ring_used[s] = true;
+    TRY(drain());
+    prev = s;
+    prev_r = r0;
+    prev_n = nr;
+    prev_slot = slot;
+  }
+  return drain();
+}
+
+int copy_h2d(Ctx &c, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+  TRY(host_h2d(c, dst, src, bytes, st, is_pinned(src)));
   CU(cudaStreamSynchronize(st));
-  cudaEventDestroy(done[0]);
-  cudaEventDestroy(done[1]);
   return FW_OK;
 }
 
 int copy_d2h(Ctx &c, void *dst, const void *src, size_t bytes, cudaStream_t st) {
-  if (is_pinned(dst)) {
-    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    return FW_OK;
-  }
-  TRY(ensure_pinned(c, 2 * kStageBytes));
-  size_t off = 0;
-  for (; off < bytes;) {
-    const size_t len = std::min(kStageBytes, bytes - off);
-    CU(cudaMemcpyAsync(c.pinned, static_cast<const char *>(src) + off, len, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    memcpy(static_cast<char *>(dst) + off, c.pinned, len);
-    off += len;
-  }
+  // as rows of kSlice bytes (+ a tail row): host_d2h stages whole rows per slice
+  const bool pinned = is_pinned(dst);
+  const size_t rows = bytes / kSlice, tail = bytes - rows * kSlice;
+  TRY(host_d2h(c, dst, kSlice, src, kSlice, kSlice, rows, st, pinned));
+  TRY(host_d2h(c, static_cast<char *>(dst) + rows * kSlice, tail, static_cast<const char *>(src) + rows * kSlice,
+               tail, tail, tail ? 1 : 0, st, pinned));
+  CU(cudaStreamSynchronize(st));
   return FW_OK;
 }
 
@@ -1077,6 +1208,7 @@ struct PipeGeom {
   int64_t n, n_pad, ld;
   int BS, R;
   std::vector<int> tb;   // chunk boundaries in tile-rows: tb[0] = 0 .. tb[C] = n_pad / 128
+  bool pinned_d = true, pinned_p = true;   // host buffers pinned (else staged through the ring)
   int nchunks() const { return (int)tb.size() - 1; }
   int64_t rows_of(int t) const { return (int64_t)t * 128; }
   int kend(int c) const { return (int)std::min<int64_t>(R, tb[c + 1]); }   // rounds [0, kend) on arrival
@@ -1094,13 +1226,13 @@ int pipe_events(Ctx &c, size_t count) {
   return FW_OK;
 }
 
-// H2D + validation of chunk ci on the copy stream; pev[ci] = landed.
+// H2D + validation of chunk ci on the copy stream; pev[ci] = landed. A pageable source is
+// staged through the pinned ring (the host returns once the chunk is in flight).
 template <typename T>
 int pipe_arrive(Ctx &c, const PipeGeom &g, int ci, const T *dist_h, T *raw, int *d_flags) {
   const int64_t r0 = g.rows_of(g.tb[ci]), nsrc = g.nsrc(ci);
   if (nsrc > 0) {
-    CU(cudaMemcpyAsync(raw + r0 * g.n, dist_h + r0 * g.n, (size_t)nsrc * g.n * sizeof(T),
-                       cudaMemcpyHostToDevice, c.copy));
+    TRY(host_h2d(c, raw + r0 * g.n, dist_h + r0 * g.n, (size_t)nsrc * g.n * sizeof(T), c.copy, g.pinned_d));
     const dim3 gr((unsigned)std::max<int64_t>(1, std::min<int64_t>((g.n / 4 + 255) / 256, 16)),
                   (unsigned)std::min<int64_t>(nsrc, 148 * 8));
     validate_kernel<T><<<gr, 256, 0, c.copy>>>(raw + r0 * g.n, g.n, nsrc, g.n, r0, d_flags, d_flags + 1);
@@ -1137,8 +1269,8 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
     }
     return rk.run_plain(st, own1, K1);               // pivots in later rows
   };
-  for (int ci = 1; ci < NC; ++ci) TRY(pipe_arrive<T>(c, g, ci, dist_h, raw, d_flags));
-  // arrival: init + rounds [0, t_c+1) of each chunk as it lands
+  // arrival: init + rounds [0, t_c+1) of each chunk as it lands; the next chunk is put in flight
+  // after this one's work is queued (a pageable copy keeps the host busy meanwhile)
   for (int ci = 0; ci < NC; ++ci) {
     const int64_t r0 = g.rows_of(g.tb[ci]);
     CU(cudaStreamWaitEvent(st, c.pev[ci], 0));
@@ -1146,6 +1278,7 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
                               P ? P + r0 * g.ld : nullptr, g.ld, g.rows_of(g.tb[ci + 1] - g.tb[ci]),
                               g.n_pad)));
     TRY(run(g.tb[ci], g.tb[ci + 1], 0, g.kend(ci)));
+    if (ci + 1 < NC) TRY(pipe_arrive<T>(c, g, ci + 1, dist_h, raw, d_flags));
   }
   // check: the whole matrix's plan must be the speculated one
   CU(cudaMemcpyAsync(h_flags, d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.copy));
@@ -1159,7 +1292,8 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
     if (rc == FW_OK) *fallback = true;
     return rc;
   }
-  // departure: chunk c final -> post-pass, out-of-place emit, D2H; rows [0, t_c) take block c.
+  // departure, (a) all compute: for c = C-1..0 chunk c is final -> its P post-pass, D emitted out
+  // of place (event pev[NC + c], max-key snapshot), then rows [0, t_c) take block range c.
   // A speculative key run (keys not statically exact) is checked before each chunk leaves: the
   // chunk's values came from sums of keys stored so far, exact iff the running max key is in
   // range then (it only grows). Its D is emitted into a separate buffer so the input survives
@@ -1187,57 +1321,63 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
         CU(cudaMemcpyAsync(c.pin_small + ci, d_flags + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
       CU(cudaEventRecord(c.pev[NC + ci], st));
     }
-    TRY(run(0, g.tb[ci], g.tb[ci], g.kend(ci)));   // queued before the host waits on the check
-    if (nsrc > 0) {
-      if (check_keys) {
-        CU(cudaEventSynchronize(c.pev[NC + ci]));
-        if (c.pin_small[ci] > spec.key_limit) {   // a stored key left the exact range
-          CU(cudaStreamSynchronize(st));
-          CU(cudaStreamSynchronize(c.side));
-          CU(cudaStreamSynchronize(c.copy));
-          *fallback = true;
-          return FW_OK;
-        }
-      }
-      CU(cudaStreamWaitEvent(c.copy, c.pev[NC + ci], 0));
-      CU(cudaMemcpyAsync(dist_h + r0 * g.n, out + r0 * g.n, (size_t)nsrc * g.n * sizeof(T),
-                         cudaMemcpyDeviceToHost, c.copy));
-      if (path_mode >= 0 && MODE != MODE_TAG)
-        CU(cudaMemcpy2DAsync(next_h + r0 * g.n, g.n * sizeof(int32_t), P + r0 * g.ld,
-                             g.ld * sizeof(int32_t), g.n * sizeof(int32_t), nsrc, cudaMemcpyDeviceToHost,
-                             c.copy));
-    }
+    TRY(run(0, g.tb[ci], g.tb[ci], g.kend(ci)));
   }
-  if (MODE == MODE_TAG && path_mode >= 0) {
-    // round tags -> last k (reading R9: valid for any round order, the last improvement in time
-    // wrote the tag) -> next hop, on the whole final D (transposed once); per row chunk of
-    // kTagRows rows, so each chunk's P copy overlaps the next chunk's search
-    constexpr int64_t kTagRows = 2048;
-    for (int64_t r0 = 0, q = 0; r0 < g.n; r0 += kTagRows, ++q) {
-      std::vector<Part<C>> part(1);
-      part[0].D = D + r0 * g.ld;
-      part[0].P = P + r0 * g.ld;
-      part[0].ld = g.ld;
-      part[0].row0 = r0;
-      part[0].nrows = std::min<int64_t>(kTagRows, g.n_pad - r0);
-      part[0].nsrc = std::min<int64_t>(kTagRows, g.n - r0);
-      if (q == 0) {   // the transpose of the whole final D (the search reads column segments)
-        TRY(c.ws_tr.ensure((size_t)g.n_pad * g.n_pad * sizeof(C)));
-        dim3 gt((unsigned)(g.n_pad / 32), (unsigned)(g.n_pad / 32));
-        transpose_kernel<C><<<gt, dim3(32, 8), 0, st>>>(D, g.ld, g.n_pad, g.n_pad, static_cast<C *>(c.ws_tr.p),
-                                                      g.n_pad);
-        CU(cudaGetLastError());
-        ++g_launches;
-      }
-      TRY(post_pass<C>(c, part, T_LOCAL, 1, g.n, g.BS, MODE_TAG, path_mode, d_flags, st, true));
-      cudaEvent_t ev_q = c.pev[2 * NC + (q & 1)];
-      CU(cudaEventRecord(ev_q, st));
-      CU(cudaStreamWaitEvent(c.copy, ev_q, 0));
-      CU(cudaMemcpy2DAsync(next_h + r0 * g.n, g.n * sizeof(int32_t), P + r0 * g.ld, g.ld * sizeof(int32_t),
-                           g.n * sizeof(int32_t), part[0].nsrc, cudaMemcpyDeviceToHost, c.copy));
+  // round tags -> last k (reading R9: valid for any round order, the last improvement in time
+  // wrote the tag) -> next hop, on the whole final D (transposed once), per row chunk of
+  // kTagRows rows so each chunk's P copy overlaps the next chunk's search
+  constexpr int64_t kTagRows = 2048;
+  const bool tag_p = MODE == MODE_TAG && path_mode >= 0;
+  const int ntag = tag_p ? (int)((g.n + kTagRows - 1) / kTagRows) : 0;
+  for (int q = 0; q < ntag; ++q) {
+    const int64_t r0 = q * kTagRows;
+    std::vector<Part<C>> part(1);
+    part[0].D = D + r0 * g.ld;
+    part[0].P = P + r0 * g.ld;
+    part[0].ld = g.ld;
+    part[0].row0 = r0;
+    part[0].nrows = std::min<int64_t>(kTagRows, g.n_pad - r0);
+    part[0].nsrc = std::min<int64_t>(kTagRows, g.n - r0);
+    if (q == 0) {   // the transpose of the whole final D (the search reads column segments)
+      TRY(c.ws_tr.ensure((size_t)g.n_pad * g.n_pad * sizeof(C)));
+      dim3 gt((unsigned)(g.n_pad / 32), (unsigned)(g.n_pad / 32));
+      transpose_kernel<C><<<gt, dim3(32, 8), 0, st>>>(D, g.ld, g.n_pad, g.n_pad, static_cast<C *>(c.ws_tr.p),
+                                                    g.n_pad);
+      CU(cudaGetLastError());
+      ++g_launches;
     }
+    TRY(post_pass<C>(c, part, T_LOCAL, 1, g.n, g.BS, MODE_TAG, path_mode, d_flags, st, true));
+    CU(cudaEventRecord(c.pev[2 * NC + q], st));
   }
   CU(cudaEventRecord(e_comp_end, st));
+  // departure, (b) the copies out, in the same order: the host waits for a chunk only where it
+  // must (a key check, or a pageable destination staged through the ring)
+  for (int ci = NC - 1; ci >= 0; --ci) {
+    const int64_t r0 = g.rows_of(g.tb[ci]), nsrc = g.nsrc(ci);
+    if (nsrc == 0) continue;
+    if (check_keys) {
+      CU(cudaEventSynchronize(c.pev[NC + ci]));
+      if (c.pin_small[ci] > spec.key_limit) {   // a stored key left the exact range
+        CU(cudaStreamSynchronize(st));
+        CU(cudaStreamSynchronize(c.side));
+        CU(cudaStreamSynchronize(c.copy));
+        *fallback = true;
+        return FW_OK;
+      }
+    }
+    CU(cudaStreamWaitEvent(c.copy, c.pev[NC + ci], 0));
+    const size_t rb = (size_t)g.n * sizeof(T);
+    TRY(host_d2h(c, dist_h + r0 * g.n, rb, out + r0 * g.n, rb, rb, nsrc, c.copy, g.pinned_d));
+    if (path_mode >= 0 && MODE != MODE_TAG)
+      TRY(host_d2h(c, next_h + r0 * g.n, g.n * sizeof(int32_t), P + r0 * g.ld, g.ld * sizeof(int32_t),
+                   g.n * sizeof(int32_t), nsrc, c.copy, g.pinned_p));
+  }
+  for (int q = 0; q < ntag; ++q) {
+    const int64_t r0 = q * kTagRows, nsrc = std::min<int64_t>(kTagRows, g.n - r0);
+    CU(cudaStreamWaitEvent(c.copy, c.pev[2 * NC + q], 0));
+    TRY(host_d2h(c, next_h + r0 * g.n, g.n * sizeof(int32_t), P + r0 * g.ld, g.ld * sizeof(int32_t),
+                 g.n * sizeof(int32_t), nsrc, c.copy, g.pinned_p));
+  }
   CU(cudaStreamWaitEvent(c.copy, e_comp_end, 0));
   return FW_OK;
 }
@@ -1292,7 +1432,9 @@ int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool
   *raw_ready = false;
   PipeGeom g{};
   g.tb = pipe_bounds(c, n);
-  if (g.tb.size() < 3 || BS != 128 || !is_pinned(dist) || (next && !is_pinned(next))) return FW_OK;
+  if (g.tb.size() < 3 || BS != 128) return FW_OK;
+  g.pinned_d = is_pinned(dist);
+  g.pinned_p = next ? is_pinned(next) : true;
   g.n = n;
   g.n_pad = (n + 127) / 128 * 128;
   g.ld = g.n_pad;
@@ -1306,7 +1448,7 @@ int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool
   if (want_p) TRY(c.ws_t.ensure((size_t)g.n_pad * g.n_pad * sizeof(int32_t)));
   TRY(c.scratch.ensure(64 + 4 * (size_t)g.R));
   TRY(ensure_events(c, 4 + 3 * (size_t)g.R + 2 * (size_t)g.R));
-  TRY(pipe_events(c, 2 * (size_t)g.nchunks() + 2));
+  TRY(pipe_events(c, 2 * (size_t)g.nchunks() + 40));   // + one per 2048-row tag chunk (n <= 65536)
   T *raw = static_cast<T *>(c.user_d.p);
   int *d_flags = static_cast<int *>(c.scratch.p);
   cudaEvent_t e_begin = c.events[0], e_end = c.events[1], e_land0 = c.events[2], e_comp = c.events[3];
@@ -1418,6 +1560,9 @@ void ctx_release(Ctx *c) {
   c->events.clear();
   for (auto e : c->pev) cudaEventDestroy(e);
   c->pev.clear();
+  for (auto e : c->ring_ev) cudaEventDestroy(e);
+  c->ring_ev.clear();
+  c->ring_used.clear();
   if (c->copy) cudaStreamDestroy(c->copy);
   c->copy = nullptr;
   if (c->stream) cudaStreamDestroy(c->stream);

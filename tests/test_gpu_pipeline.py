@@ -29,11 +29,16 @@ def pinned(a: np.ndarray):
     return t
 
 
-def solve_pinned(W, chunk_tiles, path="next", block=128):
-    """fw_solve on pinned host tensors with the given pipeline chunk; (D, P, stats)."""
+def solve_pinned(W, chunk_tiles, path="next", block=128, pin=True):
+    """fw_solve on pinned host tensors (pin=False: pageable NumPy arrays, staged through the
+    library's pinned ring) with the given pipeline chunk; (D, P, stats)."""
     flags = fw.FW_PATH_LAST_K if path == "lastk" else 0
-    hD = pinned(W)
-    hP = torch.full(W.shape, -5, dtype=torch.int32).pin_memory() if path else None
+    if pin:
+        hD = pinned(W)
+        hP = torch.full(W.shape, -5, dtype=torch.int32).pin_memory() if path else None
+    else:
+        hD = torch.from_numpy(W.copy())
+        hP = torch.full(W.shape, -5, dtype=torch.int32) if path else None
     fw.fw_init(0, flags)
     try:
         fw.fw_set_host_pipeline(chunk_tiles)
@@ -45,8 +50,8 @@ def solve_pinned(W, chunk_tiles, path="next", block=128):
     return hD.numpy(), (hP.numpy() if hP is not None else None), st
 
 
-def check(W, chunk_tiles, path="next", expect_chunks=None):
-    D, P, st = solve_pinned(W, chunk_tiles, path)
+def check(W, chunk_tiles, path="next", expect_chunks=None, pin=True):
+    D, P, st = solve_pinned(W, chunk_tiles, path, pin=pin)
     exact = exact_data(W)
     assert_D_matches(D, oracle.fw(W, None)[0], exact)
     if path:
@@ -195,18 +200,31 @@ def test_pipeline_int32_erange_late():
     np.testing.assert_array_equal(hD.numpy(), W)
 
 
-def test_pipeline_pageable_uses_standard_path():
-    W = gen.generate("complete_int", 512, 945)
+@pytest.mark.parametrize("kind,n,ct,path", [("complete_int", 512, 1, "next"), ("complete_real", 700, 2, "next"),
+                                             ("complete_int", 900, 2, "lastk"), ("complete_real", 640, 1, None),
+                                             ("er_int", 1000, 1, "next")])
+def test_pipeline_pageable(kind, n, ct, path):
+    """Pageable (NumPy) host buffers: chunks are staged through the pinned ring by the copy
+    pool, same parity as pinned buffers (keys, tags, LAST_K, D only, speculative INT32 keys)."""
+    W = gen.generate(kind, n, 945 + n, p=0.05, lo=1, hi=1000) if kind == "er_int" else gen.generate(kind, n, 945 + n)
+    check(W, ct, path=path, expect_chunks=-(-((n + 127) // 128) // ct), pin=False)
+
+
+def test_pipeline_pageable_numpy_api():
+    """The plain NumPy call a user makes: fw_solve(D, P) on pageable arrays, pipelined."""
+    W = gen.generate("complete_int", 512, 946)
     D = W.copy()
     P = np.empty(W.shape, np.int32)
     fw.fw_init(0, 0)
     try:
         fw.fw_set_host_pipeline(1)
         fw.fw_solve(D, P, block=128)
-        assert fw.fw_last_stats().host_chunks == 0
+        assert fw.fw_last_stats().host_chunks == 4
     finally:
         fw.fw_free()
     np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+    bad, first = oracle.check_paths(W, D, P)
+    assert bad == 0
 
 
 @pytest.mark.slow
@@ -256,3 +274,15 @@ def test_pipeline_speculative_keys_fail_falls_back():
     ii, jj = np.meshgrid(i, i, indexing="ij")
     np.testing.assert_array_equal(D.astype(np.int64), ((jj - ii) % n) * 1000)
     np.testing.assert_array_equal(P, np.where(ii == jj, ii, (ii + 1) % n))
+
+
+def test_pipeline_pageable_large_slices():
+    """n = 5000 with chunks of 20 tile-rows (51 MB of D per chunk): every chunk copy is larger
+    than one 32 MiB staging slice, so it is split over several slices of the ring."""
+    n = 5000
+    W = gen.generate("complete_int", n, 947)
+    D, P, st = solve_pinned(W, 20, pin=False)
+    assert st.host_chunks == 2
+    src = gen.sources(n, 947, 16)
+    np.testing.assert_array_equal(D[src].astype(np.float64), oracle.dijkstra(W, src))
+    assert next_consistency(W, D, P, exact=True, rows=src) == 0

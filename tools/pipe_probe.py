@@ -15,14 +15,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--chunks", default="0,8,16,32")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--pageable", action="store_true", help="NumPy-backed (pageable) host buffers")
 a = ap.parse_args()
 c = gen.CONFIGS[a.config]
 dW = gen.generate_torch(c["kind"], c["n"], c["seed"], device="cuda", p=c.get("p", 1.0),
                         lo=c.get("lo", 1), hi=c.get("hi", 100))
-hin = dW.cpu().pin_memory()
+hin = dW.cpu() if a.pageable else dW.cpu().pin_memory()
 del dW
-hD = torch.empty_like(hin).pin_memory()
-hP = torch.empty(hin.shape, dtype=torch.int32).pin_memory()
+hD = torch.empty_like(hin) if a.pageable else torch.empty_like(hin).pin_memory()
+hP = torch.empty(hin.shape, dtype=torch.int32)
+if not a.pageable:
+    hP = hP.pin_memory()
 n = c["n"]
 fw.fw_init(0, 0)
 f = fw.fw_solve_i32 if hin.dtype == torch.int32 else fw.fw_solve
@@ -35,7 +38,7 @@ for ct in [int(x) for x in a.chunks.split(",")]:
         dt = (time.perf_counter() - t0) * 1e3
         s = fw.fw_last_stats()
         if r:
-            print(f"chunk_tiles={ct} wall_ms={dt:.2f} gflops={2 * n ** 3 / dt / 1e6:.0f} "
+            print(f"{'pageable' if a.pageable else 'pinned'} chunk_tiles={ct} wall_ms={dt:.2f} gflops={2 * n ** 3 / dt / 1e6:.0f} "
                   f"lib_ms={s.solve_ms:.2f} chunks={s.host_chunks} h2d_exposed={s.h2d_ms:.2f} "
                   f"d2h_exposed={s.d2h_ms:.2f} launches={s.kernel_launches}", flush=True)
 fw.fw_free()
