@@ -129,7 +129,8 @@ int fw_solve(float *dist, int32_t *next, int64_t n, int block, int ngpus);
  * Results: D identical to the unpipelined solve (any order of rounds per row that reads
  * completed pivot strips gives the same distances: reading R16); P a valid next hop / last k
  * (ties may resolve differently). Error contract unchanged (validation completes before any
- * output is written). chunk_tiles: -1 = auto (16 tile-rows when n >= 8192, else off),
+ * output is written). chunk_tiles: -1 = auto (chunks of 8, 8, 16, 32, .. tile-rows when n >= 8192,
+ * two halves when 4096 <= n < 8192, else off),
  * 0 = off, k >= 1 = k tile-rows whenever the matrix has at least two chunks.
  * FW_ESTATE before fw_init; FW_EINVAL for chunk_tiles < -1. */
 int fw_set_host_pipeline(int chunk_tiles);

@@ -91,18 +91,20 @@ def run_pipeline(W, BS, tb, violate=False):
 
 
 @pytest.mark.parametrize("n,ct", [(1000, 1), (1000, 3), (8192, -1), (16384, -1), (32768, -1), (65536, -1),
-                                  (300, 2), (129, 1)])
+                                  (300, 2), (129, 1), (4096, -1), (6000, -1), (3000, -1)])
 def test_bounds_partition_tile_rows(n, ct):
     tb = fw.fw_host_pipeline_bounds(n, ct, 8)
     tiles = -(-n // 128)
     if not tb:
-        assert ct == -1 and tiles < 64 or ct > 0 and tiles < 2 * ct
+        assert ct == -1 and tiles < 32 or ct > 0 and tiles < 2 * ct
         return
     assert tb[0] == 0 and tb[-1] == tiles and len(tb) >= 3
     assert all(a < b for a, b in zip(tb, tb[1:]))
     sizes = np.diff(tb)
     if ct > 0:
         assert (sizes[:-1] == ct).all() and sizes[-1] <= ct
+    elif tiles < 64:
+        assert tb == [0, tiles // 2, tiles]
     else:
         assert sizes[0] == sizes[1] == 8
         assert all(b == 2 * a for a, b in zip(sizes[1:-2], sizes[2:-1]))
@@ -113,7 +115,8 @@ def test_bounds_auto_c4_and_errors():
     assert fw.fw_host_pipeline_bounds(16384, -1, 8) == [0, 8, 16, 32, 64, 128]
     assert fw.fw_host_pipeline_bounds(16384, -1, 16) == [0, 16, 32, 64, 128]
     assert fw.fw_host_pipeline_bounds(16384, 0, 8) == []
-    assert fw.fw_host_pipeline_bounds(4096, -1, 8) == []          # < 64 tile-rows: not pipelined
+    assert fw.fw_host_pipeline_bounds(4096, -1, 8) == [0, 16, 32]  # 32..63 tile-rows: two halves
+    assert fw.fw_host_pipeline_bounds(3968, -1, 8) == []          # < 32 tile-rows: not pipelined
     with pytest.raises(fw.FwError):
         fw.fw_host_pipeline_bounds(0, -1, 8)
     with pytest.raises(fw.FwError):
