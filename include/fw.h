@@ -194,6 +194,22 @@ int fw_dist_loopback_solve_device_f32(float *d_dist, int32_t *d_next, int64_t n,
 int fw_dist_loopback_solve_device_i32(int32_t *d_dist, int32_t *d_next, int64_t n, int64_t ld,
                                       int block, int world, void *stream);
 
+/* Path reconstruction (host-only, no GPU or fw_init needed): the vertices
+ * of the shortest i -> j path encoded by the P matrix a solve returned (n x n int32, row-major,
+ * host memory).
+ *   mode FW_PATH_NEXT_HOP: i, next[i][j], next[next[i][j]][j], ..., j.
+ *   mode FW_PATH_LAST_K:   the recursive expansion path(i,k) + path(k,j) of k = P[i][j], where
+ *                          -1 is a direct edge (iterative: no recursion depth limit).
+ * dist: the solve's D (FP32, or INT32 with dist_is_int32 = 1) for reachability (D[i][j] = INF:
+ *   no path); required in LAST_K mode (-1 there also marks unreachable pairs), optional in
+ *   next-hop mode (next = -1 marks them).
+ * out: up to max_len vertices (i first, j last); out = NULL with max_len = 0 queries the length.
+ * Returns the number of vertices (1 for i == j), 0 if j is unreachable from i, -FW_EINVAL for bad
+ * arguments or a P that does not encode a path of at most n - 1 hops, -FW_ERANGE when the path
+ * has more than max_len > 0 vertices (the first max_len are written). */
+int64_t fw_path(const int32_t *P, const void *dist, int dist_is_int32, int64_t n, int64_t i, int64_t j,
+                int mode, int32_t *out, int64_t max_len);
+
 /* Message for the last non-OK return on this thread ("" if none). */
 const char *fw_last_error(void);
 

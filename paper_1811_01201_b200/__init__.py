@@ -16,6 +16,7 @@ from ._binding import (  # noqa: F401
     fw_solve_i32,
     fw_set_host_pipeline,
     fw_host_pipeline_bounds,
+    fw_path,
     fw_solve_device_f32,
     fw_solve_device_i32,
     fw_last_error,

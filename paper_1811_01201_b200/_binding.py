@@ -58,6 +58,8 @@ _lib.fw_solve.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_solve_i32.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_set_host_pipeline.argtypes = [_I]
 _lib.fw_host_pipeline_bounds.argtypes = [_I64, _I, _I, ctypes.POINTER(ctypes.c_int32), _I]
+_lib.fw_path.argtypes = [_P, _P, _I, _I64, _I64, _I64, _I, _P, _I64]
+_lib.fw_path.restype = ctypes.c_int64
 _lib.fw_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_dist_partition.argtypes = [_I64, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
@@ -135,6 +137,25 @@ def fw_host_pipeline_bounds(n: int, chunk_tiles: int = -1, first_tiles: int = 8)
     if r < 0:
         _check(-r)
     return list(buf[:r])
+
+
+def fw_path(P, i: int, j: int, mode: int = FW_PATH_NEXT_HOP, dist=None) -> list[int]:
+    """Vertices of the shortest i -> j path encoded by P (host array from a solve; host-only).
+    [] if j is unreachable from i. dist (the solve's D) is required in LAST_K mode."""
+    n = _n_of(P, None)
+    d_addr = _addr(dist) if dist is not None else None
+    is_int = 1 if (dist is not None and str(getattr(dist, "dtype", "")).endswith("int32")) else 0
+    p_addr = _addr(P, "int32")
+    r = _lib.fw_path(p_addr, d_addr, is_int, n, i, j, mode, None, 0)
+    if r < 0:
+        _check(int(-r))
+    if r == 0:
+        return []
+    buf = (ctypes.c_int32 * int(r))()
+    r2 = _lib.fw_path(p_addr, d_addr, is_int, n, i, j, mode, ctypes.addressof(buf), int(r))
+    if r2 < 0:
+        _check(int(-r2))
+    return list(buf[:r2])
 
 
 def fw_solve_i32(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -1765,6 +1766,63 @@ int fw_set_host_pipeline(int chunk_tiles) {
   if (chunk_tiles < -1) return fail(FW_EINVAL, "chunk_tiles must be >= -1 (got %d)", chunk_tiles);
   g_ctx->pipe_tiles = chunk_tiles;
   return FW_OK;
+}
+
+int64_t fw_path(const int32_t *P, const void *dist, int dist_is_int32, int64_t n, int64_t i, int64_t j, int mode,
+                int32_t *out, int64_t max_len) {
+  if (!P || n <= 0 || n > 65536 || i < 0 || i >= n || j < 0 || j >= n || max_len < 0 || (max_len > 0 && !out) ||
+      (mode != FW_PATH_NEXT_HOP && mode != FW_PATH_LAST_K) || (mode == FW_PATH_LAST_K && !dist))
+    return -fail(FW_EINVAL, "fw_path: bad arguments (n=%lld i=%lld j=%lld mode=%d)", (long long)n, (long long)i,
+                 (long long)j, mode);
+  int64_t len = 0;
+  auto emit = [&](int64_t v) -> bool {   // false once the path is longer than a simple path
+    if (len < max_len) out[len] = (int32_t)v;
+    return ++len <= n;
+  };
+  if (dist) {   // reachability from D: INF (FP32 +inf, INT32 FW_INF_I32) = no path
+    const int64_t e = i * n + j;
+    const bool inf = dist_is_int32 ? static_cast<const int32_t *>(dist)[e] >= FW_INF_I32
+                                   : !(static_cast<const float *>(dist)[e] < INFINITY);
+    if (inf) return 0;
+  }
+  emit(i);
+  if (i == j) return 1;
+  if (mode == FW_PATH_NEXT_HOP) {   // i, next[i][j], next[next[i][j]][j], ..., j
+    int64_t h = i;
+    while (h != j) {
+      const int32_t nx = P[h * n + j];
+      if (nx < 0) {
+        if (h == i && !dist) return 0;   // unreachable (next = -1)
+        return -fail(FW_EINVAL, "fw_path: next[%lld][%lld] = %d on the way to %lld", (long long)h, (long long)j,
+                     nx, (long long)j);
+      }
+      if (nx >= n || !emit(nx))
+        return -fail(FW_EINVAL, "fw_path: next-hop chain %lld -> %lld leaves [0, n) or exceeds n - 1 hops",
+                     (long long)i, (long long)j);
+      h = nx;
+    }
+  } else {   // LAST_K: path(i,k) + path(k,j) for k = P[i][j]; -1 = direct edge
+    std::vector<std::pair<int32_t, int32_t>> stack{{(int32_t)i, (int32_t)j}};
+    while (!stack.empty()) {
+      const auto [a, b] = stack.back();
+      stack.pop_back();
+      const int32_t k = P[(int64_t)a * n + b];
+      if (k < 0) {
+        if (!emit(b))
+          return -fail(FW_EINVAL, "fw_path: LAST_K expansion of %lld -> %lld exceeds n - 1 hops", (long long)i,
+                       (long long)j);
+        continue;
+      }
+      if (k >= n || k == a || k == b || stack.size() > (size_t)n)
+        return -fail(FW_EINVAL, "fw_path: LAST_K[%d][%d] = %d is not an intermediate vertex", a, b, k);
+      stack.push_back({k, b});   // expanded after (a, k)
+      stack.push_back({a, k});
+    }
+  }
+  if (len > max_len && max_len > 0)
+    return -fail(FW_ERANGE, "fw_path: the path has %lld vertices > max_len = %lld", (long long)len,
+                 (long long)max_len);
+  return len;
 }
 
 int fw_host_pipeline_bounds(int64_t n, int chunk_tiles, int first_tiles, int32_t *out, int max_out) {

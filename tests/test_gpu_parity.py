@@ -453,3 +453,30 @@ def test_mixed_sequence_one_context():
             if path:
                 bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5)
                 assert bad == 0, (step, kind, n, block, bad, first)
+
+
+@pytest.mark.parametrize("kind,path", [("complete_int", "next"), ("complete_real", "lastk"),
+                                       ("er_int", "next"), ("er_int", "lastk")])
+def test_fw_path_on_gpu_results(kind, path):
+    """fw_path (host-only) reconstructs shortest paths from the P the GPU solve returned: every
+    sampled path starts at i, ends at j, uses edges of W, and its weights sum to D[i][j]
+    (exactly for integer data, rel 1e-5 for reals); unreachable pairs give []."""
+    n = 300
+    W = gen.generate(kind, n, 777, p=0.02, lo=1, hi=50)
+    D, P = solve(W, 128, path)
+    mode = fw.FW_PATH_LAST_K if path == "lastk" else fw.FW_PATH_NEXT_HOP
+    rng = np.random.default_rng(7)
+    w = W.astype(np.float64)
+    if W.dtype == np.int32:
+        w[W >= INF] = np.inf
+    Dd = D.astype(np.float64)
+    if W.dtype == np.int32:
+        Dd[D >= INF] = np.inf
+    for i, j in rng.integers(0, n, size=(400, 2)):
+        p = fw.fw_path(P, int(i), int(j), mode, dist=D)
+        if not np.isfinite(Dd[i, j]):
+            assert p == []
+            continue
+        assert p[0] == i and p[-1] == j and len(set(p)) == len(p)
+        s = sum(w[a, b] for a, b in zip(p, p[1:]))
+        assert abs(s - Dd[i, j]) <= 1e-5 * max(1.0, Dd[i, j]), (i, j, s, Dd[i, j])
