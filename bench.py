@@ -13,6 +13,7 @@ Prints ONE JSON line on rank 0. See DESIGN.md "Measurement" for every field.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -48,7 +49,7 @@ def dist_env():
 
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -61,7 +62,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
@@ -71,6 +72,11 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def window(self, t0: float, t1: float):
+        """Keep the samples that arrived while [t0, t1] (the timed region) was running; the
+        sampler is started before the warm-up so short timed regions still get samples."""
+        self.t0, self.t1 = t0, t1
 
     def __exit__(self, *a):
         if self.proc:
@@ -83,10 +89,18 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
+            try:   # nvidia-smi's own sample time (local time, "YYYY/MM/DD HH:MM:SS.mmm")
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            if t0 is not None and ts is not None and not (t0 - 0.05 <= ts <= t1 + 0.05):
+                continue
+            f = f[1:]
             try:
                 sm.append(float(f[1]))
                 mx = float(f[2])
@@ -224,19 +238,21 @@ def run_gpu(args, cfg):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stats = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk:   # started before the warm-up: samples from the first step on
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stats = []
+        t_start = time.time()
         e0.record(stream)
         for _ in range(args.steps):
             stats.append(step())
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.window(t_start, time.time())
     if world > 1:
         torch.distributed.barrier()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
