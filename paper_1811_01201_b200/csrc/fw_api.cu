@@ -546,7 +546,7 @@ template <typename T, int MODE, typename S>
 int run_init(cudaStream_t st, const S *src, int64_t ld_src, int64_t nsrc, int64_t n, int64_t row0,
              T *D, int32_t *P, int64_t ld, int64_t nrows, int64_t n_pad) {
   if (nrows == 0) return FW_OK;
-  dim3 g((unsigned)std::min<int64_t>((n_pad + 255) / 256, 64), (unsigned)std::min<int64_t>(nrows, 65535));
+  dim3 g((unsigned)std::min<int64_t>((n_pad / 4 + 255) / 256, 64), (unsigned)std::min<int64_t>(nrows, 2048));
   init_kernel<T, MODE, S><<<g, 256, 0, st>>>(src, ld_src, nsrc, n, row0, D, P, ld, n_pad, nrows);
   ++g_launches;
   CU(cudaGetLastError());

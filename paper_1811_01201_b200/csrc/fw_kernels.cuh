@@ -796,15 +796,38 @@ template <> __device__ __forceinline__ float to_compute<float, int32_t>(int32_t 
 template <typename T, int MODE, typename S = T>
 __global__ void init_kernel(const S *src, int64_t lds, int64_t nsrc, int64_t n, int64_t row0, T *D,
                             int32_t *P, int64_t ld, int64_t n_pad, int64_t nrows) {
+  // 4 consecutive elements per thread: 16-B loads of the source row when it is 16-B aligned and
+  // the group lies inside the n real columns, 16-B stores of D and P (ld % 128 == 0)
+  using VS = typename Vec4<S>::V;
+  using VT = typename Vec4<T>::V;
+  const bool vsrc = (lds % 4 == 0) && ((uintptr_t)src % 16 == 0);
   for (int64_t i = blockIdx.y; i < nrows; i += gridDim.y) {   // local row; global row0 + i
     const int64_t gi = row0 + i;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_pad;
-         j += (int64_t)gridDim.x * blockDim.x) {
-      T v = (i < nsrc && gi < n && j < n) ? to_compute<T, S>(src[i * lds + j]) : Num<T>::inf();
-      if (gi == j) v = 0;
-      if (MODE != MODE_PLAIN) P[i * ld + j] = -1;
-      if (is_key(MODE)) v = Num<T>::encode(v, (int)j);
-      D[i * ld + j] = v;
+    const bool row_in = i < nsrc && gi < n;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_pad / 4;
+         q += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t j = 4 * q;
+      T v[4];
+      if (row_in && vsrc && j + 4 <= n) {
+        const VS s4 = *reinterpret_cast<const VS *>(src + i * lds + j);
+        v[0] = to_compute<T, S>(s4.x);
+        v[1] = to_compute<T, S>(s4.y);
+        v[2] = to_compute<T, S>(s4.z);
+        v[3] = to_compute<T, S>(s4.w);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          v[e] = (row_in && j + e < n) ? to_compute<T, S>(src[i * lds + j + e]) : Num<T>::inf();
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (gi == j + e) v[e] = 0;
+        if (is_key(MODE)) v[e] = Num<T>::encode(v[e], (int)(j + e));
+      }
+      VT o;
+      o.x = v[0]; o.y = v[1]; o.z = v[2]; o.w = v[3];
+      *reinterpret_cast<VT *>(D + i * ld + j) = o;
+      if (MODE != MODE_PLAIN) *reinterpret_cast<int4 *>(P + i * ld + j) = make_int4(-1, -1, -1, -1);
     }
   }
 }
@@ -991,7 +1014,18 @@ finalize_paths_kernel(T *D, int32_t *P, int64_t ld, int64_t row0, int64_t n, int
     return;
   }
   int32_t *v = use_smem ? reinterpret_cast<int32_t *>(smem_raw) : row;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+  // 16-B vectors for the row passes when rows are 16-B aligned (ld, n multiples of 4)
+  const bool vec = (n % 4 == 0) && (ld % 4 == 0);
+  const int64_t j0 = vec ? n : 0;     // scalar loops start here (all of the row when !vec)
+  if (vec) {
+    for (int64_t q = threadIdx.x; q < n / 4; q += blockDim.x) {
+      const int4 t = reinterpret_cast<const int4 *>(row)[q];
+      const int32_t j = (int32_t)(4 * q);
+      reinterpret_cast<int4 *>(v)[q] = make_int4(t.x < 0 ? (j | kTerm) : t.x, t.y < 0 ? ((j + 1) | kTerm) : t.y,
+                                                 t.z < 0 ? ((j + 2) | kTerm) : t.z, t.w < 0 ? ((j + 3) | kTerm) : t.w);
+    }
+  }
+  for (int64_t j = j0 + threadIdx.x; j < n; j += blockDim.x) {
     const int32_t t = row[j];
     v[j] = t < 0 ? (int32_t)(j | kTerm) : t;
   }
@@ -1014,14 +1048,32 @@ finalize_paths_kernel(T *D, int32_t *P, int64_t ld, int64_t row0, int64_t n, int
       break;
     }
   }
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    const int32_t x = v[j];
-    const T d = Drow[j];
-    if (decode) Drow[j] = Num<T>::decode(d);
+  auto final_next = [&](int32_t x, T d, int64_t j) -> int32_t {
     int32_t out = (x & kTerm) ? (x & ~kTerm) : -1;
     if (j == i) out = (int32_t)i;
     else if (!Num<T>::finite(d)) out = -1;
-    row[j] = out;
+    return out;
+  };
+  if (vec) {
+    using VT = typename Vec4<T>::V;
+    for (int64_t q = threadIdx.x; q < n / 4; q += blockDim.x) {
+      const int4 x = reinterpret_cast<const int4 *>(v)[q];
+      const VT d = reinterpret_cast<const VT *>(Drow)[q];
+      if (decode) {
+        VT o;
+        o.x = Num<T>::decode(d.x); o.y = Num<T>::decode(d.y); o.z = Num<T>::decode(d.z); o.w = Num<T>::decode(d.w);
+        reinterpret_cast<VT *>(Drow)[q] = o;
+      }
+      const int64_t j = 4 * q;
+      reinterpret_cast<int4 *>(row)[q] = make_int4(final_next(x.x, d.x, j), final_next(x.y, d.y, j + 1),
+                                                   final_next(x.z, d.z, j + 2), final_next(x.w, d.w, j + 3));
+    }
+  }
+  for (int64_t j = j0 + threadIdx.x; j < n; j += blockDim.x) {
+    const int32_t x = v[j];
+    const T d = Drow[j];
+    if (decode) Drow[j] = Num<T>::decode(d);
+    row[j] = final_next(x, d, j);
   }
 }
 
