@@ -335,13 +335,20 @@ struct Rounds {
       return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 1, 2), st, D, P, a,
                                             maxkey);
     }
+    // a single strip (multi-GPU: the owner's row strip before the broadcast, every rank's column
+    // strip after it — both on the per-round critical path): at BS = 128 half-width tiles, twice
+    // the CTAs with half the work each. Row-strip tiles keep all 128 pivot rows (B is the tile's
+    // own columns), column-strip tiles all 128 block columns (A is the tile's own rows), so no
+    // CTA reads what another writes.
     if (row_strip) {
       put(a, 0, row);
-      TRY((launch_tile<T, B, 128, MODE>(dim3(tiles_c, 1, 1), st, D, P, a, maxkey)));
+      if (B == 128) TRY((launch_tile<T, 128, 64, MODE>(dim3(2 * tiles_c, 1, 1), st, D, P, a, maxkey)));
+      else TRY((launch_tile<T, B, 128, MODE>(dim3(tiles_c, 1, 1), st, D, P, a, maxkey)));
     }
     if (col_strip) {
       put(a, 0, col);
-      TRY((launch_tile<T, 128, B, MODE>(dim3(tiles_r, 1, 1), st, D, P, a, maxkey)));
+      if (B == 128) TRY((launch_tile<T, 64, 128, MODE>(dim3(2 * tiles_r, 1, 1), st, D, P, a, maxkey)));
+      else TRY((launch_tile<T, 128, B, MODE>(dim3(tiles_r, 1, 1), st, D, P, a, maxkey)));
     }
     return FW_OK;
   }
