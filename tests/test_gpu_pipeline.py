@@ -286,3 +286,22 @@ def test_pipeline_pageable_large_slices():
     src = gen.sources(n, 947, 16)
     np.testing.assert_array_equal(D[src].astype(np.float64), oracle.dijkstra(W, src))
     assert next_consistency(W, D, P, exact=True, rows=src) == 0
+
+
+def test_pipeline_int32_native_keys():
+    """INT32 weights above the FP32 key range (max_w > 65534): native INT32 keys (VIADDMNMX),
+    speculative because (n-1) * max_w exceeds the INT32 key bound; every chunk check passes."""
+    n = 520
+    W = gen.generate("er_int", n, 970, p=1.0, lo=1, hi=100000)
+    D, P, st = check(W, 1, expect_chunks=5)
+    assert st.p_method == 2 and st.compute_f32 == 0
+
+
+def test_pipeline_int32_round_tags():
+    """INT32 weights beyond every key range (max_w > 4194302) with no-edge entries: round tags in
+    INT32 arithmetic ((n-1) * max_w >= 2^24, so no FP32 compute; < FW_INF_I32, the domain rule)
+    through the pipeline."""
+    n = 256
+    W = gen.generate("er_int", n, 971, p=0.05, lo=4_195_000, hi=4_200_000)
+    D, P, st = check(W, 1, expect_chunks=2)
+    assert st.p_method == 1 and st.compute_f32 == 0
