@@ -180,9 +180,9 @@ int smem_attr(const void *fn, int bytes) {
 }
 
 // Largest initial/stored distance for which key sums stay exact (kernels header, KEY mode):
-// FP32: 2*(T*128+127) < 2^24; INT32: 2*(T*128+127) < FW_INF_I32 (INF + key < 2^31 as well).
-constexpr int64_t kKeyMaxF32 = 65534;
-constexpr int64_t kKeyMaxI32 = 4194302;
+// FP32: 2*(T*256+255) < 2^24; INT32: 2*(T*256+255) < FW_INF_I32 (INF + key < 2^31 as well).
+constexpr int64_t kKeyMaxF32 = 32766;
+constexpr int64_t kKeyMaxI32 = 2097150;
 
 int ensure_events(Ctx &c, size_t count) {
   while (c.events.size() < count) {
@@ -573,7 +573,7 @@ struct Attempt {
 };
 
 int key_limit_f32() {
-  const float f = (float)(kKeyMaxF32 * 128 + 127);
+  const float f = (float)(kKeyMaxF32 * kKeyMul + kKeyMask);
   int b;
   memcpy(&b, &f, 4);
   return b;
@@ -609,7 +609,7 @@ int make_plan(bool int_t, bool want_p, const int *h_flags, int64_t n, std::vecto
     const int64_t kmax = int_t ? kKeyMaxI32 : kKeyMaxF32;
     if (maxw <= (double)kmax && !(int_t && plan.size() && plan[0].key_static))
       plan.push_back({MODE_KEY, false, !has_inf || path_max <= (double)kmax,
-                      int_t ? (int)(kKeyMaxI32 * 128 + 127) : key_limit_f32()});
+                      int_t ? (int)(kKeyMaxI32 * kKeyMul + kKeyMask) : key_limit_f32()});
   }
   if (want_p && (plan.empty() || !plan.back().key_static)) plan.push_back({MODE_TAG, f32_exact, true, 0});
   if (!want_p) plan.push_back({MODE_PLAIN, f32_exact, true, 0});

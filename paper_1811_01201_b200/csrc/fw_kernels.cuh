@@ -17,11 +17,11 @@
 //
 // P modes (reading R9):
 //   PLAIN   distances only.
-//   KEY_*   integer-valued data: every stored value is a key D' = D*128 + (column & 127).
-//           A candidate a'_ik + b'_kj = (D_ik + D_kj)*128 + (k&127) + (j&127), so the
+//   KEY_*   integer-valued data: every stored value is a key D' = D*256 + (column & 255).
+//           A candidate a'_ik + b'_kj = (D_ik + D_kj)*256 + (k&255) + (j&255), so the
 //           minimum over k is the minimum distance AND, among ties, the smallest k — the
 //           arg-min comes for free with the same instruction count. The epilogue recovers
-//           k, stores D' = sum - (k&127) and P[i][j] = k (the paper's last intermediate
+//           k, stores D' = sum - (k&255) and P[i][j] = k (the paper's last intermediate
 //           vertex); a per-row pointer-jumping pass turns it into next hops.
 //           Exact while every key sum stays below 2^24 (FP32) / 2^30 (INT32); the host
 //           verifies the bound (statically, or from the max stored key after the solve).
@@ -40,6 +40,12 @@ constexpr int kBK = 32;               // k-chunk staged per pipeline stage
 constexpr int kStages = 3;            // cp.async pipeline depth (one barrier per chunk)
 constexpr int kTerm = 0x40000000;     // terminal bit used by the next-hop pointer jumping
 constexpr int kP1Side = 16;           // phase 1: kP1Side^2 threads, (BS/kP1Side)^2 elements each
+// Key encoding: a stored key is D * kKeyMul + (column & kKeyMask); the low
+// kKeyBits bits of a candidate sum carry k within a 256-aligned window of two 128-blocks, so a
+// single pass may relax through up to 256 consecutive k (two rounds of BS = 128).
+constexpr int kKeyBits = 8;
+constexpr int kKeyMul = 1 << kKeyBits;
+constexpr int kKeyMask = kKeyMul - 1;
 
 enum Mode { MODE_PLAIN = 0, MODE_TAG = 1, MODE_KEY = 2 };
 __host__ __device__ constexpr bool is_key(int m) { return m == MODE_KEY; }
@@ -51,13 +57,13 @@ template <> struct Num<float> {
   static __device__ __forceinline__ float acc_init() { return __int_as_float(0x7f800000); }
   static __device__ __forceinline__ bool bad(float v) { return !(v >= 0.0f); }  // NaN or < 0
   static __device__ __forceinline__ bool finite(float v) { return v < inf(); }
-  static __device__ __forceinline__ int low7(float v) { return (int)v & 127; }   // v < 2^24
+  static __device__ __forceinline__ int lowk(float v) { return (int)v & kKeyMask; }   // v < 2^24
   static __device__ __forceinline__ float from_int(int v) { return (float)v; }
   static __device__ __forceinline__ int bits(float v) { return __float_as_int(v); }
-  static __device__ __forceinline__ float encode(float v, int col) {       // key D*128 + col'
-    return finite(v) ? v * 128.0f + (float)(col & 127) : v;
+  static __device__ __forceinline__ float encode(float v, int col) {       // key D*256 + col'
+    return finite(v) ? v * (float)kKeyMul + (float)(col & kKeyMask) : v;
   }
-  static __device__ __forceinline__ float decode(float k) { return finite(k) ? floorf(k * 0.0078125f) : k; }
+  static __device__ __forceinline__ float decode(float k) { return finite(k) ? floorf(k * (1.0f / kKeyMul)) : k; }
 };
 template <> struct Num<int32_t> {
   static constexpr bool kIsInt = true;
@@ -65,13 +71,13 @@ template <> struct Num<int32_t> {
   static __device__ __forceinline__ int32_t acc_init() { return 0x7FFFFFFF; }
   static __device__ __forceinline__ bool bad(int32_t v) { return v < 0 || v > 0x3FFFFFFF; }
   static __device__ __forceinline__ bool finite(int32_t v) { return v < 0x3FFFFFFF; }
-  static __device__ __forceinline__ int low7(int32_t v) { return v & 127; }
+  static __device__ __forceinline__ int lowk(int32_t v) { return v & kKeyMask; }
   static __device__ __forceinline__ int32_t from_int(int v) { return v; }
   static __device__ __forceinline__ int bits(int32_t v) { return v; }
   static __device__ __forceinline__ int32_t encode(int32_t v, int col) {
-    return finite(v) ? v * 128 + (col & 127) : v;
+    return finite(v) ? v * kKeyMul + (col & kKeyMask) : v;
   }
-  static __device__ __forceinline__ int32_t decode(int32_t k) { return finite(k) ? (k >> 7) : k; }
+  static __device__ __forceinline__ int32_t decode(int32_t k) { return finite(k) ? (k >> kKeyBits) : k; }
 };
 
 template <typename T> struct Vec4;
@@ -345,7 +351,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
   const TileSlot te = tile_slot<TM, TN, DUAL>(g, ctaid(0), ctaid(1), ctaid(2));
   const int mr_lo = te.mr_lo, mr_hi = te.mr_hi, mc_lo = te.mc_lo, mc_hi = te.mc_hi;
-  const int kgrp = (g.colstrip ? te.j0 : g.kb) & ~127;
+  const int kgrp = (g.colstrip ? te.j0 : g.kb) & ~kKeyMask;
   const int tag = g.colstrip ? te.j0 >> 7 : g.tag;
   int kmax = 0;
 #pragma unroll
@@ -370,7 +376,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
         if (chg[e]) {
           any = true;
           if (is_key(MODE)) {
-            const int kk = Num<T>::low7(m - Num<T>::from_int(j & 127));   // arg-min k & 127
+            const int kk = Num<T>::lowk(m - Num<T>::from_int(j & kKeyMask));   // arg-min k & kKeyMask
             const T key = m - Num<T>::from_int(kk);
             vset(nv, e, key);
             kmax = max(kmax, Num<T>::bits(key));
@@ -439,7 +445,7 @@ __device__ __forceinline__ int tmin(int a, int b) { return min(a, b); }
 // registers (R = BS/32). Step k reads row k from sD and column k from its transposed copy
 // sDT (one vector load each); the owners of row k+1 and column k+1 publish them to shared
 // memory before the barrier, so no other element needs mirroring.
-// Key mode: candidate (d'[a][k] - (k&127)) + d'[k][b] = S*128 + (b&127) is directly the new
+// Key mode: candidate (d'[a][k] - (k&255)) + d'[k][b] = S*256 + (b&255) is directly the new
 // key when S < D, so min() keeps keys exact; P[a][b] <- k (last improving k) on change.
 // R consecutive values of shared memory into registers with the widest aligned vector loads.
 template <typename T, int R>
@@ -499,7 +505,7 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
       T colv[R], rowv[R];
       lds_vec<T, R>(colv, &colb[buf][R * ty]);   // d[a][k], own rows
       lds_vec<T, R>(rowv, &rowb[buf][R * tx]);   // d[k][b], own cols
-      const T kp = is_key(MODE) ? Num<T>::from_int((kb + k) & 127) : (T)0;
+      const T kp = is_key(MODE) ? Num<T>::from_int((kb + k) & kKeyMask) : (T)0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         // exact (keys are integers < 2^24 / 2^30); INF must stay INF (INT32 sentinel arithmetic)
@@ -630,42 +636,42 @@ phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r
 }
 
 // Phase 1, FP32 keyed mode, without a per-relaxation select for P. The running value of
-// (a, b) is kept in the form  x = D*128 - 0.5  while unchanged, and a candidate through k is
-// the integer  c_k = D[a][k]*128 + k' + D[k][b]*128  (k' = (kb + k) & 127, increasing in k
+// (a, b) is kept in the form  x = D*256 - 0.5  while unchanged, and a candidate through k is
+// the integer  c_k = D[a][k]*256 + k' + D[k][b]*256  (k' = (kb + k) & 255, increasing in k
 // inside a block): c_k < x  <=>  D[a][k] + D[k][b] < D (strict, P:125 / reading R2), and the
 // minimum over the sequence is the smallest distance reached first, with its k in the low 7
 // bits — the sequential strict-< result of the paper's loop, with one FADD + one FMNMX per
-// relaxation. Row k+1 is published as D*128 (B side), column k+1 as D*128 + k' (A side), both
-// recovered as floor((x + 0.5) / 128) * 128. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
+// relaxation. Row k+1 is published as D*256 (B side), column k+1 as D*256 + k' (A side), both
+// recovered as floor((x + 0.5) / 256) * 256. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
 template <int BS, int NT = kP1Side>
 __global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
 phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
                       int *maxkey) {
   constexpr int R = BS / NT;
   static_assert(R % 2 == 0, "step parity = register slot parity needs an even R");
-  __shared__ __align__(16) float rowb[2][2][BS];   // rows k, k+1, B form D*128  (pair parity)
-  __shared__ __align__(16) float2 colb[2][BS];     // (column k, column k+1) per row, A form D*128 + k'
+  __shared__ __align__(16) float rowb[2][2][BS];   // rows k, k+1, B form D*256  (pair parity)
+  __shared__ __align__(16) float2 colb[2][BS];     // (column k, column k+1) per row, A form D*256 + k'
   const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
   float *Dk = D + (int64_t)r0 * ld + kb;
-  const int kgrp = kb & ~127, klow = kb & 127;
+  const int kgrp = kb & ~kKeyMask, klow = kb & kKeyMask;
   float x[R][R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     float key[R];
-    lds_vec<float, R>(key, Dk + (int64_t)(R * ty + r) * ld + R * tx);  // D*128 + ((kb+b)&127) or +inf
+    lds_vec<float, R>(key, Dk + (int64_t)(R * ty + r) * ld + R * tx);  // D*256 + ((kb+b)&255) or +inf
 #pragma unroll
-    for (int c = 0; c < R; ++c) x[r][c] = key[c] - (float)(klow + R * tx + c) - 0.5f;   // D*128 - 0.5
+    for (int c = 0; c < R; ++c) x[r][c] = key[c] - (float)(klow + R * tx + c) - 0.5f;   // D*256 - 0.5
   }
   // steps k and k+1 per barrier (the sequential loop's values, two steps at a time): every
   // thread brings row / column k+1 to their state after step k itself,
-  //   col'[a] = min(col_k1[a], col_k[a] + D[k][k+1]*128 + 1)   ((k+1)' = k' + 1 inside the block)
-  //   row'[b] = min(row_k1[b], D[k+1][k]*128 + row_k[b])
+  //   col'[a] = min(col_k1[a], col_k[a] + D[k][k+1]*256 + 1)   ((k+1)' = k' + 1 inside the block)
+  //   row'[b] = min(row_k1[b], D[k+1][k]*256 + row_k[b])
   // and folds both candidates into x with FADD2 + FMNMX3: x = min(x, c_k, c'_k+1) (min is exact,
   // every candidate is the same integer sum as in the one-step loop).
   if (ty == 0) {
 #pragma unroll
     for (int c = 0; c < R; ++c) {
-      rowb[0][0][R * tx + c] = x[0][c] + 0.5f;                           // D*128
+      rowb[0][0][R * tx + c] = x[0][c] + 0.5f;                           // D*256
       rowb[0][1][R * tx + c] = x[1][c] + 0.5f;
     }
   }
@@ -682,8 +688,8 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
       float rk[R], rk1[R];
       lds_vec<float, R>(rk, &rowb[buf][0][R * tx]);    // B side, own cols
       lds_vec<float, R>(rk1, &rowb[buf][1][R * tx]);
-      const float d01 = rowb[buf][0][k + 1] + 1.0f;              // D[k][k+1]*128 + 1
-      const float d10 = colb[buf][k + 1].x - (float)(klow + k);  // D[k+1][k]*128 (exact; inf stays)
+      const float d01 = rowb[buf][0][k + 1] + 1.0f;              // D[k][k+1]*256 + 1
+      const float d10 = colb[buf][k + 1].x - (float)(klow + k);  // D[k+1][k]*256 (exact; inf stays)
 #pragma unroll
       for (int c = 0; c < R; ++c) rk1[c] = fminf(rk1[c], d10 + rk[c]);
 #pragma unroll
@@ -701,16 +707,16 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
         if (owner == ty) {
 #pragma unroll
           for (int c = 0; c < R; ++c) {
-            rowb[buf ^ 1][0][R * tx + c] = floorf((x[s2][c] + 0.5f) * 0.0078125f) * 128.0f;
-            rowb[buf ^ 1][1][R * tx + c] = floorf((x[s3][c] + 0.5f) * 0.0078125f) * 128.0f;
+            rowb[buf ^ 1][0][R * tx + c] = floorf((x[s2][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
+            rowb[buf ^ 1][1][R * tx + c] = floorf((x[s3][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
           }
         }
         if (owner == tx) {
           const float kp = (float)(klow + k + 2);
 #pragma unroll
           for (int r = 0; r < R; ++r)
-            colb[buf ^ 1][R * ty + r] = make_float2(floorf((x[r][s2] + 0.5f) * 0.0078125f) * 128.0f + kp,
-                                                    floorf((x[r][s3] + 0.5f) * 0.0078125f) * 128.0f + kp + 1.0f);
+            colb[buf ^ 1][R * ty + r] = make_float2(floorf((x[r][s2] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp,
+                                                    floorf((x[r][s3] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp + 1.0f);
         }
       }
       __syncthreads();
@@ -724,7 +730,7 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
       const float v = x[r][c];
       if (v < __int_as_float(0x7f800000) && v == floorf(v)) {   // an integer: strictly improved
         const int a = R * ty + r, b = R * tx + c;
-        const float hi = floorf(v * 0.0078125f) * 128.0f;
+        const float hi = floorf(v * (1.0f / kKeyMul)) * (float)kKeyMul;
         const int kk = (int)(v - hi);
         const float key = hi + (float)(klow + b);
         Dk[(int64_t)a * ld + b] = key;
@@ -781,7 +787,7 @@ __global__ void validate_kernel(const T *src, int64_t lds, int64_t nrows, int64_
 }
 
 // Copy W (n x n, lds) into the padded n_pad x n_pad working matrix (ld): padded entries INF,
-// diagonal 0 (R4, R11); key mode stores D*128 + (j&127). P (tags / last k) initialised to -1
+// diagonal 0 (R4, R11); key mode stores D*256 + (j&255). P (tags / last k) initialised to -1
 // ("no intermediate yet"). src may alias D (in-place solve).
 // Source value in the compute type C: identity, or INT32 -> FP32 (FW_INF_I32 -> +inf; finite
 // INT32 weights below 2^24 are exact in FP32 — the host only picks FP32 compute when every
