@@ -150,6 +150,8 @@ struct Ctx {
   std::vector<cudaEvent_t> pev;    // host pipeline: per-chunk landed / finished events
   int pipe_tiles = -1;             // host pipeline chunk in tile-rows (-1 auto, 0 off)
   int pipe_first = 8;              // auto geometry: first chunk (tile-rows; env FW_PIPE_FIRST)
+  bool pairs = true;               // two rounds per phase-3 pass for keyed / plain solves (env FW_PAIRS=0: off)
+  bool last_pairs = false;         // the last solve ran in pairs (stats layout)
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
   int rank = 0, world = 1;
   int ngpus_max = 1;               // fw_init's limit (0 there = every visible device)
@@ -416,6 +418,67 @@ struct Rounds {
     return launch_tile<T, 128, 128, MODE>(dim3((unsigned)total, 1, 1), st, D, P, a, maxkey);
   }
 
+  // ---- two rounds per phase-3 pass (keyed / plain solves, one GPU, all rows, BS = 128) ------
+  // Pair Pp = rounds a = 2Pp, b = a + 1. Its strip region (block-rows and
+  // block-columns a, b) is brought through both rounds by two sub-rounds of the usual pivot
+  // phases plus one restricted phase-3 launch each (strip3); every other tile then relaxes
+  // through blocks a and b in ONE 256-deep product (pair_bulk) — the sequential result, since A
+  // (columns a, b) and B (rows a, b) have completed both rounds — with one epilogue instead of
+  // two. The next pair's strips go first (pair_prio) so its pivot phases run on the side stream
+  // under the bulk launch.
+  int strip3(cudaStream_t st, int x, int y) {   // row y (columns != x) and column y (rows != x, y) through block x
+    const int kb = x * BS, tiles_c = (int)(n_pad / 128), tiles_r = (int)(nrows / 128);
+    TileArgs t = tile_args(ld, D + (int64_t)lrow(x) * ld, ld, kb, BS, x, nrows, n_pad);
+    const int lo = std::min(x, y) * BS;
+    put(t, 0, Strip{lrow(y), 0, 0, 0, kb, kb + BS, 0});
+    put(t, 1, Strip{0, y * BS, lo, lo + 2 * BS, 0, 0, 1});
+    return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 1, 2), st, D, P, t, maxkey);
+  }
+  int pair_pivot(cudaStream_t st, int Pp) {
+    const int a = 2 * Pp, b = a + 1;
+    TRY(phase1(st, a));
+    TRY(phase2(st, a, true, true));
+    TRY(strip3(st, a, b));
+    TRY(phase1(st, b));
+    TRY(phase2(st, b, true, true));
+    return strip3(st, b, a);
+  }
+  int pair_prio(cudaStream_t st, int Pp) {   // rows / columns c, d = a+2, a+3 through blocks a, b
+    const int a = 2 * Pp, c2 = a + 2, kb = a * BS;
+    const int tiles_c = (int)(n_pad / 128), tiles_r = (int)(nrows / 128);
+    TileArgs t = tile_args(ld, D + (int64_t)lrow(a) * ld, ld, kb, 2 * BS, a, nrows, n_pad);
+    put(t, 0, Strip{lrow(c2), 0, 0, 0, kb, kb + 2 * BS, 0});   // rows c, d (grid.y = 2)
+    put(t, 1, Strip{0, c2 * BS, kb, kb + 4 * BS, 0, 0, 1});    // columns c, d, rows outside a..d
+    return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 2, 2), st, D, P, t, maxkey);
+  }
+  int pair_bulk(cudaStream_t st, int Pp, bool last) {
+    const int a = 2 * Pp, kb = a * BS, hi = kb + (last ? 2 : 4) * BS;
+    TileArgs t = tile_args(ld, D + (int64_t)lrow(a) * ld, ld, kb, 2 * BS, a, nrows, n_pad);
+    put(t, 0, Strip{0, 0, kb, hi, kb, hi, 0});
+    return launch_tile<T, 128, 128, MODE>(dim3((unsigned)(n_pad / 128), (unsigned)(nrows / 128), 1), st, D, P,
+                                          t, maxkey);
+  }
+  int run_pairs(cudaStream_t st, const Events &e) {
+    const int NP = R / 2;
+    cudaStream_t side = c.side;
+    TRY(pair_pivot(st, 0));
+    for (int Pp = 0; Pp < NP; ++Pp) {
+      const bool last = Pp + 1 == NP;
+      if (e.timing) CU(cudaEventRecord(e.ev[3 * Pp], st));        // the pair's phase-3 work starts
+      if (!last) {
+        TRY(pair_prio(st, Pp));
+        CU(cudaEventRecord(e.sync[2 * Pp], st));
+        CU(cudaStreamWaitEvent(side, e.sync[2 * Pp], 0));
+        TRY(pair_pivot(side, Pp + 1));
+        CU(cudaEventRecord(e.sync[2 * Pp + 1], side));
+      }
+      TRY(pair_bulk(st, Pp, last));
+      if (e.timing) CU(cudaEventRecord(e.ev[3 * Pp + 2], st));    // ... and ends
+      if (!last) CU(cudaStreamWaitEvent(st, e.sync[2 * Pp + 1], 0));
+    }
+    return FW_OK;
+  }
+
   // Rounds [K0, K1) of these rows (default: all). A row range of the host pipeline runs
   // its rounds in several calls; every round's pivot strip must have completed that round.
   int run(cudaStream_t st, const Events &e, bool lookahead, int K0 = 0, int K1 = -1) {
@@ -546,6 +609,12 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
     rk.push_back(Rounds<T, MODE>{c, world, p.D, p.P, p.ld, n, n_pad, p.row0, p.nrows, BS, R, maxkey,
                                  {p.strip[0], p.strip[1]}, done});
   if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
+  c.last_pairs = false;
+  if (MODE != MODE_TAG && c.pairs && la && world == 1 && BS == 128 && R % 2 == 0 && R >= 4 &&
+      rk[0].row0 == 0 && rk[0].nrows == n_pad) {
+    c.last_pairs = true;
+    return rk[0].run_pairs(st, ev);
+  }
   return rk[0].run(st, ev, la);
 }
 
@@ -906,7 +975,7 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   float ms = 0.f;
   CU(cudaEventElapsedTime(&ms, e_begin, e_end));
   s.solve_ms = ms;
-  s.phase3_launches = R;
+  s.phase3_launches = c.last_pairs ? R - 1 : R;
   s.kernel_launches = g_launches - launches0;
   // phase-3 relaxations of this process's rows: rows and columns outside the round's strips
   double relax = 0;
@@ -916,8 +985,25 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
       const double rows = (double)p.nrows - ((kb >= p.row0 && kb < p.row0 + p.nrows) ? BS : 0);
       relax += rows * (double)(n_pad - BS) * BS;
     }
+  if (c.last_pairs)   // every pair relaxes all tiles outside its strip region through 256 k
+    relax = (double)(R / 2) * (double)(n_pad - 2 * BS) * (double)(n_pad - 2 * BS) * (2.0 * BS);
   s.phase3_relaxations = relax;
-  if (timing) {
+  if (timing && c.last_pairs) {
+    auto at = [&](cudaEvent_t e) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e_begin, e);
+      return (double)t;
+    };
+    double prev = at(e_init);
+    for (int Pp = 0; Pp < R / 2; ++Pp) {
+      const double p3s = at(ev.ev[3 * Pp]), p3e = at(ev.ev[3 * Pp + 2]);
+      s.phase3_ms += p3e - p3s;
+      s.phase1_ms += p3s - prev;     // pivot path not hidden under the previous pair (phases 1-2 + strip3)
+      if (Pp + 1 < R / 2) s.phase2_ms += at(ev.sync[2 * Pp + 1]) - at(ev.sync[2 * Pp]);   // pivot path of the next pair, side stream
+      prev = p3e;
+    }
+    s.post_ms = at(e_post) - prev;
+  } else if (timing) {
     // absolute event times (ms since e_begin); with the look-ahead, phases 1-2 of round K
     // run on the side stream from the wait for round K-1's look-ahead tiles, concurrently
     // with the rest of round K-1's phase 3
@@ -1749,6 +1835,8 @@ int fw_init(int ngpus_max, unsigned flags) {
   CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi));
   const char *la = getenv("FW_LOOKAHEAD");
   c->lookahead = !(la && la[0] == '0');
+  const char *pr = getenv("FW_PAIRS");
+  c->pairs = !(pr && pr[0] == '0');
   const char *pf = getenv("FW_PIPE_FIRST");   // tuning: first chunk of the auto host pipeline
   if (pf && atoi(pf) >= 1 && atoi(pf) <= 64) c->pipe_first = atoi(pf);
   g_ctx = c;

@@ -234,7 +234,7 @@ __device__ __forceinline__ TileSlot tile_slot(const TileArgs &g, int bxr, int by
   t.mc_lo = z ? g.mc_lo[1] : g.mc_lo[0];
   t.mc_hi = z ? g.mc_hi[1] : g.mc_hi[0];
   const int xrow = z ? g.xrow[1] : g.xrow[0];
-  const int bx = xrow ? 0 : bxr, by = xrow ? bxr : byr;
+  const int bx = xrow ? byr : bxr, by = xrow ? bxr : byr;   // xrow: blockIdx.y steps tile columns
   t.i0 = (z ? g.row0[1] : g.row0[0]) + by * TM;
   t.j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
   t.skip = (t.i0 >= t.mr_lo && t.i0 + TM <= t.mr_hi) || (t.j0 >= t.mc_lo && t.j0 + TN <= t.mc_hi) ||

@@ -480,3 +480,34 @@ def test_fw_path_on_gpu_results(kind, path):
         assert p[0] == i and p[-1] == j and len(set(p)) == len(p)
         s = sum(w[a, b] for a, b in zip(p, p[1:]))
         assert abs(s - Dd[i, j]) <= 1e-5 * max(1.0, Dd[i, j]), (i, j, s, Dd[i, j])
+
+
+# ---- two rounds per phase-3 pass: keyed / plain solves, BS = 128, R even ----
+@pytest.mark.parametrize("kind,n,path", [("complete_int", 512, "next"), ("complete_int", 700, "next"),
+                                         ("complete_int", 1000, "lastk"), ("complete_real", 768, None),
+                                         ("er_int", 1024, "next"), ("er_int_f32", 900, "next")])
+def test_pair_rounds_against_oracle(kind, n, path, monkeypatch):
+    """Pairs of rounds (strip region by two sub-rounds, bulk through 256 k in one pass): D
+    bit-exact against the oracle (rel 1e-5 for reals) and paths valid; D identical to the
+    one-round-per-pass schedule (FW_PAIRS=0) for integer data."""
+    W = gen.generate(kind, n, 990 + n, p=0.02, lo=1, hi=1000)
+    D, P = solve(W, 128, path)
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    if path:
+        bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5, mode=path)
+        assert bad == 0, f"{bad} invalid paths, first at {divmod(first, n)}"
+    monkeypatch.setenv("FW_PAIRS", "0")
+    D0, _ = solve(W, 128, path)
+    if exact:
+        np.testing.assert_array_equal(D, D0)
+
+
+def test_pair_rounds_ring_closed_form():
+    """Ring + chords (long chains through every block) under the pair schedule."""
+    n = 1280
+    W = gen.ring_with_chords(n, 5, 300)
+    D, P = solve(W, 128, "next")
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    np.testing.assert_array_equal(D, ((j - i) % n).astype(np.float32))
+    np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % n))
