@@ -383,17 +383,44 @@ struct Rounds {
   // through block K via its FIRST block-K vertex u (D[i][u] needs no block-K intermediate,
   // D[u][j] is complete), and the strip's own elements only need it before these rows' next
   // pivot phases or their end.
-  int run_plain(cudaStream_t st, int K0, int K1) {
+  // With pairs (keyed / plain, BS = 128): rounds K, K+1 (K even) share one 256-deep launch that
+  // leaves both column blocks alone; those blocks then take, after the own-block strip batch, the
+  // partner block too (colstrip = 2: even blocks through their odd partner, then odd through
+  // even, so no launch reads a tile it writes). Same argument: with pivots complete for both
+  // rounds, the first block-K or block-K+1 vertex of a path is reached from unrelaxed operands.
+  int run_plain(cudaStream_t st, int K0, int K1, bool pairs = false) {
     if (K0 >= K1 || nrows == 0) return FW_OK;
+    pairs = pairs && BS == 128 && MODE != MODE_TAG;
+    int fused0 = -1, fused1 = -1;          // blocks [fused0, fused1) went through in pairs
     for (int K = K0; K < K1; ++K) {
       const int kb = K * BS;
+      if (pairs && K % 2 == 0 && K + 1 < K1) {
+        TileArgs a = tile_args(ld, bstrip(K), ld, kb, 2 * BS, K, nrows, n_pad);
+        put(a, 0, Strip{0, 0, 0, 0, kb, kb + 2 * BS, 0});
+        TRY((launch_tile<T, 128, 128, MODE>(dim3((unsigned)(n_pad / 128), (unsigned)(nrows / 128), 1), st, D, P,
+                                            a, maxkey)));
+        if (fused0 < 0) fused0 = K;
+        fused1 = K + 2;
+        ++K;
+        continue;
+      }
       TRY(phase3(st, K, 0, 0, kb, kb + BS));
     }
     TileArgs a = tile_args(ld, Dg, ld, 0, BS, 0, nrows, n_pad);
     a.colstrip = 1;
     put(a, 0, Strip{0, K0 * BS, 0, 0, 0, 0, 0});
-    return launch_tile<T, 128, 128, MODE>(dim3((unsigned)(K1 - K0), (unsigned)(nrows / 128), 1), st, D, P, a,
-                                          maxkey);
+    TRY((launch_tile<T, 128, 128, MODE>(dim3((unsigned)(K1 - K0), (unsigned)(nrows / 128), 1), st, D, P, a,
+                                        maxkey)));
+    if (fused0 < 0) return FW_OK;
+    for (int par = 0; par < 2; ++par) {     // even blocks through their partner, then odd ones
+      TileArgs x = tile_args(ld, Dg, ld, 0, BS, 0, nrows, n_pad);
+      x.colstrip = 2;
+      x.colstep = 2;
+      put(x, 0, Strip{0, (fused0 + par) * BS, 0, 0, 0, 0, 0});
+      TRY((launch_tile<T, 128, 128, MODE>(dim3((unsigned)((fused1 - fused0) / 2), (unsigned)(nrows / 128), 1), st,
+                                          D, P, x, maxkey)));
+    }
+    return FW_OK;
   }
 
   // Look-ahead (BS = 128): one ordered phase-3 launch per round whose first nprio CTAs are
@@ -429,7 +456,7 @@ struct Rounds {
   int strip3(cudaStream_t st, int x, int y) {   // row y (columns != x) and column y (rows != x, y) through block x
     const int kb = x * BS, tiles_c = (int)(n_pad / 128), tiles_r = (int)(nrows / 128);
     TileArgs t = tile_args(ld, D + (int64_t)lrow(x) * ld, ld, kb, BS, x, nrows, n_pad);
-    const int lo = std::min(x, y) * BS;
+    const int lo = lrow(std::min(x, y));    // local rows (the pipeline's row ranges)
     put(t, 0, Strip{lrow(y), 0, 0, 0, kb, kb + BS, 0});
     put(t, 1, Strip{0, y * BS, lo, lo + 2 * BS, 0, 0, 1});
     return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 1, 2), st, D, P, t, maxkey);
@@ -447,22 +474,25 @@ struct Rounds {
     const int a = 2 * Pp, c2 = a + 2, kb = a * BS;
     const int tiles_c = (int)(n_pad / 128), tiles_r = (int)(nrows / 128);
     TileArgs t = tile_args(ld, D + (int64_t)lrow(a) * ld, ld, kb, 2 * BS, a, nrows, n_pad);
-    put(t, 0, Strip{lrow(c2), 0, 0, 0, kb, kb + 2 * BS, 0});   // rows c, d (grid.y = 2)
-    put(t, 1, Strip{0, c2 * BS, kb, kb + 4 * BS, 0, 0, 1});    // columns c, d, rows outside a..d
+    put(t, 0, Strip{lrow(c2), 0, 0, 0, kb, kb + 2 * BS, 0});                // rows c, d (grid.y = 2)
+    put(t, 1, Strip{0, c2 * BS, lrow(a), lrow(a) + 4 * BS, 0, 0, 1});       // columns c, d, rows outside a..d
     return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 2, 2), st, D, P, t, maxkey);
   }
   int pair_bulk(cudaStream_t st, int Pp, bool last) {
-    const int a = 2 * Pp, kb = a * BS, hi = kb + (last ? 2 : 4) * BS;
+    const int a = 2 * Pp, kb = a * BS, w = (last ? 2 : 4) * BS;
     TileArgs t = tile_args(ld, D + (int64_t)lrow(a) * ld, ld, kb, 2 * BS, a, nrows, n_pad);
-    put(t, 0, Strip{0, 0, kb, hi, kb, hi, 0});
+    put(t, 0, Strip{0, 0, lrow(a), lrow(a) + w, kb, kb + w, 0});
     return launch_tile<T, 128, 128, MODE>(dim3((unsigned)(n_pad / 128), (unsigned)(nrows / 128), 1), st, D, P,
                                           t, maxkey);
   }
-  int run_pairs(cudaStream_t st, const Events &e) {
-    const int NP = R / 2;
+  // Rounds [K0, K1) (K0, K1 even, blocks K0..K1-1 inside these rows) in pairs.
+  int run_pairs(cudaStream_t st, const Events &e, int K0 = 0, int K1 = -1) {
+    if (K1 < 0) K1 = R;
+    const int P0 = K0 / 2, NP = K1 / 2;
+    if (P0 >= NP) return FW_OK;
     cudaStream_t side = c.side;
-    TRY(pair_pivot(st, 0));
-    for (int Pp = 0; Pp < NP; ++Pp) {
+    TRY(pair_pivot(st, P0));
+    for (int Pp = P0; Pp < NP; ++Pp) {
       const bool last = Pp + 1 == NP;
       if (e.timing) CU(cudaEventRecord(e.ev[3 * Pp], st));        // the pair's phase-3 work starts
       if (!last) {
@@ -1356,12 +1386,19 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
     Rounds<C, MODE> rk{c, 1, D + r0 * g.ld, P ? P + r0 * g.ld : nullptr, g.ld, g.n, g.n_pad, r0,
                        g.rows_of(t1 - t0), g.BS, g.R, d_flags + 2, {nullptr, nullptr}, d_done, D};
     const int own0 = std::max(K0, std::min(K1, t0)), own1 = std::max(own0, std::min(K1, t1));
-    TRY(rk.run_plain(st, K0, own0));                 // pivots in earlier rows
-    if (own1 > own0) {
-      CU(cudaMemsetAsync(d_done, 0, 4 * (size_t)g.R, st));
-      TRY(rk.run(st, ev, la, own0, own1));           // own pivots
+    const bool plain_pairs = c.pairs && t1 - t0 >= 32;
+    TRY(rk.run_plain(st, K0, own0, plain_pairs));    // pivots in earlier rows
+    if (own1 > own0) {                               // own pivots: pairs of rounds (§4.9) or one by one
+      // (pairs only on wide row ranges: below 32 tile-rows the two sub-rounds of pivot phases
+      // take longer than the bulk launch they hide under)
+      if (MODE != MODE_TAG && c.pairs && la && own0 % 2 == 0 && (own1 - own0) % 2 == 0 && t1 - t0 >= 32) {
+        TRY(rk.run_pairs(st, ev, own0, own1));
+      } else {
+        CU(cudaMemsetAsync(d_done, 0, 4 * (size_t)g.R, st));
+        TRY(rk.run(st, ev, la, own0, own1));
+      }
     }
-    return rk.run_plain(st, own1, K1);               // pivots in later rows
+    return rk.run_plain(st, own1, K1, plain_pairs);  // pivots in later rows
   };
   // arrival: init + rounds [0, t_c+1) of each chunk as it lands; the next chunk is put in flight
   // after this one's work is queued (a pageable copy keeps the host busy meanwhile)

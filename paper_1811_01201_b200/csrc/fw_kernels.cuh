@@ -163,7 +163,8 @@ struct TileArgs {
   // Column-strip batch (host pipeline, BS = 128): every CTA relaxes its tile
   // through the block of its own columns, k in [j0, j0 + 128): A = the tile itself, B = rows
   // j0.. of the matrix whose row 0 is at g.B (pitch ldb), tag = j0 / 128 (that block's round).
-  int colstrip;
+  int colstrip;                  // 2: through the PARTNER block of a 256-aligned pair (j0 ^ 128)
+  int colstep;                   // tile-column stride of the grid (0 or 1: consecutive)
   // Ordered phase-3 launch (order = 1, 1-D grid, 128 x 128 tiles): blockIdx.x enumerates the
   // round's tiles with the look-ahead set first — A1 = tile-row rowN (next pivot block-row,
   // -1 if not local) except tile-column colK; A2 = tile-column colN except tile-rows rowK and
@@ -203,7 +204,7 @@ struct TileSlot {
   bool skip;
 };
 
-template <int TM, int TN, bool DUAL>
+template <int TM, int TN, bool DUAL, bool STEP = true>
 __device__ __forceinline__ TileSlot tile_slot(const TileArgs &g, int bxr, int byr, int bzr) {
   TileSlot t{};
   // select the strip description without dynamic indexing (keeps g out of local memory)
@@ -236,7 +237,8 @@ __device__ __forceinline__ TileSlot tile_slot(const TileArgs &g, int bxr, int by
   const int xrow = z ? g.xrow[1] : g.xrow[0];
   const int bx = xrow ? byr : bxr, by = xrow ? bxr : byr;   // xrow: blockIdx.y steps tile columns
   t.i0 = (z ? g.row0[1] : g.row0[0]) + by * TM;
-  t.j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
+  if constexpr (STEP) t.j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN * (g.colstep > 1 ? g.colstep : 1);
+  else t.j0 = (z ? g.col0[1] : g.col0[0]) + bx * TN;
   t.skip = (t.i0 >= t.mr_lo && t.i0 + TM <= t.mr_hi) || (t.j0 >= t.mc_lo && t.j0 + TN <= t.mc_hi) ||
            t.i0 >= g.rows_lim || t.j0 >= g.cols_lim;
   return t;
@@ -262,12 +264,15 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   T *smem = reinterpret_cast<T *>(smem_raw);
 
   // tile origin and exclusions (computed again after the main loop: see the epilogue)
-  const TileSlot ts = tile_slot<TM, TN, DUAL>(g, blockIdx.x, blockIdx.y, blockIdx.z);
+  // colstrip 2 / colstep (pairs of plain rounds) never occur with round tags: compiled out there
+  constexpr bool PAIRS = MODE != MODE_TAG;
+  const int cstrip = g.colstrip;
+  const TileSlot ts = tile_slot<TM, TN, DUAL, PAIRS>(g, blockIdx.x, blockIdx.y, blockIdx.z);
   if (ts.skip) return;
   const int i0 = ts.i0, j0 = ts.j0;
 
   const int64_t ld = g.ld;
-  const int kb = g.colstrip ? j0 : g.kb;
+  const int kb = PAIRS ? (cstrip ? (cstrip == 2 ? (j0 ^ 128) : j0) : g.kb) : (g.colstrip ? j0 : g.kb);
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   // Warm L2 with this tile of D for the epilogue's compare (128-B lines, per-thread
   // addresses): the tile is read once per round from HBM, and its latency was the
@@ -288,7 +293,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   const int b_r = tid / (TN / 4), b_c = (tid % (TN / 4)) * 4;
   const T *a_src = D + (int64_t)(i0 + a_r) * ld + kb + a_c;
   const int64_t ldb = g.ldb;
-  const T *b_src = static_cast<const T *>(g.B) + (int64_t)((g.colstrip ? j0 : 0) + b_r) * ldb + j0 + b_c;
+  const T *b_src = static_cast<const T *>(g.B) + (int64_t)((cstrip ? kb : 0) + b_r) * ldb + j0 + b_c;
 
   auto load_chunk = [&](int stage, int k0) {
     T *as = smem + stage * S::kStage;
@@ -349,10 +354,10 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   }
 
   // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
-  const TileSlot te = tile_slot<TM, TN, DUAL>(g, ctaid(0), ctaid(1), ctaid(2));
+  const TileSlot te = tile_slot<TM, TN, DUAL, PAIRS>(g, ctaid(0), ctaid(1), ctaid(2));
   const int mr_lo = te.mr_lo, mr_hi = te.mr_hi, mc_lo = te.mc_lo, mc_hi = te.mc_hi;
   const int kgrp = (g.colstrip ? te.j0 : g.kb) & ~kKeyMask;
-  const int tag = g.colstrip ? te.j0 >> 7 : g.tag;
+  const int tag = PAIRS ? (cstrip ? (cstrip == 2 ? (te.j0 ^ 128) : te.j0) >> 7 : g.tag) : (g.colstrip ? te.j0 >> 7 : g.tag);
   int kmax = 0;
 #pragma unroll
   for (int r = 0; r < RM; ++r) {
