@@ -953,6 +953,8 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     if (nccl) NC(g_nccl.AllReduce(d_maxkey, d_maxkey, 1, ncclInt32, ncclMax, c.comm, st));
     CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (getenv("FW_DEBUG"))
+      fprintf(stderr, "fwb: speculative key run: max stored key bits %d, limit %d\n", h_flags[2], used.key_limit);
     if (h_flags[2] <= used.key_limit || a + 1 == plan.size()) break;
     CU(cudaMemsetAsync(d_maxkey, 0, 4, st));   // a stored key left the exact range: next plan
   }
@@ -1380,13 +1382,17 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
   // rounds [K0, K1) on tile-rows [t0, t1), pivot strips read in place from the whole matrix:
   // rounds whose pivots lie outside the rows as plain phase-3 launches + one column-strip batch,
   // the rows' own rounds with their pivot phases and the look-ahead
+  bool even_bounds = true;
+  for (int t : g.tb) even_bounds = even_bounds && t % 2 == 0;
   auto run = [&](int t0, int t1, int K0, int K1) -> int {
     if (t1 <= t0 || K1 <= K0) return FW_OK;
     const int64_t r0 = g.rows_of(t0);
     Rounds<C, MODE> rk{c, 1, D + r0 * g.ld, P ? P + r0 * g.ld : nullptr, g.ld, g.n, g.n_pad, r0,
                        g.rows_of(t1 - t0), g.BS, g.R, d_flags + 2, {nullptr, nullptr}, d_done, D};
     const int own0 = std::max(K0, std::min(K1, t0)), own1 = std::max(own0, std::min(K1, t1));
-    const bool plain_pairs = c.pairs && t1 - t0 >= 32;
+    // a fused pair (K, K+1) needs both pivot blocks complete through K+1: they must lie in one
+    // chunk, which holds when every chunk boundary is even
+    const bool plain_pairs = c.pairs && t1 - t0 >= 32 && even_bounds;
     TRY(rk.run_plain(st, K0, own0, plain_pairs));    // pivots in earlier rows
     if (own1 > own0) {                               // own pivots: pairs of rounds (§4.9) or one by one
       // (pairs only on wide row ranges: below 32 tile-rows the two sub-rounds of pivot phases

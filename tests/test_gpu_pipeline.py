@@ -305,3 +305,22 @@ def test_pipeline_int32_round_tags():
     W = gen.generate("er_int", n, 971, p=0.05, lo=4_195_000, hi=4_200_000)
     D, P, st = check(W, 1, expect_chunks=2)
     assert st.p_method == 1 and st.compute_f32 == 0
+
+
+@pytest.mark.parametrize("n,ct", [(8192, 32), (8448, 33), (16384, -1)])
+def test_pipeline_pairs_ring_closed_form(n, ct):
+    """A ring of weight 1 in a complete graph of weight n (every shortest path runs through every
+    later block; no INF, so the keys are statically exact) through the host pipeline where chunks
+    are wide enough for pairs of rounds (8192 in two 32-tile-row chunks, the C4-size auto
+    geometry; 33-tile-row chunks have odd boundaries, so their plain rounds stay single):
+    D = (j - i) mod n and next = i + 1 on every row."""
+    W = np.full((n, n), np.float32(n), dtype=np.float32)
+    i = np.arange(n)
+    W[i, (i + 1) % n] = 1.0
+    D, P, st = solve_pinned(W, ct)
+    assert st.host_chunks >= 2 and st.p_method == 2
+    i = np.arange(n)
+    for r0 in range(0, n, 2048):
+        r = np.arange(r0, min(n, r0 + 2048))
+        np.testing.assert_array_equal(D[r], ((i[None, :] - r[:, None]) % n).astype(np.float32))
+        np.testing.assert_array_equal(P[r], np.where(r[:, None] == i[None, :], r[:, None], (r[:, None] + 1) % n))

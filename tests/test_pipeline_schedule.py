@@ -69,6 +69,118 @@ class Model:
             D[rows, kb] = np.minimum(D[rows, kb], minplus(D[rows, kb], D[kb, kb]))
 
 
+    # ---- two rounds per pass, blocks a, b = 2p, 2p+1 ----
+    def relax(self, rows, cols, ks):
+        """D[rows, cols] <- min(D[rows, cols], D[rows, ks] (x) D[ks, cols]) (one product; 1-D
+        index arrays, or [:, None] / [None, :] shaped ones)."""
+        D = self.D
+        rows, cols, ks = np.ravel(rows), np.ravel(cols), np.ravel(ks)
+        A = D[np.ix_(rows, ks)].copy()
+        B = D[np.ix_(ks, cols)].copy()
+        D[np.ix_(rows, cols)] = np.minimum(D[np.ix_(rows, cols)], minplus(A, B))
+
+    def own_pair(self, a, rows_lo, rows_hi, last):
+        """run_pairs for one pair on rows [rows_lo, rows_hi) (block units): strip region by two
+        sub-rounds, next pair's strips (prio), then the 256-deep bulk."""
+        BS, D = self.BS, self.D
+        n = D.shape[0]
+        blk = lambda k: slice(k * BS, (k + 1) * BS)
+        b = a + 1
+        R0, R1 = rows_lo * BS, rows_hi * BS
+        allc = np.arange(n)
+        for x, y in ((a, b), (b, a)):
+            kb = blk(x)
+            for k in range(kb.start, kb.stop):                      # phase 1 (closure of D_xx)
+                D[kb, kb] = np.minimum(D[kb, kb], D[kb, k:k + 1] + D[k:k + 1, kb])
+            Dxx = D[kb, kb].copy()
+            cols = allc[(allc < kb.start) | (allc >= kb.stop)]
+            D[kb.start:kb.stop, cols] = np.minimum(D[kb.start:kb.stop, cols], minplus(Dxx, D[kb.start:kb.stop, cols]))
+            rws = np.array([r for r in range(R0, R1) if not kb.start <= r < kb.stop])
+            D[np.ix_(rws, np.arange(kb.start, kb.stop))] = np.minimum(
+                D[np.ix_(rws, np.arange(kb.start, kb.stop))], minplus(D[np.ix_(rws, np.arange(kb.start, kb.stop))], Dxx))
+            yb = blk(y)                                              # strip3(x -> y)
+            cols_y = allc[(allc < kb.start) | (allc >= kb.stop)]
+            self.relax(np.arange(yb.start, yb.stop)[:, None], cols_y[None, :], np.arange(kb.start, kb.stop))
+            lo = min(x, y) * BS
+            rws_y = np.array([r for r in range(R0, R1) if not lo <= r < lo + 2 * BS])
+            if len(rws_y):
+                self.relax(rws_y[:, None], np.arange(yb.start, yb.stop)[None, :], np.arange(kb.start, kb.stop))
+        ks = np.arange(a * BS, (a + 2) * BS)
+        w = 2 if last else 4
+        ex = (allc >= a * BS) & (allc < (a + w) * BS)
+        if not last:                                                # prio: rows/cols c, d
+            cd = np.arange((a + 2) * BS, (a + 4) * BS)
+            self.relax(cd[:, None], allc[~((allc >= a * BS) & (allc < (a + 2) * BS))][None, :], ks)
+            rws = np.array([r for r in range(R0, R1) if not a * BS <= r < (a + 4) * BS])
+            if len(rws):
+                self.relax(rws[:, None], cd[None, :], ks)
+        rws = np.array([r for r in range(R0, R1) if not ex[r]])     # bulk
+        if len(rws):
+            self.relax(rws[:, None], allc[~ex][None, :], ks)
+
+    def plain_pairs(self, K0, K1, rows):
+        """run_plain with pairs: 256-deep launches leaving both column blocks, own-block strip
+        batch, then partner-block batches (even blocks, then odd)."""
+        BS, D = self.BS, self.D
+        n = D.shape[0]
+        allc = np.arange(n)
+        rr = np.arange(rows.start, rows.stop)[:, None]
+        fused = []
+        K = K0
+        while K < K1:
+            if K % 2 == 0 and K + 1 < K1:
+                ks = np.arange(K * BS, (K + 2) * BS)
+                self.relax(rr, allc[~((allc >= K * BS) & (allc < (K + 2) * BS))][None, :], ks)
+                fused.append(K)
+                K += 2
+            else:
+                kb = self.blk(K)
+                keep = D[rows, kb].copy()
+                D[rows, :] = np.minimum(D[rows, :], minplus(D[rows, kb].copy(), D[kb, :].copy()))
+                D[rows, kb] = keep
+                K += 1
+        for K in range(K0, K1):
+            kb = self.blk(K)
+            D[rows, kb] = np.minimum(D[rows, kb], minplus(D[rows, kb], D[kb, kb]))
+        for par in (0, 1):
+            for K in fused:
+                x, y = K + par, K + 1 - par                         # block x through partner y
+                xb, yb = self.blk(x), self.blk(y)
+                D[rows, xb] = np.minimum(D[rows, xb], minplus(D[rows, yb].copy(), D[yb, xb].copy()))
+
+
+def run_pipeline_pairs(W, BS, tb, min_rows=1, force=False):
+    """The pipeline's order of work with pairs (chunks of >= min_rows blocks use pairs; plain
+    pairs only when every chunk boundary is even, as in pipe_solve — force=True drops that
+    condition to show why it is there)."""
+    m = Model(W, BS)
+    even = force or all(t % 2 == 0 for t in tb)
+    R = len(W) // BS
+    C = len(tb) - 1
+    rows = lambda a, b: slice(a * BS, b * BS)
+    for c in range(C):                                              # arrival
+        t0, t1 = tb[c], tb[c + 1]
+        use = t1 - t0 >= min_rows
+        if use and even:
+            m.plain_pairs(0, t0, rows(t0, t1))
+        else:
+            m.plain_rounds(0, t0, rows(t0, t1))
+        k1 = min(t1, R)
+        if use and t0 % 2 == 0 and (k1 - t0) % 2 == 0:
+            for a in range(t0, k1, 2):
+                m.own_pair(a, t0, t1, last=a + 2 >= k1)
+        else:
+            for K in range(t0, k1):
+                m.own_round(K, rows(t0, t1))
+    for c in range(C - 1, -1, -1):                                  # departure
+        t0, t1 = tb[c], tb[c + 1]
+        if t0 >= min_rows and even:
+            m.plain_pairs(t0, min(t1, R), rows(0, t0))
+        else:
+            m.plain_rounds(t0, min(t1, R), rows(0, t0))
+    return m.D
+
+
 def run_pipeline(W, BS, tb, violate=False):
     """The pipeline's order of work for chunk boundaries tb (in blocks of BS)."""
     m = Model(W, BS)
@@ -159,3 +271,38 @@ def test_schedule_precondition_matters():
     D = run_pipeline(W, BS, [0, 4, 8, 16], violate=True)
     assert not np.array_equal(D, Dref)
     np.testing.assert_array_equal(run_pipeline(W, BS, [0, 4, 8, 16]), Dref)
+
+
+@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("kind", ["complete_int", "er_int", "ring"])
+def test_pair_schedule_gives_the_oracle_distances(seed, kind):
+    """Pairs of rounds in the model: the device schedule (one chunk, all rows)
+    and the pipeline's (own pairs on wide chunks, plain pairs with partner-block batches) give
+    the oracle's distances bit for bit."""
+    BS, nb = 4, 16
+    n = BS * nb
+    if kind == "ring":
+        W = gen.ring_with_chords(n, seed, 20, dtype=np.int32)
+    elif kind == "er_int":
+        W = gen.generate("er_int", n, 70 + seed, p=0.08, lo=1, hi=50)
+    else:
+        W = gen.generate("complete_int", n, 80 + seed).astype(np.int32)
+    Dref = oracle.fw(W, None)[0].astype(np.int64)
+    Dref[Dref >= gen.INF_I32] = INF
+    for tb, min_rows in (([0, 16], 1), ([0, 2, 4, 8, 16], 4), ([0, 2, 4, 8, 16], 1), ([0, 8, 16], 1),
+                         (scaled_bounds(nb, 16384), 4), ([0, 6, 10, 16], 4)):
+        D = run_pipeline_pairs(W, BS, tb, min_rows)
+        np.testing.assert_array_equal(D, Dref, err_msg=f"bounds {tb}")
+
+
+def test_pair_schedule_needs_even_chunk_bounds():
+    """A fused pair whose two pivot blocks lie in different chunks reads a pivot strip that has
+    not completed the pair's second round: with odd chunk boundaries and the even-boundary
+    condition dropped, paths are lost on a ring — the condition pipe_solve enforces."""
+    BS, nb = 4, 16
+    n = BS * nb
+    W = gen.ring_with_chords(n, 0, 20, dtype=np.int32)
+    Dref = oracle.fw(W, None)[0].astype(np.int64)
+    tb = [0, 1, 2, 4, 8, 16]
+    assert not np.array_equal(run_pipeline_pairs(W, BS, tb, 4, force=True), Dref)
+    np.testing.assert_array_equal(run_pipeline_pairs(W, BS, tb, 4), Dref)
