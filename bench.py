@@ -296,7 +296,10 @@ def run_gpu(args, cfg):
     p2_bytes = 2.0 * BS * ((n + 127) // 128 * 128) * 4 * s0.rounds   # both pivot strips read per round
     roof = {"bound": "alu", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
-            "traffic": traffic, "kernel": f"minplus_tile_kernel<{ctype},128,128,{mode}> (phase 3, rank 0)",
+            "traffic": traffic,
+            "kernel": f"minplus_tile_kernel<{ctype},128,128,{mode}> (phase 3, rank 0"
+                      + (", two rounds per pass: 256-deep bulk launches" if s0.phase3_launches < s0.rounds else "")
+                      + ")",
             "avg_launch_ms": avg_launch_ms,
             "peak_basis": f"stated FP32 add+min issue roofline: {sms} SMs x 128 lanes x {max_mhz:.0f} MHz "
                           "(2 flop per relaxation, BASELINE north_star)",

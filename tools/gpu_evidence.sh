@@ -14,6 +14,6 @@ timeout 1200 python bench.py --n 65536 --steps 1 --warmup 1 --no-e2e --no-cpu > 
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches_c4.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > $O/ncu_list.log 2>&1
 python tools/launch_summary.py $O/launches_c4.csv > $O/launches_c4_summary.txt 2>&1
 NCU="ncu --set full --import-source on --clock-control none --kernel-name-base mangled"
-timeout 600 $NCU -k regex:'minplus_tile_kernelIfLi128ELi128ELi2ELb0E' --launch-skip 64 --launch-count 1 -f -o $O/p3_c4 python tools/solve_once.py --config C4 > $O/ncu_p3.log 2>&1
+timeout 600 $NCU -k regex:'minplus_tile_kernelIfLi128ELi128ELi2ELb0E' --launch-skip 32 --launch-count 1 -f -o $O/p3_c4 python tools/solve_once.py --config C4 > $O/ncu_p3.log 2>&1
 python tools/ncu_summary.py $O/p3_c4.ncu-rep > $O/p3_c4_summary.txt 2>&1
 ncu -i $O/p3_c4.ncu-rep --page raw --csv > $O/p3_c4_raw.csv 2>/dev/null
