@@ -511,3 +511,14 @@ def test_pair_rounds_ring_closed_form():
     i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
     np.testing.assert_array_equal(D, ((j - i) % n).astype(np.float32))
     np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % n))
+
+
+@pytest.mark.parametrize("n", [768, 1000])
+def test_pair_rounds_int32_native_keys(n):
+    """INT32 weights above the FP32 key range (max_w > 32766), no INF: native INT32 keys
+    (VIADDMNMX) under two rounds per pass; bit-exact against the oracle, paths valid."""
+    W = gen.generate("er_int", n, 995 + n, p=1.0, lo=1, hi=200000)
+    D, P, s = _solve_stats(W, 128)
+    assert s.p_method == 2 and s.compute_f32 == 0 and s.phase3_launches < s.rounds
+    np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+    assert oracle.check_paths(W, D, P)[0] == 0
