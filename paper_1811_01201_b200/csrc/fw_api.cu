@@ -11,7 +11,10 @@
 // read are done first (P3a); the pivot phases and broadcast of round K+1 then run on a
 // high-priority side stream while the rest of phase 3 (P3b) runs on the main stream.
 // After the rounds the post-pass turns keys / round tags into P (reading R9).
-// One GPU is the world = 1 case of the same driver (no broadcast: B is read in place).
+// One GPU is the world = 1 case of the same driver (no broadcast: B is read in place); there,
+// keyed and distance-only solves take two rounds per phase-3 pass (Rounds::run_pairs,
+// DESIGN.md §4.9). The host entry points split the rows into chunks whose copies overlap the
+// rounds (solve_host_pipelined, reading R16).
 #include "fw_kernels.cuh"
 #include "../../include/fw.h"
 
@@ -151,6 +154,7 @@ struct Ctx {
   int pipe_tiles = -1;             // host pipeline chunk in tile-rows (-1 auto, 0 off)
   int pipe_first = 8;              // auto geometry: first chunk (tile-rows; env FW_PIPE_FIRST)
   bool pairs = true;               // two rounds per phase-3 pass for keyed / plain solves (env FW_PAIRS=0: off)
+  int pipe_pair_rows = 32;         // host pipeline: smallest chunk (tile-rows) run in pairs (env FW_PIPE_PAIR_ROWS)
   bool last_pairs = false;         // the last solve ran in pairs (stats layout)
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
   int rank = 0, world = 1;
@@ -1392,12 +1396,12 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
     const int own0 = std::max(K0, std::min(K1, t0)), own1 = std::max(own0, std::min(K1, t1));
     // a fused pair (K, K+1) needs both pivot blocks complete through K+1: they must lie in one
     // chunk, which holds when every chunk boundary is even
-    const bool plain_pairs = c.pairs && t1 - t0 >= 32 && even_bounds;
+    const bool plain_pairs = c.pairs && t1 - t0 >= c.pipe_pair_rows && even_bounds;
     TRY(rk.run_plain(st, K0, own0, plain_pairs));    // pivots in earlier rows
     if (own1 > own0) {                               // own pivots: pairs of rounds (§4.9) or one by one
       // (pairs only on wide row ranges: below 32 tile-rows the two sub-rounds of pivot phases
       // take longer than the bulk launch they hide under)
-      if (MODE != MODE_TAG && c.pairs && la && own0 % 2 == 0 && (own1 - own0) % 2 == 0 && t1 - t0 >= 32) {
+      if (MODE != MODE_TAG && c.pairs && la && own0 % 2 == 0 && (own1 - own0) % 2 == 0 && t1 - t0 >= c.pipe_pair_rows) {
         TRY(rk.run_pairs(st, ev, own0, own1));
       } else {
         CU(cudaMemsetAsync(d_done, 0, 4 * (size_t)g.R, st));
@@ -1880,6 +1884,8 @@ int fw_init(int ngpus_max, unsigned flags) {
   c->lookahead = !(la && la[0] == '0');
   const char *pr = getenv("FW_PAIRS");
   c->pairs = !(pr && pr[0] == '0');
+  const char *pp = getenv("FW_PIPE_PAIR_ROWS");
+  if (pp && atoi(pp) >= 1) c->pipe_pair_rows = atoi(pp);
   const char *pf = getenv("FW_PIPE_FIRST");   // tuning: first chunk of the auto host pipeline
   if (pf && atoi(pf) >= 1 && atoi(pf) <= 64) c->pipe_first = atoi(pf);
   g_ctx = c;

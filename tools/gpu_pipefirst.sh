@@ -1,7 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out/pf
 O=gpurun_out/pf
-for f in 4 8 16; do
-  FW_PIPE_FIRST=$f timeout 600 python tools/pipe_probe.py --config C3 --chunks -1 --reps 3 > $O/c3_$f.log 2>&1
-  FW_PIPE_FIRST=$f timeout 600 python tools/pipe_probe.py --config C4 --chunks -1 --reps 2 > $O/c4_$f.log 2>&1
+for f in 4 8 16 32; do
+  FW_PIPE_FIRST=$f timeout 600 python tools/pipe_probe.py --config C4 --chunks=-1 --reps 2 > $O/c4_$f.log 2>&1
 done
