@@ -1156,7 +1156,8 @@ class CopyPool {
     dst_ = static_cast<char *>(dst);
     src_ = static_cast<const char *>(src);
     bytes_ = bytes;
-    part_ = (bytes / (nth_ + 1) + 63) & ~size_t(63);
+    const size_t parts = (size_t)nth_ + 1;
+    part_ = ((bytes + parts - 1) / parts + 63) & ~size_t(63);   // parts * part_ >= bytes
     pending_ = nth_;
     ++gen_;
     cv_.notify_all();

@@ -324,3 +324,50 @@ def test_pipeline_pairs_ring_closed_form(n, ct):
         r = np.arange(r0, min(n, r0 + 2048))
         np.testing.assert_array_equal(D[r], ((i[None, :] - r[:, None]) % n).astype(np.float32))
         np.testing.assert_array_equal(P[r], np.where(r[:, None] == i[None, :], r[:, None], (r[:, None] + 1) % n))
+
+
+def test_pipeline_randomized_mix():
+    """A seeded mix of host solves through ONE context: sizes with ragged tails, every input
+    kind, next-hop / LAST_K / D-only, pinned and pageable buffers, chunkings from 1 tile-row to
+    off (so pairs of rounds, plain pairs, speculative keys and round tags interleave with the
+    context's cached buffers, events and staging ring) — each against the oracle."""
+    rng = np.random.default_rng(20261020)
+    kinds = ["complete_int", "complete_real", "er_int", "er_int_f32"]
+    fw.fw_init(0, 0)
+    try:
+        for step in range(14):
+            n = int(rng.integers(256, 1400))
+            kind = kinds[step % 4]
+            W = gen.generate(kind, n, 7000 + step, p=0.03, lo=1, hi=int(rng.choice([50, 1000])))
+            path = [None, "next", "next"][step % 3]
+            ct = int(rng.choice([-1, 0, 1, 2, 4]))
+            pin = bool(step % 2)
+            fw.fw_set_host_pipeline(ct)
+            hD = torch.from_numpy(W.copy())
+            hP = torch.full(W.shape, -5, dtype=torch.int32) if path else None
+            if pin:
+                hD = hD.pin_memory()
+                hP = hP.pin_memory() if hP is not None else None
+            (fw.fw_solve_i32 if W.dtype == np.int32 else fw.fw_solve)(hD, hP, block=128)
+            D = hD.numpy()
+            exact = exact_data(W)
+            assert_D_matches(D, oracle.fw(W, None)[0], exact)
+            if path:
+                bad, first = oracle.check_paths(W, D, hP.numpy(), rtol=0.0 if exact else 1e-5)
+                assert bad == 0, (step, n, kind, ct, pin, bad)
+    finally:
+        fw.fw_free()
+
+
+@pytest.mark.parametrize("n", [1087, 1500, 2049])
+def test_pageable_copy_sizes(n):
+    """Pageable host buffers whose byte counts are not multiples of the copy pool's partition
+    granularity (the parallel host copy must cover the last bytes of every slice): the standard
+    path (auto pipeline off below 32 tile-rows) and a pipelined solve, bit-exact D and the
+    diagonal / last-row next hops."""
+    W = gen.generate("er_int", n, 1200 + n, p=0.03, lo=1, hi=50)
+    for ct in (-1, 2):
+        D, P, st = solve_pinned(W, ct, pin=False)
+        np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+        assert (np.diag(P) == np.arange(n)).all()
+        assert oracle.check_paths(W, D, P)[0] == 0
