@@ -1,7 +1,8 @@
 """Seeded randomized GPU parity: many combinations of the solve's options in one run, each
 against the CPU oracle — sizes with ragged tails, block sizes, input kinds (complete / sparse
 with unreachable pairs, integer / real, FP32 / INT32), path modes (next hop, LAST_K, D only),
-host buffers (pinned / pageable) or device buffers, host-pipeline chunkings, and one or two
+host buffers (pinned / pageable), device buffers or the loopback transport (every rank of a
+2..7-way block-row partition on this GPU), host-pipeline chunkings, and one or two
 rounds per phase-3 pass (FW_PAIRS). Integer data bit-exact, reals within rel 1e-5, every path
 reconstructed (BASELINE.json north_star correctness requirements)."""
 import numpy as np
@@ -33,7 +34,8 @@ def one_case(rng, step, monkeypatch):
     W = gen.generate(kind, n, 9100 + step, p=float(rng.choice([0.002, 0.02, 0.2])), lo=1, hi=hi)
     path = [None, "next", "lastk", "next"][step % 4]
     block = int(rng.choice([0, 32, 64, 128, 128]))
-    where = ["pinned", "pageable", "device"][int(rng.integers(0, 3))]
+    where = ["pinned", "pageable", "device", "loopback"][int(rng.integers(0, 4))]
+    world = int(rng.integers(2, 8))
     ct = int(rng.choice([-1, 0, 1, 2, 3, 4]))
     pairs = bool(rng.integers(0, 2))
     monkeypatch.setenv("FW_PAIRS", "1" if pairs else "0")
@@ -42,11 +44,15 @@ def one_case(rng, step, monkeypatch):
     fw.fw_init(0, flags)
     try:
         fw.fw_set_host_pipeline(ct)
-        if where == "device":
+        if where in ("device", "loopback"):
             dD = torch.from_numpy(W.copy()).cuda()
             dP = torch.empty(W.shape, dtype=torch.int32, device="cuda") if path else None
-            (fw.fw_solve_device_i32 if is_int else fw.fw_solve_device_f32)(
-                dD, dP, block=block, stream=torch.cuda.current_stream())
+            if where == "device":
+                (fw.fw_solve_device_i32 if is_int else fw.fw_solve_device_f32)(
+                    dD, dP, block=block, stream=torch.cuda.current_stream())
+            else:   # every rank of a `world`-way block-row partition emulated on this GPU
+                (fw.fw_dist_loopback_solve_device_i32 if is_int else fw.fw_dist_loopback_solve_device_f32)(
+                    dD, dP, block=block, world=world, stream=torch.cuda.current_stream())
             D = dD.cpu().numpy()
             P = dP.cpu().numpy() if path else None
         else:
@@ -60,7 +66,8 @@ def one_case(rng, step, monkeypatch):
             P = hP.numpy() if path else None
     finally:
         fw.fw_free()
-    desc = dict(step=step, n=n, kind=kind, hi=hi, path=path, block=block, where=where, ct=ct, pairs=pairs)
+    desc = dict(step=step, n=n, kind=kind, hi=hi, path=path, block=block, where=where, ct=ct, pairs=pairs,
+                world=world)
     exact = exact_data(W)
     assert_D_matches(D, oracle.fw(W, None)[0], exact)
     if path:
