@@ -306,3 +306,24 @@ def test_pair_schedule_needs_even_chunk_bounds():
     tb = [0, 1, 2, 4, 8, 16]
     assert not np.array_equal(run_pipeline_pairs(W, BS, tb, 4, force=True), Dref)
     np.testing.assert_array_equal(run_pipeline_pairs(W, BS, tb, 4), Dref)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_geometries(seed):
+    """Random even chunk boundaries (and random odd ones, where plain pairs are switched off)
+    and random pair thresholds: both schedules give the oracle's distances on random graphs."""
+    rng = np.random.default_rng(300 + seed)
+    BS, nb = 4, 16
+    n = BS * nb
+    W = gen.generate("er_int", n, 400 + seed, p=float(rng.choice([0.03, 0.08, 0.3])), lo=1, hi=40)
+    Dref = oracle.fw(W, None)[0].astype(np.int64)
+    Dref[Dref >= gen.INF_I32] = INF
+    for _ in range(4):
+        k = int(rng.integers(1, 5))
+        even = bool(rng.integers(0, 2))
+        pool = np.arange(2, nb, 2) if even else np.arange(1, nb)
+        cuts = sorted(set(int(x) for x in rng.choice(pool, size=min(k, len(pool)), replace=False)))
+        tb = [0] + cuts + [nb]
+        np.testing.assert_array_equal(run_pipeline(W, BS, tb), Dref, err_msg=f"single {tb}")
+        np.testing.assert_array_equal(run_pipeline_pairs(W, BS, tb, int(rng.integers(1, 9))), Dref,
+                                      err_msg=f"pairs {tb}")
