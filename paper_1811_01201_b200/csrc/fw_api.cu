@@ -1179,7 +1179,8 @@ class CopyPool {
  private:
   CopyPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    nth_ = (int)std::min(7u, hw > 2 ? hw / 2 - 1 : 0u);
+    const char *e = getenv("FW_COPY_THREADS");   // tuning: helper threads of the host copy pool
+    nth_ = e ? std::max(0, atoi(e)) : (int)std::min(15u, hw > 2 ? hw * 3 / 4 - 1 : 0u);   // 11 of 16 cores
     for (int w = 1; w <= nth_; ++w) th_.emplace_back([this, w] { loop(w); });
   }
   void run_part(int w) {
