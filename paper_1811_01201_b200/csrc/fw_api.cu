@@ -154,6 +154,7 @@ struct Ctx {
   int pipe_tiles = -1;             // host pipeline chunk in tile-rows (-1 auto, 0 off)
   int pipe_first = 8;              // auto geometry: first chunk (tile-rows; env FW_PIPE_FIRST)
   bool pairs = true;               // two rounds per phase-3 pass for keyed / plain solves (env FW_PAIRS=0: off)
+  bool pair_order = true;          // pairs: the next pair's strips run beside the bulk launch (env FW_PAIR_ORDER=0: before it)
   int pipe_pair_rows = 32;         // host pipeline: smallest chunk (tile-rows) run in pairs (env FW_PIPE_PAIR_ROWS)
   bool last_pairs = false;         // the last solve ran in pairs (stats layout)
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
@@ -495,18 +496,30 @@ struct Rounds {
     const int P0 = K0 / 2, NP = K1 / 2;
     if (P0 >= NP) return FW_OK;
     cudaStream_t side = c.side;
+    const bool overlap = c.pair_order;
     TRY(pair_pivot(st, P0));
     for (int Pp = P0; Pp < NP; ++Pp) {
       const bool last = Pp + 1 == NP;
       if (e.timing) CU(cudaEventRecord(e.ev[3 * Pp], st));        // the pair's phase-3 work starts
-      if (!last) {
-        TRY(pair_prio(st, Pp));
-        CU(cudaEventRecord(e.sync[2 * Pp], st));
+      if (!last && overlap) {
+        // the next pair's strips on the (high-priority) pivot stream, concurrent with the bulk
+        // launch: their CTAs are dispatched first and the bulk fills the SMs behind their tail
+        CU(cudaEventRecord(e.sync[2 * Pp], st));                  // the previous bulk launch is done
         CU(cudaStreamWaitEvent(side, e.sync[2 * Pp], 0));
+        TRY(pair_prio(side, Pp));
         TRY(pair_pivot(side, Pp + 1));
         CU(cudaEventRecord(e.sync[2 * Pp + 1], side));
+        TRY(pair_bulk(st, Pp, last));
+      } else {
+        if (!last) {
+          TRY(pair_prio(st, Pp));
+          CU(cudaEventRecord(e.sync[2 * Pp], st));
+          CU(cudaStreamWaitEvent(side, e.sync[2 * Pp], 0));
+          TRY(pair_pivot(side, Pp + 1));
+          CU(cudaEventRecord(e.sync[2 * Pp + 1], side));
+        }
+        TRY(pair_bulk(st, Pp, last));
       }
-      TRY(pair_bulk(st, Pp, last));
       if (e.timing) CU(cudaEventRecord(e.ev[3 * Pp + 2], st));    // ... and ends
       if (!last) CU(cudaStreamWaitEvent(st, e.sync[2 * Pp + 1], 0));
     }
@@ -1886,6 +1899,8 @@ int fw_init(int ngpus_max, unsigned flags) {
   c->lookahead = !(la && la[0] == '0');
   const char *pr = getenv("FW_PAIRS");
   c->pairs = !(pr && pr[0] == '0');
+  const char *po = getenv("FW_PAIR_ORDER");
+  c->pair_order = !(po && po[0] == '0');
   const char *pp = getenv("FW_PIPE_PAIR_ROWS");
   if (pp && atoi(pp) >= 1) c->pipe_pair_rows = atoi(pp);
   const char *pf = getenv("FW_PIPE_FIRST");   // tuning: first chunk of the auto host pipeline
