@@ -931,7 +931,7 @@ template <typename T, int CH>
 __global__ void __launch_bounds__(512, 1)
 resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t row0, int64_t n,
                      int64_t n_pad, int32_t *tags, int use_smem) {
-  constexpr int U = 16;                    // elements in flight per warp (16 x 4*BS bytes)
+  constexpr int U = 12;                    // elements in flight per warp (12 x 4*BS bytes)
   constexpr int BS = 32 * CH;
   using V = typename VecN<T, CH>::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -955,10 +955,10 @@ resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t r
     tg[u] = j < nn ? trow[j] : -1;
   }
   for (int j0 = warp * U; j0 < nn; j0 += step) {
-    V b[U];                                // the global segment loads, all in flight (padded
-#pragma unroll                             // rows/blocks exist, so untagged ones load block 0)
+    V b[U];                                // the global segment loads, all in flight (untagged
+#pragma unroll                             // ones and j >= n load row n-1, block 0)
     for (int u = 0; u < U; ++u)
-      b[u] = *reinterpret_cast<const V *>(Dt + (int64_t)(j0 + u) * ldt + max(tg[u], 0) * BS + CH * lane);
+      b[u] = *reinterpret_cast<const V *>(Dt + (int64_t)min(j0 + u, nn - 1) * ldt + max(tg[u], 0) * BS + CH * lane);
     int tgn[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -971,21 +971,23 @@ resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t r
       const int j = j0 + u;
       const int k0 = max(tg[u], 0) * BS + CH * lane;
       const V a = *reinterpret_cast<const V *>(A + k0);   // row i: shared memory (or L1)
-      // lane arg-min over its CH candidates, first k on ties; k = i, k = j, k >= n excluded
-      T best = Num<T>::acc_init();
-      int bk = -1;
+      const T dij = A[min(j, nn - 1)];                    // the final D[i][j] (one broadcast)
+      // reading R9: k* = the FIRST k of block K, k not in {i, j}, with D[i][k] + D[k][j] <= D[i][j]
+      // (one exists: the improving k of the tag's round; later rounds only lowered both terms
+      // and rounding is monotone). Lane bits c = candidates k0 + c; padding k >= n is INF.
+      unsigned hit = 0;
 #pragma unroll
-      for (int c = CH - 1; c >= 0; --c) {
-        const int k = k0 + c;
+      for (int c = 0; c < CH; ++c) {
         const T sum = (T)velem(a, c) + (T)velem(b[u], c);
-        if (k != gi && k != j && k < nn && sum <= best) { best = sum; bk = k; }
+        hit |= (sum <= dij ? 1u : 0u) << c;
       }
-      // warp arg-min (non-negative FP32 orders like its bit pattern): min over the block K
-      // equals D[i][j] in exact arithmetic (reading R9), the first such k wins
-      const int key = bk >= 0 ? Num<T>::bits(best) : 0x7fffffff;
-      const int wmin = __reduce_min_sync(0xffffffffu, key);
-      const unsigned m = __ballot_sync(0xffffffffu, key == wmin && bk >= 0);
-      const int ks = __shfl_sync(0xffffffffu, bk, m ? __ffs(m) - 1 : 0);
+      const unsigned di = (unsigned)(gi - k0), dj = (unsigned)(j - k0);
+      if (di < (unsigned)CH) hit &= ~(1u << di);
+      if (dj < (unsigned)CH) hit &= ~(1u << dj);
+      const unsigned m = __ballot_sync(0xffffffffu, hit != 0);
+      const int src = m ? __ffs(m) - 1 : 0;
+      const unsigned h = __shfl_sync(0xffffffffu, hit, src);
+      const int ks = max(tg[u], 0) * BS + CH * src + __ffs(h) - 1;
       if (lane == u) res = m ? ks : -1;
     }
     if (lane < U && j0 + lane < nn) {
