@@ -154,6 +154,9 @@ struct Ctx {
   int pipe_tiles = -1;             // host pipeline chunk in tile-rows (-1 auto, 0 off)
   int pipe_first = 8;              // auto geometry: first chunk (tile-rows; env FW_PIPE_FIRST)
   bool pairs = true;               // two rounds per phase-3 pass for keyed / plain solves (env FW_PAIRS=0: off)
+  bool pair_pdl = true;            // pairs: bulk launches programmatically serialized (env FW_PDL=0: off)
+  bool last_pdl = false;           // the last solve's pairs ran with programmatic serialization
+  std::vector<cudaEvent_t> xev;    // disable-timing events between bulk launches
   bool pair_order = true;          // pairs: the next pair's strips run beside the bulk launch (env FW_PAIR_ORDER=0: before it)
   int pipe_pair_rows = 32;         // host pipeline: smallest chunk (tile-rows) run in pairs (env FW_PIPE_PAIR_ROWS)
   bool last_pairs = false;         // the last solve ran in pairs (stats layout)
@@ -191,6 +194,15 @@ int smem_attr(const void *fn, int bytes) {
 constexpr int64_t kKeyMaxF32 = 32766;
 constexpr int64_t kKeyMaxI32 = 2097150;
 
+int ensure_xev(Ctx &c, size_t count) {
+  while (c.xev.size() < count) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.xev.push_back(e);
+  }
+  return FW_OK;
+}
+
 int ensure_events(Ctx &c, size_t count) {
   while (c.events.size() < count) {
     cudaEvent_t e;
@@ -223,12 +235,27 @@ int owner_of(int64_t n, int world, int64_t row) {
 
 // ---- kernel launch wrappers ----------------------------------------------------------------
 template <typename T, int TM, int TN, int MODE>
-int launch_tile(dim3 grid, cudaStream_t st, T *D, int32_t *P, const TileArgs &a, int *maxkey) {
+int launch_tile(dim3 grid, cudaStream_t st, T *D, int32_t *P, const TileArgs &a, int *maxkey, bool pdl = false) {
   if (grid.x == 0 || grid.y == 0) return FW_OK;
   constexpr int bytes = TileShape<TM, TN>::kBytes;
   auto kern = grid.z > 1 ? minplus_tile_kernel<T, TM, TN, MODE, true>
                          : minplus_tile_kernel<T, TM, TN, MODE, false>;
   TRY(smem_attr((const void *)kern, bytes));
+  if (pdl) {   // programmatic serialization with the previous launch in st (see the kernel)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, kern, D, P, a, maxkey));
+    ++g_launches;
+    return FW_OK;
+  }
   kern<<<grid, kThreads, bytes, st>>>(D, P, a, maxkey);
   ++g_launches;
   CU(cudaGetLastError());
@@ -483,13 +510,42 @@ struct Rounds {
     put(t, 1, Strip{0, c2 * BS, lrow(a), lrow(a) + 4 * BS, 0, 0, 1});       // columns c, d, rows outside a..d
     return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 2, 2), st, D, P, t, maxkey);
   }
-  int pair_bulk(cudaStream_t st, int Pp, bool last) {
+  int pair_bulk(cudaStream_t st, int Pp, bool last, bool pdl = false) {
     const int a = 2 * Pp, kb = a * BS, w = (last ? 2 : 4) * BS;
     TileArgs t = tile_args(ld, D + (int64_t)lrow(a) * ld, ld, kb, 2 * BS, a, nrows, n_pad);
     put(t, 0, Strip{0, 0, lrow(a), lrow(a) + w, kb, kb + w, 0});
     return launch_tile<T, 128, 128, MODE>(dim3((unsigned)(n_pad / 128), (unsigned)(nrows / 128), 1), st, D, P,
-                                          t, maxkey);
+                                          t, maxkey, pdl);
   }
+  // The same schedule with each bulk launch (after the first) programmatically serialized with
+  // the previous one: its CTAs take the SMs the previous launch's last wave frees and run their
+  // main loops (which read only blocks a, b: final once the pivot stream is done) before they
+  // wait for that launch in the epilogue. Only disable-timing events sit between two bulk
+  // launches in st (a timing event there serializes them); the solve is timed from the first
+  // bulk launch to the last (e.ev[3 P0], e.ev[3 (NP-1) + 2]).
+  int run_pairs_pdl(cudaStream_t st, const Events &e, int P0, int NP) {
+    cudaStream_t side = c.side;
+    TRY(ensure_xev(c, (size_t)NP));
+    TRY(pair_pivot(st, P0));
+    if (e.timing) CU(cudaEventRecord(e.ev[3 * P0], st));
+    for (int Pp = P0; Pp < NP; ++Pp) {
+      const bool last = Pp + 1 == NP;
+      if (!last) {
+        CU(cudaEventRecord(c.xev[Pp], st));            // the previous bulk launch is done
+        CU(cudaStreamWaitEvent(side, c.xev[Pp], 0));
+        if (e.timing) CU(cudaEventRecord(e.sync[2 * Pp], side));
+        TRY(pair_prio(side, Pp));
+        TRY(pair_pivot(side, Pp + 1));
+        CU(cudaEventRecord(e.sync[2 * Pp + 1], side));
+      }
+      TRY(pair_bulk(st, Pp, last, Pp > P0));
+      if (!last) CU(cudaStreamWaitEvent(st, e.sync[2 * Pp + 1], 0));
+    }
+    if (e.timing) CU(cudaEventRecord(e.ev[3 * (NP - 1) + 2], st));
+    c.last_pdl = true;
+    return FW_OK;
+  }
+
   // Rounds [K0, K1) (K0, K1 even, blocks K0..K1-1 inside these rows) in pairs.
   int run_pairs(cudaStream_t st, const Events &e, int K0 = 0, int K1 = -1) {
     if (K1 < 0) K1 = R;
@@ -497,6 +553,7 @@ struct Rounds {
     if (P0 >= NP) return FW_OK;
     cudaStream_t side = c.side;
     const bool overlap = c.pair_order;
+    if (overlap && c.pair_pdl) return run_pairs_pdl(st, e, P0, NP);
     TRY(pair_pivot(st, P0));
     for (int Pp = P0; Pp < NP; ++Pp) {
       const bool last = Pp + 1 == NP;
@@ -657,6 +714,7 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
                                  {p.strip[0], p.strip[1]}, done});
   if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
   c.last_pairs = false;
+  c.last_pdl = false;
   if (MODE != MODE_TAG && c.pairs && la && world == 1 && BS == 128 && R % 2 == 0 && R >= 4 &&
       rk[0].row0 == 0 && rk[0].nrows == n_pad) {
     c.last_pairs = true;
@@ -1037,7 +1095,19 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   if (c.last_pairs)   // every pair relaxes all tiles outside its strip region through 256 k
     relax = (double)(R / 2) * (double)(n_pad - 2 * BS) * (double)(n_pad - 2 * BS) * (2.0 * BS);
   s.phase3_relaxations = relax;
-  if (timing && c.last_pairs) {
+  if (timing && c.last_pairs && c.last_pdl) {   // bulk launches overlap: timed as one span
+    auto at = [&](cudaEvent_t e) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e_begin, e);
+      return (double)t;
+    };
+    const int NP = R / 2;
+    const double p3s = at(ev.ev[0]), p3e = at(ev.ev[3 * (NP - 1) + 2]);
+    s.phase1_ms = p3s - at(e_init);   // the first pair's pivot path
+    s.phase3_ms = p3e - p3s;
+    for (int Pp = 0; Pp + 1 < NP; ++Pp) s.phase2_ms += at(ev.sync[2 * Pp + 1]) - at(ev.sync[2 * Pp]);
+    s.post_ms = at(e_post) - p3e;
+  } else if (timing && c.last_pairs) {
     auto at = [&](cudaEvent_t e) {
       float t = 0.f;
       cudaEventElapsedTime(&t, e_begin, e);
@@ -1899,6 +1969,8 @@ int fw_init(int ngpus_max, unsigned flags) {
   c->lookahead = !(la && la[0] == '0');
   const char *pr = getenv("FW_PAIRS");
   c->pairs = !(pr && pr[0] == '0');
+  const char *pd = getenv("FW_PDL");
+  c->pair_pdl = !(pd && pd[0] == '0');
   const char *po = getenv("FW_PAIR_ORDER");
   c->pair_order = !(po && po[0] == '0');
   const char *pp = getenv("FW_PIPE_PAIR_ROWS");

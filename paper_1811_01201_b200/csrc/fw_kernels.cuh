@@ -267,6 +267,10 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   // colstrip 2 / colstep (pairs of plain rounds) never occur with round tags: compiled out there
   constexpr bool PAIRS = MODE != MODE_TAG;
   const int cstrip = g.colstrip;
+  // a launch that follows this one with programmatic serialization (the next pair's bulk
+  // launch) may start its CTAs once every CTA of this one has started; it
+  // waits for this grid's completion only before its own epilogue (griddepcontrol.wait below)
+  asm volatile("griddepcontrol.launch_dependents;");
   const TileSlot ts = tile_slot<TM, TN, DUAL, PAIRS>(g, blockIdx.x, blockIdx.y, blockIdx.z);
   if (ts.skip) return;
   const int i0 = ts.i0, j0 = ts.j0;
@@ -354,6 +358,9 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   }
 
   // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
+  // (launched with programmatic serialization: the previous launch in the stream, which wrote
+  // this tile, must be complete before the tile is read and written; a no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const TileSlot te = tile_slot<TM, TN, DUAL, PAIRS>(g, ctaid(0), ctaid(1), ctaid(2));
   const int mr_lo = te.mr_lo, mr_hi = te.mr_hi, mc_lo = te.mc_lo, mc_hi = te.mc_hi;
   const int kgrp = (g.colstrip ? te.j0 : g.kb) & ~kKeyMask;
