@@ -8,3 +8,4 @@ $NVCC -o $B/p3x $B/p3x.cu             # phase-3 tile-shape / pipeline explorer
 $NVCC -o $B/mix_probe $B/mix_probe.cu # register- and smem-fed relaxation mix
 $NVCC -o $P/isa_probe $P/isa_probe.cu # L0 instruction throughput probe
 $NVCC -o $P/nvls_probe $P/nvls_probe.cu -L/usr/local/cuda/lib64/stubs -lcuda   # NVLS multicast probe
+$NVCC -o $P/pdl_probe $P/pdl_probe.cu   # programmatic dependent launch probe
