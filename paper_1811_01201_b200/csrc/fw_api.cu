@@ -395,16 +395,16 @@ struct Rounds {
   }
 
   // Phase 3 on the local rows except rows [rx_lo, rx_hi) and columns [cx_lo, cx_hi).
-  int phase3(cudaStream_t st, int K, int rx_lo, int rx_hi, int cx_lo, int cx_hi) {
+  int phase3(cudaStream_t st, int K, int rx_lo, int rx_hi, int cx_lo, int cx_hi, bool pdl = false) {
     TileArgs a = tile_args(ld, bstrip(K), ld, K * BS, BS, K, nrows, n_pad);
     put(a, 0, Strip{0, 0, rx_lo, rx_hi, cx_lo, cx_hi, 0});
     return launch_tile<T, 128, 128, MODE>(dim3((unsigned)(n_pad / 128), (unsigned)(nrows / 128), 1),
-                                          st, D, P, a, maxkey);
+                                          st, D, P, a, maxkey, pdl);
   }
-  int phase3_full(cudaStream_t st, int K) {
+  int phase3_full(cudaStream_t st, int K, bool pdl = false) {
     const int kb = K * BS;
     const bool own = owns(K);
-    return phase3(st, K, own ? lrow(K) : 0, own ? lrow(K) + BS : 0, kb, kb + BS);
+    return phase3(st, K, own ? lrow(K) : 0, own ? lrow(K) + BS : 0, kb, kb + BS, pdl);
   }
 
   // Rounds [K0, K1) whose pivot strips (rows of other chunks, read in place through Dg) have
@@ -459,7 +459,7 @@ struct Rounds {
   // the tiles round K+1's pivot phases read (block-row K+1 if local, block-column K+1 of the
   // local rows); they count themselves into done[K] and the pivot stream waits on that count
   // (wait_count_kernel) instead of a kernel boundary.
-  int phase3_ordered(cudaStream_t st, int K, int *done, int *nprio_out) {
+  int phase3_ordered(cudaStream_t st, int K, int *done, int *nprio_out, bool pdl = false) {
     TileArgs a = tile_args(ld, bstrip(K), ld, K * BS, BS, K, nrows, n_pad);
     a.order = 1;
     a.tiles_r = (int)(nrows / 128);
@@ -474,7 +474,7 @@ struct Rounds {
     a.done = done;
     *nprio_out = a.nprio;
     const int64_t total = (int64_t)nA1 + rows_b + (int64_t)rows_b * (a.tiles_c - 2);
-    return launch_tile<T, 128, 128, MODE>(dim3((unsigned)total, 1, 1), st, D, P, a, maxkey);
+    return launch_tile<T, 128, 128, MODE>(dim3((unsigned)total, 1, 1), st, D, P, a, maxkey, pdl);
   }
 
   // ---- two rounds per phase-3 pass (keyed / plain solves, one GPU, all rows, BS = 128) ------
@@ -600,6 +600,7 @@ struct Rounds {
       }
       return FW_OK;
     }
+    if (world == 1 && c.pair_pdl) return run_pdl(st, e, K0, K1);
     cudaStream_t side = c.side;
     TRY(phase1(st, K0));
     if (e.timing) CU(cudaEventRecord(ev[3 * K0], st));
@@ -628,6 +629,46 @@ struct Rounds {
         if (e.timing) CU(cudaEventRecord(ev[3 * K + 2], st));
       }
     }
+    return FW_OK;
+  }
+
+  // The look-ahead schedule (one GPU) with each ordered launch after the first programmatically
+  // serialized with the previous one (as run_pairs_pdl): launch K's main loop (column block K,
+  // row K: look-ahead tiles of launch K-1, final once the pivot stream's event fired) overlaps
+  // launch K-1's last wave; its epilogue waits for launch K-1. The pivot stream now also waits
+  // for launch K-1 to complete (xev[K]) before round K+1's phases, which rewrite tiles of row
+  // and column K+1 that launch K-1 may still be writing. Main-stream events between ordered
+  // launches are disable-timing (a timing record would serialize them).
+  int run_pdl(cudaStream_t st, const Events &e, int K0, int K1) {
+    cudaEvent_t *ev = e.ev;
+    cudaStream_t side = c.side;
+    TRY(ensure_xev(c, (size_t)K1));
+    TRY(phase1(st, K0));
+    if (e.timing) CU(cudaEventRecord(ev[3 * K0], st));
+    TRY(pivot_rest(st, K0));
+    if (e.timing) CU(cudaEventRecord(ev[3 * K0 + 1], st));
+    for (int K = K0; K < K1; ++K) {
+      if (K + 1 < K1) {
+        CU(cudaEventRecord(c.xev[K], st));           // launch K-1 (and round K's pivot) complete
+        int nprio = 0;
+        TRY(phase3_ordered(st, K, done + K, &nprio, K > K0));
+        CU(cudaStreamWaitEvent(side, c.xev[K], 0));
+        wait_count_kernel<<<1, 1, 0, side>>>(done + K, nprio);
+        ++g_launches;
+        CU(cudaGetLastError());
+        if (e.timing) CU(cudaEventRecord(e.sync[2 * K + 2], side));
+        TRY(phase1(side, K + 1));
+        if (e.timing) CU(cudaEventRecord(ev[3 * (K + 1)], side));
+        TRY(pivot_rest(side, K + 1));
+        if (e.timing) CU(cudaEventRecord(ev[3 * (K + 1) + 1], side));
+        CU(cudaEventRecord(e.sync[2 * K + 1], side));
+        CU(cudaStreamWaitEvent(st, e.sync[2 * K + 1], 0));
+      } else {
+        TRY(phase3_full(st, K, K > K0));
+      }
+    }
+    if (e.timing) CU(cudaEventRecord(ev[3 * (K1 - 1) + 2], st));
+    c.last_pdl = true;
     return FW_OK;
   }
 
@@ -712,9 +753,9 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
   for (auto &p : parts)
     rk.push_back(Rounds<T, MODE>{c, world, p.D, p.P, p.ld, n, n_pad, p.row0, p.nrows, BS, R, maxkey,
                                  {p.strip[0], p.strip[1]}, done});
-  if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
   c.last_pairs = false;
   c.last_pdl = false;
+  if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
   if (MODE != MODE_TAG && c.pairs && la && world == 1 && BS == 128 && R % 2 == 0 && R >= 4 &&
       rk[0].row0 == 0 && rk[0].nrows == n_pad) {
     c.last_pairs = true;
@@ -1095,7 +1136,21 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   if (c.last_pairs)   // every pair relaxes all tiles outside its strip region through 256 k
     relax = (double)(R / 2) * (double)(n_pad - 2 * BS) * (double)(n_pad - 2 * BS) * (2.0 * BS);
   s.phase3_relaxations = relax;
-  if (timing && c.last_pairs && c.last_pdl) {   // bulk launches overlap: timed as one span
+  if (timing && !c.last_pairs && c.last_pdl) {   // phase-3 launches overlap: timed as one span
+    auto at = [&](cudaEvent_t e) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e_begin, e);
+      return (double)t;
+    };
+    for (int K = 0; K < R; ++K) {
+      const double p1 = at(ev.ev[3 * K]), p2 = at(ev.ev[3 * K + 1]);
+      s.phase1_ms += p1 - (K > 0 ? at(ev.sync[2 * K]) : at(e_init));
+      s.phase2_ms += p2 - p1;
+    }
+    const double p3e = at(ev.ev[3 * (R - 1) + 2]);
+    s.phase3_ms = p3e - at(ev.ev[1]);
+    s.post_ms = at(e_post) - p3e;
+  } else if (timing && c.last_pairs && c.last_pdl) {   // bulk launches overlap: timed as one span
     auto at = [&](cudaEvent_t e) {
       float t = 0.f;
       cudaEventElapsedTime(&t, e_begin, e);
