@@ -93,7 +93,11 @@ typedef struct fw_stats {
 
 /* Create the process-wide context. ngpus_max: the most devices one fw_solve may use,
  * 0 = all visible devices; the single-GPU entry points run on the calling thread's current
- * device. flags: FW_PATH_* | FW_TIMING. Returns FW_ESTATE if already initialised. */
+ * device. flags: FW_PATH_* | FW_TIMING. Returns FW_ESTATE if already initialised.
+ * Schedule switches read here from the environment (tuning / A-B only; results are the same,
+ * DESIGN.md §4.6-4.9): FW_LOOKAHEAD=0, FW_PAIRS=0 (one round per phase-3 pass),
+ * FW_PAIR_ORDER=0, FW_PDL=0 (no programmatic dependent launch), FW_PIPE_FIRST=k,
+ * FW_PIPE_PAIR_ROWS=k, FW_COPY_THREADS=k (host copy pool). */
 int fw_init(int ngpus_max, unsigned flags);
 
 /* Release every device buffer, stream and event of the context. Idempotent. */
