@@ -522,3 +522,28 @@ def test_pair_rounds_int32_native_keys(n):
     assert s.p_method == 2 and s.compute_f32 == 0 and s.phase3_launches < s.rounds
     np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
     assert oracle.check_paths(W, D, P)[0] == 0
+
+
+# ---- programmatic dependent launch of consecutive phase-3 launches ----------
+@pytest.mark.parametrize("kind,n,path,pairs", [("complete_int", 1024, "next", "1"),
+                                               ("complete_int", 1000, "lastk", "0"),
+                                               ("complete_real", 1280, "next", "1"),
+                                               ("complete_real", 900, "next", "0"),
+                                               ("er_int", 1152, "next", "1")])
+@pytest.mark.parametrize("device", [True, False])
+def test_pdl_schedule_identical(kind, n, path, pairs, device, monkeypatch):
+    """Phase-3 launches overlapping the previous launch's last wave (main loop before
+    griddepcontrol.wait) give bitwise the same D and P as stream-ordered launches (FW_PDL=0):
+    every tile sees the same operands and the same order of rounds. Checked against the
+    oracle too; device entry point (one solve) and host entry point (row-chunk pipeline)."""
+    monkeypatch.setenv("FW_PAIRS", pairs)
+    W = gen.generate(kind, n, 1200 + n, p=0.05, lo=1, hi=1000)
+    D1, P1 = solve(W, 128, path, device=device)
+    monkeypatch.setenv("FW_PDL", "0")
+    D0, P0 = solve(W, 128, path, device=device)
+    np.testing.assert_array_equal(D1, D0)
+    np.testing.assert_array_equal(P1, P0)
+    exact = exact_data(W)
+    assert_D_matches(D1, oracle.fw(W, None)[0], exact)
+    bad, first = oracle.check_paths(W, D1, P1, rtol=0.0 if exact else 1e-5, mode=path)
+    assert bad == 0, f"{bad} invalid paths, first at {divmod(first, n)}"
