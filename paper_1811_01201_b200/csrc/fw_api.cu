@@ -1845,6 +1845,8 @@ void ctx_release(Ctx *c) {
   c->pev.clear();
   for (auto e : c->ring_ev) cudaEventDestroy(e);
   c->ring_ev.clear();
+  for (auto e : c->xev) cudaEventDestroy(e);
+  c->xev.clear();
   c->ring_used.clear();
   if (c->copy) cudaStreamDestroy(c->copy);
   c->copy = nullptr;
