@@ -145,9 +145,53 @@ def cpu_sample(cfg: dict, seconds_target: float = 15.0, W: np.ndarray | None = N
     gflops = 2.0 * n * n * ks / dt / 1e9
     cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
     return {"value": gflops, "unit": "GFLOPS", "cores": cores, "kind": "oracle",
-            "sample": f"oracle C triple loop (next-hop), k-iterations 1..{ks} of {n} on the full "
-                      f"{n}x{n} {cfg['name']} matrix ({ks} x n^2 relaxations, {dt:.1f} s); "
-                      f"GFLOPS = 2*n^2*k_steps/t"}
+            "sample": f"PROJECTION from a bounded sample: oracle C triple loop (next-hop), k-iterations "
+                      f"1..{ks} of {n} on the full {n}x{n} {cfg['name']} matrix ({ks} x n^2 "
+                      f"relaxations, {dt:.1f} s); GFLOPS = 2*n^2*k_steps/t (full solves at the sizes "
+                      f"the oracle completes: cpu_ladder)",
+            "cpu_model": lscpu_model(), "sample_seconds": dt}
+
+
+def lscpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_full_solve(name: str, threads: int, timeout: float = 240.0) -> dict:
+    """One FULL oracle solve (triple loop with next-hop P) of config `name` in a subprocess
+    with OMP_NUM_THREADS = threads (SURVEY §8(d) timing protocol: C1 at 1 thread and all
+    cores, C2, C3 — the sizes the oracle completes)."""
+    code = ("import json, time, sys; sys.path.insert(0, %r)\n"
+            "import apsp_inputs as gen, oracle\n"
+            "W = gen.config_matrix(%r); oracle.lib()\n"
+            "t0 = time.perf_counter(); oracle.fw(W, 'next'); dt = time.perf_counter() - t0\n"
+            "print(json.dumps({'s': dt, 'n': int(W.shape[0])}))\n") % (ROOT, name)
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           timeout=timeout)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:   # noqa: BLE001 — a baseline that could not be taken is reported as such
+        return {"config": name, "threads": threads, "error": str(e)[:200]}
+    n = d["n"]
+    return {"config": name, "n": n, "threads": threads, "seconds": d["s"],
+            "gflops": 2.0 * n ** 3 / d["s"] / 1e9}
+
+
+def cpu_ladder() -> dict:
+    """Full oracle solves at the sizes the oracle completes, on this host's cores."""
+    cores = len(os.sched_getaffinity(0))
+    runs = [oracle_full_solve("C1", 1), oracle_full_solve("C1", cores), oracle_full_solve("C2", cores),
+            oracle_full_solve("C3", cores)]
+    return {"kind": "oracle (plain C triple loop, next-hop P, -O3, OpenMP over i)",
+            "cpu_model": lscpu_model(), "cores": cores, "runs": runs,
+            "note": "full solves, not projections; GFLOPS = 2 n^3 / t (BASELINE configs[0..2])"}
 
 
 def config_for(name: str, n: int = 0) -> dict:
@@ -163,7 +207,8 @@ def config_for(name: str, n: int = 0) -> dict:
 def config_json(cfg: dict, block: int, world: int) -> dict:
     """The JSON `config` object (identical on both arms)."""
     n = cfg["n"]
-    return {"workload": cfg["desc"], "config": cfg["name"], "n": n, "block": block,
+    desc = cfg["desc"].replace(f"BS={cfg['block']}", f"BS={block}")
+    return {"workload": desc, "config": cfg["name"], "n": n, "block": block,
             "seed": cfg["seed"], "path": "next-hop",
             "l2": (f"inputs larger than L2 (D and P {n * n * 4 / 2**30:g} GiB each)" if n * n * 4 > 126e6
                    else f"inputs fit in L2 ({n * n * 4 / 2**20:g} MiB), not flushed between steps"),
@@ -178,22 +223,74 @@ def run_reference(args, cfg):
     W = host_matrix(cfg)
     base = cpu_sample(cfg, seconds_target=max(2.0, 20.0 / max(1, args.steps + args.warmup)), W=W)
     # each step is one bounded sample; report the median over steps
-    vals = []
+    vals, secs = [], []
     for _ in range(args.warmup):
         cpu_sample(cfg, seconds_target=3.0, W=W)
     for _ in range(args.steps):
-        vals.append(cpu_sample(cfg, seconds_target=max(2.0, 30.0 / max(1, args.steps)), W=W)["value"])
+        r = cpu_sample(cfg, seconds_target=max(2.0, 30.0 / max(1, args.steps)), W=W)
+        vals.append(r["value"])
+        secs.append(r["sample_seconds"])
     v = statistics.median(vals) if vals else base["value"]
     n = cfg["n"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOPS", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2.0 * n ** 3 / (v * 1e9) * 1e3,
+        "steps": args.steps, "warmup": args.warmup,
+        # a step is one bounded sample (k-slice) of the workload: its measured wall time; the
+        # full solve at the sampled rate would take ms_per_full_solve_projected
+        "ms_per_step": 1e3 * statistics.mean(secs) if secs else None,
+        "ms_per_full_solve_projected": 2.0 * n ** 3 / (v * 1e9) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_json(cfg, args.block or cfg["block"], args.gpus),
         "cpu_baseline": {**base, "value": v},
         "e2e": {"value": v, "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def isolated_pivot_phases(fw, solve, dD, dW, dP, n, n_pad, BS, stream, peak_tflops, mix_tflops):
+    """Phases 1 and 2 timed ALONE: one extra solve (after the timed region) with the look-ahead
+    and the two-rounds-per-pass schedule switched off (fw_set_option), so phase 1, the dual
+    phase-2 strip launch and phase 3 of every round run back to back on one stream and the
+    library's per-phase CUDA events bracket each launch on an otherwise idle GPU."""
+    fw.fw_set_option("lookahead", 0)
+    fw.fw_set_option("pairs", 0)
+    try:
+        for _ in range(2):                      # the second solve is reported
+            dD.copy_(dW)
+            solve(dD, dP, n=n, ld=n, block=BS, stream=stream)
+            s = fw.fw_last_stats()
+    finally:
+        fw.fw_set_option("lookahead", 1)
+        fw.fw_set_option("pairs", 1)
+    R = s.rounds
+    p1_us, p2_us = 1e3 * s.phase1_ms / R, 1e3 * s.phase2_ms / R
+    p2_relax = 2.0 * BS * BS * (n_pad - BS)     # row + column strip through BS k each
+    p2_bytes = 2.0 * BS * n_pad * 4             # each strip element read once (changed ones written)
+    import json as _j
+    peaks = {}
+    try:
+        peaks = _j.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    return {
+        "phase1_us_per_round": p1_us,
+        "phase1_relax_per_round": float(BS) ** 3,
+        "phase2_us_per_round": p2_us,
+        "phase2_relax_per_round": p2_relax,
+        "phase2_tflops": 2.0 * p2_relax / (p2_us * 1e-6) / 1e12 if p2_us > 0 else None,
+        "phase2_frac_stated_alu": (2.0 * p2_relax / (p2_us * 1e-6) / 1e12) / peak_tflops if p2_us > 0 else None,
+        "phase2_frac_measured_mix": (2.0 * p2_relax / (p2_us * 1e-6) / 1e12) / mix_tflops if p2_us > 0 else None,
+        "phase2_alg_bytes_per_round": p2_bytes,
+        "phase2_gbps": p2_bytes / (p2_us * 1e-6) / 1e9 if p2_us > 0 else None,
+        "phase2_frac_hbm": (p2_bytes / (p2_us * 1e-6) / 1e9) / hbm if p2_us > 0 else None,
+        "hbm_peak_gbs": hbm,
+        "solve_ms_serialized": s.solve_ms,
+        "note": "one extra solve with fw_set_option(lookahead=0, pairs=0): per-round phase-1 and dual "
+                "phase-2 launch times from the library's CUDA events, serialized on one stream. The "
+                "strips run BS relaxations per 4-byte element (32 relax/B at BS=128): ALU-bound, not "
+                "HBM-bound, so phase2_frac_measured_mix is the fraction that matters",
+    }
 
 
 def run_gpu(args, cfg):
@@ -293,14 +390,19 @@ def run_gpu(args, cfg):
     single_issue = sms * 128 * max_mhz * 1e6 * 2 / 1e12
     mix = sms * 95.53 * max_mhz * 1e6 * 2 / 1e12
     phase2_ms = sum(s.phase2_ms for s in stats) / len(stats)
-    p2_bytes = 2.0 * BS * ((n + 127) // 128 * 128) * 4 * s0.rounds   # both pivot strips read per round
+    n_pad = (n + 127) // 128 * 128
     roof = {"bound": "alu", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
             "traffic": traffic,
             "kernel": f"minplus_tile_kernel<{ctype},128,128,{mode}> (phase 3, rank 0"
                       + (", two rounds per pass: 256-deep bulk launches" if s0.phase3_launches < s0.rounds else "")
                       + ")",
+            "launches_per_step": p3_launches / len(stats),
             "avg_launch_ms": avg_launch_ms,
+            "flop_per_launch": 2.0 * p3_relax / max(1, p3_launches),
+            "timing": "phase-3 CUDA-event span of the step / bulk launches in it (library FW_TIMING "
+                      "events on the launching stream; consecutive bulk launches overlap by PDL, so "
+                      "the span is their union)",
             "peak_basis": f"stated FP32 add+min issue roofline: {sms} SMs x 128 lanes x {max_mhz:.0f} MHz "
                           "(2 flop per relaxation, BASELINE north_star)",
             "other_ceilings": {
@@ -310,17 +412,13 @@ def run_gpu(args, cfg):
                 "frac_measured_mix": (achieved_tflops / mix) if achieved_tflops else None,
                 "basis": "FADD2 (2 adds) + FMNMX3 (2 mins) = one issue slot per relaxation: "
                          "SMs x 128 relax/clk; L0 probe FADD2+FMNMX3 mix 95.5 relax/clk/SM"},
-            "phase2_hbm": {"gbps": p2_bytes / (phase2_ms * 1e-3) / 1e9 if phase2_ms > 0 else None,
-                           "bytes_per_step": p2_bytes,
-                           "note": "algorithmic reads of the row and column pivot strips per round "
-                                   "(changed-element writes not counted) over the phase-2 event time; "
-                                   "phase 2 runs on the look-ahead stream under phase 3, so this "
-                                   "understates the strip kernels' own bandwidth (ncu: "
-                                   "profiles/r01b_p2_c4_ncu_summary.txt)"},
             "phase_ms_per_step": {"phase1": sum(s.phase1_ms for s in stats) / len(stats),
                                   "phase2": phase2_ms,
                                   "phase3": p3_ms / len(stats),
                                   "post": sum(s.post_ms for s in stats) / len(stats)}}
+    if world == 1 and BS == 128 and not args.no_isolated:
+        roof["pivot_path_isolated"] = isolated_pivot_phases(fw, solve, dD, dW, dP, n, n_pad, BS, stream,
+                                                           peak_tflops, mix)
     launches = sum(s.kernel_launches for s in stats)
 
     # e2e: the same metric through the public API with pinned host buffers, H2D + solve + D2H
@@ -367,8 +465,11 @@ def run_gpu(args, cfg):
     fw.fw_free()
 
     cpu = None
+    ladder = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample(cfg, W=W)
+        if not args.no_cpu_ladder:
+            ladder = cpu_ladder()
 
     if rank == 0:
         line = {
@@ -379,6 +480,7 @@ def run_gpu(args, cfg):
             "config": config_json(cfg, BS, world),
             "roofline": roof,
             "cpu_baseline": cpu,
+            "cpu_ladder": ladder,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -401,6 +503,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-ladder", action="store_true", help="skip the full oracle solves at C1-C3")
+    ap.add_argument("--no-isolated", action="store_true", help="skip the isolated phase-1/2 solve")
     args = ap.parse_args()
     cfg = config_for(args.config, args.n)
     if args.impl == "reference":

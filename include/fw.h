@@ -80,7 +80,8 @@ typedef struct fw_stats {
   double post_ms;       /* P resolution post-pass                              */
   double h2d_ms;        /* host entry points only                              */
   double d2h_ms;
-  int64_t phase3_launches;
+  int64_t phase3_launches; /* bulk phase-3 launches: one per round, or one per pair of rounds
+                              when two rounds share a 256-deep pass       */
   double phase3_relaxations; /* relaxations issued by phase-3 launches (algorithmic) */
   int64_t kernel_launches; /* kernels this library launched for the solve (incl. validation) */
   int32_t compute_f32;  /* 1 = relaxations ran in FP32: FP32 data, or INT32 data whose stored
@@ -89,6 +90,9 @@ typedef struct fw_stats {
                            (DESIGN.md §4.8); 0 = copies not overlapped. With a pipeline,
                            h2d_ms / d2h_ms are the EXPOSED parts (until the first chunk
                            landed / after the last chunk computed) and solve_ms the whole call */
+  int64_t broadcasts;   /* ncclBroadcast calls this rank issued (pivot strips + the TAG-mode
+                           post-pass gather); 0 without a communicator                    */
+  double bcast_bytes;   /* bytes those broadcasts moved (per rank, as root or receiver)   */
 } fw_stats;
 
 /* Create the process-wide context. ngpus_max: the most devices one fw_solve may use,
@@ -99,6 +103,16 @@ typedef struct fw_stats {
  * FW_PAIR_ORDER=0, FW_PDL=0 (no programmatic dependent launch), FW_PIPE_FIRST=k,
  * FW_PIPE_PAIR_ROWS=k, FW_COPY_THREADS=k (host copy pool). */
 int fw_init(int ngpus_max, unsigned flags);
+
+/* Schedule switches of the live context (the same ones fw_init reads from the environment;
+ * tuning, A/B comparisons and isolated per-phase timing — distances are identical, P valid):
+ *   "lookahead"  0/1  phases 1-2 of round K+1 on the side stream under phase 3 of round K (§4.6)
+ *   "pairs"      0/1  two rounds per phase-3 pass for keyed / distance-only solves (§4.9)
+ *   "pdl"        0/1  programmatic dependent launch between consecutive phase-3 launches
+ *   "pair_order" 0/1  the next pair's strips beside (1) or before (0) the bulk launch
+ *   "pipe_pair_rows" k >= 1, "pipe_first" k in [1, 64]  host pipeline geometry (§4.8)
+ * FW_ESTATE before fw_init; FW_EINVAL for an unknown name or value. */
+int fw_set_option(const char *name, int value);
 
 /* Release every device buffer, stream and event of the context. Idempotent. */
 int fw_free(void);

@@ -15,6 +15,7 @@ from ._binding import (  # noqa: F401
     fw_solve,
     fw_solve_i32,
     fw_set_host_pipeline,
+    fw_set_option,
     fw_host_pipeline_bounds,
     fw_path,
     fw_solve_device_f32,

@@ -35,7 +35,7 @@ class FwStats(ctypes.Structure):
         ("post_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
         ("phase3_launches", ctypes.c_int64), ("phase3_relaxations", ctypes.c_double),
         ("kernel_launches", ctypes.c_int64), ("compute_f32", ctypes.c_int32),
-        ("host_chunks", ctypes.c_int32),
+        ("host_chunks", ctypes.c_int32), ("broadcasts", ctypes.c_int64), ("bcast_bytes", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:
@@ -57,6 +57,7 @@ _lib.fw_free.argtypes = []
 _lib.fw_solve.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_solve_i32.argtypes = [_P, _P, _I64, _I, _I]
 _lib.fw_set_host_pipeline.argtypes = [_I]
+_lib.fw_set_option.argtypes = [ctypes.c_char_p, _I]
 _lib.fw_host_pipeline_bounds.argtypes = [_I64, _I, _I, ctypes.POINTER(ctypes.c_int32), _I]
 _lib.fw_path.argtypes = [_P, _P, _I, _I64, _I64, _I64, _I, _P, _I64]
 _lib.fw_path.restype = ctypes.c_int64
@@ -103,12 +104,62 @@ def _addr(x, dtype_name: str | None = None):
 
 
 def _n_of(dist, n):
-    if n is not None:
-        return int(n)
-    shape = tuple(dist.shape)
-    if len(shape) != 2 or shape[0] != shape[1]:
+    shape = tuple(dist.shape) if hasattr(dist, "shape") else None
+    if shape is not None and (len(shape) != 2 or shape[0] != shape[1]):
         raise ValueError(f"dist must be n x n, got {shape}")
-    return shape[0]
+    if n is None:
+        if shape is None:
+            raise ValueError("n is required with a raw address")
+        return shape[0]
+    n = int(n)
+    if shape is not None and n != shape[0]:
+        raise ValueError(f"n = {n} but dist is {shape[0]} x {shape[1]}")
+    return n
+
+
+def _is_cuda(x) -> bool:
+    return bool(getattr(x, "is_cuda", False))
+
+
+def _host_matrix(x, n: int, dtype_name: str, what: str):
+    """Address of an n x n host matrix (numpy array or CPU tensor) of dtype_name; None -> NULL.
+    Raw integer addresses are passed through unchecked (the caller vouches for them)."""
+    if x is None or isinstance(x, int):
+        return x
+    if _is_cuda(x):
+        raise ValueError(f"{what}: a CUDA tensor was passed to a host entry point "
+                         "(use fw_solve_device_*)")
+    if tuple(x.shape) != (n, n):
+        raise ValueError(f"{what} must be {n} x {n}, got {tuple(x.shape)}")
+    return _addr(x, dtype_name)
+
+
+def _device_matrix(x, n: int, ld: int, dtype_name: str, what: str):
+    """Address of n rows of pitch ld on the CURRENT CUDA device (torch tensor); None -> NULL.
+    The tensor must hold at least n rows of ld elements (2-D: shape (>= n, ld))."""
+    if x is None or isinstance(x, int):
+        return x
+    if not _is_cuda(x):
+        raise ValueError(f"{what}: device entry points need a CUDA tensor (got a host array)")
+    import torch
+    if x.device.index != torch.cuda.current_device():
+        raise ValueError(f"{what} is on {x.device}, the current device is cuda:{torch.cuda.current_device()}")
+    shape = tuple(x.shape)
+    if len(shape) != 2 or shape[1] != ld or shape[0] < n:
+        raise ValueError(f"{what} must have shape (>= {n}, {ld}) for n = {n}, ld = {ld}; got {shape}")
+    return _addr(x, dtype_name)
+
+
+def _ld_of(x, n: int, ld):
+    if ld is not None:
+        ld = int(ld)
+    elif hasattr(x, "shape") and len(tuple(x.shape)) == 2:
+        ld = int(tuple(x.shape)[1])
+    else:
+        ld = n
+    if ld < n:
+        raise ValueError(f"ld = {ld} < n = {n}")
+    return ld
 
 
 def fw_init(ngpus_max: int = 0, flags: int = 0) -> None:
@@ -122,7 +173,15 @@ def fw_free() -> None:
 def fw_solve(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:
     """FP32 host solve in place (dist: n x n float32; next: n x n int32 or None).
     ngpus: 1 = current device (default here), G > 1 = devices 0..G-1, 0 = fw_init's ngpus_max."""
-    _check(_lib.fw_solve(_addr(dist, "float32"), _addr(next, "int32"), _n_of(dist, n), block, ngpus))
+    n = _n_of(dist, n)
+    _check(_lib.fw_solve(_host_matrix(dist, n, "float32", "dist"), _host_matrix(next, n, "int32", "next"), n,
+                         block, ngpus))
+
+
+def fw_set_option(name: str, value: int) -> None:
+    """Schedule switch of the live context: lookahead, pairs, pdl, pair_order (0/1),
+    pipe_pair_rows, pipe_first (see include/fw.h)."""
+    _check(_lib.fw_set_option(name.encode(), int(value)))
 
 
 def fw_set_host_pipeline(chunk_tiles: int = -1) -> None:
@@ -143,6 +202,10 @@ def fw_path(P, i: int, j: int, mode: int = FW_PATH_NEXT_HOP, dist=None) -> list[
     """Vertices of the shortest i -> j path encoded by P (host array from a solve; host-only).
     [] if j is unreachable from i. dist (the solve's D) is required in LAST_K mode."""
     n = _n_of(P, None)
+    if _is_cuda(P) or _is_cuda(dist):
+        raise ValueError("fw_path is host-only: pass host arrays")
+    if dist is not None and tuple(dist.shape) != tuple(P.shape):
+        raise ValueError(f"dist {tuple(dist.shape)} and P {tuple(P.shape)} differ in shape")
     d_addr = _addr(dist) if dist is not None else None
     is_int = 1 if (dist is not None and str(getattr(dist, "dtype", "")).endswith("int32")) else 0
     p_addr = _addr(P, "int32")
@@ -160,7 +223,9 @@ def fw_path(P, i: int, j: int, mode: int = FW_PATH_NEXT_HOP, dist=None) -> list[
 
 def fw_solve_i32(dist, next=None, n=None, block: int = 0, ngpus: int = 1) -> None:
     """INT32 host solve in place (no-edge = FW_INF_I32)."""
-    _check(_lib.fw_solve_i32(_addr(dist, "int32"), _addr(next, "int32"), _n_of(dist, n), block, ngpus))
+    n = _n_of(dist, n)
+    _check(_lib.fw_solve_i32(_host_matrix(dist, n, "int32", "dist"), _host_matrix(next, n, "int32", "next"), n,
+                             block, ngpus))
 
 
 def _stream_handle(stream):
@@ -173,16 +238,18 @@ def _stream_handle(stream):
 
 def fw_solve_device_f32(d_dist, d_next=None, n=None, ld=None, block: int = 0, stream=None) -> None:
     """FP32 device solve in place; d_dist/d_next CUDA tensors (or device addresses)."""
-    n = _n_of(d_dist, n)
-    ld = n if ld is None else ld
-    _check(_lib.fw_solve_device_f32(_addr(d_dist, "float32"), _addr(d_next, "int32"), n, ld, block,
+    n = int(n) if n is not None else _n_of(d_dist, None)
+    ld = _ld_of(d_dist, n, ld)
+    _check(_lib.fw_solve_device_f32(_device_matrix(d_dist, n, ld, "float32", "d_dist"),
+                                    _device_matrix(d_next, n, ld, "int32", "d_next"), n, ld, block,
                                     _stream_handle(stream)))
 
 
 def fw_solve_device_i32(d_dist, d_next=None, n=None, ld=None, block: int = 0, stream=None) -> None:
-    n = _n_of(d_dist, n)
-    ld = n if ld is None else ld
-    _check(_lib.fw_solve_device_i32(_addr(d_dist, "int32"), _addr(d_next, "int32"), n, ld, block,
+    n = int(n) if n is not None else _n_of(d_dist, None)
+    ld = _ld_of(d_dist, n, ld)
+    _check(_lib.fw_solve_device_i32(_device_matrix(d_dist, n, ld, "int32", "d_dist"),
+                                    _device_matrix(d_next, n, ld, "int32", "d_next"), n, ld, block,
                                     _stream_handle(stream)))
 
 
@@ -217,33 +284,47 @@ def fw_dist_solve_device_f32(d_rows, d_next_rows=None, n=None, ld=None, block: i
     """Collective FP32 solve of this rank's rows (see fw_dist_partition)."""
     if n is None:
         raise ValueError("n (global vertex count) is required")
-    ld = d_rows.shape[1] if ld is None else ld
-    _check(_lib.fw_dist_solve_device_f32(_addr(d_rows, "float32"), _addr(d_next_rows, "int32"), n, ld,
+    n = int(n)
+    ld = _ld_of(d_rows, n, ld)
+    rows = d_rows.shape[0] if hasattr(d_rows, "shape") else 0
+    if d_next_rows is not None and hasattr(d_next_rows, "shape") and hasattr(d_rows, "shape") \
+            and tuple(d_next_rows.shape) != tuple(d_rows.shape):
+        raise ValueError(f"d_next_rows {tuple(d_next_rows.shape)} != d_rows {tuple(d_rows.shape)}")
+    _check(_lib.fw_dist_solve_device_f32(_device_matrix(d_rows, rows, ld, "float32", "d_rows"),
+                                         _device_matrix(d_next_rows, rows, ld, "int32", "d_next_rows"), n, ld,
                                          block, _stream_handle(stream)))
 
 
 def fw_dist_solve_device_i32(d_rows, d_next_rows=None, n=None, ld=None, block: int = 0, stream=None) -> None:
     if n is None:
         raise ValueError("n (global vertex count) is required")
-    ld = d_rows.shape[1] if ld is None else ld
-    _check(_lib.fw_dist_solve_device_i32(_addr(d_rows, "int32"), _addr(d_next_rows, "int32"), n, ld,
+    n = int(n)
+    ld = _ld_of(d_rows, n, ld)
+    rows = d_rows.shape[0] if hasattr(d_rows, "shape") else 0
+    if d_next_rows is not None and hasattr(d_next_rows, "shape") and hasattr(d_rows, "shape") \
+            and tuple(d_next_rows.shape) != tuple(d_rows.shape):
+        raise ValueError(f"d_next_rows {tuple(d_next_rows.shape)} != d_rows {tuple(d_rows.shape)}")
+    _check(_lib.fw_dist_solve_device_i32(_device_matrix(d_rows, rows, ld, "int32", "d_rows"),
+                                         _device_matrix(d_next_rows, rows, ld, "int32", "d_next_rows"), n, ld,
                                          block, _stream_handle(stream)))
 
 
 def fw_dist_loopback_solve_device_f32(d_dist, d_next=None, n=None, ld=None, block: int = 0, world: int = 2,
                                       stream=None) -> None:
     """Every rank of a `world`-way partition emulated on this GPU (testing transport)."""
-    n = _n_of(d_dist, n)
-    ld = n if ld is None else ld
-    _check(_lib.fw_dist_loopback_solve_device_f32(_addr(d_dist, "float32"), _addr(d_next, "int32"), n, ld,
+    n = int(n) if n is not None else _n_of(d_dist, None)
+    ld = _ld_of(d_dist, n, ld)
+    _check(_lib.fw_dist_loopback_solve_device_f32(_device_matrix(d_dist, n, ld, "float32", "d_dist"),
+                                                  _device_matrix(d_next, n, ld, "int32", "d_next"), n, ld,
                                                   block, world, _stream_handle(stream)))
 
 
 def fw_dist_loopback_solve_device_i32(d_dist, d_next=None, n=None, ld=None, block: int = 0, world: int = 2,
                                       stream=None) -> None:
-    n = _n_of(d_dist, n)
-    ld = n if ld is None else ld
-    _check(_lib.fw_dist_loopback_solve_device_i32(_addr(d_dist, "int32"), _addr(d_next, "int32"), n, ld,
+    n = int(n) if n is not None else _n_of(d_dist, None)
+    ld = _ld_of(d_dist, n, ld)
+    _check(_lib.fw_dist_loopback_solve_device_i32(_device_matrix(d_dist, n, ld, "int32", "d_dist"),
+                                                  _device_matrix(d_next, n, ld, "int32", "d_next"), n, ld,
                                                   block, world, _stream_handle(stream)))
 
 

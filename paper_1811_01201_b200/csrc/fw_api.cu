@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -28,6 +29,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <map>
 #include <condition_variable>
@@ -82,6 +84,9 @@ struct Nccl {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t *, int, ncclUniqueId, int, ncclConfig_t *) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 Nccl g_nccl;
 
@@ -93,7 +98,8 @@ int load_nccl() {
   *reinterpret_cast<void **>(&g_nccl.name) = dlsym(h, "nccl" #name);                     \
   if (!g_nccl.name) return fail(FW_ENCCL, "libnccl.so.2 lacks nccl" #name);
   SYM(GetUniqueId) SYM(CommInitRank) SYM(CommInitAll) SYM(CommDestroy) SYM(Broadcast) SYM(AllReduce)
-  SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString)
+  SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString) SYM(CommInitRankConfig) SYM(CommGetAsyncError)
+  SYM(CommAbort)
 #undef SYM
   g_nccl.h = h;
   return FW_OK;
@@ -161,6 +167,8 @@ struct Ctx {
   int pipe_pair_rows = 32;         // host pipeline: smallest chunk (tile-rows) run in pairs (env FW_PIPE_PAIR_ROWS)
   bool last_pairs = false;         // the last solve ran in pairs (stats layout)
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
+  bool comm_dead = false;          // the communicator was aborted (error, timeout, failed peer)
+  std::atomic<int> *abort_flag = nullptr;   // team solve: set by the first rank that fails
   int rank = 0, world = 1;
   int ngpus_max = 1;               // fw_init's limit (0 there = every visible device)
   std::vector<Ctx *> team;         // fw_solve with ngpus > 1: one context per device, rank = device
@@ -172,6 +180,114 @@ Ctx *g_ctx = nullptr;
 // kernels this library launched (fw_stats.kernel_launches); per host thread, so the rank
 // threads of a single-process multi-GPU solve count their own launches
 thread_local int64_t g_launches = 0;
+
+// NCCL broadcasts this thread issued (fw_stats.broadcasts / bcast_bytes)
+thread_local int64_t g_bcasts = 0;
+thread_local double g_bcast_bytes = 0;
+
+// ---- NCCL failure handling --------------------------------------------------------------
+// Communicators are created non-blocking (ncclConfig_t.blocking = 0): no NCCL call blocks the
+// host, a call may return ncclInProgress and is then polled to completion here. Every wait of
+// a multi-GPU solve (NCCL calls, stream synchronisation) is bounded: it polls
+// ncclCommGetAsyncError, the team's abort flag (a rank of a single-process team failed) and a
+// timeout (env FW_NCCL_TIMEOUT_MS, default 600000), and on any of them aborts the communicator
+// (its kernels exit) so the call returns FW_ENCCL instead of hanging.
+int64_t nccl_timeout_ms() {
+  const char *e = getenv("FW_NCCL_TIMEOUT_MS");
+  const long long v = e ? atoll(e) : 0;
+  return v > 0 ? v : 600000;
+}
+
+int comm_abort(Ctx &c, const char *why) {
+  if (c.comm) g_nccl.CommAbort(c.comm);
+  c.comm = nullptr;
+  c.comm_dead = true;
+  if (c.abort_flag) c.abort_flag->store(1);
+  return fail(FW_ENCCL, "NCCL communicator aborted: %s", why);
+}
+
+bool peer_failed(const Ctx &c) { return c.abort_flag && c.abort_flag->load() != 0; }
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// One poll of the communicator's state: FW_OK while healthy (done or still in progress).
+int comm_health(Ctx &c, bool *in_progress, std::chrono::steady_clock::time_point t0, const char *what) {
+  ncclResult_t st = ncclSuccess;
+  const ncclResult_t r = g_nccl.CommGetAsyncError(c.comm, &st);
+  if (r != ncclSuccess) st = r;
+  *in_progress = st == ncclInProgress;
+  char buf[320];
+  if (st != ncclSuccess && st != ncclInProgress) {
+    snprintf(buf, sizeof buf, "%s: %s", what, g_nccl.GetErrorString(st));
+    return comm_abort(c, buf);
+  }
+  if (peer_failed(c)) {
+    snprintf(buf, sizeof buf, "%s: another rank of the team failed", what);
+    return comm_abort(c, buf);
+  }
+  if (ms_since(t0) > (double)nccl_timeout_ms()) {
+    snprintf(buf, sizeof buf, "%s: timed out after %lld ms (FW_NCCL_TIMEOUT_MS)", what,
+             (long long)nccl_timeout_ms());
+    return comm_abort(c, buf);
+  }
+  return FW_OK;
+}
+
+// Poll a non-blocking communicator until its pending operation (init, enqueue) has completed.
+int nccl_settle(Ctx &c, const char *what) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    bool busy = false;
+    TRY(comm_health(c, &busy, t0, what));
+    if (!busy) return FW_OK;
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+// NCCL call on the context's communicator (ncclInProgress polled, errors abort it).
+#define NCC(c, call)                                                                              \
+  do {                                                                                            \
+    if (!(c).comm) return fail(FW_ENCCL, "no live NCCL communicator for %s", #call);             \
+    const ncclResult_t r_ = (call);                                                               \
+    if (r_ == ncclInProgress) TRY(nccl_settle((c), #call));                                       \
+    else if (r_ != ncclSuccess) {                                                                 \
+      char b_[320];                                                                               \
+      snprintf(b_, sizeof b_, "%s: %s", #call, g_nccl.GetErrorString(r_));                        \
+      return comm_abort((c), b_);                                                                 \
+    }                                                                                             \
+  } while (0)
+
+// Wait for a stream. With a communicator (or inside a team solve) the wait polls: a hung or
+// failed collective, or a failed peer, aborts the communicator and returns FW_ENCCL.
+int sync_stream(Ctx &c, cudaStream_t st) {
+  if (!c.comm && !c.abort_flag) {
+    CU(cudaStreamSynchronize(st));
+    return FW_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return FW_OK;
+    if (e != cudaErrorNotReady) CU(e);
+    if (c.comm) {
+      bool busy = false;
+      TRY(comm_health(c, &busy, t0, "waiting for the solve's stream"));
+    } else if (peer_failed(c)) {
+      return fail(FW_ENCCL, "another rank of the team failed");
+    } else if (ms_since(t0) > (double)nccl_timeout_ms()) {
+      return fail(FW_ENCCL, "stream wait timed out (FW_NCCL_TIMEOUT_MS)");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+// NVTX ranges (host-side enqueue spans per solve / round / phase, for an nsys timeline).
+struct Nvtx {
+  explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 // Dynamic shared memory limits are a per-device function attribute: set once per
 // (kernel, device) — a process may drive several devices (fw_solve with ngpus > 1).
@@ -329,6 +445,18 @@ struct Rounds {
   int *done;     // R look-ahead tile counters (zeroed per solve)
   const T *Dg = nullptr;   // one GPU, a row range of the matrix (host pipeline): global row 0,
                            // so the pivot strips of other rows are read in place
+  bool nccl = false;       // this rank's rows of an NCCL communicator (any world size, 1 included):
+                           // every round's pivot strip goes through ncclBroadcast
+
+  // d_flags of the solve: maxkey is always d_flags + 2; bit 4 of d_flags[0] = a look-ahead
+  // wait timed out (wait_count_kernel)
+  int *errflags() const { return maxkey - 2; }
+  int wait_count(cudaStream_t st, int K, int target) {
+    wait_count_kernel<<<1, 1, 0, st>>>(done + K, target, errflags(), 20ull * 1000 * 1000 * 1000);
+    ++g_launches;
+    CU(cudaGetLastError());
+    return FW_OK;
+  }
 
   bool owns(int K) const {
     const int64_t kb = (int64_t)K * BS;
@@ -600,7 +728,7 @@ struct Rounds {
       }
       return FW_OK;
     }
-    if (world == 1 && c.pair_pdl) return run_pdl(st, e, K0, K1);
+    if (world == 1 && !nccl && c.pair_pdl) return run_pdl(st, e, K0, K1);
     cudaStream_t side = c.side;
     TRY(phase1(st, K0));
     if (e.timing) CU(cudaEventRecord(ev[3 * K0], st));
@@ -614,9 +742,7 @@ struct Rounds {
         TRY(phase3_ordered(st, K, done + K, &nprio));
         if (e.timing) CU(cudaEventRecord(ev[3 * K + 2], st));
         // pivot stream: wait for the look-ahead tiles of round K, then round K+1's pivot
-        wait_count_kernel<<<1, 1, 0, side>>>(done + K, nprio);
-        ++g_launches;
-        CU(cudaGetLastError());
+        TRY(wait_count(side, K, nprio));
         if (e.timing) CU(cudaEventRecord(e.sync[2 * K + 2], side));
         TRY(phase1(side, K + 1));
         if (e.timing) CU(cudaEventRecord(ev[3 * (K + 1)], side));
@@ -653,9 +779,7 @@ struct Rounds {
         int nprio = 0;
         TRY(phase3_ordered(st, K, done + K, &nprio, K > K0));
         CU(cudaStreamWaitEvent(side, c.xev[K], 0));
-        wait_count_kernel<<<1, 1, 0, side>>>(done + K, nprio);
-        ++g_launches;
-        CU(cudaGetLastError());
+        TRY(wait_count(side, K, nprio));
         if (e.timing) CU(cudaEventRecord(e.sync[2 * K + 2], side));
         TRY(phase1(side, K + 1));
         if (e.timing) CU(cudaEventRecord(ev[3 * (K + 1)], side));
@@ -674,12 +798,14 @@ struct Rounds {
 
   // pivot phases after phase 1: strips and (multi-GPU) the broadcast
   int pivot_rest(cudaStream_t st, int K) {
-    if (world == 1) return phase2(st, K, true, true);
+    if (!nccl) return phase2(st, K, true, true);
     TRY(phase2(st, K, true, false));
     void *buf = owns(K) ? (void *)(D + (int64_t)lrow(K) * ld) : (void *)strip[K & 1];
-    NC(g_nccl.Broadcast(buf, buf, (size_t)BS * (size_t)n_pad,
-                        std::is_integral<T>::value ? ncclInt32 : ncclFloat32,
-                        owner_of(n_pad, world, (int64_t)K * BS), c.comm, st));
+    NCC(c, g_nccl.Broadcast(buf, buf, (size_t)BS * (size_t)n_pad,
+                            std::is_integral<T>::value ? ncclInt32 : ncclFloat32,
+                            owner_of(n_pad, world, (int64_t)K * BS), c.comm, st));
+    ++g_bcasts;
+    g_bcast_bytes += (double)BS * (double)n_pad * sizeof(T);
     return phase2(st, K, false, true);
   }
 };
@@ -750,13 +876,15 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
                int R, int *maxkey, int *done, cudaStream_t st, const Events &ev, bool la) {
   const int64_t n_pad = (n + 127) / 128 * 128;
   std::vector<Rounds<T, MODE>> rk;
-  for (auto &p : parts)
+  for (auto &p : parts) {
     rk.push_back(Rounds<T, MODE>{c, world, p.D, p.P, p.ld, n, n_pad, p.row0, p.nrows, BS, R, maxkey,
                                  {p.strip[0], p.strip[1]}, done});
+    rk.back().nccl = tr == T_NCCL;
+  }
   c.last_pairs = false;
   c.last_pdl = false;
   if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
-  if (MODE != MODE_TAG && c.pairs && la && world == 1 && BS == 128 && R % 2 == 0 && R >= 4 &&
+  if (MODE != MODE_TAG && c.pairs && la && tr == T_LOCAL && BS == 128 && R % 2 == 0 && R >= 4 &&
       rk[0].row0 == 0 && rk[0].nrows == n_pad) {
     c.last_pairs = true;
     return rk[0].run_pairs(st, ev);
@@ -890,7 +1018,7 @@ template <typename T>
 int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS, int mode,
               int path_mode, int *d_flags, cudaStream_t st, bool transposed = false) {
   const int64_t n_pad = (n + 127) / 128 * 128;
-  const bool nccl = tr == T_NCCL && world > 1;
+  const bool nccl = tr == T_NCCL;
   // keyed mode: keys -> distances inside finalize_paths_kernel (decode = 1); keys only exist
   // with P (want_p), so the finalize pass always runs then
   if (mode == MODE_TAG && path_mode >= 0) {
@@ -905,16 +1033,18 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
       if (p.nrows > 0)
         CU(cudaMemcpy2DAsync(full + p.row0 * n_pad, n_pad * sizeof(T), p.D, p.ld * sizeof(T),
                              n_pad * sizeof(T), p.nrows, cudaMemcpyDeviceToDevice, st));
-      NC(g_nccl.GroupStart());
+      NCC(c, g_nccl.GroupStart());
       for (int r = 0; r < world; ++r) {
         int64_t r0, nr;
         partition(n, world, r, &r0, &nr);
         if (nr == 0) continue;
         T *dst = full + r0 * n_pad;
-        NC(g_nccl.Broadcast(dst, dst, (size_t)nr * n_pad, is_int_v<T>() ? ncclInt32 : ncclFloat32, r,
-                            c.comm, st));
+        NCC(c, g_nccl.Broadcast(dst, dst, (size_t)nr * n_pad, is_int_v<T>() ? ncclInt32 : ncclFloat32, r,
+                                c.comm, st));
+        ++g_bcasts;
+        g_bcast_bytes += (double)nr * (double)n_pad * sizeof(T);
       }
-      NC(g_nccl.GroupEnd());
+      NCC(c, g_nccl.GroupEnd());
       Dfull = full;
       ldf = n_pad;
     }
@@ -960,24 +1090,31 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
   return FW_OK;
 }
 
+template <typename T>
+int place_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int64_t n, int BS, bool want_p,
+                bool may_retry, cudaStream_t st);
+template <typename T>
+int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS,
+                 cudaStream_t st, const std::vector<Attempt> &plan, int *d_flags, int *h_flags,
+                 int64_t bcasts0, double bcast_bytes0);
+
 // Solve over `parts` (one part = one rank's rows): T_LOCAL (one GPU, all rows), T_NCCL (this
 // process's rank of an NCCL communicator), T_LOOPBACK (every rank emulated here).
 template <typename T>
 int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS,
                 cudaStream_t st) {
   const bool int_t = is_int_v<T>();
-  const int64_t n_pad = (n + 127) / 128 * 128;
   const bool want_p = parts[0].next != nullptr;
-  const bool lastk = (c.flags & FW_PATH_LAST_K) != 0;
-  const int path_mode = want_p ? (lastk ? 1 : 0) : -1;
-  const bool timing = (c.flags & FW_TIMING) != 0 && tr != T_LOOPBACK;
-  const bool nccl = tr == T_NCCL && world > 1;
+  const bool nccl = tr == T_NCCL;
+  Nvtx nv_solve("fw_solve");
+  const int64_t bcasts0 = g_bcasts;
+  const double bcast_bytes0 = g_bcast_bytes;
 
   // 1. validation (read-only; outputs untouched on error), reduced over all ranks
   const int R = (int)((n + BS - 1) / BS);  // rounds wholly inside the padding are skipped
   TRY(c.scratch.ensure(64 + 4 * (size_t)R));
-  int *d_flags = static_cast<int *>(c.scratch.p);   // [0] flags [1] max weight [2] max key
-  int *d_done = d_flags + 16;                        // R look-ahead tile counters
+  // [0] flags [1] max weight [2] max key [3] placement status; [16..16+R) look-ahead counters
+  int *d_flags = static_cast<int *>(c.scratch.p);
   CU(cudaMemsetAsync(d_flags, 0, 16, st));
   for (auto &p : parts) {
     if (p.nsrc == 0) continue;
@@ -988,14 +1125,37 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     CU(cudaGetLastError());
   }
   // flag bits are combined with max: the rank holding a bit holds the max value as well
-  if (nccl) NC(g_nccl.AllReduce(d_flags, d_flags, 2, ncclInt32, ncclMax, c.comm, st));
+  if (nccl) NCC(c, g_nccl.AllReduce(d_flags, d_flags, 2, ncclInt32, ncclMax, c.comm, st));
   int h_flags[4] = {0, 0, 0, 0};
   CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  TRY(sync_stream(c, st));
   std::vector<Attempt> plan;
   TRY(make_plan(int_t, want_p, h_flags, n, &plan));
 
-  // 3. placement
+  // 3. placement; over a communicator every rank learns whether all ranks placed their
+  //    workspaces before the first broadcast (a rank that failed to allocate must not leave its
+  //    peers waiting in a collective)
+  int place_rc = place_parts(c, parts, tr, n, BS, want_p, plan.size() > 1, st);
+  if (nccl) {
+    std::string place_err = g_err;
+    CU(cudaMemsetAsync(d_flags + 3, place_rc != FW_OK ? 1 : 0, 1, st));
+    NCC(c, g_nccl.AllReduce(d_flags + 3, d_flags + 3, 1, ncclInt32, ncclMax, c.comm, st));
+    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
+    TRY(sync_stream(c, st));
+    if (place_rc != FW_OK) return fail(place_rc, "%s", place_err.c_str());
+    if (h_flags[3]) return fail(FW_ENOMEM, "another rank failed to place its workspaces");
+  }
+  TRY(place_rc);
+  return solve_placed<T>(c, parts, tr, world, n, BS, st, plan, d_flags, h_flags, bcasts0, bcast_bytes0);
+}
+
+// Workspaces of the parts: the loopback workspace, or this rank's rows in place / padded, the
+// strip receive buffers of a communicator rank, and the backup of W for a speculative key run.
+template <typename T>
+int place_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int64_t n, int BS, bool want_p,
+                bool may_retry, cudaStream_t st) {
+  const int64_t n_pad = (n + 127) / 128 * 128;
+  const bool nccl = tr == T_NCCL;
   if (tr == T_LOOPBACK) {
     // one padded n_pad x n_pad workspace: each part uses its own rows of it
     TRY(c.ws_d.ensure((size_t)n_pad * n_pad * sizeof(T)));
@@ -1034,14 +1194,30 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
       p.strip[1] = reinterpret_cast<T *>(static_cast<char *>(c.ws_s.p) + sb);
     }
     // a speculative key run may have to be redone: keep W when solving in place
-    if (plan.size() > 1 && p.inplace && p.nsrc > 0) {
+    if (may_retry && p.inplace && p.nsrc > 0) {
       TRY(c.ws_b.ensure((size_t)p.nsrc * n * sizeof(T)));
       p.backup = static_cast<T *>(c.ws_b.p);
       CU(cudaMemcpy2DAsync(p.backup, n * sizeof(T), p.src, p.ld_src * sizeof(T), n * sizeof(T),
                            p.nsrc, cudaMemcpyDeviceToDevice, st));
     }
   }
+  return FW_OK;
+}
 
+// The solve after validation and placement: the plan's attempts, the post-pass, unpad, stats.
+template <typename T>
+int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS,
+                 cudaStream_t st, const std::vector<Attempt> &plan, int *d_flags, int *h_flags,
+                 int64_t bcasts0, double bcast_bytes0) {
+  const bool int_t = is_int_v<T>();
+  const int64_t n_pad = (n + 127) / 128 * 128;
+  const bool want_p = parts[0].next != nullptr;
+  const bool lastk = (c.flags & FW_PATH_LAST_K) != 0;
+  const int path_mode = want_p ? (lastk ? 1 : 0) : -1;
+  const bool timing = (c.flags & FW_TIMING) != 0 && tr != T_LOOPBACK;
+  const bool nccl = tr == T_NCCL;
+  const int R = (int)((n + BS - 1) / BS);
+  int *d_done = d_flags + 16;
   TRY(ensure_events(c, 4 + 3 * (size_t)R + 2 * (size_t)R));
   cudaEvent_t e_begin = c.events[0], e_end = c.events[1], e_init = c.events[2],
               e_post = c.events[3];
@@ -1066,9 +1242,9 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
       TRY((run_attempt<T, T>(c, parts, parts, tr, world, n, BS, R, used.mode, from_backup, d_maxkey,
                              d_done, st, ev, la, e_init)));
     if (!is_key(used.mode) || used.key_static) break;
-    if (nccl) NC(g_nccl.AllReduce(d_maxkey, d_maxkey, 1, ncclInt32, ncclMax, c.comm, st));
-    CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
+    if (nccl) NCC(c, g_nccl.AllReduce(d_maxkey, d_maxkey, 1, ncclInt32, ncclMax, c.comm, st));
+    CU(cudaMemcpyAsync(h_flags, d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    TRY(sync_stream(c, st));
     if (getenv("FW_DEBUG"))
       fprintf(stderr, "fwb: speculative key run: max stored key bits %d, limit %d\n", h_flags[2], used.key_limit);
     if (h_flags[2] <= used.key_limit || a + 1 == plan.size()) break;
@@ -1106,8 +1282,10 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
     }
   }
   CU(cudaEventRecord(e_end, st));
-  CU(cudaMemcpyAsync(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  CU(cudaMemcpyAsync(h_flags, d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  TRY(sync_stream(c, st));
+  if (h_flags[0] & 16)
+    return fail(FW_ECUDA, "a look-ahead wait timed out (wait_count_kernel): the results are not valid");
   if (h_flags[0] & 8)
     return fail(FW_ERANGE, "next-hop resolution did not converge (zero-weight cycle?)");
 
@@ -1123,7 +1301,10 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   float ms = 0.f;
   CU(cudaEventElapsedTime(&ms, e_begin, e_end));
   s.solve_ms = ms;
-  s.phase3_launches = c.last_pairs ? R - 1 : R;
+  // bulk phase-3 launches issued: one per pair of rounds with pairs, else one per round
+  s.phase3_launches = c.last_pairs ? R / 2 : R;
+  s.broadcasts = g_bcasts - bcasts0;
+  s.bcast_bytes = g_bcast_bytes - bcast_bytes0;
   s.kernel_launches = g_launches - launches0;
   // phase-3 relaxations of this process's rows: rows and columns outside the round's strips
   double relax = 0;
@@ -1213,7 +1394,8 @@ int solve_rows(Ctx &c, T *src, int64_t ld_src, int32_t *next, int64_t ld_next, i
   partition(n, world, rank, &p.row0, &p.nrows);
   p.nsrc = std::max<int64_t>(0, std::min(p.nrows, n - p.row0));
   std::vector<Part<T>> parts{p};
-  return solve_parts<T>(c, parts, world > 1 ? T_NCCL : T_LOCAL, world, n, BS, st);
+  // a communicator of any size (one rank included) takes the NCCL data plane
+  return solve_parts<T>(c, parts, c.comm ? T_NCCL : T_LOCAL, world, n, BS, st);
 }
 
 // Every rank of a `world`-way partition emulated in this process (loopback transport).
@@ -1776,6 +1958,8 @@ int solve_host_pipelined(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, bool
   CU(cudaEventRecord(e_end, c.copy));
   CU(cudaStreamSynchronize(c.copy));
   CU(cudaMemcpy(h_flags, d_flags, sizeof h_flags, cudaMemcpyDeviceToHost));
+  if (h_flags[0] & 16)
+    return fail(FW_ECUDA, "a look-ahead wait timed out (wait_count_kernel): the results are not valid");
   if (h_flags[0] & 8)
     return fail(FW_ERANGE, "next-hop resolution did not converge (zero-weight cycle?)");
 
@@ -1855,13 +2039,11 @@ void ctx_release(Ctx *c) {
   c->stream = c->side = nullptr;
 }
 
+void team_release(Ctx &c);
+
 int team_setup(Ctx &c, int G) {
   if ((int)c.team.size() == G) return FW_OK;
-  for (Ctx *t : c.team) {
-    ctx_release(t);
-    delete t;
-  }
-  c.team.clear();
+  team_release(c);
   TRY(load_nccl());
   std::vector<int> devs(G);
   for (int d = 0; d < G; ++d) {
@@ -1872,11 +2054,37 @@ int team_setup(Ctx &c, int G) {
     t->rank = d;
     t->world = G;
   }
-  std::vector<ncclComm_t> comms(G);
-  NC(g_nccl.CommInitAll(comms.data(), G, devs.data()));
+  // non-blocking communicators (bounded waits, abort on failure: see nccl_settle), one per
+  // device, created in one group
+  ncclUniqueId uid;
+  NC(g_nccl.GetUniqueId(&uid));
+  std::vector<ncclComm_t> comms(G, nullptr);
+  NC(g_nccl.GroupStart());
+  for (int d = 0; d < G; ++d) {
+    CU(cudaSetDevice(devs[d]));
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;
+    const ncclResult_t r = g_nccl.CommInitRankConfig(&comms[d], G, uid, d, &cfg);
+    if (r != ncclSuccess && r != ncclInProgress) {
+      g_nccl.GroupEnd();
+      return fail(FW_ENCCL, "ncclCommInitRankConfig(device %d): %s", d, g_nccl.GetErrorString(r));
+    }
+  }
+  const ncclResult_t ge = g_nccl.GroupEnd();
+  if (ge != ncclSuccess && ge != ncclInProgress)
+    return fail(FW_ENCCL, "ncclGroupEnd (team init): %s", g_nccl.GetErrorString(ge));
   for (int d = 0; d < G; ++d) c.team[d]->comm = comms[d];
+  for (int d = 0; d < G; ++d) TRY(nccl_settle(*c.team[d], "team communicator init"));
   CU(cudaSetDevice(c.dev));
   return FW_OK;
+}
+
+void team_release(Ctx &c) {
+  for (Ctx *t : c.team) {
+    ctx_release(t);
+    delete t;
+  }
+  c.team.clear();
 }
 
 // One rank of a team solve: copy its block-rows of the host matrix in, solve, copy them out.
@@ -1893,13 +2101,13 @@ int team_rank_solve(Ctx &t, T *dist, int32_t *next, int64_t n, int BS) {
   int32_t *tp = next ? static_cast<int32_t *>(t.user_t.p) : nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   if (bytes) TRY(copy_h2d(t, d, dist + row0 * n, bytes, t.stream));
-  CU(cudaStreamSynchronize(t.stream));
+  TRY(sync_stream(t, t.stream));
   const auto t1 = std::chrono::steady_clock::now();
   TRY(solve_rows<T>(t, d, n, tp, n, n, BS, t.stream));
   const auto t2 = std::chrono::steady_clock::now();
   if (bytes) TRY(copy_d2h(t, dist + row0 * n, d, bytes, t.stream));
   if (next && pbytes) TRY(copy_d2h(t, next + row0 * n, tp, pbytes, t.stream));
-  CU(cudaStreamSynchronize(t.stream));
+  TRY(sync_stream(t, t.stream));
   const auto t3 = std::chrono::steady_clock::now();
   t.stats.h2d_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   t.stats.d2h_ms = std::chrono::duration<double, std::milli>(t3 - t2).count();
@@ -1908,19 +2116,42 @@ int team_rank_solve(Ctx &t, T *dist, int32_t *next, int64_t n, int BS) {
 
 template <typename T>
 int solve_host_team(Ctx &c, T *dist, int32_t *next, int64_t n, int BS, int G) {
-  TRY(team_setup(c, G));
+  {
+    const int rc0 = team_setup(c, G);
+    if (rc0 != FW_OK) {
+      const std::string e = g_err;
+      team_release(c);
+      return fail(rc0, "%s", e.c_str());
+    }
+  }
+  // the first rank that fails raises the flag; its peers' bounded waits (sync_stream,
+  // nccl_settle) see it and abort their communicators instead of waiting in a collective
+  std::atomic<int> abort_flag{0};
+  for (Ctx *t : c.team) t->abort_flag = &abort_flag;
   std::vector<int> rc(G, FW_OK);
   std::vector<std::string> err(G);
   std::vector<std::thread> th;
   for (int d = 0; d < G; ++d)
     th.emplace_back([&, d] {
       rc[d] = team_rank_solve<T>(*c.team[d], dist, next, n, BS);
-      if (rc[d] != FW_OK) err[d] = g_err;   // g_err is thread-local
+      if (rc[d] != FW_OK) {
+        err[d] = g_err;   // g_err is thread-local
+        abort_flag.store(1);
+      }
     });
   for (auto &x : th) x.join();
+  for (Ctx *t : c.team) t->abort_flag = nullptr;
   cudaSetDevice(c.dev);
+  int first = -1;   // the rank that failed on its own (not because a peer did), else any failed rank
   for (int d = 0; d < G; ++d)
-    if (rc[d] != FW_OK) return fail(rc[d], "rank %d (device %d): %s", d, c.team[d]->dev, err[d].c_str());
+    if (rc[d] != FW_OK && (first < 0 || (rc[first] == FW_ENCCL && rc[d] != FW_ENCCL))) first = d;
+  if (first >= 0) {
+    const int code = rc[first];
+    const std::string msg = err[first];
+    const int dev = c.team[first]->dev;
+    team_release(c);   // communicators aborted or in an unknown state: rebuilt on the next call
+    return fail(code, "rank %d (device %d): %s", first, dev, msg.c_str());
+  }
   c.stats = c.team[0]->stats;   // rank 0's solve; host copies: the slowest rank
   for (int d = 1; d < G; ++d) {
     c.stats.h2d_ms = std::max(c.stats.h2d_ms, c.team[d]->stats.h2d_ms);
@@ -1990,7 +2221,9 @@ int solve_dev_entry(T *d_dist, int32_t *d_next, int64_t n, int64_t ld, int block
   if (!dist && c.comm)
     return fail(FW_ESTATE, "a multi-GPU communicator is active: use fw_dist_solve_* or fw_comm_free");
   if (dist && c.comm == nullptr)
-    return fail(FW_ESTATE, "fw_dist_solve_* needs fw_comm_init first");
+    return fail(c.comm_dead ? FW_ENCCL : FW_ESTATE,
+                c.comm_dead ? "the communicator was aborted after an NCCL failure: fw_comm_free, then fw_comm_init"
+                            : "fw_dist_solve_* needs fw_comm_init first");
   return solve_rows<T>(c, d_dist, ld, d_next, ld, n, BS, static_cast<cudaStream_t>(stream));
 }
 
@@ -2013,9 +2246,9 @@ int fw_init(int ngpus_max, unsigned flags) {
   CU(cudaGetDevice(&c->dev));
   cudaDeviceProp prop;
   CU(cudaGetDeviceProperties(&prop, c->dev));
-  if (prop.major < 10) {
+  if (prop.major != 10 || prop.minor != 0) {   // arch-specific sm_100a SASS only, no portable PTX
     delete c;
-    return fail(FW_ECUDA, "device %s is sm_%d%d; this library is built for sm_100a", prop.name,
+    return fail(FW_ECUDA, "device %s is sm_%d%d; this library is built for sm_100a only", prop.name,
                 prop.major, prop.minor);
   }
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -2036,6 +2269,21 @@ int fw_init(int ngpus_max, unsigned flags) {
   if (pf && atoi(pf) >= 1 && atoi(pf) <= 64) c->pipe_first = atoi(pf);
   g_ctx = c;
   g_err.clear();
+  return FW_OK;
+}
+
+int fw_set_option(const char *name, int value) {
+  if (!g_ctx) return fail(FW_ESTATE, "fw_init has not been called");
+  if (!name) return fail(FW_EINVAL, "name is NULL");
+  Ctx &c = *g_ctx;
+  const std::string k = name;
+  if (k == "lookahead") c.lookahead = value != 0;
+  else if (k == "pairs") c.pairs = value != 0;
+  else if (k == "pdl") c.pair_pdl = value != 0;
+  else if (k == "pair_order") c.pair_order = value != 0;
+  else if (k == "pipe_pair_rows" && value >= 1) c.pipe_pair_rows = value;
+  else if (k == "pipe_first" && value >= 1 && value <= 64) c.pipe_first = value;
+  else return fail(FW_EINVAL, "unknown option or value: %s = %d", name, value);
   return FW_OK;
 }
 
@@ -2172,7 +2420,15 @@ int fw_comm_init(const unsigned char *id, int rank, int world) {
   ncclUniqueId uid;
   memcpy(&uid, id, sizeof uid);
   CU(cudaSetDevice(g_ctx->dev));
-  NC(g_nccl.CommInitRank(&g_ctx->comm, world, uid, rank));
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.blocking = 0;   // bounded waits: a missing or failed peer ends in FW_ENCCL, not a hang
+  const ncclResult_t r = g_nccl.CommInitRankConfig(&g_ctx->comm, world, uid, rank, &cfg);
+  if (r != ncclSuccess && r != ncclInProgress) {
+    g_ctx->comm = nullptr;
+    return fail(FW_ENCCL, "ncclCommInitRankConfig: %s", g_nccl.GetErrorString(r));
+  }
+  g_ctx->comm_dead = false;
+  TRY(nccl_settle(*g_ctx, "communicator init"));
   g_ctx->rank = rank;
   g_ctx->world = world;
   return FW_OK;
@@ -2185,6 +2441,7 @@ int fw_comm_free(void) {
     g_nccl.CommDestroy(g_ctx->comm);
   }
   g_ctx->comm = nullptr;
+  g_ctx->comm_dead = false;
   g_ctx->rank = 0;
   g_ctx->world = 1;
   return FW_OK;

@@ -420,12 +420,21 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
 }
 
 // Look-ahead gate: the pivot stream waits until `target` look-ahead tiles of the running
-// ordered phase-3 launch have been stored (one thread; acquire load + back-off).
-__global__ void wait_count_kernel(const int *done, int target) {
+// ordered phase-3 launch have been stored (one thread; acquire load + back-off). Bounded: after
+// timeout_ns of global time it sets bit 4 of *flags (the host fails the solve) and returns, so
+// an aborted or never-scheduled producer cannot hang the stream.
+__global__ void wait_count_kernel(const int *done, int target, int *flags, unsigned long long timeout_ns) {
   int v;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
     if (v >= target) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      atomicOr(flags, 16);
+      break;
+    }
     __nanosleep(256);
   }
 }

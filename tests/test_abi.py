@@ -78,3 +78,25 @@ def test_binding_marshalling_errors():
         fw.fw_solve(np.zeros((3, 4), np.float32))
     with pytest.raises(ValueError):
         fw.fw_solve(np.zeros((4, 4), np.float32)[:, ::2].T)
+
+
+def test_binding_shape_and_device_checks():
+    """the binding rejects mismatched shapes and host/device mix-ups before any
+    pointer reaches the library (an overrun or a device pointer dereferenced on the host)."""
+    import torch
+    import paper_1811_01201_b200 as fw
+    D = np.zeros((4, 4), np.float32)
+    with pytest.raises(ValueError):
+        fw.fw_solve(D, np.zeros((3, 3), np.int32))           # next smaller than dist
+    with pytest.raises(ValueError):
+        fw.fw_solve(D, None, n=8)                            # explicit n beyond the array
+    with pytest.raises(ValueError):
+        fw.fw_solve_i32(np.zeros((4, 4), np.int32), np.zeros((4, 5), np.int32))
+    with pytest.raises(ValueError):                          # host tensor on a device entry
+        fw.fw_solve_device_f32(torch.zeros((4, 4)), None)
+    with pytest.raises(ValueError):
+        fw.fw_dist_loopback_solve_device_i32(torch.zeros((4, 4), dtype=torch.int32), None)
+    with pytest.raises(ValueError):
+        fw.fw_dist_solve_device_f32(torch.zeros((4, 4)), None, n=4)
+    with pytest.raises(ValueError):                          # fw_path: D and P shapes differ
+        fw.fw_path(np.zeros((4, 4), np.int32), 0, 1, dist=np.zeros((3, 3), np.float32))

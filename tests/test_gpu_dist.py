@@ -85,11 +85,13 @@ def test_loopback_fallback_to_tags():
     np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % 700))
 
 
-def test_nccl_single_rank_communicator():
-    """fw_comm_unique_id / fw_comm_init / fw_dist_solve_device_* with a one-rank communicator."""
-    n = 300
-    W = gen.generate("complete_int", n, 5)
-    fw.fw_init(0, 0)
+def _nccl_one_rank(W, block, path="next", timing=True):
+    """fw_dist_solve_device_* over a ONE-rank NCCL communicator: the NCCL data plane runs
+    (every round's pivot strip through ncclBroadcast, validation / placement / key checks
+    through ncclAllReduce, the TAG post-pass gather through grouped broadcasts)."""
+    n = W.shape[0]
+    flags = (fw.FW_TIMING if timing else 0) | (fw.FW_PATH_LAST_K if path == "lastk" else 0)
+    fw.fw_init(0, flags)
     try:
         uid = fw.fw_comm_unique_id()
         assert len(uid) == 128
@@ -97,16 +99,76 @@ def test_nccl_single_rank_communicator():
         row0, nrows = fw.fw_dist_partition(n, 1, 0)
         assert (row0, nrows) == (0, n)
         dD = torch.from_numpy(W).cuda()
-        dP = torch.empty((n, n), dtype=torch.int32, device="cuda")
-        fw.fw_dist_solve_device_f32(dD, dP, n=n, block=64, stream=torch.cuda.current_stream())
+        dP = torch.empty((n, n), dtype=torch.int32, device="cuda") if path else None
+        f = fw.fw_dist_solve_device_i32 if W.dtype == np.int32 else fw.fw_dist_solve_device_f32
+        f(dD, dP, n=n, block=block, stream=torch.cuda.current_stream())
+        s = fw.fw_last_stats()
         with pytest.raises(fw.FwError):     # single-GPU entry refused while a communicator is active
             fw.fw_solve(W.copy(), None)
         fw.fw_comm_free()
-        D, P = dD.cpu().numpy(), dP.cpu().numpy()
+        return dD.cpu().numpy(), (dP.cpu().numpy() if dP is not None else None), s
     finally:
         fw.fw_free()
-    np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
-    assert oracle.check_paths(W, D, P)[0] == 0
+
+
+@pytest.mark.parametrize("kind,n,block,path", [
+    ("complete_int", 300, 64, "next"),      # keyed P, one round per launch, BS 64
+    ("complete_int", 1000, 128, "next"),    # keyed P, look-ahead schedule with the broadcast
+    ("complete_real", 777, 128, "next"),    # round tags: the post-pass gathers D by broadcasts
+    ("er_int", 900, 128, "lastk"),          # INT32 with INF, LAST_K
+    ("complete_int", 640, 128, None),       # distance only
+])
+def test_nccl_single_rank_communicator(kind, n, block, path):
+    W = gen.generate(kind, n, 5 + n, p=0.02, lo=1, hi=1000 if kind.startswith("er") else 100)
+    D, P, s = _nccl_one_rank(W, block, path)
+    R = (n + block - 1) // block
+    # every round's pivot strip went through ncclBroadcast (a speculative key run that falls
+    # back runs the rounds again; the TAG post-pass adds one gather broadcast per rank)
+    assert s.broadcasts >= R and s.broadcasts % R == (1 if s.p_method == 1 and path else 0) % R, \
+        (s.broadcasts, R)
+    assert s.bcast_bytes >= R * block * s.n_pad * 4
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    if path:
+        bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5, mode=path)
+        assert bad == 0, (bad, divmod(first, n))
+
+
+def test_nccl_one_rank_matches_single_gpu_bitwise():
+    """The NCCL data plane (one rank) and the single-GPU schedule give the same D; P valid."""
+    W = gen.generate("complete_int", 1024, 77)
+    D1, P1, _ = _nccl_one_rank(W, 128)
+    fw.fw_init(0, 0)
+    try:
+        dD = torch.from_numpy(W).cuda()
+        dP = torch.empty(W.shape, dtype=torch.int32, device="cuda")
+        fw.fw_solve_device_f32(dD, dP, block=128, stream=torch.cuda.current_stream())
+        D0 = dD.cpu().numpy()
+    finally:
+        fw.fw_free()
+    np.testing.assert_array_equal(D1, D0)
+
+
+def test_nccl_missing_peer_times_out(monkeypatch):
+    """A two-rank communicator whose second rank never joins: the non-blocking init is polled,
+    times out (FW_NCCL_TIMEOUT_MS) and aborts with FW_ENCCL instead of hanging the process."""
+    monkeypatch.setenv("FW_NCCL_TIMEOUT_MS", "4000")
+    fw.fw_init(0, 0)
+    try:
+        uid = fw.fw_comm_unique_id()
+        with pytest.raises(fw.FwError) as e:
+            fw.fw_comm_init(uid, 0, 2)
+        assert e.value.code == fw.FW_ENCCL and "timed out" in str(e.value)
+        with pytest.raises(fw.FwError):      # no live communicator: the dist entry refuses
+            fw.fw_dist_solve_device_f32(torch.zeros((128, 128), device="cuda"), None, n=128)
+        fw.fw_comm_free()
+        # the context stays usable for single-GPU solves
+        W = gen.generate("complete_int", 200, 3)
+        D = W.copy()
+        fw.fw_solve(D, None)
+        np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+    finally:
+        fw.fw_free()
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,

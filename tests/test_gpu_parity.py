@@ -269,12 +269,27 @@ def _dijkstra_rows_check(W, D, P, seed, exact, count=64):
 
 
 def test_config_C3_er_int32():
-    """configs[2]: n=8192 ER p=0.1 INT32 [1,1000]: Dijkstra rows bitwise + O(n^2) next check."""
+    """configs[2]: n=8192 ER p=0.1 INT32 [1,1000]. n < 16384, so no sampling (BJ north_star):
+    D bit-exact against the FULL oracle triple loop on every entry, every next-hop path of
+    all n^2 pairs reconstructed and summed to D, plus 64 Dijkstra rows (independent)."""
     c = gen.CONFIGS["C3"]
     W = gen.config_matrix("C3")
     D, P = solve(W, 128)
+    Dref, _ = oracle.fw(W, None)
+    assert_D_matches(D, Dref, exact=True)
+    bad, first = oracle.check_paths(W, D, P)
+    assert bad == 0, f"{bad} invalid next-hop paths, first at {divmod(first, W.shape[0])}"
     _dijkstra_rows_check(W, D, P, c["seed"], True)
-    assert next_consistency(W, D, P, exact=True) == 0
+
+
+def test_config_C3_device_lastk_full():
+    """C3 through the device entry in LAST_K mode: full-oracle D bitwise, all LAST_K paths."""
+    W = gen.config_matrix("C3")
+    D, P = solve(W, 128, path="lastk", device=True)
+    Dref, _ = oracle.fw(W, None)
+    assert_D_matches(D, Dref, exact=True)
+    bad, first = oracle.check_paths(W, D, P, mode="lastk")
+    assert bad == 0, f"{bad} invalid LAST_K paths, first at {divmod(first, W.shape[0])}"
 
 
 def test_config_C3_sparse_unreachable():
@@ -294,6 +309,20 @@ def test_config_C4_16384():
     D, P = solve(W, 128)
     _dijkstra_rows_check(W, D, P, c["seed"], True)
     assert next_consistency(W, D, P, exact=True) == 0
+
+
+@pytest.mark.slow
+def test_config_C4_full_oracle():
+    """configs[3] against the FULL oracle triple loop (n^3 = 4.4e12 relaxations on the host
+    cores, a few minutes): D bitwise on all 2.7e8 entries, every next-hop path of every pair
+    reconstructed and summed to D. Beyond north_star's 64-source requirement at n >= 16384."""
+    W = gen.config_matrix("C4")
+    D, P = solve(W, 128)
+    Dref, _ = oracle.fw(W, None)
+    assert_D_matches(D, Dref, exact=True)
+    del Dref
+    bad, first = oracle.check_paths(W, D, P)
+    assert bad == 0, f"{bad} invalid next-hop paths, first at {divmod(first, W.shape[0])}"
 
 
 @pytest.mark.slow
@@ -547,3 +576,23 @@ def test_pdl_schedule_identical(kind, n, path, pairs, device, monkeypatch):
     assert_D_matches(D1, oracle.fw(W, None)[0], exact)
     bad, first = oracle.check_paths(W, D1, P1, rtol=0.0 if exact else 1e-5, mode=path)
     assert bad == 0, f"{bad} invalid paths, first at {divmod(first, n)}"
+
+
+@pytest.mark.parametrize("opt", ["lookahead", "pairs", "pdl", "pair_order"])
+def test_set_option_schedules_identical_D(opt):
+    """fw_set_option switches the schedule of the live context: the distances stay identical
+    (integer data) and P stays a valid next hop."""
+    W = gen.generate("complete_int", 1024, 55)
+    out = []
+    for v in (1, 0):
+        D = W.copy()
+        P = np.empty(W.shape, dtype=np.int32)
+        with Ctx(0):
+            fw.fw_set_option(opt, v)
+            fw.fw_solve(D, P, block=128)
+        out.append(D)
+        assert oracle.check_paths(W, D, P)[0] == 0
+    np.testing.assert_array_equal(out[0], out[1])
+    with Ctx(0):
+        with pytest.raises(fw.FwError):
+            fw.fw_set_option("no_such_option", 1)

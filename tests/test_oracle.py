@@ -43,7 +43,10 @@ def test_golden(name, dtype):
     if "NEXT" in g:
         np.testing.assert_array_equal(P, g["NEXT"])
     if "LASTK" in g:
-        _, PL = oracle.fw(W.astype(np.float32), "lastk")
+        # both branches of the oracle's LAST_K mode (oracle_fw_f32 / oracle_fw_i32 mode 1)
+        Wl = Wi if dtype == np.int32 else W.astype(np.float32)
+        DL, PL = oracle.fw(Wl, "lastk")
+        np.testing.assert_array_equal(DL, Dexp)
         np.testing.assert_array_equal(PL, g["LASTK"])
 
 
@@ -80,6 +83,14 @@ def test_vs_dijkstra_all_sources(kind, n, p):
     else:
         np.testing.assert_array_equal(D.astype(np.float64), R)
     assert oracle.check_paths(W, D, P)[0] == 0
+    # LAST_K branch of the same type (INT32: oracle_fw_i32 mode 1): same D, and every path
+    # expanded recursively from P sums to D over the original edges
+    DL, PL = oracle.fw(W, "lastk")
+    np.testing.assert_array_equal(DL, D)
+    assert oracle.check_paths(W, DL, PL, mode="lastk")[0] == 0
+    # -1 exactly where no intermediate vertex improved: the direct edge is optimal or no path
+    direct = (W == D) | (D >= INF if W.dtype == np.int32 else np.isinf(D))
+    assert np.all(PL[~direct] >= 0)
 
 
 def test_real_weights_within_tolerance_of_exact():
