@@ -93,6 +93,9 @@ typedef struct fw_stats {
   int64_t broadcasts;   /* ncclBroadcast calls this rank issued (pivot strips + the TAG-mode
                            post-pass gather); 0 without a communicator                    */
   double bcast_bytes;   /* bytes those broadcasts moved (per rank, as root or receiver)   */
+  int32_t persistent;   /* 1 = the rounds ran as ONE persistent launch (work items ordered by
+                           round, per-tile readiness counters): phase3_ms is
+                           that launch (all phases) and phase3_relaxations = n_pad^3        */
 } fw_stats;
 
 /* Create the process-wide context. ngpus_max: the most devices one fw_solve may use,
@@ -111,6 +114,11 @@ int fw_init(int ngpus_max, unsigned flags);
  *   "pdl"        0/1  programmatic dependent launch between consecutive phase-3 launches
  *   "pair_order" 0/1  the next pair's strips beside (1) or before (0) the bulk launch
  *   "pipe_pair_rows" k >= 1, "pipe_first" k in [1, 64]  host pipeline geometry (§4.8)
+ *   "persistent" -1/0/1  the rounds of a one-GPU BS = 128 solve as ONE persistent launch whose
+ *                        work items wait on per-tile round counters (§4.10): -1 auto (round-tag
+ *                        solves), 0 off, 1 on (env FW_PERSISTENT)
+ *   "persist_gap" k >= 0 persistent: phase-3 tiles between phase 1 and phase 2 of the next
+ *                        round in the work order (-1 auto)
  * FW_ESTATE before fw_init; FW_EINVAL for an unknown name or value. */
 int fw_set_option(const char *name, int value);
 

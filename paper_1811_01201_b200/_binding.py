@@ -36,6 +36,7 @@ class FwStats(ctypes.Structure):
         ("phase3_launches", ctypes.c_int64), ("phase3_relaxations", ctypes.c_double),
         ("kernel_launches", ctypes.c_int64), ("compute_f32", ctypes.c_int32),
         ("host_chunks", ctypes.c_int32), ("broadcasts", ctypes.c_int64), ("bcast_bytes", ctypes.c_double),
+        ("persistent", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

@@ -16,6 +16,7 @@
 // DESIGN.md §4.9). The host entry points split the rows into chunks whose copies overlap the
 // rounds (solve_host_pipelined, reading R16).
 #include "fw_kernels.cuh"
+#include "fw_persist.cuh"
 #include "../../include/fw.h"
 
 #include <cuda_runtime.h>
@@ -166,6 +167,10 @@ struct Ctx {
   bool pair_order = true;          // pairs: the next pair's strips run beside the bulk launch (env FW_PAIR_ORDER=0: before it)
   int pipe_pair_rows = 32;         // host pipeline: smallest chunk (tile-rows) run in pairs (env FW_PIPE_PAIR_ROWS)
   bool last_pairs = false;         // the last solve ran in pairs (stats layout)
+  int persistent = -1;             // one persistent launch per solve (fw_persist.cuh): -1 auto, 0 off, 1 on
+  int persist_gap = -1;            // persistent: rest tiles between P1(K+1) and P2(K+1) (-1 auto)
+  bool last_persist = false;       // the last solve ran as one persistent launch
+  DevBuf ws_ver;                   // persistent: per-tile round counters + work counter
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
   bool comm_dead = false;          // the communicator was aborted (error, timeout, failed peer)
   std::atomic<int> *abort_flag = nullptr;   // team solve: set by the first rank that fails
@@ -871,6 +876,57 @@ struct Part {
   T *backup = nullptr;
 };
 
+// The whole solve as one persistent launch (fw_persist.cuh): one GPU, all rows,
+// BS = 128. Auto: round-tag solves (real-valued data, one round per pass). Keyed and
+// distance-only solves keep the two-rounds-per-pass schedule (§4.9), whose 256-deep bulk
+// launches the persistent one-round items do not match.
+bool use_persistent(const Ctx &c, int mode, int tr, int BS, int64_t n_pad, int64_t row0, int64_t nrows) {
+  if (tr != T_LOCAL || BS != 128 || row0 != 0 || nrows != n_pad || c.persistent == 0) return false;
+  if (c.persistent == 1) return true;
+  return mode == MODE_TAG && n_pad >= 4 * 128;
+}
+
+template <typename T, int MODE>
+int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *maxkey, cudaStream_t st,
+                   const Events &e) {
+  const int Tn = (int)(n_pad / 128);
+  const size_t vbytes = (size_t)Tn * Tn * sizeof(int);
+  TRY(c.ws_ver.ensure(vbytes + 64));
+  int *ver = static_cast<int *>(c.ws_ver.p);
+  auto *next = reinterpret_cast<unsigned long long *>(static_cast<char *>(c.ws_ver.p) + vbytes);
+  CU(cudaMemsetAsync(c.ws_ver.p, 0, vbytes + 64, st));
+  auto kern = fw_persistent_kernel<T, MODE>;
+  constexpr int bytes = TileShape<128, 128>::kBytes;
+  TRY(smem_attr((const void *)kern, bytes));
+  int dev = 0, sms = 0, per_sm = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, bytes));
+  if (per_sm < 1) return fail(FW_ECUDA, "fw_persistent_kernel does not fit on an SM");
+  const int grid = per_sm * sms;
+  PersistArgs a{};
+  a.D = D;
+  a.P = P;
+  a.ld = ld;
+  a.T = Tn;
+  // P1(K+1) takes about one tile wait + 1.6 tile times; the P2(K+1) items go in after roughly that
+  // many grid-waves of round K's phase-3 tiles, so they rarely wait
+  a.gap = c.persist_gap >= 0 ? c.persist_gap : (int)(2.5 * grid);
+  a.ver = ver;
+  a.next = next;
+  a.maxkey = maxkey;
+  a.flags = maxkey - 2;
+  a.total = 2LL * Tn - 1 + (long long)Tn * Tn * Tn;
+  a.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  Nvtx nv("persistent solve");
+  if (e.timing) CU(cudaEventRecord(e.ev[0], st));
+  kern<<<grid, kThreads, bytes, st>>>(a);
+  ++g_launches;
+  CU(cudaGetLastError());
+  if (e.timing) CU(cudaEventRecord(e.ev[2], st));
+  return FW_OK;
+}
+
 template <typename T, int MODE>
 int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int64_t n, int BS,
                int R, int *maxkey, int *done, cudaStream_t st, const Events &ev, bool la) {
@@ -883,7 +939,12 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
   }
   c.last_pairs = false;
   c.last_pdl = false;
+  c.last_persist = false;
   if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
+  if (use_persistent(c, MODE, tr, BS, n_pad, rk[0].row0, rk[0].nrows)) {
+    c.last_persist = true;
+    return run_persistent<T, MODE>(c, rk[0].D, rk[0].P, rk[0].ld, n_pad, maxkey, st, ev);
+  }
   if (MODE != MODE_TAG && c.pairs && la && tr == T_LOCAL && BS == 128 && R % 2 == 0 && R >= 4 &&
       rk[0].row0 == 0 && rk[0].nrows == n_pad) {
     c.last_pairs = true;
@@ -1286,6 +1347,8 @@ int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, i
   TRY(sync_stream(c, st));
   if (h_flags[0] & 16)
     return fail(FW_ECUDA, "a look-ahead wait timed out (wait_count_kernel): the results are not valid");
+  if (h_flags[0] & 32)
+    return fail(FW_ECUDA, "a persistent-kernel dependency wait timed out: the results are not valid");
   if (h_flags[0] & 8)
     return fail(FW_ERANGE, "next-hop resolution did not converge (zero-weight cycle?)");
 
@@ -1302,7 +1365,8 @@ int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, i
   CU(cudaEventElapsedTime(&ms, e_begin, e_end));
   s.solve_ms = ms;
   // bulk phase-3 launches issued: one per pair of rounds with pairs, else one per round
-  s.phase3_launches = c.last_pairs ? R / 2 : R;
+  s.phase3_launches = c.last_persist ? 1 : c.last_pairs ? R / 2 : R;
+  s.persistent = c.last_persist ? 1 : 0;
   s.broadcasts = g_bcasts - bcasts0;
   s.bcast_bytes = g_bcast_bytes - bcast_bytes0;
   s.kernel_launches = g_launches - launches0;
@@ -1316,8 +1380,19 @@ int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, i
     }
   if (c.last_pairs)   // every pair relaxes all tiles outside its strip region through 256 k
     relax = (double)(R / 2) * (double)(n_pad - 2 * BS) * (double)(n_pad - 2 * BS) * (2.0 * BS);
+  if (c.last_persist)  // one launch does every phase: n_pad^3 relaxations (phases 1, 2 and 3)
+    relax = (double)n_pad * (double)n_pad * (double)n_pad;
   s.phase3_relaxations = relax;
-  if (timing && !c.last_pairs && c.last_pdl) {   // phase-3 launches overlap: timed as one span
+  if (timing && c.last_persist) {
+    auto at = [&](cudaEvent_t e) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e_begin, e);
+      return (double)t;
+    };
+    s.phase3_ms = at(ev.ev[2]) - at(ev.ev[0]);   // the persistent launch (all phases)
+    s.phase1_ms = at(ev.ev[0]) - at(e_init);
+    s.post_ms = at(e_post) - at(ev.ev[2]);
+  } else if (timing && !c.last_pairs && c.last_pdl) {   // phase-3 launches overlap: timed as one span
     auto at = [&](cudaEvent_t e) {
       float t = 0.f;
       cudaEventElapsedTime(&t, e_begin, e);
@@ -2016,7 +2091,7 @@ void ctx_release(Ctx *c) {
   if (c->comm) g_nccl.CommDestroy(c->comm);
   c->comm = nullptr;
   for (DevBuf *b : {&c->ws_d, &c->ws_t, &c->ws_b, &c->ws_s, &c->ws_full, &c->ws_tr, &c->user_d,
-                    &c->user_t, &c->scratch})
+                    &c->user_t, &c->scratch, &c->ws_ver})
     b->release();
   if (c->pinned) cudaFreeHost(c->pinned);
   c->pinned = nullptr;
@@ -2265,6 +2340,8 @@ int fw_init(int ngpus_max, unsigned flags) {
   c->pair_order = !(po && po[0] == '0');
   const char *pp = getenv("FW_PIPE_PAIR_ROWS");
   if (pp && atoi(pp) >= 1) c->pipe_pair_rows = atoi(pp);
+  const char *ps = getenv("FW_PERSISTENT");   // one persistent launch per solve: -1 auto, 0 off, 1 on
+  if (ps && atoi(ps) >= -1 && atoi(ps) <= 1) c->persistent = atoi(ps);
   const char *pf = getenv("FW_PIPE_FIRST");   // tuning: first chunk of the auto host pipeline
   if (pf && atoi(pf) >= 1 && atoi(pf) <= 64) c->pipe_first = atoi(pf);
   g_ctx = c;
@@ -2283,6 +2360,8 @@ int fw_set_option(const char *name, int value) {
   else if (k == "pair_order") c.pair_order = value != 0;
   else if (k == "pipe_pair_rows" && value >= 1) c.pipe_pair_rows = value;
   else if (k == "pipe_first" && value >= 1 && value <= 64) c.pipe_first = value;
+  else if (k == "persistent" && value >= -1 && value <= 1) c.persistent = value;
+  else if (k == "persist_gap" && value >= -1) c.persist_gap = value;
   else return fail(FW_EINVAL, "unknown option or value: %s = %d", name, value);
   return FW_OK;
 }

@@ -254,39 +254,21 @@ __device__ __forceinline__ int ctaid(int dim) {
   return v;
 }
 
-template <typename T, int TM, int TN, int MODE, bool DUAL = false>
-__global__ void __launch_bounds__(kThreads, TileShape<TM, TN>::kMinBlocks)
-minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g, int *maxkey) {
+// ---- the tile product, shared by the stream-ordered tile kernel and the persistent kernel ----
+// Main loop of one TM x TN tile: acc[r][c] = min over k < nch*kBK of A(i, k) + B(k, j) for the
+// thread's rows i = ty + TY*r and columns j = 4*tx + 4*TX*h + e, A(i, k) = A[(arow + i)*lda + acol + k]
+// (the tile's rows of the pivot column block), B(k, j) = B[(brow + k)*ldb + bcol + j] (the pivot
+// row block's columns of the tile). The k dimension is streamed in chunks of kBK through kStages shared-memory stages
+// (cp.async 16 B, .cg: through L2, never a stale L1 line): A row-major [i][k] (padded stride:
+// conflict-free LDS.128), B row-major [k][j]; one barrier per chunk.
+template <typename T, int TM, int TN>
+__device__ __forceinline__ void tile_mainloop(T *smem, const T *__restrict__ A, int64_t lda, int arow, int acol,
+                                              const T *__restrict__ B, int64_t ldb, int brow, int bcol, int nch,
+                                              T (&acc)[TileShape<TM, TN>::RM][4 * TileShape<TM, TN>::H]) {
   using S = TileShape<TM, TN>;
   using V = typename Vec4<T>::V;
   constexpr int RM = S::RM, H = S::H, TX = S::TX, TY = S::TY;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *smem = reinterpret_cast<T *>(smem_raw);
-
-  // tile origin and exclusions (computed again after the main loop: see the epilogue)
-  // colstrip 2 / colstep (pairs of plain rounds) never occur with round tags: compiled out there
-  constexpr bool PAIRS = MODE != MODE_TAG;
-  const int cstrip = g.colstrip;
-  // a launch that follows this one with programmatic serialization (the next pair's bulk
-  // launch, DESIGN.md §4.9) may start its CTAs once every CTA of this one has started; it
-  // waits for this grid's completion only before its own epilogue (griddepcontrol.wait below)
-  asm volatile("griddepcontrol.launch_dependents;");
-  const TileSlot ts = tile_slot<TM, TN, DUAL, PAIRS>(g, blockIdx.x, blockIdx.y, blockIdx.z);
-  if (ts.skip) return;
-  const int i0 = ts.i0, j0 = ts.j0;
-
-  const int64_t ld = g.ld;
-  const int kb = PAIRS ? (cstrip ? (cstrip == 2 ? (j0 ^ 128) : j0) : g.kb) : (g.colstrip ? j0 : g.kb);
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
-  // Warm L2 with this tile of D for the epilogue's compare (128-B lines, per-thread
-  // addresses): the tile is read once per round from HBM, and its latency was the
-  // epilogue's top stall.
-  {
-    constexpr int LPR = TN * (int)sizeof(T) / 128;   // lines per tile row
-    for (int l = tid; l < TM * LPR; l += kThreads)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)(i0 + l / LPR) * ld + j0 + (l % LPR) * (128 / (int)sizeof(T))));
-  }
-
   // cp.async assignments: A chunk TM x kBK, B chunk kBK x TN, 16 B per copy.
   constexpr int A_PER = TM * (kBK / 4) / kThreads;
   constexpr int A_ROWS = kThreads / (kBK / 4);
@@ -295,23 +277,21 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   static_assert(A_PER >= 1 && B_PER >= 1, "copy mapping");
   const int a_r = tid / (kBK / 4), a_c = (tid % (kBK / 4)) * 4;
   const int b_r = tid / (TN / 4), b_c = (tid % (TN / 4)) * 4;
-  const T *a_src = D + (int64_t)(i0 + a_r) * ld + kb + a_c;
-  const int64_t ldb = g.ldb;
-  const T *b_src = static_cast<const T *>(g.B) + (int64_t)((cstrip ? kb : 0) + b_r) * ldb + j0 + b_c;
+  const T *a_src = A + (int64_t)(arow + a_r) * lda + acol + a_c;
+  const T *b_src = B + (int64_t)(brow + b_r) * ldb + bcol + b_c;
 
   auto load_chunk = [&](int stage, int k0) {
     T *as = smem + stage * S::kStage;
     T *bs = as + S::kA;
 #pragma unroll
     for (int t = 0; t < A_PER; ++t)
-      cp_async16(as + (a_r + t * A_ROWS) * S::AS + a_c, a_src + k0 + (int64_t)t * A_ROWS * ld);
+      cp_async16(as + (a_r + t * A_ROWS) * S::AS + a_c, a_src + k0 + (int64_t)t * A_ROWS * lda);
 #pragma unroll
     for (int t = 0; t < B_PER; ++t)
       cp_async16(bs + (b_r + t * B_ROWS) * S::BSTR + b_c, b_src + (int64_t)(k0 + t * B_ROWS) * ldb);
     cp_async_commit();
   };
 
-  T acc[RM][4 * H];
 #pragma unroll
   for (int r = 0; r < RM; ++r)
 #pragma unroll
@@ -319,7 +299,6 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
 
   // kStages-deep pipeline with one barrier per chunk: after the barrier of chunk ch every warp
   // is past chunk ch-1, so chunk ch + kStages - 1 is issued into that stage.
-  const int nch = g.Kd / kBK;
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s)
     if (s < nch) load_chunk(s, s * kBK);
@@ -356,25 +335,34 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
       }
     }
   }
+}
 
-  // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
-  // (launched with programmatic serialization: the previous launch in the stream, which wrote
-  // this tile, must be complete before the tile is read and written; a no-op otherwise)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const TileSlot te = tile_slot<TM, TN, DUAL, PAIRS>(g, ctaid(0), ctaid(1), ctaid(2));
-  const int mr_lo = te.mr_lo, mr_hi = te.mr_hi, mc_lo = te.mc_lo, mc_hi = te.mc_hi;
-  const int kgrp = (g.colstrip ? te.j0 : g.kb) & ~kKeyMask;
-  const int tag = PAIRS ? (cstrip ? (cstrip == 2 ? (te.j0 ^ 128) : te.j0) >> 7 : g.tag) : (g.colstrip ? te.j0 >> 7 : g.tag);
+// Epilogue of one tile: strict improvements only ("one comparison"); 16-B stores of the
+// changed vectors, P written for changed elements (KEY: the arg-min k = kgrp + the key's k code;
+// TAG: `tag`). Rows in [mr_lo, mr_hi) and columns in [mc_lo, mc_hi) are left alone. CG: read
+// the old tile through L2 (.cg) — the persistent kernel's tiles are written by other SMs, whose
+// lines this SM's L1 may hold stale. Returns the largest stored key (KEY), else 0.
+template <typename T, int TM, int TN, int MODE, bool CG = false>
+__device__ __forceinline__ int tile_epilogue(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int i0,
+                                             int j0, int mr_lo, int mr_hi, int mc_lo, int mc_hi, int tag,
+                                             int kgrp,
+                                             const T (&acc)[TileShape<TM, TN>::RM][4 * TileShape<TM, TN>::H]) {
+  using S = TileShape<TM, TN>;
+  using V = typename Vec4<T>::V;
+  constexpr int RM = S::RM, H = S::H, TX = S::TX, TY = S::TY;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   int kmax = 0;
 #pragma unroll
   for (int r = 0; r < RM; ++r) {
-    const int i = te.i0 + ty + TY * r;
+    const int i = i0 + ty + TY * r;
     const bool row_ok = !(i >= mr_lo && i < mr_hi);
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      const int jb = te.j0 + 4 * tx + 4 * TX * h;
-      V *dp = reinterpret_cast<V *>(D + (int64_t)i * g.ld + jb);
-      const V old = *dp;
+      const int jb = j0 + 4 * tx + 4 * TX * h;
+      V *dp = reinterpret_cast<V *>(D + (int64_t)i * ld + jb);
+      V old;
+      if constexpr (CG) old = __ldcg(dp);
+      else old = *dp;
       V nv = old;
       bool any = false;
       int32_t pv[4];
@@ -403,11 +391,69 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
         if (MODE != MODE_PLAIN) {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if (chg[e]) P[(int64_t)i * g.ld + jb + e] = pv[e];
+            if (chg[e]) P[(int64_t)i * ld + jb + e] = pv[e];
         }
       }
     }
   }
+  return kmax;
+}
+
+// ---------------------------------------------------------------------------------
+// Min-plus tile kernel (phases 2 and 3). Tile origin (i0, j0) = (row0 + by*TM, col0 + bx*TN);
+// blockIdx.z selects one of two strip descriptions (phase 2 launches both strips at once).
+//   D[i][j] <- min(D[i][j], min_{k<Kd} D[i][kb+k] + B[k][j])
+// with i a LOCAL row of this GPU's block-row partition (all rows on one GPU) and B the pivot
+// row strip (rows kb..kb+Kd of the global matrix: in D on its owner, the broadcast buffer
+// elsewhere), for the tile's (i,j), excluding rows in [mr_lo, mr_hi) and columns in [mc_lo, mc_hi)
+// (strips owned by other phases). In-place use (phase 2: the tile is its own A or B)
+// is safe: a CTA reads all its A/B chunks before its epilogue writes, and no other CTA writes
+// what it reads.
+template <typename T, int TM, int TN, int MODE, bool DUAL = false>
+__global__ void __launch_bounds__(kThreads, TileShape<TM, TN>::kMinBlocks)
+minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g, int *maxkey) {
+  using S = TileShape<TM, TN>;
+  constexpr int RM = S::RM, H = S::H;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *smem = reinterpret_cast<T *>(smem_raw);
+
+  // tile origin and exclusions (computed again after the main loop: see the epilogue)
+  // colstrip 2 / colstep (pairs of plain rounds) never occur with round tags: compiled out there
+  constexpr bool PAIRS = MODE != MODE_TAG;
+  const int cstrip = g.colstrip;
+  // a launch that follows this one with programmatic serialization (the next pair's bulk
+  // launch, DESIGN.md §4.9) may start its CTAs once every CTA of this one has started; it
+  // waits for this grid's completion only before its own epilogue (griddepcontrol.wait below)
+  asm volatile("griddepcontrol.launch_dependents;");
+  const TileSlot ts = tile_slot<TM, TN, DUAL, PAIRS>(g, blockIdx.x, blockIdx.y, blockIdx.z);
+  if (ts.skip) return;
+  const int i0 = ts.i0, j0 = ts.j0;
+
+  const int64_t ld = g.ld;
+  const int kb = PAIRS ? (cstrip ? (cstrip == 2 ? (j0 ^ 128) : j0) : g.kb) : (g.colstrip ? j0 : g.kb);
+  const int tid = threadIdx.x;
+  // Warm L2 with this tile of D for the epilogue's compare (128-B lines, per-thread
+  // addresses): the tile is read once per round from HBM, and its latency was the
+  // epilogue's top stall.
+  {
+    constexpr int LPR = TN * (int)sizeof(T) / 128;   // lines per tile row
+    for (int l = tid; l < TM * LPR; l += kThreads)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)(i0 + l / LPR) * ld + j0 + (l % LPR) * (128 / (int)sizeof(T))));
+  }
+
+  T acc[RM][4 * H];
+  tile_mainloop<T, TM, TN>(smem, D, ld, i0, kb, static_cast<const T *>(g.B), g.ldb, cstrip ? kb : 0, j0,
+                           g.Kd / kBK, acc);
+
+  // ---- epilogue ----------------------------------------------------------------------------
+  // (launched with programmatic serialization: the previous launch in the stream, which wrote
+  // this tile, must be complete before the tile is read and written; a no-op otherwise)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const TileSlot te = tile_slot<TM, TN, DUAL, PAIRS>(g, ctaid(0), ctaid(1), ctaid(2));
+  const int kgrp = (g.colstrip ? te.j0 : g.kb) & ~kKeyMask;
+  const int tag = PAIRS ? (cstrip ? (cstrip == 2 ? (te.j0 ^ 128) : te.j0) >> 7 : g.tag) : (g.colstrip ? te.j0 >> 7 : g.tag);
+  int kmax = tile_epilogue<T, TM, TN, MODE>(D, P, g.ld, te.i0, te.j0, te.mr_lo, te.mr_hi, te.mc_lo, te.mc_hi,
+                                            tag, kgrp, acc);
   if (is_key(MODE)) {
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if ((tid & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
@@ -488,15 +534,44 @@ __device__ __forceinline__ void lds_vec(T (&out)[R], const T *src) {
   }
 }
 
-template <typename T, int BS, int MODE, int NT = kP1Side>
-__global__ void __launch_bounds__(NT * NT)
-phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag,
-              int *maxkey) {
+// R consecutive values of global memory into registers (vector loads); CG: through L2 (.cg),
+// for tiles other SMs wrote (the persistent kernel: this SM's L1 may hold stale lines).
+template <typename T, int R, bool CG>
+__device__ __forceinline__ void ldg_vec(T (&out)[R], const T *src) {
+  if constexpr (!CG) {
+    lds_vec<T, R>(out, src);
+  } else if constexpr (R % 4 == 0) {
+    using V = typename Vec4<T>::V;
+#pragma unroll
+    for (int q = 0; q < R / 4; ++q) {
+      const V v = __ldcg(reinterpret_cast<const V *>(src) + q);
+      out[4 * q] = v.x; out[4 * q + 1] = v.y; out[4 * q + 2] = v.z; out[4 * q + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < R; ++q) out[q] = __ldcg(src + q);
+  }
+}
+template <bool CG, typename T> __device__ __forceinline__ T ldg1(const T *p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
+
+// Shared memory of the phase-1 bodies (rows / columns k, k+1 double-buffered): 4 KB at BS = 128.
+template <typename T, int BS> struct P1Smem {
+  using T2 = typename std::conditional<Num<T>::kIsInt, int2, float2>::type;
+  __align__(16) T rowb[2][2][BS];
+  __align__(16) T2 colb[2][BS];
+};
+
+template <typename T, int BS, int MODE, int NT = kP1Side, bool CG = false>
+__device__ __forceinline__ void phase1_body(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0,
+                                            int kb, int tag, int *maxkey, P1Smem<T, BS> &sm) {
   constexpr int R = BS / NT;
   static_assert(R % 2 == 0, "step parity = register slot parity needs an even R");
   // row k and column k of the current step, double-buffered by step parity (2 KB at BS = 128)
-  __shared__ __align__(16) T rowb[2][BS];
-  __shared__ __align__(16) T colb[2][BS];
+  T (*rowb)[BS] = sm.rowb[0];
+  T (*colb)[BS] = sm.rowb[1];
   const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
   T *Dk = D + (int64_t)r0 * ld + kb;                // D_KK: local row r0, global column kb
   int32_t *Pk = P ? P + (int64_t)r0 * ld + kb : nullptr;
@@ -504,7 +579,7 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
   int32_t p[R][R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    lds_vec<T, R>(d[r], Dk + (int64_t)(R * ty + r) * ld + R * tx);   // 16-B global loads
+    ldg_vec<T, R, CG>(d[r], Dk + (int64_t)(R * ty + r) * ld + R * tx);   // 16-B global loads
 #pragma unroll
     for (int c = 0; c < R; ++c) p[r][c] = -1;
   }
@@ -562,7 +637,7 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
     for (int c = 0; c < R; ++c) {
       const int a = R * ty + r, b = R * tx + c;
       const int64_t off = (int64_t)a * ld + b;
-      if (d[r][c] < Dk[off]) {
+      if (d[r][c] < ldg1<CG>(Dk + off)) {
         Dk[off] = d[r][c];
         if (MODE == MODE_TAG) Pk[off] = tag;
         if (is_key(MODE)) {
@@ -577,23 +652,31 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
   }
 }
 
+template <typename T, int BS, int MODE, int NT = kP1Side>
+__global__ void __launch_bounds__(NT * NT)
+phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag,
+              int *maxkey) {
+  __shared__ P1Smem<T, BS> sm;
+  phase1_body<T, BS, MODE, NT>(D, P, ld, r0, kb, tag, maxkey, sm);
+}
+
 // Phase 1 for PLAIN / TAG (no per-step P), two steps per barrier: row / column k+1 are brought
 // to their state after step k by every thread (col'[a] = min(col_k1[a], col_k[a] + D[k][k+1]),
 // row'[b] = min(row_k1[b], D[k+1][k] + row_k[b])), then x = min(x, c_k, c'_k+1) — exactly the
 // sequential loop's values (min is exact; each candidate is the same single rounded sum).
-template <typename T, int BS, int MODE, int NT = kP1Side>
-__global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
-phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {
+template <typename T, int BS, int MODE, int NT = kP1Side, bool CG = false>
+__device__ __forceinline__ void phase1_pair_body(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0,
+                                                 int kb, int tag, P1Smem<T, BS> &sm) {
   constexpr int R = BS / NT;
   static_assert(R % 2 == 0 && !is_key(MODE), "pairs of steps; keyed modes use their own kernels");
   using T2 = typename std::conditional<Num<T>::kIsInt, int2, float2>::type;
-  __shared__ __align__(16) T rowb[2][2][BS];   // rows k, k+1 (pair parity)
-  __shared__ __align__(16) T2 colb[2][BS];     // (column k, column k+1) per row
+  T (*rowb)[2][BS] = sm.rowb;   // rows k, k+1 (pair parity)
+  T2 (*colb)[BS] = sm.colb;     // (column k, column k+1) per row
   const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
   T *Dk = D + (int64_t)r0 * ld + kb;
   T d[R][R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) lds_vec<T, R>(d[r], Dk + (int64_t)(R * ty + r) * ld + R * tx);
+  for (int r = 0; r < R; ++r) ldg_vec<T, R, CG>(d[r], Dk + (int64_t)(R * ty + r) * ld + R * tx);
   if (ty == 0) {
 #pragma unroll
     for (int c = 0; c < R; ++c) {
@@ -649,11 +732,18 @@ phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r
     for (int c = 0; c < R; ++c) {
       const int a = R * ty + r, b = R * tx + c;
       const int64_t off = (int64_t)a * ld + b;
-      if (d[r][c] < Dk[off]) {
+      if (d[r][c] < ldg1<CG>(Dk + off)) {
         Dk[off] = d[r][c];
         if (MODE == MODE_TAG) P[(int64_t)(r0 + a) * ld + kb + b] = tag;
       }
     }
+}
+
+template <typename T, int BS, int MODE, int NT = kP1Side>
+__global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
+phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {
+  __shared__ P1Smem<T, BS> sm;
+  phase1_pair_body<T, BS, MODE, NT>(D, P, ld, r0, kb, tag, sm);
 }
 
 // Phase 1, FP32 keyed mode, without a per-relaxation select for P. The running value of
@@ -664,14 +754,13 @@ phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r
 // bits — the sequential strict-< result of the paper's loop, with one FADD + one FMNMX per
 // relaxation. Row k+1 is published as D*256 (B side), column k+1 as D*256 + k' (A side), both
 // recovered as floor((x + 0.5) / 256) * 256. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
-template <int BS, int NT = kP1Side>
-__global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
-phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
-                      int *maxkey) {
+template <int BS, int NT = kP1Side, bool CG = false>
+__device__ __forceinline__ void phase1_key_f32_body(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld,
+                                                    int r0, int kb, int *maxkey, P1Smem<float, BS> &sm) {
   constexpr int R = BS / NT;
   static_assert(R % 2 == 0, "step parity = register slot parity needs an even R");
-  __shared__ __align__(16) float rowb[2][2][BS];   // rows k, k+1, B form D*256  (pair parity)
-  __shared__ __align__(16) float2 colb[2][BS];     // (column k, column k+1) per row, A form D*256 + k'
+  float (*rowb)[2][BS] = sm.rowb;   // rows k, k+1, B form D*256  (pair parity)
+  float2 (*colb)[BS] = sm.colb;     // (column k, column k+1) per row, A form D*256 + k'
   const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
   float *Dk = D + (int64_t)r0 * ld + kb;
   const int kgrp = kb & ~kKeyMask, klow = kb & kKeyMask;
@@ -679,7 +768,7 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     float key[R];
-    lds_vec<float, R>(key, Dk + (int64_t)(R * ty + r) * ld + R * tx);  // D*256 + ((kb+b)&255) or +inf
+    ldg_vec<float, R, CG>(key, Dk + (int64_t)(R * ty + r) * ld + R * tx);  // D*256 + ((kb+b)&255) or +inf
 #pragma unroll
     for (int c = 0; c < R; ++c) x[r][c] = key[c] - (float)(klow + R * tx + c) - 0.5f;   // D*256 - 0.5
   }
@@ -761,6 +850,14 @@ phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld
     }
   kmax = __reduce_max_sync(0xffffffffu, kmax);
   if ((threadIdx.x & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
+}
+
+template <int BS, int NT = kP1Side>
+__global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
+phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
+                      int *maxkey) {
+  __shared__ P1Smem<float, BS> sm;
+  phase1_key_f32_body<BS, NT>(D, P, ld, r0, kb, maxkey, sm);
 }
 
 // ---------------------------------------------------------------------------------

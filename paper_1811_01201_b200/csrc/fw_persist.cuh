@@ -1,0 +1,200 @@
+// fw_persist.cuh — the whole blocked Floyd–Warshall solve as ONE persistent launch (one GPU,
+// BS = 128): SURVEY §8 row f1, the "persistent K3 polling per-block-row readiness" half.
+//
+// Method: arxiv 1811.01201 §4.1. Round K relaxes every tile (I, J) of
+// 128 x 128 through block K: phase 1 on (K, K), phase 2 on row K and column K
+// and phase 3 on the rest. The paper overlaps phases 2 and 3 of a round with OpenMP
+// `nowait`; the stream-ordered driver (fw_api.cu) overlaps round K+1's pivot phases with
+// round K's phase 3 through a second stream and a kernel boundary per round. Here there is no
+// boundary at all: a grid of resident CTAs takes work items from one global counter, in a fixed
+// order, and each item waits only for the tiles it reads, through per-tile round counters:
+//
+//   ver[I][J] = number of rounds tile (I, J) has completed (stored with release semantics after
+//               the tile's stores; read with acquire before the tile is used as an operand).
+//
+// Items and what each waits for (a tile item of round K computes
+//   D[I][J] <- min(D[I][J], D[I][K] (x) D[K][J])   (min-plus product through block K):
+// the same product serves phase 2 (I == K: A is the closed diagonal block, B the tile itself;
+// J == K: A the tile itself, B the diagonal block; reading R7) and phase 3):
+//   P1(K)            ver[K][K] >= K                                 (phase 1, one CTA)
+//   tile(K, I, J)    ver[I][J] >= K, ver[I][K] >= K+1 unless J == K, ver[K][J] >= K+1 unless I == K
+// Item order (deadlock-free: every item waits only for items EARLIER in the order, which were
+// taken by CTAs that are running — no co-residency assumption is needed):
+//   P1(0), P2(0) tiles, then per round K a segment of T^2 items:
+//     prio(K)  = phase-3 tiles of round K that round K+1's pivot phases read: tile (K+1, K+1)
+//                first, then row K+1 (J != K), then column K+1 (I != K, K+1)      2T-3
+//     P1(K+1)                                                                      1
+//     rest(K)  = the other phase-3 tiles of round K, first part                   gap
+//     P2(K+1)  = row K+1 (J != K+1) and column K+1 (I != K+1) of round K+1         2T-2
+//     rest(K), second part                                                         (T-2)^2 - gap
+//   (the last segment: the (T-1)^2 phase-3 tiles of round T-1, then no-ops).
+// So round K+1's pivot path (P1, then P2) runs while round K's phase 3 drains — the cross-round
+// look-ahead without a second stream — and round K+1's phase-3 tiles start tile by tile as soon
+// as their operands are ready, not when the whole of round K has ended.
+//
+// Correctness with overlapping rounds (reading R16 of DESIGN.md): a tile may be read as an
+// operand while its owner item rewrites it for a LATER round. Every stored value is the length of
+// a real path and values only decrease (each 4-byte element is read either before or after its
+// store), so a more-relaxed operand can only lower the result towards the true distance, never
+// below it; keys and round tags stay valid by the triangle argument on the final D (R9). D is
+// therefore bitwise the standard schedule's for integer data.
+//
+// Every operand read goes through L2 (cp.async.cg, ld.global.cg): tiles are written by other SMs
+// and this SM's L1 may hold stale lines of them.
+#pragma once
+#include "fw_kernels.cuh"
+
+namespace fwb {
+
+struct PersistArgs {
+  void *D;
+  int32_t *P;
+  int64_t ld;
+  int T;                   // tiles per dimension = rounds (BS = 128)
+  int gap;                 // rest(K) tiles between P1(K+1) and P2(K+1)
+  int *ver;                // T x T per-tile round counters (zeroed)
+  unsigned long long *next;   // work counter (zeroed)
+  int *maxkey;             // KEY: largest stored key (speculative key runs)
+  int *flags;              // bit 5: a dependency wait timed out (the host fails the solve)
+  long long total;         // number of items
+  unsigned long long timeout_ns;
+};
+
+enum ItemType { IT_NONE = 0, IT_P1 = 1, IT_TILE = 2 };
+struct Item {
+  int type, K, I, J;
+};
+
+// Item `it` of the fixed order above.
+__device__ __forceinline__ Item persist_decode(const PersistArgs &a, long long it) {
+  const int T = a.T;
+  Item w{IT_NONE, 0, 0, 0};
+  if (it == 0) return Item{IT_P1, 0, 0, 0};
+  const long long pre = 2LL * T - 1;              // P1(0) + the 2(T-1) phase-2 tiles of round 0
+  if (it < pre) {                                 // P2(0): row 0 (J = 1..T-1), column 0 (I = 1..T-1)
+    const int q = (int)(it - 1);
+    return q < T - 1 ? Item{IT_TILE, 0, 0, q + 1} : Item{IT_TILE, 0, q - (T - 1) + 1, 0};
+  }
+  const long long t2 = (long long)T * T;
+  const int K = (int)((it - pre) / t2);
+  int q = (int)((it - pre) % t2);
+  if (K >= T) return w;
+  if (K == T - 1) {                               // last round: its phase-3 tiles, then no-ops
+    const int m = T - 1;
+    if (q >= m * m) return w;
+    return Item{IT_TILE, K, skip2(q / m, K, -1), skip2(q % m, K, -1)};
+  }
+  const int N = K + 1;
+  if (q < T - 1) {                                // prio: row K+1, (K+1, K+1) first
+    return Item{IT_TILE, K, N, q == 0 ? N : skip2(q - 1, K, N)};
+  }
+  q -= T - 1;
+  if (q < T - 2) return Item{IT_TILE, K, skip2(q, K, N), N};   // prio: column K+1
+  q -= T - 2;
+  if (q == 0) return Item{IT_P1, N, N, N};
+  q -= 1;
+  const int m = T - 2, rest = m * m;
+  const int gap = a.gap < rest ? a.gap : rest;
+  if (q < gap) return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N)};
+  q -= gap;
+  if (q < 2 * (T - 1)) {                          // P2(K+1): row K+1, then column K+1
+    return q < T - 1 ? Item{IT_TILE, N, N, skip2(q, N, -1)} : Item{IT_TILE, N, skip2(q - (T - 1), N, -1), N};
+  }
+  q -= 2 * (T - 1);
+  q += gap;
+  return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N)};
+}
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin (one thread) until *p >= v; bounded: after timeout_ns set bit 5 of *flags and give up.
+__device__ __forceinline__ void wait_ge(const PersistArgs &a, const int *p, int v, unsigned long long t0) {
+  while (ld_acquire(p) < v) {
+    if (globaltimer() - t0 > a.timeout_ns) {
+      atomicOr(a.flags, 32);
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+
+template <typename T, int MODE>
+__device__ __forceinline__ void persist_phase1(const PersistArgs &a, int K, unsigned char *smem) {
+  T *D = static_cast<T *>(a.D);
+  const int kb = K * 128;
+  if constexpr (std::is_same<T, float>::value && is_key(MODE)) {
+    phase1_key_f32_body<128, kP1Side, true>(D, a.P, a.ld, kb, kb, a.maxkey,
+                                             *reinterpret_cast<P1Smem<float, 128> *>(smem));
+  } else if constexpr (!is_key(MODE)) {
+    phase1_pair_body<T, 128, MODE, kP1Side, true>(D, a.P, a.ld, kb, kb, K,
+                                                  *reinterpret_cast<P1Smem<T, 128> *>(smem));
+  } else {
+    phase1_body<T, 128, MODE, kP1Side, true>(D, a.P, a.ld, kb, kb, K, a.maxkey,
+                                             *reinterpret_cast<P1Smem<T, 128> *>(smem));
+  }
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kThreads, 2)
+fw_persistent_kernel(const PersistArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ long long s_item;
+  using S = TileShape<128, 128>;
+  const int tid = threadIdx.x;
+  T *D = static_cast<T *>(a.D);
+  for (;;) {
+    if (tid == 0) s_item = (long long)atomicAdd(a.next, 1ull);
+    __syncthreads();
+    const long long it = s_item;
+    if (it >= a.total) break;
+    const Item w = persist_decode(a, it);
+    if (w.type != IT_NONE) {
+      if (tid == 0) {   // the operands this item reads, and its own tile, at the required round
+        const unsigned long long t0 = globaltimer();
+        const int *v = a.ver;
+        const int T_ = a.T;
+        if (w.type == IT_P1) {
+          wait_ge(a, v + (int64_t)w.K * T_ + w.K, w.K, t0);
+        } else {
+          wait_ge(a, v + (int64_t)w.I * T_ + w.J, w.K, t0);
+          if (w.J != w.K) wait_ge(a, v + (int64_t)w.I * T_ + w.K, w.K + 1, t0);
+          if (w.I != w.K) wait_ge(a, v + (int64_t)w.K * T_ + w.J, w.K + 1, t0);
+        }
+      }
+      __syncthreads();
+      if (w.type == IT_P1) {
+        persist_phase1<T, MODE>(a, w.K, smem_raw);
+      } else {
+        T acc[S::RM][4 * S::H];
+        tile_mainloop<T, 128, 128>(reinterpret_cast<T *>(smem_raw), D, a.ld, w.I * 128, w.K * 128, D, a.ld,
+                                   w.K * 128, w.J * 128, 128 / kBK, acc);
+        // the item again from shared memory: nothing but the accumulators lives across the loop
+        const Item e = persist_decode(a, s_item);
+        int kmax = tile_epilogue<T, 128, 128, MODE, true>(D, a.P, a.ld, e.I * 128, e.J * 128, 0, 0, 0, 0, e.K,
+                                                          (e.K * 128) & ~kKeyMask, acc);
+        if (is_key(MODE)) {
+          kmax = __reduce_max_sync(0xffffffffu, kmax);
+          if ((tid & 31) == 0 && kmax > 0) atomicMax(a.maxkey, kmax);
+        }
+      }
+      __syncthreads();   // every thread's stores of the tile precede the release below
+      if (tid == 0) {
+        const Item e = persist_decode(a, s_item);
+        __threadfence();
+        int *vp = a.ver + (int64_t)e.I * a.T + e.J;
+        asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(vp), "r"(e.K + 1) : "memory");
+      }
+    }
+    __syncthreads();   // s_item is rewritten by the next iteration
+  }
+}
+
+}  // namespace fwb

@@ -596,3 +596,81 @@ def test_set_option_schedules_identical_D(opt):
     with Ctx(0):
         with pytest.raises(fw.FwError):
             fw.fw_set_option("no_such_option", 1)
+
+
+# ---- one persistent launch per solve (fw_persist.cuh) ----------
+PERSIST_CASES = [
+    ("complete_int", 129, "next"), ("complete_int", 640, "next"), ("complete_int", 1000, "lastk"),
+    ("complete_real", 300, "next"), ("complete_real", 777, "next"), ("complete_real", 1024, "lastk"),
+    ("er_int", 700, "next"), ("er_int", 513, "lastk"), ("er_int_f32", 900, "next"),
+    ("complete_int", 600, None), ("complete_real", 500, None),
+]
+
+
+@pytest.mark.parametrize("kind,n,path", PERSIST_CASES)
+@pytest.mark.parametrize("device", [False, True])
+def test_persistent_against_oracle(kind, n, path, device):
+    """The whole solve as one persistent launch (work items in round order, per-tile round
+    counters) for every P method (FP32 keys, INT32 keys / tags, round tags, distance only):
+    D against the oracle (bitwise for integer data), P valid by reconstruction; for integer
+    data D bitwise equal to the stream-ordered schedule."""
+    W = gen.generate(kind, n, 900 + n, p=0.02, lo=1, hi=1000 if kind.startswith("er") else 100)
+    flags = (fw.FW_PATH_LAST_K if path == "lastk" else 0) | fw.FW_TIMING
+    out = {}
+    for persist in (1, 0):
+        D = W.copy()
+        P = np.empty(W.shape, dtype=np.int32) if path else None
+        with Ctx(flags):
+            fw.fw_set_option("persistent", persist)
+            if device:
+                dD = torch.from_numpy(D).cuda()
+                dP = torch.from_numpy(P).cuda() if P is not None else None
+                f = fw.fw_solve_device_i32 if W.dtype == np.int32 else fw.fw_solve_device_f32
+                f(dD, dP, block=128, stream=torch.cuda.current_stream())
+                D = dD.cpu().numpy()
+                P = dP.cpu().numpy() if dP is not None else None
+            else:
+                fw.fw_set_host_pipeline(0)
+                (fw.fw_solve_i32 if W.dtype == np.int32 else fw.fw_solve)(D, P, block=128)
+            s = fw.fw_last_stats()
+        assert s.persistent == persist
+        out[persist] = (D, P)
+    D, P = out[1]
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    if path:
+        bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5, mode=path)
+        assert bad == 0, f"{bad} invalid paths, first at {divmod(first, n)}"
+    if exact:
+        np.testing.assert_array_equal(D, out[0][0])
+
+
+@pytest.mark.parametrize("gap", [0, 1, 7, 100000])
+def test_persistent_gap_extremes(gap):
+    """Any position of the next round's phase-2 items in the work order is correct (the order only
+    decides how long items wait): P2(K+1) right after P1(K+1), or after all of round K."""
+    W = gen.generate("complete_real", 896, 5)
+    D = W.copy()
+    P = np.empty(W.shape, dtype=np.int32)
+    with Ctx(0):
+        fw.fw_set_option("persistent", 1)
+        fw.fw_set_option("persist_gap", gap)
+        fw.fw_set_host_pipeline(0)
+        fw.fw_solve(D, P, block=128)
+    assert_D_matches(D, oracle.fw(W, None)[0], False)
+    assert oracle.check_paths(W, D, P, rtol=1e-5)[0] == 0
+
+
+def test_persistent_ring_closed_form():
+    """Long chains (every path through many rounds): ring of weight 1, n = 1000."""
+    n = 1000
+    W = gen.ring(n, 1)
+    D = W.copy()
+    P = np.empty(W.shape, dtype=np.int32)
+    with Ctx(0):
+        fw.fw_set_option("persistent", 1)
+        fw.fw_set_host_pipeline(0)
+        fw.fw_solve(D, P, block=128)
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    np.testing.assert_array_equal(D.astype(np.int64), (j - i) % n)
+    np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % n))
