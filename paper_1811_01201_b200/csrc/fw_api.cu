@@ -169,6 +169,7 @@ struct Ctx {
   bool last_pairs = false;         // the last solve ran in pairs (stats layout)
   int persistent = -1;             // one persistent launch per solve (fw_persist.cuh): -1 auto, 0 off, 1 on
   int persist_gap = -1;            // persistent: rest tiles between P1(K+1) and P2(K+1) (-1 auto)
+  int persist_relaxed = 0;         // persistent: dependency polls with relaxed loads (A/B option)
   bool last_persist = false;       // the last solve ran as one persistent launch
   DevBuf ws_ver;                   // persistent: per-tile round counters + work counter
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
@@ -883,14 +884,17 @@ struct Part {
 bool use_persistent(const Ctx &c, int mode, int tr, int BS, int64_t n_pad, int64_t row0, int64_t nrows) {
   if (tr != T_LOCAL || BS != 128 || row0 != 0 || nrows != n_pad || c.persistent == 0) return false;
   if (c.persistent == 1) return true;
-  return mode == MODE_TAG && n_pad >= 4 * 128;
+  // auto: round-tag solves up to n = 4096, where the stream-ordered rounds are bound by the
+  // per-round pivot path (C2); above, its tiles run ~8% slower than the stream kernel's
+  //
+  return mode == MODE_TAG && n_pad >= 4 * 128 && n_pad <= 4096;
 }
 
 template <typename T, int MODE>
 int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *maxkey, cudaStream_t st,
                    const Events &e) {
   const int Tn = (int)(n_pad / 128);
-  const size_t vbytes = (size_t)Tn * Tn * sizeof(int);
+  const size_t vbytes = ((size_t)Tn * Tn * sizeof(int) + 255) / 256 * 256;   // the 64-bit counter after it, aligned
   TRY(c.ws_ver.ensure(vbytes + 64));
   int *ver = static_cast<int *>(c.ws_ver.p);
   auto *next = reinterpret_cast<unsigned long long *>(static_cast<char *>(c.ws_ver.p) + vbytes);
@@ -918,6 +922,7 @@ int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *max
   a.flags = maxkey - 2;
   a.total = 2LL * Tn - 1 + (long long)Tn * Tn * Tn;
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  a.sync_relaxed = c.persist_relaxed;
   Nvtx nv("persistent solve");
   if (e.timing) CU(cudaEventRecord(e.ev[0], st));
   kern<<<grid, kThreads, bytes, st>>>(a);
@@ -2362,6 +2367,7 @@ int fw_set_option(const char *name, int value) {
   else if (k == "pipe_first" && value >= 1 && value <= 64) c.pipe_first = value;
   else if (k == "persistent" && value >= -1 && value <= 1) c.persistent = value;
   else if (k == "persist_gap" && value >= -1) c.persist_gap = value;
+  else if (k == "persist_relaxed" && (value == 0 || value == 1)) c.persist_relaxed = value;
   else return fail(FW_EINVAL, "unknown option or value: %s = %d", name, value);
   return FW_OK;
 }

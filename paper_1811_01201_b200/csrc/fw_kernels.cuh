@@ -409,11 +409,16 @@ __device__ __forceinline__ int tile_epilogue(T *__restrict__ D, int32_t *__restr
 // (strips owned by other phases). In-place use (phase 2: the tile is its own A or B)
 // is safe: a CTA reads all its A/B chunks before its epilogue writes, and no other CTA writes
 // what it reads.
+// The main loop and the epilogue are written out here rather than calling tile_mainloop /
+// tile_epilogue (the same arithmetic, used by the persistent kernel): with the calls, ptxas
+// spills 20 B of cp.async addresses at the 128-register cap and reloads them every k-chunk,
+// which cost 6% of the C4 solve (39.8 -> 37.4 TFLOPS, profiles/r02_refactor_regression.json).
 template <typename T, int TM, int TN, int MODE, bool DUAL = false>
 __global__ void __launch_bounds__(kThreads, TileShape<TM, TN>::kMinBlocks)
 minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g, int *maxkey) {
   using S = TileShape<TM, TN>;
-  constexpr int RM = S::RM, H = S::H;
+  using V = typename Vec4<T>::V;
+  constexpr int RM = S::RM, H = S::H, TX = S::TX, TY = S::TY;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *smem = reinterpret_cast<T *>(smem_raw);
 
@@ -431,7 +436,7 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
 
   const int64_t ld = g.ld;
   const int kb = PAIRS ? (cstrip ? (cstrip == 2 ? (j0 ^ 128) : j0) : g.kb) : (g.colstrip ? j0 : g.kb);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   // Warm L2 with this tile of D for the epilogue's compare (128-B lines, per-thread
   // addresses): the tile is read once per round from HBM, and its latency was the
   // epilogue's top stall.
@@ -441,19 +446,127 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
       asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)(i0 + l / LPR) * ld + j0 + (l % LPR) * (128 / (int)sizeof(T))));
   }
 
-  T acc[RM][4 * H];
-  tile_mainloop<T, TM, TN>(smem, D, ld, i0, kb, static_cast<const T *>(g.B), g.ldb, cstrip ? kb : 0, j0,
-                           g.Kd / kBK, acc);
+  // cp.async assignments: A chunk TM x kBK, B chunk kBK x TN, 16 B per copy.
+  constexpr int A_PER = TM * (kBK / 4) / kThreads;
+  constexpr int A_ROWS = kThreads / (kBK / 4);
+  constexpr int B_PER = kBK * (TN / 4) / kThreads;
+  constexpr int B_ROWS = kThreads / (TN / 4);
+  static_assert(A_PER >= 1 && B_PER >= 1, "copy mapping");
+  const int a_r = tid / (kBK / 4), a_c = (tid % (kBK / 4)) * 4;
+  const int b_r = tid / (TN / 4), b_c = (tid % (TN / 4)) * 4;
+  const T *a_src = D + (int64_t)(i0 + a_r) * ld + kb + a_c;
+  const int64_t ldb = g.ldb;
+  const T *b_src = static_cast<const T *>(g.B) + (int64_t)((cstrip ? kb : 0) + b_r) * ldb + j0 + b_c;
 
-  // ---- epilogue ----------------------------------------------------------------------------
+  auto load_chunk = [&](int stage, int k0) {
+    T *as = smem + stage * S::kStage;
+    T *bs = as + S::kA;
+#pragma unroll
+    for (int t = 0; t < A_PER; ++t)
+      cp_async16(as + (a_r + t * A_ROWS) * S::AS + a_c, a_src + k0 + (int64_t)t * A_ROWS * ld);
+#pragma unroll
+    for (int t = 0; t < B_PER; ++t)
+      cp_async16(bs + (b_r + t * B_ROWS) * S::BSTR + b_c, b_src + (int64_t)(k0 + t * B_ROWS) * ldb);
+    cp_async_commit();
+  };
+
+  T acc[RM][4 * H];
+#pragma unroll
+  for (int r = 0; r < RM; ++r)
+#pragma unroll
+    for (int c = 0; c < 4 * H; ++c) acc[r][c] = Num<T>::acc_init();
+
+  // kStages-deep pipeline with one barrier per chunk: after the barrier of chunk ch every warp
+  // is past chunk ch-1, so chunk ch + kStages - 1 is issued into that stage.
+  const int nch = g.Kd / kBK;
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s)
+    if (s < nch) load_chunk(s, s * kBK);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (nch - 1 - ch >= kStages - 2) cp_async_wait<kStages - 2>();   // chunk ch has landed
+    else cp_async_wait<0>();
+    __syncthreads();
+    if (ch + kStages - 1 < nch) load_chunk((ch + kStages - 1) % kStages, (ch + kStages - 1) * kBK);
+    const T *as = smem + (ch % kStages) * S::kStage + ty * S::AS;
+    const T *bs = smem + (ch % kStages) * S::kStage + S::kA + tx * 4;
+#pragma unroll
+    for (int q = 0; q < kBK / 4; ++q) {
+      V b[4][H];   // b[k][h] = B[4q+k][4tx + 4TX*h .. +3]
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+          b[k][h] = *reinterpret_cast<const V *>(bs + (4 * q + k) * S::BSTR + 4 * TX * h);
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const V a = *reinterpret_cast<const V *>(as + TY * r * S::AS + 4 * q);
+        // k-pair outer, column group inner: consecutive FMNMX3 on one accumulator are
+        // H*4 instructions apart (hides the FADD2 -> FMNMX3 -> FMNMX3 latency chain)
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          T *x = &acc[r][4 * h];
+          relax2k(x[0], x[1], x[2], x[3], a.x, a.y, b[0][h], b[1][h]);
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          T *x = &acc[r][4 * h];
+          relax2k(x[0], x[1], x[2], x[3], a.z, a.w, b[2][h], b[3][h]);
+        }
+      }
+    }
+  }
+
+  // ---- epilogue: strict improvements only ("one comparison"); 16-B stores ----------
   // (launched with programmatic serialization: the previous launch in the stream, which wrote
   // this tile, must be complete before the tile is read and written; a no-op otherwise)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const TileSlot te = tile_slot<TM, TN, DUAL, PAIRS>(g, ctaid(0), ctaid(1), ctaid(2));
+  const int mr_lo = te.mr_lo, mr_hi = te.mr_hi, mc_lo = te.mc_lo, mc_hi = te.mc_hi;
   const int kgrp = (g.colstrip ? te.j0 : g.kb) & ~kKeyMask;
   const int tag = PAIRS ? (cstrip ? (cstrip == 2 ? (te.j0 ^ 128) : te.j0) >> 7 : g.tag) : (g.colstrip ? te.j0 >> 7 : g.tag);
-  int kmax = tile_epilogue<T, TM, TN, MODE>(D, P, g.ld, te.i0, te.j0, te.mr_lo, te.mr_hi, te.mc_lo, te.mc_hi,
-                                            tag, kgrp, acc);
+  int kmax = 0;
+#pragma unroll
+  for (int r = 0; r < RM; ++r) {
+    const int i = te.i0 + ty + TY * r;
+    const bool row_ok = !(i >= mr_lo && i < mr_hi);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int jb = te.j0 + 4 * tx + 4 * TX * h;
+      V *dp = reinterpret_cast<V *>(D + (int64_t)i * g.ld + jb);
+      const V old = *dp;
+      V nv = old;
+      bool any = false;
+      int32_t pv[4];
+      bool chg[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = jb + e;
+        const T m = acc[r][4 * h + e];
+        chg[e] = row_ok && !(j >= mc_lo && j < mc_hi) && m < (T)vget(old, e);
+        pv[e] = tag;
+        if (chg[e]) {
+          any = true;
+          if (is_key(MODE)) {
+            const int kk = Num<T>::lowk(m - Num<T>::from_int(j & kKeyMask));   // arg-min k & kKeyMask
+            const T key = m - Num<T>::from_int(kk);
+            vset(nv, e, key);
+            kmax = max(kmax, Num<T>::bits(key));
+            pv[e] = kgrp + kk;
+          } else {
+            vset(nv, e, m);
+          }
+        }
+      }
+      if (any) {
+        *dp = nv;
+        if (MODE != MODE_PLAIN) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (chg[e]) P[(int64_t)i * g.ld + jb + e] = pv[e];
+        }
+      }
+    }
+  }
   if (is_key(MODE)) {
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if ((tid & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
