@@ -171,7 +171,8 @@ struct Ctx {
   int persist_gap = -1;            // persistent: rest tiles between P1(K+1) and P2(K+1) (-1 auto)
   int persist_relaxed = 0;         // persistent: dependency polls with relaxed loads (A/B option)
   bool last_persist = false;       // the last solve ran as one persistent launch
-  DevBuf ws_ver;                   // persistent: per-tile round counters + work counter
+  DevBuf ws_ver;                   // persistent: per-tile round counters, pub flags, work counter, items
+  DevBuf ws_ring;                  // persistent loopback: every rank's pivot-row ring (n_pad^2 each)
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
   bool comm_dead = false;          // the communicator was aborted (error, timeout, failed peer)
   std::atomic<int> *abort_flag = nullptr;   // team solve: set by the first rank that fails
@@ -877,6 +878,8 @@ struct Part {
   T *backup = nullptr;
 };
 
+template <typename R> int *maxkey_of(std::vector<R> &rk) { return rk[0].maxkey; }
+
 // The whole solve as one persistent launch (fw_persist.cuh): one GPU, all rows,
 // BS = 128. Auto: round-tag solves (real-valued data, one round per pass). Keyed and
 // distance-only solves keep the two-rounds-per-pass schedule (§4.9), whose 256-deep bulk
@@ -890,15 +893,85 @@ bool use_persistent(const Ctx &c, int mode, int tr, int BS, int64_t n_pad, int64
   return mode == MODE_TAG && n_pad >= 4 * 128 && n_pad <= 4096;
 }
 
+// Item table of a multi-rank persistent solve (fw_persist.cuh): per round K a segment
+//   A  prio(K): every rank's round-K tiles of row K+1 (its owner; (K+1, K+1) first) and of
+//      column K+1 (rows outside K, K+1)
+//   B  P1(K+1) on the owner of block K+1
+//   C  the first `gap` other phase-3 tiles of round K, per rank
+//   D  P2(K+1): the owner's row K+1 tiles, then every rank's column K+1 tiles
+//   E  the remaining phase-3 tiles of round K
+// (preamble: P1(0), P2(0); the last segment: round T-1's phase-3 tiles). Every item depends only
+// on items earlier in this order (same argument as the one-rank order; cross-rank: a rank's
+// phase-2 column tiles and phase-3 tiles read published pivot tiles from segments B / D or
+// earlier). self >= 0: that rank's items only (a team: one grid per GPU) — each GPU's sequence
+// is then a subsequence of the global order, whose cross-GPU dependencies point only to earlier
+// segments or to the owner's phase B / D items, which depend on nothing later: no cycle.
+void persist_items(int T, int world, const std::vector<int> &t0, const std::vector<int> &t1, int self, int gap,
+                   std::vector<unsigned> *out) {
+  std::vector<unsigned> &v = *out;
+  v.clear();
+  auto owner = [&](int K) {
+    int o = 0;
+    for (int q = 1; q < world; ++q)
+      if (K >= t0[q]) o = q;
+    return o;
+  };
+  auto take = [&](int r) { return self < 0 || r == self; };
+  auto tile = [&](int r, int K, int I, int J) {
+    if (take(r)) v.push_back(pack_item(r, IT_TILE, K, I, J));
+  };
+  const int o0 = owner(0);
+  if (take(o0)) v.push_back(pack_item(o0, IT_P1, 0, 0, 0));
+  for (int J = 1; J < T; ++J) tile(o0, 0, 0, J);
+  for (int r = 0; r < world; ++r)
+    for (int I = t0[r]; I < t1[r]; ++I)
+      if (I != 0) tile(r, 0, I, 0);
+  for (int K = 0; K < T; ++K) {
+    const int N = K + 1;
+    if (N == T) {
+      for (int r = 0; r < world; ++r)
+        for (int I = t0[r]; I < t1[r]; ++I)
+          if (I != K)
+            for (int J = 0; J < T; ++J)
+              if (J != K) tile(r, K, I, J);
+      break;
+    }
+    const int oN = owner(N);
+    tile(oN, K, N, N);                                                  // A
+    for (int J = 0; J < T; ++J)
+      if (J != K && J != N) tile(oN, K, N, J);
+    for (int r = 0; r < world; ++r)
+      for (int I = t0[r]; I < t1[r]; ++I)
+        if (I != K && I != N) tile(r, K, I, N);
+    if (take(oN)) v.push_back(pack_item(oN, IT_P1, N, N, N));          // B
+    std::vector<std::vector<unsigned>> rest(world);
+    for (int r = 0; r < world; ++r)
+      for (int I = t0[r]; I < t1[r]; ++I)
+        if (I != K && I != N)
+          for (int J = 0; J < T; ++J)
+            if (J != K && J != N) rest[r].push_back(pack_item(r, IT_TILE, K, I, J));
+    for (int r = 0; r < world; ++r)                                      // C
+      if (take(r))
+        for (size_t q = 0; q < rest[r].size() && (int)q < gap; ++q) v.push_back(rest[r][q]);
+    for (int J = 0; J < T; ++J)                                          // D
+      if (J != N) tile(oN, N, N, J);
+    for (int r = 0; r < world; ++r)
+      for (int I = t0[r]; I < t1[r]; ++I)
+        if (I != N) tile(r, N, I, N);
+    for (int r = 0; r < world; ++r)                                      // E
+      if (take(r))
+        for (size_t q = gap; q < rest[r].size(); ++q) v.push_back(rest[r][q]);
+  }
+}
+
+// One persistent launch over the ranks of `views` (world = 1: all rows of one GPU, items
+// decoded arithmetically; world > 1: a loopback partition emulated in ONE grid — the guide's way
+// to test ranks that wait on one another on one GPU — with the item table and the rings).
 template <typename T, int MODE>
-int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *maxkey, cudaStream_t st,
-                   const Events &e) {
-  const int Tn = (int)(n_pad / 128);
-  const size_t vbytes = ((size_t)Tn * Tn * sizeof(int) + 255) / 256 * 256;   // the 64-bit counter after it, aligned
-  TRY(c.ws_ver.ensure(vbytes + 64));
-  int *ver = static_cast<int *>(c.ws_ver.p);
-  auto *next = reinterpret_cast<unsigned long long *>(static_cast<char *>(c.ws_ver.p) + vbytes);
-  CU(cudaMemsetAsync(c.ws_ver.p, 0, vbytes + 64, st));
+int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t n_pad, int *maxkey,
+                      cudaStream_t st, const Events &e) {
+  const int Tn = (int)(n_pad / 128), W = (int)views.size();
+  if (W > kMaxRanks) return fail(FW_EINVAL, "persistent solve: at most %d ranks", kMaxRanks);
   auto kern = fw_persistent_kernel<T, MODE>;
   constexpr int bytes = TileShape<128, 128>::kBytes;
   TRY(smem_attr((const void *)kern, bytes));
@@ -908,21 +981,52 @@ int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *max
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, bytes));
   if (per_sm < 1) return fail(FW_ECUDA, "fw_persistent_kernel does not fit on an SM");
   const int grid = per_sm * sms;
+  // counters: per rank its tiles' round counters, and (W > 1) pub flags of its ring; then the
+  // 64-bit work counter, 256-B aligned
+  size_t off = 0;
+  std::vector<size_t> ver_off(W), pub_off(W);
+  for (int r = 0; r < W; ++r) {
+    ver_off[r] = off;
+    off += ((size_t)(views[r].t1 - views[r].t0) * Tn * sizeof(int) + 255) / 256 * 256;
+    pub_off[r] = off;
+    if (W > 1) off += ((size_t)Tn * Tn * sizeof(int) + 255) / 256 * 256;
+  }
+  const size_t next_off = off;
+  off += 256;
+  const int gap = c.persist_gap >= 0 ? c.persist_gap : (int)(2.5 * grid);
+  std::vector<unsigned> items;
+  if (W > 1) {
+    std::vector<int> t0(W), t1(W);
+    for (int r = 0; r < W; ++r) t0[r] = views[r].t0, t1[r] = views[r].t1;
+    persist_items(Tn, W, t0, t1, -1, gap, &items);
+  }
+  const size_t items_off = off;
+  off += items.size() * sizeof(unsigned);
+  TRY(c.ws_ver.ensure(off));
+  char *base = static_cast<char *>(c.ws_ver.p);
+  CU(cudaMemsetAsync(base, 0, items_off, st));
+  if (!items.empty())
+    CU(cudaMemcpyAsync(base + items_off, items.data(), items.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
   PersistArgs a{};
-  a.D = D;
-  a.P = P;
   a.ld = ld;
+  a.ldr = n_pad;
   a.T = Tn;
   // P1(K+1) takes about one tile wait + 1.6 tile times; the P2(K+1) items go in after roughly that
   // many grid-waves of round K's phase-3 tiles, so they rarely wait
-  a.gap = c.persist_gap >= 0 ? c.persist_gap : (int)(2.5 * grid);
-  a.ver = ver;
-  a.next = next;
+  a.gap = gap;
+  a.world = W;
+  a.items = items.empty() ? nullptr : reinterpret_cast<const unsigned *>(base + items_off);
+  a.next = reinterpret_cast<unsigned long long *>(base + next_off);
   a.maxkey = maxkey;
   a.flags = maxkey - 2;
-  a.total = 2LL * Tn - 1 + (long long)Tn * Tn * Tn;
+  a.total = W > 1 ? (long long)items.size() : 2LL * Tn - 1 + (long long)Tn * Tn * Tn;
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.sync_relaxed = c.persist_relaxed;
+  for (int r = 0; r < W; ++r) {
+    a.rk[r] = views[r];
+    a.rk[r].ver = reinterpret_cast<int *>(base + ver_off[r]);
+    a.rk[r].pub = W > 1 ? reinterpret_cast<int *>(base + pub_off[r]) : nullptr;
+  }
   Nvtx nv("persistent solve");
   if (e.timing) CU(cudaEventRecord(e.ev[0], st));
   kern<<<grid, kThreads, bytes, st>>>(a);
@@ -930,6 +1034,32 @@ int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *max
   CU(cudaGetLastError());
   if (e.timing) CU(cudaEventRecord(e.ev[2], st));
   return FW_OK;
+}
+
+template <typename T, int MODE>
+int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *maxkey, cudaStream_t st,
+                   const Events &e) {
+  std::vector<RankView> v(1);
+  v[0] = RankView{D, P, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, (int)(n_pad / 128)};
+  return launch_persistent<T, MODE>(c, v, ld, n_pad, maxkey, st, e);
+}
+
+// Loopback partition (every rank of a W-way block-row partition in this process, one GPU) as ONE
+// persistent grid with the fused publish: each rank's own rows, its own ring (the pivot-row
+// history the owners publish into) and pub flags. Tests the multi-GPU publish / poll protocol.
+template <typename T, int MODE>
+int run_loopback_persistent(Ctx &c, std::vector<Rounds<T, MODE>> &rk, cudaStream_t st, const Events &e) {
+  const int W = (int)rk.size();
+  const int64_t n_pad = rk[0].n_pad;
+  const size_t rb = (size_t)n_pad * n_pad * sizeof(T);
+  TRY(c.ws_ring.ensure(rb * W));
+  std::vector<RankView> v(W);
+  for (int r = 0; r < W; ++r) {
+    void *ring = static_cast<char *>(c.ws_ring.p) + rb * r;
+    v[r] = RankView{rk[r].D, rk[r].P, nullptr, nullptr, ring, nullptr, nullptr, rk[r].row0,
+                    (int)(rk[r].row0 / 128), (int)((rk[r].row0 + rk[r].nrows) / 128)};
+  }
+  return launch_persistent<T, MODE>(c, v, rk[0].ld, n_pad, maxkey_of(rk), st, e);
 }
 
 template <typename T, int MODE>
@@ -945,7 +1075,13 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
   c.last_pairs = false;
   c.last_pdl = false;
   c.last_persist = false;
-  if (tr == T_LOOPBACK) return run_loopback<T, MODE>(rk, st, la);
+  if (tr == T_LOOPBACK) {
+    if (c.persistent == 1 && BS == 128 && (int)rk.size() <= kMaxRanks) {
+      c.last_persist = true;
+      return run_loopback_persistent<T, MODE>(c, rk, st, ev);
+    }
+    return run_loopback<T, MODE>(rk, st, la);
+  }
   if (use_persistent(c, MODE, tr, BS, n_pad, rk[0].row0, rk[0].nrows)) {
     c.last_persist = true;
     return run_persistent<T, MODE>(c, rk[0].D, rk[0].P, rk[0].ld, n_pad, maxkey, st, ev);
@@ -2096,7 +2232,7 @@ void ctx_release(Ctx *c) {
   if (c->comm) g_nccl.CommDestroy(c->comm);
   c->comm = nullptr;
   for (DevBuf *b : {&c->ws_d, &c->ws_t, &c->ws_b, &c->ws_s, &c->ws_full, &c->ws_tr, &c->user_d,
-                    &c->user_t, &c->scratch, &c->ws_ver})
+                    &c->user_t, &c->scratch, &c->ws_ver, &c->ws_ring})
     b->release();
   if (c->pinned) cudaFreeHost(c->pinned);
   c->pinned = nullptr;

@@ -46,35 +46,62 @@
 
 namespace fwb {
 
-struct PersistArgs {
+constexpr int kMaxRanks = 8;   // ranks of one persistent grid (loopback) / of a team
+
+// One rank's rows of a block-row partition (world = 1: all rows). Local row i of D / P is global
+// row row0 + i; ver holds the round counters of the rank's tiles (tile-rows [t0, t1) x T);
+// ring is the rank's pivot-row history: global rows of block K at ring + K*128*ldr, written by
+// the owner of block K when those tiles are final for round K (the fused publish), with pub[K][J]
+// = K + 1 once tile (K, J) is there. The owner reads its own pivot rows in place instead.
+struct RankView {
   void *D;
   int32_t *P;
-  int64_t ld;
+  int *ver;
+  int *pub;
+  void *ring;
+  void *ring_mc;          // multicast address of the rings (NVLS), or null: per-peer stores
+  int *pub_mc;
+  int64_t row0;
+  int t0, t1;
+};
+
+struct PersistArgs {
+  int64_t ld;              // D / P pitch (elements)
+  int64_t ldr;             // ring pitch (n_pad)
   int T;                   // tiles per dimension = rounds (BS = 128)
   int gap;                 // rest(K) tiles between P1(K+1) and P2(K+1)
-  int *ver;                // T x T per-tile round counters (zeroed)
+  int world;               // ranks in rk[]
+  const unsigned *items;   // packed item table (multi-rank), or null: the one-rank order, decoded
   unsigned long long *next;   // work counter (zeroed)
   int *maxkey;             // KEY: largest stored key (speculative key runs)
   int *flags;              // bit 5: a dependency wait timed out (the host fails the solve)
   long long total;         // number of items
   unsigned long long timeout_ns;
   int sync_relaxed;        // dependency polls with relaxed loads (A/B option; see the kernel)
+  RankView rk[kMaxRanks];
 };
 
 enum ItemType { IT_NONE = 0, IT_P1 = 1, IT_TILE = 2 };
 struct Item {
-  int type, K, I, J;
+  int type, K, I, J, r;    // r: the rank whose rows hold tile (I, J)
 };
+// packed item (host-built tables): rank 3 | type 2 | K 9 | I 9 | J 9 bits
+__host__ __device__ __forceinline__ unsigned pack_item(int r, int type, int K, int I, int J) {
+  return ((unsigned)r << 29) | ((unsigned)type << 27) | ((unsigned)K << 18) | ((unsigned)I << 9) | (unsigned)J;
+}
+__device__ __forceinline__ Item unpack_item(unsigned u) {
+  return Item{(int)((u >> 27) & 3), (int)((u >> 18) & 511), (int)((u >> 9) & 511), (int)(u & 511), (int)(u >> 29)};
+}
 
 // Item `it` of the fixed order above.
 __device__ __forceinline__ Item persist_decode(const PersistArgs &a, long long it) {
   const int T = a.T;
-  Item w{IT_NONE, 0, 0, 0};
-  if (it == 0) return Item{IT_P1, 0, 0, 0};
+  Item w{IT_NONE, 0, 0, 0, 0};
+  if (it == 0) return Item{IT_P1, 0, 0, 0, 0};
   const long long pre = 2LL * T - 1;              // P1(0) + the 2(T-1) phase-2 tiles of round 0
   if (it < pre) {                                 // P2(0): row 0 (J = 1..T-1), column 0 (I = 1..T-1)
     const int q = (int)(it - 1);
-    return q < T - 1 ? Item{IT_TILE, 0, 0, q + 1} : Item{IT_TILE, 0, q - (T - 1) + 1, 0};
+    return q < T - 1 ? Item{IT_TILE, 0, 0, q + 1, 0} : Item{IT_TILE, 0, q - (T - 1) + 1, 0, 0};
   }
   // T^3 + 2T < 2^31 for T <= 512 (n <= 65536): 32-bit division
   const int t2 = T * T, r = (int)(it - pre);
@@ -84,27 +111,27 @@ __device__ __forceinline__ Item persist_decode(const PersistArgs &a, long long i
   if (K == T - 1) {                               // last round: its phase-3 tiles, then no-ops
     const int m = T - 1;
     if (q >= m * m) return w;
-    return Item{IT_TILE, K, skip2(q / m, K, -1), skip2(q % m, K, -1)};
+    return Item{IT_TILE, K, skip2(q / m, K, -1), skip2(q % m, K, -1), 0};
   }
   const int N = K + 1;
   if (q < T - 1) {                                // prio: row K+1, (K+1, K+1) first
-    return Item{IT_TILE, K, N, q == 0 ? N : skip2(q - 1, K, N)};
+    return Item{IT_TILE, K, N, q == 0 ? N : skip2(q - 1, K, N), 0};
   }
   q -= T - 1;
-  if (q < T - 2) return Item{IT_TILE, K, skip2(q, K, N), N};   // prio: column K+1
+  if (q < T - 2) return Item{IT_TILE, K, skip2(q, K, N), N, 0};   // prio: column K+1
   q -= T - 2;
-  if (q == 0) return Item{IT_P1, N, N, N};
+  if (q == 0) return Item{IT_P1, N, N, N, 0};
   q -= 1;
   const int m = T - 2, rest = m * m;
   const int gap = a.gap < rest ? a.gap : rest;
-  if (q < gap) return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N)};
+  if (q < gap) return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N), 0};
   q -= gap;
   if (q < 2 * (T - 1)) {                          // P2(K+1): row K+1, then column K+1
-    return q < T - 1 ? Item{IT_TILE, N, N, skip2(q, N, -1)} : Item{IT_TILE, N, skip2(q - (T - 1), N, -1), N};
+    return q < T - 1 ? Item{IT_TILE, N, N, skip2(q, N, -1), 0} : Item{IT_TILE, N, skip2(q - (T - 1), N, -1), N, 0};
   }
   q -= 2 * (T - 1);
   q += gap;
-  return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N)};
+  return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N), 0};
 }
 
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -129,18 +156,48 @@ __device__ __forceinline__ void wait_ge(const PersistArgs &a, const int *p, int 
 }
 
 template <typename T, int MODE>
-__device__ __forceinline__ void persist_phase1(const PersistArgs &a, int K, unsigned char *smem) {
-  T *D = static_cast<T *>(a.D);
-  const int kb = K * 128;
+__device__ __forceinline__ void persist_phase1(const PersistArgs &a, const RankView &v, int K, unsigned char *smem) {
+  T *D = static_cast<T *>(v.D);
+  const int kb = K * 128, r0 = (int)(kb - v.row0);
   if constexpr (std::is_same<T, float>::value && is_key(MODE)) {
-    phase1_key_f32_body<128, kP1Side, true>(D, a.P, a.ld, kb, kb, a.maxkey,
+    phase1_key_f32_body<128, kP1Side, true>(D, v.P, a.ld, r0, kb, a.maxkey,
                                              *reinterpret_cast<P1Smem<float, 128> *>(smem));
   } else if constexpr (!is_key(MODE)) {
-    phase1_pair_body<T, 128, MODE, kP1Side, true>(D, a.P, a.ld, kb, kb, K,
+    phase1_pair_body<T, 128, MODE, kP1Side, true>(D, v.P, a.ld, r0, kb, K,
                                                   *reinterpret_cast<P1Smem<T, 128> *>(smem));
   } else {
-    phase1_body<T, 128, MODE, kP1Side, true>(D, a.P, a.ld, kb, kb, K, a.maxkey,
+    phase1_body<T, 128, MODE, kP1Side, true>(D, v.P, a.ld, r0, kb, K, a.maxkey,
                                              *reinterpret_cast<P1Smem<T, 128> *>(smem));
+  }
+}
+
+// The fused publish: tile (K, J) of the owner's rows is final for round K (phase
+// 1 / the phase-2 row strip) — copy it into every other rank's pivot-row ring and raise that
+// rank's pub[K][J] (system-scope release: the rings of a team live on peer GPUs, written over
+// NVLink). With a multicast object (NVLS) one multimem store reaches every ring at once.
+template <typename T>
+__device__ __forceinline__ void persist_publish(const PersistArgs &a, int self, int K, int J) {
+  using V = typename Vec4<T>::V;
+  const RankView &o = a.rk[self];
+  const T *src = static_cast<const T *>(o.D) + (int64_t)(K * 128 - o.row0) * a.ld + J * 128;
+  const int64_t dst_off = (int64_t)K * 128 * a.ldr + J * 128;
+  for (int q = 0; q < a.world; ++q) {
+    if (q == self) continue;
+    T *dst = static_cast<T *>(a.rk[q].ring) + dst_off;
+    for (int e = threadIdx.x; e < 128 * 32; e += kThreads) {   // 128 rows x 32 float4
+      const int row = e >> 5, c4 = (e & 31) * 4;
+      const V x = __ldcg(reinterpret_cast<const V *>(src + (int64_t)row * a.ld + c4));
+      __stcg(reinterpret_cast<V *>(dst + (int64_t)row * a.ldr + c4), x);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < a.world; ++q) {
+      if (q == self) continue;
+      int *f = a.rk[q].pub + (int64_t)K * a.T + J;
+      asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(K + 1) : "memory");
+    }
   }
 }
 
@@ -148,6 +205,13 @@ __device__ __forceinline__ int ld_relaxed(const int *p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ int owner_rank(const PersistArgs &a, int K) {
+  int o = 0;
+  for (int q = 1; q < a.world; ++q)
+    if (K >= a.rk[q].t0) o = q;
+  return o;
 }
 
 template <typename T, int MODE>
@@ -164,7 +228,6 @@ fw_persistent_kernel(const PersistArgs a) {
   __shared__ long long s_next;
   using S = TileShape<128, 128>;
   const int tid = threadIdx.x;
-  T *D = static_cast<T *>(a.D);
   if (tid == 0) s_next = (long long)atomicAdd(a.next, 1ull);
   for (;;) {
     __syncthreads();   // the previous item is done with s_cur
@@ -172,20 +235,23 @@ fw_persistent_kernel(const PersistArgs a) {
       const long long it = s_next;
       if (it < a.total) {
         s_next = (long long)atomicAdd(a.next, 1ull);
-        s_cur = persist_decode(a, it);
+        s_cur = a.items ? unpack_item(a.items[it]) : persist_decode(a, it);
       } else {
-        s_cur = Item{-1, 0, 0, 0};
+        s_cur = Item{-1, 0, 0, 0, 0};
       }
     }
     __syncthreads();
     const Item w = s_cur;
     if (w.type < 0) break;
     if (w.type == IT_NONE) continue;
+    const RankView &v = a.rk[w.r];
+    T *D = static_cast<T *>(v.D);
+    const int li = w.I - v.t0;                      // local tile-row of the item's tile
     if (w.type == IT_TILE) {
       // warm L2 with the tile for the epilogue's compare (read once per round from HBM; its
       // latency is otherwise the epilogue's top stall), as the stream-ordered kernel does
       for (int l = tid; l < 128 * 4; l += kThreads)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)(w.I * 128 + l / 4) * a.ld + w.J * 128 + (l % 4) * 32));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)(li * 128 + l / 4) * a.ld + w.J * 128 + (l % 4) * 32));
     }
     if (tid < 3) {   // the operands this item reads and its own tile at the required round: one
                      // thread per counter, so the three loads are in flight together
@@ -193,21 +259,23 @@ fw_persistent_kernel(const PersistArgs a) {
       const int *p = nullptr;
       int need = 0;
       if (w.type == IT_P1) {
-        if (tid == 0) p = a.ver + w.K * T_ + w.K, need = w.K;
+        if (tid == 0) p = v.ver + li * T_ + w.K, need = w.K;
       } else if (tid == 0) {
-        p = a.ver + w.I * T_ + w.J, need = w.K;
+        p = v.ver + li * T_ + w.J, need = w.K;                      // own tile, round K-1 done
       } else if (tid == 1) {
-        if (w.J != w.K) p = a.ver + w.I * T_ + w.K, need = w.K + 1;
-      } else if (w.I != w.K) {
-        p = a.ver + w.K * T_ + w.J, need = w.K + 1;
+        if (w.J != w.K) p = v.ver + li * T_ + w.K, need = w.K + 1;  // A = (I, K), this rank's rows
+      } else if (w.I != w.K) {                                     // B = (K, J): in place on the
+        const bool own = w.K >= v.t0 && w.K < v.t1;                // owner, else the ring
+        p = own ? v.ver + (int64_t)(w.K - v.t0) * T_ + w.J : v.pub + w.K * T_ + w.J;
+        need = w.K + 1;
       }
       if (p) {
         // acquire (LDG.STRONG + an L1 invalidate), or relaxed when every operand read of the
         // kernel bypasses L1 anyway (cp.async.cg / ld.global.cg: a_sync_relaxed, A/B option)
-        int v = a.sync_relaxed ? ld_relaxed(p) : ld_acquire(p);
-        if (v < need) {
+        int val = a.sync_relaxed ? ld_relaxed(p) : ld_acquire(p);
+        if (val < need) {
           const unsigned long long t0 = globaltimer();
-          while ((v = a.sync_relaxed ? ld_relaxed(p) : ld_acquire(p)) < need) {
+          while ((val = a.sync_relaxed ? ld_relaxed(p) : ld_acquire(p)) < need) {
             if (globaltimer() - t0 > a.timeout_ns) {
               atomicOr(a.flags, 32);
               break;
@@ -219,15 +287,20 @@ fw_persistent_kernel(const PersistArgs a) {
     }
     __syncthreads();
     if (w.type == IT_P1) {
-      persist_phase1<T, MODE>(a, w.K, smem_raw);
+      persist_phase1<T, MODE>(a, v, w.K, smem_raw);
     } else {
+      const bool own_b = w.K >= v.t0 && w.K < v.t1;
+      const T *B = own_b ? D : static_cast<const T *>(v.ring);
+      const int64_t ldb = own_b ? a.ld : a.ldr;
+      const int brow = own_b ? (w.K - v.t0) * 128 : w.K * 128;
       T acc[S::RM][4 * S::H];
-      tile_mainloop<T, 128, 128>(reinterpret_cast<T *>(smem_raw), D, a.ld, w.I * 128, w.K * 128, D, a.ld,
-                                 w.K * 128, w.J * 128, 128 / kBK, acc);
+      tile_mainloop<T, 128, 128>(reinterpret_cast<T *>(smem_raw), D, a.ld, li * 128, w.K * 128, B, ldb, brow,
+                                 w.J * 128, 128 / kBK, acc);
       // the item again from shared memory: nothing but the accumulators lives across the loop
       const Item e = s_cur;
-      int kmax = tile_epilogue<T, 128, 128, MODE, true>(D, a.P, a.ld, e.I * 128, e.J * 128, 0, 0, 0, 0, e.K,
-                                                        (e.K * 128) & ~kKeyMask, acc);
+      const RankView &ve = a.rk[e.r];
+      int kmax = tile_epilogue<T, 128, 128, MODE, true>(static_cast<T *>(ve.D), ve.P, a.ld, (e.I - ve.t0) * 128,
+                                                        e.J * 128, 0, 0, 0, 0, e.K, (e.K * 128) & ~kKeyMask, acc);
       if (is_key(MODE)) {
         kmax = __reduce_max_sync(0xffffffffu, kmax);
         if ((tid & 31) == 0 && kmax > 0) atomicMax(a.maxkey, kmax);
@@ -235,9 +308,11 @@ fw_persistent_kernel(const PersistArgs a) {
     }
     __syncthreads();   // every thread's stores of the tile precede the release below (bar.sync
                        // orders them before thread 0's release, which is cumulative)
+    const Item e = s_cur;
+    if (a.world > 1 && e.I == e.K) persist_publish<T>(a, e.r, e.K, e.J);   // a final pivot-row tile
     if (tid == 0) {
-      const Item e = s_cur;
-      int *vp = a.ver + (int64_t)e.I * a.T + e.J;
+      const RankView &ve = a.rk[e.r];
+      int *vp = ve.ver + (int64_t)(e.I - ve.t0) * a.T + e.J;
       asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(vp), "r"(e.K + 1) : "memory");
     }
   }

@@ -197,3 +197,52 @@ def test_team_solve_matches_single_gpu(kind, n, block):
     else:
         np.testing.assert_allclose(out[1][0], out[0][0], rtol=1e-5)
     assert oracle.check_paths(W, out[1][0], out[1][1], rtol=0.0 if exact else 1e-5)[0] == 0
+
+
+# ---- persistent loopback: every rank in ONE persistent grid, the fused publish ----
+def loopback_persistent(W, world, path="next"):
+    fw.fw_init(0, (fw.FW_PATH_LAST_K if path == "lastk" else 0) | fw.FW_TIMING)
+    try:
+        fw.fw_set_option("persistent", 1)
+        dD = torch.from_numpy(W).cuda()
+        dP = torch.empty(W.shape, dtype=torch.int32, device="cuda") if path else None
+        f = fw.fw_dist_loopback_solve_device_i32 if W.dtype == np.int32 else fw.fw_dist_loopback_solve_device_f32
+        f(dD, dP, block=128, world=world, stream=torch.cuda.current_stream())
+        s = fw.fw_last_stats()
+        return dD.cpu().numpy(), (dP.cpu().numpy() if dP is not None else None), s
+    finally:
+        fw.fw_free()
+
+
+PCASES = [
+    ("complete_int", 1000, 2, "next"), ("complete_int", 1024, 8, "next"), ("complete_real", 700, 3, "next"),
+    ("complete_real", 900, 4, "lastk"), ("er_int", 800, 3, "next"), ("er_int_f32", 640, 5, "next"),
+    ("complete_int", 300, 4, "next"),   # a rank with padding rows only
+    ("complete_int", 768, 2, None),
+]
+
+
+@pytest.mark.parametrize("kind,n,world,path", PCASES)
+def test_loopback_persistent_publish(kind, n, world, path):
+    """The multi-rank persistent solve: each rank's phase-2 row strip / phase-1 tiles are copied
+    by the producing CTA into every other rank's pivot-row ring with a release flag per tile
+    (the fused publish), and the other ranks' tiles poll those flags — all ranks in one grid.
+    D against the oracle (bitwise for integer data), P valid."""
+    W = gen.generate(kind, n, 50 + n, p=0.03, lo=1, hi=1000 if kind.startswith("er") else 100)
+    D, P, s = loopback_persistent(W, world, path)
+    assert s.persistent == 1
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    if path:
+        bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5, mode=path)
+        assert bad == 0, (bad, divmod(first, n))
+
+
+def test_loopback_persistent_matches_single_gpu_bitwise():
+    """Integer data: the persistent partitioned solve gives the single-GPU distances bit for bit."""
+    W = gen.generate("complete_int", 896, 77)
+    D1, _ = loopback(W, 128, 1)
+    for world in (2, 7):
+        Dw, Pw, _ = loopback_persistent(W, world)
+        np.testing.assert_array_equal(Dw, D1)
+        assert oracle.check_paths(W, Dw, Pw)[0] == 0
