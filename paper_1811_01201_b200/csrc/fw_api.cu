@@ -34,6 +34,7 @@
 #include <chrono>
 #include <map>
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -82,6 +83,7 @@ struct Nccl {
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -98,7 +100,7 @@ int load_nccl() {
 #define SYM(name)                                                                        \
   *reinterpret_cast<void **>(&g_nccl.name) = dlsym(h, "nccl" #name);                     \
   if (!g_nccl.name) return fail(FW_ENCCL, "libnccl.so.2 lacks nccl" #name);
-  SYM(GetUniqueId) SYM(CommInitRank) SYM(CommInitAll) SYM(CommDestroy) SYM(Broadcast) SYM(AllReduce)
+  SYM(GetUniqueId) SYM(CommInitRank) SYM(CommInitAll) SYM(CommDestroy) SYM(Broadcast) SYM(AllReduce) SYM(AllGather)
   SYM(GroupStart) SYM(GroupEnd) SYM(GetErrorString) SYM(CommInitRankConfig) SYM(CommGetAsyncError)
   SYM(CommAbort)
 #undef SYM
@@ -172,7 +174,10 @@ struct Ctx {
   int persist_relaxed = 0;         // persistent: dependency polls with relaxed loads (A/B option)
   bool last_persist = false;       // the last solve ran as one persistent launch
   DevBuf ws_ver;                   // persistent: per-tile round counters, pub flags, work counter, items
-  DevBuf ws_ring;                  // persistent loopback: every rank's pivot-row ring (n_pad^2 each)
+  DevBuf ws_ring;                  // persistent: pivot-row ring(s) (n_pad^2 each) [+ pub flags, NCCL mode]
+  DevBuf ws_ipc;                   // persistent NCCL mode: all-gathered IPC handles
+  std::vector<void *> peer_ring;   // persistent NCCL mode: the peers' rings, IPC-mapped
+  std::vector<cudaIpcMemHandle_t> peer_handle;
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
   bool comm_dead = false;          // the communicator was aborted (error, timeout, failed peer)
   std::atomic<int> *abort_flag = nullptr;   // team solve: set by the first rank that fails
@@ -880,6 +885,11 @@ struct Part {
 
 template <typename R> int *maxkey_of(std::vector<R> &rk) { return rk[0].maxkey; }
 
+template <typename T, int MODE>
+int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t n_pad, int *maxkey,
+                      cudaStream_t st, const Events &e, int self = -1,
+                      const std::function<int()> &barrier = nullptr);
+
 // The whole solve as one persistent launch (fw_persist.cuh): one GPU, all rows,
 // BS = 128. Auto: round-tag solves (real-valued data, one round per pass). Keyed and
 // distance-only solves keep the two-rounds-per-pass schedule (§4.9), whose 256-deep bulk
@@ -967,9 +977,12 @@ void persist_items(int T, int world, const std::vector<int> &t0, const std::vect
 // One persistent launch over the ranks of `views` (world = 1: all rows of one GPU, items
 // decoded arithmetically; world > 1: a loopback partition emulated in ONE grid — the guide's way
 // to test ranks that wait on one another on one GPU — with the item table and the rings).
+// self >= 0: this process runs rank `self` of a communicator (its items only); the views' ring /
+// pub pointers (peers' mapped through CUDA IPC) and the zeroing of its pub flags are the
+// caller's, and `barrier` runs between the zeroing and the launch.
 template <typename T, int MODE>
 int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t n_pad, int *maxkey,
-                      cudaStream_t st, const Events &e) {
+                      cudaStream_t st, const Events &e, int self, const std::function<int()> &barrier) {
   const int Tn = (int)(n_pad / 128), W = (int)views.size();
   if (W > kMaxRanks) return fail(FW_EINVAL, "persistent solve: at most %d ranks", kMaxRanks);
   auto kern = fw_persistent_kernel<T, MODE>;
@@ -989,7 +1002,7 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
     ver_off[r] = off;
     off += ((size_t)(views[r].t1 - views[r].t0) * Tn * sizeof(int) + 255) / 256 * 256;
     pub_off[r] = off;
-    if (W > 1) off += ((size_t)Tn * Tn * sizeof(int) + 255) / 256 * 256;
+    if (W > 1 && self < 0) off += ((size_t)Tn * Tn * sizeof(int) + 255) / 256 * 256;
   }
   const size_t next_off = off;
   off += 256;
@@ -998,7 +1011,7 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   if (W > 1) {
     std::vector<int> t0(W), t1(W);
     for (int r = 0; r < W; ++r) t0[r] = views[r].t0, t1[r] = views[r].t1;
-    persist_items(Tn, W, t0, t1, -1, gap, &items);
+    persist_items(Tn, W, t0, t1, self, gap, &items);
   }
   const size_t items_off = off;
   off += items.size() * sizeof(unsigned);
@@ -1025,8 +1038,9 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   for (int r = 0; r < W; ++r) {
     a.rk[r] = views[r];
     a.rk[r].ver = reinterpret_cast<int *>(base + ver_off[r]);
-    a.rk[r].pub = W > 1 ? reinterpret_cast<int *>(base + pub_off[r]) : nullptr;
+    if (self < 0) a.rk[r].pub = W > 1 ? reinterpret_cast<int *>(base + pub_off[r]) : nullptr;
   }
+  if (barrier) TRY(barrier());
   Nvtx nv("persistent solve");
   if (e.timing) CU(cudaEventRecord(e.ev[0], st));
   kern<<<grid, kThreads, bytes, st>>>(a);
@@ -1042,6 +1056,63 @@ int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *max
   std::vector<RankView> v(1);
   v[0] = RankView{D, P, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0, (int)(n_pad / 128)};
   return launch_persistent<T, MODE>(c, v, ld, n_pad, maxkey, st, e);
+}
+
+// One rank of a communicator (one process per GPU) as a persistent grid with the fused publish
+// (opt-in: fw_set_option("persistent", 1)): every rank allocates its pivot-row
+// ring + pub flags, the CUDA IPC handles are all-gathered over NCCL and mapped (NVLink peer
+// access), each rank zeroes its own flags, an NCCL all-reduce is the barrier before the launch,
+// and the owner of each pivot-row tile stores it straight into the peers' rings (P2P stores over
+// NVLink) with a system-scope release flag — no ncclBroadcast in the rounds. The all-reduces of
+// the next solve's validation order its zeroing after every peer's kernel. NOT run on hardware:
+// the gpurun boxes have one GPU (the protocol is tested by the loopback grid above).
+template <typename T, int MODE>
+int run_nccl_persistent(Ctx &c, Rounds<T, MODE> &rk, cudaStream_t st, const Events &e) {
+  const int W = rk.world, self = c.rank;
+  if (W > kMaxRanks) return fail(FW_EINVAL, "persistent multi-GPU solve: at most %d ranks", kMaxRanks);
+  const int64_t n_pad = rk.n_pad;
+  const int Tn = (int)(n_pad / 128);
+  const size_t rb = ((size_t)n_pad * n_pad * sizeof(T) + 255) / 256 * 256, pb = (size_t)Tn * Tn * sizeof(int);
+  TRY(c.ws_ring.ensure(rb + pb));
+  // exchange the ring allocations' IPC handles (every solve: 64 B per rank; mapped once per change)
+  TRY(c.ws_ipc.ensure((size_t)W * sizeof(cudaIpcMemHandle_t) * 2));
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, c.ws_ring.p));
+  char *dh = static_cast<char *>(c.ws_ipc.p);
+  CU(cudaMemcpyAsync(dh, &h, sizeof h, cudaMemcpyHostToDevice, st));
+  NCC(c, g_nccl.AllGather(dh, dh + W * sizeof h, sizeof h, ncclChar, c.comm, st));
+  std::vector<cudaIpcMemHandle_t> all(W);
+  CU(cudaMemcpyAsync(all.data(), dh + W * sizeof h, W * sizeof h, cudaMemcpyDeviceToHost, st));
+  TRY(sync_stream(c, st));
+  if ((int)c.peer_ring.size() != W) {
+    c.peer_ring.assign(W, nullptr);
+    c.peer_handle.assign(W, cudaIpcMemHandle_t{});
+  }
+  for (int q = 0; q < W; ++q) {
+    if (q == self) continue;
+    if (c.peer_ring[q] && memcmp(&c.peer_handle[q], &all[q], sizeof h) == 0) continue;
+    if (c.peer_ring[q]) cudaIpcCloseMemHandle(c.peer_ring[q]);
+    c.peer_ring[q] = nullptr;
+    CU(cudaIpcOpenMemHandle(&c.peer_ring[q], all[q], cudaIpcMemLazyEnablePeerAccess));
+    c.peer_handle[q] = all[q];
+  }
+  std::vector<RankView> v(W);
+  for (int q = 0; q < W; ++q) {
+    int64_t r0, nr;
+    partition(n_pad, W, q, &r0, &nr);
+    char *ring = q == self ? static_cast<char *>(c.ws_ring.p) : static_cast<char *>(c.peer_ring[q]);
+    v[q] = RankView{nullptr, nullptr, nullptr, reinterpret_cast<int *>(ring + rb), ring, nullptr, nullptr, r0,
+                    (int)(r0 / 128), (int)((r0 + nr) / 128)};
+  }
+  v[self].D = rk.D;
+  v[self].P = rk.P;
+  CU(cudaMemsetAsync(static_cast<char *>(c.ws_ring.p) + rb, 0, pb, st));
+  int *d_bar = rk.errflags() + 4;   // d_flags[4]: a scratch int for the barrier all-reduce
+  auto barrier = [&]() -> int {
+    NCC(c, g_nccl.AllReduce(d_bar, d_bar, 1, ncclInt32, ncclMax, c.comm, st));
+    return FW_OK;
+  };
+  return launch_persistent<T, MODE>(c, v, rk.ld, n_pad, rk.maxkey, st, e, self, barrier);
 }
 
 // Loopback partition (every rank of a W-way block-row partition in this process, one GPU) as ONE
@@ -1081,6 +1152,10 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
       return run_loopback_persistent<T, MODE>(c, rk, st, ev);
     }
     return run_loopback<T, MODE>(rk, st, la);
+  }
+  if (tr == T_NCCL && c.persistent == 1 && BS == 128 && world <= kMaxRanks) {
+    c.last_persist = true;
+    return run_nccl_persistent<T, MODE>(c, rk[0], st, ev);
   }
   if (use_persistent(c, MODE, tr, BS, n_pad, rk[0].row0, rk[0].nrows)) {
     c.last_persist = true;
@@ -2231,8 +2306,12 @@ void ctx_release(Ctx *c) {
   cudaSetDevice(c->dev);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   c->comm = nullptr;
+  for (void *pr : c->peer_ring)
+    if (pr) cudaIpcCloseMemHandle(pr);
+  c->peer_ring.clear();
+  c->peer_handle.clear();
   for (DevBuf *b : {&c->ws_d, &c->ws_t, &c->ws_b, &c->ws_s, &c->ws_full, &c->ws_tr, &c->user_d,
-                    &c->user_t, &c->scratch, &c->ws_ver, &c->ws_ring})
+                    &c->user_t, &c->scratch, &c->ws_ver, &c->ws_ring, &c->ws_ipc})
     b->release();
   if (c->pinned) cudaFreeHost(c->pinned);
   c->pinned = nullptr;

@@ -85,7 +85,7 @@ def test_loopback_fallback_to_tags():
     np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % 700))
 
 
-def _nccl_one_rank(W, block, path="next", timing=True):
+def _nccl_one_rank(W, block, path="next", timing=True, persistent=None):
     """fw_dist_solve_device_* over a ONE-rank NCCL communicator: the NCCL data plane runs
     (every round's pivot strip through ncclBroadcast, validation / placement / key checks
     through ncclAllReduce, the TAG post-pass gather through grouped broadcasts)."""
@@ -96,6 +96,8 @@ def _nccl_one_rank(W, block, path="next", timing=True):
         uid = fw.fw_comm_unique_id()
         assert len(uid) == 128
         fw.fw_comm_init(uid, 0, 1)
+        if persistent is not None:
+            fw.fw_set_option("persistent", persistent)
         row0, nrows = fw.fw_dist_partition(n, 1, 0)
         assert (row0, nrows) == (0, n)
         dD = torch.from_numpy(W).cuda()
@@ -246,3 +248,18 @@ def test_loopback_persistent_matches_single_gpu_bitwise():
         Dw, Pw, _ = loopback_persistent(W, world)
         np.testing.assert_array_equal(Dw, D1)
         assert oracle.check_paths(W, Dw, Pw)[0] == 0
+
+
+@pytest.mark.parametrize("kind,n,path", [("complete_int", 1000, "next"), ("complete_real", 640, "next"),
+                                         ("er_int", 513, "lastk")])
+def test_nccl_single_rank_persistent(kind, n, path):
+    """The communicator path of the persistent solve (opt-in) on a one-rank communicator: the
+    ring allocation's CUDA IPC handle is all-gathered over NCCL, the pub flags zeroed, an NCCL
+    all-reduce is the barrier before the launch, and the persistent grid runs this rank's items."""
+    W = gen.generate(kind, n, 60 + n, p=0.03, lo=1, hi=1000 if kind.startswith("er") else 100)
+    D, P, s = _nccl_one_rank(W, 128, path, persistent=1)
+    assert s.persistent == 1
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5, mode=path)
+    assert bad == 0, (bad, divmod(first, n))
