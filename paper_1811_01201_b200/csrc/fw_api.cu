@@ -421,12 +421,15 @@ int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int 
                      int *maxkey) {
   // the tile lives in registers; shared memory holds only row / column k (static, 2 KB at BS = 128),
   // so the CTA fits beside a phase-3 CTA on one SM (the look-ahead starts it early)
+  // 256 threads of (BS/16)^2 elements (512 threads of 8 x 4 or 4 x 8 at BS = 128 measured slower:
+  // C2 TAG 39.6 -> 48.3 / 47.0 us, C4 keys 55.1 -> 59.9 / 58.0 us per round)
+  constexpr int R1 = BS / kP1Side;
   if (std::is_same<T, float>::value && is_key(MODE)) {   // FP32 keys: select-free variant
-    phase1_key_f32_kernel<BS><<<1, kP1Side * kP1Side, 0, st>>>(reinterpret_cast<float *>(D), P, ld, r0, kb,
-                                                              maxkey);
+    phase1_key_f32_kernel<BS, R1, R1><<<1, kP1Side * kP1Side, 0, st>>>(reinterpret_cast<float *>(D), P, ld, r0, kb,
+                                                                      maxkey);
   } else if (!is_key(MODE)) {                             // PLAIN / TAG: two steps per barrier
-    phase1_pair_kernel<T, BS, is_key(MODE) ? MODE_PLAIN : MODE><<<1, kP1Side * kP1Side, 0, st>>>(D, P, ld, r0,
-                                                                                               kb, K);
+    phase1_pair_kernel<T, BS, is_key(MODE) ? MODE_PLAIN : MODE, R1, R1><<<1, kP1Side * kP1Side, 0, st>>>(D, P, ld,
+                                                                                                       r0, kb, K);
   } else {                                                // INT32 keys: per-step P select
     phase1_kernel<T, BS, MODE><<<1, kP1Side * kP1Side, 0, st>>>(D, P, ld, r0, kb, K, maxkey);
   }

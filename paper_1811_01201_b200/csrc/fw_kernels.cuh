@@ -436,6 +436,21 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
 
   const int64_t ld = g.ld;
   const int kb = PAIRS ? (cstrip ? (cstrip == 2 ? (j0 ^ 128) : j0) : g.kb) : (g.colstrip ? j0 : g.kb);
+  // TAG / PLAIN: the cp.async source addresses are recomputed every chunk from the tile origin in
+  // shared memory and a fresh %tid.x, so no address lives across the main loop — with the two
+  // 64-bit source pointers live, ptxas spilled them (20 B) and reloaded them after every
+  // chunk's barrier, the same pattern that cost the KEY variant 6% when it appeared there
+  // (profiles/r02_refactor_regression.json). The KEY variant allocates spill-free as it is.
+  __shared__ int s_org[4];
+  if constexpr (MODE != MODE_KEY) {
+    if (threadIdx.x == 0) {
+      s_org[0] = i0;
+      s_org[1] = j0;
+      s_org[2] = kb;
+      s_org[3] = cstrip;
+    }
+    __syncthreads();
+  }
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   // Warm L2 with this tile of D for the epilogue's compare (128-B lines, per-thread
   // addresses): the tile is read once per round from HBM, and its latency was the
@@ -461,12 +476,27 @@ minplus_tile_kernel(T *__restrict__ D, int32_t *__restrict__ P, const TileArgs g
   auto load_chunk = [&](int stage, int k0) {
     T *as = smem + stage * S::kStage;
     T *bs = as + S::kA;
+    if constexpr (MODE == MODE_KEY) {
 #pragma unroll
-    for (int t = 0; t < A_PER; ++t)
-      cp_async16(as + (a_r + t * A_ROWS) * S::AS + a_c, a_src + k0 + (int64_t)t * A_ROWS * ld);
+      for (int t = 0; t < A_PER; ++t)
+        cp_async16(as + (a_r + t * A_ROWS) * S::AS + a_c, a_src + k0 + (int64_t)t * A_ROWS * ld);
 #pragma unroll
-    for (int t = 0; t < B_PER; ++t)
-      cp_async16(bs + (b_r + t * B_ROWS) * S::BSTR + b_c, b_src + (int64_t)(k0 + t * B_ROWS) * ldb);
+      for (int t = 0; t < B_PER; ++t)
+        cp_async16(bs + (b_r + t * B_ROWS) * S::BSTR + b_c, b_src + (int64_t)(k0 + t * B_ROWS) * ldb);
+    } else {
+      int tv;
+      asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tv));
+      const int oi = s_org[0], oj = s_org[1], okb = s_org[2], ocs = s_org[3];
+      const int ar = tv / (kBK / 4), ac = (tv % (kBK / 4)) * 4, br = tv / (TN / 4), bc = (tv % (TN / 4)) * 4;
+      const T *asrc = D + (int64_t)(oi + ar) * ld + okb + ac;
+      const T *bsrc = static_cast<const T *>(g.B) + (int64_t)((ocs ? okb : 0) + br) * ldb + oj + bc;
+#pragma unroll
+      for (int t = 0; t < A_PER; ++t)
+        cp_async16(as + (ar + t * A_ROWS) * S::AS + ac, asrc + k0 + (int64_t)t * A_ROWS * ld);
+#pragma unroll
+      for (int t = 0; t < B_PER; ++t)
+        cp_async16(bs + (br + t * B_ROWS) * S::BSTR + bc, bsrc + (int64_t)(k0 + t * B_ROWS) * ldb);
+    }
     cp_async_commit();
   };
 
@@ -777,73 +807,82 @@ phase1_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, in
 // to their state after step k by every thread (col'[a] = min(col_k1[a], col_k[a] + D[k][k+1]),
 // row'[b] = min(row_k1[b], D[k+1][k] + row_k[b])), then x = min(x, c_k, c'_k+1) — exactly the
 // sequential loop's values (min is exact; each candidate is the same single rounded sum).
-template <typename T, int BS, int MODE, int NT = kP1Side, bool CG = false>
+// Thread layout of the two-steps-per-barrier phase-1 bodies: RY rows x RX columns per thread,
+// (BS/RY) x (BS/RX) threads (BS = 128: 256 threads of 8 x 8; 512 threads of 8 x 4 or 4 x 8 fit
+// in half the register file only with spills and measured slower).
+template <int BS, int RY, int RX> struct P1Layout {
+  static constexpr int NX = BS / RX, NY = BS / RY, kThreads = NX * NY;
+  static constexpr int U = RY > RX ? RY : RX;   // k unroll period: row / column slots compile-time
+  static_assert(RY % 2 == 0 && RX % 2 == 0 && U % RY == 0 && U % RX == 0 && BS % U == 0, "phase-1 layout");
+};
+
+template <typename T, int BS, int MODE, int RY, int RX, bool CG = false>
 __device__ __forceinline__ void phase1_pair_body(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0,
                                                  int kb, int tag, P1Smem<T, BS> &sm) {
-  constexpr int R = BS / NT;
-  static_assert(R % 2 == 0 && !is_key(MODE), "pairs of steps; keyed modes use their own kernels");
+  using L = P1Layout<BS, RY, RX>;
+  static_assert(!is_key(MODE), "pairs of steps; keyed modes use their own kernels");
   using T2 = typename std::conditional<Num<T>::kIsInt, int2, float2>::type;
   T (*rowb)[2][BS] = sm.rowb;   // rows k, k+1 (pair parity)
   T2 (*colb)[BS] = sm.colb;     // (column k, column k+1) per row
-  const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
+  const int tx = threadIdx.x % L::NX, ty = threadIdx.x / L::NX;
   T *Dk = D + (int64_t)r0 * ld + kb;
-  T d[R][R];
+  T d[RY][RX];
 #pragma unroll
-  for (int r = 0; r < R; ++r) ldg_vec<T, R, CG>(d[r], Dk + (int64_t)(R * ty + r) * ld + R * tx);
+  for (int r = 0; r < RY; ++r) ldg_vec<T, RX, CG>(d[r], Dk + (int64_t)(RY * ty + r) * ld + RX * tx);
   if (ty == 0) {
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
-      rowb[0][0][R * tx + c] = d[0][c];
-      rowb[0][1][R * tx + c] = d[1][c];
+    for (int c = 0; c < RX; ++c) {
+      rowb[0][0][RX * tx + c] = d[0][c];
+      rowb[0][1][RX * tx + c] = d[1][c];
     }
   }
   if (tx == 0) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) colb[0][R * ty + r] = T2{d[r][0], d[r][1]};
+    for (int r = 0; r < RY; ++r) colb[0][RY * ty + r] = T2{d[r][0], d[r][1]};
   }
   __syncthreads();
-  for (int k0 = 0; k0 < BS; k0 += R) {
+  for (int k0 = 0; k0 < BS; k0 += L::U) {
 #pragma unroll
-    for (int kr = 0; kr < R; kr += 2) {
+    for (int kr = 0; kr < L::U; kr += 2) {
       const int k = k0 + kr, buf = (k >> 1) & 1;
-      T rk[R], rk1[R];
-      lds_vec<T, R>(rk, &rowb[buf][0][R * tx]);
-      lds_vec<T, R>(rk1, &rowb[buf][1][R * tx]);
+      T rk[RX], rk1[RX];
+      lds_vec<T, RX>(rk, &rowb[buf][0][RX * tx]);
+      lds_vec<T, RX>(rk1, &rowb[buf][1][RX * tx]);
       const T d01 = rowb[buf][0][k + 1];   // D[k][k+1]
       const T d10 = colb[buf][k + 1].x;    // D[k+1][k]
 #pragma unroll
-      for (int c = 0; c < R; ++c) rk1[c] = tmin(rk1[c], d10 + rk[c]);   // INT32: <= 2 INF, no overflow
+      for (int c = 0; c < RX; ++c) rk1[c] = tmin(rk1[c], d10 + rk[c]);   // INT32: <= 2 INF, no overflow
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const T2 ca = colb[buf][R * ty + r];
+      for (int r = 0; r < RY; ++r) {
+        const T2 ca = colb[buf][RY * ty + r];
         const T ck1 = tmin(ca.y, ca.x + d01);
 #pragma unroll
-        for (int c = 0; c < R; c += 2)
+        for (int c = 0; c < RX; c += 2)
           relax_pair2(d[r][c], d[r][c + 1], ca.x, ck1, rk[c], rk[c + 1], rk1[c], rk1[c + 1]);
       }
-      if (k + 2 < BS) {
-        const int s2 = (kr + 2) % R, s3 = (kr + 3) % R;
-        const int owner = (k + 2) / R;
-        if (owner == ty) {
+      if (k + 2 < BS) {   // publish rows / columns k+2, k+3 (slots of one owner: k+2 is even)
+        if ((k + 2) / RY == ty) {
+          const int s2 = (kr + 2) % RY, s3 = (kr + 3) % RY;
 #pragma unroll
-          for (int c = 0; c < R; ++c) {
-            rowb[buf ^ 1][0][R * tx + c] = d[s2][c];
-            rowb[buf ^ 1][1][R * tx + c] = d[s3][c];
+          for (int c = 0; c < RX; ++c) {
+            rowb[buf ^ 1][0][RX * tx + c] = d[s2][c];
+            rowb[buf ^ 1][1][RX * tx + c] = d[s3][c];
           }
         }
-        if (owner == tx) {
+        if ((k + 2) / RX == tx) {
+          const int s2 = (kr + 2) % RX, s3 = (kr + 3) % RX;
 #pragma unroll
-          for (int r = 0; r < R; ++r) colb[buf ^ 1][R * ty + r] = T2{d[r][s2], d[r][s3]};
+          for (int r = 0; r < RY; ++r) colb[buf ^ 1][RY * ty + r] = T2{d[r][s2], d[r][s3]};
         }
       }
       __syncthreads();
     }
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int r = 0; r < RY; ++r)
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
-      const int a = R * ty + r, b = R * tx + c;
+    for (int c = 0; c < RX; ++c) {
+      const int a = RY * ty + r, b = RX * tx + c;
       const int64_t off = (int64_t)a * ld + b;
       if (d[r][c] < ldg1<CG>(Dk + off)) {
         Dk[off] = d[r][c];
@@ -852,11 +891,11 @@ __device__ __forceinline__ void phase1_pair_body(T *__restrict__ D, int32_t *__r
     }
 }
 
-template <typename T, int BS, int MODE, int NT = kP1Side>
-__global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
+template <typename T, int BS, int MODE, int RY, int RX>
+__global__ void __launch_bounds__(P1Layout<BS, RY, RX>::kThreads, 2)   // half the register file: fits beside a phase-3 CTA
 phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {
   __shared__ P1Smem<T, BS> sm;
-  phase1_pair_body<T, BS, MODE, NT>(D, P, ld, r0, kb, tag, sm);
+  phase1_pair_body<T, BS, MODE, RY, RX>(D, P, ld, r0, kb, tag, sm);
 }
 
 // Phase 1, FP32 keyed mode, without a per-relaxation select for P. The running value of
@@ -867,23 +906,22 @@ phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r
 // bits — the sequential strict-< result of the paper's loop, with one FADD + one FMNMX per
 // relaxation. Row k+1 is published as D*256 (B side), column k+1 as D*256 + k' (A side), both
 // recovered as floor((x + 0.5) / 256) * 256. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
-template <int BS, int NT = kP1Side, bool CG = false>
+template <int BS, int RY, int RX, bool CG = false>
 __device__ __forceinline__ void phase1_key_f32_body(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld,
                                                     int r0, int kb, int *maxkey, P1Smem<float, BS> &sm) {
-  constexpr int R = BS / NT;
-  static_assert(R % 2 == 0, "step parity = register slot parity needs an even R");
+  using L = P1Layout<BS, RY, RX>;
   float (*rowb)[2][BS] = sm.rowb;   // rows k, k+1, B form D*256  (pair parity)
   float2 (*colb)[BS] = sm.colb;     // (column k, column k+1) per row, A form D*256 + k'
-  const int tx = threadIdx.x % NT, ty = threadIdx.x / NT;
+  const int tx = threadIdx.x % L::NX, ty = threadIdx.x / L::NX;
   float *Dk = D + (int64_t)r0 * ld + kb;
   const int kgrp = kb & ~kKeyMask, klow = kb & kKeyMask;
-  float x[R][R];
+  float x[RY][RX];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    float key[R];
-    ldg_vec<float, R, CG>(key, Dk + (int64_t)(R * ty + r) * ld + R * tx);  // D*256 + ((kb+b)&255) or +inf
+  for (int r = 0; r < RY; ++r) {
+    float key[RX];
+    ldg_vec<float, RX, CG>(key, Dk + (int64_t)(RY * ty + r) * ld + RX * tx);  // D*256 + ((kb+b)&255) or +inf
 #pragma unroll
-    for (int c = 0; c < R; ++c) x[r][c] = key[c] - (float)(klow + R * tx + c) - 0.5f;   // D*256 - 0.5
+    for (int c = 0; c < RX; ++c) x[r][c] = key[c] - (float)(klow + RX * tx + c) - 0.5f;   // D*256 - 0.5
   }
   // steps k and k+1 per barrier (the sequential loop's values, two steps at a time): every
   // thread brings row / column k+1 to their state after step k itself,
@@ -893,53 +931,53 @@ __device__ __forceinline__ void phase1_key_f32_body(float *__restrict__ D, int32
   // every candidate is the same integer sum as in the one-step loop).
   if (ty == 0) {
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
-      rowb[0][0][R * tx + c] = x[0][c] + 0.5f;                           // D*256
-      rowb[0][1][R * tx + c] = x[1][c] + 0.5f;
+    for (int c = 0; c < RX; ++c) {
+      rowb[0][0][RX * tx + c] = x[0][c] + 0.5f;                           // D*256
+      rowb[0][1][RX * tx + c] = x[1][c] + 0.5f;
     }
   }
   if (tx == 0) {
 #pragma unroll
-    for (int r = 0; r < R; ++r)                                          // + k'
-      colb[0][R * ty + r] = make_float2(x[r][0] + 0.5f + (float)klow, x[r][1] + 0.5f + (float)(klow + 1));
+    for (int r = 0; r < RY; ++r)                                          // + k'
+      colb[0][RY * ty + r] = make_float2(x[r][0] + 0.5f + (float)klow, x[r][1] + 0.5f + (float)(klow + 1));
   }
   __syncthreads();
-  for (int k0 = 0; k0 < BS; k0 += R) {
+  for (int k0 = 0; k0 < BS; k0 += L::U) {
 #pragma unroll
-    for (int kr = 0; kr < R; kr += 2) {
+    for (int kr = 0; kr < L::U; kr += 2) {
       const int k = k0 + kr, buf = (k >> 1) & 1;
-      float rk[R], rk1[R];
-      lds_vec<float, R>(rk, &rowb[buf][0][R * tx]);    // B side, own cols
-      lds_vec<float, R>(rk1, &rowb[buf][1][R * tx]);
+      float rk[RX], rk1[RX];
+      lds_vec<float, RX>(rk, &rowb[buf][0][RX * tx]);    // B side, own cols
+      lds_vec<float, RX>(rk1, &rowb[buf][1][RX * tx]);
       const float d01 = rowb[buf][0][k + 1] + 1.0f;              // D[k][k+1]*256 + 1
       const float d10 = colb[buf][k + 1].x - (float)(klow + k);  // D[k+1][k]*256 (exact; inf stays)
 #pragma unroll
-      for (int c = 0; c < R; ++c) rk1[c] = fminf(rk1[c], d10 + rk[c]);
+      for (int c = 0; c < RX; ++c) rk1[c] = fminf(rk1[c], d10 + rk[c]);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const float2 ca = colb[buf][R * ty + r];                 // A side, own row (broadcast)
+      for (int r = 0; r < RY; ++r) {
+        const float2 ca = colb[buf][RY * ty + r];                // A side, own row (broadcast)
         const float ck1 = fminf(ca.y, ca.x + d01);
 #pragma unroll
-        for (int c = 0; c < R; c += 2)
+        for (int c = 0; c < RX; c += 2)
           relax_pair2(x[r][c], x[r][c + 1], ca.x, ck1, rk[c], rk[c + 1], rk1[c], rk1[c + 1]);
       }
-      // publish rows / columns k+2 and k+3 (register slots (kr+2)%R, (kr+3)%R of one owner)
+      // publish rows / columns k+2 and k+3 (slots of one owner: k+2 is even)
       if (k + 2 < BS) {
-        const int s2 = (kr + 2) % R, s3 = (kr + 3) % R;
-        const int owner = (k + 2) / R;
-        if (owner == ty) {
+        if ((k + 2) / RY == ty) {
+          const int s2 = (kr + 2) % RY, s3 = (kr + 3) % RY;
 #pragma unroll
-          for (int c = 0; c < R; ++c) {
-            rowb[buf ^ 1][0][R * tx + c] = floorf((x[s2][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
-            rowb[buf ^ 1][1][R * tx + c] = floorf((x[s3][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
+          for (int c = 0; c < RX; ++c) {
+            rowb[buf ^ 1][0][RX * tx + c] = floorf((x[s2][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
+            rowb[buf ^ 1][1][RX * tx + c] = floorf((x[s3][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
           }
         }
-        if (owner == tx) {
+        if ((k + 2) / RX == tx) {
+          const int s2 = (kr + 2) % RX, s3 = (kr + 3) % RX;
           const float kp = (float)(klow + k + 2);
 #pragma unroll
-          for (int r = 0; r < R; ++r)
-            colb[buf ^ 1][R * ty + r] = make_float2(floorf((x[r][s2] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp,
-                                                    floorf((x[r][s3] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp + 1.0f);
+          for (int r = 0; r < RY; ++r)
+            colb[buf ^ 1][RY * ty + r] = make_float2(floorf((x[r][s2] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp,
+                                                     floorf((x[r][s3] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp + 1.0f);
         }
       }
       __syncthreads();
@@ -947,12 +985,12 @@ __device__ __forceinline__ void phase1_key_f32_body(float *__restrict__ D, int32
   }
   int kmax = 0;
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int r = 0; r < RY; ++r)
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
+    for (int c = 0; c < RX; ++c) {
       const float v = x[r][c];
       if (v < __int_as_float(0x7f800000) && v == floorf(v)) {   // an integer: strictly improved
-        const int a = R * ty + r, b = R * tx + c;
+        const int a = RY * ty + r, b = RX * tx + c;
         const float hi = floorf(v * (1.0f / kKeyMul)) * (float)kKeyMul;
         const int kk = (int)(v - hi);
         const float key = hi + (float)(klow + b);
@@ -965,12 +1003,12 @@ __device__ __forceinline__ void phase1_key_f32_body(float *__restrict__ D, int32
   if ((threadIdx.x & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
 }
 
-template <int BS, int NT = kP1Side>
-__global__ void __launch_bounds__(NT * NT, 2)   // <= 128 registers: fits beside a phase-3 CTA
+template <int BS, int RY, int RX>
+__global__ void __launch_bounds__(P1Layout<BS, RY, RX>::kThreads, 2)   // half the register file: fits beside a phase-3 CTA
 phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
                       int *maxkey) {
   __shared__ P1Smem<float, BS> sm;
-  phase1_key_f32_body<BS, NT>(D, P, ld, r0, kb, maxkey, sm);
+  phase1_key_f32_body<BS, RY, RX>(D, P, ld, r0, kb, maxkey, sm);
 }
 
 // ---------------------------------------------------------------------------------

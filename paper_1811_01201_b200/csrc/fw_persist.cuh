@@ -160,10 +160,10 @@ __device__ __forceinline__ void persist_phase1(const PersistArgs &a, const RankV
   T *D = static_cast<T *>(v.D);
   const int kb = K * 128, r0 = (int)(kb - v.row0);
   if constexpr (std::is_same<T, float>::value && is_key(MODE)) {
-    phase1_key_f32_body<128, kP1Side, true>(D, v.P, a.ld, r0, kb, a.maxkey,
+    phase1_key_f32_body<128, 8, 8, true>(D, v.P, a.ld, r0, kb, a.maxkey,
                                              *reinterpret_cast<P1Smem<float, 128> *>(smem));
   } else if constexpr (!is_key(MODE)) {
-    phase1_pair_body<T, 128, MODE, kP1Side, true>(D, v.P, a.ld, r0, kb, K,
+    phase1_pair_body<T, 128, MODE, 8, 8, true>(D, v.P, a.ld, r0, kb, K,
                                                   *reinterpret_cast<P1Smem<T, 128> *>(smem));
   } else {
     phase1_body<T, 128, MODE, kP1Side, true>(D, v.P, a.ld, r0, kb, K, a.maxkey,

@@ -44,6 +44,6 @@ for spec in a.sets.split(";"):
     fw.fw_free()
     m = statistics.median(ms)
     print(json.dumps({"config": a.config, "n": n, "opts": opts, "solve_ms": m, "min_ms": min(ms),
-                      "tflops": 2 * n ** 3 / (m * 1e-3) / 1e12, "persistent": st.persistent,
+                      "tflops": 2 * n ** 3 / (m * 1e-3) / 1e12, "persistent": st.persistent, "phase1_ms": st.phase1_ms, "phase2_ms": st.phase2_ms, "rounds": st.rounds,
                       "p_method": st.p_method, "phase3_ms": st.phase3_ms, "post_ms": st.post_ms,
                       "launches": st.kernel_launches}), flush=True)
