@@ -236,6 +236,16 @@ int fw_dist_loopback_solve_device_i32(int32_t *d_dist, int32_t *d_next, int64_t 
 int64_t fw_path(const int32_t *P, const void *dist, int dist_is_int32, int64_t n, int64_t i, int64_t j,
                 int mode, int32_t *out, int64_t max_len);
 
+/* Host-only (no GPU, no fw_init): the work-item order of the persistent solve
+ * for n vertices on a `world`-way block-row partition (world in [1, 8]); rank = -1: every rank's
+ * items (the loopback grid), else that rank's subsequence (one GPU of a communicator); rank = -2
+ * (world 1): the one-GPU kernel's own arithmetic decode of the order, run on the host; gap = the
+ * phase-3 tiles placed between P1(K+1) and the phase-2 items of round K+1. Each item is packed as
+ * rank << 29 | type << 27 | K << 18 | I << 9 | J (type 1 = phase 1 on tile (K, K), 2 = tile (I, J)
+ * relaxed through block K). With out = NULL, max_out = 0 returns the count. Returns the number of
+ * items, or -FW_EINVAL (bad arguments, max_out too small). For tests of the order's invariants. */
+int64_t fw_persist_schedule(int64_t n, int world, int rank, int gap, uint32_t *out, int64_t max_out);
+
 /* Message for the last non-OK return on this thread ("" if none). */
 const char *fw_last_error(void);
 

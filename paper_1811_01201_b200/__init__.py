@@ -31,6 +31,7 @@ from ._binding import (  # noqa: F401
     fw_dist_loopback_solve_device_f32,
     fw_dist_loopback_solve_device_i32,
     fw_last_stats,
+    fw_persist_schedule,
     fw_version,
     library_path,
 )

@@ -73,6 +73,8 @@ _lib.fw_dist_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_dist_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _P]
 _lib.fw_dist_loopback_solve_device_f32.argtypes = [_P, _P, _I64, _I64, _I, _I, _P]
 _lib.fw_dist_loopback_solve_device_i32.argtypes = [_P, _P, _I64, _I64, _I, _I, _P]
+_lib.fw_persist_schedule.argtypes = [_I64, _I, _I, _I, _P, _I64]
+_lib.fw_persist_schedule.restype = ctypes.c_int64
 _lib.fw_last_error.restype = ctypes.c_char_p
 _lib.fw_last_stats.argtypes = [ctypes.POINTER(FwStats)]
 _lib.fw_version.restype = ctypes.c_char_p
@@ -327,6 +329,20 @@ def fw_dist_loopback_solve_device_i32(d_dist, d_next=None, n=None, ld=None, bloc
     _check(_lib.fw_dist_loopback_solve_device_i32(_device_matrix(d_dist, n, ld, "int32", "d_dist"),
                                                   _device_matrix(d_next, n, ld, "int32", "d_next"), n, ld,
                                                   block, world, _stream_handle(stream)))
+
+
+def fw_persist_schedule(n: int, world: int = 1, rank: int = -1, gap: int = 0):
+    """Work-item order of the persistent solve (host-only): a numpy uint32 array of packed
+    items (rank << 29 | type << 27 | K << 18 | I << 9 | J)."""
+    import numpy as np
+    cnt = _lib.fw_persist_schedule(n, world, rank, gap, None, 0)
+    if cnt < 0:
+        _check(int(-cnt))
+    out = np.empty(int(cnt), dtype=np.uint32)
+    r = _lib.fw_persist_schedule(n, world, rank, gap, out.ctypes.data, int(cnt))
+    if r < 0:
+        _check(int(-r))
+    return out
 
 
 def fw_last_error() -> str:

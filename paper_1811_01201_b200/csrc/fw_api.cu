@@ -2677,6 +2677,39 @@ int fw_host_pipeline_bounds(int64_t n, int chunk_tiles, int first_tiles, int32_t
   return (int)tb.size();
 }
 
+int64_t fw_persist_schedule(int64_t n, int world, int rank, int gap, uint32_t *out, int64_t max_out) {
+  if (n <= 0 || n > 65536 || world < 1 || world > kMaxRanks || rank < -2 || rank >= world || gap < 0 ||
+      max_out < 0 || (max_out > 0 && !out) || (rank == -2 && world != 1))
+    return -fail(FW_EINVAL, "fw_persist_schedule: bad arguments (n=%lld world=%d rank=%d gap=%d)", (long long)n, world,
+                 rank, gap);
+  const int64_t n_pad = (n + 127) / 128 * 128;
+  const int T = (int)(n_pad / 128);
+  std::vector<int> t0(world), t1(world);
+  for (int r = 0; r < world; ++r) {
+    int64_t r0, nr;
+    partition(n_pad, world, r, &r0, &nr);
+    t0[r] = (int)(r0 / 128);
+    t1[r] = (int)((r0 + nr) / 128);
+  }
+  std::vector<unsigned> items;
+  if (rank == -2) {   // the one-GPU kernel's arithmetic decode (persist_decode), run on the host
+    PersistArgs a{};
+    a.T = T;
+    a.gap = gap;
+    const long long total = 2LL * T - 1 + (long long)T * T * T;
+    for (long long it = 0; it < total; ++it) {
+      const Item w = persist_decode(a, it);
+      if (w.type != IT_NONE) items.push_back(pack_item(0, w.type, w.K, w.I, w.J));
+    }
+  } else {
+    persist_items(T, world, t0, t1, rank, gap, &items);
+  }
+  if ((int64_t)items.size() > max_out && max_out > 0)
+    return -fail(FW_EINVAL, "fw_persist_schedule: %zu items > max_out = %lld", items.size(), (long long)max_out);
+  if (max_out > 0) memcpy(out, items.data(), items.size() * sizeof(unsigned));
+  return (int64_t)items.size();
+}
+
 int fw_solve_i32(int32_t *dist, int32_t *next, int64_t n, int block, int ngpus) {
   return solve_host<int32_t>(dist, next, n, block, ngpus);
 }

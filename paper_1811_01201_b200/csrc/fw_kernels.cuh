@@ -179,7 +179,7 @@ struct TileArgs {
 };
 
 // k-th element of {0, .., n-1} \ {x, y} (x, y < 0 or distinct: not excluded twice)
-__device__ __forceinline__ int skip2(int k, int x, int y) {
+__host__ __device__ __forceinline__ int skip2(int k, int x, int y) {
   const int lo = (x >= 0 && y >= 0) ? min(x, y) : max(x, y), hi = (x >= 0 && y >= 0) ? max(x, y) : -1;
   if (lo >= 0 && k >= lo) ++k;
   if (hi >= 0 && k >= hi) ++k;

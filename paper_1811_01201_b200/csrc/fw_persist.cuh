@@ -94,7 +94,7 @@ __device__ __forceinline__ Item unpack_item(unsigned u) {
 }
 
 // Item `it` of the fixed order above.
-__device__ __forceinline__ Item persist_decode(const PersistArgs &a, long long it) {
+__host__ __device__ __forceinline__ Item persist_decode(const PersistArgs &a, long long it) {
   const int T = a.T;
   Item w{IT_NONE, 0, 0, 0, 0};
   if (it == 0) return Item{IT_P1, 0, 0, 0, 0};
