@@ -254,16 +254,26 @@ __device__ __forceinline__ int ctaid(int dim) {
   return v;
 }
 
-// ---- the tile product, shared by the stream-ordered tile kernel and the persistent kernel ----
+// ---- the tile product of the persistent kernel (fw_persist.cuh) ---------------------------------
+// Operand origins of one tile, in shared memory: A(i, k) = a[i*lda + k] (the tile's rows of the
+// pivot column block), B(k, j) = b[k*ldb + j] (the pivot row block's columns of the tile).
+template <typename T> struct TileSrc {
+  const T *a;
+  const T *b;
+  int64_t lda, ldb;
+};
+
 // Main loop of one TM x TN tile: acc[r][c] = min over k < nch*kBK of A(i, k) + B(k, j) for the
-// thread's rows i = ty + TY*r and columns j = 4*tx + 4*TX*h + e, A(i, k) = A[(arow + i)*lda + acol + k]
-// (the tile's rows of the pivot column block), B(k, j) = B[(brow + k)*ldb + bcol + j] (the pivot
-// row block's columns of the tile). The k dimension is streamed in chunks of kBK through kStages shared-memory stages
-// (cp.async 16 B, .cg: through L2, never a stale L1 line): A row-major [i][k] (padded stride:
-// conflict-free LDS.128), B row-major [k][j]; one barrier per chunk.
+// thread's rows i = ty + TY*r and columns j = 4*tx + 4*TX*h + e. The k dimension is streamed in
+// chunks of kBK through kStages shared-memory stages (cp.async 16 B, .cg: through L2, never a
+// stale L1 line): A row-major [i][k] (padded stride: conflict-free LDS.128), B row-major [k][j];
+// one barrier per chunk. The cp.async source addresses are recomputed every chunk from `src`
+// (shared memory) and a fresh %tid.x, so no address lives across the loop: with them live, the
+// 128-register allocation spilled them and reloaded them after every chunk's barrier (the
+// pattern that cost the stream kernel 6%). The same arithmetic as the stream
+// kernel below (which writes it out to keep its spill-free allocation).
 template <typename T, int TM, int TN>
-__device__ __forceinline__ void tile_mainloop(T *smem, const T *__restrict__ A, int64_t lda, int arow, int acol,
-                                              const T *__restrict__ B, int64_t ldb, int brow, int bcol, int nch,
+__device__ __forceinline__ void tile_mainloop(T *smem, const TileSrc<T> *src, int nch,
                                               T (&acc)[TileShape<TM, TN>::RM][4 * TileShape<TM, TN>::H]) {
   using S = TileShape<TM, TN>;
   using V = typename Vec4<T>::V;
@@ -275,20 +285,22 @@ __device__ __forceinline__ void tile_mainloop(T *smem, const T *__restrict__ A, 
   constexpr int B_PER = kBK * (TN / 4) / kThreads;
   constexpr int B_ROWS = kThreads / (TN / 4);
   static_assert(A_PER >= 1 && B_PER >= 1, "copy mapping");
-  const int a_r = tid / (kBK / 4), a_c = (tid % (kBK / 4)) * 4;
-  const int b_r = tid / (TN / 4), b_c = (tid % (TN / 4)) * 4;
-  const T *a_src = A + (int64_t)(arow + a_r) * lda + acol + a_c;
-  const T *b_src = B + (int64_t)(brow + b_r) * ldb + bcol + b_c;
 
   auto load_chunk = [&](int stage, int k0) {
     T *as = smem + stage * S::kStage;
     T *bs = as + S::kA;
+    int tv;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tv));
+    const int ar = tv / (kBK / 4), ac = (tv % (kBK / 4)) * 4, br = tv / (TN / 4), bc = (tv % (TN / 4)) * 4;
+    const int64_t lda = src->lda, ldb = src->ldb;
+    const T *asrc = src->a + (int64_t)ar * lda + ac;
+    const T *bsrc = src->b + (int64_t)br * ldb + bc;
 #pragma unroll
     for (int t = 0; t < A_PER; ++t)
-      cp_async16(as + (a_r + t * A_ROWS) * S::AS + a_c, a_src + k0 + (int64_t)t * A_ROWS * lda);
+      cp_async16(as + (ar + t * A_ROWS) * S::AS + ac, asrc + k0 + (int64_t)t * A_ROWS * lda);
 #pragma unroll
     for (int t = 0; t < B_PER; ++t)
-      cp_async16(bs + (b_r + t * B_ROWS) * S::BSTR + b_c, b_src + (int64_t)(k0 + t * B_ROWS) * ldb);
+      cp_async16(bs + (br + t * B_ROWS) * S::BSTR + bc, bsrc + (int64_t)(k0 + t * B_ROWS) * ldb);
     cp_async_commit();
   };
 

@@ -226,6 +226,7 @@ fw_persistent_kernel(const PersistArgs a) {
   // static assignment measured 6% slower at C5.
   __shared__ Item s_cur;
   __shared__ long long s_next;
+  __shared__ TileSrc<T> s_src;   // the current tile's operand origins (tile_mainloop)
   using S = TileShape<128, 128>;
   const int tid = threadIdx.x;
   if (tid == 0) s_next = (long long)atomicAdd(a.next, 1ull);
@@ -235,7 +236,18 @@ fw_persistent_kernel(const PersistArgs a) {
       const long long it = s_next;
       if (it < a.total) {
         s_next = (long long)atomicAdd(a.next, 1ull);
-        s_cur = a.items ? unpack_item(a.items[it]) : persist_decode(a, it);
+        const Item w = a.items ? unpack_item(a.items[it]) : persist_decode(a, it);
+        s_cur = w;
+        if (w.type == IT_TILE) {   // A = (I, K) of this rank's rows; B = (K, J) in place or the ring
+          const RankView &v = a.rk[w.r];
+          const bool own_b = w.K >= v.t0 && w.K < v.t1;
+          const T *Dv = static_cast<const T *>(v.D);
+          s_src.a = Dv + (int64_t)(w.I - v.t0) * 128 * a.ld + w.K * 128;
+          s_src.lda = a.ld;
+          s_src.b = own_b ? Dv + (int64_t)(w.K - v.t0) * 128 * a.ld + w.J * 128
+                          : static_cast<const T *>(v.ring) + (int64_t)w.K * 128 * a.ldr + w.J * 128;
+          s_src.ldb = own_b ? a.ld : a.ldr;
+        }
       } else {
         s_cur = Item{-1, 0, 0, 0, 0};
       }
@@ -289,13 +301,8 @@ fw_persistent_kernel(const PersistArgs a) {
     if (w.type == IT_P1) {
       persist_phase1<T, MODE>(a, v, w.K, smem_raw);
     } else {
-      const bool own_b = w.K >= v.t0 && w.K < v.t1;
-      const T *B = own_b ? D : static_cast<const T *>(v.ring);
-      const int64_t ldb = own_b ? a.ld : a.ldr;
-      const int brow = own_b ? (w.K - v.t0) * 128 : w.K * 128;
       T acc[S::RM][4 * S::H];
-      tile_mainloop<T, 128, 128>(reinterpret_cast<T *>(smem_raw), D, a.ld, li * 128, w.K * 128, B, ldb, brow,
-                                 w.J * 128, 128 / kBK, acc);
+      tile_mainloop<T, 128, 128>(reinterpret_cast<T *>(smem_raw), &s_src, 128 / kBK, acc);
       // the item again from shared memory: nothing but the accumulators lives across the loop
       const Item e = s_cur;
       const RankView &ve = a.rk[e.r];
