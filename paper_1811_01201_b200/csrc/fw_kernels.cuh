@@ -1173,7 +1173,9 @@ __global__ void emit_rows_kernel(const T *D, int64_t ld, int64_t n, int64_t rows
 // 512-B segment loads in flight and the next group's tags are loaded before the current
 // group is searched: the kernel reads ~4*BS bytes per element (~n^2 * 512 B at BS = 128).
 
-// Dt = D^T for a rows x cols matrix (pitch ld -> pitch ldt), 32x32 shared-memory tiles.
+// Dt = D^T for a rows x cols matrix (pitch ld -> pitch ldt), 32x32 shared-memory tiles. The
+// diagonal of Dt is written as INF: the resolve below then never picks k = j (D[i][j] + D[j][j]
+// = D[i][j] holds trivially) without testing for it.
 template <typename T>
 __global__ void transpose_kernel(const T *D, int64_t ld, int64_t rows, int64_t cols, T *Dt,
                                  int64_t ldt) {
@@ -1186,7 +1188,7 @@ __global__ void transpose_kernel(const T *D, int64_t ld, int64_t rows, int64_t c
   __syncthreads();
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int64_t c = c0 + y, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) Dt[c * ldt + r] = tile[threadIdx.x][y];
+    if (r < rows && c < cols) Dt[c * ldt + r] = r == c ? Num<T>::inf() : tile[threadIdx.x][y];
   }
 }
 
@@ -1217,13 +1219,15 @@ resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t r
   const T *Drow = D + li * ld;
   int32_t *trow = tags + li * ld;
   if (use_smem) {
-    for (int j = threadIdx.x; j < (int)n_pad; j += blockDim.x) srow[j] = Drow[j];
+    // row i of the final D, with D[i][i] read as INF: k = i is never picked (D[i][i] + D[i][j] =
+    // D[i][j] trivially) without testing for it; k = j is excluded by Dt's INF diagonal
+    for (int j = threadIdx.x; j < (int)n_pad; j += blockDim.x) srow[j] = j == gi ? Num<T>::inf() : Drow[j];
     __syncthreads();
   }
   const T *A = use_smem ? srow : Drow;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int step = nw * U;
-  // group metadata (tags, D[i][j]) is loaded one group ahead of the segment loads
+  // group metadata (tags) is loaded one group ahead of the segment loads
   int tg[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -1247,24 +1251,19 @@ resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t r
       const int j = j0 + u;
       const int k0 = max(tg[u], 0) * BS + CH * lane;
       const V a = *reinterpret_cast<const V *>(A + k0);   // row i: shared memory (or L1)
-      const T dij = A[min(j, nn - 1)];                    // the final D[i][j] (one broadcast)
+      const T dij = A[min(j, nn - 1)];   // the final D[i][j] (j = i reads INF: untagged, discarded)
       // reading R9: k* = the FIRST k of block K, k not in {i, j}, with D[i][k] + D[k][j] <= D[i][j]
-      // (one exists: the improving k of the tag's round; later rounds only lowered both terms
-      // and rounding is monotone). Lane bits c = candidates k0 + c; padding k >= n is INF.
-      unsigned hit = 0;
+      // (one exists: the improving k of the tag's round; later rounds only lowered both terms and
+      // rounding is monotone). Each lane takes its first hit among its CH candidates, the warp the
+      // smallest: one min-reduction (REDUX) per element. Padding k >= n is INF.
+      int kl = 0x7fffffff;
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
+      for (int c = CH - 1; c >= 0; --c) {
         const T sum = (T)velem(a, c) + (T)velem(b[u], c);
-        hit |= (sum <= dij ? 1u : 0u) << c;
+        kl = (sum <= dij && (use_smem || k0 + c != gi)) ? k0 + c : kl;
       }
-      const unsigned di = (unsigned)(gi - k0), dj = (unsigned)(j - k0);
-      if (di < (unsigned)CH) hit &= ~(1u << di);
-      if (dj < (unsigned)CH) hit &= ~(1u << dj);
-      const unsigned m = __ballot_sync(0xffffffffu, hit != 0);
-      const int src = m ? __ffs(m) - 1 : 0;
-      const unsigned h = __shfl_sync(0xffffffffu, hit, src);
-      const int ks = max(tg[u], 0) * BS + CH * src + __ffs(h) - 1;
-      if (lane == u) res = m ? ks : -1;
+      const int km = __reduce_min_sync(0xffffffffu, kl);
+      if (lane == u) res = km == 0x7fffffff ? -1 : km;
     }
     if (lane < U && j0 + lane < nn) {
       // tg[lane] without dynamic register indexing
