@@ -416,6 +416,10 @@ void put(TileArgs &a, int z, const Strip &s) {
   a.mc_lo[z] = s.mc_lo; a.mc_hi[z] = s.mc_hi; a.xrow[z] = s.xrow;
 }
 
+// phase 1 of PLAIN / TAG solves at BS = 128 as the blocked closure (env FW_P1_BLOCKED=0: the
+// 64 pair-steps of phase1_pair_kernel instead; A/B)
+int g_p1_blocked = 1;
+
 template <typename T, int BS, int MODE>
 int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int kb, int K,
                      int *maxkey) {
@@ -423,6 +427,16 @@ int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int 
   // so the CTA fits beside a phase-3 CTA on one SM (the look-ahead starts it early)
   // 256 threads of (BS/16)^2 elements (512 threads of 8 x 4 or 4 x 8 at BS = 128 measured slower:
   // C2 TAG 39.6 -> 48.3 / 47.0 us, C4 keys 55.1 -> 59.9 / 58.0 us per round)
+  if constexpr (BS == 128 && !is_key(MODE)) {
+    if (g_p1_blocked) {   // PLAIN / TAG: the blocked closure (4 sub-rounds of 32)
+      auto kern = phase1_blocked_kernel<T, MODE>;
+      TRY(smem_attr((const void *)kern, (int)sizeof(P1BSmem<T>)));
+      kern<<<1, 256, sizeof(P1BSmem<T>), st>>>(D, P, ld, r0, kb, K);
+      ++g_launches;
+      CU(cudaGetLastError());
+      return FW_OK;
+    }
+  }
   constexpr int R1 = BS / kP1Side;
   if (std::is_same<T, float>::value && is_key(MODE)) {   // FP32 keys: select-free variant
     phase1_key_f32_kernel<BS, R1, R1><<<1, kP1Side * kP1Side, 0, st>>>(reinterpret_cast<float *>(D), P, ld, r0, kb,
@@ -1038,6 +1052,7 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   a.total = W > 1 ? (long long)items.size() : 2LL * Tn - 1 + (long long)Tn * Tn * Tn;
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.sync_relaxed = c.persist_relaxed;
+  a.p1_blocked = g_p1_blocked;
   for (int r = 0; r < W; ++r) {
     a.rk[r] = views[r];
     a.rk[r].ver = reinterpret_cast<int *>(base + ver_off[r]);
@@ -2563,6 +2578,8 @@ int fw_init(int ngpus_max, unsigned flags) {
   c->pair_order = !(po && po[0] == '0');
   const char *pp = getenv("FW_PIPE_PAIR_ROWS");
   if (pp && atoi(pp) >= 1) c->pipe_pair_rows = atoi(pp);
+  const char *pb1 = getenv("FW_P1_BLOCKED");
+  if (pb1) g_p1_blocked = atoi(pb1) != 0;
   const char *ps = getenv("FW_PERSISTENT");   // one persistent launch per solve: -1 auto, 0 off, 1 on
   if (ps && atoi(ps) >= -1 && atoi(ps) <= 1) c->persistent = atoi(ps);
   const char *pf = getenv("FW_PIPE_FIRST");   // tuning: first chunk of the auto host pipeline

@@ -903,6 +903,218 @@ __device__ __forceinline__ void phase1_pair_body(T *__restrict__ D, int32_t *__r
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Phase 1, blocked (PLAIN / TAG, BS = 128, 256 threads): the closure of D_KK computed as the
+// paper's own blocked Floyd–Warshall one level down (P:101-112 applied to the 128 x 128 block
+// with 32 x 32 sub-blocks), instead of 128 sequential steps of the whole CTA. For each
+// sub-round s of 4:
+//   (a) closure of the diagonal sub-block (s, s): ONE warp, lane a holding row a in registers,
+//       two steps per __syncwarp (rows k, k+1 published through shared memory; the pair-step
+//       algebra of phase1_pair_body) — 16 warp-level syncs instead of 64 CTA barriers;
+//   (b) the row / column sub-strips (s, t), (t, s) as min-plus products with the closed
+//       sub-block (reading R7): 128 threads each;
+//   (c) the other 9 sub-blocks (t, u) <- min(., (t, s) (x) (s, u)): 256 threads of 6 x 6.
+// Same distances as the sequential loop (R7, R8: min is exact, every candidate one rounded
+// add). The 128 x 128 block lives in shared memory (pitch 132: conflict-free 16-B row reads
+// by consecutive lanes), 68 KB: one CTA still fits beside a phase-3 CTA.
+constexpr int kP1BPitch = 132;
+template <typename T> struct P1BSmem {
+  __align__(16) T t[128 * kP1BPitch];
+  __align__(16) T rb[2][2][32];   // sub-phase (a): rows k, k+1 by pair parity
+};
+
+// x[r][2p + e] = min(x, min_k A(r, k) + B(k, 2p + e)) over 32 k: A rows at a[r] (k contiguous),
+// B column pairs at b[p] (row pitch kP1BPitch). FADD2 + FMNMX3 over two k per instruction pair.
+template <typename T, int RY, int NP>
+__device__ __forceinline__ void p1b_product(T (&x)[RY][2 * NP], const T *sm, const int (&a)[RY], const int (&b)[NP]) {
+  using V = typename Vec4<T>::V;
+  using T2 = typename std::conditional<Num<T>::kIsInt, int2, float2>::type;
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    V av[RY];
+#pragma unroll
+    for (int r = 0; r < RY; ++r) av[r] = *reinterpret_cast<const V *>(sm + a[r] + k);
+#pragma unroll
+    for (int kk = 0; kk < 4; kk += 2) {
+      T2 b0[NP], b1[NP];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        b0[q] = *reinterpret_cast<const T2 *>(sm + b[q] + (k + kk) * kP1BPitch);
+        b1[q] = *reinterpret_cast<const T2 *>(sm + b[q] + (k + kk + 1) * kP1BPitch);
+      }
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const T a0 = kk ? av[r].z : av[r].x, a1 = kk ? av[r].w : av[r].y;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) relax_pair2(x[r][2 * q], x[r][2 * q + 1], a0, a1, b0[q].x, b0[q].y, b1[q].x, b1[q].y);
+      }
+    }
+  }
+}
+
+// index g in [0, 96) of the three sub-blocks other than s -> tile index in [0, 128)
+__device__ __forceinline__ int p1b_other(int g, int s) {
+  const int q = g >> 5;
+  return ((q < s ? q : q + 1) << 5) + (g & 31);
+}
+
+template <typename T, int MODE, bool CG = false>
+__device__ __forceinline__ void phase1_blocked_body(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0,
+                                                    int kb, int tag, P1BSmem<T> &sm) {
+  static_assert(!is_key(MODE), "plain distances / round tags");
+  using V = typename Vec4<T>::V;
+  T *t = sm.t;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  T *Dk = D + (int64_t)r0 * ld + kb;
+  for (int e = tid; e < 128 * 32; e += 256) {   // the block into shared memory (16-B loads)
+    const int r = e >> 5, c4 = (e & 31) * 4;
+    V v;
+    if constexpr (CG) v = __ldcg(reinterpret_cast<const V *>(Dk + (int64_t)r * ld + c4));
+    else v = *reinterpret_cast<const V *>(Dk + (int64_t)r * ld + c4);
+    *reinterpret_cast<V *>(t + r * kP1BPitch + c4) = v;
+  }
+  __syncthreads();
+  for (int s = 0; s < 4; ++s) {
+    const int o = s * 32;
+    // (a) closure of sub-block (s, s) by warp 0: lane a holds row a
+    if (warp == 0) {
+      T x[32];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const V v = *reinterpret_cast<const V *>(t + (o + lane) * kP1BPitch + o + 4 * q);
+        x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+      }
+      if (lane < 2) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) sm.rb[0][lane][c] = x[c];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 32; k += 2) {
+        const int pb = (k >> 1) & 1;
+        T rk[32], rk1[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const V v0 = *reinterpret_cast<const V *>(&sm.rb[pb][0][4 * q]);
+          const V v1 = *reinterpret_cast<const V *>(&sm.rb[pb][1][4 * q]);
+          rk[4 * q] = v0.x; rk[4 * q + 1] = v0.y; rk[4 * q + 2] = v0.z; rk[4 * q + 3] = v0.w;
+          rk1[4 * q] = v1.x; rk1[4 * q + 1] = v1.y; rk1[4 * q + 2] = v1.z; rk1[4 * q + 3] = v1.w;
+        }
+        const T d01 = rk[k + 1], d10 = rk1[k];   // S[k][k+1], S[k+1][k]
+#pragma unroll
+        for (int c = 0; c < 32; ++c) rk1[c] = tmin(rk1[c], d10 + rk[c]);   // row k+1 after step k
+        const T ak = x[k], ak1 = tmin(x[k + 1], x[k] + d01);             // own column k, k+1
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) relax_pair2(x[c], x[c + 1], ak, ak1, rk[c], rk[c + 1], rk1[c], rk1[c + 1]);
+        if (k + 2 < 32) {
+          if (lane == k + 2 || lane == k + 3) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) sm.rb[pb ^ 1][lane - k - 2][c] = x[c];
+          }
+          __syncwarp();
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        V v;
+        v.x = x[4 * q]; v.y = x[4 * q + 1]; v.z = x[4 * q + 2]; v.w = x[4 * q + 3];
+        *reinterpret_cast<V *>(t + (o + lane) * kP1BPitch + o + 4 * q) = v;
+      }
+    }
+    __syncthreads();
+    // (b) row sub-strips (s, t) = S* (x) (s, t) [threads 0..127: 4 rows x 3 column pairs] and
+    //     column sub-strips (t, s) = (t, s) (x) S* [threads 128..255: 6 rows x 2 column pairs];
+    //     every operand is read before the barrier, the results stored after it (in place)
+    {
+      T xr[6][6];
+      int nr = 0, np = 0, orow[6], ocol[3];
+      if (tid < 128) {
+        const int ry = tid >> 4, cx = tid & 15;   // 8 row groups x 16 column groups
+        int a[4], b[3];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) { orow[r] = o + 4 * ry + r; a[r] = orow[r] * kP1BPitch + o; }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { ocol[q] = p1b_other(6 * cx + 2 * q, s); b[q] = o * kP1BPitch + ocol[q]; }
+        T x4[4][6];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) x4[r][c] = t[orow[r] * kP1BPitch + ocol[c >> 1] + (c & 1)];
+        p1b_product<T, 4, 3>(x4, t, a, b);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) xr[r][c] = x4[r][c];
+        nr = 4;
+        np = 3;
+      } else {
+        const int u = tid - 128, ry = u >> 3, cx = u & 7;   // 16 row groups x 8 column groups
+        int a[6], b[2];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) { orow[r] = p1b_other(6 * ry + r, s); a[r] = orow[r] * kP1BPitch + o; }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) { ocol[q] = o + 4 * cx + 2 * q; b[q] = o * kP1BPitch + ocol[q]; }
+        T x6[6][4];
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) x6[r][c] = t[orow[r] * kP1BPitch + ocol[c >> 1] + (c & 1)];
+        p1b_product<T, 6, 2>(x6, t, a, b);
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) xr[r][c] = x6[r][c];
+        nr = 6;
+        np = 2;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          if (r < nr && (c >> 1) < np) t[orow[r] * kP1BPitch + ocol[c >> 1] + (c & 1)] = xr[r][c];
+    }
+    __syncthreads();
+    // (c) the 9 other sub-blocks (t, u) <- min(., (t, s) (x) (s, u)): 16 x 16 threads of 6 rows x 3
+    //     column pairs; each output is read and written by its own thread only
+    {
+      const int ry = tid >> 4, cx = tid & 15;
+      int orow[6], ocol[3], a[6], b[3];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) { orow[r] = p1b_other(6 * ry + r, s); a[r] = orow[r] * kP1BPitch + o; }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) { ocol[q] = p1b_other(6 * cx + 2 * q, s); b[q] = o * kP1BPitch + ocol[q]; }
+      T x[6][6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) x[r][c] = t[orow[r] * kP1BPitch + ocol[c >> 1] + (c & 1)];
+      p1b_product<T, 6, 3>(x, t, a, b);
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) t[orow[r] * kP1BPitch + ocol[c >> 1] + (c & 1)] = x[r][c];
+    }
+    __syncthreads();
+  }
+  // strict improvements only: the changed elements and, TAG, their round
+  for (int e = tid; e < 128 * 128; e += 256) {
+    const int r = e >> 7, c = e & 127;
+    const T v = t[r * kP1BPitch + c];
+    if (v < ldg1<CG>(Dk + (int64_t)r * ld + c)) {
+      Dk[(int64_t)r * ld + c] = v;
+      if (MODE == MODE_TAG) P[(int64_t)(r0 + r) * ld + kb + c] = tag;
+    }
+  }
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256, 2)
+phase1_blocked_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  phase1_blocked_body<T, MODE>(D, P, ld, r0, kb, tag, *reinterpret_cast<P1BSmem<T> *>(smem_raw));
+}
+
 template <typename T, int BS, int MODE, int RY, int RX>
 __global__ void __launch_bounds__(P1Layout<BS, RY, RX>::kThreads, 2)   // half the register file: fits beside a phase-3 CTA
 phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {

@@ -78,6 +78,7 @@ struct PersistArgs {
   long long total;         // number of items
   unsigned long long timeout_ns;
   int sync_relaxed;        // dependency polls with relaxed loads (A/B option; see the kernel)
+  int p1_blocked;          // PLAIN / TAG phase 1 as the blocked closure (phase1_blocked_body)
   RankView rk[kMaxRanks];
 };
 
@@ -163,8 +164,10 @@ __device__ __forceinline__ void persist_phase1(const PersistArgs &a, const RankV
     phase1_key_f32_body<128, 8, 8, true>(D, v.P, a.ld, r0, kb, a.maxkey,
                                              *reinterpret_cast<P1Smem<float, 128> *>(smem));
   } else if constexpr (!is_key(MODE)) {
-    phase1_pair_body<T, 128, MODE, 8, 8, true>(D, v.P, a.ld, r0, kb, K,
-                                                  *reinterpret_cast<P1Smem<T, 128> *>(smem));
+    if (a.p1_blocked)
+      phase1_blocked_body<T, MODE, true>(D, v.P, a.ld, r0, kb, K, *reinterpret_cast<P1BSmem<T> *>(smem));
+    else
+      phase1_pair_body<T, 128, MODE, 8, 8, true>(D, v.P, a.ld, r0, kb, K, *reinterpret_cast<P1Smem<T, 128> *>(smem));
   } else {
     phase1_body<T, 128, MODE, kP1Side, true>(D, v.P, a.ld, r0, kb, K, a.maxkey,
                                              *reinterpret_cast<P1Smem<T, 128> *>(smem));
