@@ -427,6 +427,16 @@ int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int 
   // so the CTA fits beside a phase-3 CTA on one SM (the look-ahead starts it early)
   // 256 threads of (BS/16)^2 elements (512 threads of 8 x 4 or 4 x 8 at BS = 128 measured slower:
   // C2 TAG 39.6 -> 48.3 / 47.0 us, C4 keys 55.1 -> 59.9 / 58.0 us per round)
+  if constexpr (BS == 128 && is_key(MODE) && std::is_same<T, float>::value) {
+    if (g_p1_blocked) {   // FP32 keys: the blocked closure on keys
+      TRY(smem_attr((const void *)phase1_blocked_key_kernel, (int)sizeof(P1BSmem<float>)));
+      phase1_blocked_key_kernel<<<1, 256, sizeof(P1BSmem<float>), st>>>(reinterpret_cast<float *>(D), P, ld, r0,
+                                                                         kb, maxkey);
+      ++g_launches;
+      CU(cudaGetLastError());
+      return FW_OK;
+    }
+  }
   if constexpr (BS == 128 && !is_key(MODE)) {
     if (g_p1_blocked) {   // PLAIN / TAG: the blocked closure (4 sub-rounds of 32)
       auto kern = phase1_blocked_kernel<T, MODE>;

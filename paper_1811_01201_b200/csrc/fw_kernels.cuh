@@ -903,24 +903,153 @@ __device__ __forceinline__ void phase1_pair_body(T *__restrict__ D, int32_t *__r
     }
 }
 
+
+template <typename T, int BS, int MODE, int RY, int RX>
+__global__ void __launch_bounds__(P1Layout<BS, RY, RX>::kThreads, 2)   // half the register file: fits beside a phase-3 CTA
+phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {
+  __shared__ P1Smem<T, BS> sm;
+  phase1_pair_body<T, BS, MODE, RY, RX>(D, P, ld, r0, kb, tag, sm);
+}
+
+// Phase 1, FP32 keyed mode, without a per-relaxation select for P. The running value of
+// (a, b) is kept in the form  x = D*256 - 0.5  while unchanged, and a candidate through k is
+// the integer  c_k = D[a][k]*256 + k' + D[k][b]*256  (k' = (kb + k) & 255, increasing in k
+// inside a block): c_k < x  <=>  D[a][k] + D[k][b] < D (strict, P:125 / reading R2), and the
+// minimum over the sequence is the smallest distance reached first, with its k in the low 7
+// bits — the sequential strict-< result of the paper's loop, with one FADD + one FMNMX per
+// relaxation. Row k+1 is published as D*256 (B side), column k+1 as D*256 + k' (A side), both
+// recovered as floor((x + 0.5) / 256) * 256. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
+// core: the block at Dk (pitch ld), its P at Pk (pitch ldp); column / intermediate codes are
+// klow + local index (klow + BS <= 256), P values kgrp + code.
+template <int BS, int RY, int RX, bool CG = false>
+__device__ __forceinline__ void phase1_key_f32_core(float *__restrict__ Dk, int64_t ld, int32_t *__restrict__ Pk,
+                                                    int64_t ldp, int kgrp, int klow, int *maxkey,
+                                                    P1Smem<float, BS> &sm) {
+  using L = P1Layout<BS, RY, RX>;
+  float (*rowb)[2][BS] = sm.rowb;   // rows k, k+1, B form D*256  (pair parity)
+  float2 (*colb)[BS] = sm.colb;     // (column k, column k+1) per row, A form D*256 + k'
+  const int tx = threadIdx.x % L::NX, ty = threadIdx.x / L::NX;
+  float x[RY][RX];
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    float key[RX];
+    ldg_vec<float, RX, CG>(key, Dk + (int64_t)(RY * ty + r) * ld + RX * tx);  // D*256 + ((kb+b)&255) or +inf
+#pragma unroll
+    for (int c = 0; c < RX; ++c) x[r][c] = key[c] - (float)(klow + RX * tx + c) - 0.5f;   // D*256 - 0.5
+  }
+  // steps k and k+1 per barrier (the sequential loop's values, two steps at a time): every
+  // thread brings row / column k+1 to their state after step k itself,
+  //   col'[a] = min(col_k1[a], col_k[a] + D[k][k+1]*256 + 1)   ((k+1)' = k' + 1 inside the block)
+  //   row'[b] = min(row_k1[b], D[k+1][k]*256 + row_k[b])
+  // and folds both candidates into x with FADD2 + FMNMX3: x = min(x, c_k, c'_k+1) (min is exact,
+  // every candidate is the same integer sum as in the one-step loop).
+  if (ty == 0) {
+#pragma unroll
+    for (int c = 0; c < RX; ++c) {
+      rowb[0][0][RX * tx + c] = x[0][c] + 0.5f;                           // D*256
+      rowb[0][1][RX * tx + c] = x[1][c] + 0.5f;
+    }
+  }
+  if (tx == 0) {
+#pragma unroll
+    for (int r = 0; r < RY; ++r)                                          // + k'
+      colb[0][RY * ty + r] = make_float2(x[r][0] + 0.5f + (float)klow, x[r][1] + 0.5f + (float)(klow + 1));
+  }
+  __syncthreads();
+  for (int k0 = 0; k0 < BS; k0 += L::U) {
+#pragma unroll
+    for (int kr = 0; kr < L::U; kr += 2) {
+      const int k = k0 + kr, buf = (k >> 1) & 1;
+      float rk[RX], rk1[RX];
+      lds_vec<float, RX>(rk, &rowb[buf][0][RX * tx]);    // B side, own cols
+      lds_vec<float, RX>(rk1, &rowb[buf][1][RX * tx]);
+      const float d01 = rowb[buf][0][k + 1] + 1.0f;              // D[k][k+1]*256 + 1
+      const float d10 = colb[buf][k + 1].x - (float)(klow + k);  // D[k+1][k]*256 (exact; inf stays)
+#pragma unroll
+      for (int c = 0; c < RX; ++c) rk1[c] = fminf(rk1[c], d10 + rk[c]);
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const float2 ca = colb[buf][RY * ty + r];                // A side, own row (broadcast)
+        const float ck1 = fminf(ca.y, ca.x + d01);
+#pragma unroll
+        for (int c = 0; c < RX; c += 2)
+          relax_pair2(x[r][c], x[r][c + 1], ca.x, ck1, rk[c], rk[c + 1], rk1[c], rk1[c + 1]);
+      }
+      // publish rows / columns k+2 and k+3 (slots of one owner: k+2 is even)
+      if (k + 2 < BS) {
+        if ((k + 2) / RY == ty) {
+          const int s2 = (kr + 2) % RY, s3 = (kr + 3) % RY;
+#pragma unroll
+          for (int c = 0; c < RX; ++c) {
+            rowb[buf ^ 1][0][RX * tx + c] = floorf((x[s2][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
+            rowb[buf ^ 1][1][RX * tx + c] = floorf((x[s3][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
+          }
+        }
+        if ((k + 2) / RX == tx) {
+          const int s2 = (kr + 2) % RX, s3 = (kr + 3) % RX;
+          const float kp = (float)(klow + k + 2);
+#pragma unroll
+          for (int r = 0; r < RY; ++r)
+            colb[buf ^ 1][RY * ty + r] = make_float2(floorf((x[r][s2] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp,
+                                                     floorf((x[r][s3] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp + 1.0f);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int kmax = 0;
+#pragma unroll
+  for (int r = 0; r < RY; ++r)
+#pragma unroll
+    for (int c = 0; c < RX; ++c) {
+      const float v = x[r][c];
+      if (v < __int_as_float(0x7f800000) && v == floorf(v)) {   // an integer: strictly improved
+        const int a = RY * ty + r, b = RX * tx + c;
+        const float hi = floorf(v * (1.0f / kKeyMul)) * (float)kKeyMul;
+        const int kk = (int)(v - hi);
+        const float key = hi + (float)(klow + b);
+        Dk[(int64_t)a * ld + b] = key;
+        Pk[(int64_t)a * ldp + b] = kgrp + kk;
+        kmax = max(kmax, __float_as_int(key));
+      }
+    }
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if ((threadIdx.x & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
+}
+
+template <int BS, int RY, int RX, bool CG = false>
+__device__ __forceinline__ void phase1_key_f32_body(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld,
+                                                    int r0, int kb, int *maxkey, P1Smem<float, BS> &sm) {
+  phase1_key_f32_core<BS, RY, RX, CG>(D + (int64_t)r0 * ld + kb, ld, P + (int64_t)r0 * ld + kb, ld, kb & ~kKeyMask,
+                                      kb & kKeyMask, maxkey, sm);
+}
+
+template <int BS, int RY, int RX>
+__global__ void __launch_bounds__(P1Layout<BS, RY, RX>::kThreads, 2)   // half the register file: fits beside a phase-3 CTA
+phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
+                      int *maxkey) {
+  __shared__ P1Smem<float, BS> sm;
+  phase1_key_f32_body<BS, RY, RX>(D, P, ld, r0, kb, maxkey, sm);
+}
+
 // ---------------------------------------------------------------------------------
 // Phase 1, blocked (PLAIN / TAG, BS = 128, 256 threads): the closure of D_KK computed as the
 // paper's own blocked Floyd–Warshall one level down (P:101-112 applied to the 128 x 128 block
 // with 32 x 32 sub-blocks), instead of 128 sequential steps of the whole CTA. For each
 // sub-round s of 4:
-//   (a) closure of the diagonal sub-block (s, s): ONE warp, lane a holding row a in registers,
-//       two steps per __syncwarp (rows k, k+1 published through shared memory; the pair-step
-//       algebra of phase1_pair_body) — 16 warp-level syncs instead of 64 CTA barriers;
+//   (a) closure of the diagonal sub-block (s, s): phase1_pair_body on the 32 x 32 sub-block in
+//       shared memory (256 threads of 2 x 2, 16 barriers);
 //   (b) the row / column sub-strips (s, t), (t, s) as min-plus products with the closed
 //       sub-block (reading R7): 128 threads each;
 //   (c) the other 9 sub-blocks (t, u) <- min(., (t, s) (x) (s, u)): 256 threads of 6 x 6.
 // Same distances as the sequential loop (R7, R8: min is exact, every candidate one rounded
 // add). The 128 x 128 block lives in shared memory (pitch 132: conflict-free 16-B row reads
-// by consecutive lanes), 68 KB: one CTA still fits beside a phase-3 CTA.
+// by consecutive lanes), 69 KB: one CTA still fits beside a phase-3 CTA.
 constexpr int kP1BPitch = 132;
 template <typename T> struct P1BSmem {
   __align__(16) T t[128 * kP1BPitch];
-  __align__(16) T rb[2][2][32];   // sub-phase (a): rows k, k+1 by pair parity
+  __align__(16) T rb[2][2][32];   // sub-phase (a), keyed: rows k, k+1 by pair parity
+  P1Smem<T, 32> p1;               // sub-phase (a), plain: the pair-step body on the sub-block
 };
 
 // x[r][2p + e] = min(x, min_k A(r, k) + B(k, 2p + e)) over 32 k: A rows at a[r] (k contiguous),
@@ -964,7 +1093,7 @@ __device__ __forceinline__ void phase1_blocked_body(T *__restrict__ D, int32_t *
   static_assert(!is_key(MODE), "plain distances / round tags");
   using V = typename Vec4<T>::V;
   T *t = sm.t;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   T *Dk = D + (int64_t)r0 * ld + kb;
   for (int e = tid; e < 128 * 32; e += 256) {   // the block into shared memory (16-B loads)
     const int r = e >> 5, c4 = (e & 31) * 4;
@@ -976,51 +1105,10 @@ __device__ __forceinline__ void phase1_blocked_body(T *__restrict__ D, int32_t *
   __syncthreads();
   for (int s = 0; s < 4; ++s) {
     const int o = s * 32;
-    // (a) closure of sub-block (s, s) by warp 0: lane a holds row a
-    if (warp == 0) {
-      T x[32];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const V v = *reinterpret_cast<const V *>(t + (o + lane) * kP1BPitch + o + 4 * q);
-        x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
-      }
-      if (lane < 2) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) sm.rb[0][lane][c] = x[c];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 32; k += 2) {
-        const int pb = (k >> 1) & 1;
-        T rk[32], rk1[32];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const V v0 = *reinterpret_cast<const V *>(&sm.rb[pb][0][4 * q]);
-          const V v1 = *reinterpret_cast<const V *>(&sm.rb[pb][1][4 * q]);
-          rk[4 * q] = v0.x; rk[4 * q + 1] = v0.y; rk[4 * q + 2] = v0.z; rk[4 * q + 3] = v0.w;
-          rk1[4 * q] = v1.x; rk1[4 * q + 1] = v1.y; rk1[4 * q + 2] = v1.z; rk1[4 * q + 3] = v1.w;
-        }
-        const T d01 = rk[k + 1], d10 = rk1[k];   // S[k][k+1], S[k+1][k]
-#pragma unroll
-        for (int c = 0; c < 32; ++c) rk1[c] = tmin(rk1[c], d10 + rk[c]);   // row k+1 after step k
-        const T ak = x[k], ak1 = tmin(x[k + 1], x[k] + d01);             // own column k, k+1
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) relax_pair2(x[c], x[c + 1], ak, ak1, rk[c], rk[c + 1], rk1[c], rk1[c + 1]);
-        if (k + 2 < 32) {
-          if (lane == k + 2 || lane == k + 3) {
-#pragma unroll
-            for (int c = 0; c < 32; ++c) sm.rb[pb ^ 1][lane - k - 2][c] = x[c];
-          }
-          __syncwarp();
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        V v;
-        v.x = x[4 * q]; v.y = x[4 * q + 1]; v.z = x[4 * q + 2]; v.w = x[4 * q + 3];
-        *reinterpret_cast<V *>(t + (o + lane) * kP1BPitch + o + 4 * q) = v;
-      }
-    }
+    // (a) closure of sub-block (s, s): the two-steps-per-barrier body on the 32 x 32 sub-block in
+    //     shared memory, 256 threads of 2 x 2 (16 barriers; one warp alone measured 64 us per
+    //     phase 1 against 40 for the unblocked kernel — every latency exposed)
+    phase1_pair_body<T, 32, MODE_PLAIN, 2, 2, false>(t, nullptr, kP1BPitch, o, o, 0, sm.p1);
     __syncthreads();
     // (b) row sub-strips (s, t) = S* (x) (s, t) [threads 0..127: 4 rows x 3 column pairs] and
     //     column sub-strips (t, s) = (t, s) (x) S* [threads 128..255: 6 rows x 2 column pairs];
@@ -1108,131 +1196,138 @@ __device__ __forceinline__ void phase1_blocked_body(T *__restrict__ D, int32_t *
   }
 }
 
+// Phase 1, blocked, FP32 keyed mode (the stored values are keys D*256 + (column & 255), DESIGN.md
+// §4.3). (a) is phase1_key_f32_core (the select-free pair-step algebra: x = D*256 - 0.5 while
+// unchanged, a candidate through k the integer D[a][k]*256 + k' + D[k][b]*256) on the sub-block
+// in shared memory. (b) and (c) are products on the keys themselves: a candidate key sum is
+// (D_ak + D_kb)*256 + k' + b', so the minimum with the old key D_ab*256 + b' is the smallest
+// distance and, among ties, the smallest k, and it is below the old key iff strictly shorter
+// (the tile epilogue's rule). Every improvement writes P (its last write is the final value).
+template <bool CG = false>
+__device__ __forceinline__ void phase1_blocked_key_body(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld,
+                                                        int r0, int kb, int *maxkey, P1BSmem<float> &sm) {
+  float *t = sm.t;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int kgrp = kb & ~kKeyMask, klow = kb & kKeyMask;
+  float *Dk = D + (int64_t)r0 * ld + kb;
+  int32_t *Pk = P + (int64_t)r0 * ld + kb;
+  int kmax = 0;
+  for (int e = tid; e < 128 * 32; e += 256) {
+    const int r = e >> 5, c4 = (e & 31) * 4;
+    float4 v;
+    if constexpr (CG) v = __ldcg(reinterpret_cast<const float4 *>(Dk + (int64_t)r * ld + c4));
+    else v = *reinterpret_cast<const float4 *>(Dk + (int64_t)r * ld + c4);
+    *reinterpret_cast<float4 *>(t + r * kP1BPitch + c4) = v;
+  }
+  __syncthreads();
+  // keyed epilogue of one product output (row, col of the tile): store the new key, record P
+  auto settle = [&](int row, int col, float m) {
+    const float old = t[row * kP1BPitch + col];
+    if (m < old) {
+      const int kk = ((int)(m - (float)(klow + col))) & kKeyMask;   // the arg-min's k code
+      const float key = m - (float)kk;
+      t[row * kP1BPitch + col] = key;
+      Pk[(int64_t)row * ld + col] = kgrp + kk;
+      kmax = max(kmax, __float_as_int(key));
+    }
+  };
+  for (int s = 0; s < 4; ++s) {
+    const int o = s * 32;
+    // (a): the select-free keyed pair-step body on the 32 x 32 sub-block in shared memory, 256
+    //     threads of 2 x 2; codes klow + o + local index, P into the block's rows in global memory
+    phase1_key_f32_core<32, 2, 2, false>(t + o * kP1BPitch + o, kP1BPitch, Pk + (int64_t)o * ld + o, ld, kgrp,
+                                         klow + o, maxkey, sm.p1);
+    __syncthreads();
+    {   // (b) row sub-strips [threads 0..127: 4 rows x 3 column pairs], column sub-strips [6 x 2]
+      float xr[6][6];
+      int nr = 0, np = 0, orow[6], ocol[3];
+      if (tid < 128) {
+        const int ry = tid >> 4, cx = tid & 15;
+        int a[4], b[3];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) { orow[r] = o + 4 * ry + r; a[r] = orow[r] * kP1BPitch + o; }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { ocol[q] = p1b_other(6 * cx + 2 * q, s); b[q] = o * kP1BPitch + ocol[q]; }
+        float x4[4][6];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) x4[r][c] = t[orow[r] * kP1BPitch + ocol[c >> 1] + (c & 1)];
+        p1b_product<float, 4, 3>(x4, t, a, b);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) xr[r][c] = x4[r][c];
+        nr = 4;
+        np = 3;
+      } else {
+        const int u = tid - 128, ry = u >> 3, cx = u & 7;
+        int a[6], b[2];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) { orow[r] = p1b_other(6 * ry + r, s); a[r] = orow[r] * kP1BPitch + o; }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) { ocol[q] = o + 4 * cx + 2 * q; b[q] = o * kP1BPitch + ocol[q]; }
+        float x6[6][4];
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) x6[r][c] = t[orow[r] * kP1BPitch + ocol[c >> 1] + (c & 1)];
+        p1b_product<float, 6, 2>(x6, t, a, b);
+#pragma unroll
+        for (int r = 0; r < 6; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) xr[r][c] = x6[r][c];
+        nr = 6;
+        np = 2;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          if (r < nr && (c >> 1) < np) settle(orow[r], ocol[c >> 1] + (c & 1), xr[r][c]);
+    }
+    __syncthreads();
+    {   // (c) the other 9 sub-blocks
+      const int ry = tid >> 4, cx = tid & 15;
+      int orow[6], ocol[3], a[6], b[3];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) { orow[r] = p1b_other(6 * ry + r, s); a[r] = orow[r] * kP1BPitch + o; }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) { ocol[q] = p1b_other(6 * cx + 2 * q, s); b[q] = o * kP1BPitch + ocol[q]; }
+      float x[6][6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) x[r][c] = t[orow[r] * kP1BPitch + ocol[c >> 1] + (c & 1)];
+      p1b_product<float, 6, 3>(x, t, a, b);
+#pragma unroll
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) settle(orow[r], ocol[c >> 1] + (c & 1), x[r][c]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < 128 * 128; e += 256) {   // the improved keys (P was written on the way)
+    const int r = e >> 7, c = e & 127;
+    const float v = t[r * kP1BPitch + c];
+    if (v < ldg1<CG>(Dk + (int64_t)r * ld + c)) Dk[(int64_t)r * ld + c] = v;
+  }
+  kmax = __reduce_max_sync(0xffffffffu, kmax);
+  if (lane == 0 && kmax > 0) atomicMax(maxkey, kmax);
+}
+
+__global__ void __launch_bounds__(256, 2)
+phase1_blocked_key_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int *maxkey) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  phase1_blocked_key_body(D, P, ld, r0, kb, maxkey, *reinterpret_cast<P1BSmem<float> *>(smem_raw));
+}
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256, 2)
 phase1_blocked_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   phase1_blocked_body<T, MODE>(D, P, ld, r0, kb, tag, *reinterpret_cast<P1BSmem<T> *>(smem_raw));
-}
-
-template <typename T, int BS, int MODE, int RY, int RX>
-__global__ void __launch_bounds__(P1Layout<BS, RY, RX>::kThreads, 2)   // half the register file: fits beside a phase-3 CTA
-phase1_pair_kernel(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb, int tag) {
-  __shared__ P1Smem<T, BS> sm;
-  phase1_pair_body<T, BS, MODE, RY, RX>(D, P, ld, r0, kb, tag, sm);
-}
-
-// Phase 1, FP32 keyed mode, without a per-relaxation select for P. The running value of
-// (a, b) is kept in the form  x = D*256 - 0.5  while unchanged, and a candidate through k is
-// the integer  c_k = D[a][k]*256 + k' + D[k][b]*256  (k' = (kb + k) & 255, increasing in k
-// inside a block): c_k < x  <=>  D[a][k] + D[k][b] < D (strict, P:125 / reading R2), and the
-// minimum over the sequence is the smallest distance reached first, with its k in the low 7
-// bits — the sequential strict-< result of the paper's loop, with one FADD + one FMNMX per
-// relaxation. Row k+1 is published as D*256 (B side), column k+1 as D*256 + k' (A side), both
-// recovered as floor((x + 0.5) / 256) * 256. Exact: keys < 2^23 (kKeyMaxF32), half-integers.
-template <int BS, int RY, int RX, bool CG = false>
-__device__ __forceinline__ void phase1_key_f32_body(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld,
-                                                    int r0, int kb, int *maxkey, P1Smem<float, BS> &sm) {
-  using L = P1Layout<BS, RY, RX>;
-  float (*rowb)[2][BS] = sm.rowb;   // rows k, k+1, B form D*256  (pair parity)
-  float2 (*colb)[BS] = sm.colb;     // (column k, column k+1) per row, A form D*256 + k'
-  const int tx = threadIdx.x % L::NX, ty = threadIdx.x / L::NX;
-  float *Dk = D + (int64_t)r0 * ld + kb;
-  const int kgrp = kb & ~kKeyMask, klow = kb & kKeyMask;
-  float x[RY][RX];
-#pragma unroll
-  for (int r = 0; r < RY; ++r) {
-    float key[RX];
-    ldg_vec<float, RX, CG>(key, Dk + (int64_t)(RY * ty + r) * ld + RX * tx);  // D*256 + ((kb+b)&255) or +inf
-#pragma unroll
-    for (int c = 0; c < RX; ++c) x[r][c] = key[c] - (float)(klow + RX * tx + c) - 0.5f;   // D*256 - 0.5
-  }
-  // steps k and k+1 per barrier (the sequential loop's values, two steps at a time): every
-  // thread brings row / column k+1 to their state after step k itself,
-  //   col'[a] = min(col_k1[a], col_k[a] + D[k][k+1]*256 + 1)   ((k+1)' = k' + 1 inside the block)
-  //   row'[b] = min(row_k1[b], D[k+1][k]*256 + row_k[b])
-  // and folds both candidates into x with FADD2 + FMNMX3: x = min(x, c_k, c'_k+1) (min is exact,
-  // every candidate is the same integer sum as in the one-step loop).
-  if (ty == 0) {
-#pragma unroll
-    for (int c = 0; c < RX; ++c) {
-      rowb[0][0][RX * tx + c] = x[0][c] + 0.5f;                           // D*256
-      rowb[0][1][RX * tx + c] = x[1][c] + 0.5f;
-    }
-  }
-  if (tx == 0) {
-#pragma unroll
-    for (int r = 0; r < RY; ++r)                                          // + k'
-      colb[0][RY * ty + r] = make_float2(x[r][0] + 0.5f + (float)klow, x[r][1] + 0.5f + (float)(klow + 1));
-  }
-  __syncthreads();
-  for (int k0 = 0; k0 < BS; k0 += L::U) {
-#pragma unroll
-    for (int kr = 0; kr < L::U; kr += 2) {
-      const int k = k0 + kr, buf = (k >> 1) & 1;
-      float rk[RX], rk1[RX];
-      lds_vec<float, RX>(rk, &rowb[buf][0][RX * tx]);    // B side, own cols
-      lds_vec<float, RX>(rk1, &rowb[buf][1][RX * tx]);
-      const float d01 = rowb[buf][0][k + 1] + 1.0f;              // D[k][k+1]*256 + 1
-      const float d10 = colb[buf][k + 1].x - (float)(klow + k);  // D[k+1][k]*256 (exact; inf stays)
-#pragma unroll
-      for (int c = 0; c < RX; ++c) rk1[c] = fminf(rk1[c], d10 + rk[c]);
-#pragma unroll
-      for (int r = 0; r < RY; ++r) {
-        const float2 ca = colb[buf][RY * ty + r];                // A side, own row (broadcast)
-        const float ck1 = fminf(ca.y, ca.x + d01);
-#pragma unroll
-        for (int c = 0; c < RX; c += 2)
-          relax_pair2(x[r][c], x[r][c + 1], ca.x, ck1, rk[c], rk[c + 1], rk1[c], rk1[c + 1]);
-      }
-      // publish rows / columns k+2 and k+3 (slots of one owner: k+2 is even)
-      if (k + 2 < BS) {
-        if ((k + 2) / RY == ty) {
-          const int s2 = (kr + 2) % RY, s3 = (kr + 3) % RY;
-#pragma unroll
-          for (int c = 0; c < RX; ++c) {
-            rowb[buf ^ 1][0][RX * tx + c] = floorf((x[s2][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
-            rowb[buf ^ 1][1][RX * tx + c] = floorf((x[s3][c] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul;
-          }
-        }
-        if ((k + 2) / RX == tx) {
-          const int s2 = (kr + 2) % RX, s3 = (kr + 3) % RX;
-          const float kp = (float)(klow + k + 2);
-#pragma unroll
-          for (int r = 0; r < RY; ++r)
-            colb[buf ^ 1][RY * ty + r] = make_float2(floorf((x[r][s2] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp,
-                                                     floorf((x[r][s3] + 0.5f) * (1.0f / kKeyMul)) * (float)kKeyMul + kp + 1.0f);
-        }
-      }
-      __syncthreads();
-    }
-  }
-  int kmax = 0;
-#pragma unroll
-  for (int r = 0; r < RY; ++r)
-#pragma unroll
-    for (int c = 0; c < RX; ++c) {
-      const float v = x[r][c];
-      if (v < __int_as_float(0x7f800000) && v == floorf(v)) {   // an integer: strictly improved
-        const int a = RY * ty + r, b = RX * tx + c;
-        const float hi = floorf(v * (1.0f / kKeyMul)) * (float)kKeyMul;
-        const int kk = (int)(v - hi);
-        const float key = hi + (float)(klow + b);
-        Dk[(int64_t)a * ld + b] = key;
-        P[(int64_t)(r0 + a) * ld + kb + b] = kgrp + kk;
-        kmax = max(kmax, __float_as_int(key));
-      }
-    }
-  kmax = __reduce_max_sync(0xffffffffu, kmax);
-  if ((threadIdx.x & 31) == 0 && kmax > 0) atomicMax(maxkey, kmax);
-}
-
-template <int BS, int RY, int RX>
-__global__ void __launch_bounds__(P1Layout<BS, RY, RX>::kThreads, 2)   // half the register file: fits beside a phase-3 CTA
-phase1_key_f32_kernel(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int r0, int kb,
-                      int *maxkey) {
-  __shared__ P1Smem<float, BS> sm;
-  phase1_key_f32_body<BS, RY, RX>(D, P, ld, r0, kb, maxkey, sm);
 }
 
 // ---------------------------------------------------------------------------------

@@ -161,8 +161,10 @@ __device__ __forceinline__ void persist_phase1(const PersistArgs &a, const RankV
   T *D = static_cast<T *>(v.D);
   const int kb = K * 128, r0 = (int)(kb - v.row0);
   if constexpr (std::is_same<T, float>::value && is_key(MODE)) {
-    phase1_key_f32_body<128, 8, 8, true>(D, v.P, a.ld, r0, kb, a.maxkey,
-                                             *reinterpret_cast<P1Smem<float, 128> *>(smem));
+    if (a.p1_blocked)
+      phase1_blocked_key_body<true>(D, v.P, a.ld, r0, kb, a.maxkey, *reinterpret_cast<P1BSmem<float> *>(smem));
+    else
+      phase1_key_f32_body<128, 8, 8, true>(D, v.P, a.ld, r0, kb, a.maxkey, *reinterpret_cast<P1Smem<float, 128> *>(smem));
   } else if constexpr (!is_key(MODE)) {
     if (a.p1_blocked)
       phase1_blocked_body<T, MODE, true>(D, v.P, a.ld, r0, kb, K, *reinterpret_cast<P1BSmem<T> *>(smem));
