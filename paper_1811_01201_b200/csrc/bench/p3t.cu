@@ -11,6 +11,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <vector>
+#include <stdlib.h>
 #include "../fw_kernels.cuh"
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
@@ -48,7 +49,10 @@ constexpr int NS = 3, BK = 32, TM = 128, TN = 128;
 #endif
 constexpr int A_BYTES = TM * BK * 4, B_BYTES = BK * TN * 4, ST_BYTES = A_BYTES + B_BYTES;   // 16 + 16 KB
 
-// VAR: 1 = keyed epilogue with P (as the library's KEY mode)
+// VAR: 1 = keyed epilogue with P (as the library's KEY mode); 2 = round-2 scheme: thread 0 alone
+// waits on the stage's full mbarrier, then ONE __syncthreads per chunk (as the library's cp.async
+// pipeline) releases the stage and orders the reads (no empty barriers, no per-thread waits);
+// 4 = 128-B swizzled A reads (else dense 128-B rows, 2-way bank conflicts on the A loads)
 template <int VAR>
 __global__ void __launch_bounds__(256, 2)
 p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUtensorMap mapA,
@@ -70,7 +74,7 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
   }
   __syncthreads();
   if (tid == 0) {
-    for (int s = 0; s < NS && s < nch; ++s) {
+    for (int s = 0; s < ((VAR & 2) ? NS - 1 : NS) && s < nch; ++s) {
       mbar_expect_tx(&full[s], ST_BYTES);
       tma_2d(sm + s * ST_BYTES, &mapA, kb + s * BK, i0, &full[s]);
       tma_2d(sm + s * ST_BYTES + A_BYTES, &mapB, j0, kb + s * BK, &full[s]);
@@ -82,10 +86,22 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[r][c] = __int_as_float(0x7f800000);
   const int sw = ty & 7;   // 128-B swizzle: 16-B chunk q of row r sits at chunk q ^ (r & 7); r & 7 == ty & 7
-#pragma unroll
+#pragma unroll 1
   for (int ch = 0; ch < nch; ++ch) {
     const int s = ch % NS;
-    mbar_wait(&full[s], (ch / NS) & 1);
+    if (VAR & 2) {
+      if (tid == 0) mbar_wait(&full[s], (ch / NS) & 1);
+      __syncthreads();   // chunk ch visible to all; every warp is past chunk ch-1
+      if (tid == 0 && ch + NS - 1 < nch && ch >= 1) {   // refill the stage chunk ch-1 used
+        const int s2 = (ch + NS - 1) % NS;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&full[s2], ST_BYTES);
+        tma_2d(sm + s2 * ST_BYTES, &mapA, kb + (ch + NS - 1) * BK, i0, &full[s2]);
+        tma_2d(sm + s2 * ST_BYTES + A_BYTES, &mapB, j0, kb + (ch + NS - 1) * BK, &full[s2]);
+      }
+    } else {
+      mbar_wait(&full[s], (ch / NS) & 1);
+    }
     const unsigned char *as = sm + s * ST_BYTES + ty * 128;                 // row ty (+16 r)
     const float *bs = reinterpret_cast<const float *>(sm + s * ST_BYTES + A_BYTES) + tx * 4;
 #pragma unroll
@@ -97,7 +113,7 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
         for (int h = 0; h < 2; ++h) b[k][h] = *reinterpret_cast<const float4 *>(bs + (4 * q + k) * TN + 64 * h);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const float4 a = *reinterpret_cast<const float4 *>(as + r * 16 * 128 + (SWZ ? ((q ^ sw) << 4) : (q << 4)));
+        const float4 a = *reinterpret_cast<const float4 *>(as + r * 16 * 128 + ((VAR & 4) ? ((q ^ sw) << 4) : (q << 4)));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float *x = &acc[r][4 * h];
@@ -110,6 +126,7 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
         }
       }
     }
+    if (VAR & 2) continue;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (tid == 0 && ch + NS < nch) {   // refill this stage once every warp has released it
@@ -120,7 +137,7 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
     }
   }
   // epilogue (as the library's KEY mode)
-  const int kgrp = kb & ~127;
+  const int kgrp = kb & ~255;
   int kmax = 0;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
@@ -144,7 +161,7 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
           any = true;
           float key = m;
           if (VAR & 1) {
-            const int kk = (int)(m - (float)(j & 127)) & 127;
+            const int kk = (int)(m - (float)(j & 255)) & 255;
             key = m - (float)kk;
             kmax = max(kmax, __float_as_int(key));
             pv[e] = kgrp + kk;
@@ -191,17 +208,20 @@ int main() {
     for (int64_t j = 0; j < n; ++j) {
       x ^= x << 13; x ^= x >> 7; x ^= x << 17;
       const int w = i == j ? 0 : 1 + (int)(x % 100);
-      init[i * n + j] = (float)(w * 128 + (j & 127));
+      init[i * n + j] = (float)(w * 256 + (j & 255));
     }
   float *D, *D2; int32_t *P, *P2; int *mk;
   CK(cudaMalloc(&D, n * n * 4)); CK(cudaMalloc(&P, n * n * 4)); CK(cudaMalloc(&mk, 4));
   CK(cudaMalloc(&D2, n * n * 4)); CK(cudaMalloc(&P2, n * n * 4));
   const int kb = 128 * 50;
   CUtensorMap mA, mB;
-  if (make_map(&mA, D, n, BK, TM, SWZ ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE)) return 1;
+  const int var0 = getenv("P3T_VAR") ? atoi(getenv("P3T_VAR")) : 1;
+  if (make_map(&mA, D, n, BK, TM, (var0 & 4) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE)) return 1;
   if (make_map(&mB, D, n, TN, BK, CU_TENSOR_MAP_SWIZZLE_NONE)) return 1;
   const int bytes = NS * ST_BYTES + 1024 + 64;
-  auto kern = p3t<1>;
+  const int var = getenv("P3T_VAR") ? atoi(getenv("P3T_VAR")) : 1;
+  auto kern = var == 3 ? p3t<3> : var == 7 ? p3t<7> : var == 5 ? p3t<5> : p3t<1>;
+  if ((var & 4) != (SWZ ? 4 : 0) && (var & 4)) { printf("build with -DSWZ=1 for VAR & 4\n"); }
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   cudaFuncAttributes fa; CK(cudaFuncGetAttributes(&fa, kern));
   int occ = 0; CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, bytes));
@@ -252,7 +272,7 @@ int main() {
       CK(cudaEventSynchronize(e1));
       float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
       printf("{\"variant\": \"%s\", \"regs\": %d, \"spill\": %d, \"occ\": %d, \"ms\": %.4f, \"relax_per_clk_sm_at_max_clock\": %.2f}\n",
-             which == 0 ? "tma-3st" : "library", which == 0 ? fa.numRegs : fl.numRegs,
+             which == 0 ? (var == 1 ? "tma-3st-mbar" : var == 3 ? "tma-3st-1wait-sync" : var == 7 ? "tma-3st-1wait-sync-swz" : "tma-3st-mbar-swz") : "library", which == 0 ? fa.numRegs : fl.numRegs,
              (int)(which == 0 ? fa.localSizeBytes : fl.localSizeBytes), which == 0 ? occ : 2, ms,
              relax / (ms * 1e-3) / (sms * (double)clk * 1e3));
       fflush(stdout);

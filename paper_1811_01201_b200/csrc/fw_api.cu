@@ -416,9 +416,12 @@ void put(TileArgs &a, int z, const Strip &s) {
   a.mc_lo[z] = s.mc_lo; a.mc_hi[z] = s.mc_hi; a.xrow[z] = s.xrow;
 }
 
-// phase 1 of PLAIN / TAG solves at BS = 128 as the blocked closure (env FW_P1_BLOCKED=0: the
-// 64 pair-steps of phase1_pair_kernel instead; A/B)
-int g_p1_blocked = 1;
+// phase 1 at BS = 128 as the blocked closure (phase1_blocked_body / _key_body): the persistent
+// kernel's phase-1 items use it by default (C2 persistent 6.49 -> 6.10 ms: the pair body spills
+// inside that kernel), the stream-ordered launches keep the pair-step kernels, which are faster
+// alone (isolated, per round: round tags 39.6 vs 41.9 us, FP32 keys 53.9 vs 61.7 us;
+// profiles/r02_p1_blocked_ab.jsonl). Env FW_P1_BLOCKED=0/1 forces either everywhere (A/B).
+int g_p1_blocked = -1;
 
 template <typename T, int BS, int MODE>
 int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int kb, int K,
@@ -428,7 +431,7 @@ int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int 
   // 256 threads of (BS/16)^2 elements (512 threads of 8 x 4 or 4 x 8 at BS = 128 measured slower:
   // C2 TAG 39.6 -> 48.3 / 47.0 us, C4 keys 55.1 -> 59.9 / 58.0 us per round)
   if constexpr (BS == 128 && is_key(MODE) && std::is_same<T, float>::value) {
-    if (g_p1_blocked) {   // FP32 keys: the blocked closure on keys
+    if (g_p1_blocked == 1) {   // FP32 keys: the blocked closure on keys
       TRY(smem_attr((const void *)phase1_blocked_key_kernel, (int)sizeof(P1BSmem<float>)));
       phase1_blocked_key_kernel<<<1, 256, sizeof(P1BSmem<float>), st>>>(reinterpret_cast<float *>(D), P, ld, r0,
                                                                          kb, maxkey);
@@ -438,7 +441,7 @@ int launch_phase1_bs(cudaStream_t st, T *D, int32_t *P, int64_t ld, int r0, int 
     }
   }
   if constexpr (BS == 128 && !is_key(MODE)) {
-    if (g_p1_blocked) {   // PLAIN / TAG: the blocked closure (4 sub-rounds of 32)
+    if (g_p1_blocked == 1) {   // PLAIN / TAG: the blocked closure (4 sub-rounds of 32)
       auto kern = phase1_blocked_kernel<T, MODE>;
       TRY(smem_attr((const void *)kern, (int)sizeof(P1BSmem<T>)));
       kern<<<1, 256, sizeof(P1BSmem<T>), st>>>(D, P, ld, r0, kb, K);
@@ -1062,7 +1065,7 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   a.total = W > 1 ? (long long)items.size() : 2LL * Tn - 1 + (long long)Tn * Tn * Tn;
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.sync_relaxed = c.persist_relaxed;
-  a.p1_blocked = g_p1_blocked;
+  a.p1_blocked = g_p1_blocked != 0;
   for (int r = 0; r < W; ++r) {
     a.rk[r] = views[r];
     a.rk[r].ver = reinterpret_cast<int *>(base + ver_off[r]);
