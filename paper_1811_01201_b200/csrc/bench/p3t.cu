@@ -47,7 +47,10 @@ constexpr int NS = 3, BK = 32, TM = 128, TN = 128;
 #ifndef SWZ
 #define SWZ 0
 #endif
-constexpr int A_BYTES = TM * BK * 4, B_BYTES = BK * TN * 4, ST_BYTES = A_BYTES + B_BYTES;   // 16 + 16 KB
+// A box: BK columns, or BK + 4 (VAR & 8: rows of 144 B, the library's conflict-free padded stride;
+// the 4 extra columns are loaded and ignored)
+constexpr int A_W = BK + 4;
+constexpr int A_BYTES = TM * A_W * 4, B_BYTES = BK * TN * 4, ST_BYTES = A_BYTES + B_BYTES;   // 18 + 16 KB
 
 // VAR: 1 = keyed epilogue with P (as the library's KEY mode); 2 = round-2 scheme: thread 0 alone
 // waits on the stage's full mbarrier, then ONE __syncthreads per chunk (as the library's cp.async
@@ -65,6 +68,11 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
   if ((i0 + TM > kb && i0 < kb + 128) || (j0 + TN > kb && j0 < kb + 128)) return;
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16, lane = tid & 31;
   constexpr int nch = 128 / BK;
+  constexpr unsigned TXB = ((VAR & 8) ? A_W : BK) * TM * 4 + B_BYTES;   // bytes one stage's TMA pair lands
+  if (VAR & 16) {   // warm L2 with the epilogue's tile, as the library kernel does
+    for (int l = tid; l < TM * 4; l += 256)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)(i0 + l / 4) * ld + j0 + (l % 4) * 32));
+  }
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
@@ -75,7 +83,7 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
   __syncthreads();
   if (tid == 0) {
     for (int s = 0; s < ((VAR & 2) ? NS - 1 : NS) && s < nch; ++s) {
-      mbar_expect_tx(&full[s], ST_BYTES);
+      mbar_expect_tx(&full[s], TXB);
       tma_2d(sm + s * ST_BYTES, &mapA, kb + s * BK, i0, &full[s]);
       tma_2d(sm + s * ST_BYTES + A_BYTES, &mapB, j0, kb + s * BK, &full[s]);
     }
@@ -92,17 +100,18 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
     if (VAR & 2) {
       if (tid == 0) mbar_wait(&full[s], (ch / NS) & 1);
       __syncthreads();   // chunk ch visible to all; every warp is past chunk ch-1
-      if (tid == 0 && ch + NS - 1 < nch && ch >= 1) {   // refill the stage chunk ch-1 used
+      if (tid == 0 && ch + NS - 1 < nch) {   // chunk ch+2 into the stage chunk ch-1 used (free at ch = 0)
         const int s2 = (ch + NS - 1) % NS;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&full[s2], ST_BYTES);
+        mbar_expect_tx(&full[s2], TXB);
         tma_2d(sm + s2 * ST_BYTES, &mapA, kb + (ch + NS - 1) * BK, i0, &full[s2]);
         tma_2d(sm + s2 * ST_BYTES + A_BYTES, &mapB, j0, kb + (ch + NS - 1) * BK, &full[s2]);
       }
     } else {
       mbar_wait(&full[s], (ch / NS) & 1);
     }
-    const unsigned char *as = sm + s * ST_BYTES + ty * 128;                 // row ty (+16 r)
+    constexpr int ARB = (VAR & 8) ? A_W * 4 : BK * 4;                        // A row pitch (bytes)
+    const unsigned char *as = sm + s * ST_BYTES + ty * ARB;                   // row ty (+16 r)
     const float *bs = reinterpret_cast<const float *>(sm + s * ST_BYTES + A_BYTES) + tx * 4;
 #pragma unroll
     for (int q = 0; q < BK / 4; ++q) {
@@ -113,7 +122,7 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
         for (int h = 0; h < 2; ++h) b[k][h] = *reinterpret_cast<const float4 *>(bs + (4 * q + k) * TN + 64 * h);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const float4 a = *reinterpret_cast<const float4 *>(as + r * 16 * 128 + ((VAR & 4) ? ((q ^ sw) << 4) : (q << 4)));
+        const float4 a = *reinterpret_cast<const float4 *>(as + r * 16 * ARB + ((VAR & 4) ? ((q ^ sw) << 4) : (q << 4)));
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float *x = &acc[r][4 * h];
@@ -131,7 +140,7 @@ p3t(float *__restrict__ D, int32_t *__restrict__ P, const __grid_constant__ CUte
     if (lane == 0) mbar_arrive(&empty[s]);
     if (tid == 0 && ch + NS < nch) {   // refill this stage once every warp has released it
       mbar_wait(&empty[s], (ch / NS) & 1);
-      mbar_expect_tx(&full[s], ST_BYTES);
+      mbar_expect_tx(&full[s], TXB);
       tma_2d(sm + s * ST_BYTES, &mapA, kb + (ch + NS) * BK, i0, &full[s]);
       tma_2d(sm + s * ST_BYTES + A_BYTES, &mapB, j0, kb + (ch + NS) * BK, &full[s]);
     }
@@ -216,11 +225,11 @@ int main() {
   const int kb = 128 * 50;
   CUtensorMap mA, mB;
   const int var0 = getenv("P3T_VAR") ? atoi(getenv("P3T_VAR")) : 1;
-  if (make_map(&mA, D, n, BK, TM, (var0 & 4) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE)) return 1;
+  if (make_map(&mA, D, n, (var0 & 8) ? A_W : BK, TM, (var0 & 4) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE)) return 1;
   if (make_map(&mB, D, n, TN, BK, CU_TENSOR_MAP_SWIZZLE_NONE)) return 1;
   const int bytes = NS * ST_BYTES + 1024 + 64;
   const int var = getenv("P3T_VAR") ? atoi(getenv("P3T_VAR")) : 1;
-  auto kern = var == 3 ? p3t<3> : var == 7 ? p3t<7> : var == 5 ? p3t<5> : p3t<1>;
+  auto kern = var == 3 ? p3t<3> : var == 19 ? p3t<19> : var == 11 ? p3t<11> : var == 7 ? p3t<7> : var == 5 ? p3t<5> : p3t<1>;
   if ((var & 4) != (SWZ ? 4 : 0) && (var & 4)) { printf("build with -DSWZ=1 for VAR & 4\n"); }
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   cudaFuncAttributes fa; CK(cudaFuncGetAttributes(&fa, kern));
@@ -250,7 +259,8 @@ int main() {
     CK(cudaMemcpy(q2.data(), P2, n * n * 4, cudaMemcpyDeviceToHost));
     int64_t bad = 0, changed = 0;
     for (int64_t e = 0; e < n * n; ++e) { bad += h1[e] != h2[e] || q1[e] != q2[e]; changed += h1[e] != init[e]; }
-    printf("{\"check\": \"tma vs library kernel\", \"mismatches\": %lld, \"changed\": %lld}\n", (long long)bad, (long long)changed);
+    printf("{\"check\": \"tma vs library kernel\", \"var\": %d, \"mismatches\": %lld, \"changed\": %lld}\n", var, (long long)bad, (long long)changed);
+    fflush(stdout);
   }
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int reps = 10;
@@ -272,7 +282,7 @@ int main() {
       CK(cudaEventSynchronize(e1));
       float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
       printf("{\"variant\": \"%s\", \"regs\": %d, \"spill\": %d, \"occ\": %d, \"ms\": %.4f, \"relax_per_clk_sm_at_max_clock\": %.2f}\n",
-             which == 0 ? (var == 1 ? "tma-3st-mbar" : var == 3 ? "tma-3st-1wait-sync" : var == 7 ? "tma-3st-1wait-sync-swz" : "tma-3st-mbar-swz") : "library", which == 0 ? fa.numRegs : fl.numRegs,
+             which == 0 ? (var == 1 ? "tma-3st-mbar" : var == 3 ? "tma-3st-1wait-sync" : var == 11 ? "tma-3st-1wait-sync-pad36" : var == 19 ? "tma-3st-1wait-sync-prefetch" : var == 7 ? "tma-3st-1wait-sync-swz" : "tma-3st-mbar-swz") : "library", which == 0 ? fa.numRegs : fl.numRegs,
              (int)(which == 0 ? fa.localSizeBytes : fl.localSizeBytes), which == 0 ? occ : 2, ms,
              relax / (ms * 1e-3) / (sms * (double)clk * 1e3));
       fflush(stdout);
