@@ -119,6 +119,16 @@ int fw_init(int ngpus_max, unsigned flags);
  *                        solves), 0 off, 1 on (env FW_PERSISTENT)
  *   "persist_gap" k >= 0 persistent: phase-3 tiles between phase 1 and phase 2 of the next
  *                        round in the work order (-1 auto)
+ *   "async"      0/1     fw_solve_device_* (one GPU) return as soon as the solve is enqueued on
+ *                        the caller's stream: no validation kernel and no host round trip, so a
+ *                        solve can be captured into a CUDA graph (after one warm-up solve of the
+ *                        same size has allocated the workspaces). The caller guarantees the
+ *                        domain (FP32: weights >= 0, no NaN; INT32: weights in [0, FW_INF_I32] and
+ *                        (n-1) * max weight < FW_INF_I32) — outside it the results are undefined
+ *                        instead of FW_EINVAL / FW_ERANGE. P comes from round tags (valid for every
+ *                        such input; D is bitwise the keyed solve's for integer data). Device-side
+ *                        failures (a dependency-wait timeout, non-converging next hops) are
+ *                        returned by the next fw_last_stats, which also waits for the solve
  * FW_ESTATE before fw_init; FW_EINVAL for an unknown name or value. */
 int fw_set_option(const char *name, int value);
 

@@ -173,6 +173,10 @@ struct Ctx {
   int persist_gap = -1;            // persistent: rest tiles between P1(K+1) and P2(K+1) (-1 auto)
   int persist_relaxed = 0;         // persistent: dependency polls with relaxed loads (A/B option)
   bool last_persist = false;       // the last solve ran as one persistent launch
+  bool async = false;              // device entry: no validation, no host synchronisation (fw_set_option)
+  bool in_host_entry = false;      // inside fw_solve / fw_solve_i32 (async never applies there)
+  bool pending = false;            // an async solve's stats are completed by fw_last_stats
+  cudaStream_t pending_st = nullptr;
   DevBuf ws_ver;                   // persistent: per-tile round counters, pub flags, work counter, items
   DevBuf ws_ring;                  // persistent: pivot-row ring(s) (n_pad^2 each) [+ pub flags, NCCL mode]
   DevBuf ws_ipc;                   // persistent NCCL mode: all-gathered IPC handles
@@ -1424,6 +1428,17 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
   // [0] flags [1] max weight [2] max key [3] placement status; [16..16+R) look-ahead counters
   int *d_flags = static_cast<int *>(c.scratch.p);
   CU(cudaMemsetAsync(d_flags, 0, 16, st));
+  c.pending = false;
+  if (c.async && tr == T_LOCAL && !c.in_host_entry) {
+    // asynchronous device solve: no validation and no host round trip — the caller guarantees
+    // the domain (fw.h). The round-tag plan is valid for every such input: FP32 data relax in
+    // FP32 (bitwise the keyed result for integer data: every sum of integers < 2^24 is exact),
+    // INT32 data in INT32; P through round tags and the post-pass.
+    std::vector<Attempt> plan{{want_p ? MODE_TAG : MODE_PLAIN, !int_t, true, 0}};
+    int h_flags[4] = {0, 0, 0, 0};
+    TRY(place_parts(c, parts, tr, n, BS, want_p, false, st));
+    return solve_placed<T>(c, parts, tr, world, n, BS, st, plan, d_flags, h_flags, bcasts0, bcast_bytes0);
+  }
   for (auto &p : parts) {
     if (p.nsrc == 0) continue;
     const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 16)),
@@ -1590,6 +1605,24 @@ int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, i
     }
   }
   CU(cudaEventRecord(e_end, st));
+  if (c.async && tr == T_LOCAL && !c.in_host_entry) {   // everything is enqueued: return without waiting
+    fw_stats s{};
+    s.n = n;
+    s.n_pad = n_pad;
+    s.block = BS;
+    s.rounds = R;
+    s.is_int = int_t;
+    s.path_mode = path_mode;
+    s.p_method = used.mode;
+    s.compute_f32 = (used.f32 || !int_t) ? 1 : 0;
+    s.persistent = c.last_persist ? 1 : 0;
+    s.kernel_launches = g_launches - launches0;
+    c.stats = s;
+    c.has_stats = true;
+    c.pending = true;
+    c.pending_st = st;
+    return FW_OK;
+  }
   CU(cudaMemcpyAsync(h_flags, d_flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
   TRY(sync_stream(c, st));
   if (h_flags[0] & 16)
@@ -2501,6 +2534,11 @@ int solve_host(T *dist, int32_t *next, int64_t n, int block, int ngpus) {
     return fail(FW_ESTATE, "a multi-GPU communicator is active: use fw_dist_solve_* or fw_comm_free");
   if (ngpus > 1) return solve_host_team<T>(c, dist, next, n, BS, ngpus);
   CU(cudaSetDevice(c.dev));
+  struct HostEntry {   // the asynchronous device mode never applies to the host entry points
+    Ctx &c;
+    explicit HostEntry(Ctx &x) : c(x) { c.in_host_entry = true; }
+    ~HostEntry() { c.in_host_entry = false; }
+  } host_entry(c);
   bool piped = false, raw_ready = false;
   TRY(solve_host_pipelined<T>(c, dist, next, n, BS, &piped, &raw_ready));
   if (piped) return FW_OK;
@@ -2616,6 +2654,7 @@ int fw_set_option(const char *name, int value) {
   else if (k == "persistent" && value >= -1 && value <= 1) c.persistent = value;
   else if (k == "persist_gap" && value >= -1) c.persist_gap = value;
   else if (k == "persist_relaxed" && (value == 0 || value == 1)) c.persist_relaxed = value;
+  else if (k == "async" && (value == 0 || value == 1)) c.async = value != 0;
   else return fail(FW_EINVAL, "unknown option or value: %s = %d", name, value);
   return FW_OK;
 }
@@ -2848,7 +2887,19 @@ const char *fw_last_error(void) { return g_err.c_str(); }
 int fw_last_stats(fw_stats *out) {
   if (!g_ctx || !g_ctx->has_stats) return fail(FW_ESTATE, "no solve has completed yet");
   if (!out) return fail(FW_EINVAL, "out is NULL");
-  *out = g_ctx->stats;
+  Ctx &c = *g_ctx;
+  if (c.pending) {   // an asynchronous solve: wait for it, then its time and device-side errors
+    c.pending = false;
+    CU(cudaEventSynchronize(c.events[1]));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, c.events[0], c.events[1]));
+    c.stats.solve_ms = ms;
+    int h[4] = {0, 0, 0, 0};
+    CU(cudaMemcpy(h, c.scratch.p, sizeof h, cudaMemcpyDeviceToHost));
+    if (h[0] & (16 | 32)) return fail(FW_ECUDA, "a dependency wait of the last (asynchronous) solve timed out");
+    if (h[0] & 8) return fail(FW_ERANGE, "next-hop resolution of the last (asynchronous) solve did not converge");
+  }
+  *out = c.stats;
   return FW_OK;
 }
 

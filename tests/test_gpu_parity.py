@@ -674,3 +674,55 @@ def test_persistent_ring_closed_form():
     i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
     np.testing.assert_array_equal(D.astype(np.int64), (j - i) % n)
     np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % n))
+
+
+# ---- asynchronous device solve (fw_set_option("async", 1)): no validation, no host round trip ----
+@pytest.mark.parametrize("kind,n", [("complete_int", 640), ("complete_real", 513), ("er_int", 700),
+                                    ("complete_int", 3000), ("complete_real", 4096)])
+def test_async_device_solve(kind, n):
+    """The asynchronous device entry returns once the solve is enqueued; after the stream is
+    synchronised D matches the oracle (bitwise for integer data) and P is valid; fw_last_stats
+    waits for the solve and reports its time."""
+    W = gen.generate(kind, n, 400 + n, p=0.02, lo=1, hi=1000 if kind.startswith("er") else 100)
+    with Ctx(0):
+        fw.fw_set_option("async", 1)
+        dD = torch.from_numpy(W).cuda()
+        dP = torch.empty(W.shape, dtype=torch.int32, device="cuda")
+        f = fw.fw_solve_device_i32 if W.dtype == np.int32 else fw.fw_solve_device_f32
+        s = torch.cuda.Stream()
+        f(dD, dP, block=0, stream=s)
+        s.synchronize()
+        st = fw.fw_last_stats()
+        D, P = dD.cpu().numpy(), dP.cpu().numpy()
+    assert st.solve_ms > 0 and st.p_method == 1
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5)
+    assert bad == 0, f"{bad} invalid paths, first at {divmod(first, n)}"
+
+
+@pytest.mark.parametrize("kind,n", [("complete_int", 1024), ("complete_real", 2048)])
+def test_async_solve_captured_in_cuda_graph(kind, n):
+    """With the workspaces allocated by a warm-up solve, an asynchronous solve captures into a
+    CUDA graph; replaying the graph on a fresh copy of the input gives the oracle's D."""
+    W = gen.generate(kind, n, 77 + n)
+    dW = torch.from_numpy(W).cuda()
+    dD = dW.clone()
+    dP = torch.empty(W.shape, dtype=torch.int32, device="cuda")
+    with Ctx(0):
+        fw.fw_set_option("async", 1)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            fw.fw_solve_device_f32(dD, dP, block=128, stream=s)   # warm-up: allocations, attributes
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+            dD.copy_(dW)
+            fw.fw_solve_device_f32(dD, dP, block=128, stream=s)
+        dD.fill_(0)
+        g.replay()
+        torch.cuda.synchronize()
+        D, P = dD.cpu().numpy(), dP.cpu().numpy()
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    assert oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5)[0] == 0
