@@ -726,3 +726,21 @@ def test_async_solve_captured_in_cuda_graph(kind, n):
     exact = exact_data(W)
     assert_D_matches(D, oracle.fw(W, None)[0], exact)
     assert oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5)[0] == 0
+
+
+@pytest.mark.parametrize("path", ["next", "lastk"])
+def test_persistent_int32_keys(path):
+    """Weights up to 100000 rule out FP32 keys (key range 32766) but not INT32 keys (2097150):
+    the persistent launch runs the INT32 keyed items (phase 1 with the per-step P select)."""
+    n = 600
+    W = gen.generate("er_int", n, 91, p=1.0, lo=1, hi=100000)
+    D = W.copy()
+    P = np.empty(W.shape, dtype=np.int32)
+    with Ctx(fw.FW_PATH_LAST_K if path == "lastk" else 0):
+        fw.fw_set_option("persistent", 1)
+        fw.fw_set_host_pipeline(0)
+        fw.fw_solve_i32(D, P, block=128)
+        s = fw.fw_last_stats()
+    assert s.persistent == 1 and s.p_method == 2 and s.compute_f32 == 0
+    np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
+    assert oracle.check_paths(W, D, P, mode=path)[0] == 0
