@@ -172,6 +172,7 @@ struct Ctx {
   int persistent = -1;             // one persistent launch per solve (fw_persist.cuh): -1 auto, 0 off, 1 on
   int persist_gap = -1;            // persistent: rest tiles between P1(K+1) and P2(K+1) (-1 auto)
   int persist_relaxed = 0;         // persistent: dependency polls with relaxed loads (A/B option)
+  int persist_quarters = 1;        // persistent, one GPU: critical-path tiles as 64 x 64 quarter items
   bool last_persist = false;       // the last solve ran as one persistent launch
   bool async = false;              // device entry: no validation, no host synchronisation (fw_set_option)
   bool in_host_entry = false;      // inside fw_solve / fw_solve_i32 (async never applies there)
@@ -1038,6 +1039,8 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
     pub_off[r] = off;
     if (W > 1 && self < 0) off += ((size_t)Tn * Tn * sizeof(int) + 255) / 256 * 256;
   }
+  const size_t qcnt_off = off;   // one GPU: per-tile count of finished quarter items
+  off += W == 1 ? ((size_t)Tn * Tn * sizeof(int) + 255) / 256 * 256 : 0;
   const size_t next_off = off;
   off += 256;
   const int gap = c.persist_gap >= 0 ? c.persist_gap : (int)(2.5 * grid);
@@ -1066,7 +1069,11 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   a.next = reinterpret_cast<unsigned long long *>(base + next_off);
   a.maxkey = maxkey;
   a.flags = maxkey - 2;
-  a.total = W > 1 ? (long long)items.size() : 2LL * Tn - 1 + (long long)Tn * Tn * Tn;
+  a.quarters = W == 1 && c.persist_quarters ? 1 : 0;
+  a.qcnt = reinterpret_cast<int *>(base + qcnt_off);
+  const int Q = a.quarters ? 4 : 1;
+  a.total = W > 1 ? (long long)items.size()
+                  : 1 + (long long)Q * 2 * (Tn - 1) + (long long)Tn * ((long long)Tn * Tn + (Q - 1) * (4LL * Tn - 5));
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.sync_relaxed = c.persist_relaxed;
   a.p1_blocked = g_p1_blocked != 0;
@@ -2655,6 +2662,7 @@ int fw_set_option(const char *name, int value) {
   else if (k == "persist_gap" && value >= -1) c.persist_gap = value;
   else if (k == "persist_relaxed" && (value == 0 || value == 1)) c.persist_relaxed = value;
   else if (k == "async" && (value == 0 || value == 1)) c.async = value != 0;
+  else if (k == "persist_quarters" && (value == 0 || value == 1)) c.persist_quarters = value;
   else return fail(FW_EINVAL, "unknown option or value: %s = %d", name, value);
   return FW_OK;
 }
@@ -2747,8 +2755,8 @@ int fw_host_pipeline_bounds(int64_t n, int chunk_tiles, int first_tiles, int32_t
 }
 
 int64_t fw_persist_schedule(int64_t n, int world, int rank, int gap, uint32_t *out, int64_t max_out) {
-  if (n <= 0 || n > 65536 || world < 1 || world > kMaxRanks || rank < -2 || rank >= world || gap < 0 ||
-      max_out < 0 || (max_out > 0 && !out) || (rank == -2 && world != 1))
+  if (n <= 0 || n > 65536 || world < 1 || world > kMaxRanks || rank < -3 || rank >= world || gap < 0 ||
+      max_out < 0 || (max_out > 0 && !out) || (rank <= -2 && world != 1))
     return -fail(FW_EINVAL, "fw_persist_schedule: bad arguments (n=%lld world=%d rank=%d gap=%d)", (long long)n, world,
                  rank, gap);
   const int64_t n_pad = (n + 127) / 128 * 128;
@@ -2761,14 +2769,17 @@ int64_t fw_persist_schedule(int64_t n, int world, int rank, int gap, uint32_t *o
     t1[r] = (int)((r0 + nr) / 128);
   }
   std::vector<unsigned> items;
-  if (rank == -2) {   // the one-GPU kernel's arithmetic decode (persist_decode), run on the host
+  if (rank <= -2) {   // the one-GPU kernel's arithmetic decode (persist_decode), run on the host;
+                      // -3: with quarter items (the quarter in the rank bits)
     PersistArgs a{};
     a.T = T;
     a.gap = gap;
-    const long long total = 2LL * T - 1 + (long long)T * T * T;
+    a.quarters = rank == -3;
+    const int Q = a.quarters ? 4 : 1;
+    const long long total = 1 + (long long)Q * 2 * (T - 1) + (long long)T * ((long long)T * T + (Q - 1) * (4LL * T - 5));
     for (long long it = 0; it < total; ++it) {
       const Item w = persist_decode(a, it);
-      if (w.type != IT_NONE) items.push_back(pack_item(0, w.type, w.K, w.I, w.J));
+      if (w.type != IT_NONE) items.push_back(pack_item(w.type == IT_QTILE ? w.r : 0, w.type, w.K, w.I, w.J));
     }
   } else {
     persist_items(T, world, t0, t1, rank, gap, &items);

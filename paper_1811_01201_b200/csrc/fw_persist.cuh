@@ -79,12 +79,14 @@ struct PersistArgs {
   unsigned long long timeout_ns;
   int sync_relaxed;        // dependency polls with relaxed loads (A/B option; see the kernel)
   int p1_blocked;          // PLAIN / TAG phase 1 as the blocked closure (phase1_blocked_body)
+  int quarters;            // one GPU: critical-path tiles as four 64 x 64 items (persist_decode)
+  int *qcnt;               // per-tile count of finished quarters (zeroed)
   RankView rk[kMaxRanks];
 };
 
-enum ItemType { IT_NONE = 0, IT_P1 = 1, IT_TILE = 2 };
+enum ItemType { IT_NONE = 0, IT_P1 = 1, IT_TILE = 2, IT_QTILE = 3 };
 struct Item {
-  int type, K, I, J, r;    // r: the rank whose rows hold tile (I, J)
+  int type, K, I, J, r;    // r: the rank whose rows hold tile (I, J); IT_QTILE: the quarter (0..3)
 };
 // packed item (host-built tables): rank 3 | type 2 | K 9 | I 9 | J 9 bits
 __host__ __device__ __forceinline__ unsigned pack_item(int r, int type, int K, int I, int J) {
@@ -94,20 +96,25 @@ __device__ __forceinline__ Item unpack_item(unsigned u) {
   return Item{(int)((u >> 27) & 3), (int)((u >> 18) & 511), (int)((u >> 9) & 511), (int)(u & 511), (int)(u >> 29)};
 }
 
-// Item `it` of the fixed order above.
+// Item `it` of the fixed order above (one GPU). With quarters (a.quarters = 1) every tile on
+// the per-round critical path — round K+1's phase-2 tiles and the round-K tiles its phase 1 and
+// phase 2 read (prio) — is split into four 64 x 64 items (quarter q: rows 64*(q>>1), columns
+// 64*(q&1) of the tile, all 128 k), taken back to back: the chain P2(K) -> prio(K) -> P1(K+1)
+// -> P2(K+1) then advances in quarter-tile steps, which at small n (C2) is the round's critical
+// path. A tile's round counter advances when its fourth quarter is done.
 __host__ __device__ __forceinline__ Item persist_decode(const PersistArgs &a, long long it) {
-  const int T = a.T;
+  const int T = a.T, Q = a.quarters ? 4 : 1, TQ = a.quarters ? IT_QTILE : IT_TILE;
   Item w{IT_NONE, 0, 0, 0, 0};
   if (it == 0) return Item{IT_P1, 0, 0, 0, 0};
-  const long long pre = 2LL * T - 1;              // P1(0) + the 2(T-1) phase-2 tiles of round 0
+  const long long pre = 1 + (long long)Q * 2 * (T - 1);   // P1(0) + the phase-2 tiles of round 0
   if (it < pre) {                                 // P2(0): row 0 (J = 1..T-1), column 0 (I = 1..T-1)
-    const int q = (int)(it - 1);
-    return q < T - 1 ? Item{IT_TILE, 0, 0, q + 1, 0} : Item{IT_TILE, 0, q - (T - 1) + 1, 0, 0};
+    const int q = (int)(it - 1), t = q / Q, qq = q % Q;
+    return t < T - 1 ? Item{TQ, 0, 0, t + 1, qq} : Item{TQ, 0, t - (T - 1) + 1, 0, qq};
   }
-  // T^3 + 2T < 2^31 for T <= 512 (n <= 65536): 32-bit division
-  const int t2 = T * T, r = (int)(it - pre);
-  const int K = r / t2;
-  int q = r - K * t2;
+  // (T^2 + 12 T) T + 8 T < 2^31 for T <= 512 (n <= 65536): 32-bit division
+  const int seg = T * T + (Q - 1) * (4 * T - 5), r = (int)(it - pre);
+  const int K = r / seg;
+  int q = r - K * seg;
   if (K >= T) return w;
   if (K == T - 1) {                               // last round: its phase-3 tiles, then no-ops
     const int m = T - 1;
@@ -115,22 +122,23 @@ __host__ __device__ __forceinline__ Item persist_decode(const PersistArgs &a, lo
     return Item{IT_TILE, K, skip2(q / m, K, -1), skip2(q % m, K, -1), 0};
   }
   const int N = K + 1;
-  if (q < T - 1) {                                // prio: row K+1, (K+1, K+1) first
-    return Item{IT_TILE, K, N, q == 0 ? N : skip2(q - 1, K, N), 0};
+  if (q < Q * (2 * T - 3)) {                      // prio: row K+1 ((K+1, K+1) first), column K+1
+    const int t = q / Q, qq = q % Q;
+    if (t < T - 1) return Item{TQ, K, N, t == 0 ? N : skip2(t - 1, K, N), qq};
+    return Item{TQ, K, skip2(t - (T - 1), K, N), N, qq};
   }
-  q -= T - 1;
-  if (q < T - 2) return Item{IT_TILE, K, skip2(q, K, N), N, 0};   // prio: column K+1
-  q -= T - 2;
+  q -= Q * (2 * T - 3);
   if (q == 0) return Item{IT_P1, N, N, N, 0};
   q -= 1;
   const int m = T - 2, rest = m * m;
   const int gap = a.gap < rest ? a.gap : rest;
   if (q < gap) return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N), 0};
   q -= gap;
-  if (q < 2 * (T - 1)) {                          // P2(K+1): row K+1, then column K+1
-    return q < T - 1 ? Item{IT_TILE, N, N, skip2(q, N, -1), 0} : Item{IT_TILE, N, skip2(q - (T - 1), N, -1), N, 0};
+  if (q < Q * 2 * (T - 1)) {                      // P2(K+1): row K+1, then column K+1
+    const int t = q / Q, qq = q % Q;
+    return t < T - 1 ? Item{TQ, N, N, skip2(t, N, -1), qq} : Item{TQ, N, skip2(t - (T - 1), N, -1), N, qq};
   }
-  q -= 2 * (T - 1);
+  q -= Q * 2 * (T - 1);
   q += gap;
   return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N), 0};
 }
@@ -243,6 +251,15 @@ fw_persistent_kernel(const PersistArgs a) {
         s_next = (long long)atomicAdd(a.next, 1ull);
         const Item w = a.items ? unpack_item(a.items[it]) : persist_decode(a, it);
         s_cur = w;
+        if (w.type == IT_QTILE) {   // one GPU: rows / columns 64 * (quarter bits) of tile (I, J)
+          const RankView &v = a.rk[0];
+          const T *Dv = static_cast<const T *>(v.D);
+          const int qi = (w.r >> 1) * 64, qj = (w.r & 1) * 64;
+          s_src.a = Dv + (int64_t)(w.I * 128 + qi) * a.ld + w.K * 128;
+          s_src.lda = a.ld;
+          s_src.b = Dv + (int64_t)w.K * 128 * a.ld + w.J * 128 + qj;
+          s_src.ldb = a.ld;
+        }
         if (w.type == IT_TILE) {   // A = (I, K) of this rank's rows; B = (K, J) in place or the ring
           const RankView &v = a.rk[w.r];
           const bool own_b = w.K >= v.t0 && w.K < v.t1;
@@ -261,7 +278,7 @@ fw_persistent_kernel(const PersistArgs a) {
     const Item w = s_cur;
     if (w.type < 0) break;
     if (w.type == IT_NONE) continue;
-    const RankView &v = a.rk[w.r];
+    const RankView &v = a.rk[w.type == IT_QTILE ? 0 : w.r];
     T *D = static_cast<T *>(v.D);
     const int li = w.I - v.t0;                      // local tile-row of the item's tile
     if (w.type == IT_TILE) {
@@ -305,6 +322,18 @@ fw_persistent_kernel(const PersistArgs a) {
     __syncthreads();
     if (w.type == IT_P1) {
       persist_phase1<T, MODE>(a, v, w.K, smem_raw);
+    } else if (w.type == IT_QTILE) {
+      using S64 = TileShape<64, 64>;
+      T acc[S64::RM][4 * S64::H];
+      tile_mainloop<T, 64, 64>(reinterpret_cast<T *>(smem_raw), &s_src, 128 / kBK, acc);
+      const Item e = s_cur;
+      int kmax = tile_epilogue<T, 64, 64, MODE, true>(D, a.rk[0].P, a.ld, e.I * 128 + (e.r >> 1) * 64,
+                                                      e.J * 128 + (e.r & 1) * 64, 0, 0, 0, 0, e.K,
+                                                      (e.K * 128) & ~kKeyMask, acc);
+      if (is_key(MODE)) {
+        kmax = __reduce_max_sync(0xffffffffu, kmax);
+        if ((tid & 31) == 0 && kmax > 0) atomicMax(a.maxkey, kmax);
+      }
     } else {
       T acc[S::RM][4 * S::H];
       tile_mainloop<T, 128, 128>(reinterpret_cast<T *>(smem_raw), &s_src, 128 / kBK, acc);
@@ -323,9 +352,14 @@ fw_persistent_kernel(const PersistArgs a) {
     const Item e = s_cur;
     if (a.world > 1 && e.I == e.K) persist_publish<T>(a, e.r, e.K, e.J);   // a final pivot-row tile
     if (tid == 0) {
-      const RankView &ve = a.rk[e.r];
+      const RankView &ve = a.rk[e.type == IT_QTILE ? 0 : e.r];
       int *vp = ve.ver + (int64_t)(e.I - ve.t0) * a.T + e.J;
-      asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(vp), "r"(e.K + 1) : "memory");
+      bool last = true;
+      if (e.type == IT_QTILE) {   // the tile is done for round K when its fourth quarter is
+        __threadfence();          // this quarter's stores before its count
+        last = (atomicAdd(a.qcnt + (int64_t)e.I * a.T + e.J, 1) & 3) == 3;
+      }
+      if (last) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(vp), "r"(e.K + 1) : "memory");
     }
   }
 }

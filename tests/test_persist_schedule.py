@@ -87,3 +87,25 @@ def test_one_gpu_decode_matches_table(n, gap):
     """The one-GPU persistent kernel decodes its items arithmetically (persist_decode); run on the
     host, that order is exactly the table order checked above (skipping the last round's no-ops)."""
     np.testing.assert_array_equal(fw.fw_persist_schedule(n, 1, -2, gap), fw.fw_persist_schedule(n, 1, -1, gap))
+
+
+@pytest.mark.parametrize("n,gap", [(256, 0), (700, 5), (1024, 40), (4096, 740)])
+def test_one_gpu_quarters_collapse_to_table(n, gap):
+    """With quarter items (the critical-path tiles of the one-GPU order as four 64 x 64 items),
+    every quartered tile appears as its four quarters back to back (quarters 0..3 in the rank
+    bits, type 3); collapsing them gives exactly the full-tile order."""
+    full = fw.fw_persist_schedule(n, 1, -1, gap)
+    q = fw.fw_persist_schedule(n, 1, -3, gap)
+    r, ty, K, I, J = unpack(q)
+    out, i = [], 0
+    while i < len(q):
+        if ty[i] == 3:
+            assert list(r[i:i + 4]) == [0, 1, 2, 3] and np.all(ty[i:i + 4] == 3)
+            assert len({(K[x], I[x], J[x]) for x in range(i, i + 4)}) == 1
+            out.append((2 << 27) | (int(K[i]) << 18) | (int(I[i]) << 9) | int(J[i]))
+            i += 4
+        else:
+            out.append(int(q[i]))
+            i += 1
+    np.testing.assert_array_equal(np.array(out, dtype=np.uint32), full)
+    assert np.sum(ty == 3) > 0
