@@ -254,6 +254,7 @@ def isolated_pivot_phases(fw, solve, dD, dW, dP, n, n_pad, BS, stream, peak_tflo
     library's per-phase CUDA events bracket each launch on an otherwise idle GPU."""
     fw.fw_set_option("lookahead", 0)
     fw.fw_set_option("pairs", 0)
+    fw.fw_set_option("persistent", 0)          # the stream schedule: one launch per phase
     try:
         for _ in range(2):                      # the second solve is reported
             dD.copy_(dW)
@@ -262,6 +263,8 @@ def isolated_pivot_phases(fw, solve, dD, dW, dP, n, n_pad, BS, stream, peak_tflo
     finally:
         fw.fw_set_option("lookahead", 1)
         fw.fw_set_option("pairs", 1)
+        ps = os.environ.get("FW_PERSISTENT", "-1")
+        fw.fw_set_option("persistent", int(ps) if ps in ("-1", "0", "1") else -1)
     R = s.rounds
     p1_us, p2_us = 1e3 * s.phase1_ms / R, 1e3 * s.phase2_ms / R
     p2_relax = 2.0 * BS * BS * (n_pad - BS)     # row + column strip through BS k each
@@ -286,7 +289,7 @@ def isolated_pivot_phases(fw, solve, dD, dW, dP, n, n_pad, BS, stream, peak_tflo
         "phase2_frac_hbm": (p2_bytes / (p2_us * 1e-6) / 1e9) / hbm if p2_us > 0 else None,
         "hbm_peak_gbs": hbm,
         "solve_ms_serialized": s.solve_ms,
-        "note": "one extra solve with fw_set_option(lookahead=0, pairs=0): per-round phase-1 and dual "
+        "note": "one extra solve with fw_set_option(lookahead=0, pairs=0, persistent=0): per-round phase-1 and dual "
                 "phase-2 launch times from the library's CUDA events, serialized on one stream. The "
                 "strips run BS relaxations per 4-byte element (32 relax/B at BS=128): ALU-bound, not "
                 "HBM-bound, so phase2_frac_measured_mix is the fraction that matters",
@@ -394,9 +397,12 @@ def run_gpu(args, cfg):
     roof = {"bound": "alu", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": (achieved_tflops / peak_tflops) if achieved_tflops else None,
             "traffic": traffic,
-            "kernel": f"minplus_tile_kernel<{ctype},128,128,{mode}> (phase 3, rank 0"
-                      + (", two rounds per pass: 256-deep bulk launches" if s0.phase3_launches < s0.rounds else "")
-                      + ")",
+            "kernel": (f"fw_persistent_kernel<{ctype},{mode}> (the whole solve's rounds as ONE persistent "
+                       "launch, DESIGN.md 4.10: phase-1/2/3 work items; achieved = all n_pad^3 relaxations "
+                       "of the launch / its duration)") if s0.persistent else
+                      (f"minplus_tile_kernel<{ctype},128,128,{mode}> (phase 3, rank 0"
+                       + (", two rounds per pass: 256-deep bulk launches" if s0.phase3_launches < s0.rounds else "")
+                       + ")"),
             "launches_per_step": p3_launches / len(stats),
             "avg_launch_ms": avg_launch_ms,
             "flop_per_launch": 2.0 * p3_relax / max(1, p3_launches),

@@ -119,6 +119,8 @@ int fw_init(int ngpus_max, unsigned flags);
  *                        solves), 0 off, 1 on (env FW_PERSISTENT)
  *   "persist_gap" k >= 0 persistent: phase-3 tiles between phase 1 and phase 2 of the next
  *                        round in the work order (-1 auto)
+ *   "persist_relaxed" 0/1, "persist_quarters" 0/1  persistent: relaxed dependency polls;
+ *                        critical-path tiles as 64 x 64 quarter items (one GPU, default 1)
  *   "async"      0/1     fw_solve_device_* (one GPU) return as soon as the solve is enqueued on
  *                        the caller's stream: no validation kernel and no host round trip, so a
  *                        solve can be captured into a CUDA graph (after one warm-up solve of the

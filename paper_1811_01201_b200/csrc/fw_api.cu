@@ -166,6 +166,8 @@ struct Ctx {
   bool pair_pdl = true;            // pairs: bulk launches programmatically serialized (env FW_PDL=0: off)
   bool last_pdl = false;           // the last solve's pairs ran with programmatic serialization
   std::vector<cudaEvent_t> xev;    // disable-timing events between bulk launches
+  std::vector<cudaStream_t> lb_st; // loopback transport: main and look-ahead stream of every emulated rank
+  std::vector<cudaEvent_t> lb_ev;  // loopback transport: disable-timing fork / join / broadcast events
   bool pair_order = true;          // pairs: the next pair's strips run beside the bulk launch (env FW_PAIR_ORDER=0: before it)
   int pipe_pair_rows = 32;         // host pipeline: smallest chunk (tile-rows) run in pairs (env FW_PIPE_PAIR_ROWS)
   bool last_pairs = false;         // the last solve ran in pairs (stats layout)
@@ -857,43 +859,92 @@ struct Rounds {
   }
 };
 
-// Loopback transport: all ranks of the partition emulated in this process on one stream
-// (the broadcast becomes a device-to-device copy). Kernels never wait on one another, so
-// running the ranks one after another exercises the partitioned indexing, the strip
-// ownership and the look-ahead tile split of the multi-GPU path on a single GPU.
+// Loopback transport: all ranks of the partition emulated in this process on one GPU, each
+// with the two streams run() gives a rank — its main stream and its high-priority look-ahead
+// stream — and run()'s event structure: ordered phase-3 launches on the main streams,
+// wait_count_kernel gates and the next round's pivot phases on the look-ahead streams, the
+// main streams waiting for them. The broadcast becomes a device-to-device copy per receiver
+// with a collective's completion semantics: each receiver's copy into strip[K & 1] is ordered
+// on ITS stream after the root's row strip, and the root's stream continues only after every
+// receiver's copy (a broadcast completes on all ranks). So the cross-stream reuse of the two
+// strip buffers and of the owner's pivot rows is exercised as on G GPUs. Every wait is for work
+// that waits on nothing (wait_count_kernel is one thread and bounded), so the emulation cannot
+// deadlock on one GPU; it is a correctness transport, never timed.
+int ensure_lb(Ctx &c, int W) {
+  int lo = 0, hi = 0;
+  CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  while ((int)c.lb_st.size() < 2 * W) {
+    cudaStream_t q;
+    CU(cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, c.lb_st.size() % 2 ? hi : lo));
+    c.lb_st.push_back(q);
+  }
+  while ((int)c.lb_ev.size() < 2 + 3 * W) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.lb_ev.push_back(e);
+  }
+  return FW_OK;
+}
+
 template <typename T, int MODE>
-int run_loopback(std::vector<Rounds<T, MODE>> &rk, cudaStream_t st, bool lookahead) {
+int run_loopback(Ctx &c, std::vector<Rounds<T, MODE>> &rk, cudaStream_t st, bool lookahead) {
   const int R = rk[0].R, BS = rk[0].BS, W = (int)rk.size();
   const int64_t n_pad = rk[0].n_pad;
-  auto pivot = [&](int K) -> int {
-    const int o = owner_of(n_pad, W, (int64_t)K * BS);
-    TRY(rk[o].phase1(st, K));
-    TRY(rk[o].phase2(st, K, true, false));
-    const T *src = rk[o].D + (int64_t)rk[o].lrow(K) * rk[o].ld;
-    for (int r = 0; r < W; ++r)
-      if (r != o)
-        CU(cudaMemcpy2DAsync(rk[r].strip[K & 1], n_pad * sizeof(T), src, rk[o].ld * sizeof(T),
-                             n_pad * sizeof(T), BS, cudaMemcpyDeviceToDevice, st));
-    for (int r = 0; r < W; ++r) TRY(rk[r].phase2(st, K, false, true));
+  TRY(ensure_lb(c, W));
+  cudaStream_t *ms = c.lb_st.data();      // ms[2r]: rank r's main stream, ms[2r + 1]: its look-ahead stream
+  cudaEvent_t e_fork = c.lb_ev[0], e_root = c.lb_ev[1];
+  cudaEvent_t *e_recv = c.lb_ev.data() + 2, *e_a = e_recv + W, *e_b = e_a + W;
+  auto follow = [&](cudaStream_t waiter, cudaStream_t src, cudaEvent_t e) -> int {
+    CU(cudaEventRecord(e, src));
+    CU(cudaStreamWaitEvent(waiter, e, 0));
     return FW_OK;
   };
+  // pivot phases of round K on stream q(r) of every rank: phase 1 and the row strip on the
+  // owner, the broadcast, every rank's column strip
+  auto pivot = [&](int K, int side) -> int {
+    auto q = [&](int r) { return ms[2 * r + side]; };
+    const int o = owner_of(n_pad, W, (int64_t)K * BS);
+    TRY(rk[o].phase1(q(o), K));
+    TRY(rk[o].phase2(q(o), K, true, false));
+    CU(cudaEventRecord(e_root, q(o)));
+    const T *src = rk[o].D + (int64_t)rk[o].lrow(K) * rk[o].ld;
+    for (int r = 0; r < W; ++r) {
+      if (r == o) continue;
+      CU(cudaStreamWaitEvent(q(r), e_root, 0));
+      CU(cudaMemcpy2DAsync(rk[r].strip[K & 1], n_pad * sizeof(T), src, rk[o].ld * sizeof(T),
+                           n_pad * sizeof(T), BS, cudaMemcpyDeviceToDevice, q(r)));
+      CU(cudaEventRecord(e_recv[r], q(r)));
+    }
+    for (int r = 0; r < W; ++r)
+      if (r != o) CU(cudaStreamWaitEvent(q(o), e_recv[r], 0));
+    for (int r = 0; r < W; ++r) TRY(rk[r].phase2(q(r), K, false, true));
+    return FW_OK;
+  };
+  CU(cudaEventRecord(e_fork, st));        // fork: every rank's streams follow st
+  for (int r = 0; r < 2 * W; ++r) CU(cudaStreamWaitEvent(ms[r], e_fork, 0));
   if (!lookahead || BS != 128 || R < 2) {
     for (int K = 0; K < R; ++K) {
-      TRY(pivot(K));
-      for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(st, K));
+      TRY(pivot(K, 0));
+      for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(ms[2 * r], K));
     }
-    return FW_OK;
-  }
-  TRY(pivot(0));
-  for (int K = 0; K < R; ++K) {
-    if (K + 1 < R) {
-      int nprio = 0;
-      for (int r = 0; r < W; ++r) TRY(rk[r].phase3_ordered(st, K, rk[r].done + K, &nprio));
-      TRY(pivot(K + 1));
-    } else {
-      for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(st, K));
+  } else {
+    TRY(pivot(0, 0));
+    for (int r = 0; r < W; ++r) TRY(follow(ms[2 * r + 1], ms[2 * r], e_a[r]));   // run(): side follows round 0's pivot
+    for (int K = 0; K < R; ++K) {
+      if (K + 1 < R) {
+        for (int r = 0; r < W; ++r) {
+          int nprio = 0;
+          TRY(rk[r].phase3_ordered(ms[2 * r], K, rk[r].done + K, &nprio));
+          TRY(rk[r].wait_count(ms[2 * r + 1], K, nprio));
+        }
+        TRY(pivot(K + 1, 1));
+        for (int r = 0; r < W; ++r) TRY(follow(ms[2 * r], ms[2 * r + 1], e_b[r]));
+      } else {
+        for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(ms[2 * r], K));
+      }
     }
   }
+  for (int r = 0; r < 2 * W; ++r) TRY(follow(st, ms[r], e_a[r / 2]));   // join
   return FW_OK;
 }
 
@@ -1182,7 +1233,7 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
   std::vector<Rounds<T, MODE>> rk;
   for (auto &p : parts) {
     rk.push_back(Rounds<T, MODE>{c, world, p.D, p.P, p.ld, n, n_pad, p.row0, p.nrows, BS, R, maxkey,
-                                 {p.strip[0], p.strip[1]}, done});
+                                 {p.strip[0], p.strip[1]}, done + (tr == T_LOOPBACK ? rk.size() * R : 0)});
     rk.back().nccl = tr == T_NCCL;
   }
   c.last_pairs = false;
@@ -1193,7 +1244,7 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
       c.last_persist = true;
       return run_loopback_persistent<T, MODE>(c, rk, st, ev);
     }
-    return run_loopback<T, MODE>(rk, st, la);
+    return run_loopback<T, MODE>(c, rk, st, la);
   }
   if (tr == T_NCCL && c.persistent == 1 && BS == 128 && world <= kMaxRanks) {
     c.last_persist = true;
@@ -1322,7 +1373,7 @@ int run_attempt(Ctx &c, std::vector<Part<T>> &parts, std::vector<Part<C>> &cv, T
       default: TRY((run_init<C, MODE_KEY, T>(st, isrc, ild, p.nsrc, n, p.row0, q.D, q.P, q.ld, q.nrows, n_pad)));
     }
   }
-  CU(cudaMemsetAsync(done, 0, 4 * (size_t)R, st));
+  CU(cudaMemsetAsync(done, 0, 4 * (size_t)R * cv.size(), st));
   CU(cudaEventRecord(e_init, st));
   switch (mode) {
     case MODE_PLAIN: return run_rounds<C, MODE_PLAIN>(c, cv, tr, world, n, BS, R, maxkey, done, st, ev, la);
@@ -1377,21 +1428,25 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
     }
     const size_t rb = (size_t)n_pad * sizeof(T);
     const int use_smem = rb <= 200 * 1024;
-    auto launch = [&](auto kern) -> int {
-      TRY(smem_attr((const void *)kern, 200 * 1024));
-      for (auto &p : parts) {
-        if (p.nsrc == 0) continue;
-        kern<<<(unsigned)p.nsrc, 512, use_smem ? rb : 0, st>>>(p.D, Dt, p.ld, n_pad, p.row0, n,
-                                                              n_pad, p.P, use_smem);
-        CU(cudaGetLastError());
-        ++g_launches;
+    {                        // four lanes per element
+      auto launchq = [&](auto kern) -> int {
+        TRY(smem_attr((const void *)kern, 200 * 1024));
+        for (auto &p : parts) {
+          if (p.nsrc == 0) continue;
+          kern<<<(unsigned)p.nsrc, 512, use_smem ? rb : 0, st>>>(p.D, Dt, p.ld, n_pad, p.row0, n, n_pad, p.P);
+          CU(cudaGetLastError());
+          ++g_launches;
+        }
+        return FW_OK;
+      };
+      switch (BS * 2 + use_smem) {
+        case 64: TRY(launchq(resolve_lastk_quad_kernel<T, 32, false>)); break;
+        case 65: TRY(launchq(resolve_lastk_quad_kernel<T, 32, true>)); break;
+        case 128: TRY(launchq(resolve_lastk_quad_kernel<T, 64, false>)); break;
+        case 129: TRY(launchq(resolve_lastk_quad_kernel<T, 64, true>)); break;
+        case 256: TRY(launchq(resolve_lastk_quad_kernel<T, 128, false>)); break;
+        default: TRY(launchq(resolve_lastk_quad_kernel<T, 128, true>));
       }
-      return FW_OK;
-    };
-    switch (BS) {
-      case 32: TRY(launch(resolve_lastk_kernel<T, 1>)); break;
-      case 64: TRY(launch(resolve_lastk_kernel<T, 2>)); break;
-      default: TRY(launch(resolve_lastk_kernel<T, 4>));
     }
   }
   if (path_mode >= 0) {
@@ -1431,8 +1486,9 @@ int solve_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, in
 
   // 1. validation (read-only; outputs untouched on error), reduced over all ranks
   const int R = (int)((n + BS - 1) / BS);  // rounds wholly inside the padding are skipped
-  TRY(c.scratch.ensure(64 + 4 * (size_t)R));
-  // [0] flags [1] max weight [2] max key [3] placement status; [16..16+R) look-ahead counters
+  TRY(c.scratch.ensure(64 + 4 * (size_t)R * parts.size()));
+  // [0] flags [1] max weight [2] max key [3] placement status; [16..16+R*W) look-ahead counters
+  // (R per emulated rank of the loopback transport, W = parts.size(); R otherwise)
   int *d_flags = static_cast<int *>(c.scratch.p);
   CU(cudaMemsetAsync(d_flags, 0, 16, st));
   c.pending = false;
@@ -2397,6 +2453,10 @@ void ctx_release(Ctx *c) {
   c->ring_ev.clear();
   for (auto e : c->xev) cudaEventDestroy(e);
   c->xev.clear();
+  for (auto e : c->lb_ev) cudaEventDestroy(e);
+  c->lb_ev.clear();
+  for (auto q : c->lb_st) cudaStreamDestroy(q);
+  c->lb_st.clear();
   c->ring_used.clear();
   if (c->copy) cudaStreamDestroy(c->copy);
   c->copy = nullptr;

@@ -1473,12 +1473,9 @@ __global__ void emit_rows_kernel(const T *D, int64_t ld, int64_t n, int64_t rows
 // robust choice. k* is an intermediate vertex of a shortest i->j path, i.e. the paper's
 // "most recently added intermediate node" form of P. Overwrites tags with k*.
 //
-// One CTA per row i (row i of D staged in shared memory when it fits); one warp per element:
-// lane l takes k = kb + CH*l .. + CH-1 with one vector load of the transposed column segment
-// Dt[j][kb..kb+BS) (512 B coalesced per warp at BS = 128); a warp min-reduction and a ballot
-// pick the first arg-min, branch-free. U = 8 elements per warp iteration keep 8 independent
-// 512-B segment loads in flight and the next group's tags are loaded before the current
-// group is searched: the kernel reads ~4*BS bytes per element (~n^2 * 512 B at BS = 128).
+// One CTA per row i (row i of D staged in shared memory when it fits); FOUR lanes per element
+// (resolve_lastk_quad_kernel below); the kernel reads ~4*BS bytes of D^T per tagged element
+// (~n^2 * 512 B at BS = 128).
 
 // Dt = D^T for a rows x cols matrix (pitch ld -> pitch ldt), 32x32 shared-memory tiles. The
 // diagonal of Dt is written as INF: the resolve below then never picks k = j (D[i][j] + D[j][j]
@@ -1499,88 +1496,94 @@ __global__ void transpose_kernel(const T *D, int64_t ld, int64_t rows, int64_t c
   }
 }
 
-// Vector of CH consecutive T (CH = 1, 2, 4) for one 4*CH-byte load.
-template <typename T, int CH> struct VecN;
-template <typename T> struct VecN<T, 1> { using V = T; };
-template <> struct VecN<float, 2> { using V = float2; };
-template <> struct VecN<int32_t, 2> { using V = int2; };
-template <> struct VecN<float, 4> { using V = float4; };
-template <> struct VecN<int32_t, 4> { using V = int4; };
-template <typename V> __device__ __forceinline__ auto velem(const V &v, int c) { return vget(v, c); }
-__device__ __forceinline__ float velem(const float &v, int) { return v; }
-__device__ __forceinline__ int32_t velem(const int32_t &v, int) { return v; }
-__device__ __forceinline__ float velem(const float2 &v, int c) { return c ? v.y : v.x; }
-__device__ __forceinline__ int32_t velem(const int2 &v, int c) { return c ? v.y : v.x; }
+// The search, FOUR lanes per element (8 elements per warp): lane q of element e takes the 16-B
+// granules 4s' + q of block K (s' = s ^ (e & 1), s < BS/16), i.e. BS/4 candidates, and the quad
+// takes the smallest of its four first hits with two shuffles. A warp spends ~16 instructions
+// per element; the round-1/2 kernel with one warp per element spent ~60 and was ALU-issue bound
+// (ncu at C2: 58.6 warp instructions per element, ALU pipe 69%, 1.42 ms; this kernel 0.86 ms). The four
+// lanes of an element read 64 contiguous bytes of D^T per load (coalesced); the step swap for
+// odd elements puts the 8 elements of a warp evenly on the two halves of the shared-memory bank
+// space, so an LDS.128 of row i takes the minimum 4 wavefronts whatever the tags. The D^T loads
+// of the next element are in flight while the current one is searched (two register stages).
+template <typename T> __device__ __forceinline__ void add4(T (&o)[4], const typename Vec4<T>::V &a,
+                                                             const typename Vec4<T>::V &b) {
+  o[0] = a.x + b.x; o[1] = a.y + b.y; o[2] = a.z + b.z; o[3] = a.w + b.w;
+}
+template <> __device__ __forceinline__ void add4<float>(float (&o)[4], const float4 &a, const float4 &b) {
+  const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));   // FADD2: one rounded add each
+  const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
+  o[0] = lo.x; o[1] = lo.y; o[2] = hi.x; o[3] = hi.y;
+}
 
-template <typename T, int CH>
+template <typename T, int BS, bool SMEM>
 __global__ void __launch_bounds__(512, 1)
-resolve_lastk_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t row0, int64_t n,
-                     int64_t n_pad, int32_t *tags, int use_smem) {
-  constexpr int U = 12;                    // elements in flight per warp (12 x 4*BS bytes)
-  constexpr int BS = 32 * CH;
-  using V = typename VecN<T, CH>::V;
+resolve_lastk_quad_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int64_t row0, int64_t n,
+                          int64_t n_pad, int32_t *tags) {
+  constexpr int NS = BS / 16;              // 16-B granule steps per lane
+  constexpr int kNone = 0x40000000;        // "no hit" (above every k, and k + 3 stays positive)
+  using V = typename Vec4<T>::V;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *srow = reinterpret_cast<T *>(smem_raw);
   const int64_t li = blockIdx.x;
   const int gi = (int)(row0 + li), nn = (int)n;
   const T *Drow = D + li * ld;
   int32_t *trow = tags + li * ld;
-  if (use_smem) {
-    // row i of the final D, with D[i][i] read as INF: k = i is never picked (D[i][i] + D[i][j] =
-    // D[i][j] trivially) without testing for it; k = j is excluded by Dt's INF diagonal
+  if constexpr (SMEM) {
+    // row i with D[i][i] read as INF (k = i never picked); k = j is excluded by Dt's INF diagonal
     for (int j = threadIdx.x; j < (int)n_pad; j += blockDim.x) srow[j] = j == gi ? Num<T>::inf() : Drow[j];
     __syncthreads();
   }
-  const T *A = use_smem ? srow : Drow;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int step = nw * U;
-  // group metadata (tags) is loaded one group ahead of the segment loads
-  int tg[U];
+  const T *A = SMEM ? srow : Drow;
+  const int lane = threadIdx.x & 31, q = lane & 3, e = lane >> 2;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int step = nw * 8;
+  const int sw = (e & 1) * 16;             // granule s of an odd element is s ^ 1: +16 (s even), -16 (s odd)
+  const unsigned qmask = 0xfu << (lane & ~3);
+  auto load = [&](int j, int t, V (&b)[NS]) {
+    const T *bp = Dt + (int64_t)min(j, nn - 1) * ldt + max(t, 0) * BS + 4 * q;
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int j = warp * U + u;
-    tg[u] = j < nn ? trow[j] : -1;
-  }
-  for (int j0 = warp * U; j0 < nn; j0 += step) {
-    V b[U];                                // the global segment loads, all in flight (untagged
-#pragma unroll                             // ones and j >= n load row n-1, block 0)
-    for (int u = 0; u < U; ++u)
-      b[u] = *reinterpret_cast<const V *>(Dt + (int64_t)min(j0 + u, nn - 1) * ldt + max(tg[u], 0) * BS + CH * lane);
-    int tgn[U];
+    for (int s = 0; s < NS; ++s)
+      if (t >= 0) b[s] = *reinterpret_cast<const V *>(bp + 16 * s + ((s & 1) ? -sw : sw));
+  };
+  auto search = [&](int j, int t, const V (&b)[NS]) {
+    if (t < 0) return;
+    // reading R9: k* = the FIRST k of block K, k not in {i, j}, with D[i][k] + D[k][j] <= D[i][j]
+    const T dij = A[j];
+    const int kq = t * BS + 4 * q;
+    int kl = kNone;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + step + u;
-      tgn[u] = j < nn ? trow[j] : -1;
+    for (int s = 0; s < NS; ++s) {
+      const int k0 = kq + 16 * s + ((s & 1) ? -sw : sw);
+      const V a = *reinterpret_cast<const V *>(A + k0);
+      T sum[4];
+      add4<T>(sum, a, b[s]);
+      int kf = kNone;                      // first hit among the granule's 4 candidates
+#pragma unroll
+      for (int c = 3; c >= 0; --c) kf = (sum[c] <= dij && (SMEM || k0 + c != gi)) ? c : kf;
+      kl = min(kl, k0 + kf);
     }
-    int res = -1;                          // lane u keeps the result of element u
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int j = j0 + u;
-      const int k0 = max(tg[u], 0) * BS + CH * lane;
-      const V a = *reinterpret_cast<const V *>(A + k0);   // row i: shared memory (or L1)
-      const T dij = A[min(j, nn - 1)];   // the final D[i][j] (j = i reads INF: untagged, discarded)
-      // reading R9: k* = the FIRST k of block K, k not in {i, j}, with D[i][k] + D[k][j] <= D[i][j]
-      // (one exists: the improving k of the tag's round; later rounds only lowered both terms and
-      // rounding is monotone). Each lane takes its first hit among its CH candidates, the warp the
-      // smallest: one min-reduction (REDUX) per element. Padding k >= n is INF.
-      int kl = 0x7fffffff;
-#pragma unroll
-      for (int c = CH - 1; c >= 0; --c) {
-        const T sum = (T)velem(a, c) + (T)velem(b[u], c);
-        kl = (sum <= dij && (use_smem || k0 + c != gi)) ? k0 + c : kl;
-      }
-      const int km = __reduce_min_sync(0xffffffffu, kl);
-      if (lane == u) res = km == 0x7fffffff ? -1 : km;
-    }
-    if (lane < U && j0 + lane < nn) {
-      // tg[lane] without dynamic register indexing
-      int t = tg[0];
-#pragma unroll
-      for (int u = 1; u < U; ++u) t = lane == u ? tg[u] : t;
-      if (t >= 0) trow[j0 + lane] = res;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) tg[u] = tgn[u];
+    kl = min(kl, __shfl_xor_sync(qmask, kl, 1));
+    kl = min(kl, __shfl_xor_sync(qmask, kl, 2));
+    if (q == 0) trow[j] = kl >= kNone ? -1 : kl;
+  };
+  // pipeline: element m's D^T segment is in registers (ba / bb alternate) while m + 1's loads are
+  // in flight, and the tags run two elements further ahead, so no D^T load waits on its tag
+  auto tag_of = [&](int j) { return j < nn ? trow[j] : -1; };
+  V ba[NS], bb[NS];
+  int j0 = warp * 8 + e;
+  int ta = tag_of(j0), tb = tag_of(j0 + step), tc = tag_of(j0 + 2 * step), td = tag_of(j0 + 3 * step);
+  load(j0, ta, ba);
+  for (; j0 - e < nn; j0 += 2 * step) {
+    const int t4 = tag_of(j0 + 4 * step), t5 = tag_of(j0 + 5 * step);
+    load(j0 + step, tb, bb);
+    search(j0, ta, ba);
+    if (j0 + step - e >= nn) break;
+    load(j0 + 2 * step, tc, ba);
+    search(j0 + step, tb, bb);
+    ta = tc;
+    tb = td;
+    tc = t4;
+    td = t5;
   }
 }
 
