@@ -147,7 +147,6 @@ struct Ctx {
   DevBuf ws_d, ws_t;               // padded local workspaces (D, tags/P)
   DevBuf ws_b;                     // backup of W for a speculative key run (in place)
   DevBuf ws_s;                     // two pivot-strip receive buffers (multi-GPU)
-  DevBuf ws_full;                  // gathered final D (multi-GPU, round tags only)
   DevBuf ws_tr;                    // transposed final D (round tags only)
   DevBuf user_d, user_t;           // device copies of host buffers (host entry points)
   DevBuf scratch;                  // flags / reductions
@@ -494,8 +493,6 @@ struct Rounds {
   int *done;     // R look-ahead tile counters (zeroed per solve)
   const T *Dg = nullptr;   // one GPU, a row range of the matrix (host pipeline): global row 0,
                            // so the pivot strips of other rows are read in place
-  bool nccl = false;       // this rank's rows of an NCCL communicator (any world size, 1 included):
-                           // every round's pivot strip goes through ncclBroadcast
 
   // d_flags of the solve: maxkey is always d_flags + 2; bit 4 of d_flags[0] = a look-ahead
   // wait timed out (wait_count_kernel)
@@ -679,17 +676,50 @@ struct Rounds {
     TRY(phase2(st, b, true, true));
     return strip3(st, b, a);
   }
+  // B operand of pair Pp: rows a, b = 2Pp, 2Pp+1 (both rounds complete) — in place on their
+  // owner (one GPU: always; host pipeline: through Dg), the broadcast buffer elsewhere
+  const T *bpair(int Pp) const {
+    const int a = 2 * Pp;
+    if (owns(a) || Dg || world == 1) return D + (int64_t)lrow(a) * ld;
+    return strip[Pp & 1];
+  }
   int pair_prio(cudaStream_t st, int Pp) {   // rows / columns c, d = a+2, a+3 through blocks a, b
     const int a = 2 * Pp, c2 = a + 2, kb = a * BS;
     const int tiles_c = (int)(n_pad / 128), tiles_r = (int)(nrows / 128);
-    TileArgs t = tile_args(ld, D + (int64_t)lrow(a) * ld, ld, kb, 2 * BS, a, nrows, n_pad);
-    put(t, 0, Strip{lrow(c2), 0, 0, 0, kb, kb + 2 * BS, 0});                // rows c, d (grid.y = 2)
-    put(t, 1, Strip{0, c2 * BS, lrow(a), lrow(a) + 4 * BS, 0, 0, 1});       // columns c, d, rows outside a..d
+    TileArgs t = tile_args(ld, bpair(Pp), ld, kb, 2 * BS, a, nrows, n_pad);
+    // rows c, d (grid.y = 2) when they are this rank's (else a row origin past the local rows:
+    // every tile of that strip exits), then columns c, d of the local rows outside a..d (the
+    // exclusion is in local row numbers; it misses the local rows when a..d are another rank's)
+    put(t, 0, Strip{owns(c2) || Dg || world == 1 ? lrow(c2) : (int)nrows, 0, 0, 0, kb, kb + 2 * BS, 0});
+    put(t, 1, Strip{0, c2 * BS, lrow(a), lrow(a) + 4 * BS, 0, 0, 1});
     return launch_tile<T, 128, 128, MODE>(dim3(std::max(tiles_c, tiles_r), 2, 2), st, D, P, t, maxkey);
+  }
+  // Non-owner ranks of pair Pp (block-row partition): bring the local columns a, b through both
+  // rounds with B = the received rows a, b (final for both rounds). Exact (reading R16): a
+  // shortest i -> v path (v in a or b) through blocks <= b has a first vertex u in a or b, and
+  // D[u][v] is final, so relaxing (i, a) through a and (i, b) through b, then (i, a) through b
+  // with the new (i, b), then (i, b) through a with the new (i, a) reaches it — three launches
+  // (colstrip 1: each column block through itself; colstrip 2: through its partner, even blocks
+  // first, so no launch reads a tile it writes), the host pipeline's column-strip batch.
+  int pair_cols(cudaStream_t st, int Pp) {
+    const int a = 2 * Pp;
+    const T *B0 = strip[Pp & 1] - (int64_t)a * BS * ld;   // row 0 of a virtual matrix: rows a, b at a*BS
+    TileArgs x = tile_args(ld, B0, ld, 0, BS, 0, nrows, n_pad);
+    x.colstrip = 1;
+    put(x, 0, Strip{0, a * BS, 0, 0, 0, 0, 0});
+    TRY((launch_tile<T, 128, 128, MODE>(dim3(2, (unsigned)(nrows / 128), 1), st, D, P, x, maxkey)));
+    for (int par = 0; par < 2; ++par) {
+      TileArgs y = tile_args(ld, B0, ld, 0, BS, 0, nrows, n_pad);
+      y.colstrip = 2;
+      y.colstep = 2;
+      put(y, 0, Strip{0, (a + par) * BS, 0, 0, 0, 0, 0});
+      TRY((launch_tile<T, 128, 128, MODE>(dim3(1, (unsigned)(nrows / 128), 1), st, D, P, y, maxkey)));
+    }
+    return FW_OK;
   }
   int pair_bulk(cudaStream_t st, int Pp, bool last, bool pdl = false) {
     const int a = 2 * Pp, kb = a * BS, w = (last ? 2 : 4) * BS;
-    TileArgs t = tile_args(ld, D + (int64_t)lrow(a) * ld, ld, kb, 2 * BS, a, nrows, n_pad);
+    TileArgs t = tile_args(ld, bpair(Pp), ld, kb, 2 * BS, a, nrows, n_pad);
     put(t, 0, Strip{0, 0, lrow(a), lrow(a) + w, kb, kb + w, 0});
     return launch_tile<T, 128, 128, MODE>(dim3((unsigned)(n_pad / 128), (unsigned)(nrows / 128), 1), st, D, P,
                                           t, maxkey, pdl);
@@ -777,7 +807,7 @@ struct Rounds {
       }
       return FW_OK;
     }
-    if (world == 1 && !nccl && c.pair_pdl) return run_pdl(st, e, K0, K1);
+    if (world == 1 && c.pair_pdl) return run_pdl(st, e, K0, K1);
     cudaStream_t side = c.side;
     TRY(phase1(st, K0));
     if (e.timing) CU(cudaEventRecord(ev[3 * K0], st));
@@ -846,30 +876,30 @@ struct Rounds {
   }
 
   // pivot phases after phase 1: strips and (multi-GPU) the broadcast
-  int pivot_rest(cudaStream_t st, int K) {
-    if (!nccl) return phase2(st, K, true, true);
-    TRY(phase2(st, K, true, false));
-    void *buf = owns(K) ? (void *)(D + (int64_t)lrow(K) * ld) : (void *)strip[K & 1];
-    NCC(c, g_nccl.Broadcast(buf, buf, (size_t)BS * (size_t)n_pad,
-                            std::is_integral<T>::value ? ncclInt32 : ncclFloat32,
-                            owner_of(n_pad, world, (int64_t)K * BS), c.comm, st));
-    ++g_bcasts;
-    g_bcast_bytes += (double)BS * (double)n_pad * sizeof(T);
-    return phase2(st, K, false, true);
-  }
+  int pivot_rest(cudaStream_t st, int K) { return phase2(st, K, true, true); }
 };
 
-// Loopback transport: all ranks of the partition emulated in this process on one GPU, each
-// with the two streams run() gives a rank — its main stream and its high-priority look-ahead
-// stream — and run()'s event structure: ordered phase-3 launches on the main streams,
-// wait_count_kernel gates and the next round's pivot phases on the look-ahead streams, the
-// main streams waiting for them. The broadcast becomes a device-to-device copy per receiver
-// with a collective's completion semantics: each receiver's copy into strip[K & 1] is ordered
-// on ITS stream after the root's row strip, and the root's stream continues only after every
-// receiver's copy (a broadcast completes on all ranks). So the cross-stream reuse of the two
-// strip buffers and of the owner's pivot rows is exercised as on G GPUs. Every wait is for work
-// that waits on nothing (wait_count_kernel is one thread and bounded), so the emulation cannot
-// deadlock on one GPU; it is a correctness transport, never timed.
+// ---- the multi-rank round driver (SURVEY §8 e) --------------------------------------------
+// The ranks of a block-row partition that this host thread drives: ONE (this process's rank of
+// an NCCL communicator, any world size) or ALL W (the loopback transport: every rank emulated on
+// this GPU). Every rank has a main stream and a high-priority look-ahead stream with run()'s
+// event structure — the look-ahead tiles first in an ordered phase-3 launch on the main stream,
+// a wait_count_kernel gate and the next round's pivot phases on the look-ahead stream, the main
+// stream waiting for them — and the pivot rows go from their owner to every other rank through
+// ncclBroadcast (NCCL) or, in the loopback, a device copy per receiver with a collective's
+// completion semantics: each receiver's copy is ordered on ITS stream after the owner's strips,
+// and the owner's stream continues only after every receiver's copy. So the schedule the NCCL
+// ranks run is exactly the one the loopback tests run on one GPU, concurrently: the cross-stream
+// reuse of the two strip buffers and of the owner's pivot rows is exercised — on G GPUs it is
+// safe only through the chain "look-ahead tiles of launch K done => launch K started => launch
+// K-1, the last reader of strip[(K+1) & 1], complete". Every wait is for work that waits on
+// nothing (wait_count_kernel is one thread and bounded), so the emulation cannot deadlock.
+//
+// Pairs (keyed / plain solves, BS = 128, R even, every rank's rows aligned to 256; DESIGN.md
+// §4.9, §9): the owner of blocks a, b = 2P, 2P+1 runs the one-GPU pair pivot on its rows, the
+// 256 rows a, b go out in ONE broadcast, the other ranks bring their columns a, b through both
+// rounds (pair_cols), and every rank relaxes its other tiles through 256 k in one bulk launch;
+// the next pair's strips (pair_prio) and pivot path run on the look-ahead streams under it.
 int ensure_lb(Ctx &c, int W) {
   int lo = 0, hi = 0;
   CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -878,7 +908,7 @@ int ensure_lb(Ctx &c, int W) {
     CU(cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, c.lb_st.size() % 2 ? hi : lo));
     c.lb_st.push_back(q);
   }
-  while ((int)c.lb_ev.size() < 2 + 3 * W) {
+  while ((int)c.lb_ev.size() < 1 + 3 * W) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c.lb_ev.push_back(e);
@@ -886,66 +916,187 @@ int ensure_lb(Ctx &c, int W) {
   return FW_OK;
 }
 
+// every rank's rows start on a 256-row boundary (pairs of blocks never straddle two ranks)
+bool pairs_aligned(int64_t n, int world) {
+  for (int r = 0; r < world; ++r) {
+    int64_t r0, nr;
+    partition(n, world, r, &r0, &nr);
+    if (r0 % 256) return false;
+  }
+  return true;
+}
+
 template <typename T, int MODE>
-int run_loopback(Ctx &c, std::vector<Rounds<T, MODE>> &rk, cudaStream_t st, bool lookahead) {
-  const int R = rk[0].R, BS = rk[0].BS, W = (int)rk.size();
-  const int64_t n_pad = rk[0].n_pad;
-  TRY(ensure_lb(c, W));
-  cudaStream_t *ms = c.lb_st.data();      // ms[2r]: rank r's main stream, ms[2r + 1]: its look-ahead stream
-  cudaEvent_t e_fork = c.lb_ev[0], e_root = c.lb_ev[1];
-  cudaEvent_t *e_recv = c.lb_ev.data() + 2, *e_a = e_recv + W, *e_b = e_a + W;
-  auto follow = [&](cudaStream_t waiter, cudaStream_t src, cudaEvent_t e) -> int {
-    CU(cudaEventRecord(e, src));
-    CU(cudaStreamWaitEvent(waiter, e, 0));
+struct Team {
+  Ctx &c;
+  std::vector<Rounds<T, MODE>> &rk;
+  bool nccl;                   // one local rank of an NCCL communicator; else the loopback
+  const Events &e;             // timing events of local rank 0 (NCCL only)
+  cudaStream_t st;             // the solve's stream
+  cudaStream_t *ms = nullptr;  // ms[2r]: local rank r's main stream, ms[2r + 1]: its look-ahead stream
+  cudaStream_t pair_nccl[2] = {nullptr, nullptr};
+  cudaEvent_t *ev = nullptr;   // [0] root, [1 + r] receive, [1 + W + r], [1 + 2W + r] follow
+  int W() const { return (int)rk.size(); }
+  cudaStream_t q(int r, int side) const { return ms[2 * r + side]; }
+  int BS() const { return rk[0].BS; }
+
+  int setup() {
+    if (nccl) {
+      pair_nccl[0] = st;
+      pair_nccl[1] = c.side;
+      ms = pair_nccl;
+      TRY(ensure_lb(c, 1));        // events only
+      ev = c.lb_ev.data();
+      return FW_OK;
+    }
+    TRY(ensure_lb(c, W()));
+    ms = c.lb_st.data();
+    ev = c.lb_ev.data();
+    CU(cudaEventRecord(ev[0], st));                    // fork: every rank's streams follow st
+    for (int r = 0; r < 2 * W(); ++r) CU(cudaStreamWaitEvent(ms[r], ev[0], 0));
     return FW_OK;
-  };
-  // pivot phases of round K on stream q(r) of every rank: phase 1 and the row strip on the
-  // owner, the broadcast, every rank's column strip
-  auto pivot = [&](int K, int side) -> int {
-    auto q = [&](int r) { return ms[2 * r + side]; };
-    const int o = owner_of(n_pad, W, (int64_t)K * BS);
-    TRY(rk[o].phase1(q(o), K));
-    TRY(rk[o].phase2(q(o), K, true, false));
-    CU(cudaEventRecord(e_root, q(o)));
+  }
+  int join() {
+    if (nccl) return FW_OK;       // the main stream is st
+    for (int r = 0; r < 2 * W(); ++r) TRY(follow(st, ms[r], ev[1 + W() + r / 2]));
+    return FW_OK;
+  }
+  int follow(cudaStream_t waiter, cudaStream_t src, cudaEvent_t x) {
+    CU(cudaEventRecord(x, src));
+    CU(cudaStreamWaitEvent(waiter, x, 0));
+    return FW_OK;
+  }
+  void mark(cudaEvent_t x, int r, int side) {   // a timing event of local rank 0
+    if (e.timing && r == 0) cudaEventRecord(x, q(0, side));
+  }
+
+  // rows [K*BS, (K+nb)*BS) from their owner into strip[slot] of every other rank
+  int bcast(int K, int nb, int slot, int side) {
+    Rounds<T, MODE> &x0 = rk[0];
+    const int64_t n_pad = x0.n_pad;
+    const size_t count = (size_t)nb * BS() * (size_t)n_pad;
+    if (nccl) {
+      void *buf = x0.owns(K) ? (void *)(x0.D + (int64_t)x0.lrow(K) * x0.ld) : (void *)x0.strip[slot];
+      NCC(c, g_nccl.Broadcast(buf, buf, count, std::is_integral<T>::value ? ncclInt32 : ncclFloat32,
+                              owner_of(n_pad, x0.world, (int64_t)K * BS()), c.comm, q(0, side)));
+      ++g_bcasts;
+      g_bcast_bytes += (double)count * sizeof(T);
+      return FW_OK;
+    }
+    const int o = owner_of(n_pad, W(), (int64_t)K * BS());
+    CU(cudaEventRecord(ev[0], q(o, side)));
     const T *src = rk[o].D + (int64_t)rk[o].lrow(K) * rk[o].ld;
-    for (int r = 0; r < W; ++r) {
+    for (int r = 0; r < W(); ++r) {
       if (r == o) continue;
-      CU(cudaStreamWaitEvent(q(r), e_root, 0));
-      CU(cudaMemcpy2DAsync(rk[r].strip[K & 1], n_pad * sizeof(T), src, rk[o].ld * sizeof(T),
-                           n_pad * sizeof(T), BS, cudaMemcpyDeviceToDevice, q(r)));
-      CU(cudaEventRecord(e_recv[r], q(r)));
+      CU(cudaStreamWaitEvent(q(r, side), ev[0], 0));
+      CU(cudaMemcpy2DAsync(rk[r].strip[slot], n_pad * sizeof(T), src, rk[o].ld * sizeof(T), n_pad * sizeof(T),
+                           (size_t)nb * BS(), cudaMemcpyDeviceToDevice, q(r, side)));
+      CU(cudaEventRecord(ev[1 + r], q(r, side)));
     }
-    for (int r = 0; r < W; ++r)
-      if (r != o) CU(cudaStreamWaitEvent(q(o), e_recv[r], 0));
-    for (int r = 0; r < W; ++r) TRY(rk[r].phase2(q(r), K, false, true));
+    for (int r = 0; r < W(); ++r)
+      if (r != o) CU(cudaStreamWaitEvent(q(o, side), ev[1 + r], 0));
     return FW_OK;
-  };
-  CU(cudaEventRecord(e_fork, st));        // fork: every rank's streams follow st
-  for (int r = 0; r < 2 * W; ++r) CU(cudaStreamWaitEvent(ms[r], e_fork, 0));
-  if (!lookahead || BS != 128 || R < 2) {
-    for (int K = 0; K < R; ++K) {
-      TRY(pivot(K, 0));
-      for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(ms[2 * r], K));
+  }
+
+  // round K's pivot phases: phase 1 and the row strip on the owner, the broadcast, every rank's
+  // column strip (phase1 / the row strip are no-ops on ranks that do not own block K)
+  int pivot(int K, int side) {
+    for (int r = 0; r < W(); ++r) {
+      TRY(rk[r].phase1(q(r, side), K));
+      mark(e.ev[3 * K], r, side);
+      TRY(rk[r].phase2(q(r, side), K, true, false));
     }
-  } else {
+    TRY(bcast(K, 1, K & 1, side));
+    for (int r = 0; r < W(); ++r) {
+      TRY(rk[r].phase2(q(r, side), K, false, true));
+      mark(e.ev[3 * K + 1], r, side);
+    }
+    return FW_OK;
+  }
+
+  int run_rounds(bool lookahead) {
+    Rounds<T, MODE> &x0 = rk[0];
+    const int R = x0.R;
+    if (!lookahead || BS() != 128 || R < 2) {
+      for (int K = 0; K < R; ++K) {
+        TRY(pivot(K, 0));
+        for (int r = 0; r < W(); ++r) {
+          TRY(rk[r].phase3_full(q(r, 0), K));
+          mark(e.ev[3 * K + 2], r, 0);
+        }
+      }
+      return FW_OK;
+    }
     TRY(pivot(0, 0));
-    for (int r = 0; r < W; ++r) TRY(follow(ms[2 * r + 1], ms[2 * r], e_a[r]));   // run(): side follows round 0's pivot
+    for (int r = 0; r < W(); ++r) TRY(follow(q(r, 1), q(r, 0), ev[1 + W() + r]));   // side follows round 0's pivot
     for (int K = 0; K < R; ++K) {
       if (K + 1 < R) {
-        for (int r = 0; r < W; ++r) {
+        for (int r = 0; r < W(); ++r) {
           int nprio = 0;
-          TRY(rk[r].phase3_ordered(ms[2 * r], K, rk[r].done + K, &nprio));
-          TRY(rk[r].wait_count(ms[2 * r + 1], K, nprio));
+          TRY(rk[r].phase3_ordered(q(r, 0), K, rk[r].done + K, &nprio));
+          mark(e.ev[3 * K + 2], r, 0);
+          TRY(rk[r].wait_count(q(r, 1), K, nprio));
+          mark(e.sync[2 * K + 2], r, 1);
         }
         TRY(pivot(K + 1, 1));
-        for (int r = 0; r < W; ++r) TRY(follow(ms[2 * r], ms[2 * r + 1], e_b[r]));
+        for (int r = 0; r < W(); ++r) TRY(follow(q(r, 0), q(r, 1), ev[1 + 2 * W() + r]));
       } else {
-        for (int r = 0; r < W; ++r) TRY(rk[r].phase3_full(ms[2 * r], K));
+        for (int r = 0; r < W(); ++r) {
+          TRY(rk[r].phase3_full(q(r, 0), K));
+          mark(e.ev[3 * K + 2], r, 0);
+        }
       }
     }
+    return FW_OK;
   }
-  for (int r = 0; r < 2 * W; ++r) TRY(follow(st, ms[r], e_a[r / 2]));   // join
-  return FW_OK;
+
+  // pair Pp's pivot path: the owner's pair pivot on its rows, ONE broadcast of rows a, b, the
+  // other ranks' columns a, b
+  int pair_pivot(int Pp, int side) {
+    const int a = 2 * Pp;
+    for (int r = 0; r < W(); ++r)
+      if (rk[r].owns(a)) TRY(rk[r].pair_pivot(q(r, side), Pp));
+    TRY(bcast(a, 2, Pp & 1, side));
+    for (int r = 0; r < W(); ++r)
+      if (!rk[r].owns(a)) TRY(rk[r].pair_cols(q(r, side), Pp));
+    return FW_OK;
+  }
+
+  int run_pairs() {
+    const int NP = rk[0].R / 2;
+    TRY(pair_pivot(0, 0));
+    for (int Pp = 0; Pp < NP; ++Pp) {
+      const bool last = Pp + 1 == NP;
+      for (int r = 0; r < W(); ++r) mark(e.ev[3 * Pp], r, 0);           // the pair's phase-3 work starts
+      if (!last) {
+        for (int r = 0; r < W(); ++r) {
+          TRY(follow(q(r, 1), q(r, 0), ev[1 + W() + r]));               // the previous bulk launch is done
+          mark(e.sync[2 * Pp], r, 1);
+          TRY(rk[r].pair_prio(q(r, 1), Pp));
+        }
+        TRY(pair_pivot(Pp + 1, 1));
+        for (int r = 0; r < W(); ++r) {
+          mark(e.sync[2 * Pp + 1], r, 1);
+          CU(cudaEventRecord(ev[1 + 2 * W() + r], q(r, 1)));
+        }
+      }
+      for (int r = 0; r < W(); ++r) {
+        TRY(rk[r].pair_bulk(q(r, 0), Pp, last));
+        mark(e.ev[3 * Pp + 2], r, 0);
+        if (!last) CU(cudaStreamWaitEvent(q(r, 0), ev[1 + 2 * W() + r], 0));
+      }
+    }
+    return FW_OK;
+  }
+};
+
+template <typename T, int MODE>
+int run_team(Ctx &c, std::vector<Rounds<T, MODE>> &rk, bool nccl, cudaStream_t st, const Events &e, bool la,
+             bool pairs) {
+  Team<T, MODE> t{c, rk, nccl, e, st};
+  TRY(t.setup());
+  TRY(pairs ? t.run_pairs() : t.run_rounds(la));
+  return t.join();
 }
 
 
@@ -1234,21 +1385,23 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
   for (auto &p : parts) {
     rk.push_back(Rounds<T, MODE>{c, world, p.D, p.P, p.ld, n, n_pad, p.row0, p.nrows, BS, R, maxkey,
                                  {p.strip[0], p.strip[1]}, done + (tr == T_LOOPBACK ? rk.size() * R : 0)});
-    rk.back().nccl = tr == T_NCCL;
   }
   c.last_pairs = false;
   c.last_pdl = false;
   c.last_persist = false;
-  if (tr == T_LOOPBACK) {
-    if (c.persistent == 1 && BS == 128 && (int)rk.size() <= kMaxRanks) {
-      c.last_persist = true;
-      return run_loopback_persistent<T, MODE>(c, rk, st, ev);
-    }
-    return run_loopback<T, MODE>(c, rk, st, la);
+  if (tr == T_LOOPBACK && c.persistent == 1 && BS == 128 && (int)rk.size() <= kMaxRanks) {
+    c.last_persist = true;
+    return run_loopback_persistent<T, MODE>(c, rk, st, ev);
   }
   if (tr == T_NCCL && c.persistent == 1 && BS == 128 && world <= kMaxRanks) {
     c.last_persist = true;
     return run_nccl_persistent<T, MODE>(c, rk[0], st, ev);
+  }
+  if (tr != T_LOCAL) {   // the multi-rank driver: pairs when every pair of blocks sits on one rank
+    const bool pairs = MODE != MODE_TAG && c.pairs && la && BS == 128 && R % 2 == 0 && R >= 4 &&
+                       pairs_aligned(n, world);
+    c.last_pairs = pairs;
+    return run_team<T, MODE>(c, rk, tr == T_NCCL, st, ev, la, pairs);
   }
   if (use_persistent(c, MODE, tr, BS, n_pad, rk[0].row0, rk[0].nrows)) {
     c.last_persist = true;
@@ -1392,39 +1545,40 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
   // keyed mode: keys -> distances inside finalize_paths_kernel (decode = 1); keys only exist
   // with P (want_p), so the finalize pass always runs then
   if (mode == MODE_TAG && path_mode >= 0) {
-    // the search reads column segments D[kb..kb+BS)[j] of rows wherever they live: gather the
-    // final D (multi-GPU), then transpose it so each segment is one contiguous 4*BS-byte read
-    const T *Dfull = parts[0].D - (tr == T_LOOPBACK ? parts[0].row0 * n_pad : 0);
-    int64_t ldf = parts[0].ld;
-    if (nccl) {
+    // the search reads column segments D[kb..kb+BS)[j] of rows wherever they live: the final D
+    // transposed into block panels (transpose_panels_kernel: each segment one contiguous
+    // 4*BS-byte read). Multi-GPU: each rank transposes ONLY its own rows — their panels are one
+    // contiguous range of Dt — and the ranks exchange panel ranges with grouped broadcasts, so
+    // no rank gathers the row-major D or transposes more than its rows.
+    TRY(c.ws_tr.ensure((size_t)n_pad * n_pad * sizeof(T)));
+    T *Dt = static_cast<T *>(c.ws_tr.p);
+    auto transpose = [&](const T *src, int64_t ld, int64_t rows, int64_t g0) -> int {
+      if (rows == 0) return FW_OK;
+      dim3 g((unsigned)(n_pad / 32), (unsigned)(rows / 32));
+      transpose_panels_kernel<T><<<g, dim3(32, 8), 0, st>>>(src, ld, rows, n_pad, g0, BS, Dt);
+      CU(cudaGetLastError());
+      ++g_launches;
+      return FW_OK;
+    };
+    if (transposed) {
+      // host pipeline: the caller transposed the final D once for all chunks
+    } else if (nccl) {
       Part<T> &p = parts[0];
-      TRY(c.ws_full.ensure((size_t)n_pad * n_pad * sizeof(T)));
-      T *full = static_cast<T *>(c.ws_full.p);
-      if (p.nrows > 0)
-        CU(cudaMemcpy2DAsync(full + p.row0 * n_pad, n_pad * sizeof(T), p.D, p.ld * sizeof(T),
-                             n_pad * sizeof(T), p.nrows, cudaMemcpyDeviceToDevice, st));
+      TRY(transpose(p.D, p.ld, p.nrows, p.row0));
       NCC(c, g_nccl.GroupStart());
       for (int r = 0; r < world; ++r) {
         int64_t r0, nr;
         partition(n, world, r, &r0, &nr);
         if (nr == 0) continue;
-        T *dst = full + r0 * n_pad;
+        T *dst = Dt + r0 * n_pad;   // the panels of rows [r0, r0 + nr)
         NCC(c, g_nccl.Broadcast(dst, dst, (size_t)nr * n_pad, is_int_v<T>() ? ncclInt32 : ncclFloat32, r,
                                 c.comm, st));
         ++g_bcasts;
         g_bcast_bytes += (double)nr * (double)n_pad * sizeof(T);
       }
       NCC(c, g_nccl.GroupEnd());
-      Dfull = full;
-      ldf = n_pad;
-    }
-    TRY(c.ws_tr.ensure((size_t)n_pad * n_pad * sizeof(T)));
-    T *Dt = static_cast<T *>(c.ws_tr.p);
-    if (!transposed) {   // host pipeline: the caller transposed the final D once for all chunks
-      dim3 g((unsigned)(n_pad / 32), (unsigned)(n_pad / 32));
-      transpose_kernel<T><<<g, dim3(32, 8), 0, st>>>(Dfull, ldf, n_pad, n_pad, Dt, n_pad);
-      CU(cudaGetLastError());
-      ++g_launches;
+    } else {   // one GPU, or every rank of the loopback: the rows are one n_pad x n_pad matrix
+      TRY(transpose(parts[0].D - (tr == T_LOOPBACK ? parts[0].row0 * n_pad : 0), parts[0].ld, n_pad, 0));
     }
     const size_t rb = (size_t)n_pad * sizeof(T);
     const int use_smem = rb <= 200 * 1024;
@@ -1546,7 +1700,7 @@ int place_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int64_t n, in
     // one padded n_pad x n_pad workspace: each part uses its own rows of it
     TRY(c.ws_d.ensure((size_t)n_pad * n_pad * sizeof(T)));
     if (want_p) TRY(c.ws_t.ensure((size_t)n_pad * n_pad * sizeof(int32_t)));
-    const size_t sb = (size_t)BS * n_pad * sizeof(T);
+    const size_t sb = (size_t)(BS == 128 ? 2 : 1) * BS * n_pad * sizeof(T);   // pairs: rows a, b
     TRY(c.ws_s.ensure(2 * sb * parts.size()));
     for (size_t r = 0; r < parts.size(); ++r) {
       Part<T> &p = parts[r];
@@ -1574,7 +1728,7 @@ int place_parts(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int64_t n, in
     }
     if (!want_p) p.P = nullptr;
     if (nccl) {
-      const size_t sb = (size_t)BS * n_pad * sizeof(T);
+      const size_t sb = (size_t)(BS == 128 ? 2 : 1) * BS * n_pad * sizeof(T);   // pairs: rows a, b
       TRY(c.ws_s.ensure(2 * sb));
       p.strip[0] = static_cast<T *>(c.ws_s.p);
       p.strip[1] = reinterpret_cast<T *>(static_cast<char *>(c.ws_s.p) + sb);
@@ -1721,8 +1875,15 @@ int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, i
       const double rows = (double)p.nrows - ((kb >= p.row0 && kb < p.row0 + p.nrows) ? BS : 0);
       relax += rows * (double)(n_pad - BS) * BS;
     }
-  if (c.last_pairs)   // every pair relaxes all tiles outside its strip region through 256 k
-    relax = (double)(R / 2) * (double)(n_pad - 2 * BS) * (double)(n_pad - 2 * BS) * (2.0 * BS);
+  if (c.last_pairs) {  // every pair relaxes all local tiles outside its strip region through 256 k
+    relax = 0;
+    for (auto &p : parts)
+      for (int Pp = 0; Pp < R / 2; ++Pp) {
+        const int64_t kb = (int64_t)Pp * 2 * BS;
+        const double rows = (double)p.nrows - ((kb >= p.row0 && kb < p.row0 + p.nrows) ? 2 * BS : 0);
+        relax += rows * (double)(n_pad - 2 * BS) * (2.0 * BS);
+      }
+  }
   if (c.last_persist)  // one launch does every phase: n_pad^3 relaxations (phases 1, 2 and 3)
     relax = (double)n_pad * (double)n_pad * (double)n_pad;
   s.phase3_relaxations = relax;
@@ -2222,8 +2383,8 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
     if (q == 0) {   // the transpose of the whole final D (the search reads column segments)
       TRY(c.ws_tr.ensure((size_t)g.n_pad * g.n_pad * sizeof(C)));
       dim3 gt((unsigned)(g.n_pad / 32), (unsigned)(g.n_pad / 32));
-      transpose_kernel<C><<<gt, dim3(32, 8), 0, st>>>(D, g.ld, g.n_pad, g.n_pad, static_cast<C *>(c.ws_tr.p),
-                                                    g.n_pad);
+      transpose_panels_kernel<C><<<gt, dim3(32, 8), 0, st>>>(D, g.ld, g.n_pad, g.n_pad, 0, g.BS,
+                                                           static_cast<C *>(c.ws_tr.p));
       CU(cudaGetLastError());
       ++g_launches;
     }
@@ -2437,7 +2598,7 @@ void ctx_release(Ctx *c) {
     if (pr) cudaIpcCloseMemHandle(pr);
   c->peer_ring.clear();
   c->peer_handle.clear();
-  for (DevBuf *b : {&c->ws_d, &c->ws_t, &c->ws_b, &c->ws_s, &c->ws_full, &c->ws_tr, &c->user_d,
+  for (DevBuf *b : {&c->ws_d, &c->ws_t, &c->ws_b, &c->ws_s, &c->ws_tr, &c->user_d,
                     &c->user_t, &c->scratch, &c->ws_ver, &c->ws_ring, &c->ws_ipc})
     b->release();
   if (c->pinned) cudaFreeHost(c->pinned);

@@ -1477,12 +1477,17 @@ __global__ void emit_rows_kernel(const T *D, int64_t ld, int64_t n, int64_t rows
 // (resolve_lastk_quad_kernel below); the kernel reads ~4*BS bytes of D^T per tagged element
 // (~n^2 * 512 B at BS = 128).
 
-// Dt = D^T for a rows x cols matrix (pitch ld -> pitch ldt), 32x32 shared-memory tiles. The
-// diagonal of Dt is written as INF: the resolve below then never picks k = j (D[i][j] + D[j][j]
-// = D[i][j] holds trivially) without testing for it.
+// Dt = D^T in BLOCK PANELS: for every block K of BS rows, panel K is the n_pad x BS matrix
+// Dt[(K n_pad + j) BS + k] = D[K BS + k][j] — so the column segment D[K BS .. K BS + BS)[j] the
+// resolve searches is BS contiguous elements, and the panels of a block-row range are ONE
+// contiguous range of Dt (a rank of a block-row partition transposes only its own rows and the
+// ranks exchange their panel ranges, DESIGN.md §4.5 / §9). Rows [r0, r0 + rows) of D (global
+// rows g0 + r0 ..), pitch ld; 32 x 32 shared-memory tiles. The diagonal (global row == column)
+// is written as INF: the resolve below then never picks k = j (D[i][j] + D[j][j] = D[i][j]
+// holds trivially) without testing for it.
 template <typename T>
-__global__ void transpose_kernel(const T *D, int64_t ld, int64_t rows, int64_t cols, T *Dt,
-                                 int64_t ldt) {
+__global__ void transpose_panels_kernel(const T *D, int64_t ld, int64_t rows, int64_t cols, int64_t g0,
+                                        int BS, T *Dt) {
   __shared__ T tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
@@ -1491,8 +1496,9 @@ __global__ void transpose_kernel(const T *D, int64_t ld, int64_t rows, int64_t c
   }
   __syncthreads();
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
-    const int64_t c = c0 + y, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) Dt[c * ldt + r] = r == c ? Num<T>::inf() : tile[threadIdx.x][y];
+    const int64_t c = c0 + y, r = r0 + threadIdx.x, gr = g0 + r;
+    if (r < rows && c < cols)
+      Dt[((gr / BS) * cols + c) * BS + gr % BS] = gr == c ? Num<T>::inf() : tile[threadIdx.x][y];
   }
 }
 
@@ -1540,7 +1546,7 @@ resolve_lastk_quad_kernel(const T *D, const T *Dt, int64_t ld, int64_t ldt, int6
   const int sw = (e & 1) * 16;             // granule s of an odd element is s ^ 1: +16 (s even), -16 (s odd)
   const unsigned qmask = 0xfu << (lane & ~3);
   auto load = [&](int j, int t, V (&b)[NS]) {
-    const T *bp = Dt + (int64_t)min(j, nn - 1) * ldt + max(t, 0) * BS + 4 * q;
+    const T *bp = Dt + ((int64_t)max(t, 0) * ldt + min(j, nn - 1)) * BS + 4 * q;   // panel t, row j
 #pragma unroll
     for (int s = 0; s < NS; ++s)
       if (t >= 0) b[s] = *reinterpret_cast<const V *>(bp + 16 * s + ((s & 1) ? -sw : sw));

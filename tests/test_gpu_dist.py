@@ -77,6 +77,59 @@ def test_loopback_matches_single_gpu_bitwise():
         np.testing.assert_array_equal(Pw, P1)
 
 
+def loopback_stats(W, world, path="next", pairs=True):
+    fw.fw_init(0, fw.FW_PATH_LAST_K if path == "lastk" else 0)
+    try:
+        fw.fw_set_option("pairs", 1 if pairs else 0)
+        dD = torch.from_numpy(W).cuda()
+        dP = torch.empty(W.shape, dtype=torch.int32, device="cuda") if path else None
+        f = fw.fw_dist_loopback_solve_device_i32 if W.dtype == np.int32 else fw.fw_dist_loopback_solve_device_f32
+        f(dD, dP, block=128, world=world, stream=torch.cuda.current_stream())
+        s = fw.fw_last_stats()
+        return dD.cpu().numpy(), (dP.cpu().numpy() if dP is not None else None), s
+    finally:
+        fw.fw_free()
+
+
+@pytest.mark.parametrize("kind,n,world,path", [
+    ("complete_int", 2000, 2, "next"), ("complete_int", 2000, 4, "next"), ("complete_int", 2048, 8, "next"),
+    ("complete_int", 1024, 2, "lastk"), ("er_int", 1500, 4, "next"), ("er_int_f32", 1024, 4, "next"),
+    ("complete_int", 1536, 3, None),     # 12 tile rows over 3 ranks: 4 each, pair-aligned
+    ("complete_int", 1024, 3, "next"),   # 3/3/2 tile rows: not pair-aligned -> one round per pass
+    ("complete_int", 2048, 5, "next"),   # not pair-aligned -> one round per pass
+])
+def test_loopback_pairs(kind, n, world, path):
+    """Two rounds per phase-3 pass in the partitioned schedule (keyed / distance-only solves,
+    every rank's rows on 256-row boundaries): the owner of blocks a, b runs the pair pivot, the
+    256 rows a, b go out in one broadcast, the other ranks bring their columns a, b through both
+    rounds (pair_cols), every rank relaxes the rest through 256 k — on the loopback's per-rank
+    concurrent streams. D bitwise the one-GPU solve's (integer data), P valid."""
+    W = gen.generate(kind, n, 90 + n + world, p=0.03, lo=1, hi=1000 if kind.startswith("er") else 100)
+    D, P, s = loopback_stats(W, world, path)
+    n_pad = (n + 127) // 128 * 128
+    R = n_pad // 128
+    tiles = [fw.fw_dist_partition(n_pad, world, r)[0] // 128 for r in range(world)]
+    aligned = all(t % 2 == 0 for t in tiles)
+    if s.p_method != 1:   # keyed / distance-only (a speculative key run may fall back to tags)
+        assert (s.phase3_launches == R // 2) == aligned, (s.phase3_launches, R, tiles)
+    D1, P1 = loopback(W, 128, 1, path=path)
+    np.testing.assert_array_equal(D, D1)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact_data(W))
+    if path:
+        bad, first = oracle.check_paths(W, D, P, rtol=0.0, mode=path)
+        assert bad == 0, (bad, divmod(first, n))
+
+
+def test_loopback_pairs_off_same_distances():
+    """fw_set_option("pairs", 0) takes the one-round schedule on the same partition: same D."""
+    W = gen.generate("complete_int", 2000, 5)
+    Dp, Pp, sp = loopback_stats(W, 4, pairs=True)
+    Ds, Ps, ss = loopback_stats(W, 4, pairs=False)
+    assert sp.phase3_launches == sp.rounds // 2 and ss.phase3_launches == ss.rounds
+    np.testing.assert_array_equal(Dp, Ds)
+    assert oracle.check_paths(W, Dp, Pp)[0] == 0 and oracle.check_paths(W, Ds, Ps)[0] == 0
+
+
 def test_loopback_fallback_to_tags():
     W = gen.ring(700, 1000, np.float32)
     D, P = loopback(W, 128, 3)
@@ -124,10 +177,16 @@ def test_nccl_single_rank_communicator(kind, n, block, path):
     W = gen.generate(kind, n, 5 + n, p=0.02, lo=1, hi=1000 if kind.startswith("er") else 100)
     D, P, s = _nccl_one_rank(W, block, path)
     R = (n + block - 1) // block
-    # every round's pivot strip went through ncclBroadcast (a speculative key run that falls
-    # back runs the rounds again; the TAG post-pass adds one gather broadcast per rank)
-    assert s.broadcasts >= R and s.broadcasts % R == (1 if s.p_method == 1 and path else 0) % R, \
-        (s.broadcasts, R)
+    # every round's pivot strip went through ncclBroadcast — one broadcast per round, or per
+    # pair of rounds (rows a, b together) when the keyed / distance-only solve ran in pairs (a
+    # speculative key run that falls back runs the rounds again; the TAG post-pass adds one
+    # gather broadcast per rank)
+    pairs = s.phase3_launches == R // 2 and s.p_method != 1
+    assert pairs == (s.p_method != 1 and block == 128 and R % 2 == 0 and R >= 4), (s.phase3_launches, R)
+    per_solve = R // 2 if pairs else R
+    assert s.broadcasts >= per_solve, (s.broadcasts, R)
+    if s.p_method == 1:
+        assert s.broadcasts % R == (1 if path else 0) % R, (s.broadcasts, R)
     assert s.bcast_bytes >= R * block * s.n_pad * 4
     exact = exact_data(W)
     assert_D_matches(D, oracle.fw(W, None)[0], exact)
