@@ -156,3 +156,104 @@ def test_partitioned_schedule_gloo(world, n, BS):
     np.testing.assert_array_equal(D, Dref)
     P = np.where(np.isinf(D) | np.eye(n, dtype=bool), -1, P).astype(np.int32)
     assert oracle.check_paths(W, D, P, mode="lastk")[0] == 0
+
+
+# ---- the pair schedule of the partitioned solve (two rounds per phase-3 pass) ----------------
+def _rank_main_pairs(rank, world, port, n, seed, out):
+    """Two rounds per pass on a pair-aligned partition (BS = 128): owner(a, b)
+    runs the one-GPU pair pivot on its rows, the 256 rows a, b are the only data broadcast, the
+    other ranks bring their columns a, b through both rounds (pair_cols), and every rank relaxes
+    the rest of its rows through 256 k in one product."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    BS = 128
+    n_pad = (n + 127) // 128 * 128
+    W = gen.generate("er_int_f32", n, seed, p=0.2, lo=1, hi=50)
+    row0, nsrc = fw.fw_dist_partition(n, world, rank)
+    nxt = fw.fw_dist_partition(n, world, rank + 1)[0] if rank + 1 < world else n_pad
+    nrows = max(0, nxt - row0) if row0 < n_pad else 0
+    assert row0 % 256 == 0                             # the case the pair schedule runs on
+    D = np.full((nrows, n_pad), np.inf, dtype=np.float32)
+    D[:nsrc, :n] = W[row0:row0 + nsrc]
+    for i in range(nrows):
+        D[i, row0 + i] = 0
+    P = np.full((nrows, n_pad), -1, dtype=np.int32)
+    R = n_pad // BS
+    allc = np.ones(n_pad, dtype=bool)
+
+    def mask_out(lo, hi, size):
+        m = np.ones(size, dtype=bool)
+        m[max(lo, 0):max(hi, 0)] = False
+        return m
+
+    for Pp in range(R // 2):
+        a, b = 2 * Pp, 2 * Pp + 1
+        ka, kb_ = a * BS, b * BS
+        owner = fw.fw_dist_owner(n, world, ka)
+        assert owner == fw.fw_dist_owner(n, world, kb_)
+        strip = torch.empty((2 * BS, n_pad), dtype=torch.float32)
+        if owner == rank:                              # pair_pivot on the owner's rows
+            for x, y in ((a, b), (b, a)):
+                kx, ky = x * BS, y * BS
+                rx, ry = kx - row0, ky - row0
+                _phase1(D, P, rx, kx, BS)
+                # phase 2: row x (columns != x), column x (own rows != x)
+                _relax(D[rx:rx + BS], P[rx:rx + BS], D[rx:rx + BS, kx:kx + BS], D[rx:rx + BS].copy(), kx,
+                       cols_mask=mask_out(kx, kx + BS, n_pad))
+                _relax(D[:, kx:kx + BS], P[:, kx:kx + BS], D[:, kx:kx + BS].copy(), D[rx:rx + BS, kx:kx + BS].copy(),
+                       kx, rows_mask=mask_out(rx, rx + BS, nrows))
+                # strip3(x, y): row y (columns != x) and column y (rows outside a, b) through block x
+                _relax(D[ry:ry + BS], P[ry:ry + BS], D[ry:ry + BS, kx:kx + BS].copy(), D[rx:rx + BS].copy(), kx,
+                       cols_mask=mask_out(kx, kx + BS, n_pad))
+                lo = min(rx, ry)
+                _relax(D[:, ky:ky + BS], P[:, ky:ky + BS], D[:, kx:kx + BS].copy(), D[rx:rx + BS, ky:ky + BS].copy(),
+                       kx, rows_mask=mask_out(lo, lo + 2 * BS, nrows))
+            strip = torch.from_numpy(D[ka - row0:ka - row0 + 2 * BS].copy())
+        dist.broadcast(strip, src=owner)               # rows a, b: the only exchange of the pair
+        B = strip.numpy()
+        if owner != rank:                              # pair_cols
+            for x in (a, b):
+                kx = x * BS
+                _relax(D[:, kx:kx + BS], P[:, kx:kx + BS], D[:, kx:kx + BS].copy(),
+                       B[kx - ka:kx - ka + BS, kx:kx + BS], kx)
+            for x, y in ((a, b), (b, a)):              # x through its partner y, even block first
+                kx, ky = x * BS, y * BS
+                _relax(D[:, kx:kx + BS], P[:, kx:kx + BS], D[:, ky:ky + BS].copy(),
+                       B[ky - ka:ky - ka + BS, kx:kx + BS], ky)
+        # bulk: the local rows outside a, b, the columns outside a, b, through 256 k
+        rows = mask_out(ka - row0, ka - row0 + 2 * BS, nrows)
+        _relax(D, P, D[:, ka:ka + 2 * BS].copy(), B, ka, rows_mask=rows, cols_mask=mask_out(ka, ka + 2 * BS, n_pad))
+    Dt = torch.from_numpy(np.ascontiguousarray(D[:nsrc, :n]))
+    Pt = torch.from_numpy(np.ascontiguousarray(P[:nsrc, :n]))
+    gD = [None] * world
+    gP = [None] * world
+    dist.all_gather_object(gD, Dt)
+    dist.all_gather_object(gP, Pt)
+    if rank == 0:
+        out.put((np.concatenate([g.numpy() for g in gD]), np.concatenate([g.numpy() for g in gP])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 1000), (4, 1024), (3, 1536)])
+def test_partitioned_pair_schedule_gloo(world, n):
+    """The pair schedule on a pair-aligned partition reproduces the oracle's D bitwise (integer
+    data) with a valid LAST_K P; the rows of a pair are the only data crossing ranks."""
+    for r in range(world):
+        assert fw.fw_dist_partition(n, world, r)[0] % 256 == 0
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main_pairs, args=(r, world, port, n, 9, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    D, P = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    W = gen.generate("er_int_f32", n, 9, p=0.2, lo=1, hi=50)
+    Dref, _ = oracle.fw(W, None)
+    np.testing.assert_array_equal(D, Dref)
+    P = np.where(np.isinf(D) | np.eye(n, dtype=bool), -1, P).astype(np.int32)
+    assert oracle.check_paths(W, D, P, mode="lastk")[0] == 0
