@@ -301,7 +301,8 @@ int sync_stream(Ctx &c, cudaStream_t st) {
   }
 }
 
-// NVTX ranges (host-side enqueue spans per solve / round / phase, for an nsys timeline).
+// NVTX ranges (host-side enqueue spans per solve / round or pair / pivot phases / broadcast,
+// for an nsys timeline: the GPU work of a range is what it enqueued).
 struct Nvtx {
   explicit Nvtx(const char *name) { nvtxRangePushA(name); }
   ~Nvtx() { nvtxRangePop(); }
@@ -736,6 +737,7 @@ struct Rounds {
     TRY(pair_pivot(st, P0));
     if (e.timing) CU(cudaEventRecord(e.ev[3 * P0], st));
     for (int Pp = P0; Pp < NP; ++Pp) {
+      Nvtx nv("pair");
       const bool last = Pp + 1 == NP;
       if (!last) {
         CU(cudaEventRecord(c.xev[Pp], st));            // the previous bulk launch is done
@@ -763,6 +765,7 @@ struct Rounds {
     if (overlap && c.pair_pdl) return run_pairs_pdl(st, e, P0, NP);
     TRY(pair_pivot(st, P0));
     for (int Pp = P0; Pp < NP; ++Pp) {
+      Nvtx nv("pair");
       const bool last = Pp + 1 == NP;
       if (e.timing) CU(cudaEventRecord(e.ev[3 * Pp], st));        // the pair's phase-3 work starts
       if (!last && overlap) {
@@ -816,6 +819,7 @@ struct Rounds {
     CU(cudaEventRecord(e.sync[2 * K0], st));
     CU(cudaStreamWaitEvent(side, e.sync[2 * K0], 0));   // the pivot stream follows round K0's pivot
     for (int K = K0; K < K1; ++K) {
+      Nvtx nv("round");
       if (K + 1 < K1) {
         int nprio = 0;
         TRY(phase3_ordered(st, K, done + K, &nprio));
@@ -853,6 +857,7 @@ struct Rounds {
     TRY(pivot_rest(st, K0));
     if (e.timing) CU(cudaEventRecord(ev[3 * K0 + 1], st));
     for (int K = K0; K < K1; ++K) {
+      Nvtx nv("round");
       if (K + 1 < K1) {
         CU(cudaEventRecord(c.xev[K], st));           // launch K-1 (and round K's pivot) complete
         int nprio = 0;
@@ -972,6 +977,7 @@ struct Team {
 
   // rows [K*BS, (K+nb)*BS) from their owner into strip[slot] of every other rank
   int bcast(int K, int nb, int slot, int side) {
+    Nvtx nv("broadcast");
     Rounds<T, MODE> &x0 = rk[0];
     const int64_t n_pad = x0.n_pad;
     const size_t count = (size_t)nb * BS() * (size_t)n_pad;
@@ -1001,6 +1007,7 @@ struct Team {
   // round K's pivot phases: phase 1 and the row strip on the owner, the broadcast, every rank's
   // column strip (phase1 / the row strip are no-ops on ranks that do not own block K)
   int pivot(int K, int side) {
+    Nvtx nv("pivot phases");
     for (int r = 0; r < W(); ++r) {
       TRY(rk[r].phase1(q(r, side), K));
       mark(e.ev[3 * K], r, side);
@@ -1031,6 +1038,7 @@ struct Team {
     for (int r = 0; r < W(); ++r) TRY(follow(q(r, 1), q(r, 0), ev[1 + W() + r]));   // side follows round 0's pivot
     for (int K = 0; K < R; ++K) {
       if (K + 1 < R) {
+        Nvtx nv("round");
         for (int r = 0; r < W(); ++r) {
           int nprio = 0;
           TRY(rk[r].phase3_ordered(q(r, 0), K, rk[r].done + K, &nprio));
@@ -1053,6 +1061,7 @@ struct Team {
   // pair Pp's pivot path: the owner's pair pivot on its rows, ONE broadcast of rows a, b, the
   // other ranks' columns a, b
   int pair_pivot(int Pp, int side) {
+    Nvtx nv("pair pivot");
     const int a = 2 * Pp;
     for (int r = 0; r < W(); ++r)
       if (rk[r].owns(a)) TRY(rk[r].pair_pivot(q(r, side), Pp));
@@ -1066,6 +1075,7 @@ struct Team {
     const int NP = rk[0].R / 2;
     TRY(pair_pivot(0, 0));
     for (int Pp = 0; Pp < NP; ++Pp) {
+      Nvtx nv("pair");
       const bool last = Pp + 1 == NP;
       for (int r = 0; r < W(); ++r) mark(e.ev[3 * Pp], r, 0);           // the pair's phase-3 work starts
       if (!last) {
@@ -1555,7 +1565,9 @@ int post_pass(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int6
     auto transpose = [&](const T *src, int64_t ld, int64_t rows, int64_t g0) -> int {
       if (rows == 0) return FW_OK;
       dim3 g((unsigned)(n_pad / 32), (unsigned)(rows / 32));
-      transpose_panels_kernel<T><<<g, dim3(32, 8), 0, st>>>(src, ld, rows, n_pad, g0, BS, Dt);
+      auto kern = BS == 32 ? transpose_panels_kernel<T, 32>
+                           : BS == 64 ? transpose_panels_kernel<T, 64> : transpose_panels_kernel<T, 128>;
+      kern<<<g, dim3(32, 8), 0, st>>>(src, ld, rows, n_pad, g0, Dt);
       CU(cudaGetLastError());
       ++g_launches;
       return FW_OK;
@@ -2383,8 +2395,8 @@ int pipe_solve(Ctx &c, const PipeGeom &g, T *dist_h, int32_t *next_h, T *raw, C 
     if (q == 0) {   // the transpose of the whole final D (the search reads column segments)
       TRY(c.ws_tr.ensure((size_t)g.n_pad * g.n_pad * sizeof(C)));
       dim3 gt((unsigned)(g.n_pad / 32), (unsigned)(g.n_pad / 32));
-      transpose_panels_kernel<C><<<gt, dim3(32, 8), 0, st>>>(D, g.ld, g.n_pad, g.n_pad, 0, g.BS,
-                                                           static_cast<C *>(c.ws_tr.p));
+      transpose_panels_kernel<C, 128><<<gt, dim3(32, 8), 0, st>>>(D, g.ld, g.n_pad, g.n_pad, 0,
+                                                                static_cast<C *>(c.ws_tr.p));   // pipeline: BS = 128
       CU(cudaGetLastError());
       ++g_launches;
     }
