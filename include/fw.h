@@ -95,7 +95,9 @@ typedef struct fw_stats {
   double bcast_bytes;   /* bytes those broadcasts moved (per rank, as root or receiver)   */
   int32_t persistent;   /* 1 = the rounds ran as ONE persistent launch (work items ordered by
                            round, per-tile readiness counters): phase3_ms is
-                           that launch (all phases) and phase3_relaxations = n_pad^3        */
+                           that launch (all phases) and phase3_relaxations = n_pad^3; 2 = the
+                           same over a communicator with the pivot-row tiles published through
+                           an NVLS multicast object (one multimem store reaches every rank)  */
 } fw_stats;
 
 /* Create the process-wide context. ngpus_max: the most devices one fw_solve may use,
@@ -121,6 +123,11 @@ int fw_init(int ngpus_max, unsigned flags);
  *                        round in the work order (-1 auto)
  *   "persist_relaxed" 0/1, "persist_quarters" 0/1  persistent: relaxed dependency polls;
  *                        critical-path tiles as 64 x 64 quarter items (one GPU, default 1)
+ *   "nvls"       -1/0/1  persistent over a communicator: publish the pivot-row tiles through an
+ *                        NVLS multicast object when there are several ranks and every device
+ *                        supports it (-1, default; set up collectively, any failure falls back
+ *                        to the IPC peer rings), never (0), or try even with one rank (1: tests
+ *                        the collective setup and its fallback on one GPU)
  *   "async"      0/1     fw_solve_device_* (one GPU) return as soon as the solve is enqueued on
  *                        the caller's stream: no validation kernel and no host round trip, so a
  *                        solve can be captured into a CUDA graph (after one warm-up solve of the

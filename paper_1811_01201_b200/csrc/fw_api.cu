@@ -19,6 +19,7 @@
 #include "fw_persist.cuh"
 #include "../../include/fw.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -182,6 +183,16 @@ struct Ctx {
   DevBuf ws_ver;                   // persistent: per-tile round counters, pub flags, work counter, items
   DevBuf ws_ring;                  // persistent: pivot-row ring(s) (n_pad^2 each) [+ pub flags, NCCL mode]
   DevBuf ws_ipc;                   // persistent NCCL mode: all-gathered IPC handles
+  struct Nvls {                    // persistent NCCL mode: the rings as ONE multicast object (NVLS)
+    bool active = false;
+    CUmemGenericAllocationHandle mc = 0, mem = 0;
+    CUdeviceptr uc = 0, mcva = 0;  // this rank's ring (unicast) and the multicast address of all rings
+    size_t size = 0;
+    int world = 0;
+  } nvls;
+  int nvls_opt = -1;               // -1: the multicast publish when W > 1 and every device supports it,
+                                   // 0: never, 1: also try with one rank (tests the setup / fallback)
+  bool last_nvls = false;          // the last solve published through the multicast object
   std::vector<void *> peer_ring;   // persistent NCCL mode: the peers' rings, IPC-mapped
   std::vector<cudaIpcMemHandle_t> peer_handle;
   ncclComm_t comm = nullptr;       // multi-GPU communicator (fw_comm_init, or the team's)
@@ -1263,10 +1274,20 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
     persist_items(Tn, W, t0, t1, self, gap, &items);
   }
   const size_t items_off = off;
-  off += items.size() * sizeof(unsigned);
+  off += (items.size() * sizeof(unsigned) + 255) / 256 * 256;
+  // FW_PERSIST_TRACE=path (development): every item's {taken, operands ready, done} times and
+  // its SM / CTA, written to `path` after the launch (tools/persist_trace.py reads it)
+  const char *trace_path = getenv("FW_PERSIST_TRACE");
+  const int Qt = W == 1 && c.persist_quarters ? 4 : 1;
+  const long long total_items = W > 1 ? (long long)items.size()
+                                      : 1 + (long long)Qt * 2 * (Tn - 1) +
+                                            (long long)Tn * ((long long)Tn * Tn + (Qt - 1) * (4LL * Tn - 5));
+  const size_t trace_off = off;
+  if (trace_path && *trace_path) off += (size_t)total_items * 32;
   TRY(c.ws_ver.ensure(off));
   char *base = static_cast<char *>(c.ws_ver.p);
   CU(cudaMemsetAsync(base, 0, items_off, st));
+  if (trace_path && *trace_path) CU(cudaMemsetAsync(base + trace_off, 0, (size_t)total_items * 32, st));
   if (!items.empty())
     CU(cudaMemcpyAsync(base + items_off, items.data(), items.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
   PersistArgs a{};
@@ -1283,10 +1304,9 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   a.flags = maxkey - 2;
   a.quarters = W == 1 && c.persist_quarters ? 1 : 0;
   a.qcnt = reinterpret_cast<int *>(base + qcnt_off);
-  const int Q = a.quarters ? 4 : 1;
-  a.total = W > 1 ? (long long)items.size()
-                  : 1 + (long long)Q * 2 * (Tn - 1) + (long long)Tn * ((long long)Tn * Tn + (Q - 1) * (4LL * Tn - 5));
+  a.total = total_items;
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  a.trace = trace_path && *trace_path ? reinterpret_cast<unsigned long long *>(base + trace_off) : nullptr;
   a.sync_relaxed = c.persist_relaxed;
   a.p1_blocked = g_p1_blocked != 0;
   for (int r = 0; r < W; ++r) {
@@ -1301,6 +1321,17 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   ++g_launches;
   CU(cudaGetLastError());
   if (e.timing) CU(cudaEventRecord(e.ev[2], st));
+  if (a.trace) {
+    std::vector<unsigned long long> h((size_t)total_items * 4);
+    CU(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (FILE *f = fopen(trace_path, "wb")) {
+      const long long hdr[8] = {0x46575452, Tn, W, total_items, a.quarters, a.gap, grid, self};
+      fwrite(hdr, sizeof hdr, 1, f);
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   return FW_OK;
 }
 
@@ -1320,6 +1351,175 @@ int run_persistent(Ctx &c, T *D, int32_t *P, int64_t ld, int64_t n_pad, int *max
 // NVLink) with a system-scope release flag — no ncclBroadcast in the rounds. The all-reduces of
 // the next solve's validation order its zeroing after every peer's kernel. NOT run on hardware:
 // the gpurun boxes have one GPU (the protocol is tested by the loopback grid above).
+// ---- NVLS: the pivot-row rings of a communicator as one multicast object --------
+// With NVSwitch multicast (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED) every rank's ring is physical
+// memory bound to ONE multicast object, so the fused publish stores each final pivot-row tile once
+// (multimem.st) and the switch replicates it into every ring — instead of G-1 peer copies through
+// the owner's links. Set up collectively over the communicator: rank 0 creates the
+// object and exports a fabric handle, the others import it, every rank adds its device, binds its
+// ring memory and maps it twice (unicast: its own ring; multicast: the publish address). Any
+// failure on any rank (no multicast support, no fabric handles — e.g. a pool that shows each
+// process one GPU) drops every rank back to the IPC peer rings; the driver API is reached through
+// cudaGetDriverEntryPoint (no link-time libcuda dependency).
+struct CuApi {
+  bool tried = false, ok = false;
+  decltype(&cuDeviceGetAttribute) DeviceGetAttribute;
+  decltype(&cuDeviceGet) DeviceGet;
+  decltype(&cuMulticastGetGranularity) MulticastGetGranularity;
+  decltype(&cuMulticastCreate) MulticastCreate;
+  decltype(&cuMulticastAddDevice) MulticastAddDevice;
+  decltype(&cuMulticastBindMem) MulticastBindMem;
+  decltype(&cuMulticastUnbind) MulticastUnbind;
+  decltype(&cuMemExportToShareableHandle) MemExportToShareableHandle;
+  decltype(&cuMemImportFromShareableHandle) MemImportFromShareableHandle;
+  decltype(&cuMemCreate) MemCreate;
+  decltype(&cuMemRelease) MemRelease;
+  decltype(&cuMemAddressReserve) MemAddressReserve;
+  decltype(&cuMemAddressFree) MemAddressFree;
+  decltype(&cuMemMap) MemMap;
+  decltype(&cuMemUnmap) MemUnmap;
+  decltype(&cuMemSetAccess) MemSetAccess;
+} g_cu;
+
+bool load_cu() {
+  if (g_cu.tried) return g_cu.ok;
+  g_cu.tried = true;
+  bool ok = true;
+  auto get = [&](const char *name, auto &fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      ok = false;
+      return;
+    }
+    fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+  };
+  get("cuDeviceGetAttribute", g_cu.DeviceGetAttribute);
+  get("cuDeviceGet", g_cu.DeviceGet);
+  get("cuMulticastGetGranularity", g_cu.MulticastGetGranularity);
+  get("cuMulticastCreate", g_cu.MulticastCreate);
+  get("cuMulticastAddDevice", g_cu.MulticastAddDevice);
+  get("cuMulticastBindMem", g_cu.MulticastBindMem);
+  get("cuMulticastUnbind", g_cu.MulticastUnbind);
+  get("cuMemExportToShareableHandle", g_cu.MemExportToShareableHandle);
+  get("cuMemImportFromShareableHandle", g_cu.MemImportFromShareableHandle);
+  get("cuMemCreate", g_cu.MemCreate);
+  get("cuMemRelease", g_cu.MemRelease);
+  get("cuMemAddressReserve", g_cu.MemAddressReserve);
+  get("cuMemAddressFree", g_cu.MemAddressFree);
+  get("cuMemMap", g_cu.MemMap);
+  get("cuMemUnmap", g_cu.MemUnmap);
+  get("cuMemSetAccess", g_cu.MemSetAccess);
+  g_cu.ok = ok;
+  return ok;
+}
+
+void nvls_release(Ctx &c) {
+  Ctx::Nvls &v = c.nvls;
+  if (!g_cu.ok) return;
+  if (v.mcva) g_cu.MemUnmap(v.mcva, v.size), g_cu.MemAddressFree(v.mcva, v.size);
+  if (v.uc) g_cu.MemUnmap(v.uc, v.size), g_cu.MemAddressFree(v.uc, v.size);
+  CUdevice dev;
+  if (v.mc && v.mem && g_cu.DeviceGet(&dev, c.dev) == CUDA_SUCCESS) g_cu.MulticastUnbind(v.mc, dev, 0, v.size);
+  if (v.mem) g_cu.MemRelease(v.mem);
+  if (v.mc) g_cu.MemRelease(v.mc);
+  v = Ctx::Nvls{};
+}
+
+// Collective: every rank of c.comm calls it with the same bytes. *ok = the multicast rings are
+// usable on every rank (else all ranks use the IPC peer rings).
+int nvls_setup(Ctx &c, size_t bytes, int W, int self, int *d_scratch, cudaStream_t st, bool *ok) {
+  *ok = false;
+  Ctx::Nvls &v = c.nvls;
+  if (v.active && v.size >= bytes && v.world == W) {
+    *ok = true;
+    return FW_OK;
+  }
+  nvls_release(c);
+  // one collective step: the minimum of every rank's status (1 = fine so far)
+  auto agree = [&](int local, bool *all) -> int {
+    CU(cudaMemcpyAsync(d_scratch, &local, sizeof local, cudaMemcpyHostToDevice, st));
+    NCC(c, g_nccl.AllReduce(d_scratch, d_scratch, 1, ncclInt32, ncclMin, c.comm, st));
+    int r = 0;
+    CU(cudaMemcpyAsync(&r, d_scratch, sizeof r, cudaMemcpyDeviceToHost, st));
+    TRY(sync_stream(c, st));
+    *all = r == 1;
+    return FW_OK;
+  };
+  bool all = false;
+  CUdevice dev = 0;
+  int mcs = 0;
+  const int supported = c.nvls_opt != 0 && load_cu() && g_cu.DeviceGet(&dev, c.dev) == CUDA_SUCCESS &&
+                        g_cu.DeviceGetAttribute(&mcs, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev) == CUDA_SUCCESS &&
+                        mcs == 1;
+  TRY(agree(supported ? 1 : 0, &all));
+  if (!all) return FW_OK;
+  // rank 0: the multicast object and its fabric handle -> every rank
+  struct Blob {
+    int status;
+    unsigned long long size;
+    CUmemFabricHandle h;
+  } blob{};
+  if (self == 0) {
+    CUmulticastObjectProp mp{};
+    mp.numDevices = (unsigned)W;
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+    mp.size = bytes;
+    size_t gran = 0;
+    blob.status = g_cu.MulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS &&
+                  gran > 0;
+    if (blob.status) {
+      mp.size = (bytes + gran - 1) / gran * gran;
+      blob.size = mp.size;
+      blob.status = g_cu.MulticastCreate(&v.mc, &mp) == CUDA_SUCCESS;
+      if (blob.status)
+        blob.status = g_cu.MemExportToShareableHandle(&blob.h, v.mc, CU_MEM_HANDLE_TYPE_FABRIC, 0) == CUDA_SUCCESS;
+    }
+  }
+  TRY(c.ws_ipc.ensure(sizeof(Blob)));
+  CU(cudaMemcpyAsync(c.ws_ipc.p, &blob, sizeof blob, cudaMemcpyHostToDevice, st));
+  NCC(c, g_nccl.Broadcast(c.ws_ipc.p, c.ws_ipc.p, sizeof blob, ncclChar, 0, c.comm, st));
+  CU(cudaMemcpyAsync(&blob, c.ws_ipc.p, sizeof blob, cudaMemcpyDeviceToHost, st));
+  TRY(sync_stream(c, st));
+  if (!blob.status) {
+    nvls_release(c);
+    return FW_OK;
+  }
+  v.size = (size_t)blob.size;
+  int good = 1;
+  if (self != 0) good = g_cu.MemImportFromShareableHandle(&v.mc, &blob.h, CU_MEM_HANDLE_TYPE_FABRIC) == CUDA_SUCCESS;
+  if (good) good = g_cu.MulticastAddDevice(v.mc, dev) == CUDA_SUCCESS;
+  TRY(agree(good, &all));   // every device is added before any memory is bound
+  if (all) {
+    CUmemAllocationProp ap{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = c.dev;
+    CUmemAccessDesc ad{};
+    ad.location = ap.location;
+    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    good = g_cu.MemCreate(&v.mem, v.size, &ap, 0) == CUDA_SUCCESS;
+    if (good) good = g_cu.MulticastBindMem(v.mc, 0, v.mem, 0, v.size, 0) == CUDA_SUCCESS;
+    if (good) good = g_cu.MemAddressReserve(&v.uc, v.size, 0, 0, 0) == CUDA_SUCCESS;
+    if (good) good = g_cu.MemMap(v.uc, v.size, 0, v.mem, 0) == CUDA_SUCCESS;
+    if (good) good = g_cu.MemSetAccess(v.uc, v.size, &ad, 1) == CUDA_SUCCESS;
+    if (good) good = g_cu.MemAddressReserve(&v.mcva, v.size, 0, 0, 0) == CUDA_SUCCESS;
+    if (good) good = g_cu.MemMap(v.mcva, v.size, 0, v.mc, 0) == CUDA_SUCCESS;
+    if (good) good = g_cu.MemSetAccess(v.mcva, v.size, &ad, 1) == CUDA_SUCCESS;
+    TRY(agree(good, &all));
+  }
+  if (!all) {
+    nvls_release(c);
+    return FW_OK;
+  }
+  v.active = true;
+  v.world = W;
+  *ok = true;
+  return FW_OK;
+}
+
 template <typename T, int MODE>
 int run_nccl_persistent(Ctx &c, Rounds<T, MODE> &rk, cudaStream_t st, const Events &e) {
   const int W = rk.world, self = c.rank;
@@ -1327,6 +1527,30 @@ int run_nccl_persistent(Ctx &c, Rounds<T, MODE> &rk, cudaStream_t st, const Even
   const int64_t n_pad = rk.n_pad;
   const int Tn = (int)(n_pad / 128);
   const size_t rb = ((size_t)n_pad * n_pad * sizeof(T) + 255) / 256 * 256, pb = (size_t)Tn * Tn * sizeof(int);
+  int *d_bar = rk.errflags() + 4;   // d_flags[4]: a scratch int for the barrier all-reduce
+  auto barrier = [&]() -> int {
+    NCC(c, g_nccl.AllReduce(d_bar, d_bar, 1, ncclInt32, ncclMax, c.comm, st));
+    return FW_OK;
+  };
+  bool mc = false;
+  c.last_nvls = false;
+  if (W > 1 || c.nvls_opt == 1) TRY(nvls_setup(c, rb + pb, W, self, d_bar, st, &mc));
+  if (getenv("FW_DEBUG")) fprintf(stderr, "[fw] persistent over a communicator: %s publish\n", mc ? "NVLS multicast" : "IPC peer-ring");
+  if (mc) {   // every ring is bound to the multicast object: no IPC exchange, one store per publish
+    std::vector<RankView> v(W);
+    char *uc = reinterpret_cast<char *>(c.nvls.uc), *mca = reinterpret_cast<char *>(c.nvls.mcva);
+    for (int q = 0; q < W; ++q) {
+      int64_t r0, nr;
+      partition(n_pad, W, q, &r0, &nr);
+      v[q] = RankView{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, r0, (int)(r0 / 128),
+                      (int)((r0 + nr) / 128)};
+    }
+    v[self] = RankView{rk.D, rk.P, nullptr, reinterpret_cast<int *>(uc + rb), uc, mca,
+                       reinterpret_cast<int *>(mca + rb), v[self].row0, v[self].t0, v[self].t1};
+    CU(cudaMemsetAsync(uc + rb, 0, pb, st));
+    c.last_nvls = true;
+    return launch_persistent<T, MODE>(c, v, rk.ld, n_pad, rk.maxkey, st, e, self, barrier);
+  }
   TRY(c.ws_ring.ensure(rb + pb));
   // exchange the ring allocations' IPC handles (every solve: 64 B per rank; mapped once per change)
   TRY(c.ws_ipc.ensure((size_t)W * sizeof(cudaIpcMemHandle_t) * 2));
@@ -1361,11 +1585,6 @@ int run_nccl_persistent(Ctx &c, Rounds<T, MODE> &rk, cudaStream_t st, const Even
   v[self].D = rk.D;
   v[self].P = rk.P;
   CU(cudaMemsetAsync(static_cast<char *>(c.ws_ring.p) + rb, 0, pb, st));
-  int *d_bar = rk.errflags() + 4;   // d_flags[4]: a scratch int for the barrier all-reduce
-  auto barrier = [&]() -> int {
-    NCC(c, g_nccl.AllReduce(d_bar, d_bar, 1, ncclInt32, ncclMax, c.comm, st));
-    return FW_OK;
-  };
   return launch_persistent<T, MODE>(c, v, rk.ld, n_pad, rk.maxkey, st, e, self, barrier);
 }
 
@@ -1399,6 +1618,7 @@ int run_rounds(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, int
   c.last_pairs = false;
   c.last_pdl = false;
   c.last_persist = false;
+  c.last_nvls = false;
   if (tr == T_LOOPBACK && c.persistent == 1 && BS == 128 && (int)rk.size() <= kMaxRanks) {
     c.last_persist = true;
     return run_loopback_persistent<T, MODE>(c, rk, st, ev);
@@ -1844,7 +2064,7 @@ int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, i
     s.path_mode = path_mode;
     s.p_method = used.mode;
     s.compute_f32 = (used.f32 || !int_t) ? 1 : 0;
-    s.persistent = c.last_persist ? 1 : 0;
+    s.persistent = c.last_persist ? (c.last_nvls ? 2 : 1) : 0;
     s.kernel_launches = g_launches - launches0;
     c.stats = s;
     c.has_stats = true;
@@ -1875,7 +2095,7 @@ int solve_placed(Ctx &c, std::vector<Part<T>> &parts, Transport tr, int world, i
   s.solve_ms = ms;
   // bulk phase-3 launches issued: one per pair of rounds with pairs, else one per round
   s.phase3_launches = c.last_persist ? 1 : c.last_pairs ? R / 2 : R;
-  s.persistent = c.last_persist ? 1 : 0;
+  s.persistent = c.last_persist ? (c.last_nvls ? 2 : 1) : 0;
   s.broadcasts = g_bcasts - bcasts0;
   s.bcast_bytes = g_bcast_bytes - bcast_bytes0;
   s.kernel_launches = g_launches - launches0;
@@ -2606,6 +2826,7 @@ void ctx_release(Ctx *c) {
   cudaSetDevice(c->dev);
   if (c->comm) g_nccl.CommDestroy(c->comm);
   c->comm = nullptr;
+  nvls_release(*c);
   for (void *pr : c->peer_ring)
     if (pr) cudaIpcCloseMemHandle(pr);
   c->peer_ring.clear();
@@ -2896,6 +3117,7 @@ int fw_set_option(const char *name, int value) {
   else if (k == "persist_relaxed" && (value == 0 || value == 1)) c.persist_relaxed = value;
   else if (k == "async" && (value == 0 || value == 1)) c.async = value != 0;
   else if (k == "persist_quarters" && (value == 0 || value == 1)) c.persist_quarters = value;
+  else if (k == "nvls" && value >= -1 && value <= 1) c.nvls_opt = value;
   else return fail(FW_EINVAL, "unknown option or value: %s = %d", name, value);
   return FW_OK;
 }
@@ -3089,6 +3311,7 @@ int fw_comm_free(void) {
     cudaDeviceSynchronize();
     g_nccl.CommDestroy(g_ctx->comm);
   }
+  nvls_release(*g_ctx);
   g_ctx->comm = nullptr;
   g_ctx->comm_dead = false;
   g_ctx->rank = 0;

@@ -81,6 +81,8 @@ struct PersistArgs {
   int p1_blocked;          // PLAIN / TAG phase 1 as the blocked closure (phase1_blocked_body)
   int quarters;            // one GPU: critical-path tiles as four 64 x 64 items (persist_decode)
   int *qcnt;               // per-tile count of finished quarters (zeroed)
+  unsigned long long *trace;   // per item {taken, operands ready, done} (%globaltimer ns) and
+                               // (smid << 32 | blockIdx.x), or null (env FW_PERSIST_TRACE)
   RankView rk[kMaxRanks];
 };
 
@@ -194,6 +196,24 @@ __device__ __forceinline__ void persist_publish(const PersistArgs &a, int self, 
   const RankView &o = a.rk[self];
   const T *src = static_cast<const T *>(o.D) + (int64_t)(K * 128 - o.row0) * a.ld + J * 128;
   const int64_t dst_off = (int64_t)K * 128 * a.ldr + J * 128;
+  if (o.ring_mc) {   // NVLS: one multimem store per vector, replicated into every rank's ring
+    float *dst = reinterpret_cast<float *>(static_cast<T *>(o.ring_mc) + dst_off);
+    for (int e = threadIdx.x; e < 128 * 32; e += kThreads) {
+      const int row = e >> 5, c4 = (e & 31) * 4;
+      const V x = __ldcg(reinterpret_cast<const V *>(src + (int64_t)row * a.ld + c4));
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(dst + (int64_t)row * a.ldr + c4),
+                   "f"(__int_as_float(Num<T>::bits(x.x))), "f"(__int_as_float(Num<T>::bits(x.y))),
+                   "f"(__int_as_float(Num<T>::bits(x.z))), "f"(__int_as_float(Num<T>::bits(x.w)))
+                   : "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      int *f = o.pub_mc + (int64_t)K * a.T + J;
+      asm volatile("multimem.st.release.sys.global.b32 [%0], %1;" ::"l"(f), "r"(K + 1) : "memory");
+    }
+    return;
+  }
   for (int q = 0; q < a.world; ++q) {
     if (q == self) continue;
     T *dst = static_cast<T *>(a.rk[q].ring) + dst_off;
@@ -240,6 +260,8 @@ fw_persistent_kernel(const PersistArgs a) {
   __shared__ Item s_cur;
   __shared__ long long s_next;
   __shared__ TileSrc<T> s_src;   // the current tile's operand origins (tile_mainloop)
+  __shared__ long long s_it;     // the current item's index (trace)
+  __shared__ unsigned long long s_t0, s_t1;
   using S = TileShape<128, 128>;
   const int tid = threadIdx.x;
   if (tid == 0) s_next = (long long)atomicAdd(a.next, 1ull);
@@ -248,6 +270,7 @@ fw_persistent_kernel(const PersistArgs a) {
     if (tid == 0) {
       const long long it = s_next;
       if (it < a.total) {
+        if (a.trace) s_it = it, s_t0 = globaltimer();
         s_next = (long long)atomicAdd(a.next, 1ull);
         const Item w = a.items ? unpack_item(a.items[it]) : persist_decode(a, it);
         s_cur = w;
@@ -320,6 +343,7 @@ fw_persistent_kernel(const PersistArgs a) {
       }
     }
     __syncthreads();
+    if (a.trace && tid == 0) s_t1 = globaltimer();
     if (w.type == IT_P1) {
       persist_phase1<T, MODE>(a, v, w.K, smem_raw);
     } else if (w.type == IT_QTILE) {
@@ -360,6 +384,15 @@ fw_persistent_kernel(const PersistArgs a) {
         last = (atomicAdd(a.qcnt + (int64_t)e.I * a.T + e.J, 1) & 3) == 3;
       }
       if (last) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(vp), "r"(e.K + 1) : "memory");
+      if (a.trace) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long *rec = a.trace + 4 * s_it;
+        rec[0] = s_t0;
+        rec[1] = s_t1;
+        rec[2] = globaltimer();
+        rec[3] = ((unsigned long long)smid << 32) | blockIdx.x;
+      }
     }
   }
 }

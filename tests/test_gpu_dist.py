@@ -138,7 +138,7 @@ def test_loopback_fallback_to_tags():
     np.testing.assert_array_equal(P, np.where(i == j, i, (i + 1) % 700))
 
 
-def _nccl_one_rank(W, block, path="next", timing=True, persistent=None):
+def _nccl_one_rank(W, block, path="next", timing=True, persistent=None, nvls=None):
     """fw_dist_solve_device_* over a ONE-rank NCCL communicator: the NCCL data plane runs
     (every round's pivot strip through ncclBroadcast, validation / placement / key checks
     through ncclAllReduce, the TAG post-pass gather through grouped broadcasts)."""
@@ -151,6 +151,8 @@ def _nccl_one_rank(W, block, path="next", timing=True, persistent=None):
         fw.fw_comm_init(uid, 0, 1)
         if persistent is not None:
             fw.fw_set_option("persistent", persistent)
+        if nvls is not None:
+            fw.fw_set_option("nvls", nvls)
         row0, nrows = fw.fw_dist_partition(n, 1, 0)
         assert (row0, nrows) == (0, n)
         dD = torch.from_numpy(W).cuda()
@@ -321,4 +323,20 @@ def test_nccl_single_rank_persistent(kind, n, path):
     exact = exact_data(W)
     assert_D_matches(D, oracle.fw(W, None)[0], exact)
     bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5, mode=path)
+    assert bad == 0, (bad, divmod(first, n))
+
+
+@pytest.mark.parametrize("kind,n", [("complete_int", 1000), ("complete_real", 640)])
+def test_nccl_single_rank_persistent_nvls_setup(kind, n):
+    """fw_set_option("nvls", 1): the collective NVLS setup (support check agreed over the
+    communicator, multicast object + fabric handle from rank 0, bind and map on every rank) runs
+    even with one rank. Where the pool cannot create a multicast object (one GPU per process) every
+    rank falls back to the IPC peer rings; either way the solve is correct (persistent = 2: the
+    multicast publish, 1: the peer rings)."""
+    W = gen.generate(kind, n, 70 + n)
+    D, P, s = _nccl_one_rank(W, 128, "next", persistent=1, nvls=1)
+    assert s.persistent in (1, 2)
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5)
     assert bad == 0, (bad, divmod(first, n))
