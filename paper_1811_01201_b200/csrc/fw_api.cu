@@ -1283,11 +1283,11 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
                                       : 1 + (long long)Qt * 2 * (Tn - 1) +
                                             (long long)Tn * ((long long)Tn * Tn + (Qt - 1) * (4LL * Tn - 5));
   const size_t trace_off = off;
-  if (trace_path && *trace_path) off += (size_t)total_items * 32;
+  if (trace_path && *trace_path) off += (size_t)total_items * 64;
   TRY(c.ws_ver.ensure(off));
   char *base = static_cast<char *>(c.ws_ver.p);
   CU(cudaMemsetAsync(base, 0, items_off, st));
-  if (trace_path && *trace_path) CU(cudaMemsetAsync(base + trace_off, 0, (size_t)total_items * 32, st));
+  if (trace_path && *trace_path) CU(cudaMemsetAsync(base + trace_off, 0, (size_t)total_items * 64, st));
   if (!items.empty())
     CU(cudaMemcpyAsync(base + items_off, items.data(), items.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
   PersistArgs a{};
@@ -1322,11 +1322,11 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   CU(cudaGetLastError());
   if (e.timing) CU(cudaEventRecord(e.ev[2], st));
   if (a.trace) {
-    std::vector<unsigned long long> h((size_t)total_items * 4);
+    std::vector<unsigned long long> h((size_t)total_items * 8);
     CU(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (FILE *f = fopen(trace_path, "wb")) {
-      const long long hdr[8] = {0x46575452, Tn, W, total_items, a.quarters, a.gap, grid, self};
+      const long long hdr[8] = {0x46575453, Tn, W, total_items, a.quarters, a.gap, grid, self};
       fwrite(hdr, sizeof hdr, 1, f);
       fwrite(h.data(), 8, h.size(), f);
       fclose(f);

@@ -22,8 +22,8 @@ ap.add_argument("--bins", type=int, default=40)
 a = ap.parse_args()
 raw = np.fromfile(a.path, dtype=np.int64)
 magic, T, W, total, quarters, gap, grid, self_ = raw[:8]
-assert magic == 0x46575452 and W == 1, "one-GPU traces only"
-rec = raw[8:].reshape(-1, 4).astype(np.uint64)
+assert magic == 0x46575453 and W == 1, "one-GPU traces only"
+rec = raw[8:].reshape(-1, 8).astype(np.uint64)
 items = fw.fw_persist_schedule(a.n, 1, -3 if quarters else -2, int(gap))
 m = min(len(items), len(rec))
 rec = rec[:m]
@@ -53,6 +53,14 @@ for t in (1, 2, 3):
         per[names[t]] = {"count": int(s.sum()), "mean_compute_us": float((t2 - t1)[s].mean()),
                          "mean_wait_us": float((t1 - t0)[s].mean()), "max_wait_us": float((t1 - t0)[s].max())}
 out["per_type"] = per
+# the steps between taking a tile and starting it (thread 0's clock): decode (incl. the next
+# index's atomic), the barrier after it, the dependency polls, the barrier after them
+ta = (rec[:, 4].astype(np.float64) - base) / 1e3
+tb = (rec[:, 5].astype(np.float64) - base) / 1e3
+tc = (rec[:, 6].astype(np.float64) - base) / 1e3
+s = ok & (typ == 2)
+out["tile_take_to_start_us"] = {"decode_and_atomic": float((ta - t0)[s].mean()), "barrier1": float((tb - ta)[s].mean()),
+                                "polls": float((tc - tb)[s].mean()), "barrier2": float((t1 - tc)[s].mean())}
 p1 = ok & (typ == 1)
 p1_done = np.sort(t2[p1])
 out["p1_done_interval_us"] = {"mean": float(np.diff(p1_done).mean()) if len(p1_done) > 1 else None,
