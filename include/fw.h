@@ -121,8 +121,8 @@ int fw_init(int ngpus_max, unsigned flags);
  *                        solves), 0 off, 1 on (env FW_PERSISTENT)
  *   "persist_gap" k >= 0 persistent: phase-3 tiles between phase 1 and phase 2 of the next
  *                        round in the work order (-1 auto)
- *   "persist_relaxed" 0/1, "persist_quarters" 0/1  persistent: relaxed dependency polls;
- *                        critical-path tiles as 64 x 64 quarter items (one GPU, default 1)
+ *   "persist_relaxed" 0/1, "persist_quarters" -1/0/1  persistent: relaxed dependency polls;
+ *                        critical-path tiles as 64 x 64 quarter items (one GPU; -1 auto: n < 4096)
  *   "nvls"       -1/0/1  persistent over a communicator: publish the pivot-row tiles through an
  *                        NVLS multicast object when there are several ranks and every device
  *                        supports it (-1, default; set up collectively, any failure falls back

@@ -174,7 +174,8 @@ struct Ctx {
   int persistent = -1;             // one persistent launch per solve (fw_persist.cuh): -1 auto, 0 off, 1 on
   int persist_gap = -1;            // persistent: rest tiles between P1(K+1) and P2(K+1) (-1 auto)
   int persist_relaxed = 0;         // persistent: dependency polls with relaxed loads (A/B option)
-  int persist_quarters = 1;        // persistent, one GPU: critical-path tiles as 64 x 64 quarter items
+  int persist_quarters = -1;       // persistent, one GPU: critical-path tiles as 64 x 64 quarter items
+                                   // (-1 auto: when T < 32 tiles per side, i.e. n < 4096)
   bool last_persist = false;       // the last solve ran as one persistent launch
   bool async = false;              // device entry: no validation, no host synchronisation (fw_set_option)
   bool in_host_entry = false;      // inside fw_solve / fw_solve_i32 (async never applies there)
@@ -1278,7 +1279,11 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   // FW_PERSIST_TRACE=path (development): every item's {taken, operands ready, done} times and
   // its SM / CTA, written to `path` after the launch (tools/persist_trace.py reads it)
   const char *trace_path = getenv("FW_PERSIST_TRACE");
-  const int Qt = W == 1 && c.persist_quarters ? 4 : 1;
+  // quarters shorten the per-round pivot chain, which bounds small solves (n = 2048: 2.07 -> 1.50
+  // ms, n = 3072: 3.37 -> 2.78 ms); at T = 32 (C2) the chain and the phase-3 work are balanced and
+  // the smaller items cost more than they save (5.66 vs 5.70 ms, profiles/r02c_persist_quarters_ab.jsonl)
+  const bool quarters = W == 1 && (c.persist_quarters < 0 ? Tn < 32 : c.persist_quarters != 0);
+  const int Qt = quarters ? 4 : 1;
   const long long total_items = W > 1 ? (long long)items.size()
                                       : 1 + (long long)Qt * 2 * (Tn - 1) +
                                             (long long)Tn * ((long long)Tn * Tn + (Qt - 1) * (4LL * Tn - 5));
@@ -1302,7 +1307,7 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   a.next = reinterpret_cast<unsigned long long *>(base + next_off);
   a.maxkey = maxkey;
   a.flags = maxkey - 2;
-  a.quarters = W == 1 && c.persist_quarters ? 1 : 0;
+  a.quarters = quarters ? 1 : 0;
   a.qcnt = reinterpret_cast<int *>(base + qcnt_off);
   a.total = total_items;
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
@@ -3116,7 +3121,7 @@ int fw_set_option(const char *name, int value) {
   else if (k == "persist_gap" && value >= -1) c.persist_gap = value;
   else if (k == "persist_relaxed" && (value == 0 || value == 1)) c.persist_relaxed = value;
   else if (k == "async" && (value == 0 || value == 1)) c.async = value != 0;
-  else if (k == "persist_quarters" && (value == 0 || value == 1)) c.persist_quarters = value;
+  else if (k == "persist_quarters" && value >= -1 && value <= 1) c.persist_quarters = value;
   else if (k == "nvls" && value >= -1 && value <= 1) c.nvls_opt = value;
   else return fail(FW_EINVAL, "unknown option or value: %s = %d", name, value);
   return FW_OK;

@@ -1,0 +1,6 @@
+#!/bin/bash
+O=gpurun_out/quarters
+mkdir -p $O
+timeout 600 python tools/ab_options.py --config C2 --sets "persist_quarters=0;persist_quarters=1;persist_quarters=0;persist_quarters=1;persist_quarters=0;persist_quarters=1;persist_quarters=0,persist_gap=600;persist_quarters=0,persist_gap=900" --reps 15 > $O/ab_c2.jsonl 2>&1
+timeout 600 python tools/ab_options.py --config C2 --n 3072 --sets "persist_quarters=0;persist_quarters=1;persist_quarters=0;persist_quarters=1" --reps 15 > $O/ab_n3072.jsonl 2>&1
+timeout 600 python tools/ab_options.py --config C2 --n 2048 --sets "persist_quarters=0;persist_quarters=1;persist_quarters=0;persist_quarters=1" --reps 15 > $O/ab_n2048.jsonl 2>&1
