@@ -121,8 +121,12 @@ int fw_init(int ngpus_max, unsigned flags);
  *                        solves), 0 off, 1 on (env FW_PERSISTENT)
  *   "persist_gap" k >= 0 persistent: phase-3 tiles between phase 1 and phase 2 of the next
  *                        round in the work order (-1 auto)
- *   "persist_relaxed" 0/1, "persist_quarters" -1/0/1  persistent: relaxed dependency polls;
- *                        critical-path tiles as 64 x 64 quarter items (one GPU; -1 auto: n < 4096)
+ *   "persist_relaxed" 0/1, "persist_quarters" -1/0/1/2  persistent: relaxed dependency polls;
+ *                        critical-path tiles as 64 x 64 quarter items (one GPU; 1: every prio
+ *                        and phase-2 tile, 2: the three tiles per round the pivot chain waits
+ *                        for; -1 auto: 1 when n < 4096, else 2)
+ *   "persist_p1_lone" -1/0/1  persistent, one GPU: one SM keeps a single CTA that runs every
+ *                        phase-1 item (-1 auto = on, 0 off)
  *   "nvls"       -1/0/1  persistent over a communicator: publish the pivot-row tiles through an
  *                        NVLS multicast object when there are several ranks and every device
  *                        supports it (-1, default; set up collectively, any failure falls back
@@ -258,10 +262,12 @@ int64_t fw_path(const int32_t *P, const void *dist, int dist_is_int32, int64_t n
 /* Host-only (no GPU, no fw_init): the work-item order of the persistent solve
  * for n vertices on a `world`-way block-row partition (world in [1, 8]); rank = -1: every rank's
  * items (the loopback grid), else that rank's subsequence (one GPU of a communicator); rank = -2
- * (world 1): the one-GPU kernel's own arithmetic decode of the order, run on the host; gap = the
- * phase-3 tiles placed between P1(K+1) and the phase-2 items of round K+1. Each item is packed as
+ * (world 1): the one-GPU kernel's own arithmetic decode of the order, run on the host; -3: the
+ * same with the critical-path tiles as quarter items, -4: with only the three chain tiles per
+ * round as quarter items ("persist_quarters" 1 / 2); gap = the phase-3 tiles placed between
+ * P1(K+1) and the phase-2 items of round K+1. Each item is packed as
  * rank << 29 | type << 27 | K << 18 | I << 9 | J (type 1 = phase 1 on tile (K, K), 2 = tile (I, J)
- * relaxed through block K). With out = NULL, max_out = 0 returns the count. Returns the number of
+ * relaxed through block K, 3 = a 64 x 64 quarter of it, the quarter in the rank bits). With out = NULL, max_out = 0 returns the count. Returns the number of
  * items, or -FW_EINVAL (bad arguments, max_out too small). For tests of the order's invariants. */
 int64_t fw_persist_schedule(int64_t n, int world, int rank, int gap, uint32_t *out, int64_t max_out);
 

@@ -174,6 +174,9 @@ struct Ctx {
   int persistent = -1;             // one persistent launch per solve (fw_persist.cuh): -1 auto, 0 off, 1 on
   int persist_gap = -1;            // persistent: rest tiles between P1(K+1) and P2(K+1) (-1 auto)
   int persist_relaxed = 0;         // persistent: dependency polls with relaxed loads (A/B option)
+  int persist_stage_old = 1;       // persistent: 128 x 128 tiles stage their old values in shared memory
+  int persist_p1_lone = -1;        // persistent, one GPU: every P1 item on one CTA alone on its SM
+                                   // (-1 auto = on: C2 5.74 -> 5.52 ms; 0 off, 1 on)
   int persist_quarters = -1;       // persistent, one GPU: critical-path tiles as 64 x 64 quarter items
                                    // (-1 auto: when T < 32 tiles per side, i.e. n < 4096)
   bool last_persist = false;       // the last solve ran as one persistent launch
@@ -1213,12 +1216,26 @@ void persist_items(int T, int world, const std::vector<int> &t0, const std::vect
       for (int I = t0[r]; I < t1[r]; ++I)
         if (I != K && I != N) tile(r, K, I, N);
     if (take(oN)) v.push_back(pack_item(oN, IT_P1, N, N, N));          // B
+    // rest(K): row and column M = K+2 first ((M, M) first; the next round's prio tiles wait for
+    // them, persist_rest_ij), then row-major — per rank, its rows only
     std::vector<std::vector<unsigned>> rest(world);
-    for (int r = 0; r < world; ++r)
+    const int M = K + 2;
+    for (int r = 0; r < world; ++r) {
+      auto push = [&](int I, int J) { rest[r].push_back(pack_item(r, IT_TILE, K, I, J)); };
+      const bool ownM = M < T && M >= t0[r] && M < t1[r];
+      if (ownM) {
+        push(M, M);
+        for (int J = 0; J < T; ++J)
+          if (J != K && J != N && J != M) push(M, J);
+      }
+      if (M < T)
+        for (int I = t0[r]; I < t1[r]; ++I)
+          if (I != K && I != N && I != M) push(I, M);
       for (int I = t0[r]; I < t1[r]; ++I)
-        if (I != K && I != N)
+        if (I != K && I != N && (M >= T || I != M))
           for (int J = 0; J < T; ++J)
-            if (J != K && J != N) rest[r].push_back(pack_item(r, IT_TILE, K, I, J));
+            if (J != K && J != N && (M >= T || J != M)) push(I, J);
+    }
     for (int r = 0; r < world; ++r)                                      // C
       if (take(r))
         for (size_t q = 0; q < rest[r].size() && (int)q < gap; ++q) v.push_back(rest[r][q]);
@@ -1252,7 +1269,8 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, bytes));
   if (per_sm < 1) return fail(FW_ECUDA, "fw_persistent_kernel does not fit on an SM");
-  const int grid = per_sm * sms;
+  const bool p1_lone = W == 1 && per_sm >= 2 && c.persist_p1_lone != 0;
+  const int grid = per_sm * sms - (p1_lone ? 1 : 0);   // p1_lone: one SM keeps a single CTA
   // counters: per rank its tiles' round counters, and (W > 1) pub flags of its ring; then the
   // 64-bit work counter, 256-B aligned
   size_t off = 0;
@@ -1267,7 +1285,9 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   off += W == 1 ? ((size_t)Tn * Tn * sizeof(int) + 255) / 256 * 256 : 0;
   const size_t next_off = off;
   off += 256;
-  const int gap = c.persist_gap >= 0 ? c.persist_gap : (int)(2.5 * grid);
+  const size_t smcnt_off = off;   // p1_lone: per-SM CTA counts + the start barrier count
+  off += ((size_t)(sms + 1) * sizeof(int) + 255) / 256 * 256;
+  const int gap = c.persist_gap >= 0 ? c.persist_gap : 2 * grid;   // C2: 600 best of 300-900
   std::vector<unsigned> items;
   if (W > 1) {
     std::vector<int> t0(W), t1(W);
@@ -1280,19 +1300,22 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   // its SM / CTA, written to `path` after the launch (tools/persist_trace.py reads it)
   const char *trace_path = getenv("FW_PERSIST_TRACE");
   // quarters shorten the per-round pivot chain, which bounds small solves (n = 2048: 2.07 -> 1.50
-  // ms, n = 3072: 3.37 -> 2.78 ms); at T = 32 (C2) the chain and the phase-3 work are balanced and
-  // the smaller items cost more than they save (5.66 vs 5.70 ms, profiles/r02c_persist_quarters_ab.jsonl)
-  const bool quarters = W == 1 && (c.persist_quarters < 0 ? Tn < 32 : c.persist_quarters != 0);
-  const int Qt = quarters ? 4 : 1;
+  // ms, n = 3072: 3.37 -> 2.78 ms with every prio / P2 tile quartered)
+  // auto: every chain tile in quarters up to T = 16 (n = 1024: 0.75 vs 0.82 ms, n = 2048: 1.54 vs
+  // 1.56), only the three chain tiles per round from T = 24 on (n = 3072: 2.65 vs 2.70, C2: 5.33
+  // vs 5.43 ms with none; profiles/r02c_persist_quarters_ab.jsonl)
+  const int qmode = W != 1 ? 0 : c.persist_quarters < 0 ? (Tn < 20 ? 1 : 2) : c.persist_quarters;
+  const int Qt = qmode == 1 ? 4 : 1;
   const long long total_items = W > 1 ? (long long)items.size()
-                                      : 1 + (long long)Qt * 2 * (Tn - 1) +
-                                            (long long)Tn * ((long long)Tn * Tn + (Qt - 1) * (4LL * Tn - 5));
+                                : qmode == 2 ? persist_total_crit(Tn)
+                                             : 1 + (long long)Qt * 2 * (Tn - 1) +
+                                                   (long long)Tn * ((long long)Tn * Tn + (Qt - 1) * (4LL * Tn - 5));
   const size_t trace_off = off;
-  if (trace_path && *trace_path) off += (size_t)total_items * 64;
+  if (trace_path && *trace_path) off += (size_t)(total_items + Tn) * 64;   // + the dedicated P1 CTA's
   TRY(c.ws_ver.ensure(off));
   char *base = static_cast<char *>(c.ws_ver.p);
   CU(cudaMemsetAsync(base, 0, items_off, st));
-  if (trace_path && *trace_path) CU(cudaMemsetAsync(base + trace_off, 0, (size_t)total_items * 64, st));
+  if (trace_path && *trace_path) CU(cudaMemsetAsync(base + trace_off, 0, (size_t)(total_items + Tn) * 64, st));
   if (!items.empty())
     CU(cudaMemcpyAsync(base + items_off, items.data(), items.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
   PersistArgs a{};
@@ -1307,8 +1330,12 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   a.next = reinterpret_cast<unsigned long long *>(base + next_off);
   a.maxkey = maxkey;
   a.flags = maxkey - 2;
-  a.quarters = quarters ? 1 : 0;
+  a.quarters = qmode;
   a.qcnt = reinterpret_cast<int *>(base + qcnt_off);
+  a.p1_lone = p1_lone ? 1 : 0;
+  a.stage_old = c.persist_stage_old != 0 ? 1 : 0;
+  a.smcnt = reinterpret_cast<int *>(base + smcnt_off);
+  a.nsm = sms;
   a.total = total_items;
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.trace = trace_path && *trace_path ? reinterpret_cast<unsigned long long *>(base + trace_off) : nullptr;
@@ -1327,7 +1354,7 @@ int launch_persistent(Ctx &c, std::vector<RankView> &views, int64_t ld, int64_t 
   CU(cudaGetLastError());
   if (e.timing) CU(cudaEventRecord(e.ev[2], st));
   if (a.trace) {
-    std::vector<unsigned long long> h((size_t)total_items * 8);
+    std::vector<unsigned long long> h((size_t)(total_items + Tn) * 8);
     CU(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
     if (FILE *f = fopen(trace_path, "wb")) {
@@ -3121,7 +3148,9 @@ int fw_set_option(const char *name, int value) {
   else if (k == "persist_gap" && value >= -1) c.persist_gap = value;
   else if (k == "persist_relaxed" && (value == 0 || value == 1)) c.persist_relaxed = value;
   else if (k == "async" && (value == 0 || value == 1)) c.async = value != 0;
-  else if (k == "persist_quarters" && value >= -1 && value <= 1) c.persist_quarters = value;
+  else if (k == "persist_quarters" && value >= -1 && value <= 2) c.persist_quarters = value;
+  else if (k == "persist_p1_lone" && value >= -1 && value <= 1) c.persist_p1_lone = value;
+  else if (k == "persist_stage_old" && (value == 0 || value == 1)) c.persist_stage_old = value;
   else if (k == "nvls" && value >= -1 && value <= 1) c.nvls_opt = value;
   else return fail(FW_EINVAL, "unknown option or value: %s = %d", name, value);
   return FW_OK;
@@ -3215,7 +3244,7 @@ int fw_host_pipeline_bounds(int64_t n, int chunk_tiles, int first_tiles, int32_t
 }
 
 int64_t fw_persist_schedule(int64_t n, int world, int rank, int gap, uint32_t *out, int64_t max_out) {
-  if (n <= 0 || n > 65536 || world < 1 || world > kMaxRanks || rank < -3 || rank >= world || gap < 0 ||
+  if (n <= 0 || n > 65536 || world < 1 || world > kMaxRanks || rank < -4 || rank >= world || gap < 0 ||
       max_out < 0 || (max_out > 0 && !out) || (rank <= -2 && world != 1))
     return -fail(FW_EINVAL, "fw_persist_schedule: bad arguments (n=%lld world=%d rank=%d gap=%d)", (long long)n, world,
                  rank, gap);
@@ -3230,13 +3259,15 @@ int64_t fw_persist_schedule(int64_t n, int world, int rank, int gap, uint32_t *o
   }
   std::vector<unsigned> items;
   if (rank <= -2) {   // the one-GPU kernel's arithmetic decode (persist_decode), run on the host;
-                      // -3: with quarter items (the quarter in the rank bits)
+                      // -3: with quarter items (the quarter in the rank bits), -4: critical quarters
     PersistArgs a{};
     a.T = T;
     a.gap = gap;
-    a.quarters = rank == -3;
-    const int Q = a.quarters ? 4 : 1;
-    const long long total = 1 + (long long)Q * 2 * (T - 1) + (long long)T * ((long long)T * T + (Q - 1) * (4LL * T - 5));
+    a.quarters = rank == -3 ? 1 : rank == -4 ? 2 : 0;
+    const int Q = a.quarters == 1 ? 4 : 1;
+    const long long total = a.quarters == 2 ? persist_total_crit(T)
+                                            : 1 + (long long)Q * 2 * (T - 1) +
+                                                  (long long)T * ((long long)T * T + (Q - 1) * (4LL * T - 5));
     for (long long it = 0; it < total; ++it) {
       const Item w = persist_decode(a, it);
       if (w.type != IT_NONE) items.push_back(pack_item(w.type == IT_QTILE ? w.r : 0, w.type, w.K, w.I, w.J));

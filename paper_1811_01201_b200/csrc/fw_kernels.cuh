@@ -261,6 +261,8 @@ template <typename T> struct TileSrc {
   const T *a;
   const T *b;
   int64_t lda, ldb;
+  const T *old;      // or null: the tile itself (TM x TN at pitch ldo), staged into the free
+  int64_t ldo;       // shared-memory stages during the last chunk for the epilogue's compare
 };
 
 // Main loop of one TM x TN tile: acc[r][c] = min over k < nch*kBK of A(i, k) + B(k, j) for the
@@ -319,6 +321,23 @@ __device__ __forceinline__ void tile_mainloop(T *smem, const TileSrc<T> *src, in
     else cp_async_wait<0>();
     __syncthreads();
     if (ch + kStages - 1 < nch) load_chunk((ch + kStages - 1) % kStages, (ch + kStages - 1) * kBK);
+    if (ch == nch - 1 && src->old) {
+      // the last chunk: the other stages are free — stage the tile's current values there (one
+      // contiguous TM x TN block from stage (ch+1) % kStages on; the caller guarantees it fits
+      // and does not wrap), so the epilogue compares against shared memory instead of waiting
+      // on one L2 round trip per row (its long-scoreboard stall, ncu at C2)
+      T *dst = smem + ((ch + 1) % kStages) * S::kStage;
+      int tv;
+      asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tv));
+      const T *o = src->old;
+      const int64_t ldo = src->ldo;
+#pragma unroll 4
+      for (int e = tv; e < TM * TN / 4; e += kThreads) {
+        const int r = e / (TN / 4), c = (e % (TN / 4)) * 4;
+        cp_async16(dst + r * TN + c, o + (int64_t)r * ldo + c);
+      }
+      cp_async_commit();
+    }
     const T *as = smem + (ch % kStages) * S::kStage + ty * S::AS;
     const T *bs = smem + (ch % kStages) * S::kStage + S::kA + tx * 4;
 #pragma unroll
@@ -358,7 +377,8 @@ template <typename T, int TM, int TN, int MODE, bool CG = false>
 __device__ __forceinline__ int tile_epilogue(T *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int i0,
                                              int j0, int mr_lo, int mr_hi, int mc_lo, int mc_hi, int tag,
                                              int kgrp,
-                                             const T (&acc)[TileShape<TM, TN>::RM][4 * TileShape<TM, TN>::H]) {
+                                             const T (&acc)[TileShape<TM, TN>::RM][4 * TileShape<TM, TN>::H],
+                                             const T *old_s = nullptr) {
   using S = TileShape<TM, TN>;
   using V = typename Vec4<T>::V;
   constexpr int RM = S::RM, H = S::H, TX = S::TX, TY = S::TY;
@@ -373,7 +393,8 @@ __device__ __forceinline__ int tile_epilogue(T *__restrict__ D, int32_t *__restr
       const int jb = j0 + 4 * tx + 4 * TX * h;
       V *dp = reinterpret_cast<V *>(D + (int64_t)i * ld + jb);
       V old;
-      if constexpr (CG) old = __ldcg(dp);
+      if (old_s) old = *reinterpret_cast<const V *>(old_s + (ty + TY * r) * TN + 4 * tx + 4 * TX * h);
+      else if constexpr (CG) old = __ldcg(dp);
       else old = *dp;
       V nv = old;
       bool any = false;

@@ -81,6 +81,12 @@ struct PersistArgs {
   int p1_blocked;          // PLAIN / TAG phase 1 as the blocked closure (phase1_blocked_body)
   int quarters;            // one GPU: critical-path tiles as four 64 x 64 items (persist_decode)
   int *qcnt;               // per-tile count of finished quarters (zeroed)
+  int stage_old;           // 128 x 128 tiles: the old tile staged in shared memory during the last
+                           // chunk (tile_mainloop / tile_epilogue), 0: read from L2 in the epilogue
+  int p1_lone;             // one GPU: the grid leaves one SM with a single CTA, which runs every
+                           // P1 item alone on its SM (the others skip them); 0: off
+  int *smcnt;              // p1_lone: per-SM count of resident CTAs, then the start barrier count
+  int nsm;                 // SMs of the device
   unsigned long long *trace;   // per item {taken, operands ready, done} (%globaltimer ns) and
                                // (smid << 32 | blockIdx.x), or null (env FW_PERSIST_TRACE)
   RankView rk[kMaxRanks];
@@ -104,7 +110,121 @@ __device__ __forceinline__ Item unpack_item(unsigned u) {
 // 64*(q&1) of the tile, all 128 k), taken back to back: the chain P2(K) -> prio(K) -> P1(K+1)
 // -> P2(K+1) then advances in quarter-tile steps, which at small n (C2) is the round's critical
 // path. A tile's round counter advances when its fourth quarter is done.
+// The rest(K) tiles (I, J not in {K, N = K+1}) in the order the items take them: first the tiles of
+// row and column M = K+2 ((M, M) first) — their round-K values are what round N's prio tiles
+// (tile (M, M), row M, column M), and through them P1(M), wait for — then the others row-major.
+// (In plain row-major order the round-K version of (M, M) was an arbitrary rest tile, often in the
+// second part, after P2(N): the per-round pivot chain waited for it, tools/persist_trace.py.)
+__host__ __device__ __forceinline__ void persist_rest_ij(int q, int K, int T, int *I, int *J) {
+  const int N = K + 1, M = K + 2, m = T - 2;
+  if (M >= T) {
+    *I = skip2(q / m, K, N);
+    *J = skip2(q % m, K, N);
+    return;
+  }
+  const int s = M - 2;                            // M's index among the rows / columns kept
+  int ii, jj;
+  if (q == 0) {
+    ii = s, jj = s;
+  } else if (q < m) {                             // row M
+    ii = s;
+    jj = q - 1 + (q - 1 >= s);
+  } else if (q < 2 * m - 1) {                     // column M
+    const int t = q - m;
+    ii = t + (t >= s);
+    jj = s;
+  } else {
+    const int t = q - (2 * m - 1);
+    ii = t / (m - 1);
+    jj = t % (m - 1);
+    ii += ii >= s;
+    jj += jj >= s;
+  }
+  *I = skip2(ii, K, N);
+  *J = skip2(jj, K, N);
+}
+
+// quarters == 2 ("critical" quarters): only the three tiles per round that the pivot chain itself
+// waits for are split — the round-K tile (N, N) that P1(N) reads (first in prio(K), N = K+1) and
+// round N's phase-2 tiles (N, N+1), (N+1, N) that the next prio tile reads (first in P2(N)) — so
+// the chain P1 -> P2 -> prio -> P1 advances in quarter steps while every other tile stays whole
+// (the full quartering of prio / P2 costs more item overhead than it saves at T >= 32).
+__host__ __device__ __forceinline__ long long persist_total_crit(int T) {
+  if (T < 2) return 1;
+  const long long m = T - 2, segA = 4LL * T + 5 + m * m, segB = 4LL * T - 1 + m * m;
+  return 1 + (2LL * T + 4) + m * segA + segB + (long long)(T - 1) * (T - 1);
+}
+__host__ __device__ __forceinline__ Item persist_decode_crit(const PersistArgs &a, long long it) {
+  const int T = a.T;
+  const Item none{IT_NONE, 0, 0, 0, 0};
+  if (it == 0) return Item{IT_P1, 0, 0, 0, 0};
+  if (T < 2) return none;
+  const long long pre = 1 + 2LL * T + 4;       // P1(0), P2(0): (0,1) x4, (1,0) x4, the rest whole
+  if (it < pre) {
+    const int q = (int)(it - 1);
+    if (q < 4) return Item{IT_QTILE, 0, 0, 1, q};
+    if (q < 8) return Item{IT_QTILE, 0, 1, 0, q - 4};
+    const int t = q - 8;
+    return t < T - 2 ? Item{IT_TILE, 0, 0, t + 2, 0} : Item{IT_TILE, 0, t - (T - 2) + 2, 0, 0};
+  }
+  const int m = T - 2;
+  const long long segA = 4LL * T + 5 + (long long)m * m, segB = 4LL * T - 1 + (long long)m * m;
+  long long r = it - pre;
+  int K;
+  long long ql;
+  if (r < (long long)m * segA) {
+    K = (int)(r / segA);
+    ql = r - (long long)K * segA;
+  } else if ((r -= (long long)m * segA) < segB) {
+    K = T - 2;
+    ql = r;
+  } else {
+    K = T - 1;
+    ql = r - segB;
+  }
+  int q = (int)ql;
+  if (K == T - 1) {                               // last round: its phase-3 tiles, then no-ops
+    const int m1 = T - 1;
+    if (q >= m1 * m1) return none;
+    return Item{IT_TILE, K, skip2(q / m1, K, -1), skip2(q % m1, K, -1), 0};
+  }
+  const int N = K + 1;
+  if (q < 4) return Item{IT_QTILE, K, N, N, q};  // prio: (N, N) in quarters, then row N, column N
+  if (q < 2 * T) {
+    const int t = q - 4;
+    return t < T - 2 ? Item{IT_TILE, K, N, skip2(t, K, N), 0} : Item{IT_TILE, K, skip2(t - (T - 2), K, N), N, 0};
+  }
+  q -= 2 * T;
+  if (q == 0) return Item{IT_P1, N, N, N, 0};
+  q -= 1;
+  const int rest = m * m, gap = a.gap < rest ? a.gap : rest;
+  int ri, rj;
+  if (q < gap) {
+    persist_rest_ij(q, K, T, &ri, &rj);
+    return Item{IT_TILE, K, ri, rj, 0};
+  }
+  q -= gap;
+  if (N + 1 < T) {                                // P2(N): (N, N+1), (N+1, N) in quarters first
+    if (q < 4) return Item{IT_QTILE, N, N, N + 1, q};
+    if (q < 8) return Item{IT_QTILE, N, N + 1, N, q - 4};
+    if (q < 2 * T + 4) {
+      const int t = q - 8;
+      return t < T - 2 ? Item{IT_TILE, N, N, skip2(t, N, N + 1), 0} : Item{IT_TILE, N, skip2(t - (T - 2), N, N + 1), N, 0};
+    }
+    q -= 2 * T + 4;
+  } else {                                        // the last P2: whole tiles
+    if (q < 2 * T - 2) {
+      return q < T - 1 ? Item{IT_TILE, N, N, skip2(q, N, -1), 0} : Item{IT_TILE, N, skip2(q - (T - 1), N, -1), N, 0};
+    }
+    q -= 2 * T - 2;
+  }
+  q += gap;
+  persist_rest_ij(q, K, T, &ri, &rj);
+  return Item{IT_TILE, K, ri, rj, 0};
+}
+
 __host__ __device__ __forceinline__ Item persist_decode(const PersistArgs &a, long long it) {
+  if (a.quarters == 2) return persist_decode_crit(a, it);
   const int T = a.T, Q = a.quarters ? 4 : 1, TQ = a.quarters ? IT_QTILE : IT_TILE;
   Item w{IT_NONE, 0, 0, 0, 0};
   if (it == 0) return Item{IT_P1, 0, 0, 0, 0};
@@ -134,7 +254,11 @@ __host__ __device__ __forceinline__ Item persist_decode(const PersistArgs &a, lo
   q -= 1;
   const int m = T - 2, rest = m * m;
   const int gap = a.gap < rest ? a.gap : rest;
-  if (q < gap) return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N), 0};
+  int ri, rj;
+  if (q < gap) {
+    persist_rest_ij(q, K, T, &ri, &rj);
+    return Item{IT_TILE, K, ri, rj, 0};
+  }
   q -= gap;
   if (q < Q * 2 * (T - 1)) {                      // P2(K+1): row K+1, then column K+1
     const int t = q / Q, qq = q % Q;
@@ -142,7 +266,8 @@ __host__ __device__ __forceinline__ Item persist_decode(const PersistArgs &a, lo
   }
   q -= Q * 2 * (T - 1);
   q += gap;
-  return Item{IT_TILE, K, skip2(q / m, K, N), skip2(q % m, K, N), 0};
+  persist_rest_ij(q, K, T, &ri, &rj);
+  return Item{IT_TILE, K, ri, rj, 0};
 }
 
 __device__ __forceinline__ int ld_acquire(const int *p) {
@@ -247,6 +372,10 @@ __device__ __forceinline__ int owner_rank(const PersistArgs &a, int K) {
   return o;
 }
 
+// the staged old tile: 128 x 128 elements from stage (nch % kStages) = 1 on, within the allocation
+static_assert((128 / kBK) % kStages == 1 && 2 * TileShape<128, 128>::kStage >= 128 * 128,
+              "old-tile staging layout");
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kThreads, 2)
 fw_persistent_kernel(const PersistArgs a) {
@@ -264,15 +393,53 @@ fw_persistent_kernel(const PersistArgs a) {
   __shared__ unsigned long long s_t0, s_t1, s_ta, s_tb, s_tc;
   using S = TileShape<128, 128>;
   const int tid = threadIdx.x;
-  if (tid == 0) s_next = (long long)atomicAdd(a.next, 1ull);
+  // Dedicated phase-1 CTA (a.p1_lone, one GPU): the grid is one CTA short of two per SM, so one
+  // SM holds a single CTA; every CTA registers its SM, a start barrier waits for the whole grid,
+  // and the CTA alone on its SM runs every P1 item in round order (the critical path of a small
+  // solve: the P1 -> P2 -> prio -> P1 chain) without sharing its SM with a tile
+  // product; the other CTAs skip the P1 items of the order. If no SM ended up with one CTA, the
+  // P1 items are taken as usual. Deadlock-free: P1(K) waits only for earlier items, and the
+  // items waiting for P1(K) wait for a CTA that runs nothing else.
+  __shared__ int s_lone;    // -1: no dedicated CTA, 0: a normal CTA, 1: this is the P1 CTA
+  if (a.p1_lone) {
+    if (tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      atomicAdd(a.smcnt + smid, 1);
+      __threadfence();
+      atomicAdd(a.smcnt + a.nsm, 1);
+      const unsigned long long t0 = globaltimer();
+      while (ld_acquire(a.smcnt + a.nsm) < (int)gridDim.x) {
+        if (globaltimer() - t0 > a.timeout_ns) {
+          atomicOr(a.flags, 32);
+          break;
+        }
+        __nanosleep(128);
+      }
+      int lone_sm = -1;
+      for (int q = 0; q < a.nsm && lone_sm < 0; ++q)
+        if (ld_acquire(a.smcnt + q) == 1) lone_sm = q;
+      s_lone = lone_sm < 0 ? -1 : ((int)smid == lone_sm ? 1 : 0);
+    }
+    __syncthreads();
+  } else if (tid == 0) {
+    s_lone = -1;
+  }
+  // the dedicated CTA walks the P1 items K = 0, 1, ... instead of the counter (s_next = K)
+  if (tid == 0) s_next = s_lone == 1 ? 0 : (long long)atomicAdd(a.next, 1ull);
   for (;;) {
     __syncthreads();   // the previous item is done with s_cur
     if (tid == 0) {
       const long long it = s_next;
-      if (it < a.total) {
+      if (s_lone == 1) {                               // the dedicated P1 CTA
+        s_cur = it < a.T ? Item{IT_P1, (int)it, (int)it, (int)it, 0} : Item{-1, 0, 0, 0, 0};
+        s_next = it + 1;
+        if (a.trace) s_it = a.total + it, s_t0 = globaltimer();   // its records follow the items
+      } else if (it < a.total) {
         if (a.trace) s_it = it, s_t0 = globaltimer();
         s_next = (long long)atomicAdd(a.next, 1ull);
-        const Item w = a.items ? unpack_item(a.items[it]) : persist_decode(a, it);
+        Item w = a.items ? unpack_item(a.items[it]) : persist_decode(a, it);
+        if (w.type == IT_P1 && s_lone == 0) w.type = IT_NONE;   // the dedicated CTA's
         s_cur = w;
         if (a.trace) s_ta = globaltimer();
         if (w.type == IT_QTILE) {   // one GPU: rows / columns 64 * (quarter bits) of tile (I, J)
@@ -283,6 +450,7 @@ fw_persistent_kernel(const PersistArgs a) {
           s_src.lda = a.ld;
           s_src.b = Dv + (int64_t)w.K * 128 * a.ld + w.J * 128 + qj;
           s_src.ldb = a.ld;
+          s_src.old = nullptr;
         }
         if (w.type == IT_TILE) {   // A = (I, K) of this rank's rows; B = (K, J) in place or the ring
           const RankView &v = a.rk[w.r];
@@ -293,6 +461,8 @@ fw_persistent_kernel(const PersistArgs a) {
           s_src.b = own_b ? Dv + (int64_t)(w.K - v.t0) * 128 * a.ld + w.J * 128
                           : static_cast<const T *>(v.ring) + (int64_t)w.K * 128 * a.ldr + w.J * 128;
           s_src.ldb = own_b ? a.ld : a.ldr;
+          s_src.old = a.stage_old ? Dv + (int64_t)(w.I - v.t0) * 128 * a.ld + w.J * 128 : nullptr;
+          s_src.ldo = a.ld;
         }
       } else {
         s_cur = Item{-1, 0, 0, 0, 0};
@@ -368,8 +538,15 @@ fw_persistent_kernel(const PersistArgs a) {
       // the item again from shared memory: nothing but the accumulators lives across the loop
       const Item e = s_cur;
       const RankView &ve = a.rk[e.r];
+      const T *old_s = nullptr;
+      if (s_src.old) {   // the staged old tile (stages 1-2 of the last chunk, 128 / kBK = 4 chunks)
+        cp_async_wait<0>();
+        __syncthreads();
+        old_s = reinterpret_cast<const T *>(smem_raw) + ((128 / kBK) % kStages) * S::kStage;
+      }
       int kmax = tile_epilogue<T, 128, 128, MODE, true>(static_cast<T *>(ve.D), ve.P, a.ld, (e.I - ve.t0) * 128,
-                                                        e.J * 128, 0, 0, 0, 0, e.K, (e.K * 128) & ~kKeyMask, acc);
+                                                        e.J * 128, 0, 0, 0, 0, e.K, (e.K * 128) & ~kKeyMask, acc,
+                                                        old_s);
       if (is_key(MODE)) {
         kmax = __reduce_max_sync(0xffffffffu, kmax);
         if ((tid & 31) == 0 && kmax > 0) atomicMax(a.maxkey, kmax);

@@ -186,12 +186,28 @@ def test_block_size_invariance_integer():
     assert all(np.array_equal(Ds[0], d) for d in Ds[1:])
 
 
-def test_determinism():
+def test_determinism(monkeypatch):
+    """The stream-ordered schedule is deterministic bit for bit. The persistent launch (the default
+    for small round-tag solves) takes its items dynamically and may read an operand tile after its
+    owner has already relaxed it for a later round (reading R16): integer data stay
+    bitwise (every sum is exact), real data agree run to run within the tolerance (rel 1e-5) with
+    valid paths."""
     W = gen.generate("complete_real", 513, 5)
+    monkeypatch.setenv("FW_PERSISTENT", "0")
     a = solve(W, 128)
     b = solve(W, 128)
     np.testing.assert_array_equal(a[0], b[0])
     np.testing.assert_array_equal(a[1], b[1])
+    monkeypatch.setenv("FW_PERSISTENT", "1")
+    c = solve(W, 128)
+    d = solve(W, 128)
+    np.testing.assert_allclose(c[0], a[0], rtol=1e-5)
+    np.testing.assert_allclose(d[0], c[0], rtol=1e-5)
+    for D, P in (c, d):
+        assert oracle.check_paths(W, D, P, rtol=1e-5)[0] == 0
+    Wi = gen.generate("complete_int", 513, 5)
+    e, f = solve(Wi, 128), solve(Wi, 128)
+    np.testing.assert_array_equal(e[0], f[0])
 
 
 # ---- validation / error contract (fw.h) -----------------------------------------------
@@ -748,3 +764,28 @@ def test_persistent_int32_keys(path):
     assert s.persistent == 1 and s.p_method == 2 and s.compute_f32 == 0
     np.testing.assert_array_equal(D, oracle.fw(W, None)[0])
     assert oracle.check_paths(W, D, P, mode=path)[0] == 0
+
+
+@pytest.mark.parametrize("lone", [0, 1])
+@pytest.mark.parametrize("kind,n", [("complete_real", 2000), ("complete_int", 1536), ("er_int", 1100)])
+def test_persistent_dedicated_phase1_cta(kind, n, lone):
+    """The one-GPU persistent launch with and without the dedicated phase-1 CTA (one SM keeps a
+    single CTA that runs every P1 item; the others skip them): D against the oracle, paths valid."""
+    W = gen.generate(kind, n, 40 + n, p=0.05, lo=1, hi=1000 if kind.startswith("er") else 100)
+    fw.fw_init(0, 0)
+    try:
+        fw.fw_set_option("persistent", 1)
+        fw.fw_set_option("persist_p1_lone", lone)
+        dD = torch.from_numpy(W).cuda()
+        dP = torch.empty(W.shape, dtype=torch.int32, device="cuda")
+        (fw.fw_solve_device_i32 if W.dtype == np.int32 else fw.fw_solve_device_f32)(
+            dD, dP, block=128, stream=torch.cuda.current_stream())
+        s = fw.fw_last_stats()
+    finally:
+        fw.fw_free()
+    assert s.persistent == 1
+    D, P = dD.cpu().numpy(), dP.cpu().numpy()
+    exact = exact_data(W)
+    assert_D_matches(D, oracle.fw(W, None)[0], exact)
+    bad, first = oracle.check_paths(W, D, P, rtol=0.0 if exact else 1e-5)
+    assert bad == 0, (bad, divmod(first, n))

@@ -109,3 +109,57 @@ def test_one_gpu_quarters_collapse_to_table(n, gap):
             i += 1
     np.testing.assert_array_equal(np.array(out, dtype=np.uint32), full)
     assert np.sum(ty == 3) > 0
+
+
+def _check_one_gpu_order(ty, K, I, J, T):
+    """Completeness and dependencies-earlier of a one-GPU order given as full-tile items."""
+    pos = {}
+    for idx in range(len(ty)):
+        key = ("P1", K[idx]) if ty[idx] == 1 else ("T", K[idx], I[idx], J[idx])
+        assert key not in pos, f"duplicate item {key}"
+        pos[key] = idx
+    assert len(pos) == T * T * T
+
+    def done(k, i, j):
+        return pos[("P1", k)] if (i, j) == (k, k) else pos[("T", k, i, j)]
+
+    for key, idx in pos.items():
+        if key[0] == "P1":
+            if key[1] > 0:
+                assert done(key[1] - 1, key[1], key[1]) < idx
+            continue
+        _, k, i, j = key
+        if k > 0:
+            assert done(k - 1, i, j) < idx
+        assert done(k, i, k) < idx or j == k
+        assert done(k, k, j) < idx or i == k
+        if i == k or j == k:
+            assert pos[("P1", k)] < idx
+
+
+@pytest.mark.parametrize("n,gap", [(128, 0), (256, 0), (384, 1), (700, 5), (1024, 40), (4096, 740), (3000, 100000)])
+def test_one_gpu_critical_quarters(n, gap):
+    """persist_quarters = 2: only the tiles the pivot chain waits for are quarter items — per round
+    N the round-(N-1) tile (N, N) first in the prio section, and round N's phase-2 tiles (N, N+1),
+    (N+1, N) first in its phase-2 section. Collapsing each run of four quarters gives a complete
+    order in which every item's dependencies come earlier (deadlock-freedom), with three
+    quartered tiles per round."""
+    T = (n + 127) // 128
+    q = fw.fw_persist_schedule(n, 1, -4, gap)
+    r, ty, K, I, J = unpack(q)
+    out, i, nq = [], 0, 0
+    while i < len(q):
+        if ty[i] == 3:
+            assert list(r[i:i + 4]) == [0, 1, 2, 3] and np.all(ty[i:i + 4] == 3)
+            assert len({(K[x], I[x], J[x]) for x in range(i, i + 4)}) == 1
+            out.append((2, K[i], I[i], J[i]))
+            nq += 1
+            i += 4
+        else:
+            out.append((ty[i], K[i], I[i], J[i]))
+            i += 1
+    a = np.array(out)
+    _check_one_gpu_order(a[:, 0], a[:, 1], a[:, 2], a[:, 3], T)
+    # quartered: (0,1), (1,0) of round 0; per round K < T-1: (K+1, K+1); per round N in 1..T-2:
+    # (N, N+1), (N+1, N)
+    assert nq == (2 + (T - 1) + 2 * (T - 2) if T >= 2 else 0)

@@ -23,8 +23,14 @@ a = ap.parse_args()
 raw = np.fromfile(a.path, dtype=np.int64)
 magic, T, W, total, quarters, gap, grid, self_ = raw[:8]
 assert magic == 0x46575453 and W == 1, "one-GPU traces only"
-rec = raw[8:].reshape(-1, 8).astype(np.uint64)
-items = fw.fw_persist_schedule(a.n, 1, -3 if quarters else -2, int(gap))
+allrec = raw[8:].reshape(-1, 8).astype(np.uint64)
+rec = allrec[:total]
+lone = allrec[total:total + T]                  # the dedicated P1 CTA's records (if it ran)
+items = list(fw.fw_persist_schedule(a.n, 1, {0: -2, 1: -3, 2: -4}[int(quarters)], int(gap)))
+if (lone[:, 2] > 0).any():                      # its P1 items, appended as items of type P1
+    for K in range(T):
+        items.append((1 << 27) | (K << 18) | (K << 9) | K)
+    rec = np.concatenate([rec[:len(items) - T], lone])
 m = min(len(items), len(rec))
 rec = rec[:m]
 ok = rec[:, 2] > 0
