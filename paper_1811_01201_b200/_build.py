@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfwb200.so")
 SOURCES = [os.path.join(CSRC, "fw_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "fw_kernels.cuh"), os.path.join(ROOT, "include", "fw.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "fw_kernels.cuh"), os.path.join(CSRC, "fw_persist.cuh"), os.path.join(ROOT, "include", "fw.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-shared", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-ldl"]
