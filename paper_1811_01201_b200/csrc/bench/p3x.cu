@@ -455,6 +455,8 @@ int runk(const char *tag, float *D, int32_t *P, const float *Sp, int *mk, int64_
 }
 
 
+__device__ int g_smslot[256];
+__device__ long long g_stagger_clk;
 // Persistent variant of the 3-stage / one-barrier 8x8 kernel: grid = 2 CTAs per SM, each CTA
 // walks tiles blockIdx.x, blockIdx.x + gridDim.x, ... and the cp.async chunk stream runs across
 // tile boundaries (the next tile's first chunks load during this tile's last chunk + epilogue).
@@ -497,6 +499,21 @@ p3p(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
     cpc();
   };
   float acc[RM][4 * H];
+  if (VAR & 4) {
+    // staggered start: the second CTA to arrive on an SM waits about half a tile, so the two
+    // co-resident CTAs stop running their epilogues (and the next tile's pipeline fill) in lock-step
+    __shared__ int slot;
+    if (tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      slot = atomicAdd(g_smslot + smid, 1) & 1;
+    }
+    __syncthreads();
+    if (slot) {
+      const long long t0 = clock64();
+      while (clock64() - t0 < g_stagger_clk) __nanosleep(1000);
+    }
+  }
   if (total > 0) load(0);
   if (total > 1) load(1);
 #pragma unroll 1
@@ -587,6 +604,7 @@ p3p(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
   }
 }
 
+static long long g_stagger = 0;
 template <int VAR>
 int runp(const char *tag, float *D, int32_t *P, int *mk, int64_t n, int sms, int clk_khz, int per_sm) {
   const int bytes = 3 * (128 * 36 + 32 * 128) * 4;
@@ -597,6 +615,7 @@ int runp(const char *tag, float *D, int32_t *P, int *mk, int64_t n, int sms, int
   CK(cudaMemcpy(D, g_init.data(), n * n * 4, cudaMemcpyHostToDevice));
   const int tiles = (int)(n / 128), kb = 128 * 50;
   const int grid = sms * per_sm;
+  CK(cudaMemcpyToSymbol(g_stagger_clk, &g_stagger, sizeof(long long)));
   for (int w = 0; w < 2; ++w) kern<<<grid, 256, bytes>>>(D, P, n, kb, mk, tiles);
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1;
@@ -642,7 +661,14 @@ int main() {
   }
   run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar", D, P, mk, n, sms, clk);
   runp<3>("persistent-3st", D, P, mk, n, sms, clk, 2);
-  runp<1>("persistent-3st-nopf", D, P, mk, n, sms, clk, 2);
+  // staggered persistent CTAs: the second CTA of each SM starts g_stagger clocks late
+  const long long st[] = {8000, 16000, 32000, 48000};
+  const char *nm[] = {"persistent-stagger-8k", "persistent-stagger-16k", "persistent-stagger-32k", "persistent-stagger-48k"};
+  for (int v = 0; v < 4; ++v) {
+    g_stagger = st[v];
+    runp<7>(nm[v], D, P, mk, n, sms, clk, 2);
+  }
+  g_stagger = 0;
   run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar-again", D, P, mk, n, sms, clk);
   runp<3>("persistent-3st-again", D, P, mk, n, sms, clk, 2);
   return 0;
