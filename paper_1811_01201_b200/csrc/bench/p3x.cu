@@ -45,6 +45,8 @@ __device__ __forceinline__ void relax2v(float &x0, float &x1, float &x2, float &
 
 // VAR bits: 1 = key epilogue with P (else plain), 2 = L2 prefetch of the epilogue tile,
 //           4 = k-outer order (all rows for k-pair 0 then k-pair 1 per q), 8 = no epilogue store
+__device__ int g_kd = 128;   // k depth of one launch (128: one round; 256: a pair of rounds)
+static int h_kd = 128;
 template <int RM, int H, int TX, int TY, int MINB, int BK, int NS, int VAR>
 __global__ void __launch_bounds__(TX * TY, MINB)
 p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *maxkey) {
@@ -52,7 +54,8 @@ p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
   constexpr int SA = TM * AS, SB = BK * TN, ST = SA + SB;
   extern __shared__ __align__(16) float sm[];
   const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
-  if ((i0 + TM > kb && i0 < kb + 128) || (j0 + TN > kb && j0 < kb + 128)) return;
+  const int kd = g_kd;
+  if ((i0 + TM > kb && i0 < kb + kd) || (j0 + TN > kb && j0 < kb + kd)) return;
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   if (VAR & 2) {
     constexpr int LPR = TN * 4 / 128;
@@ -84,7 +87,7 @@ p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
   for (int r = 0; r < RM; ++r)
 #pragma unroll
     for (int c = 0; c < 4 * H; ++c) acc[r][c] = __int_as_float(0x7f800000);
-  constexpr int nch = 128 / BK;
+  const int nch = kd / BK;
 #pragma unroll 1
   for (int s = 0; s < NS - 1; ++s) load(s, s * BK);
 #pragma unroll 1
@@ -140,7 +143,39 @@ p3x(float *__restrict__ D, int32_t *__restrict__ P, int64_t ld, int kb, int *max
       for (int k = 0; k < 4; ++k)
 #pragma unroll
         for (int h = 0; h < H; ++h) b[k][h] = *reinterpret_cast<const float4 *>(bs + (4 * q + k) * TN + 4 * TX * h);
-      if (VAR & 4) {
+      if (VAR & 12288) {   // 4096 / 8192: rows in groups of G = 4 / 2, per group k-pair outer, then
+                           // column pair, then the G rows (mix_probe lds-G4: 78.0 vs 74.5)
+        constexpr int G = (VAR & 4096) ? 4 : 2;
+#pragma unroll
+        for (int r = 0; r < RM; r += G) {
+          float4 a[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) a[g] = *reinterpret_cast<const float4 *>(as + TY * (r + g) * AS + 4 * q);
+#pragma unroll
+          for (int kp = 0; kp < 2; ++kp)
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+#pragma unroll
+              for (int pos = 0; pos < 2; ++pos) {
+                const float4 bk = b[2 * kp][h], bk1 = b[2 * kp + 1][h];
+                const float2 b0 = pos ? make_float2(bk.z, bk.w) : make_float2(bk.x, bk.y);
+                const float2 b1 = pos ? make_float2(bk1.z, bk1.w) : make_float2(bk1.x, bk1.y);
+                float2 s0[G], s1[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                  const float a0 = kp ? a[g].z : a[g].x, a1 = kp ? a[g].w : a[g].y;
+                  s0[g] = __fadd2_rn(make_float2(a0, a0), b0);
+                  s1[g] = __fadd2_rn(make_float2(a1, a1), b1);
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                  float *x = &acc[r + g][4 * h + 2 * pos];
+                  x[0] = fminf(x[0], fminf(s0[g].x, s1[g].x));
+                  x[1] = fminf(x[1], fminf(s0[g].y, s1[g].y));
+                }
+              }
+        }
+      } else if (VAR & 4) {
         float4 a[RM];
 #pragma unroll
         for (int r = 0; r < RM; ++r) a[r] = *reinterpret_cast<const float4 *>(as + TY * r * AS + 4 * q);
@@ -270,6 +305,7 @@ int run(const char *tag, float *D, int32_t *P, int *mk, int64_t n, int sms, int 
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TX * TY, bytes));
   CK(cudaMemcpy(D, g_init.data(), n * n * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpyToSymbol(g_kd, &h_kd, sizeof(int)));
   dim3 g(n / TN, n / TM);
   const int kb = 128 * 50;
   for (int w = 0; w < 2; ++w) kern<<<g, TX * TY, bytes>>>(D, P, n, kb, mk);
@@ -284,12 +320,44 @@ int run(const char *tag, float *D, int32_t *P, int *mk, int64_t n, int sms, int 
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   ms /= reps;
   // relaxations actually done: tiles outside the excluded strip (TM/TN-aligned exclusion)
-  const int64_t tr = n / TM - (128 + TM - 1) / TM, tc = n / TN - (128 + TN - 1) / TN;
-  const double relax = (double)tr * TM * tc * TN * 128 * ((VAR & 32) ? 8 : 1);
-  printf("{\"variant\": \"%s\", \"RM\": %d, \"H\": %d, \"TX\": %d, \"TY\": %d, \"minb\": %d, \"BK\": %d, \"NS\": %d, \"var\": %d, "
+  const int64_t tr = n / TM - (h_kd + TM - 1) / TM, tc = n / TN - (h_kd + TN - 1) / TN;
+  const double relax = (double)tr * TM * tc * TN * h_kd * ((VAR & 32) ? 8 : 1);
+  printf("{\"variant\": \"%s\", \"kd\": %d, \"RM\": %d, \"H\": %d, \"TX\": %d, \"TY\": %d, \"minb\": %d, \"BK\": %d, \"NS\": %d, \"var\": %d, "
          "\"regs\": %d, \"spill\": %d, \"occ\": %d, \"ms\": %.4f, \"relax_per_clk_sm_at_max_clock\": %.2f, \"tflops\": %.3f}\n",
-         tag, RM, H, TX, TY, MINB, BK, NS, VAR, fa.numRegs, (int)fa.localSizeBytes, occ, ms,
+         tag, h_kd, RM, H, TX, TY, MINB, BK, NS, VAR, fa.numRegs, (int)fa.localSizeBytes, occ, ms,
          relax / (ms * 1e-3) / (sms * (double)clk_khz * 1e3), 2 * relax / (ms * 1e-3) / 1e12);
+  fflush(stdout);
+  return 0;
+}
+
+// the library's stream kernel (KEY, 128 x 128) on the same launch
+int runlib(const char *tag, float *D, int32_t *P, int *mk, int64_t n, int sms, int clk_khz) {
+  auto lib = fwb::minplus_tile_kernel<float, 128, 128, fwb::MODE_KEY, false>;
+  const int lbytes = fwb::TileShape<128, 128>::kBytes;
+  CK(cudaFuncSetAttribute(lib, cudaFuncAttributeMaxDynamicSharedMemorySize, lbytes));
+  cudaFuncAttributes fl; CK(cudaFuncGetAttributes(&fl, lib));
+  const int kb = 128 * 50;
+  fwb::TileArgs a{};
+  a.ld = n; a.B = D + (int64_t)kb * n; a.ldb = n; a.kb = kb; a.Kd = h_kd;
+  a.rows_lim = (int)n; a.cols_lim = (int)n;
+  a.mr_lo[0] = kb; a.mr_hi[0] = kb + h_kd; a.mc_lo[0] = kb; a.mc_hi[0] = kb + h_kd;
+  CK(cudaMemcpy(D, g_init.data(), n * n * 4, cudaMemcpyHostToDevice));
+  dim3 g(n / 128, n / 128);
+  for (int w = 0; w < 2; ++w) lib<<<g, 256, lbytes>>>(D, P, a, mk);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int reps = 10;
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) lib<<<g, 256, lbytes>>>(D, P, a, mk);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  const int64_t t = n / 128 - h_kd / 128;
+  const double relax = (double)t * 128 * t * 128 * h_kd;
+  printf("{\"variant\": \"%s\", \"kd\": %d, \"regs\": %d, \"spill\": %d, \"ms\": %.4f, \"relax_per_clk_sm_at_max_clock\": %.2f, \"tflops\": %.3f}\n",
+         tag, h_kd, fl.numRegs, (int)fl.localSizeBytes, ms, relax / (ms * 1e-3) / (sms * (double)clk_khz * 1e3), 2 * relax / (ms * 1e-3) / 1e12);
   fflush(stdout);
   return 0;
 }
@@ -659,17 +727,13 @@ int main() {
       for (int64_t j = 0; j < n; ++j) { sp[(k / 2) * 2 * n + 2 * j] = g_init[k * n + j]; sp[(k / 2) * 2 * n + 2 * j + 1] = g_init[(k + 1) * n + j]; }
     CK(cudaMemcpy(Sp, sp.data(), n * n * 4, cudaMemcpyHostToDevice));
   }
-  run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar", D, P, mk, n, sms, clk);
-  runp<3>("persistent-3st", D, P, mk, n, sms, clk, 2);
-  // staggered persistent CTAs: the second CTA of each SM starts g_stagger clocks late
-  const long long st[] = {8000, 16000, 32000, 48000};
-  const char *nm[] = {"persistent-stagger-8k", "persistent-stagger-16k", "persistent-stagger-32k", "persistent-stagger-48k"};
-  for (int v = 0; v < 4; ++v) {
-    g_stagger = st[v];
-    runp<7>(nm[v], D, P, mk, n, sms, clk, 2);
+  for (int kd = 128; kd <= 256; kd += 128) {
+    h_kd = kd;
+    runlib("library-key", D, P, mk, n, sms, clk);
+    run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar", D, P, mk, n, sms, clk);
+    run<8, 2, 16, 16, 2, 32, 3, 1024 + 3 + 4>("3st-1bar-kouter", D, P, mk, n, sms, clk);
+    run<8, 2, 16, 16, 2, 32, 3, 1024 + 3 + 4096>("3st-1bar-G4", D, P, mk, n, sms, clk);
+    runlib("library-key-again", D, P, mk, n, sms, clk);
   }
-  g_stagger = 0;
-  run<8, 2, 16, 16, 2, 32, 3, 1024 + 3>("3st-1bar-again", D, P, mk, n, sms, clk);
-  runp<3>("persistent-3st-again", D, P, mk, n, sms, clk, 2);
   return 0;
 }
