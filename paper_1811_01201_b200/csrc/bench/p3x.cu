@@ -734,6 +734,11 @@ int main() {
     run<8, 2, 16, 16, 2, 32, 3, 1024 + 3 + 4>("3st-1bar-kouter", D, P, mk, n, sms, clk);
     run<8, 2, 16, 16, 2, 32, 3, 1024 + 3 + 4096>("3st-1bar-G4", D, P, mk, n, sms, clk);
     runlib("library-key-again", D, P, mk, n, sms, clk);
+    // one CTA of 512 threads per SM (same registers per SM): 256 x 128 and 128 x 256 tiles
+    run<8, 2, 16, 32, 1, 32, 3, 1024 + 3>("512t-256x128-3st", D, P, mk, n, sms, clk);
+    run<8, 2, 16, 32, 1, 32, 4, 1024 + 3>("512t-256x128-4st", D, P, mk, n, sms, clk);
+    run<8, 2, 32, 16, 1, 32, 3, 1024 + 3>("512t-128x256-3st", D, P, mk, n, sms, clk);
+    run<8, 2, 16, 32, 1, 32, 3, 1024 + 3 + 4>("512t-256x128-3st-kouter", D, P, mk, n, sms, clk);
   }
   return 0;
 }
