@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256, MINB) probe(float *out, int iters, float 
     // ptxas CSEs the FADD2s across iterations (8 extra FADD2 per 8*RM, not counted)
 #pragma unroll
     for (int i = 0; i < 8; ++i) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(b[i]) : "l"(zero));
+    const int mrun = (int)wmask - it;   // never in [0, 64): wmask is all ones at run time
 #pragma unroll
     for (int r = 0; r < RM; ++r) {
       if (ORDER == 0) {   // production order: per 4 columns: 4 FADD2 then 4 FMNMX3
@@ -53,6 +54,29 @@ __global__ void __launch_bounds__(256, MINB) probe(float *out, int iters, float 
           min3v(xx[1], hi(s0), hi(s1));
           min3v(xx[2], lo(s2), lo(s3));
           min3v(xx[3], hi(s2), hi(s3));
+        }
+      } else if (ORDER >= 64) {
+        // forced runs with a REAL basic-block boundary (session 5): a never-taken branch on a value
+        // that changes every iteration (ISETP + BRA) between the FADD2 run (consecutive FADD2s share
+        // the 64-bit b operand: .reuse) and the FMNMX3 run, so ptxas cannot interleave them
+        constexpr int G = (ORDER & 15) ? (ORDER & 15) : 1;
+        if (r % G == 0) {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int b0 = 4 * (p / 2) + 2 * (p % 2), b1 = b0 + 1;
+            unsigned long long s0[G], s1[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) s0[g] = fadd2b(a[2 * (r + g)], b[b0]);
+#pragma unroll
+            for (int g = 0; g < G; ++g) s1[g] = fadd2b(a[2 * (r + g) + 1], b[b1]);
+            if (mrun == 2 * (r * 4 + p)) asm volatile("trap;");
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              min3v(x[8 * (r + g) + 2 * p], lo(s0[g]), lo(s1[g]));
+              min3v(x[8 * (r + g) + 2 * p + 1], hi(s0[g]), hi(s1[g]));
+            }
+            if (mrun == 2 * (r * 4 + p) + 1) asm volatile("trap;");
+          }
         }
       } else if (ORDER >= 16) {
         // forced runs (session 5): G rows; a scheduling fence between the FADD2 run (consecutive
@@ -457,6 +481,8 @@ int main() {
   run<8, 1, 0>("64acc-8w", out, sms, clk);
   run<2, 4, 0>("16acc-32w", out, sms, clk);
   run<8, 2, 0>("64acc-16w-again", out, sms, clk);
+  run<8, 2, 64 + 4>("bbfence-G4", out, sms, clk);
+  run<8, 2, 64 + 8>("bbfence-G8", out, sms, clk);
   run<8, 2, 16 + 4>("fence-warpsync-G4", out, sms, clk);
   run<8, 2, 16 + 8>("fence-warpsync-G8", out, sms, clk);
   run<8, 2, 32 + 4>("fence-1warpsync-G4", out, sms, clk);
