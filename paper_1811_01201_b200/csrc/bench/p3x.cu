@@ -331,15 +331,16 @@ int run(const char *tag, float *D, int32_t *P, int *mk, int64_t n, int sms, int 
 }
 
 // the library's stream kernel (KEY, 128 x 128) on the same launch
+template <int MODE = fwb::MODE_KEY>
 int runlib(const char *tag, float *D, int32_t *P, int *mk, int64_t n, int sms, int clk_khz) {
-  auto lib = fwb::minplus_tile_kernel<float, 128, 128, fwb::MODE_KEY, false>;
+  auto lib = fwb::minplus_tile_kernel<float, 128, 128, MODE, false>;
   const int lbytes = fwb::TileShape<128, 128>::kBytes;
   CK(cudaFuncSetAttribute(lib, cudaFuncAttributeMaxDynamicSharedMemorySize, lbytes));
   cudaFuncAttributes fl; CK(cudaFuncGetAttributes(&fl, lib));
   const int kb = 128 * 50;
   fwb::TileArgs a{};
   a.ld = n; a.B = D + (int64_t)kb * n; a.ldb = n; a.kb = kb; a.Kd = h_kd;
-  a.rows_lim = (int)n; a.cols_lim = (int)n;
+  a.rows_lim = (int)n; a.cols_lim = (int)n; a.tag = kb / 128;
   a.mr_lo[0] = kb; a.mr_hi[0] = kb + h_kd; a.mc_lo[0] = kb; a.mc_hi[0] = kb + h_kd;
   CK(cudaMemcpy(D, g_init.data(), n * n * 4, cudaMemcpyHostToDevice));
   dim3 g(n / 128, n / 128);
@@ -734,11 +735,9 @@ int main() {
     run<8, 2, 16, 16, 2, 32, 3, 1024 + 3 + 4>("3st-1bar-kouter", D, P, mk, n, sms, clk);
     run<8, 2, 16, 16, 2, 32, 3, 1024 + 3 + 4096>("3st-1bar-G4", D, P, mk, n, sms, clk);
     runlib("library-key-again", D, P, mk, n, sms, clk);
+    runlib<fwb::MODE_TAG>("library-tag", D, P, mk, n, sms, clk);
+    runlib<fwb::MODE_PLAIN>("library-plain", D, P, mk, n, sms, clk);
     // one CTA of 512 threads per SM (same registers per SM): 256 x 128 and 128 x 256 tiles
-    run<8, 2, 16, 32, 1, 32, 3, 1024 + 3>("512t-256x128-3st", D, P, mk, n, sms, clk);
-    run<8, 2, 16, 32, 1, 32, 4, 1024 + 3>("512t-256x128-4st", D, P, mk, n, sms, clk);
-    run<8, 2, 32, 16, 1, 32, 3, 1024 + 3>("512t-128x256-3st", D, P, mk, n, sms, clk);
-    run<8, 2, 16, 32, 1, 32, 3, 1024 + 3 + 4>("512t-256x128-3st-kouter", D, P, mk, n, sms, clk);
   }
   return 0;
 }
