@@ -85,3 +85,31 @@ extern "C" __global__ void __launch_bounds__(256, 2) reuse_pair(float *out, cons
   for (int i = 0; i < NA; ++i) sum += x[i] * (float)(i + 1);
   out[blockIdx.x * blockDim.x + threadIdx.x] = sum;
 }
+
+// The L0 mix probe's pattern (isa_probe.cu OP_MIX_FADD2_FMNMX3): x += y (packed, in place, y one
+// broadcast scalar shared by every chain), acc = min(acc, x.lo, x.hi); 8 chains per thread.
+// ptxas flags y's .reuse on every FADD2; `reuse_patch.py --clear` removes the flags.
+extern "C" __global__ void __launch_bounds__(256) reuse_l0(float *out, const float *in, int iters) {
+  constexpr int CH = 8;
+  unsigned long long x[CH];
+  float acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    float p = in[(threadIdx.x * 8 + c) & 4095], q = in[(threadIdx.x * 3 + c + 100) & 4095];
+    asm("mov.b64 %0, {%1,%2};" : "=l"(x[c]) : "f"(p), "f"(q));
+    acc[c] = 1e30f;
+  }
+  unsigned long long y;
+  { float z0 = in[4095]; asm("mov.b64 %0, {%1,%1};" : "=l"(y) : "f"(z0)); }
+  for (int it = 0; it < iters * 16; ++it) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(x[c]) : "l"(y));
+      min3v(acc[c], lo(x[c]), hi(x[c]));
+    }
+  }
+  float s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += acc[c] * (float)(c + 1);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
