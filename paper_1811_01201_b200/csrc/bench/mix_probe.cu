@@ -42,7 +42,20 @@ __global__ void __launch_bounds__(256, MINB) probe(float *out, int iters, float 
     const int mrun = (int)wmask - it;   // never in [0, 64): wmask is all ones at run time
 #pragma unroll
     for (int r = 0; r < RM; ++r) {
-      if (ORDER == 5) {   // cross variant (NOT min-plus): production FADD2 form, but each FMNMX3 reads
+      if (ORDER == 6) {   // boustrophedon: a_k, a_k+1 | a_k+1, a_k | a_k, ... so every second FADD2 shares its scalar
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const unsigned long long s0 = fadd2b(a[2 * r], b[4 * h + 0]);
+          const unsigned long long s1 = fadd2b(a[2 * r + 1], b[4 * h + 1]);
+          float *xx = &x[8 * r + 4 * h];
+          min3v(xx[0], lo(s0), lo(s1));
+          min3v(xx[1], hi(s0), hi(s1));
+          const unsigned long long s3 = fadd2b(a[2 * r + 1], b[4 * h + 3]);
+          const unsigned long long s2 = fadd2b(a[2 * r], b[4 * h + 2]);
+          min3v(xx[2], lo(s2), lo(s3));
+          min3v(xx[3], hi(s2), hi(s3));
+        }
+      } else if (ORDER == 5) {   // cross variant (NOT min-plus): production FADD2 form, but each FMNMX3 reads
                           // the two halves of ONE result pair — isolates the FMNMX3 operand layout
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -510,6 +523,7 @@ int main() {
   run<8, 2, 0>("64acc-16w-again", out, sms, clk);
   run<8, 2, 3>("scalar-pairs-64acc-16w", out, sms, clk);
   run<8, 2, 5>("cross-prodFADD2-pairFMNMX3-64acc-16w", out, sms, clk);
+  run<8, 2, 6>("boustrophedon-64acc-16w", out, sms, clk);
   run<8, 2, 64 + 4>("bbfence-G4", out, sms, clk);
   run<8, 2, 64 + 8>("bbfence-G8", out, sms, clk);
   run<8, 2, 16 + 4>("fence-warpsync-G4", out, sms, clk);

@@ -21,11 +21,14 @@ __device__ __forceinline__ unsigned long long pk(float a, float b) {
 
 // op ids
 enum { OP_FADD, OP_FADD2, OP_FMNMX, OP_FMNMX3, OP_MIX_FADD2_FMNMX3, OP_VIADDMNMX,
-       OP_VIMNMX3, OP_IADD_VIMNMX3, OP_SELECT, OP_FADD_FMNMX, OP_COUNT };
+       OP_VIMNMX3, OP_IADD_VIMNMX3, OP_SELECT, OP_FADD_FMNMX,
+       OP_MIX_PINGPONG, OP_MIX_OWN_SCALAR, OP_MIX_PAIR_PAIR, OP_MIX_BCAST_FIRST, OP_COUNT };
 static const char* NAMES[] = {"FADD", "FADD2", "FMNMX", "FMNMX3", "FADD2+FMNMX3",
-  "VIADDMNMX", "VIMNMX3", "IADD+VIMNMX3", "FADD+FSETP+FSEL+SEL", "FADD+FMNMX"};
+  "VIADDMNMX", "VIMNMX3", "IADD+VIMNMX3", "FADD+FSETP+FSEL+SEL", "FADD+FMNMX",
+  "mix: FADD2 not in place (x2 = x + y, x = x2 + y)", "mix: own scalar per chain", "mix: pair + pair in place",
+  "mix: scalar + pair -> fresh pair (production form), FMNMX3 on its halves"};
 // relaxation-equivalents (lane-ops counted as relaxations) per inner step per chain
-static const double RELAX_PER_STEP[] = {1, 2, 2, 2, 2, 1, 3, 2, 1, 1};  // lane-ops per step
+static const double RELAX_PER_STEP[] = {1, 2, 2, 2, 2, 1, 3, 2, 1, 1, 4, 2, 2, 2};  // lane-ops per step
 
 template <int OP>
 __global__ void __launch_bounds__(1024) probe(float* sink, long long* cyc, float seed) {
@@ -59,6 +62,36 @@ __global__ void __launch_bounds__(1024) probe(float* sink, long long* cyc, float
         asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y));
         asm("mov.b64 {%0,%1}, %2;" : "=f"(a[c]), "=f"(b[c]) : "l"(x));
         asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(acc[c]) : "f"(a[c]), "f"(b[c]));
+      } else if (OP == OP_MIX_PINGPONG) {
+        // two steps: x2 = x + y, acc = min(acc, x2); x = x2 + y, acc = min(acc, x) — destinations differ from sources
+        unsigned long long x = pk(a[c], b[c]), y = pk(seed, seed), x2;
+        asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(x2) : "l"(x), "l"(y));
+        float p, q; asm("mov.b64 {%0,%1}, %2;" : "=f"(p), "=f"(q) : "l"(x2));
+        asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(acc[c]) : "f"(p), "f"(q));
+        asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(x) : "l"(x2), "l"(y));
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(a[c]), "=f"(b[c]) : "l"(x));
+        asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(acc[c]) : "f"(a[c]), "f"(b[c]));
+      } else if (OP == OP_MIX_OWN_SCALAR) {
+        // every chain adds its own broadcast scalar (nothing shared between consecutive FADD2s)
+        float sc = __int_as_float(ia[c]);
+        unsigned long long x = pk(a[c], b[c]), y = pk(sc, sc);
+        asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y));
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(a[c]), "=f"(b[c]) : "l"(x));
+        asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(acc[c]) : "f"(a[c]), "f"(b[c]));
+      } else if (OP == OP_MIX_PAIR_PAIR) {
+        // every chain adds its own PAIR (two registers): the pair + pair form, in place
+        unsigned long long x = pk(a[c], b[c]), y = pk(__int_as_float(ia[c]), __int_as_float(ib[c]));
+        asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y));
+        asm("mov.b64 {%0,%1}, %2;" : "=f"(a[c]), "=f"(b[c]) : "l"(x));
+        asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(acc[c]) : "f"(a[c]), "f"(b[c]));
+      } else if (OP == OP_MIX_BCAST_FIRST) {
+        // production form: fresh result pair = own scalar (broadcast) + a loop-invariant pair; FMNMX3 on its halves;
+        // the scalar is loop-carried through the accumulator's chain so nothing is hoisted
+        float sc = acc[c];
+        unsigned long long y = pk(a[c], b[c]), s2, t = pk(sc, sc);
+        asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(s2) : "l"(t), "l"(y));
+        float p, q; asm("mov.b64 {%0,%1}, %2;" : "=f"(p), "=f"(q) : "l"(s2));
+        asm volatile("min.f32 %0, %0, %1, %2;" : "+f"(acc[c]) : "f"(p), "f"(q));
       } else if (OP == OP_VIADDMNMX) {
         iacc[c] = __viaddmin_s32(iacc[c], ib[c], ia[c]);   // min(iacc+ib, ia): loop-carried
       } else if (OP == OP_VIMNMX3) {
@@ -133,5 +166,9 @@ int main() {
   rc |= run<OP_VIMNMX3>(sms, sink, dcyc, hcyc);
   rc |= run<OP_IADD_VIMNMX3>(sms, sink, dcyc, hcyc);
   rc |= run<OP_SELECT>(sms, sink, dcyc, hcyc);
+  rc |= run<OP_MIX_PINGPONG>(sms, sink, dcyc, hcyc);
+  rc |= run<OP_MIX_OWN_SCALAR>(sms, sink, dcyc, hcyc);
+  rc |= run<OP_MIX_PAIR_PAIR>(sms, sink, dcyc, hcyc);
+  rc |= run<OP_MIX_BCAST_FIRST>(sms, sink, dcyc, hcyc);
   return rc;
 }
