@@ -448,7 +448,7 @@ def run_gpu(args, cfg):
                 "frac_operand_pattern": (achieved_tflops / pattern) if achieved_tflops else None,
                 "basis_operand_pattern": "register-only probe of the kernel's own FADD2 (broadcast scalar "
                                          "+ pair) / FMNMX3 (two pairs) operand pattern, 16 warps/SM: 78.4 "
-                                         "relax/clk/SM; the 95.5 mix probe uses an operand pattern a min-plus tile does not have",
+                                         "relax/clk/SM; the 95.5 mix probe shares one scalar register between consecutive FADD2s (75.8 without)",
                 "basis": "FADD2 (2 adds) + FMNMX3 (2 mins) = one issue slot per relaxation: "
                          "SMs x 128 relax/clk; L0 probe FADD2+FMNMX3 mix 95.5 relax/clk/SM"},
             "phase_ms_per_step": {"phase1": sum(s.phase1_ms for s in stats) / len(stats),
