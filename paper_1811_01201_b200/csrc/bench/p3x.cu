@@ -735,11 +735,11 @@ int main() {
     run<8, 2, 16, 16, 2, 32, 3, 1024 + 3 + 4>("3st-1bar-kouter", D, P, mk, n, sms, clk);
     run<8, 2, 16, 16, 2, 32, 3, 1024 + 3 + 4096>("3st-1bar-G4", D, P, mk, n, sms, clk);
     runlib("library-key-again", D, P, mk, n, sms, clk);
+    // four CTAs of 128 threads per SM (same registers, 16 warps): 8 x 8 per thread, 128 x 64 tiles
+    run<8, 2, 8, 16, 4, 16, 3, 1024 + 3>("4cta-128thr-128x64-bk16-3st", D, P, mk, n, sms, clk);
+    run<8, 2, 8, 16, 4, 16, 4, 1024 + 3>("4cta-128thr-128x64-bk16-4st", D, P, mk, n, sms, clk);
+    run<8, 2, 8, 16, 4, 16, 4, 1024 + 3 + 4>("4cta-128thr-128x64-bk16-4st-kouter", D, P, mk, n, sms, clk);
     // three CTAs per SM (24 warps): 4 x 8 per thread, 64 x 128 tiles
-    run<4, 2, 16, 16, 3, 16, 3, 1024 + 3>("3cta-64x128-bk16-3st", D, P, mk, n, sms, clk);
-    run<4, 2, 16, 16, 3, 16, 4, 1024 + 3>("3cta-64x128-bk16-4st", D, P, mk, n, sms, clk);
-    run<4, 2, 16, 16, 3, 32, 2, 3>("3cta-64x128-bk32-2st", D, P, mk, n, sms, clk);
-    run<4, 2, 16, 16, 3, 16, 4, 1024 + 3 + 4>("3cta-64x128-bk16-4st-kouter", D, P, mk, n, sms, clk);
     runlib<fwb::MODE_TAG>("library-tag", D, P, mk, n, sms, clk);
     runlib<fwb::MODE_PLAIN>("library-plain", D, P, mk, n, sms, clk);
     // one CTA of 512 threads per SM (same registers per SM): 256 x 128 and 128 x 256 tiles
